@@ -1,0 +1,269 @@
+/* include/airg_c.h -- C-ABI of the B200-native AIRG hot path.
+ *
+ * This is the drop-in boundary. Every entry point replaces
+ * one reference C++ entry point of namespace airgraph in
+ * /root/reference/proj/include/airgraph/ (cited per function below); the
+ * C++ mirror in paper_2408_08262_b200/cpp/airgraph_gpu.hpp rebuilds those
+ * signatures and exception types on top of this ABI, and the Python mirror
+ * (paper_2408_08262_b200/airg.py) binds it with ctypes.
+ *
+ * Conventions
+ *  - Every function returns AIRG_OK (0) or a negative status; the message
+ *    (with the offending row index where the reference reports one) is
+ *    available from airg_last_error(), which is thread-local.
+ *      AIRG_EINVAL   <-> std::invalid_argument  (shape / argument errors)
+ *      AIRG_ERUNTIME <-> std::runtime_error     (zero diagonal, stall, ...)
+ *      AIRG_ECUDA    CUDA runtime failure; AIRG_ENOMEM allocation failure.
+ *  - Host-side CSR arrays use the reference layout: int64 row offsets and
+ *    column indices, fp64 values (sparse.hpp:89-93). Device CSR is int32
+ *    indices + fp64 values; upload checks the int32 range.
+ *  - "d_" pointers are device pointers on the context's device; "h_"
+ *    pointers are host pointers. All work is ordered on the context stream.
+ *  - No torch types appear here; plain pointers and sizes only.
+ */
+#ifndef AIRG_C_H_
+#define AIRG_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AIRG_OK 0
+#define AIRG_EINVAL (-1)
+#define AIRG_ERUNTIME (-2)
+#define AIRG_ECUDA (-3)
+#define AIRG_ENOMEM (-4)
+#define AIRG_ELOGIC (-5)
+
+/* CF labels, as airgraph::CfLabel (sparse.hpp:22). */
+#define AIRG_F 0
+#define AIRG_C 1
+#define AIRG_UNASSIGNED 2
+
+/* Mirrors airgraph::SetupConfig (air.hpp:16-43); same defaults from
+ * airg_setup_config_default(). */
+typedef struct airg_setup_config {
+  double strength_alpha;      /* 0.5 */
+  int32_t cf;                 /* 0 = PMISR (only GPU mode), 1 PMIS, 2 PMIS-swap */
+  int32_t ddc_enabled;        /* 1 */
+  double ddc_fraction;        /* 0.10 */
+  int64_t ddc_bins;           /* 1000 */
+  int64_t max_loops;          /* 3 */
+  int64_t poly_order;         /* 6 */
+  int64_t sparsity_order;     /* 1 */
+  double drop_coarse;         /* 0.001 */
+  double drop_restrict;       /* 0.01 */
+  int64_t coarse_size_target; /* 3000 */
+  int64_t coarse_poly_order;  /* 12 */
+  int64_t coarse_iterations;  /* 3 */
+  int64_t max_levels;         /* 0 = unlimited */
+  int32_t prolongation;       /* 0 = one-point (1 = ideal: test hook, EINVAL on GPU) */
+  int32_t weight_mode;        /* 0 = |S|+|S^T|, 1 = |S u S^T| */
+  uint64_t seed;              /* 0 */
+} airg_setup_config;
+
+/* Mirrors airgraph::SolveConfig (solve.hpp:11-19) plus the outer solver
+ * selection (outer GMRES is new, BASELINE.json config 0 / SURVEY §8f-1). */
+typedef struct airg_solve_config {
+  double rtol;                /* 1e-10 */
+  int64_t max_iterations;     /* 200 */
+  int64_t up_f_smooths;       /* 2 */
+  int64_t down_smooths;       /* 0 */
+  int64_t coarse_iterations;  /* 3 */
+  int32_t collect_timing;     /* 1 */
+  int32_t outer;              /* 0 = Richardson (reference), 1 = right-preconditioned GMRES */
+  int64_t nddofs;             /* 0 */
+  int64_t gmres_restart;      /* 30 */
+} airg_solve_config;
+
+/* Mirrors airgraph::SolveStats (solve.hpp:21-39). */
+typedef struct airg_solve_stats {
+  int64_t iterations;
+  int32_t converged;
+  int32_t _pad;
+  double final_relative_residual;
+  uint64_t flops;
+  uint64_t shadow_flops;
+  double work_units;
+  double grid_complexity;
+  double operator_complexity;
+  double storage_complexity;
+  double solve_seconds;
+  double wu_ratio;
+  double c_grind_ns;
+  double d_grind_ns;
+  int64_t history_len; /* entries written to the caller's history buffer */
+} airg_solve_stats;
+
+/* Per-level summary of a built hierarchy (air.hpp:49-66). */
+typedef struct airg_level_info {
+  int64_t n, nnz;           /* level operator A_l */
+  int64_t n_f, n_c;         /* after DDC */
+  int64_t n_f_pre;          /* after PMISR, before DDC */
+  int64_t ddc_converted;
+  int64_t nnz_ff, nnz_fc, nnz_cf, nnz_ffinv, nnz_r, nnz_p;
+  double max_theta_pre, alpha_diag, max_theta_post;
+  double smoother_growth;
+  int64_t poly_attempts;
+  int64_t effective_order;
+  double coefficients[32];  /* poly_order + 1 <= 32 */
+} airg_level_info;
+
+typedef struct airg_hier_info {
+  int64_t n_levels;         /* number of fine levels (Hierarchy::levels.size()) */
+  int64_t coarse_n, coarse_nnz, coarse_inv_nnz;
+  int64_t coarse_effective_order;
+  int64_t coarse_attempts;
+  double coarse_growth;
+  double coarse_coefficients[32];
+  double grid_complexity, operator_complexity, storage_complexity;
+} airg_hier_info;
+
+/* Coefficient injection: the polynomial coefficients are
+ * computed in x87 long double through Eigen upstream (gmres_poly.cpp:63-171)
+ * and cannot be reproduced bit-for-bit on a GPU. With an injection table the
+ * GPU setup uses the given per-level coefficients (and the given coarse
+ * level / coarse polynomial) instead of its own double-double fit, which
+ * makes the whole hierarchy bit-identical to the reference's. */
+typedef struct airg_injection {
+  int64_t n_levels;                  /* fine levels to build */
+  int64_t stride;                    /* doubles per level in level_coeffs */
+  const double* level_coeffs;        /* n_levels x stride */
+  const int64_t* level_eff_order;    /* n_levels */
+  const double* coarse_coeffs;       /* coarse_poly_order + 1 values */
+  int64_t coarse_eff_order;
+} airg_injection;
+
+typedef struct airg_ctx airg_ctx;
+typedef struct airg_csr airg_csr;
+typedef struct airg_hier airg_hier;
+
+/* ---- errors and defaults ---------------------------------------------- */
+int airg_last_error(char* buf, size_t len);
+void airg_setup_config_default(airg_setup_config* cfg);
+void airg_solve_config_default(airg_solve_config* cfg);
+const char* airg_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+int airg_ctx_create(int device, airg_ctx** out);
+int airg_ctx_destroy(airg_ctx* ctx);
+/* Use an external cudaStream_t (passed as void*); NULL restores the
+ * context's own stream. */
+int airg_ctx_set_stream(airg_ctx* ctx, void* stream);
+int airg_ctx_synchronize(airg_ctx* ctx);
+/* Number of kernels this library launched on the context since creation
+ * (bench.py reports the delta over the timed region as gpu_launches). */
+int airg_ctx_launch_count(airg_ctx* ctx, uint64_t* out);
+
+/* ---- CSR (airgraph::SparseMatrix, sparse.hpp:33-94) ---------------------- */
+/* Validating upload from the reference layout (ctor checks sparse.cpp:18-46). */
+int airg_csr_upload(airg_ctx* ctx, int64_t nrows, int64_t ncols,
+                    const int64_t* h_row_offsets, const int64_t* h_cols,
+                    const double* h_vals, airg_csr** out);
+int airg_csr_info(const airg_csr* a, int64_t* nrows, int64_t* ncols,
+                  int64_t* nnz);
+int airg_csr_download(airg_ctx* ctx, const airg_csr* a, int64_t* h_row_offsets,
+                      int64_t* h_cols, double* h_vals);
+/* Device views of the CSR arrays (int32 offsets/cols, fp64 values). */
+int airg_csr_device_ptrs(const airg_csr* a, const int32_t** d_row_offsets,
+                         const int32_t** d_cols, const double** d_vals);
+int airg_csr_destroy(airg_csr* a);
+
+/* ---- L0 kernels ---------------------------------------------------------- */
+/* y = A x (sparse.cpp:185-201): sequential per-row accumulation in column
+ * order without FMA, bit-identical to the reference. */
+int airg_spmv(airg_ctx* ctx, const airg_csr* a, const double* d_x, double* d_y);
+/* C = A B (sparse.cpp:203-242), cancellation zeros kept, contributions to
+ * each entry accumulated in A-row order. */
+int airg_spgemm(airg_ctx* ctx, const airg_csr* a, const airg_csr* b,
+                airg_csr** out);
+/* drop_entries (sparse.cpp:244-268). */
+int airg_drop(airg_ctx* ctx, const airg_csr* a, double tol, int keep_diagonal,
+              airg_csr** out);
+/* SparseMatrix::with_full_diagonal (sparse.cpp:132-160). */
+int airg_with_full_diagonal(airg_ctx* ctx, const airg_csr* a, airg_csr** out);
+
+/* ---- L1a CF splitting (coarsening.hpp) ----------------------------------- */
+/* strength (coarsening.cpp:83-105): S as a pattern CSR (values 1.0). */
+int airg_strength(airg_ctx* ctx, const airg_csr* a, double alpha,
+                  airg_csr** s_out);
+/* strength -> pmisr (coarsening.cpp:107-167) on the GPU. d_labels gets the
+ * PMISR labels (n bytes), d_weights (nullable) the weights. */
+int airg_pmisr(airg_ctx* ctx, const airg_csr* a, double alpha,
+               int64_t max_loops, uint64_t seed, int32_t weight_mode,
+               uint8_t* d_labels, double* d_weights);
+typedef struct airg_cf_report {
+  int64_t n_f_pre, n_f, n_c, n_converted;
+  double max_theta, alpha_diag;
+  int64_t s_nnz;
+} airg_cf_report;
+/* The fused CF split strength -> pmisr -> extract_blocks -> ddc
+ * (air.cpp:466-494) with the global 1000-bin histogram (coarsening.cpp:
+ * 219-330). d_labels_pre (nullable) receives the PMISR labels. */
+int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha,
+                  int64_t max_loops, uint64_t seed, int32_t weight_mode,
+                  int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
+                  uint8_t* d_labels, uint8_t* d_labels_pre,
+                  airg_cf_report* report);
+/* ddc on given labels (coarsening.cpp:252-330); selection 0 = histogram,
+ * 2 = direct (alpha_diag given). Converts in place. */
+int airg_ddc(airg_ctx* ctx, const airg_csr* a, uint8_t* d_labels,
+             double fraction, int64_t bins, int32_t selection,
+             double direct_alpha_diag, airg_cf_report* report);
+/* extract_blocks (sparse.cpp:292-340): A_ff, A_fc, A_cf (A_cc unused). */
+int airg_extract_blocks(airg_ctx* ctx, const airg_csr* a,
+                        const uint8_t* d_labels, airg_csr** aff,
+                        airg_csr** afc, airg_csr** acf);
+
+/* ---- L1b polynomials (gmres_poly.hpp) ------------------------------------ */
+/* compute_coefficients (gmres_poly.cpp:63-171): power basis and Gram matrix
+ * in double-double on the GPU, rank cut and least squares in double-double
+ * on the host. h_coeffs gets m values. */
+int airg_poly_coefficients(airg_ctx* ctx, const airg_csr* a, int64_t m,
+                           uint64_t seed, double* h_coeffs,
+                           int64_t* effective_order);
+/* assemble_fixed_sparsity (gmres_poly.cpp:197-280). */
+int airg_poly_assemble(airg_ctx* ctx, const airg_csr* a, const double* h_coeffs,
+                       int64_t n_coeffs, int64_t effective_order,
+                       int64_t sparsity_order, airg_csr** out);
+
+/* ---- L2 setup (air.hpp) ---------------------------------------------------- */
+/* setup (air.cpp:285-410). inj may be NULL (native coefficients). */
+int airg_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
+               const airg_injection* inj, airg_hier** out);
+int airg_hier_info_get(const airg_hier* h, airg_hier_info* info);
+int airg_hier_level_info(const airg_hier* h, int64_t level,
+                         airg_level_info* info);
+/* which: 0 A, 1 A_ff, 2 A_fc, 3 A_cf, 4 Aff_inv, 5 R, 6 P; level ==
+ * n_levels with which 0 / 4 gives the coarse A / coarse inverse. Returns a
+ * borrowed handle owned by the hierarchy. */
+int airg_hier_matrix(const airg_hier* h, int64_t level, int32_t which,
+                     const airg_csr** out);
+int airg_hier_labels(airg_ctx* ctx, const airg_hier* h, int64_t level,
+                     uint8_t* h_labels);
+int airg_hier_destroy(airg_hier* h);
+
+/* ---- L3 solve (solve.hpp) -------------------------------------------------- */
+/* vcycle (solve.cpp:150-165) from x = 0 (x_is_zero): d_x = V(d_b). */
+int airg_vcycle(airg_ctx* ctx, const airg_hier* h, const airg_solve_config* cfg,
+                const double* d_b, double* d_x);
+/* richardson_solve (solve.cpp:167-259) or outer GMRES per cfg->outer, with
+ * device-resident b and x. h_history (nullable) gets up to history_cap
+ * relative residuals. */
+int airg_solve(airg_ctx* ctx, const airg_hier* h, const airg_solve_config* cfg,
+               const double* d_b, double* d_x, airg_solve_stats* stats,
+               double* h_history, int64_t history_cap);
+/* The reference-facing call with HOST buffers: H2D of b, solve, D2H of x. */
+int airg_solve_host(airg_ctx* ctx, const airg_hier* h,
+                    const airg_solve_config* cfg, const double* h_b,
+                    double* h_x, airg_solve_stats* stats, double* h_history,
+                    int64_t history_cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AIRG_C_H_ */

@@ -1,0 +1,429 @@
+// oracle/ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" driver over the UNMODIFIED reference library compiled
+// from /root/reference/proj/src (see oracle/Makefile). It lets tests/ and
+// bench.py (reference arm / cpu_baseline leg) call the reference's own
+// airgraph:: entry points through ctypes with the same plain-pointer shapes
+// as include/airg_c.h. Nothing here is product code; the product never
+// loads oracle/_ref.
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "airg_c.h"
+#include "airgraph/air.hpp"
+#include "airgraph/coarsening.hpp"
+#include "airgraph/gmres_poly.hpp"
+#include "airgraph/partition_model.hpp"
+#include "airgraph/solve.hpp"
+#include "airgraph/sparse.hpp"
+#include "airgraph/transport.hpp"
+
+using namespace airgraph;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return AIRG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return AIRG_EINVAL;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return AIRG_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return AIRG_ELOGIC;
+  }
+}
+
+SparseMatrix make(int64_t n, int64_t m, const int64_t* rp, const int64_t* ci,
+                  const double* v) {
+  std::vector<index_t> o(rp, rp + n + 1);
+  std::vector<index_t> c(ci, ci + rp[n]);
+  std::vector<double> x(v, v + rp[n]);
+  return SparseMatrix(n, m, std::move(o), std::move(c), std::move(x));
+}
+
+SetupConfig to_cfg(const airg_setup_config* c) {
+  SetupConfig s;
+  s.strength_alpha = c->strength_alpha;
+  s.cf = static_cast<CfSplitting>(c->cf);
+  s.ddc_enabled = c->ddc_enabled != 0;
+  s.ddc_fraction = c->ddc_fraction;
+  s.ddc_bins = c->ddc_bins;
+  s.max_loops = c->max_loops;
+  s.poly_order = c->poly_order;
+  s.sparsity_order = c->sparsity_order;
+  s.drop_coarse = c->drop_coarse;
+  s.drop_restrict = c->drop_restrict;
+  s.coarse_size_target = c->coarse_size_target;
+  s.coarse_poly_order = c->coarse_poly_order;
+  s.coarse_iterations = c->coarse_iterations;
+  s.max_levels = c->max_levels;
+  s.prolongation = static_cast<ProlongationKind>(c->prolongation);
+  s.weight_mode = static_cast<WeightMode>(c->weight_mode);
+  s.seed = c->seed;
+  return s;
+}
+
+SolveConfig to_scfg(const airg_solve_config* c) {
+  SolveConfig s;
+  s.rtol = c->rtol;
+  s.max_iterations = c->max_iterations;
+  s.up_f_smooths = c->up_f_smooths;
+  s.down_smooths = c->down_smooths;
+  s.coarse_iterations = c->coarse_iterations;
+  s.collect_timing = c->collect_timing != 0;
+  s.nddofs = c->nddofs;
+  return s;
+}
+
+struct RefHier {
+  Hierarchy h;
+};
+
+const SparseMatrix* level_matrix(const Hierarchy& h, int64_t l, int which) {
+  const int64_t nl = static_cast<int64_t>(h.levels.size());
+  if (l == nl) {
+    if (which == 0) return &h.coarse_a;
+    if (which == 4) return &*h.coarse_inv.assembled;
+    throw std::invalid_argument("coarse level has only A (0) and inverse (4)");
+  }
+  if (l < 0 || l > nl) throw std::invalid_argument("level out of range");
+  const Level& lv = h.levels[l];
+  switch (which) {
+    case 0: return &lv.a;
+    case 1: return &lv.a_ff;
+    case 2: return &lv.a_fc;
+    case 3: return &lv.a_cf;
+    case 4: return &*lv.ff_inv.assembled;
+    case 5: return &lv.r;
+    case 6: return &lv.p;
+  }
+  throw std::invalid_argument("bad matrix selector");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return static_cast<int>(g_err.size());
+}
+
+// ---- generic matrix handles ------------------------------------------------
+int ref_mat_new(int64_t n, int64_t m, const int64_t* rp, const int64_t* ci,
+                const double* v, void** out) {
+  return guard([&] { *out = new SparseMatrix(make(n, m, rp, ci, v)); });
+}
+int ref_mat_dims(const void* h, int64_t* n, int64_t* m, int64_t* nnz) {
+  auto* a = static_cast<const SparseMatrix*>(h);
+  *n = a->nrows();
+  *m = a->ncols();
+  *nnz = a->nnz();
+  return AIRG_OK;
+}
+int ref_mat_copy(const void* h, int64_t* rp, int64_t* ci, double* v) {
+  auto* a = static_cast<const SparseMatrix*>(h);
+  std::memcpy(rp, a->row_offsets().data(), sizeof(int64_t) * (a->nrows() + 1));
+  std::memcpy(ci, a->col_indices().data(), sizeof(int64_t) * a->nnz());
+  std::memcpy(v, a->values().data(), sizeof(double) * a->nnz());
+  return AIRG_OK;
+}
+int ref_mat_free(void* h) {
+  delete static_cast<SparseMatrix*>(h);
+  return AIRG_OK;
+}
+
+// ---- L0 -------------------------------------------------------------------
+int ref_spmv(const void* a, const double* x, double* y) {
+  return guard([&] {
+    auto* m = static_cast<const SparseMatrix*>(a);
+    auto r = spmv(*m, std::span<const double>(x, m->ncols()));
+    std::memcpy(y, r.data(), sizeof(double) * r.size());
+  });
+}
+int ref_spgemm(const void* a, const void* b, void** out) {
+  return guard([&] {
+    *out = new SparseMatrix(spgemm(*static_cast<const SparseMatrix*>(a),
+                                   *static_cast<const SparseMatrix*>(b)));
+  });
+}
+int ref_drop(const void* a, double tol, int keep_diag, void** out) {
+  return guard([&] {
+    *out = new SparseMatrix(
+        drop_entries(*static_cast<const SparseMatrix*>(a), tol, keep_diag != 0));
+  });
+}
+int ref_with_full_diagonal(const void* a, void** out) {
+  return guard([&] {
+    *out = new SparseMatrix(static_cast<const SparseMatrix*>(a)->with_full_diagonal());
+  });
+}
+int ref_extract_blocks(const void* a, const uint8_t* labels, void** aff,
+                       void** afc, void** acf) {
+  return guard([&] {
+    auto* m = static_cast<const SparseMatrix*>(a);
+    std::vector<CfLabel> l(m->nrows());
+    for (index_t i = 0; i < m->nrows(); ++i) l[i] = static_cast<CfLabel>(labels[i]);
+    BlockSplit s = extract_blocks(*m, l);
+    *aff = new SparseMatrix(std::move(s.a_ff));
+    *afc = new SparseMatrix(std::move(s.a_fc));
+    *acf = new SparseMatrix(std::move(s.a_cf));
+  });
+}
+
+// ---- L1a: CF splitting ---------------------------------------------------------
+int ref_strength(const void* a, double alpha, void** s_out, int64_t* st_nnz) {
+  return guard([&] {
+    StrengthGraph g = strength(*static_cast<const SparseMatrix*>(a), alpha);
+    std::vector<double> ones(g.s_cols.size(), 1.0);
+    *s_out = new SparseMatrix(g.n, g.n, g.s_offsets, g.s_cols, std::move(ones));
+    if (st_nnz) *st_nnz = static_cast<int64_t>(g.st_cols.size());
+  });
+}
+int ref_pmisr(const void* a, double alpha, int64_t max_loops, uint64_t seed,
+              int32_t weight_mode, uint8_t* labels, double* weights) {
+  return guard([&] {
+    StrengthGraph g = strength(*static_cast<const SparseMatrix*>(a), alpha);
+    CfLabels l = pmisr(g, max_loops, seed, static_cast<WeightMode>(weight_mode));
+    for (index_t i = 0; i < g.n; ++i) labels[i] = static_cast<uint8_t>(l.label[i]);
+    if (weights) std::memcpy(weights, l.weight.data(), sizeof(double) * g.n);
+  });
+}
+int ref_pmisr_with_weights(const void* s_pattern, int64_t max_loops,
+                           const double* w, uint8_t* labels) {
+  return guard([&] {
+    auto* s = static_cast<const SparseMatrix*>(s_pattern);
+    std::vector<std::vector<index_t>> rows(s->nrows());
+    for (index_t i = 0; i < s->nrows(); ++i) {
+      auto c = s->row_cols(i);
+      rows[i].assign(c.begin(), c.end());
+    }
+    StrengthGraph g = StrengthGraph::from_pattern(s->nrows(), rows);
+    CfLabels l = pmisr_with_weights(g, max_loops,
+                                    std::vector<double>(w, w + s->nrows()));
+    for (index_t i = 0; i < g.n; ++i) labels[i] = static_cast<uint8_t>(l.label[i]);
+  });
+}
+// strength -> pmisr -> extract_blocks -> ddc, exactly as air.cpp:466-494.
+int ref_cf_split(const void* a, double alpha, int64_t max_loops, uint64_t seed,
+                 int32_t weight_mode, int32_t ddc_enabled, double fraction,
+                 int64_t bins, uint8_t* labels, uint8_t* labels_pre,
+                 airg_cf_report* rep) {
+  return guard([&] {
+    auto* m = static_cast<const SparseMatrix*>(a);
+    StrengthGraph g = strength(*m, alpha);
+    CfLabels l = pmisr(g, max_loops, seed, static_cast<WeightMode>(weight_mode));
+    if (labels_pre)
+      for (index_t i = 0; i < g.n; ++i) labels_pre[i] = static_cast<uint8_t>(l.label[i]);
+    BlockSplit split = extract_blocks(*m, l.label);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->n_f_pre = split.map.n_f();
+    rep->s_nnz = static_cast<int64_t>(g.s_cols.size());
+    if (ddc_enabled && split.map.n_f() > 0) {
+      DdcOptions opt;
+      opt.fraction = fraction;
+      opt.bins = bins;
+      DdcResult res = ddc(split.a_ff, l, split.map, opt);
+      rep->max_theta = res.report.max_theta;
+      rep->alpha_diag = res.alpha_diag;
+      rep->n_converted = static_cast<int64_t>(res.converted.size());
+      if (!res.converted.empty()) l = std::move(res.labels);
+    }
+    index_t nf = 0;
+    for (index_t i = 0; i < g.n; ++i) {
+      labels[i] = static_cast<uint8_t>(l.label[i]);
+      nf += l.label[i] == CfLabel::F;
+    }
+    rep->n_f = nf;
+    rep->n_c = g.n - nf;
+  });
+}
+int ref_ddc(const void* a, uint8_t* labels, double fraction, int64_t bins,
+            int32_t selection, double direct_alpha, airg_cf_report* rep) {
+  return guard([&] {
+    auto* m = static_cast<const SparseMatrix*>(a);
+    CfLabels l;
+    l.label.resize(m->nrows());
+    for (index_t i = 0; i < m->nrows(); ++i) l.label[i] = static_cast<CfLabel>(labels[i]);
+    l.weight.assign(m->nrows(), 0.5);
+    BlockSplit split = extract_blocks(*m, l.label);
+    DdcOptions opt;
+    opt.fraction = fraction;
+    opt.bins = bins;
+    opt.selection = static_cast<DdcSelection>(selection);
+    opt.direct_alpha_diag = direct_alpha;
+    DdcResult res = ddc(split.a_ff, l, split.map, opt);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->n_f_pre = split.map.n_f();
+    rep->max_theta = res.report.max_theta;
+    rep->alpha_diag = res.alpha_diag;
+    rep->n_converted = static_cast<int64_t>(res.converted.size());
+    for (index_t i = 0; i < m->nrows(); ++i) labels[i] = static_cast<uint8_t>(res.labels.label[i]);
+  });
+}
+
+// ---- L1b: polynomials ---------------------------------------------------------
+int ref_poly_coefficients(const void* a, int64_t m, uint64_t seed,
+                          double* coeffs, int64_t* eff) {
+  return guard([&] {
+    GmresPolynomial p = compute_coefficients(*static_cast<const SparseMatrix*>(a), m, seed);
+    std::memcpy(coeffs, p.coefficients.data(), sizeof(double) * p.coefficients.size());
+    *eff = p.effective_order;
+  });
+}
+int ref_poly_assemble(const void* a, const double* coeffs, int64_t ncoeffs,
+                      int64_t eff, int64_t s, void** out) {
+  return guard([&] {
+    GmresPolynomial p;
+    p.order = ncoeffs - 1;
+    p.coefficients.assign(coeffs, coeffs + ncoeffs);
+    p.effective_order = eff;
+    *out = new SparseMatrix(
+        assemble_fixed_sparsity(*static_cast<const SparseMatrix*>(a), p, s));
+  });
+}
+
+// ---- L2: setup ------------------------------------------------------------------
+int ref_setup(const void* a, const airg_setup_config* cfg, void** out) {
+  return guard([&] {
+    auto* rh = new RefHier;
+    try {
+      rh->h = setup(*static_cast<const SparseMatrix*>(a), to_cfg(cfg));
+    } catch (...) {
+      delete rh;
+      throw;
+    }
+    *out = rh;
+  });
+}
+int ref_hier_free(void* h) {
+  delete static_cast<RefHier*>(h);
+  return AIRG_OK;
+}
+int ref_hier_info(const void* hp, airg_hier_info* info) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    std::memset(info, 0, sizeof(*info));
+    info->n_levels = static_cast<int64_t>(h.levels.size());
+    info->coarse_n = h.coarse_a.nrows();
+    info->coarse_nnz = h.coarse_a.nnz();
+    info->coarse_inv_nnz = h.coarse_inv.assembled ? h.coarse_inv.assembled->nnz() : 0;
+    info->coarse_effective_order = h.coarse_inv.effective_order;
+    info->coarse_growth = h.coarse_growth;
+    for (size_t k = 0; k < h.coarse_inv.coefficients.size() && k < 32; ++k)
+      info->coarse_coefficients[k] = h.coarse_inv.coefficients[k];
+    info->grid_complexity = h.metrics.grid_complexity;
+    info->operator_complexity = h.metrics.operator_complexity;
+    info->storage_complexity = h.metrics.storage_complexity;
+  });
+}
+int ref_level_info(const void* hp, int64_t l, airg_level_info* info) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    if (l < 0 || l >= static_cast<int64_t>(h.levels.size()))
+      throw std::invalid_argument("level out of range");
+    const Level& lv = h.levels[l];
+    std::memset(info, 0, sizeof(*info));
+    info->n = lv.a.nrows();
+    info->nnz = lv.a.nnz();
+    info->n_f = lv.map.n_f();
+    info->n_c = lv.map.n_c();
+    info->ddc_converted = static_cast<int64_t>(lv.ddc_converted.size());
+    info->n_f_pre = info->n_f + info->ddc_converted;
+    info->nnz_ff = lv.a_ff.nnz();
+    info->nnz_fc = lv.a_fc.nnz();
+    info->nnz_cf = lv.a_cf.nnz();
+    info->nnz_ffinv = lv.ff_inv.assembled->nnz();
+    info->nnz_r = lv.r.nnz();
+    info->nnz_p = lv.p.nnz();
+    info->max_theta_pre = lv.theta_pre.max_theta;
+    info->alpha_diag = lv.theta_pre.alpha_diag;
+    info->max_theta_post = lv.theta_post.max_theta;
+    info->smoother_growth = lv.smoother_growth;
+    info->poly_attempts = lv.poly_attempts;
+    info->effective_order = lv.ff_inv.effective_order;
+    for (size_t k = 0; k < lv.ff_inv.coefficients.size() && k < 32; ++k)
+      info->coefficients[k] = lv.ff_inv.coefficients[k];
+  });
+}
+int ref_hier_matrix(const void* hp, int64_t l, int32_t which, const void** out) {
+  return guard([&] {
+    *out = level_matrix(static_cast<const RefHier*>(hp)->h, l, which);
+  });
+}
+int ref_hier_labels(const void* hp, int64_t l, uint8_t* labels) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    const Level& lv = h.levels.at(l);
+    for (size_t i = 0; i < lv.map.label.size(); ++i)
+      labels[i] = static_cast<uint8_t>(lv.map.label[i]);
+  });
+}
+
+// ---- L3: solve -------------------------------------------------------------------
+int ref_vcycle(const void* hp, const airg_solve_config* cfg, const double* b,
+               double* x) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    const index_t n = h.top().nrows();
+    std::vector<double> x0(n, 0.0);
+    auto r = vcycle(h, std::span<const double>(b, n), x0, to_scfg(cfg));
+    std::memcpy(x, r.data(), sizeof(double) * n);
+  });
+}
+int ref_solve(const void* hp, const airg_solve_config* cfg, const double* b,
+              double* x, airg_solve_stats* st, double* hist, int64_t cap) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    const index_t n = h.top().nrows();
+    std::vector<double> xo;
+    SolveStats s = richardson_solve(h, std::span<const double>(b, n), to_scfg(cfg), &xo);
+    std::memcpy(x, xo.data(), sizeof(double) * n);
+    std::memset(st, 0, sizeof(*st));
+    st->iterations = s.iterations;
+    st->converged = s.converged;
+    st->final_relative_residual = s.final_relative_residual;
+    st->flops = s.flops;
+    st->shadow_flops = s.shadow_flops;
+    st->work_units = s.work_units;
+    st->grid_complexity = s.grid_complexity;
+    st->operator_complexity = s.operator_complexity;
+    st->storage_complexity = s.storage_complexity;
+    st->solve_seconds = s.solve_seconds;
+    st->wu_ratio = s.wu_ratio;
+    st->c_grind_ns = s.c_grind_ns;
+    st->d_grind_ns = s.d_grind_ns;
+    const int64_t k = std::min<int64_t>(cap, s.residual_history.size());
+    if (hist) std::memcpy(hist, s.residual_history.data(), sizeof(double) * k);
+    st->history_len = static_cast<int64_t>(s.residual_history.size());
+  });
+}
+
+// ---- side: the reference's own desk operator (transport.cpp) --------------
+int ref_desk_problem(int64_t nx, uint64_t seed, double jitter, void** a_out,
+                     double* b_out, int64_t b_cap, int64_t* n_out) {
+  return guard([&] {
+    StreamingProblem p = assemble_streaming(generate_mesh(nx, seed, jitter));
+    *n_out = p.a.nrows();
+    if (b_out && b_cap >= p.a.nrows())
+      std::memcpy(b_out, p.b.data(), sizeof(double) * p.b.size());
+    *a_out = new SparseMatrix(std::move(p.a));
+  });
+}
+
+}  // extern "C"
