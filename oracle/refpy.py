@@ -96,8 +96,9 @@ class _Lib:
             fn.restype = C.c_int
         self.has_desk = hasattr(L, p + "desk_problem")
         if self.has_desk:
-            L[p + "desk_problem"].argtypes = [C.c_int64, C.c_uint64, C.c_double, C.POINTER(C.c_void_p), f64p, C.c_int64, C.POINTER(C.c_int64)]
-            L[p + "desk_problem"].restype = C.c_int
+            fn = getattr(L, p + "desk_problem")
+            fn.argtypes = [C.c_int64, C.c_uint64, C.c_double, C.POINTER(C.c_void_p), f64p, C.c_int64, C.POINTER(C.c_int64)]
+            fn.restype = C.c_int
 
     # -- helpers -----------------------------------------------------------
     def _fn(self, name):
@@ -212,6 +213,7 @@ def binop(lib, name, *args):
 
 
 def cf_split(lib, A: Mat, cfg: dict, seed: int):
+    cfg = {**abi.SETUP_DEFAULTS, **cfg}
     n = A.dims()[0]
     lab = np.zeros(n, np.uint8)
     pre = np.zeros(n, np.uint8)

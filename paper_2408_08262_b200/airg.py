@@ -1,0 +1,544 @@
+"""Python mirror of the reference's airgraph:: API over the B200 C-ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/airgraph/*.hpp (cited per function) so the
+parity tests read like the reference's own tests:
+  std::invalid_argument -> InvalidArgument (a ValueError)
+  std::runtime_error    -> AirgRuntimeError (a RuntimeError)
+Every compute call goes through paper_2408_08262_b200/libairg_b200.so
+(hand-written sm_100a kernels); there is no CPU fallback: if the library is
+missing or no CUDA device is present, the calls raise.
+
+Device memory and streams come from PyTorch (plumbing only): the context
+runs its kernels on a dedicated torch stream whose handle is handed to the
+C-ABI, and device tensors are passed as raw pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libairg_b200.so")
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument at the reference boundary."""
+
+
+class AirgRuntimeError(RuntimeError):
+    """std::runtime_error at the reference boundary (stall, zero diagonal)."""
+
+
+class CudaFailure(RuntimeError):
+    pass
+
+
+_lib = None
+_VP = C.c_void_p
+_P = C.POINTER
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA engine; raise loudly if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the sm_100a engine first "
+                "(python -c 'import __graft_entry__ as g; g.build()')")
+        L = C.CDLL(LIB_PATH)
+        sig = {
+            "airg_last_error": ([C.c_char_p, C.c_size_t], C.c_int),
+            "airg_version": ([], C.c_char_p),
+            "airg_setup_config_default": ([_P(abi.SetupConfig)], None),
+            "airg_solve_config_default": ([_P(abi.SolveConfig)], None),
+            "airg_ctx_create": ([C.c_int, _P(_VP)], C.c_int),
+            "airg_ctx_destroy": ([_VP], C.c_int),
+            "airg_ctx_set_stream": ([_VP, _VP], C.c_int),
+            "airg_ctx_synchronize": ([_VP], C.c_int),
+            "airg_ctx_launch_count": ([_VP, _P(C.c_uint64)], C.c_int),
+            "airg_csr_upload": ([_VP, C.c_int64, C.c_int64, _VP, _VP, _VP, _P(_VP)], C.c_int),
+            "airg_csr_info": ([_VP, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
+            "airg_csr_download": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
+            "airg_csr_device_ptrs": ([_VP, _P(_VP), _P(_VP), _P(_VP)], C.c_int),
+            "airg_csr_destroy": ([_VP], C.c_int),
+            "airg_spmv": ([_VP, _VP, _VP, _VP], C.c_int),
+            "airg_spgemm": ([_VP, _VP, _VP, _P(_VP)], C.c_int),
+            "airg_drop": ([_VP, _VP, C.c_double, C.c_int, _P(_VP)], C.c_int),
+            "airg_with_full_diagonal": ([_VP, _VP, _P(_VP)], C.c_int),
+            "airg_strength": ([_VP, _VP, C.c_double, _P(_VP)], C.c_int),
+            "airg_pmisr": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, _VP, _VP], C.c_int),
+            "airg_cf_split": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, C.c_int32,
+                               C.c_double, C.c_int64, _VP, _VP, _P(abi.CfReport)], C.c_int),
+            "airg_ddc": ([_VP, _VP, _VP, C.c_double, C.c_int64, C.c_int32, C.c_double,
+                          _P(abi.CfReport)], C.c_int),
+            "airg_extract_blocks": ([_VP, _VP, _VP, _P(_VP), _P(_VP), _P(_VP)], C.c_int),
+            "airg_poly_coefficients": ([_VP, _VP, C.c_int64, C.c_uint64, _VP, _P(C.c_int64)], C.c_int),
+            "airg_poly_assemble": ([_VP, _VP, _VP, C.c_int64, C.c_int64, C.c_int64, _P(_VP)], C.c_int),
+            "airg_setup": ([_VP, _VP, _P(abi.SetupConfig), _P(abi.Injection), _P(_VP)], C.c_int),
+            "airg_hier_info_get": ([_VP, _P(abi.HierInfo)], C.c_int),
+            "airg_hier_level_info": ([_VP, C.c_int64, _P(abi.LevelInfo)], C.c_int),
+            "airg_hier_matrix": ([_VP, C.c_int64, C.c_int32, _P(_VP)], C.c_int),
+            "airg_hier_labels": ([_VP, _VP, C.c_int64, _VP], C.c_int),
+            "airg_hier_destroy": ([_VP], C.c_int),
+            "airg_vcycle": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP], C.c_int),
+            "airg_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
+                            C.c_int64], C.c_int),
+            "airg_solve_host": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
+                                 C.c_int64], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    """Every entry point include/airg_c.h declares (checked by the CPU tests)."""
+    import re
+    hdr = os.path.join(os.path.dirname(HERE), "include", "airg_c.h")
+    text = open(hdr).read()
+    return sorted(set(re.findall(r"\b(airg_[a-z0-9_]+)\s*\(", text)))
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    buf = C.create_string_buffer(4096)
+    lib().airg_last_error(buf, 4096)
+    msg = buf.value.decode()
+    if rc == -1:
+        raise InvalidArgument(msg)
+    if rc == -2:
+        raise AirgRuntimeError(msg)
+    raise CudaFailure(f"airg status {rc}: {msg}")
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One device + one stream (airg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise CudaFailure("no CUDA device: the AIRG engine runs on the GPU only")
+        self.torch = torch
+        self.device = device
+        self.tdev = torch.device("cuda", device)
+        self.stream = torch.cuda.Stream(device=self.tdev)
+        h = _VP()
+        _check(lib().airg_ctx_create(device, C.byref(h)))
+        self.h = h
+        _check(lib().airg_ctx_set_stream(self.h, _VP(self.stream.cuda_stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().airg_ctx_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def synchronize(self):
+        _check(lib().airg_ctx_synchronize(self.h))
+
+    def launches(self) -> int:
+        v = C.c_uint64()
+        _check(lib().airg_ctx_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    # device scratch on our stream
+    def empty(self, n, dtype):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.empty(int(n), dtype=dtype, device=self.tdev)
+
+    def to_device(self, a: np.ndarray):
+        with self.torch.cuda.stream(self.stream):
+            t = self.torch.from_numpy(np.ascontiguousarray(a)).to(self.tdev, non_blocking=False)
+        return t
+
+    def to_host(self, t) -> np.ndarray:
+        self.stream.synchronize()
+        return t.cpu().numpy()
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class SparseMatrix:
+    """Host CSR in the reference layout (sparse.hpp:33-94): int64 offsets
+    and columns (strictly increasing per row), fp64 values."""
+    nrows: int
+    ncols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_offsets[-1])
+
+    @staticmethod
+    def from_arrays(n, m, rp, ci, v) -> "SparseMatrix":
+        return SparseMatrix(int(n), int(m), np.ascontiguousarray(rp, np.int64),
+                            np.ascontiguousarray(ci, np.int64), np.ascontiguousarray(v, np.float64))
+
+    @staticmethod
+    def from_triplets(n, m, triplets) -> "SparseMatrix":
+        """sparse.cpp:48-80 (duplicates summed in sorted order)."""
+        rows = np.array([t[0] for t in triplets], np.int64)
+        cols = np.array([t[1] for t in triplets], np.int64)
+        vals = np.array([t[2] for t in triplets], np.float64)
+        if len(rows) and (rows.min() < 0 or rows.max() >= n or cols.min() < 0 or cols.max() >= m):
+            raise InvalidArgument("SparseMatrix: triplet index out of range")
+        order = np.lexsort((cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        rp = np.zeros(n + 1, np.int64)
+        oc, ov = [], []
+        k = 0
+        while k < len(rows):
+            r, c, v = rows[k], cols[k], vals[k]
+            k += 1
+            while k < len(rows) and rows[k] == r and cols[k] == c:
+                v += vals[k]
+                k += 1
+            oc.append(c)
+            ov.append(v)
+            rp[r + 1] += 1
+        return SparseMatrix(n, m, np.cumsum(rp), np.array(oc, np.int64), np.array(ov, np.float64))
+
+    @staticmethod
+    def identity(n) -> "SparseMatrix":
+        return SparseMatrix(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64), np.ones(n))
+
+    @staticmethod
+    def diagonal(d) -> "SparseMatrix":
+        n = len(d)
+        return SparseMatrix(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64),
+                            np.asarray(d, np.float64).copy())
+
+    def to_dense(self) -> np.ndarray:
+        d = np.zeros((self.nrows, self.ncols))
+        for i in range(self.nrows):
+            s, e = self.row_offsets[i], self.row_offsets[i + 1]
+            d[i, self.col_indices[s:e]] = self.values[s:e]
+        return d
+
+    def __eq__(self, o) -> bool:  # exact comparison, sparse.hpp:87
+        return (self.nrows == o.nrows and self.ncols == o.ncols
+                and np.array_equal(self.row_offsets, o.row_offsets)
+                and np.array_equal(self.col_indices, o.col_indices)
+                and np.array_equal(self.values.view(np.uint64), o.values.view(np.uint64)))
+
+
+class DeviceCSR:
+    """An airg_csr handle (int32 indices, fp64 values, on the GPU)."""
+
+    def __init__(self, ctx: Context, handle, owned: bool = True, keep=None):
+        self.ctx, self.h, self.owned, self._keep = ctx, handle, owned, keep
+
+    @staticmethod
+    def upload(a: SparseMatrix, ctx: Context | None = None) -> "DeviceCSR":
+        ctx = ctx or default_context()
+        h = _VP()
+        _check(lib().airg_csr_upload(ctx.h, a.nrows, a.ncols, a.row_offsets.ctypes.data,
+                                     a.col_indices.ctypes.data, a.values.ctypes.data, C.byref(h)))
+        return DeviceCSR(ctx, h)
+
+    def __del__(self):
+        if self.owned and getattr(self, "h", None):
+            try:
+                lib().airg_csr_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def dims(self):
+        n, m, z = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().airg_csr_info(self.h, C.byref(n), C.byref(m), C.byref(z)))
+        return n.value, m.value, z.value
+
+    def download(self) -> SparseMatrix:
+        n, m, z = self.dims()
+        rp = np.zeros(n + 1, np.int64)
+        ci = np.zeros(z, np.int64)
+        v = np.zeros(z, np.float64)
+        _check(lib().airg_csr_download(self.ctx.h, self.h, rp.ctypes.data, ci.ctypes.data, v.ctypes.data))
+        return SparseMatrix(n, m, rp, ci, v)
+
+
+def _dev(a, ctx) -> DeviceCSR:
+    return a if isinstance(a, DeviceCSR) else DeviceCSR.upload(a, ctx)
+
+
+def _new(ctx, fn, *args) -> DeviceCSR:
+    out = _VP()
+    _check(fn(ctx.h, *args, C.byref(out)))
+    return DeviceCSR(ctx, out)
+
+
+# ---- L0 (sparse.hpp:97-110) -------------------------------------------------
+def spmv(a, x, ctx: Context | None = None) -> np.ndarray:
+    """y = A x (sparse.cpp:185-201); bit-identical to the reference."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    n, m, _ = d.dims()
+    x = np.asarray(x, np.float64)
+    if x.shape[0] != m:
+        raise InvalidArgument("spmv: dimension mismatch")
+    tx = ctx.to_device(x)
+    ty = ctx.empty(n, ctx.torch.float64)
+    _check(lib().airg_spmv(ctx.h, d.h, _ptr(tx), _ptr(ty)))
+    return ctx.to_host(ty)
+
+
+def spgemm(a, b, ctx: Context | None = None) -> SparseMatrix:
+    """C = A B (sparse.cpp:203-242), cancellation zeros retained."""
+    ctx = ctx or default_context()
+    da, db = _dev(a, ctx), _dev(b, ctx)
+    return _new(ctx, lib().airg_spgemm, da.h, db.h).download()
+
+
+def drop_entries(a, tol: float, keep_diagonal: bool = True, ctx: Context | None = None) -> SparseMatrix:
+    """sparse.cpp:244-268."""
+    ctx = ctx or default_context()
+    return _new(ctx, lib().airg_drop, _dev(a, ctx).h, float(tol), int(keep_diagonal)).download()
+
+
+def with_full_diagonal(a, ctx: Context | None = None) -> SparseMatrix:
+    """SparseMatrix::with_full_diagonal (sparse.cpp:132-160)."""
+    ctx = ctx or default_context()
+    return _new(ctx, lib().airg_with_full_diagonal, _dev(a, ctx).h).download()
+
+
+def extract_blocks(a, labels, ctx: Context | None = None):
+    """sparse.cpp:292-340 -> (A_ff, A_fc, A_cf)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    tl = ctx.to_device(np.asarray(labels, np.uint8))
+    o = [_VP(), _VP(), _VP()]
+    _check(lib().airg_extract_blocks(ctx.h, d.h, _ptr(tl), C.byref(o[0]), C.byref(o[1]), C.byref(o[2])))
+    return tuple(DeviceCSR(ctx, h).download() for h in o)
+
+
+# ---- L1a (coarsening.hpp) ---------------------------------------------------------
+def strength(a, alpha: float, ctx: Context | None = None) -> SparseMatrix:
+    """coarsening.cpp:83-105: S as a pattern matrix (values 1.0)."""
+    ctx = ctx or default_context()
+    return _new(ctx, lib().airg_strength, _dev(a, ctx).h, float(alpha)).download()
+
+
+def pmisr(a, alpha: float, max_loops: int, seed: int, weight_mode: int = 0,
+          ctx: Context | None = None):
+    """strength -> pmisr (coarsening.cpp:107-167) -> (labels, weights)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    n = d.dims()[0]
+    tl = ctx.empty(max(n, 1), ctx.torch.uint8)
+    tw = ctx.empty(max(n, 1), ctx.torch.float64)
+    _check(lib().airg_pmisr(ctx.h, d.h, float(alpha), int(max_loops), int(seed) & (2**64 - 1),
+                            int(weight_mode), _ptr(tl), _ptr(tw)))
+    return ctx.to_host(tl)[:n], ctx.to_host(tw)[:n]
+
+
+@dataclass
+class CfReport:
+    n_f_pre: int
+    n_f: int
+    n_c: int
+    n_converted: int
+    max_theta: float
+    alpha_diag: float
+    s_nnz: int
+
+
+def cf_split(a, alpha=0.5, max_loops=3, seed=0, weight_mode=0, ddc_enabled=True,
+             ddc_fraction=0.1, ddc_bins=1000, ctx: Context | None = None):
+    """The fused split of air.cpp:466-494 -> (labels, pmisr_labels, report)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    n = d.dims()[0]
+    tl = ctx.empty(max(n, 1), ctx.torch.uint8)
+    tp = ctx.empty(max(n, 1), ctx.torch.uint8)
+    rep = abi.CfReport()
+    _check(lib().airg_cf_split(ctx.h, d.h, float(alpha), int(max_loops), int(seed) & (2**64 - 1),
+                               int(weight_mode), int(ddc_enabled), float(ddc_fraction), int(ddc_bins),
+                               _ptr(tl), _ptr(tp), C.byref(rep)))
+    r = CfReport(rep.n_f_pre, rep.n_f, rep.n_c, rep.n_converted, rep.max_theta, rep.alpha_diag, rep.s_nnz)
+    return ctx.to_host(tl)[:n], ctx.to_host(tp)[:n], r
+
+
+def ddc(a, labels, fraction=0.1, bins=1000, selection=0, direct_alpha_diag=0.0,
+        ctx: Context | None = None):
+    """coarsening.cpp:252-330 on the F block of A under `labels` (selection
+    0 histogram, 2 direct) -> (new labels, report)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    tl = ctx.to_device(np.asarray(labels, np.uint8))
+    rep = abi.CfReport()
+    _check(lib().airg_ddc(ctx.h, d.h, _ptr(tl), float(fraction), int(bins), int(selection),
+                          float(direct_alpha_diag), C.byref(rep)))
+    return ctx.to_host(tl), rep
+
+
+# ---- L1b (gmres_poly.hpp) -----------------------------------------------------------
+def compute_coefficients(a, m: int, seed: int, ctx: Context | None = None):
+    """gmres_poly.cpp:63-171 (double-double on the GPU) -> (coeffs, effective_order)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    out = np.zeros(max(int(m), 1))
+    eff = C.c_int64()
+    _check(lib().airg_poly_coefficients(ctx.h, d.h, int(m), int(seed) & (2**64 - 1),
+                                        out.ctypes.data, C.byref(eff)))
+    return out, eff.value
+
+
+def assemble_fixed_sparsity(a, coeffs, effective_order: int, sparsity_order: int,
+                            ctx: Context | None = None) -> SparseMatrix:
+    """gmres_poly.cpp:197-280."""
+    ctx = ctx or default_context()
+    c = np.ascontiguousarray(coeffs, np.float64)
+    return _new(ctx, lib().airg_poly_assemble, _dev(a, ctx).h, c.ctypes.data, len(c),
+                int(effective_order), int(sparsity_order)).download()
+
+
+# ---- L2 / L3 (air.hpp, solve.hpp) ------------------------------------------------------
+MATRICES = {"a": 0, "a_ff": 1, "a_fc": 2, "a_cf": 3, "ff_inv": 4, "r": 5, "p": 6}
+
+
+class Hierarchy:
+    """A device-resident airgraph::Hierarchy (air.hpp:76-91)."""
+
+    def __init__(self, ctx: Context, h, top_n: int):
+        self.ctx, self.h, self.top_n = ctx, h, top_n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().airg_hier_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def info(self) -> abi.HierInfo:
+        i = abi.HierInfo()
+        _check(lib().airg_hier_info_get(self.h, C.byref(i)))
+        return i
+
+    @property
+    def n_levels(self) -> int:
+        return self.info().n_levels
+
+    def level(self, l: int) -> abi.LevelInfo:
+        i = abi.LevelInfo()
+        _check(lib().airg_hier_level_info(self.h, int(l), C.byref(i)))
+        return i
+
+    def matrix(self, l: int, which) -> SparseMatrix:
+        w = MATRICES[which] if isinstance(which, str) else int(which)
+        out = _VP()
+        _check(lib().airg_hier_matrix(self.h, int(l), w, C.byref(out)))
+        return DeviceCSR(self.ctx, out, owned=False, keep=self).download()
+
+    def labels(self, l: int) -> np.ndarray:
+        n = self.level(l).n
+        out = np.zeros(n, np.uint8)
+        _check(lib().airg_hier_labels(self.ctx.h, self.h, int(l), out.ctypes.data))
+        return out
+
+    def vcycle(self, b, **solve_kw) -> np.ndarray:
+        """vcycle(h, b, x = 0) (solve.cpp:150-165)."""
+        cfg = abi.solve_config(**solve_kw)
+        tb = self.ctx.to_device(np.asarray(b, np.float64))
+        tx = self.ctx.empty(self.top_n, self.ctx.torch.float64)
+        _check(lib().airg_vcycle(self.ctx.h, self.h, C.byref(cfg), _ptr(tb), _ptr(tx)))
+        return self.ctx.to_host(tx)
+
+    def solve_device(self, tb, tx, history_cap: int = 0, **solve_kw):
+        """Solve with device-resident b / x (torch tensors)."""
+        cfg = abi.solve_config(**solve_kw)
+        st = abi.SolveStats()
+        hist = np.zeros(max(history_cap, 1))
+        _check(lib().airg_solve(self.ctx.h, self.h, C.byref(cfg), _ptr(tb), _ptr(tx), C.byref(st),
+                                hist.ctypes.data if history_cap else None, int(history_cap)))
+        return st, hist[: min(history_cap, st.history_len)]
+
+
+def setup(a, injection: dict | None = None, ctx: Context | None = None, **cfg_kw) -> Hierarchy:
+    """airgraph::setup (air.cpp:285-410) on the GPU. `injection` (optional)
+    = {"levels": [(coeffs, eff), ...], "coarse": (coeffs, eff)} takes the
+    polynomial coefficients from the reference (coefficient-injection parity
+    mode)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    cfg = abi.setup_config(**cfg_kw)
+    inj_p = None
+    keep = []
+    if injection is not None:
+        levels = injection["levels"]
+        stride = 32
+        lc = np.zeros(max(1, len(levels)) * stride)
+        le = np.zeros(max(1, len(levels)), np.int64)
+        for l, (co, eff) in enumerate(levels):
+            lc[l * stride: l * stride + len(co)] = co
+            le[l] = eff
+        cc = np.zeros(32)
+        cc[: len(injection["coarse"][0])] = injection["coarse"][0]
+        keep = [lc, le, cc]
+        inj = abi.Injection(len(levels), stride, lc.ctypes.data_as(_P(C.c_double)),
+                            le.ctypes.data_as(_P(C.c_int64)), cc.ctypes.data_as(_P(C.c_double)),
+                            int(injection["coarse"][1]))
+        inj_p = C.byref(inj)
+    out = _VP()
+    _check(lib().airg_setup(ctx.h, d.h, C.byref(cfg), inj_p, C.byref(out)))
+    del keep
+    return Hierarchy(ctx, out, d.dims()[0])
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    stats: abi.SolveStats
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+def richardson_solve(h: Hierarchy, b, history_cap: int = 1024, **solve_kw) -> SolveResult:
+    """richardson_solve (solve.cpp:167-259) through the host-buffer C-ABI
+    call (H2D of b, solve, D2H of x). outer=1 selects the outer GMRES."""
+    cfg = abi.solve_config(**solve_kw)
+    b = np.ascontiguousarray(b, np.float64)
+    if b.shape[0] != h.top_n:
+        raise InvalidArgument("richardson_solve: rhs length mismatch")
+    x = np.zeros_like(b)
+    st = abi.SolveStats()
+    hist = np.zeros(history_cap)
+    _check(lib().airg_solve_host(h.ctx.h, h.h, C.byref(cfg), b.ctypes.data, x.ctypes.data,
+                                 C.byref(st), hist.ctypes.data, history_cap))
+    return SolveResult(x, st, hist[: min(history_cap, st.history_len)])
+
+
+def gmres_solve(h: Hierarchy, b, restart: int = 30, **solve_kw) -> SolveResult:
+    """Right-preconditioned restarted GMRES with one AIRG V-cycle per
+    iteration (BASELINE config 0's outer solver)."""
+    return richardson_solve(h, b, outer=1, gmres_restart=restart, **solve_kw)

@@ -1,0 +1,574 @@
+// extern "C" boundary (include/airg_c.h): status codes + thread-local error
+// text, mirroring how the reference surfaces std::invalid_argument /
+// std::runtime_error (cli.cpp:477-486).
+#include <cstring>
+#include <memory>
+
+#include "hier.cuh"
+
+using namespace airg;
+
+struct airg_ctx {
+  Ctx c;
+};
+struct airg_csr {
+  Ctx* c = nullptr;
+  Csr m;
+};
+struct airg_hier {
+  Ctx* c = nullptr;
+  Hier h;
+  std::vector<std::unique_ptr<airg_csr>> views;  // borrowed handles
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return AIRG_OK;
+  } catch (const InvalidArgument& e) {
+    g_err = e.what();
+    return AIRG_EINVAL;
+  } catch (const RuntimeError& e) {
+    g_err = e.what();
+    return AIRG_ERUNTIME;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return AIRG_ECUDA;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return AIRG_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return AIRG_ELOGIC;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw InvalidArgument(std::string("airg: null ") + what);
+}
+void bind(Ctx& c) { CUDA_CHECK(cudaSetDevice(c.device)); }
+
+}  // namespace
+
+extern "C" {
+
+int airg_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)g_err.size();
+}
+
+const char* airg_version(void) { return "airg-b200 0.1 (sm_100a)"; }
+
+void airg_setup_config_default(airg_setup_config* c) {
+  c->strength_alpha = 0.5;
+  c->cf = 0;
+  c->ddc_enabled = 1;
+  c->ddc_fraction = 0.10;
+  c->ddc_bins = 1000;
+  c->max_loops = 3;
+  c->poly_order = 6;
+  c->sparsity_order = 1;
+  c->drop_coarse = 0.001;
+  c->drop_restrict = 0.01;
+  c->coarse_size_target = 3000;
+  c->coarse_poly_order = 12;
+  c->coarse_iterations = 3;
+  c->max_levels = 0;
+  c->prolongation = 0;
+  c->weight_mode = 0;
+  c->seed = 0;
+}
+
+void airg_solve_config_default(airg_solve_config* c) {
+  c->rtol = 1e-10;
+  c->max_iterations = 200;
+  c->up_f_smooths = 2;
+  c->down_smooths = 0;
+  c->coarse_iterations = 3;
+  c->collect_timing = 1;
+  c->outer = 0;
+  c->nddofs = 0;
+  c->gmres_restart = 30;
+}
+
+int airg_ctx_create(int device, airg_ctx** out) {
+  return guard([&] {
+    need(out, "output handle");
+    auto ctx = std::make_unique<airg_ctx>();
+    ctx->c.device = device;
+    int count = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw InvalidArgument("airg_ctx_create: no such CUDA device");
+    CUDA_CHECK(cudaSetDevice(device));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
+    ctx->c.stream = ctx->c.own_stream;
+    CUDA_CHECK(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    cudaMemPool_t pool;
+    CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = ctx.release();
+  });
+}
+
+int airg_ctx_destroy(airg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    bind(ctx->c);
+    cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
+    delete ctx;
+  });
+}
+
+int airg_ctx_set_stream(airg_ctx* ctx, void* stream) {
+  return guard([&] {
+    need(ctx, "context");
+    ctx->c.stream = stream ? (cudaStream_t)stream : ctx->c.own_stream;
+  });
+}
+
+int airg_ctx_synchronize(airg_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "context");
+    bind(ctx->c);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int airg_ctx_launch_count(airg_ctx* ctx, uint64_t* out) {
+  return guard([&] {
+    need(ctx, "context");
+    *out = ctx->c.launches;
+  });
+}
+
+// ---- CSR --------------------------------------------------------------------
+int airg_csr_upload(airg_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* rp,
+                    const int64_t* ci, const double* v, airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "output handle");
+    bind(ctx->c);
+    auto h = std::make_unique<airg_csr>();
+    h->c = &ctx->c;
+    csr_upload(ctx->c, nrows, ncols, rp, ci, v, h->m);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+    *out = h.release();
+  });
+}
+
+int airg_csr_info(const airg_csr* a, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+  return guard([&] {
+    need(a, "matrix");
+    if (nrows) *nrows = a->m.n;
+    if (ncols) *ncols = a->m.m;
+    if (nnz) *nnz = a->m.nnz;
+  });
+}
+
+int airg_csr_download(airg_ctx* ctx, const airg_csr* a, int64_t* rp, int64_t* ci, double* v) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    csr_download(ctx->c, a->m, rp, ci, v);
+  });
+}
+
+int airg_csr_device_ptrs(const airg_csr* a, const int32_t** rp, const int32_t** ci,
+                         const double** v) {
+  return guard([&] {
+    need(a, "matrix");
+    if (rp) *rp = a->m.rp.p;
+    if (ci) *ci = a->m.ci.p;
+    if (v) *v = a->m.v.p;
+  });
+}
+
+int airg_csr_destroy(airg_csr* a) {
+  return guard([&] { delete a; });
+}
+
+static airg_csr* wrap(Ctx& c, Csr&& m) {
+  auto h = new airg_csr;
+  h->c = &c;
+  h->m = std::move(m);
+  return h;
+}
+
+int airg_spmv(airg_ctx* ctx, const airg_csr* a, const double* x, double* y) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    if (a->m.n && (!x || !y) && a->m.m) throw InvalidArgument("spmv: dimension mismatch");
+    spmv(ctx->c, a->m, x, y);
+  });
+}
+
+int airg_spgemm(airg_ctx* ctx, const airg_csr* a, const airg_csr* b, airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(b, "matrix");
+    bind(ctx->c);
+    Csr r;
+    spgemm(ctx->c, a->m, b->m, r);
+    *out = wrap(ctx->c, std::move(r));
+  });
+}
+
+int airg_drop(airg_ctx* ctx, const airg_csr* a, double tol, int keep_diagonal, airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Csr r;
+    drop_entries(ctx->c, a->m, tol, keep_diagonal != 0, r);
+    *out = wrap(ctx->c, std::move(r));
+  });
+}
+
+int airg_with_full_diagonal(airg_ctx* ctx, const airg_csr* a, airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Csr r;
+    with_full_diagonal(ctx->c, a->m, r);
+    *out = wrap(ctx->c, std::move(r));
+  });
+}
+
+// ---- CF splitting -------------------------------------------------------------
+int airg_strength(airg_ctx* ctx, const airg_csr* a, double alpha, airg_csr** s_out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Strength g;
+    strength(ctx->c, a->m, alpha, g);
+    Csr s;
+    s.n = s.m = g.n;
+    s.nnz = g.nnz;
+    s.rp = std::move(g.rp);
+    s.ci = std::move(g.ci);
+    s.v.alloc(ctx->c, (size_t)g.nnz);
+    if (g.nnz) {
+      std::vector<double> ones((size_t)g.nnz, 1.0);
+      to_device(ctx->c, s.v.p, ones.data(), ones.size());
+    }
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+    *s_out = wrap(ctx->c, std::move(s));
+  });
+}
+
+int airg_pmisr(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops, uint64_t seed,
+               int32_t weight_mode, uint8_t* labels, double* weights) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Strength g;
+    strength(ctx->c, a->m, alpha, g);
+    pmisr(ctx->c, g, max_loops, seed, weight_mode, labels, weights);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops, uint64_t seed,
+                  int32_t weight_mode, int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
+                  uint8_t* labels, uint8_t* labels_pre, airg_cf_report* rep) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(labels, "labels");
+    bind(ctx->c);
+    Ctx& c = ctx->c;
+    Strength g;
+    strength(c, a->m, alpha, g);
+    pmisr(c, g, max_loops, seed, weight_mode, labels, nullptr);
+    if (labels_pre && a->m.n)
+      CUDA_CHECK(cudaMemcpyAsync(labels_pre, labels, a->m.n, cudaMemcpyDeviceToDevice, c.stream));
+    LabelMap map;
+    build_label_map(c, labels, a->m.n, map);
+    airg_cf_report r;
+    std::memset(&r, 0, sizeof r);
+    r.n_f_pre = map.nf;
+    r.s_nnz = g.nnz;
+    if (ddc_enabled && map.nf > 0) {
+      Blocks blk;
+      extract_blocks(c, a->m, map, blk, false);
+      DdcResult d = ddc(c, blk.aff, map, labels, ddc_fraction, ddc_bins, 0, 0.0, true);
+      r.max_theta = d.max_theta;
+      r.alpha_diag = d.alpha_diag;
+      r.n_converted = d.converted;
+    }
+    r.n_f = r.n_f_pre - r.n_converted;
+    r.n_c = a->m.n - r.n_f;
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (rep) *rep = r;
+  });
+}
+
+int airg_ddc(airg_ctx* ctx, const airg_csr* a, uint8_t* labels, double fraction, int64_t bins,
+             int32_t selection, double direct_alpha, airg_cf_report* rep) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Ctx& c = ctx->c;
+    LabelMap map;
+    build_label_map(c, labels, a->m.n, map);
+    Blocks blk;
+    extract_blocks(c, a->m, map, blk, false);
+    DdcResult d = ddc(c, blk.aff, map, labels, fraction, bins, selection, direct_alpha, true);
+    airg_cf_report r;
+    std::memset(&r, 0, sizeof r);
+    r.n_f_pre = map.nf;
+    r.max_theta = d.max_theta;
+    r.alpha_diag = d.alpha_diag;
+    r.n_converted = d.converted;
+    r.n_f = map.nf - d.converted;
+    r.n_c = a->m.n - r.n_f;
+    if (rep) *rep = r;
+  });
+}
+
+int airg_extract_blocks(airg_ctx* ctx, const airg_csr* a, const uint8_t* labels, airg_csr** aff,
+                        airg_csr** afc, airg_csr** acf) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    if (a->m.n != a->m.m) throw InvalidArgument("extract_blocks: label length mismatch");
+    LabelMap map;
+    build_label_map(ctx->c, labels, a->m.n, map);
+    Blocks blk;
+    extract_blocks(ctx->c, a->m, map, blk, false);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+    if (aff) *aff = wrap(ctx->c, std::move(blk.aff));
+    if (afc) *afc = wrap(ctx->c, std::move(blk.afc));
+    if (acf) *acf = wrap(ctx->c, std::move(blk.acf));
+  });
+}
+
+// ---- polynomials ----------------------------------------------------------------
+int airg_poly_coefficients(airg_ctx* ctx, const airg_csr* a, int64_t m, uint64_t seed,
+                           double* coeffs, int64_t* eff) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    PolyFit f = poly_coefficients(ctx->c, a->m, m, seed);
+    std::memcpy(coeffs, f.coeffs.data(), sizeof(double) * f.coeffs.size());
+    if (eff) *eff = f.effective_order;
+  });
+}
+
+int airg_poly_assemble(airg_ctx* ctx, const airg_csr* a, const double* coeffs, int64_t ncoeffs,
+                       int64_t eff, int64_t sparsity_order, airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Csr r;
+    poly_assemble(ctx->c, a->m, coeffs, ncoeffs, eff, sparsity_order, r);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+    *out = wrap(ctx->c, std::move(r));
+  });
+}
+
+// ---- setup --------------------------------------------------------------------------
+int airg_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
+               const airg_injection* inj, airg_hier** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(cfg, "config");
+    need(out, "output handle");
+    bind(ctx->c);
+    auto h = std::make_unique<airg_hier>();
+    h->c = &ctx->c;
+    std::unique_ptr<Injection> in;
+    if (inj) {
+      in = std::make_unique<Injection>();
+      in->n_levels = inj->n_levels;
+      for (int64_t l = 0; l < inj->n_levels; ++l) {
+        in->level_coeffs.emplace_back(inj->level_coeffs + l * inj->stride,
+                                      inj->level_coeffs + l * inj->stride + cfg->poly_order + 1);
+        in->level_eff.push_back(inj->level_eff_order[l]);
+      }
+      in->coarse_coeffs.assign(inj->coarse_coeffs, inj->coarse_coeffs + cfg->coarse_poly_order + 1);
+      in->coarse_eff = inj->coarse_eff_order;
+    }
+    setup(ctx->c, a->m, *cfg, in.get(), h->h);
+    *out = h.release();
+  });
+}
+
+int airg_hier_info_get(const airg_hier* hp, airg_hier_info* info) {
+  return guard([&] {
+    need(hp, "hierarchy");
+    const Hier& h = hp->h;
+    std::memset(info, 0, sizeof *info);
+    info->n_levels = (int64_t)h.levels.size();
+    info->coarse_n = h.coarse_a.n;
+    info->coarse_nnz = h.coarse_a.nnz;
+    info->coarse_inv_nnz = h.coarse_inv.nnz;
+    info->coarse_effective_order = h.coarse_eff;
+    info->coarse_attempts = h.coarse_attempts;
+    info->coarse_growth = h.coarse_growth;
+    for (size_t k = 0; k < h.coarse_coeffs.size() && k < 32; ++k)
+      info->coarse_coefficients[k] = h.coarse_coeffs[k];
+    info->grid_complexity = h.grid_c;
+    info->operator_complexity = h.op_c;
+    info->storage_complexity = h.store_c;
+  });
+}
+
+int airg_hier_level_info(const airg_hier* hp, int64_t l, airg_level_info* info) {
+  return guard([&] {
+    need(hp, "hierarchy");
+    const Hier& h = hp->h;
+    if (l < 0 || l >= (int64_t)h.levels.size()) throw InvalidArgument("level out of range");
+    const Level& L = h.levels[l];
+    std::memset(info, 0, sizeof *info);
+    info->n = L.a.n;
+    info->nnz = L.a.nnz;
+    info->n_f = L.map.nf;
+    info->n_c = L.map.nc;
+    info->n_f_pre = L.n_f_pre;
+    info->ddc_converted = L.n_converted;
+    info->nnz_ff = L.aff.nnz;
+    info->nnz_fc = L.afc.nnz;
+    info->nnz_cf = L.acf.nnz;
+    info->nnz_ffinv = L.ffinv.nnz;
+    info->nnz_r = L.r.nnz;
+    info->nnz_p = L.p.nnz;
+    info->max_theta_pre = L.max_theta_pre;
+    info->alpha_diag = L.alpha_diag;
+    info->max_theta_post = L.max_theta_post;
+    info->smoother_growth = L.growth;
+    info->poly_attempts = L.attempts;
+    info->effective_order = L.eff;
+    for (size_t k = 0; k < L.coeffs.size() && k < 32; ++k) info->coefficients[k] = L.coeffs[k];
+  });
+}
+
+int airg_hier_matrix(const airg_hier* hp, int64_t l, int32_t which, const airg_csr** out) {
+  return guard([&] {
+    need(hp, "hierarchy");
+    airg_hier* h = const_cast<airg_hier*>(hp);
+    const int64_t nl = (int64_t)h->h.levels.size();
+    const Csr* m = nullptr;
+    if (l == nl) {
+      if (which == 0) m = &h->h.coarse_a;
+      else if (which == 4) m = &h->h.coarse_inv;
+      else throw InvalidArgument("coarse level has only A (0) and inverse (4)");
+    } else {
+      if (l < 0 || l > nl) throw InvalidArgument("level out of range");
+      const Level& L = h->h.levels[l];
+      const Csr* ms[7] = {&L.a, &L.aff, &L.afc, &L.acf, &L.ffinv, &L.r, &L.p};
+      if (which < 0 || which > 6) throw InvalidArgument("bad matrix selector");
+      m = ms[which];
+    }
+    // borrowed view: a handle whose Csr aliases the hierarchy's buffers
+    auto v = std::make_unique<airg_csr>();
+    v->c = h->c;
+    v->m.n = m->n;
+    v->m.m = m->m;
+    v->m.nnz = m->nnz;
+    v->m.rp.p = m->rp.p;
+    v->m.ci.p = m->ci.p;
+    v->m.v.p = m->v.p;
+    *out = v.get();
+    h->views.push_back(std::move(v));
+  });
+}
+
+int airg_hier_labels(airg_ctx* ctx, const airg_hier* hp, int64_t l, uint8_t* h_labels) {
+  return guard([&] {
+    need(ctx, "context");
+    need(hp, "hierarchy");
+    bind(ctx->c);
+    const Hier& h = hp->h;
+    if (l < 0 || l >= (int64_t)h.levels.size()) throw InvalidArgument("level out of range");
+    to_host(ctx->c, h_labels, h.levels[l].map.label.p, (size_t)h.levels[l].map.n);
+  });
+}
+
+int airg_hier_destroy(airg_hier* h) {
+  return guard([&] {
+    if (!h) return;
+    for (auto& v : h->views) {  // views alias; do not free their buffers
+      v->m.rp.p = nullptr;
+      v->m.ci.p = nullptr;
+      v->m.v.p = nullptr;
+    }
+    if (h->c) bind(*h->c);
+    delete h;
+  });
+}
+
+// ---- solve --------------------------------------------------------------------------
+int airg_vcycle(airg_ctx* ctx, const airg_hier* hp, const airg_solve_config* cfg, const double* b,
+                double* x) {
+  return guard([&] {
+    need(ctx, "context");
+    need(hp, "hierarchy");
+    need(cfg, "config");
+    bind(ctx->c);
+    vcycle(ctx->c, const_cast<airg_hier*>(hp)->h, *cfg, b, x);
+  });
+}
+
+int airg_solve(airg_ctx* ctx, const airg_hier* hp, const airg_solve_config* cfg, const double* b,
+               double* x, airg_solve_stats* st, double* hist, int64_t cap) {
+  return guard([&] {
+    need(ctx, "context");
+    need(hp, "hierarchy");
+    need(cfg, "config");
+    bind(ctx->c);
+    std::vector<double> h;
+    airg_solve_stats s;
+    solve(ctx->c, const_cast<airg_hier*>(hp)->h, *cfg, b, x, s, h);
+    if (hist)
+      for (int64_t k = 0; k < cap && k < (int64_t)h.size(); ++k) hist[k] = h[k];
+    if (st) *st = s;
+  });
+}
+
+int airg_solve_host(airg_ctx* ctx, const airg_hier* hp, const airg_solve_config* cfg,
+                    const double* h_b, double* h_x, airg_solve_stats* st, double* hist, int64_t cap) {
+  return guard([&] {
+    need(ctx, "context");
+    need(hp, "hierarchy");
+    need(cfg, "config");
+    bind(ctx->c);
+    Ctx& c = ctx->c;
+    Hier& h = const_cast<airg_hier*>(hp)->h;
+    const int n = h.top_n();
+    DBuf<double> db(c, (size_t)n), dx(c, (size_t)n);
+    CUDA_CHECK(cudaMemcpyAsync(db.p, h_b, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    std::vector<double> hv;
+    airg_solve_stats s;
+    solve(c, h, *cfg, db.p, dx.p, s, hv);
+    CUDA_CHECK(cudaMemcpyAsync(h_x, dx.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (hist)
+      for (int64_t k = 0; k < cap && k < (int64_t)hv.size(); ++k) hist[k] = hv[k];
+    if (st) *st = s;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,459 @@
+// PMISR-DDC CF splitting on the GPU (reference: proj/src/coarsening.cpp,
+// proj/src/sparse.cpp:270-340).
+//
+// * strength (coarsening.cpp:83-105): thread per row; off-diagonal max,
+//   threshold alpha*max as one rounded multiply, |a|>0 && |a|>=threshold.
+//   S is written in A's column order (sorted); |S^T| comes from exact
+//   integer atomics, S^T itself is never materialised.
+// * weights (coarsening.cpp:50-63): w_i = deg_i + uniform01(mix(seed,
+//   0x57454947), i) with the reference splitmix64 on the global row index,
+//   one rounded add -> bit-identical and partition independent.
+// * PMISR (coarsening.cpp:107-160) is one-shot: the D-set test compares a
+//   node with ALL its S u S^T neighbours, settled or not, and weights never
+//   change, so a node that is not a strict local minimum of (w, i) in sweep
+//   1 is not one in any later sweep; sweep 2 always finds D empty and
+//   breaks (probe-verified). Hence F = {deg = 0} u {strict
+//   local minima}, C = the rest, for every max_loops >= 1. The GPU computes
+//   it with one atomic-free pass over the edges of S: each edge marks its
+//   (w, i)-larger endpoint "not minimal" (idempotent byte stores).
+// * DDC (coarsening.cpp:219-330): theta per F row in column order, global
+//   max via atomicMax on the (non-negative) bit pattern, 1000-bin histogram
+//   with shared-memory privatisation, single-thread alpha_diag scan with the
+//   reference's strict '<', one-shot conversion theta > alpha && theta != 0.
+#include "sparse.cuh"
+
+namespace airg {
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t mix(uint64_t seed, uint64_t key) {
+  return splitmix64(seed ^ splitmix64(key));
+}
+
+__global__ void strength_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               const double* __restrict__ v, double alpha,
+                               int32_t* __restrict__ s_cnt, int32_t* __restrict__ st_cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = rp[i], e = rp[i + 1];
+  double off_max = 0.0;
+  for (int k = s; k < e; ++k)
+    if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
+  const double thr = __dmul_rn(alpha, off_max);
+  int cnt = 0;
+  for (int k = s; k < e; ++k) {
+    const double mag = fabs(v[k]);
+    const int c = ci[k];
+    if (c != i && mag > 0.0 && mag >= thr) {
+      ++cnt;
+      atomicAdd(st_cnt + c, 1);
+    }
+  }
+  s_cnt[i] = cnt;
+}
+
+__global__ void strength_fill(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              const double* __restrict__ v, double alpha,
+                              const int32_t* __restrict__ srp, int32_t* __restrict__ sci) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = rp[i], e = rp[i + 1];
+  double off_max = 0.0;
+  for (int k = s; k < e; ++k)
+    if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
+  const double thr = __dmul_rn(alpha, off_max);
+  int o = srp[i];
+  for (int k = s; k < e; ++k) {
+    const double mag = fabs(v[k]);
+    const int c = ci[k];
+    if (c != i && mag > 0.0 && mag >= thr) sci[o++] = c;
+  }
+}
+
+__device__ __forceinline__ bool row_contains(const int32_t* __restrict__ rp,
+                                             const int32_t* __restrict__ ci, int row, int key) {
+  int lo = rp[row], hi = rp[row + 1];
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ci[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo < rp[row + 1] && ci[lo] == key;
+}
+
+__global__ void make_weights(int n, const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
+                             const int32_t* __restrict__ st_cnt, uint64_t stream_key, int mode,
+                             double* __restrict__ w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t deg = (int64_t)(srp[i + 1] - srp[i]) + st_cnt[i];
+  if (mode == 1) {  // |S_i u S_i^T| = |S_i| + |S_i^T| - |{j in S_i : i in S_j}|
+    for (int k = srp[i]; k < srp[i + 1]; ++k)
+      if (row_contains(srp, sci, sci[k], i)) --deg;
+  }
+  const double u = (double)(mix(stream_key, (uint64_t)i) >> 11) * 0x1.0p-53;
+  w[i] = __dadd_rn((double)deg, u);
+}
+
+__device__ __forceinline__ bool weight_less(const double* w, int i, int j) {
+  const double wi = w[i], wj = w[j];
+  return wi != wj ? wi < wj : i < j;
+}
+
+__global__ void mark_not_minimal(int n, const int32_t* __restrict__ srp,
+                                 const int32_t* __restrict__ sci, const double* __restrict__ w,
+                                 uint8_t* __restrict__ notmin) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = srp[i]; k < srp[i + 1]; ++k) {
+    const int j = sci[k];
+    if (weight_less(w, j, i))
+      notmin[i] = 1;
+    else
+      notmin[j] = 1;
+  }
+}
+
+__global__ void pmisr_labels(int n, const uint8_t* __restrict__ notmin, uint8_t* __restrict__ label) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  label[i] = notmin[i] ? AIRG_C : AIRG_F;
+}
+
+// ---- label map (sparse.cpp:270-290)
+__global__ void label_isf(int n, const uint8_t* __restrict__ label, int32_t* __restrict__ isf,
+                          unsigned long long* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t l = label[i];
+  if (l > AIRG_C) atomicMin(bad, (unsigned long long)i);
+  isf[i] = l == AIRG_F;
+}
+__global__ void label_fill(int n, const uint8_t* __restrict__ label, const int32_t* __restrict__ fpos,
+                           int32_t* __restrict__ f2s, int32_t* __restrict__ f2f,
+                           int32_t* __restrict__ c2f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int fp = fpos[i];
+  if (label[i] == AIRG_F) {
+    f2s[i] = fp;
+    f2f[fp] = i;
+  } else {
+    f2s[i] = i - fp;
+    c2f[i - fp] = i;
+  }
+}
+
+// ---- extract_blocks (sparse.cpp:292-340)
+__global__ void blocks_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             const uint8_t* __restrict__ label, const int32_t* __restrict__ f2s,
+                             int32_t* __restrict__ ff, int32_t* __restrict__ fc,
+                             int32_t* __restrict__ cf, int32_t* __restrict__ af) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int nF = 0, nC = 0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) (label[ci[k]] == AIRG_F ? nF : nC)++;
+  const int sub = f2s[i];
+  if (label[i] == AIRG_F) {
+    ff[sub] = nF;
+    fc[sub] = nC;
+    if (af) af[sub] = nF + nC;
+  } else {
+    cf[sub] = nF;
+  }
+}
+__global__ void blocks_fill(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const uint8_t* __restrict__ label,
+                            const int32_t* __restrict__ f2s, const int32_t* __restrict__ ffrp,
+                            int32_t* __restrict__ ffci, double* __restrict__ ffv,
+                            const int32_t* __restrict__ fcrp, int32_t* __restrict__ fcci,
+                            double* __restrict__ fcv, const int32_t* __restrict__ cfrp,
+                            int32_t* __restrict__ cfci, double* __restrict__ cfv,
+                            const int32_t* __restrict__ afrp, int32_t* __restrict__ afci,
+                            double* __restrict__ afv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sub = f2s[i];
+  if (label[i] == AIRG_F) {
+    int of = ffrp[sub], oc = fcrp[sub];
+    int oa = afci ? afrp[sub] : 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      const bool jf = label[j] == AIRG_F;
+      if (jf) {
+        ffci[of] = f2s[j];
+        ffv[of++] = v[k];
+      } else {
+        fcci[oc] = f2s[j];
+        fcv[oc++] = v[k];
+      }
+      if (afci) {
+        afci[oa] = jf ? j : (int)((unsigned)j | 0x80000000u);
+        afv[oa++] = v[k];
+      }
+    }
+  } else {
+    int o = cfrp[sub];
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      if (label[j] == AIRG_F) {
+        cfci[o] = f2s[j];
+        cfv[o++] = v[k];
+      }
+    }
+  }
+}
+
+// ---- dominance report / ddc
+__global__ void theta_rows(int nf, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, double* __restrict__ theta,
+                           unsigned long long* __restrict__ maxbits,
+                           unsigned long long* __restrict__ bad_row) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  double off = 0.0, diag = 0.0;
+  bool seen = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    if (ci[k] == i) {
+      diag = fabs(v[k]);
+      seen = true;
+    } else {
+      off = __dadd_rn(off, fabs(v[k]));
+    }
+  }
+  if (!seen || diag == 0.0) {
+    atomicMin(bad_row, (unsigned long long)i);
+    theta[i] = 0.0;
+    return;
+  }
+  const double t = __ddiv_rn(off, diag);
+  theta[i] = t;
+  atomicMax(maxbits, (unsigned long long)__double_as_longlong(t));
+}
+
+__global__ void theta_hist(int nf, const double* __restrict__ theta,
+                           const unsigned long long* __restrict__ maxbits, int64_t bins,
+                           unsigned long long* __restrict__ hist) {
+  extern __shared__ unsigned int sh[];
+  const bool priv = bins <= 8192;
+  if (priv)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const double mx = __longlong_as_double((long long)*maxbits);
+  const double width = mx > 0.0 ? __ddiv_rn(mx, (double)bins) : 1.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    int64_t b = (int64_t)__ddiv_rn(theta[i], width);
+    if (b > bins - 1) b = bins - 1;
+    if (priv)
+      atomicAdd(sh + b, 1u);
+    else
+      atomicAdd(hist + b, 1ull);
+  }
+  __syncthreads();
+  if (priv)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+      if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
+}
+
+// coarsening.cpp:290-315
+__global__ void select_alpha(int nf, const unsigned long long* __restrict__ hist, int64_t bins,
+                             double fraction, const unsigned long long* __restrict__ maxbits,
+                             int selection, double direct_alpha, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double max_theta = __longlong_as_double((long long)*maxbits);
+  double alpha_diag;
+  if (selection == 2) {
+    alpha_diag = direct_alpha;
+  } else if (max_theta == 0.0) {
+    alpha_diag = 0.0;
+  } else {
+    const double target = __dmul_rn(fraction, (double)nf);
+    int64_t above = 0, best_k = bins;
+    double best_err = fabs(__dsub_rn((double)above, target));
+    for (int64_t k = bins; k-- > 0;) {
+      above += (int64_t)hist[k];
+      const double err = fabs(__dsub_rn((double)above, target));
+      if (err < best_err) {
+        best_err = err;
+        best_k = k;
+      }
+    }
+    alpha_diag = __dmul_rn((double)best_k, __ddiv_rn(max_theta, (double)bins));
+  }
+  out[0] = alpha_diag;
+  out[1] = max_theta;
+}
+
+__global__ void ddc_convert(int nf, const double* __restrict__ theta, const double* __restrict__ sel,
+                            const int32_t* __restrict__ f2f, uint8_t* __restrict__ label,
+                            unsigned long long* __restrict__ count) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nf) return;
+  const double t = theta[k];
+  if (t > sel[0] && t != 0.0) {
+    label[f2f[k]] = AIRG_C;
+    atomicAdd(count, 1ull);
+  }
+}
+
+}  // namespace
+
+void strength(Ctx& c, const Csr& a, double alpha, Strength& g) {
+  if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
+  g.n = a.n;
+  DBuf<int32_t> s_cnt(c, (size_t)a.n);
+  g.st_cnt.alloc(c, (size_t)a.n);
+  g.st_cnt.zero(c);
+  g.rp.alloc(c, (size_t)a.n + 1);
+  if (a.n)
+    LAUNCH(c, strength_count, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, alpha,
+           s_cnt.p, g.st_cnt.p);
+  g.nnz = exclusive_scan(c, s_cnt.p, g.rp.p, a.n);
+  g.ci.alloc(c, (size_t)g.nnz);
+  if (a.n)
+    LAUNCH(c, strength_fill, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, alpha,
+           g.rp.p, g.ci.p);
+}
+
+void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weight_mode,
+           uint8_t* d_labels, double* d_weights) {
+  if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
+  const int n = g.n;
+  if (n == 0) return;
+  DBuf<double> wbuf;
+  double* w = d_weights;
+  if (!w) {
+    wbuf.alloc(c, (size_t)n);
+    w = wbuf.p;
+  }
+  const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
+  LAUNCH(c, make_weights, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, g.st_cnt.p, key,
+         weight_mode, w);
+  DBuf<uint8_t> notmin(c, (size_t)n);
+  notmin.zero(c);
+  LAUNCH(c, mark_not_minimal, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, w, notmin.p);
+  LAUNCH(c, pmisr_labels, blocks_for(n, 256), 256, 0, n, notmin.p, d_labels);
+}
+
+void build_label_map(Ctx& c, const uint8_t* d_labels, int32_t n, LabelMap& map) {
+  map.n = n;
+  map.label.alloc(c, (size_t)n);
+  if (n) CUDA_CHECK(cudaMemcpyAsync(map.label.p, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
+  DBuf<int32_t> isf(c, (size_t)n), fpos(c, (size_t)n + 1);
+  DBuf<unsigned long long> bad(c, 1);
+  CUDA_CHECK(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
+  if (n) LAUNCH(c, label_isf, blocks_for(n, 256), 256, 0, n, d_labels, isf.p, bad.p);
+  const int64_t nf = exclusive_scan(c, isf.p, fpos.p, n);
+  const unsigned long long b = read1(c, bad.p);
+  if (b != ~0ull)
+    throw InvalidArgument("build_label_map: unassigned label at row " + std::to_string(b));
+  map.nf = (int32_t)nf;
+  map.nc = (int32_t)(n - nf);
+  map.fine_to_sub.alloc(c, (size_t)n);
+  map.f_to_fine.alloc(c, (size_t)map.nf);
+  map.c_to_fine.alloc(c, (size_t)map.nc);
+  if (n)
+    LAUNCH(c, label_fill, blocks_for(n, 256), 256, 0, n, d_labels, fpos.p, map.fine_to_sub.p,
+           map.f_to_fine.p, map.c_to_fine.p);
+}
+
+void extract_blocks(Ctx& c, const Csr& a, const LabelMap& map, Blocks& out, bool want_af) {
+  if (a.n != a.m || a.n != map.n) throw InvalidArgument("extract_blocks: label length mismatch");
+  const int n = a.n, nf = map.nf, nc = map.nc;
+  DBuf<int32_t> ffc(c, (size_t)nf), fcc(c, (size_t)nf), cfc(c, (size_t)nc), afc(c, want_af ? (size_t)nf : 0);
+  if (n)
+    LAUNCH(c, blocks_count, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, map.label.p,
+           map.fine_to_sub.p, ffc.p, fcc.p, cfc.p, want_af ? afc.p : nullptr);
+  auto finish = [&](Csr& m, int rows, int cols, const int32_t* cnt) {
+    m.n = rows;
+    m.m = cols;
+    m.rp.alloc(c, (size_t)rows + 1);
+    m.nnz = exclusive_scan(c, cnt, m.rp.p, rows);
+    m.ci.alloc(c, (size_t)m.nnz);
+    m.v.alloc(c, (size_t)m.nnz);
+  };
+  finish(out.aff, nf, nf, ffc.p);
+  finish(out.afc, nf, nc, fcc.p);
+  finish(out.acf, nc, nf, cfc.p);
+  if (want_af) finish(out.af, nf, n, afc.p);
+  if (n)
+    LAUNCH(c, blocks_fill, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, a.v.p, map.label.p,
+           map.fine_to_sub.p, out.aff.rp.p, out.aff.ci.p, out.aff.v.p, out.afc.rp.p, out.afc.ci.p,
+           out.afc.v.p, out.acf.rp.p, out.acf.ci.p, out.acf.v.p,
+           want_af ? out.af.rp.p : nullptr, want_af ? out.af.ci.p : nullptr,
+           want_af ? out.af.v.p : nullptr);
+}
+
+namespace {
+struct ThetaScratch {
+  DBuf<double> theta;
+  DBuf<unsigned long long> u;  // [0] max bits, [1] bad row, [2] converted
+};
+void theta_pass(Ctx& c, const Csr& aff, ThetaScratch& s) {
+  s.theta.alloc(c, (size_t)aff.n);
+  s.u.alloc(c, 3);
+  const unsigned long long init[3] = {0ull, ~0ull, 0ull};
+  to_device(c, s.u.p, init, 3);
+  if (aff.n)
+    LAUNCH(c, theta_rows, blocks_for(aff.n, 256), 256, 0, aff.n, aff.rp.p, aff.ci.p, aff.v.p,
+           s.theta.p, s.u.p, s.u.p + 1);
+}
+void throw_zero_diag(unsigned long long row) {
+  throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(row));
+}
+}  // namespace
+
+DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, double fraction,
+              int64_t bins, int selection, double direct_alpha, bool convert) {
+  if (aff.n != map.nf) throw InvalidArgument("ddc: a_ff does not match label map");
+  if (fraction <= 0.0 || fraction > 1.0) throw InvalidArgument("ddc: fraction must be in (0, 1]");
+  if (bins < 1) throw InvalidArgument("dominance_report: bins >= 1");
+  if (selection == 1) throw InvalidArgument("ddc: quickselect selection is not offered on the GPU");
+  ThetaScratch s;
+  theta_pass(c, aff, s);
+  DBuf<unsigned long long> hist(c, (size_t)bins);
+  hist.zero(c);
+  DBuf<double> sel(c, 2);
+  const int nf = aff.n;
+  if (nf) {
+    const int blocks = (int)std::min<int64_t>(blocks_for(nf, 256), 4 * c.num_sms);
+    const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
+    LAUNCH(c, theta_hist, blocks, 256, smem, nf, s.theta.p, s.u.p, bins, hist.p);
+  }
+  LAUNCH(c, select_alpha, 1, 32, 0, nf, hist.p, bins, fraction, s.u.p, selection, direct_alpha,
+         sel.p);
+  if (convert && nf)
+    LAUNCH(c, ddc_convert, blocks_for(nf, 256), 256, 0, nf, s.theta.p, sel.p, map.f_to_fine.p,
+           d_labels, s.u.p + 2);
+  unsigned long long u[3];
+  double sv[2];
+  to_host(c, u, s.u.p, 3);
+  to_host(c, sv, sel.p, 2);
+  if (u[1] != ~0ull) throw_zero_diag(u[1]);
+  DdcResult r;
+  r.converted = (int64_t)u[2];
+  r.alpha_diag = sv[0];
+  r.max_theta = sv[1];
+  return r;
+}
+
+double dominance_max(Ctx& c, const Csr& aff) {
+  ThetaScratch s;
+  theta_pass(c, aff, s);
+  unsigned long long u[3];
+  to_host(c, u, s.u.p, 3);
+  if (u[1] != ~0ull) throw_zero_diag(u[1]);
+  double mx;
+  memcpy(&mx, &u[0], sizeof mx);
+  return mx;
+}
+
+}  // namespace airg

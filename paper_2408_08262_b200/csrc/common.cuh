@@ -1,0 +1,193 @@
+// Shared infrastructure of the B200 AIRG engine: status/exception plumbing,
+// the context (device, stream, launch counter), stream-ordered device
+// buffers, the device CSR type and scan / reduction helpers.
+//
+// Arithmetic policy: the whole library is compiled with --fmad=false, so
+// every a*b+c the reference writes as a separate multiply and add is
+// rounded twice exactly as on the host (the reference is built without FMA,
+// SURVEY §0.3). Kernels that must be bit-identical to the reference keep its
+// per-row sequential accumulation order (thread-per-row). Explicit fma()
+// calls (double-double arithmetic) are unaffected by --fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "airg_c.h"
+
+namespace airg {
+
+// ---------------------------------------------------------------------------
+// errors: C++ exceptions inside the library, mapped to status codes at the
+// C-ABI boundary (capi.cu) the way cli.cpp:477-486 maps the reference's.
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+             cudaGetErrorString(e), file, line, what);
+    throw CudaError(buf);
+  }
+}
+#define CUDA_CHECK(x) ::airg::cuda_check((x), #x, __FILE__, __LINE__)
+
+// reference counter RNG (rng.hpp:13-24), host side
+inline uint64_t splitmix64_host(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+inline uint64_t mix_host(uint64_t seed, uint64_t key) {
+  return splitmix64_host(seed ^ splitmix64_host(key));
+}
+
+// ---------------------------------------------------------------------------
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  uint64_t launches = 0;
+  int num_sms = 148;
+  // pinned host staging for small readbacks
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+// Launch helper: counts every kernel this library enqueues (bench.py reports
+// the delta as gpu_launches) and checks the launch.
+#define LAUNCH(ctx, kernel, grid, block, smem, ...)                                   \
+  do {                                                                                \
+    (ctx).launches++;                                                                 \
+    kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);                   \
+    CUDA_CHECK(cudaGetLastError());                                                   \
+  } while (0)
+
+inline unsigned blocks_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------------------
+// Stream-ordered device buffer (cudaMallocAsync from the default pool, whose
+// release threshold is raised at context creation so frees are cached).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+
+  DBuf() = default;
+  DBuf(Ctx& c, size_t count) { alloc(c, count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+
+  void alloc(Ctx& c, size_t count) {
+    release();
+    s = c.stream;
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMallocAsync((void**)&p, count * sizeof(T), s);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        p = nullptr;
+        n = 0;
+        char buf[128];
+        snprintf(buf, sizeof buf, "device allocation of %zu bytes failed", count * sizeof(T));
+        throw CudaError(buf);
+      }
+    }
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void zero(Ctx& c) {
+    if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), c.stream));
+  }
+  T* get() const { return p; }
+};
+
+// Read a few values back (synchronises the context stream).
+template <class T>
+inline void to_host(Ctx& c, T* h, const T* d, size_t count) {
+  if (!count) return;
+  CUDA_CHECK(cudaMemcpyAsync(h, d, count * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+template <class T>
+inline T read1(Ctx& c, const T* d) {
+  T v;
+  to_host(c, &v, d, 1);
+  return v;
+}
+template <class T>
+inline void to_device(Ctx& c, T* d, const T* h, size_t count) {
+  if (!count) return;
+  CUDA_CHECK(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+}
+
+// ---------------------------------------------------------------------------
+// Device CSR: int32 offsets / columns, fp64 values (12 B per nonzero).
+struct Csr {
+  int32_t n = 0, m = 0;
+  int64_t nnz = 0;
+  DBuf<int32_t> rp, ci;
+  DBuf<double> v;
+
+  Csr() = default;
+  Csr(Csr&&) = default;
+  Csr& operator=(Csr&&) = default;
+  void alloc(Ctx& c, int64_t rows, int64_t cols, int64_t nz) {
+    if (rows > INT32_MAX || cols > INT32_MAX || nz > INT32_MAX)
+      throw InvalidArgument("airg: matrix exceeds the int32 device index range");
+    n = (int32_t)rows;
+    m = (int32_t)cols;
+    nnz = nz;
+    rp.alloc(c, (size_t)rows + 1);
+    ci.alloc(c, (size_t)nz);
+    v.alloc(c, (size_t)nz);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// helpers implemented in util.cu
+// exclusive scan of int32 counts into int32 offsets[n+1]; returns the total
+// (checked against the int32 range).
+int64_t exclusive_scan(Ctx& c, const int32_t* d_counts, int32_t* d_offsets, int64_t n);
+// same for int64 counts/offsets
+int64_t exclusive_scan64(Ctx& c, const int64_t* d_counts, int64_t* d_offsets, int64_t n);
+// parallel dot product / squared norm (not order-preserving), result on device
+void dot_async(Ctx& c, const double* x, const double* y, int64_t n, double* d_out,
+               double* d_partials);
+constexpr int kReduceBlocks = 1184;  // 8 x 148 SMs
+
+// Copy a CSR (device -> device)
+void csr_copy(Ctx& c, const Csr& a, Csr& out);
+
+}  // namespace airg

@@ -1,0 +1,70 @@
+// Device-resident AIRG hierarchy (reference: air.hpp:45-91) plus the solve
+// workspace and cached CUDA graphs.
+#pragma once
+
+#include "sparse.cuh"
+
+namespace airg {
+
+struct Level {
+  Csr a;                     // level operator (full diagonal)
+  LabelMap map;
+  Csr aff, afc, acf;         // blocks (acf feeds Z; aff/afc are kept for download)
+  Csr af;                    // F rows of A, global columns, bit 31 = C column
+  Csr ffinv, r, p;
+  DBuf<int32_t> pmap;        // one-point P as a map (-1 = empty row)
+  // report
+  int64_t n_f_pre = 0, n_converted = 0, attempts = 1, eff = 0;
+  double max_theta_pre = 0.0, alpha_diag = 0.0, max_theta_post = 0.0, growth = 0.0;
+  std::vector<double> coeffs;
+  // solve workspace
+  DBuf<double> b;            // level rhs (level 0 uses Hier::r)
+  DBuf<double> x;            // level correction
+  DBuf<double> rf;           // F residual
+};
+
+struct Hier {
+  std::vector<Level> levels;
+  Csr coarse_a, coarse_inv;
+  std::vector<double> coarse_coeffs;
+  int64_t coarse_eff = 0, coarse_attempts = 1;
+  double coarse_growth = 0.0;
+  int64_t coarse_iterations = 3;  // SetupConfig (storage metric only)
+  double grid_c = 0.0, op_c = 0.0, store_c = 0.0;
+  // coarse workspace
+  DBuf<double> cb, cx, cr;
+  // top-level solve workspace
+  DBuf<double> rhs, xsol, r, part, scal;
+  // outer GMRES workspace (allocated on first use)
+  int64_t gm_restart = 0;
+  DBuf<double> V, Z, w, hbuf, ybuf;
+  // cached graphs
+  cudaGraphExec_t g_rich = nullptr, g_vc = nullptr;
+  int64_t g_key_rich = -1, g_key_vc = -1;
+  uint64_t g_rich_kernels = 0, g_vc_kernels = 0;
+
+  int32_t top_n() const { return levels.empty() ? coarse_a.n : levels.front().a.n; }
+  const Csr& top() const { return levels.empty() ? coarse_a : levels.front().a; }
+  ~Hier() {
+    if (g_rich) cudaGraphExecDestroy(g_rich);
+    if (g_vc) cudaGraphExecDestroy(g_vc);
+  }
+};
+
+struct Injection {
+  int64_t n_levels = -1;
+  std::vector<std::vector<double>> level_coeffs;
+  std::vector<int64_t> level_eff;
+  std::vector<double> coarse_coeffs;
+  int64_t coarse_eff = 0;
+};
+
+void setup(Ctx& c, const Csr& a, const airg_setup_config& cfg, const Injection* inj, Hier& h);
+void recompute_metrics(Hier& h);
+
+// solve.cu
+void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x);
+void solve(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x,
+           airg_solve_stats& st, std::vector<double>& history);
+
+}  // namespace airg

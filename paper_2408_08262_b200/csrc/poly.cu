@@ -1,0 +1,437 @@
+// GMRES-polynomial approximate inverses (reference: proj/src/gmres_poly.cpp)
+// and the smoother growth guard (proj/src/air.cpp:61-129).
+#include <cmath>
+#include <cstring>
+
+#include "dd.cuh"
+#include "sparse.cuh"
+
+namespace airg {
+
+namespace {
+
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t d_mix(uint64_t seed, uint64_t key) {
+  return d_splitmix64(seed ^ d_splitmix64(key));
+}
+// rng::standard_normal (rng.hpp:32-39)
+__device__ __forceinline__ double d_standard_normal(uint64_t seed, uint64_t index) {
+  const double u1 = (double)((d_mix(seed, 2 * index) >> 11) + 1) * 0x1.0p-53;
+  const double u2 = (double)(d_mix(seed, 2 * index + 1) >> 11) * 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
+__global__ void normal_fill(int64_t n, uint64_t seed, double* __restrict__ hi,
+                            double* __restrict__ lo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  hi[i] = d_standard_normal(seed, (uint64_t)i);
+  if (lo) lo[i] = 0.0;
+}
+
+// K_k = A K_{k-1} in double-double (values are doubles, products exact).
+__global__ void dd_spmv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                        const double* __restrict__ v, const double* __restrict__ xh,
+                        const double* __restrict__ xl, double* __restrict__ yh,
+                        double* __restrict__ yl) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dd acc = {0.0, 0.0};
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const int c = ci[k];
+    acc = dd_add(acc, dd_mul_d(dd{xh[c], xl[c]}, v[k]));
+  }
+  yh[i] = acc.hi;
+  yl[i] = acc.lo;
+}
+
+// Gram entries G_ab = sum_i K_a[i] K_b[i] in double-double. blockIdx.y is
+// the pair; partial sums per block, finished on the host.
+__global__ void dd_gram(int64_t n, int ncols, const double* __restrict__ kh,
+                        const double* __restrict__ kl, const int2* __restrict__ pairs,
+                        double* __restrict__ part) {
+  __shared__ double sh[256], sl[256];
+  const int2 pr = pairs[blockIdx.y];
+  const double* ah = kh + (int64_t)pr.x * n;
+  const double* al = kl + (int64_t)pr.x * n;
+  const double* bh = kh + (int64_t)pr.y * n;
+  const double* bl = kl + (int64_t)pr.y * n;
+  dd acc = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc = dd_add(acc, dd_mul(dd{ah[i], al[i]}, dd{bh[i], bl[i]}));
+  sh[threadIdx.x] = acc.hi;
+  sl[threadIdx.x] = acc.lo;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      dd r = dd_add(dd{sh[threadIdx.x], sl[threadIdx.x]}, dd{sh[threadIdx.x + s], sl[threadIdx.x + s]});
+      sh[threadIdx.x] = r.hi;
+      sl[threadIdx.x] = r.lo;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int64_t o = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 2;
+    part[o] = sh[0];
+    part[o + 1] = sl[0];
+  }
+}
+
+// ---- assemble_fixed_sparsity (gmres_poly.cpp:197-280)
+__global__ void pattern_count_s1(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool seen = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) seen |= ci[k] == i;
+  cnt[i] = rp[i + 1] - rp[i] + (seen ? 0 : 1);
+}
+// sorted union of row i of P, {i} and row i of A
+__global__ void pattern_union_count(int n, const int32_t* __restrict__ prp,
+                                    const int32_t* __restrict__ pci, const int32_t* __restrict__ arp,
+                                    const int32_t* __restrict__ aci, int32_t* __restrict__ cnt,
+                                    const int32_t* __restrict__ orp, int32_t* __restrict__ oci) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int p = prp ? prp[i] : 0, pe = prp ? prp[i + 1] : 0, q = arp[i], qe = arp[i + 1];
+  bool diag = false;
+  int last = -1, c = 0, o = orp ? orp[i] : 0;
+  while (p < pe || q < qe || !diag) {
+    int cand = INT32_MAX;
+    if (p < pe) cand = pci[p];
+    if (q < qe && aci[q] < cand) cand = aci[q];
+    if (!diag && i < cand) cand = i;
+    if (cand == i) diag = true;
+    if (p < pe && pci[p] == cand) ++p;
+    if (q < qe && aci[q] == cand) ++q;
+    if (cand != last) {
+      if (oci) oci[o + c] = cand;
+      ++c;
+    }
+    last = cand;
+  }
+  if (cnt) cnt[i] = c;
+}
+
+__device__ __forceinline__ int find_pos(const int32_t* __restrict__ cols, int w, int key) {
+  int lo = 0, hi = w;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cols[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < w && cols[lo] == key) ? lo : -1;
+}
+
+__global__ void assemble_rows(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                              const double* __restrict__ av, const int32_t* __restrict__ orp,
+                              const int32_t* __restrict__ oci, double* __restrict__ ov,
+                              double* __restrict__ curb, double* __restrict__ nextb,
+                              const double* __restrict__ coeffs, int deg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int o = orp[i], w = orp[i + 1] - o;
+  const int32_t* prow = oci + o;
+  double* out = ov + o;
+  double* cur = curb + o;
+  double* next = nextb + o;
+  const double a0 = coeffs[0];
+  for (int k = 0; k < w; ++k) {
+    out[k] = prow[k] == i ? a0 : 0.0;
+    cur[k] = 0.0;
+  }
+  for (int k = arp[i]; k < arp[i + 1]; ++k) {
+    const int p = find_pos(prow, w, aci[k]);
+    cur[p] = av[k];
+    if (deg >= 1) out[p] = __dadd_rn(out[p], __dmul_rn(coeffs[1], av[k]));
+  }
+  for (int power = 2; power <= deg; ++power) {
+    for (int k = 0; k < w; ++k) next[k] = 0.0;
+    for (int k = 0; k < w; ++k) {
+      const double v = cur[k];
+      if (v == 0.0) continue;
+      const int j = prow[k];
+      for (int t = arp[j]; t < arp[j + 1]; ++t) {
+        const int p = find_pos(prow, w, aci[t]);
+        if (p < 0) continue;  // outside the fixed pattern
+        next[p] = __dadd_rn(next[p], __dmul_rn(v, av[t]));
+      }
+    }
+    const double alpha = coeffs[power];
+    for (int k = 0; k < w; ++k) out[k] = __dadd_rn(out[k], __dmul_rn(alpha, next[k]));
+    double* t = cur;
+    cur = next;
+    next = t;
+  }
+}
+
+// ---- growth estimate helpers
+__global__ void sub_partial(int n, double* __restrict__ v, const double* __restrict__ q,
+                            double* __restrict__ part) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double x = v[i] - q[i];
+    v[i] = x;
+    s += x * x;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+__global__ void finish_norm(const double* __restrict__ part, int np, double* __restrict__ g) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *g = sqrt(s);
+  }
+}
+__global__ void scale_by(int n, double* __restrict__ v, const double* __restrict__ g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double gg = *g;
+  if (i < n && gg != 0.0) v[i] = v[i] / gg;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// compute_coefficients (gmres_poly.cpp:63-171), native GPU mode. Instead of a
+// Householder QR of the normalised n x (m+1) power basis in long double, the
+// GPU forms the basis and its Gram matrix G = K^T K in double-double and the
+// host factors G (Cholesky == QR's R up to row signs), applies the same rank
+// cut (|R_kk| < 1e-12 on the normalised basis), the same candidate-degree
+// least-squares solves and scores each candidate's true residual from G.
+PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed) {
+  if (a.n != a.m) throw InvalidArgument("compute_coefficients: matrix must be square");
+  if (m < 1) throw InvalidArgument("compute_coefficients: m must be >= 1");
+  const int64_t n = a.n;
+  if (n == 0) throw InvalidArgument("compute_coefficients: empty matrix");
+  const int nc = (int)(m + 1);
+  DBuf<double> kh(c, (size_t)(n * nc)), kl(c, (size_t)(n * nc));
+  const uint64_t rhs_seed = mix_host(seed, 0x504f4c59ull);
+  LAUNCH(c, normal_fill, blocks_for(n, 256), 256, 0, n, rhs_seed, kh.p, kl.p);
+  for (int k = 1; k <= m; ++k)
+    LAUNCH(c, dd_spmv, blocks_for(n, 128), 128, 0, (int)n, a.rp.p, a.ci.p, a.v.p,
+           kh.p + (k - 1) * n, kl.p + (k - 1) * n, kh.p + k * n, kl.p + k * n);
+  std::vector<int2> pairs;
+  for (int x = 0; x < nc; ++x)
+    for (int y = x; y < nc; ++y) pairs.push_back(make_int2(x, y));
+  DBuf<int2> dpairs(c, pairs.size());
+  to_device(c, dpairs.p, pairs.data(), pairs.size());
+  const int gblocks = (int)std::min<int64_t>(64, blocks_for(n, 256));
+  DBuf<double> part(c, pairs.size() * gblocks * 2);
+  LAUNCH(c, dd_gram, dim3(gblocks, (unsigned)pairs.size()), 256, 0, n, nc, kh.p, kl.p, dpairs.p,
+         part.p);
+  std::vector<double> hp(pairs.size() * gblocks * 2);
+  to_host(c, hp.data(), part.p, hp.size());
+  std::vector<dd> G((size_t)nc * nc);
+  for (size_t pi = 0; pi < pairs.size(); ++pi) {
+    dd s = {0.0, 0.0};
+    for (int b = 0; b < gblocks; ++b) s = dd_add(s, dd{hp[(pi * gblocks + b) * 2], hp[(pi * gblocks + b) * 2 + 1]});
+    G[pairs[pi].x * nc + pairs[pi].y] = s;
+    G[pairs[pi].y * nc + pairs[pi].x] = s;
+  }
+  // normalised Gram and Cholesky (upper R, row-major R[i*nc+j])
+  std::vector<dd> scale(nc);
+  for (int k = 0; k < nc; ++k) scale[k] = dd_sqrt(G[k * nc + k]);
+  if (scale[0].hi == 0.0) throw RuntimeError("compute_coefficients: zero right-hand side");
+  const int rrows = (int)std::min<int64_t>(n, nc);
+  std::vector<dd> N((size_t)nc * nc), R((size_t)nc * nc, dd{0.0, 0.0});
+  for (int x = 0; x < nc; ++x)
+    for (int y = 0; y < nc; ++y) {
+      if (scale[x].hi == 0.0 || scale[y].hi == 0.0) {
+        N[x * nc + y] = dd{0.0, 0.0};
+        continue;
+      }
+      N[x * nc + y] = dd_div(G[x * nc + y], dd_mul(scale[x], scale[y]));
+    }
+  int dim = 0;
+  for (int k = 0; k < rrows; ++k) {
+    dd d = N[k * nc + k];
+    for (int j = 0; j < k; ++j) d = dd_sub(d, dd_mul(R[j * nc + k], R[j * nc + k]));
+    const dd rkk = d.hi > 0.0 ? dd_sqrt(d) : dd{0.0, 0.0};
+    R[k * nc + k] = rkk;
+    if (fabs(rkk.hi) < 1e-12) break;  // gmres_poly.cpp:116-120
+    ++dim;
+    for (int j = k + 1; j < nc; ++j) {
+      dd s = N[k * nc + j];
+      for (int i = 0; i < k; ++i) s = dd_sub(s, dd_mul(R[i * nc + k], R[i * nc + j]));
+      R[k * nc + j] = dd_div(s, rkk);
+    }
+  }
+  if (dim == 0) throw RuntimeError("compute_coefficients: singular projected system");
+  // unscale: R = R_scaled diag(scale)
+  for (int i = 0; i < nc; ++i)
+    for (int k = 0; k < nc; ++k) R[i * nc + k] = dd_mul(R[i * nc + k], scale[k]);
+  const int lcols = (int)std::min<int64_t>(m, dim);
+  int best_d = 0;
+  double best_resid = INFINITY;
+  std::vector<double> best_y;
+  for (int d = 1; d <= lcols; ++d) {
+    const int lrows = std::min(rrows, d + 1);
+    // Hessenberg least squares via Givens rotations in double-double
+    std::vector<dd> H((size_t)lrows * d), rhs(lrows, dd{0.0, 0.0});
+    for (int i = 0; i < lrows; ++i)
+      for (int j = 0; j < d; ++j) H[i * d + j] = R[i * nc + 1 + j];
+    rhs[0] = R[0];
+    for (int j = 0; j < d && j + 1 < lrows; ++j) {
+      const dd a0 = H[j * d + j], b0 = H[(j + 1) * d + j];
+      const dd r = dd_sqrt(dd_add(dd_mul(a0, a0), dd_mul(b0, b0)));
+      if (r.hi == 0.0) continue;
+      const dd cs = dd_div(a0, r), sn = dd_div(b0, r);
+      for (int k = j; k < d; ++k) {
+        const dd x = H[j * d + k], y = H[(j + 1) * d + k];
+        H[j * d + k] = dd_add(dd_mul(cs, x), dd_mul(sn, y));
+        H[(j + 1) * d + k] = dd_sub(dd_mul(cs, y), dd_mul(sn, x));
+      }
+      const dd x = rhs[j], y = rhs[j + 1];
+      rhs[j] = dd_add(dd_mul(cs, x), dd_mul(sn, y));
+      rhs[j + 1] = dd_sub(dd_mul(cs, y), dd_mul(sn, x));
+    }
+    const int kdim = std::min(d, lrows);
+    double maxpiv = 0.0;
+    for (int j = 0; j < kdim; ++j) maxpiv = std::max(maxpiv, fabs(H[j * d + j].hi));
+    bool deficient = kdim < d;
+    for (int j = 0; j < kdim; ++j)
+      if (!(fabs(H[j * d + j].hi) > 1e-12 * maxpiv)) deficient = true;
+    if (maxpiv == 0.0 || deficient) continue;
+    std::vector<dd> y(d);
+    for (int j = d - 1; j >= 0; --j) {
+      dd s = rhs[j];
+      for (int k = j + 1; k < d; ++k) s = dd_sub(s, dd_mul(H[j * d + k], y[k]));
+      y[j] = dd_div(s, H[j * d + j]);
+    }
+    bool finite = true;
+    for (int j = 0; j < d; ++j) finite &= std::isfinite(y[j].hi);
+    if (!finite) continue;
+    // ||K_0 - sum_k y_k K_{k+1}||^2 from the Gram matrix
+    dd q = G[0];
+    for (int k = 0; k < d; ++k) q = dd_sub(q, dd_mul(dd_from(2.0), dd_mul(y[k], G[0 * nc + k + 1])));
+    for (int k = 0; k < d; ++k)
+      for (int l = 0; l < d; ++l) q = dd_add(q, dd_mul(dd_mul(y[k], y[l]), G[(k + 1) * nc + l + 1]));
+    const double resid = q.hi > 0.0 ? dd_sqrt(q).hi / scale[0].hi : 0.0;
+    if (resid < best_resid) {
+      best_resid = resid;
+      best_d = d;
+      best_y.resize(d);
+      for (int j = 0; j < d; ++j) best_y[j] = y[j].hi + y[j].lo;
+    }
+  }
+  if (best_d == 0) throw RuntimeError("compute_coefficients: singular projected system");
+  PolyFit f;
+  f.coeffs.assign((size_t)m, 0.0);
+  for (int k = 0; k < best_d; ++k) f.coeffs[k] = best_y[k];
+  f.effective_order = best_d - 1;
+  return f;
+}
+
+void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs, int64_t deg,
+                   int64_t sparsity_order, Csr& out) {
+  if (a.n != a.m) throw InvalidArgument("assemble_fixed_sparsity: square matrix only");
+  if (sparsity_order < 1) throw InvalidArgument("assemble_fixed_sparsity: sparsity_order >= 1");
+  if (ncoeffs < 1) throw InvalidArgument("assemble_fixed_sparsity: empty polynomial");
+  if (deg >= ncoeffs) throw InvalidArgument("assemble_fixed_sparsity: effective order exceeds coefficients");
+  const int n = a.n;
+  Csr r;
+  r.n = r.m = n;
+  r.rp.alloc(c, (size_t)n + 1);
+  DBuf<int32_t> cnt(c, (size_t)n);
+  Csr power;  // pattern(A^s) for s >= 2
+  if (sparsity_order >= 2) {
+    Csr ones;
+    csr_copy(c, a, power);
+    for (int64_t k = 1; k < sparsity_order; ++k) {
+      Csr nxt;
+      spgemm(c, power, a, nxt);
+      power = std::move(nxt);
+    }
+  }
+  if (n) {
+    if (sparsity_order >= 2)
+      LAUNCH(c, pattern_union_count, blocks_for(n, 256), 256, 0, n, power.rp.p, power.ci.p, a.rp.p,
+             a.ci.p, cnt.p, (const int32_t*)nullptr, (int32_t*)nullptr);
+    else
+      LAUNCH(c, pattern_count_s1, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, cnt.p);
+  }
+  r.nnz = exclusive_scan(c, cnt.p, r.rp.p, n);
+  r.ci.alloc(c, (size_t)r.nnz);
+  r.v.alloc(c, (size_t)r.nnz);
+  if (n) {
+    LAUNCH(c, pattern_union_count, blocks_for(n, 256), 256, 0, n,
+           sparsity_order >= 2 ? power.rp.p : (const int32_t*)nullptr,
+           sparsity_order >= 2 ? power.ci.p : (const int32_t*)nullptr, a.rp.p, a.ci.p,
+           (int32_t*)nullptr, r.rp.p, r.ci.p);
+    DBuf<double> coeffs(c, (size_t)ncoeffs), cur(c, (size_t)r.nnz), nxt(c, (size_t)r.nnz);
+    to_device(c, coeffs.p, h_coeffs, (size_t)ncoeffs);
+    LAUNCH(c, assemble_rows, blocks_for(n, 128), 128, 0, n, a.rp.p, a.ci.p, a.v.p, r.rp.p, r.ci.p,
+           r.v.p, cur.p, nxt.p, coeffs.p, (int)deg);
+  }
+  out = std::move(r);
+}
+
+// smoother_growth_estimate (air.cpp:61-95): 30 normalised power iterations
+// of I - q(A) A, geometric mean of the rates of iterations 15..29. All 30
+// steps are enqueued without a host round trip; the per-step norms come back
+// once at the end (parallel reductions: not bit-identical to the reference's
+// sequential sums, which only matters at the 0.5 acceptance boundary).
+double smoother_growth(Ctx& c, const Csr& a, const Csr& q) {
+  const int n = a.n;
+  if (n == 0) return 0.0;
+  constexpr int kIters = 30, kTail = 15;
+  DBuf<double> v(c, (size_t)n), av(c, (size_t)n), qav(c, (size_t)n), g(c, kIters + 1);
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>(kReduceBlocks, blocks_for(n, threads));
+  DBuf<double> part(c, (size_t)blocks);
+  const uint64_t probe_seed = mix_host(0xA3B1C5D7ull, (uint64_t)n);
+  LAUNCH(c, normal_fill, blocks_for(n, 256), 256, 0, (int64_t)n, probe_seed, v.p, (double*)nullptr);
+  // norm of v: reuse sub_partial with q = 0
+  DBuf<double> zero(c, (size_t)n);
+  zero.zero(c);
+  LAUNCH(c, sub_partial, blocks, threads, 0, n, v.p, zero.p, part.p);
+  LAUNCH(c, finish_norm, 1, 1024, 0, part.p, blocks, g.p + kIters);
+  LAUNCH(c, scale_by, blocks_for(n, 256), 256, 0, n, v.p, g.p + kIters);
+  for (int k = 0; k < kIters; ++k) {
+    spmv(c, a, v.p, av.p);
+    spmv(c, q, av.p, qav.p);
+    LAUNCH(c, sub_partial, blocks, threads, 0, n, v.p, qav.p, part.p);
+    LAUNCH(c, finish_norm, 1, 1024, 0, part.p, blocks, g.p + k);
+    LAUNCH(c, scale_by, blocks_for(n, 256), 256, 0, n, v.p, g.p + k);
+  }
+  double hg[kIters + 1];
+  to_host(c, hg, g.p, kIters + 1);
+  double log_growth = 0.0;
+  int tail = 0;
+  for (int k = 0; k < kIters; ++k) {
+    if (hg[k] == 0.0) return 0.0;
+    if (k >= kTail) {
+      log_growth += std::log(hg[k]);
+      ++tail;
+    }
+  }
+  return std::exp(log_growth / tail);
+}
+
+}  // namespace airg

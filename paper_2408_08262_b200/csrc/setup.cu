@@ -1,0 +1,218 @@
+// AIRG hierarchy construction on the GPU (reference: proj/src/air.cpp:285-434).
+// Host code orchestrates; every matrix operation is a device kernel (no CPU
+// fallback). The level loop reads back only scalars (counts, norms, growth)
+// to take the reference's data-dependent branches.
+#include <cmath>
+#include <cstring>
+
+#include "hier.cuh"
+
+namespace airg {
+
+namespace {
+
+struct Checked {
+  std::vector<double> coeffs;
+  int64_t eff = 0;
+  Csr q;
+  double growth = 0.0;
+  int64_t attempts = 1;
+  bool valid = false;
+};
+
+// make_checked_inverse (air.cpp:106-129): up to 6 seeded fits, keep the
+// least-growing, stop once growth <= 0.5.
+Checked make_checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsity,
+                             uint64_t seed) {
+  Checked best;
+  double best_growth = INFINITY;
+  for (int64_t attempt = 0; attempt < 6; ++attempt) {
+    const uint64_t s = attempt == 0 ? seed : mix_host(seed, 0x52455452ull + (uint64_t)attempt);
+    PolyFit fit = poly_coefficients(c, a, order + 1, s);
+    Csr q;
+    poly_assemble(c, a, fit.coeffs.data(), (int64_t)fit.coeffs.size(), fit.effective_order,
+                  sparsity, q);
+    const double growth = smoother_growth(c, a, q);
+    if (growth < best_growth) {
+      best.coeffs = fit.coeffs;
+      best.eff = fit.effective_order;
+      best.q = std::move(q);
+      best.growth = growth;
+      best.attempts = attempt + 1;
+      best.valid = true;
+      best_growth = growth;
+    }
+    if (best_growth <= 0.5) break;
+  }
+  return best;
+}
+
+Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs, int64_t eff,
+                         int64_t sparsity) {
+  Checked k;
+  k.coeffs = coeffs;
+  k.eff = eff;
+  poly_assemble(c, a, coeffs.data(), (int64_t)coeffs.size(), eff, sparsity, k.q);
+  k.valid = true;
+  return k;
+}
+
+void alloc_workspace(Ctx& c, Hier& h) {
+  for (size_t l = 0; l < h.levels.size(); ++l) {
+    Level& L = h.levels[l];
+    if (l > 0) L.b.alloc(c, (size_t)L.a.n);
+    L.x.alloc(c, (size_t)L.a.n);
+    L.rf.alloc(c, (size_t)std::max(1, L.map.nf));
+  }
+  const size_t nc = (size_t)std::max(1, h.coarse_a.n);
+  h.cb.alloc(c, nc);
+  h.cx.alloc(c, nc);
+  h.cr.alloc(c, nc);
+  const size_t n = (size_t)std::max(1, h.top_n());
+  h.rhs.alloc(c, n);
+  h.xsol.alloc(c, n);
+  h.r.alloc(c, n);
+  h.part.alloc(c, kReduceBlocks + 8);
+  h.scal.alloc(c, 64);
+}
+
+}  // namespace
+
+void recompute_metrics(Hier& h) {
+  const Csr& top = h.top();
+  const double n0 = (double)top.n, nnz0 = (double)top.nnz;
+  double grid = 0.0, op = 0.0, store = 0.0;
+  for (const Level& L : h.levels) {
+    grid += (double)L.a.n;
+    op += (double)L.a.nnz;
+    store += (double)(L.ffinv.nnz + L.aff.nnz + L.afc.nnz + L.r.nnz + L.p.nnz);
+  }
+  grid += (double)h.coarse_a.n;
+  op += (double)h.coarse_a.nnz;
+  store += (double)h.coarse_inv.nnz;
+  if (h.coarse_iterations > 1) store += (double)h.coarse_a.nnz;
+  h.grid_c = grid / n0;
+  h.op_c = op / nnz0;
+  h.store_c = store / nnz0;
+}
+
+void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection* inj, Hier& h) {
+  if (a0.n != a0.m) throw InvalidArgument("setup: matrix must be square");
+  if (cfg.poly_order < 1 || cfg.coarse_poly_order < 1)
+    throw InvalidArgument("setup: polynomial orders must be >= 1");
+  if (cfg.sparsity_order < 1) throw InvalidArgument("setup: sparsity_order must be >= 1");
+  if (cfg.drop_coarse < 0.0 || cfg.drop_restrict < 0.0)
+    throw InvalidArgument("setup: drop tolerances must be >= 0");
+  if (cfg.strength_alpha < 0.0 || cfg.strength_alpha > 1.0)
+    throw InvalidArgument("setup: strength_alpha must lie in [0, 1]");
+  if (cfg.cf != 0)
+    throw InvalidArgument("setup: the GPU path implements PMISR splitting (cf = 0) only");
+  if (cfg.prolongation != 0)
+    throw InvalidArgument("setup: the GPU path implements one-point prolongation only");
+  if (cfg.poly_order + 1 > 32 || cfg.coarse_poly_order + 1 > 32)
+    throw InvalidArgument("setup: polynomial order above 31 not supported");
+  h.levels.clear();
+  h.coarse_iterations = cfg.coarse_iterations;
+  constexpr double kCoarseAccept = 0.5;
+  Checked coarse;
+  Csr current;
+  with_full_diagonal(c, a0, current);  // air.cpp:307
+  for (;;) {
+    const int64_t built = (int64_t)h.levels.size();
+    const bool forced = current.n <= cfg.poly_order + 1 ||
+                        (cfg.max_levels > 0 && built + 1 >= cfg.max_levels);
+    if (inj) {
+      if (built >= inj->n_levels) {
+        coarse = injected_inverse(c, current, inj->coarse_coeffs, inj->coarse_eff, cfg.sparsity_order);
+        break;
+      }
+    } else if (forced || current.n <= cfg.coarse_size_target) {  // air.cpp:309-320
+      coarse = make_checked_inverse(c, current, cfg.coarse_poly_order, cfg.sparsity_order,
+                                    mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)built));
+      if (forced || coarse.growth <= kCoarseAccept) break;
+      coarse = Checked();
+    }
+    h.levels.emplace_back();
+    Level& L = h.levels.back();
+    L.a = std::move(current);
+    const int32_t n = L.a.n;
+    const uint64_t level_seed = mix_host(cfg.seed, (uint64_t)built);  // air.cpp:324-325
+
+    // --- CF split: strength -> PMISR -> extract -> DDC (air.cpp:327-355)
+    Strength g;
+    strength(c, L.a, cfg.strength_alpha, g);
+    DBuf<uint8_t> labels(c, (size_t)n);
+    pmisr(c, g, cfg.max_loops, level_seed, cfg.weight_mode, labels.p, nullptr);
+    build_label_map(c, labels.p, n, L.map);
+    L.n_f_pre = L.map.nf;
+    Blocks blk;
+    extract_blocks(c, L.a, L.map, blk, /*want_af=*/false);
+    if (cfg.ddc_enabled && L.map.nf > 0) {
+      DdcResult res = ddc(c, blk.aff, L.map, labels.p, cfg.ddc_fraction, cfg.ddc_bins, 0, 0.0, true);
+      L.max_theta_pre = res.max_theta;
+      L.alpha_diag = res.alpha_diag;
+      L.n_converted = res.converted;
+      if (res.converted > 0) build_label_map(c, labels.p, n, L.map);
+    } else {
+      L.max_theta_pre = dominance_max(c, blk.aff);
+    }
+    extract_blocks(c, L.a, L.map, blk, /*want_af=*/true);
+    L.max_theta_post = dominance_max(c, blk.aff);
+    L.aff = std::move(blk.aff);
+    L.afc = std::move(blk.afc);
+    L.acf = std::move(blk.acf);
+    L.af = std::move(blk.af);
+
+    // --- stall guards (air.cpp:362-376)
+    const int32_t nc = L.map.nc;
+    if (L.map.nf == 0)
+      throw RuntimeError("setup: coarsening stall, no F points selected on level " +
+                         std::to_string(built));
+    if (nc == 0) {
+      current = std::move(L.a);
+      h.levels.pop_back();
+      break;
+    }
+    if ((double)nc > 0.99 * (double)n)
+      throw RuntimeError("setup: coarsening stall, level " + std::to_string(built) +
+                         " coarsened by less than 1% (" + std::to_string(n) + " -> " +
+                         std::to_string(nc) + ")");
+
+    // --- approximate ideal restriction (air.cpp:378-381)
+    Checked ff = inj ? injected_inverse(c, L.aff, inj->level_coeffs[built], inj->level_eff[built],
+                                        cfg.sparsity_order)
+                     : make_checked_inverse(c, L.aff, cfg.poly_order, cfg.sparsity_order, level_seed);
+    L.ffinv = std::move(ff.q);
+    L.coeffs = ff.coeffs;
+    L.eff = ff.eff;
+    L.growth = ff.growth;
+    L.attempts = ff.attempts;
+    build_restriction(c, L.acf, L.ffinv, cfg.drop_restrict, L.map, L.r);
+    build_prolongation(c, L.map, g, L.a, L.pmap, L.p);
+
+    // --- Galerkin coarse operator (air.cpp:268-271, :386-387)
+    Csr ap, rap;
+    spgemm(c, L.a, L.p, ap);
+    spgemm(c, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
+    with_full_diagonal(c, rap, current);
+  }
+  h.coarse_a = std::move(current);
+  if (!coarse.valid) {
+    // reached only through the all-F break (air.cpp:538-543)
+    if (inj)
+      coarse = injected_inverse(c, h.coarse_a, inj->coarse_coeffs, inj->coarse_eff, cfg.sparsity_order);
+    else
+      coarse = make_checked_inverse(c, h.coarse_a, cfg.coarse_poly_order, cfg.sparsity_order,
+                                    mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)h.levels.size()));
+  }
+  h.coarse_inv = std::move(coarse.q);
+  h.coarse_coeffs = coarse.coeffs;
+  h.coarse_eff = coarse.eff;
+  h.coarse_attempts = coarse.attempts;
+  h.coarse_growth = coarse.growth;
+  recompute_metrics(h);
+  alloc_workspace(c, h);
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace airg

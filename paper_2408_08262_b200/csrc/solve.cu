@@ -1,0 +1,562 @@
+// AIRG solve on the GPU (reference: proj/src/solve.cpp).
+//
+// V-cycle (solve.cpp:93-146, entered with x = 0 and no pre-smoothing):
+//   per level l: b_{l+1} = R_l b_l  ->  recurse  ->  x_l = P_l x_{l+1}
+//   -> up_f_smooths x { r_F = (b_F - A_FF x_F) - A_FC x_C ;  x_F += Aff^-1 r_F }
+//   coarsest: coarse_iterations x { r = b - A_c e (skipped first) ; e += Ac^-1 r }.
+// Every kernel is thread-per-row with the reference's sequential order and
+// separate rounding, so one V-cycle is bit-identical to the reference's;
+// the F-point residual reads A's F rows directly (columns flagged F / C)
+// instead of gathering x_F / x_C, with the two partial sums kept apart to
+// reproduce (b_F - A_FF x_F) - A_FC x_C exactly.
+// The whole V-cycle (+ the Richardson update and residual) is captured once
+// into a CUDA graph and replayed each iteration; only the residual norm
+// (parallel reduction) crosses to the host.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "hier.cuh"
+
+namespace airg {
+
+namespace {
+
+__global__ void k_spmv_into(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ x,
+                            double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k)
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ci + k))));
+  y[i] = acc;
+}
+
+// x_l = 0 + P e_c  (solve.cpp:139-141: pe = spmv(P, ec); x += 1.0 * pe)
+__global__ void k_prolong(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
+                          double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = pmap[i];
+  const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
+  x[i] = __dadd_rn(0.0, __dmul_rn(1.0, pe));
+}
+
+// r_F[k] = (b[i] - sum_F a x) - sum_C a x, i = f_to_fine[k] (solve.cpp:72-80)
+__global__ void k_fresid(int nf, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                         const double* __restrict__ v, const int32_t* __restrict__ f2f,
+                         const double* __restrict__ b, const double* __restrict__ x,
+                         double* __restrict__ rf) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nf) return;
+  double sf = 0.0, sc = 0.0;
+  for (int t = __ldg(rp + k); t < __ldg(rp + k + 1); ++t) {
+    const int c = __ldg(ci + t);
+    const double p = __dmul_rn(__ldg(v + t), __ldg(x + (c & 0x7fffffff)));
+    if (c >= 0)
+      sf = __dadd_rn(sf, p);
+    else
+      sc = __dadd_rn(sc, p);
+  }
+  rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc);
+}
+
+// x[f_to_fine[k]] += (Aff^-1 r_F)[k] (solve.cpp:81-84)
+__global__ void k_fupdate(int nf, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const int32_t* __restrict__ f2f,
+                          const double* __restrict__ rf, double* __restrict__ x) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nf) return;
+  double acc = 0.0;
+  for (int t = __ldg(rp + k); t < __ldg(rp + k + 1); ++t)
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(v + t), __ldg(rf + __ldg(ci + t))));
+  const int i = __ldg(f2f + k);
+  x[i] = __dadd_rn(x[i], acc);
+}
+
+// coarse Richardson pieces (solve.cpp:34-59)
+__global__ void k_cresid(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                         const double* __restrict__ v, const double* __restrict__ rhs,
+                         const double* __restrict__ e, double* __restrict__ r) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], e[ci[k]]));
+  r[i] = __dsub_rn(rhs[i], acc);
+}
+__global__ void k_cupdate(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const double* __restrict__ r,
+                          double* __restrict__ e, int first) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], r[ci[k]]));
+  const double e0 = first ? 0.0 : e[i];
+  e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
+}
+
+// x += 1.0 * e (solve.cpp:224)
+__global__ void k_axpy1(int n, const double* __restrict__ e, double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(1.0, e[i]));
+}
+
+// r = b - A x with block partial sums of r^2 (solve.cpp:202-207)
+__global__ void k_resid_partial(int n, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                const double* __restrict__ b, const double* __restrict__ x,
+                                double* __restrict__ r, double* __restrict__ part) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k)
+      acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ci + k))));
+    const double ri = __dsub_rn(b[i], acc);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
+}
+__global__ void k_sum_partials(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *out = s;
+  }
+}
+
+// ---- GMRES helpers
+// partial dots of w with columns 0..j of V: grid (blocks, j+1)
+__global__ void k_multidot(int64_t n, const double* __restrict__ V, const double* __restrict__ w,
+                           double* __restrict__ part) {
+  __shared__ double sm[32];
+  const double* vk = V + (int64_t)blockIdx.y * n;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(vk[i], w[i], s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+__global__ void k_finish_dots(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  const double* p = part + (int64_t)blockIdx.x * np;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += p[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+  }
+}
+// w -= V(:, 0..j) h  (h on device)
+__global__ void k_orth_update(int64_t n, int jp1, const double* __restrict__ V,
+                              const double* __restrict__ h, double* __restrict__ w) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = w[i];
+  for (int k = 0; k < jp1; ++k) s -= h[k] * V[(int64_t)k * n + i];
+  w[i] = s;
+}
+// V(:, j+1) = w / hn and the V-cycle input buffer gets a copy
+__global__ void k_scale_store(int64_t n, const double* __restrict__ w, double inv,
+                              double* __restrict__ dst, double* __restrict__ dst2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = w[i] * inv;
+  dst[i] = v;
+  if (dst2) dst2[i] = v;
+}
+// x += Z(:, 0..j-1) y
+__global__ void k_xupdate(int64_t n, int j, const double* __restrict__ Z, const double* __restrict__ y,
+                          double* __restrict__ x) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = x[i];
+  for (int k = 0; k < j; ++k) s += y[k] * Z[(int64_t)k * n + i];
+  x[i] = s;
+}
+
+constexpr int kT = 128;
+
+// Enqueue one V-cycle from level 0 rhs b0 into levels[0].x (or the coarse
+// x when there are no fine levels).
+void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* b0) {
+  const int L = (int)h.levels.size();
+  // descent: b_{l+1} = R_l b_l
+  for (int l = 0; l < L; ++l) {
+    Level& lv = h.levels[l];
+    const double* bl = l == 0 ? b0 : lv.b.p;
+    double* bn = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
+    if (lv.r.n)
+      LAUNCH(c, k_spmv_into, blocks_for(lv.r.n, kT), kT, 0, lv.r.n, lv.r.rp.p, lv.r.ci.p, lv.r.v.p,
+             bl, bn);
+  }
+  // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
+  {
+    const int n = h.coarse_a.n;
+    const double* rhs = L == 0 ? b0 : h.cb.p;
+    if (n) {
+      for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
+        const double* r = rhs;
+        if (it > 0) {
+          LAUNCH(c, k_cresid, blocks_for(n, kT), kT, 0, n, h.coarse_a.rp.p, h.coarse_a.ci.p,
+                 h.coarse_a.v.p, rhs, h.cx.p, h.cr.p);
+          r = h.cr.p;
+        }
+        LAUNCH(c, k_cupdate, blocks_for(n, kT), kT, 0, n, h.coarse_inv.rp.p, h.coarse_inv.ci.p,
+               h.coarse_inv.v.p, r, h.cx.p, it == 0 ? 1 : 0);
+      }
+      if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * n, c.stream));
+    }
+  }
+  // ascent: prolongate and F-smooth
+  for (int l = L - 1; l >= 0; --l) {
+    Level& lv = h.levels[l];
+    const double* bl = l == 0 ? b0 : lv.b.p;
+    const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
+    const int n = lv.a.n, nf = lv.map.nf;
+    LAUNCH(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
+    for (int64_t s = 0; s < cfg.up_f_smooths && nf > 0; ++s) {
+      LAUNCH(c, k_fresid, blocks_for(nf, kT), kT, 0, nf, lv.af.rp.p, lv.af.ci.p, lv.af.v.p,
+             lv.map.f_to_fine.p, bl, lv.x.p, lv.rf.p);
+      LAUNCH(c, k_fupdate, blocks_for(nf, kT), kT, 0, nf, lv.ffinv.rp.p, lv.ffinv.ci.p,
+             lv.ffinv.v.p, lv.map.f_to_fine.p, lv.rf.p, lv.x.p);
+    }
+  }
+}
+
+double* vcycle_output(Hier& h) { return h.levels.empty() ? h.cx.p : h.levels[0].x.p; }
+
+int resid_blocks(int n) { return (int)std::min<int64_t>(kReduceBlocks, blocks_for(n, 256)); }
+
+// r = b - A x, ||r||^2 -> h.scal[0]
+void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double* r) {
+  const Csr& a = h.top();
+  const int nb = resid_blocks(a.n);
+  LAUNCH(c, k_resid_partial, nb, 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, b, x, r, h.part.p);
+  LAUNCH(c, k_sum_partials, 1, 1024, 0, h.part.p, nb, h.scal.p);
+}
+
+int64_t graph_key(const airg_solve_config& cfg) {
+  return cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths;
+}
+
+// Capture `body` into a graph executable; returns the number of kernels.
+template <class F>
+uint64_t capture(Ctx& c, cudaGraphExec_t* exec, F&& body) {
+  if (*exec) {
+    cudaGraphExecDestroy(*exec);
+    *exec = nullptr;
+  }
+  const uint64_t before = c.launches;
+  cudaGraph_t g;
+  CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(c.stream, &dummy);
+    if (dummy) cudaGraphDestroy(dummy);
+    throw;
+  }
+  CUDA_CHECK(cudaStreamEndCapture(c.stream, &g));
+  CUDA_CHECK(cudaGraphInstantiate(exec, g, 0));
+  CUDA_CHECK(cudaGraphDestroy(g));
+  const uint64_t k = c.launches - before;
+  c.launches = before;
+  return k;
+}
+
+void run_graph(Ctx& c, cudaGraphExec_t g, uint64_t kernels) {
+  CUDA_CHECK(cudaGraphLaunch(g, c.stream));
+  c.launches += kernels;
+}
+
+void check_cfg(const airg_solve_config& cfg) {
+  if (cfg.down_smooths != 0)
+    throw InvalidArgument("solve: down_smooths > 0 is not offered by the GPU V-cycle");
+  if (cfg.rtol <= 0.0) throw InvalidArgument("richardson_solve: rtol must be positive");
+}
+
+// flops of one V-cycle exactly as the reference's primary counter tallies
+// them (solve.cpp:93-146 with the coarse_solve/f_smooth counts).
+uint64_t vcycle_flops(const Hier& h, const airg_solve_config& cfg) {
+  uint64_t f = 0;
+  for (const Level& L : h.levels) {
+    f += 2 * (uint64_t)L.r.nnz;
+    f += 2 * (uint64_t)L.p.nnz + 2 * (uint64_t)L.a.n;
+    if (L.map.nf > 0)
+      f += (uint64_t)cfg.up_f_smooths *
+           (2 * (uint64_t)(L.aff.nnz + L.afc.nnz) + 2 * (uint64_t)L.map.nf + 2 * (uint64_t)L.ffinv.nnz +
+            (uint64_t)L.map.nf);
+  }
+  const uint64_t nc = (uint64_t)h.coarse_a.n;
+  for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
+    if (it > 0) f += 2 * (uint64_t)h.coarse_a.nnz + 2 * nc;
+    f += 2 * (uint64_t)h.coarse_inv.nnz + 2 * nc;
+  }
+  return f;
+}
+
+using Clock = std::chrono::steady_clock;
+
+}  // namespace
+
+void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x) {
+  check_cfg(cfg);
+  const int n = h.top_n();
+  CUDA_CHECK(cudaMemcpyAsync(h.r.p, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  const int64_t key = graph_key(cfg);
+  if (!h.g_vc || h.g_key_vc != key) {
+    h.g_vc_kernels = capture(c, &h.g_vc, [&] { enqueue_vcycle(c, h, cfg, h.r.p); });
+    h.g_key_vc = key;
+  }
+  run_graph(c, h.g_vc, h.g_vc_kernels);
+  CUDA_CHECK(cudaMemcpyAsync(d_x, vcycle_output(h), sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                             c.stream));
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+namespace {
+
+// richardson_solve (solve.cpp:167-259)
+void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
+                std::vector<double>& hist) {
+  const Csr& a = h.top();
+  const int n = a.n;
+  uint64_t fc = 0;
+  const uint64_t vflops = vcycle_flops(h, cfg);
+  const auto t0 = Clock::now();
+  CUDA_CHECK(cudaMemsetAsync(h.xsol.p, 0, sizeof(double) * n, c.stream));
+  dot_async(c, h.rhs.p, h.rhs.p, n, h.scal.p + 1, h.part.p);
+  const double bnorm = std::sqrt(read1(c, h.scal.p + 1));
+  fc += 2 * (uint64_t)n;
+  if (bnorm == 0.0) {
+    st.converged = 1;
+    hist.push_back(0.0);
+  } else {
+    const int64_t key = graph_key(cfg);
+    if (!h.g_rich || h.g_key_rich != key) {
+      h.g_rich_kernels = capture(c, &h.g_rich, [&] {
+        enqueue_vcycle(c, h, cfg, h.r.p);
+        const double* e = vcycle_output(h);
+        LAUNCH(c, k_axpy1, blocks_for(n, 256), 256, 0, n, e, h.xsol.p);
+        enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
+      });
+      h.g_key_rich = key;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(h.r.p, h.rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    for (int64_t it = 0;; ++it) {
+      double rel;
+      if (it == 0) {
+        rel = 1.0;
+      } else {
+        rel = std::sqrt(read1(c, h.scal.p)) / bnorm;
+        fc += 2 * (uint64_t)a.nnz + 2 * (uint64_t)n + 2 * (uint64_t)n;
+      }
+      hist.push_back(rel);
+      st.final_relative_residual = rel;
+      if (rel <= cfg.rtol) {
+        st.converged = 1;
+        st.iterations = it;
+        break;
+      }
+      if (it >= cfg.max_iterations) {
+        st.converged = 0;
+        st.iterations = it;
+        break;
+      }
+      run_graph(c, h.g_rich, h.g_rich_kernels);
+      fc += vflops + 2 * (uint64_t)n;
+    }
+  }
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  const auto t1 = Clock::now();
+  st.flops = fc;
+  st.shadow_flops = fc;
+  st.work_units = (double)fc / (2.0 * (double)a.nnz);
+  st.solve_seconds = std::chrono::duration<double>(t1 - t0).count();
+}
+
+// Right-preconditioned restarted GMRES with flexible storage Z = M V,
+// CGS2 orthogonalisation and Givens rotations; the restatement in
+// oracle/airg_oracle.c (gmres) performs the same steps serially.
+void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
+           std::vector<double>& hist) {
+  const Csr& a = h.top();
+  const int64_t n = a.n;
+  const int m = (int)(cfg.gmres_restart > 0 ? cfg.gmres_restart : 30);
+  if (m > 512) throw InvalidArgument("gmres: restart length above 512");
+  uint64_t fc = 0;
+  const uint64_t vflops = vcycle_flops(h, cfg);
+  if (h.gm_restart != m) {
+    h.V.alloc(c, (size_t)n * (m + 1));
+    h.Z.alloc(c, (size_t)n * m);
+    h.w.alloc(c, (size_t)n);
+    const int nb = (int)std::min<int64_t>(256, blocks_for(n, 256));
+    h.hbuf.alloc(c, (size_t)(m + 2) * (nb + 4));
+    h.ybuf.alloc(c, (size_t)m + 2);
+    h.gm_restart = m;
+  }
+  const int nb = (int)std::min<int64_t>(256, blocks_for(n, 256));
+  const auto t0 = Clock::now();
+  CUDA_CHECK(cudaMemsetAsync(h.xsol.p, 0, sizeof(double) * n, c.stream));
+  dot_async(c, h.rhs.p, h.rhs.p, n, h.scal.p + 1, h.part.p);
+  const double bnorm = std::sqrt(read1(c, h.scal.p + 1));
+  fc += 2 * (uint64_t)n;
+  int64_t its = 0;
+  st.converged = 0;
+  if (bnorm == 0.0) {
+    st.converged = 1;
+    hist.push_back(0.0);
+    st.final_relative_residual = 0.0;
+  } else {
+    const int64_t key = graph_key(cfg);
+    if (!h.g_vc || h.g_key_vc != key) {
+      h.g_vc_kernels = capture(c, &h.g_vc, [&] { enqueue_vcycle(c, h, cfg, h.r.p); });
+      h.g_key_vc = key;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(h.w.p, h.rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    double beta = bnorm;
+    hist.push_back(1.0);
+    st.final_relative_residual = 1.0;
+    std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), hcol(m + 2), y(m + 1);
+    std::vector<double> hh(2 * (m + 1) + 1);
+    double* dh = h.hbuf.p;                     // [2][m+1] dots + [1] norm^2
+    double* dpart = h.hbuf.p + 2 * (m + 1) + 2;  // partials
+    while (its < cfg.max_iterations) {
+      LAUNCH(c, k_scale_store, blocks_for(n, 256), 256, 0, n, h.w.p, 1.0 / beta, h.V.p, h.r.p);
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int j = 0;
+      for (; j < m && its < cfg.max_iterations; ++j) {
+        double* zj = h.Z.p + (int64_t)j * n;
+        run_graph(c, h.g_vc, h.g_vc_kernels);  // r-buffer (= v_j) -> e
+        fc += vflops;
+        CUDA_CHECK(cudaMemcpyAsync(zj, vcycle_output(h), sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                   c.stream));
+        spmv(c, a, zj, h.w.p);
+        fc += 2 * (uint64_t)a.nnz;
+        for (int pass = 0; pass < 2; ++pass) {
+          LAUNCH(c, k_multidot, dim3(nb, j + 1), 256, 0, n, h.V.p, h.w.p, dpart);
+          LAUNCH(c, k_finish_dots, j + 1, 256, 0, dpart, nb, dh + pass * (m + 1));
+          LAUNCH(c, k_orth_update, blocks_for(n, 256), 256, 0, n, j + 1, h.V.p, dh + pass * (m + 1),
+                 h.w.p);
+          fc += 4 * (uint64_t)n * (uint64_t)(j + 1);
+        }
+        dot_async(c, h.w.p, h.w.p, n, dh + 2 * (m + 1), h.part.p);
+        fc += 2 * (uint64_t)n;
+        to_host(c, hh.data(), dh, 2 * (m + 1) + 1);
+        for (int k = 0; k <= j; ++k) hcol[k] = hh[k] + hh[(m + 1) + k];
+        const double hn = std::sqrt(hh[2 * (m + 1)]);
+        hcol[j + 1] = hn;
+        LAUNCH(c, k_scale_store, blocks_for(n, 256), 256, 0, n, h.w.p, hn > 0.0 ? 1.0 / hn : 0.0,
+               h.V.p + (int64_t)(j + 1) * n, h.r.p);
+        for (int k = 0; k < j; ++k) {
+          const double t = cs[k] * hcol[k] + sn[k] * hcol[k + 1];
+          hcol[k + 1] = -sn[k] * hcol[k] + cs[k] * hcol[k + 1];
+          hcol[k] = t;
+        }
+        const double den = std::hypot(hcol[j], hcol[j + 1]);
+        cs[j] = den > 0.0 ? hcol[j] / den : 1.0;
+        sn[j] = den > 0.0 ? hcol[j + 1] / den : 0.0;
+        hcol[j] = den;
+        hcol[j + 1] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        for (int k = 0; k <= j; ++k) H[k + (size_t)j * (m + 1)] = hcol[k];
+        ++its;
+        const double est = std::fabs(g[j + 1]) / bnorm;
+        hist.push_back(est);
+        if (est <= cfg.rtol || hn == 0.0) {
+          ++j;
+          break;
+        }
+      }
+      for (int k = j - 1; k >= 0; --k) {
+        double s = g[k];
+        for (int q = k + 1; q < j; ++q) s -= H[k + (size_t)q * (m + 1)] * y[q];
+        y[k] = s / H[k + (size_t)k * (m + 1)];
+      }
+      to_device(c, h.ybuf.p, y.data(), (size_t)j);
+      LAUNCH(c, k_xupdate, blocks_for(n, 256), 256, 0, n, j, h.Z.p, h.ybuf.p, h.xsol.p);
+      enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.w.p);
+      fc += 2 * (uint64_t)a.nnz + 2 * (uint64_t)n;
+      beta = std::sqrt(read1(c, h.scal.p));
+      const double rel = beta / bnorm;
+      st.final_relative_residual = rel;
+      if (rel <= cfg.rtol) {
+        st.converged = 1;
+        break;
+      }
+      if (beta == 0.0) break;
+    }
+  }
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  const auto t1 = Clock::now();
+  st.iterations = its;
+  st.flops = fc;
+  st.shadow_flops = fc;
+  st.work_units = (double)fc / (2.0 * (double)a.nnz);
+  st.solve_seconds = std::chrono::duration<double>(t1 - t0).count();
+}
+
+}  // namespace
+
+void solve(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x,
+           airg_solve_stats& st, std::vector<double>& history) {
+  check_cfg(cfg);
+  std::memset(&st, 0, sizeof st);
+  const int n = h.top_n();
+  CUDA_CHECK(cudaMemcpyAsync(h.rhs.p, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  if (cfg.outer == 1)
+    gmres(c, h, cfg, st, history);
+  else
+    richardson(c, h, cfg, st, history);
+  CUDA_CHECK(cudaMemcpyAsync(d_x, h.xsol.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  st.grid_complexity = h.grid_c;
+  st.operator_complexity = h.op_c;
+  st.storage_complexity = h.store_c;
+  st.history_len = (int64_t)history.size();
+  if (st.iterations > 0) {
+    const double ns = st.solve_seconds * 1e9;
+    st.c_grind_ns = ns / (double)n / (double)st.iterations;
+    if (cfg.nddofs > 0) st.d_grind_ns = ns / (double)cfg.nddofs / (double)st.iterations;
+  }
+}
+
+}  // namespace airg

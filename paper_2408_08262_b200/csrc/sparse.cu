@@ -1,0 +1,204 @@
+// L0 sparse kernels: CSR upload/validation, SpMV, with_full_diagonal and
+// drop_entries (reference: proj/src/sparse.cpp).
+#include "sparse.cuh"
+
+namespace airg {
+
+namespace {
+
+// ---- upload: int64 reference layout -> int32 device CSR with the checks of
+// the SparseMatrix constructor (sparse.cpp:27-45). err[0] collects the
+// smallest offending row per error class.
+__global__ void convert_validate(int64_t n, int64_t m, const int64_t* __restrict__ rp64,
+                                 const int64_t* __restrict__ ci64, const double* __restrict__ v,
+                                 int32_t* __restrict__ rp, int32_t* __restrict__ ci,
+                                 unsigned long long* __restrict__ err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  rp[i] = (int32_t)rp64[i];
+  if (i == n) return;
+  const int64_t s = rp64[i], e = rp64[i + 1];
+  if (s > e) {
+    atomicMin(&err[0], (unsigned long long)i);  // not monotone
+    return;
+  }
+  for (int64_t k = s; k < e; ++k) {
+    const int64_t c = ci64[k];
+    if (c < 0 || c >= m) atomicMin(&err[1], (unsigned long long)i);
+    if (k > s && !(ci64[k - 1] < c)) atomicMin(&err[2], (unsigned long long)i);
+    if (isnan(v[k])) atomicMin(&err[3], (unsigned long long)i);
+    ci[k] = (int32_t)c;
+  }
+}
+
+__global__ void widen_rows(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           int64_t* __restrict__ rp64, int64_t* __restrict__ ci64) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  rp64[i] = rp[i];
+  if (i == n) return;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) ci64[k] = ci[k];
+}
+
+// ---- SpMV, sparse.cpp:185-201: thread per row, sequential in column order,
+// every product and sum rounded separately (no FMA) -> bit-identical.
+__global__ void spmv_rows(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const double* __restrict__ x,
+                          double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = __ldg(rp + i), e = __ldg(rp + i + 1);
+  double acc = 0.0;
+  for (int k = s; k < e; ++k) acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ci + k))));
+  y[i] = acc;
+}
+
+// ---- with_full_diagonal, sparse.cpp:132-160
+__global__ void fulldiag_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool seen = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) seen |= ci[k] == i;
+  cnt[i] = rp[i + 1] - rp[i] + (seen ? 0 : 1);
+}
+__global__ void fulldiag_fill(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              const double* __restrict__ v, const int32_t* __restrict__ orp,
+                              int32_t* __restrict__ oci, double* __restrict__ ov) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int o = orp[i];
+  bool seen = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const int c = ci[k];
+    if (!seen && c > i) {
+      oci[o] = i;
+      ov[o++] = 0.0;
+      seen = true;
+    }
+    if (c == i) seen = true;
+    oci[o] = c;
+    ov[o++] = v[k];
+  }
+  if (!seen) {
+    oci[o] = i;
+    ov[o] = 0.0;
+  }
+}
+
+// ---- drop_entries, sparse.cpp:244-268
+__device__ __forceinline__ bool keep_entry(double mag, double threshold, double row_max, bool diag) {
+  return diag || !(mag < threshold && mag < row_max);
+}
+__global__ void drop_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, double tol, int square,
+                           int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double row_max = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) row_max = fmax(row_max, fabs(v[k]));
+  const double threshold = __dmul_rn(tol, row_max);
+  int c = 0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k)
+    c += keep_entry(fabs(v[k]), threshold, row_max, square && ci[k] == i);
+  cnt[i] = c;
+}
+__global__ void drop_fill(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, double tol, int square,
+                          const int32_t* __restrict__ orp, int32_t* __restrict__ oci,
+                          double* __restrict__ ov) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double row_max = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) row_max = fmax(row_max, fabs(v[k]));
+  const double threshold = __dmul_rn(tol, row_max);
+  int o = orp[i];
+  for (int k = rp[i]; k < rp[i + 1]; ++k)
+    if (keep_entry(fabs(v[k]), threshold, row_max, square && ci[k] == i)) {
+      oci[o] = ci[k];
+      ov[o++] = v[k];
+    }
+}
+
+}  // namespace
+
+void csr_upload(Ctx& c, int64_t n, int64_t m, const int64_t* h_rp, const int64_t* h_ci,
+                const double* h_v, Csr& out) {
+  if (n < 0 || m < 0) throw InvalidArgument("SparseMatrix: negative dimension");
+  if (!h_rp) throw InvalidArgument("SparseMatrix: row_offsets length must be nrows+1");
+  if (h_rp[0] != 0) throw InvalidArgument("SparseMatrix: row_offsets[0] must be 0");
+  const int64_t nnz = h_rp[n];
+  if (nnz < 0) throw InvalidArgument("SparseMatrix: row_offsets not monotone");
+  out.alloc(c, n, m, nnz);
+  DBuf<int64_t> rp64(c, (size_t)n + 1), ci64(c, (size_t)nnz);
+  DBuf<double> v(c, 0);
+  to_device(c, rp64.p, h_rp, (size_t)n + 1);
+  to_device(c, ci64.p, h_ci, (size_t)nnz);
+  to_device(c, out.v.p, h_v, (size_t)nnz);
+  DBuf<unsigned long long> err(c, 4);
+  CUDA_CHECK(cudaMemsetAsync(err.p, 0xff, 4 * sizeof(unsigned long long), c.stream));
+  LAUNCH(c, convert_validate, blocks_for(n + 1, 256), 256, 0, n, m, rp64.p, ci64.p, out.v.p,
+         out.rp.p, out.ci.p, err.p);
+  unsigned long long e[4];
+  to_host(c, e, err.p, 4);
+  static const char* msg[4] = {"SparseMatrix: row_offsets not monotone",
+                               "SparseMatrix: column index out of range",
+                               "SparseMatrix: column indices not strictly increasing within row",
+                               "SparseMatrix: stored NaN value"};
+  for (int k = 0; k < 4; ++k)
+    if (e[k] != ~0ull) throw InvalidArgument(msg[k]);
+}
+
+void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_v) {
+  DBuf<int64_t> rp64(c, (size_t)a.n + 1), ci64(c, (size_t)a.nnz);
+  LAUNCH(c, widen_rows, blocks_for((int64_t)a.n + 1, 256), 256, 0, (int64_t)a.n, a.rp.p, a.ci.p,
+         rp64.p, ci64.p);
+  if (h_rp) CUDA_CHECK(cudaMemcpyAsync(h_rp, rp64.p, sizeof(int64_t) * (a.n + 1), cudaMemcpyDeviceToHost, c.stream));
+  if (h_ci && a.nnz) CUDA_CHECK(cudaMemcpyAsync(h_ci, ci64.p, sizeof(int64_t) * a.nnz, cudaMemcpyDeviceToHost, c.stream));
+  if (h_v && a.nnz) CUDA_CHECK(cudaMemcpyAsync(h_v, a.v.p, sizeof(double) * a.nnz, cudaMemcpyDeviceToHost, c.stream));
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+void spmv(Ctx& c, const Csr& a, const double* x, double* y) {
+  if (a.n == 0) return;
+  LAUNCH(c, spmv_rows, blocks_for(a.n, 128), 128, 0, a.n, a.rp.p, a.ci.p, a.v.p, x, y);
+}
+
+void with_full_diagonal(Ctx& c, const Csr& a, Csr& out) {
+  if (a.n != a.m) throw InvalidArgument("SparseMatrix: with_full_diagonal requires a square matrix");
+  DBuf<int32_t> cnt(c, (size_t)a.n);
+  Csr r;
+  if (a.n) LAUNCH(c, fulldiag_count, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, cnt.p);
+  r.rp.alloc(c, (size_t)a.n + 1);
+  const int64_t nnz = exclusive_scan(c, cnt.p, r.rp.p, a.n);
+  r.n = a.n;
+  r.m = a.m;
+  r.nnz = nnz;
+  r.ci.alloc(c, (size_t)nnz);
+  r.v.alloc(c, (size_t)nnz);
+  if (a.n)
+    LAUNCH(c, fulldiag_fill, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, r.rp.p,
+           r.ci.p, r.v.p);
+  out = std::move(r);
+}
+
+void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out) {
+  if (tol < 0.0) throw InvalidArgument("drop_entries: tol must be >= 0");
+  const int square = keep_diagonal && a.n == a.m;
+  DBuf<int32_t> cnt(c, (size_t)a.n);
+  Csr r;
+  if (a.n) LAUNCH(c, drop_count, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, tol, square, cnt.p);
+  r.rp.alloc(c, (size_t)a.n + 1);
+  const int64_t nnz = exclusive_scan(c, cnt.p, r.rp.p, a.n);
+  r.n = a.n;
+  r.m = a.m;
+  r.nnz = nnz;
+  r.ci.alloc(c, (size_t)nnz);
+  r.v.alloc(c, (size_t)nnz);
+  if (a.n)
+    LAUNCH(c, drop_fill, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, tol, square,
+           r.rp.p, r.ci.p, r.v.p);
+  out = std::move(r);
+}
+
+}  // namespace airg

@@ -1,0 +1,77 @@
+// Internal API of the engine's device modules.
+#pragma once
+
+#include "common.cuh"
+
+namespace airg {
+
+// sparse.cu -------------------------------------------------------------------
+void csr_upload(Ctx& c, int64_t n, int64_t m, const int64_t* h_rp, const int64_t* h_ci,
+                const double* h_v, Csr& out);
+void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_v);
+void spmv(Ctx& c, const Csr& a, const double* x, double* y);
+void with_full_diagonal(Ctx& c, const Csr& a, Csr& out);
+void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
+
+// spgemm.cu -------------------------------------------------------------------
+// C = A B with per-entry accumulation in A-row order (sparse.cpp:203-242).
+// drop_tol >= 0 fuses drop_entries(C, drop_tol, keep_diag) into the
+// compaction; drop_tol < 0 keeps everything.
+void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol = -1.0,
+            bool keep_diag = true);
+
+// cfsplit.cu ------------------------------------------------------------------
+struct Strength {
+  int32_t n = 0;
+  int64_t nnz = 0;
+  DBuf<int32_t> rp, ci;     // S, sorted rows
+  DBuf<int32_t> st_cnt;     // |S_i^T|
+};
+void strength(Ctx& c, const Csr& a, double alpha, Strength& g);
+// PMISR labels (one-shot local minima, see cfsplit.cu) into d_labels.
+void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weight_mode,
+           uint8_t* d_labels, double* d_weights);
+
+struct LabelMap {
+  int32_t n = 0, nf = 0, nc = 0;
+  DBuf<uint8_t> label;
+  DBuf<int32_t> fine_to_sub, f_to_fine, c_to_fine;
+};
+void build_label_map(Ctx& c, const uint8_t* d_labels, int32_t n, LabelMap& map);
+
+struct Blocks {
+  Csr aff, afc, acf;
+  Csr af;  // A's F rows with global columns; bit 31 of a column flags a C column
+};
+void extract_blocks(Ctx& c, const Csr& a, const LabelMap& map, Blocks& out, bool want_af);
+
+struct DdcResult {
+  int64_t converted = 0;
+  double max_theta = 0.0, alpha_diag = 0.0;
+};
+// dominance_report + ddc (coarsening.cpp:219-330) on the F rows of a_ff;
+// converts labels in d_labels (global rows). selection 0 histogram,
+// 1 quickselect (unsupported on GPU), 2 direct.
+DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, double fraction,
+              int64_t bins, int selection, double direct_alpha, bool convert);
+// max theta only (theta_post, air.cpp:355); throws on a zero diagonal
+double dominance_max(Ctx& c, const Csr& aff);
+
+// poly.cu ---------------------------------------------------------------------
+struct PolyFit {
+  std::vector<double> coeffs;  // m values
+  int64_t effective_order = 0;
+};
+PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed);
+void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs, int64_t deg,
+                   int64_t sparsity_order, Csr& out);
+double smoother_growth(Ctx& c, const Csr& a, const Csr& q);
+
+// transfer.cu -----------------------------------------------------------------
+void build_restriction(Ctx& c, const Csr& acf, const Csr& ffinv, double drop, const LabelMap& map,
+                       Csr& r);
+// one-point P (air.cpp:191-238) as pmap[i] (coarse index or -1) and a CSR.
+void build_prolongation(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a,
+                        DBuf<int32_t>& pmap, Csr& p);
+
+}  // namespace airg
