@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""AIRG benchmark (driver contract: one JSON line from rank 0).
+
+Workload (BASELINE.json configs[2], the largest structured single-GPU case):
+3D 7-point upwind streaming operator, 128^3 cells = 2,097,152 unknowns,
+fp64, alpha 0.5, DDC 0.1, poly order 4, truncation at 5,000 rows, coarse
+poly order 8, Richardson to rtol 1e-10 from x = 0. Synthetic seeded input
+(problems.py; no dataset exists for this operator).
+
+One STEP = one complete AIRG solve (Richardson, V(0,2) cycles) of that
+system with b already resident in HBM; value = unknowns solved per second
+over all ranks. The hierarchy is built once before timing (setup time and
+the CF-split time are reported alongside as setup_ms / cf_split_ms).
+L2 is flushed (512 MiB write) before every timed step; the hierarchy
+(~1.8 GB) is larger than L2 as well.
+
+--impl reference times the reference's own serial CPU implementation
+(oracle/_ref built from /root/reference, else the C restatement) on the
+same configuration; each step is one full Richardson solve.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(f[1]), smax=float(f[2]), hw=f[5], hwt=f[6], swt=f[7], pcap=f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        reasons = set()
+        for r in rows:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
+                            ("swt", "sw_thermal_slowdown"), ("pcap", "sw_power_cap")):
+                if r[k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows), "sm_max_mhz": max(r["smax"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_lib():
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import refpy  # cpu_baseline / reference arm only
+    ref = None
+    if os.path.exists(os.path.join(REPO, "oracle", "_ref", "libairgraph_ref.so")):
+        ref = refpy.ref()
+    return refpy, (ref if ref is not None else refpy.port()), ("reference" if ref is not None else "port")
+
+
+def cpu_solve_sample(cfg_idx: int, nx: int):
+    """Bounded CPU sample: the reference (or its restatement) on the same
+    generator at nx^3, setup untimed, one Richardson solve timed."""
+    from paper_2408_08262_b200 import problems
+    refpy, lib, kind = oracle_lib()
+    p = problems.c2_structured_3d(nx)
+    prm = problems.setup_params(cfg_idx)
+    A = lib.mat_from_problem(p)
+    h = refpy.setup(lib, A, **prm)
+    t0 = time.perf_counter()
+    x, st, _ = h.solve(p.b, refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"]))
+    t = time.perf_counter() - t0
+    return {"value": p.n / t, "unit": "DOF/s", "cores": 1, "kind": kind,
+            "sample": f"C2 generator at {nx}^3 ({p.n} unknowns): one serial Richardson solve "
+                      f"({st.iterations} its, {t:.2f} s; setup untimed) on {cpu_model()}"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2408_08262_b200 import problems
+    refpy, lib, kind = oracle_lib()
+    p = problems.make(args.config, args.scale)
+    prm = problems.setup_params(args.config)
+    A = lib.mat_from_problem(p)
+    t0 = time.perf_counter()
+    h = refpy.setup(lib, A, **prm)
+    setup_s = time.perf_counter() - t0
+    scfg = refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"])
+    for _ in range(args.warmup):
+        h.solve(p.b, scfg)
+    times = []
+    its = 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        x, st, _ = h.solve(p.b, scfg)
+        times.append(time.perf_counter() - t0)
+        its = st.iterations
+    tot = sum(times)
+    value = p.n * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args, p, "serial CPU"),
+        "iterations": its, "final_relative_residual": st.final_relative_residual,
+        "setup_ms": 1e3 * setup_s,
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": kind,
+                         "sample": f"full workload, one Richardson solve per step on {cpu_model()} "
+                                   f"(serial reference; {cpu_cores()} cores visible)"},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "AIRG solve DOFs/s (Richardson to rtol 1e-10, V(0,2) cycles)"
+
+
+def config_dict(args, p, par):
+    names = {0: "C0 2D structured upwind 128^2", 1: "C1 2D unstructured upwind 512^2 quads",
+             2: "C2 3D structured 7-point upwind 128^3", 3: "C3 2D S_n 256^2 x 64 angles",
+             4: "C4 3D unstructured tets 2M/GPU"}
+    return {"workload": names.get(args.config, str(args.config)) + (f" (scale {args.scale})" if args.scale != 1 else ""),
+            "unknowns": int(p.n), "nnz": int(p.nnz), "alpha": 0.5, "ddc_fraction": 0.1, "poly_order": 4,
+            "parallelism": par, "l2": "flushed (512 MiB write) before each timed step; hierarchy > L2"}
+
+
+def run_gpu(args):
+    import torch
+    from paper_2408_08262_b200 import airg, problems
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    ctx = airg.Context(dev)
+    stream = ctx.stream
+    p = problems.make(args.config, args.scale)
+    prm = problems.setup_params(args.config)
+    a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
+    dA = airg.DeviceCSR.upload(a, ctx)
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        return e
+
+    # ---- setup (warm once, then time)
+    h = airg.setup(dA, ctx=ctx, **prm)
+    del h
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    h = airg.setup(dA, ctx=ctx, **prm)
+    e1.record(stream)
+    e1.synchronize()
+    setup_ms = e0.elapsed_time(e1)
+    info = h.info()
+
+    # ---- CF split time: strength + PMISR + extract + DDC on every level's A
+    cf_ms = 0.0
+    for rep in range(2):
+        tot = 0.0
+        for l in range(info.n_levels):
+            Al = h.matrix_handle(l, 0)
+            seed = int(problems.mix(np.uint64(0), np.uint64(l)))
+            s0, s1 = ev(), ev()
+            s0.record(stream)
+            airg.cf_split_device(Al, prm["strength_alpha"], prm["max_loops"], seed, ctx=ctx)
+            s1.record(stream)
+            s1.synchronize()
+            tot += s0.elapsed_time(s1)
+        cf_ms = tot
+
+    # ---- device-resident solve steps
+    with torch.cuda.stream(stream):
+        tb = torch.from_numpy(p.b).to(ctx.tdev)
+        tx = torch.empty(p.n, dtype=torch.float64, device=ctx.tdev)
+        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=ctx.tdev)
+    torch.cuda.synchronize()
+    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    for _ in range(args.warmup):
+        st, _ = h.solve_device(tb, tx, **sk)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    times = []
+    l0 = ctx.launches()
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            s0, s1 = ev(), ev()
+            s0.record(stream)
+            st, _ = h.solve_device(tb, tx, **sk)
+            s1.record(stream)
+            s1.synchronize()
+            times.append(s0.elapsed_time(s1))
+    launches = ctx.launches() - l0
+    torch.cuda.synchronize()
+    local_ms = sum(times)
+    tot_ms = local_ms
+    if ws > 1:
+        t = torch.tensor([local_ms], device=ctx.tdev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = p.n * ws * args.steps / (tot_ms / 1e3)
+    x = ctx.to_host(tx)
+    rel = np.linalg.norm(p.b - airg.spmv(dA, x, ctx=ctx)) / np.linalg.norm(p.b)
+
+    # ---- end-to-end through the reference-facing call (host b -> host x)
+    hb = torch.from_numpy(p.b.copy()).pin_memory()
+    hx = torch.empty(p.n, dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for k in range(args.warmup + args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        s0, s1 = ev(), ev()
+        s0.record(stream)
+        res = h.solve_host_ptr(hb.data_ptr(), hx.data_ptr(), **sk)
+        s1.record(stream)
+        s1.synchronize()
+        if k >= args.warmup:
+            e2e_times.append(s0.elapsed_time(s1))
+    e2e_ms = sum(e2e_times) / len(e2e_times)
+    e2e_value = p.n * ws / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel: the level-0 CSR SpMV (y = A x) ----
+    # algorithmic bytes = 12 nnz + 4 (n+1) + 8 n (x) + 8 n (y)
+    A0 = h.matrix_handle(0, 0) if info.n_levels else dA
+    n0, _, nnz0 = A0.dims()
+    alg_bytes = 12 * nnz0 + 4 * (n0 + 1) + 8 * n0 + 8 * n0
+    with torch.cuda.stream(stream):
+        xv = torch.rand(n0, dtype=torch.float64, device=ctx.tdev)
+        yv = torch.empty(n0, dtype=torch.float64, device=ctx.tdev)
+    reps = 50
+    for _ in range(5):
+        airg.spmv_device(A0, xv, yv, ctx=ctx)
+    k0, k1 = ev(), ev()
+    k0.record(stream)
+    for _ in range(reps):
+        airg.spmv_device(A0, xv, yv, ctx=ctx)
+    k1.record(stream)
+    k1.synchronize()
+    kern_ms = k0.elapsed_time(k1) / reps
+    peak, peak_kind = hbm_peak()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(REPO, "profiles", "spmv_dram_bytes.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_solve_sample(args.config, args.cpu_nx)
+        except Exception as exc:  # keep the GPU line even if the checker fails
+            cpu = {"value": None, "unit": "DOF/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, p, "replicas (one independent system per GPU)" if ws > 1 else "single GPU"),
+        "iterations": int(st.iterations), "final_relative_residual": float(rel),
+        "levels": int(info.n_levels), "operator_complexity": info.operator_complexity,
+        "setup_ms": setup_ms, "cf_split_ms": cf_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "spmv_rows (level-0 A, thread-per-row exact CSR SpMV)",
+                     "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_ms, "peak_kind": peak_kind},
+        "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 8 * p.n,
+                "d2h_bytes_per_step": 8 * p.n, "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="airg", choices=["airg", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu-nx", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "airg":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

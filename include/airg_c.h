@@ -195,6 +195,11 @@ int airg_strength(airg_ctx* ctx, const airg_csr* a, double alpha,
 int airg_pmisr(airg_ctx* ctx, const airg_csr* a, double alpha,
                int64_t max_loops, uint64_t seed, int32_t weight_mode,
                uint8_t* d_labels, double* d_weights);
+/* pmisr_with_weights (coarsening.hpp:83-84) on a caller-supplied strength
+ * pattern S (StrengthGraph::from_pattern) and caller weights (device). */
+int airg_pmisr_with_weights(airg_ctx* ctx, const airg_csr* s_pattern,
+                            int64_t max_loops, const double* d_weights,
+                            uint8_t* d_labels);
 typedef struct airg_cf_report {
   int64_t n_f_pre, n_f, n_c, n_converted;
   double max_theta, alpha_diag;

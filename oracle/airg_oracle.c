@@ -57,7 +57,7 @@ static void fail(int code, const char* fmt, ...) {
   int rc__ = setjmp(jb__);        \
   if (rc__ != 0) {                \
     g_jb = prev__;                \
-    return -rc__;                 \
+    return rc__;                  \
   }                               \
   g_jb = &jb__;
 #define API_END \

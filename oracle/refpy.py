@@ -201,8 +201,11 @@ def new_out():
 
 def spmv(lib, A: Mat, x):
     n, m, _ = A.dims()
+    x = np.ascontiguousarray(x, np.float64)
+    if x.shape[0] != m:  # sparse.cpp:187-188
+        raise OracleValueError("spmv: dimension mismatch")
     y = np.zeros(n)
-    lib.call("spmv", A.h, np.ascontiguousarray(x, np.float64), y)
+    lib.call("spmv", A.h, x, y)
     return y
 
 

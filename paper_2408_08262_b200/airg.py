@@ -74,6 +74,7 @@ def lib() -> C.CDLL:
             "airg_with_full_diagonal": ([_VP, _VP, _P(_VP)], C.c_int),
             "airg_strength": ([_VP, _VP, C.c_double, _P(_VP)], C.c_int),
             "airg_pmisr": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, _VP, _VP], C.c_int),
+            "airg_pmisr_with_weights": ([_VP, _VP, C.c_int64, _VP, _VP], C.c_int),
             "airg_cf_split": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, C.c_int32,
                                C.c_double, C.c_int64, _VP, _VP, _P(abi.CfReport)], C.c_int),
             "airg_ddc": ([_VP, _VP, _VP, C.c_double, C.c_int64, C.c_int32, C.c_double,
@@ -362,6 +363,19 @@ def pmisr(a, alpha: float, max_loops: int, seed: int, weight_mode: int = 0,
     return ctx.to_host(tl)[:n], ctx.to_host(tw)[:n]
 
 
+def pmisr_with_weights(s_pattern: SparseMatrix, max_loops: int, weights,
+                       ctx: Context | None = None) -> np.ndarray:
+    """pmisr_with_weights (coarsening.cpp:107-160) on an explicit strength
+    pattern (StrengthGraph::from_pattern) and explicit weights."""
+    ctx = ctx or default_context()
+    d = _dev(s_pattern, ctx)
+    n = d.dims()[0]
+    tw = ctx.to_device(np.asarray(weights, np.float64))
+    tl = ctx.empty(max(n, 1), ctx.torch.uint8)
+    _check(lib().airg_pmisr_with_weights(ctx.h, d.h, int(max_loops), _ptr(tw), _ptr(tl)))
+    return ctx.to_host(tl)[:n]
+
+
 @dataclass
 class CfReport:
     n_f_pre: int
@@ -387,6 +401,25 @@ def cf_split(a, alpha=0.5, max_loops=3, seed=0, weight_mode=0, ddc_enabled=True,
                                _ptr(tl), _ptr(tp), C.byref(rep)))
     r = CfReport(rep.n_f_pre, rep.n_f, rep.n_c, rep.n_converted, rep.max_theta, rep.alpha_diag, rep.s_nnz)
     return ctx.to_host(tl)[:n], ctx.to_host(tp)[:n], r
+
+
+def cf_split_device(d: DeviceCSR, alpha=0.5, max_loops=3, seed=0, weight_mode=0, ddc_enabled=True,
+                    ddc_fraction=0.1, ddc_bins=1000, labels=None, ctx: Context | None = None):
+    """cf_split on a device-resident matrix into a device label tensor."""
+    ctx = ctx or d.ctx
+    n = d.dims()[0]
+    tl = labels if labels is not None else ctx.empty(max(n, 1), ctx.torch.uint8)
+    rep = abi.CfReport()
+    _check(lib().airg_cf_split(ctx.h, d.h, float(alpha), int(max_loops), int(seed) & (2**64 - 1),
+                               int(weight_mode), int(ddc_enabled), float(ddc_fraction), int(ddc_bins),
+                               _ptr(tl), None, C.byref(rep)))
+    return tl, rep
+
+
+def spmv_device(d: DeviceCSR, tx, ty, ctx: Context | None = None) -> None:
+    """y = A x on device tensors (no synchronisation)."""
+    ctx = ctx or d.ctx
+    _check(lib().airg_spmv(ctx.h, d.h, _ptr(tx), _ptr(ty)))
 
 
 def ddc(a, labels, fraction=0.1, bins=1000, selection=0, direct_alpha_diag=0.0,
@@ -460,6 +493,20 @@ class Hierarchy:
         out = _VP()
         _check(lib().airg_hier_matrix(self.h, int(l), w, C.byref(out)))
         return DeviceCSR(self.ctx, out, owned=False, keep=self).download()
+
+    def matrix_handle(self, l: int, which) -> DeviceCSR:
+        """Borrowed device handle of a level matrix (no copy)."""
+        w = MATRICES[which] if isinstance(which, str) else int(which)
+        out = _VP()
+        _check(lib().airg_hier_matrix(self.h, int(l), w, C.byref(out)))
+        return DeviceCSR(self.ctx, out, owned=False, keep=self)
+
+    def solve_host_ptr(self, hb: int, hx: int, **solve_kw) -> abi.SolveStats:
+        """The host-buffer C-ABI solve on raw (pinned) host pointers."""
+        cfg = abi.solve_config(**solve_kw)
+        st = abi.SolveStats()
+        _check(lib().airg_solve_host(self.ctx.h, self.h, C.byref(cfg), hb, hx, C.byref(st), None, 0))
+        return st
 
     def labels(self, l: int) -> np.ndarray:
         n = self.level(l).n

@@ -285,6 +285,19 @@ int airg_pmisr(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops
   });
 }
 
+int airg_pmisr_with_weights(airg_ctx* ctx, const airg_csr* s_pattern, int64_t max_loops,
+                            const double* weights, uint8_t* labels) {
+  return guard([&] {
+    need(ctx, "context");
+    need(s_pattern, "pattern");
+    bind(ctx->c);
+    Strength g;
+    strength_from_pattern(ctx->c, s_pattern->m, g);
+    pmisr_with_weights(ctx->c, g, max_loops, weights, labels);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
 int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops, uint64_t seed,
                   int32_t weight_mode, int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
                   uint8_t* labels, uint8_t* labels_pre, airg_cf_report* rep) {

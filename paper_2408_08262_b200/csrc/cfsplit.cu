@@ -122,10 +122,19 @@ __global__ void mark_not_minimal(int n, const int32_t* __restrict__ srp,
   }
 }
 
-__global__ void pmisr_labels(int n, const uint8_t* __restrict__ notmin, uint8_t* __restrict__ label) {
+// F = {w < 1} u {strict local minima}; everything else C (see header).
+__global__ void pmisr_labels(int n, const uint8_t* __restrict__ notmin, const double* __restrict__ w,
+                             uint8_t* __restrict__ label) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  label[i] = notmin[i] ? AIRG_C : AIRG_F;
+  label[i] = (w[i] < 1.0 || !notmin[i]) ? AIRG_F : AIRG_C;
+}
+
+__global__ void in_degree(int n, const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
+                          int32_t* __restrict__ st_cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = srp[i]; k < srp[i + 1]; ++k) atomicAdd(st_cnt + sci[k], 1);
 }
 
 // ---- label map (sparse.cpp:270-290)
@@ -337,10 +346,31 @@ void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weig
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
   LAUNCH(c, make_weights, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, g.st_cnt.p, key,
          weight_mode, w);
+  pmisr_with_weights(c, g, max_loops, w, d_labels);
+}
+
+void pmisr_with_weights(Ctx& c, const Strength& g, int64_t max_loops, const double* w,
+                        uint8_t* d_labels) {
+  if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
+  const int n = g.n;
+  if (n == 0) return;
   DBuf<uint8_t> notmin(c, (size_t)n);
   notmin.zero(c);
   LAUNCH(c, mark_not_minimal, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, w, notmin.p);
-  LAUNCH(c, pmisr_labels, blocks_for(n, 256), 256, 0, n, notmin.p, d_labels);
+  LAUNCH(c, pmisr_labels, blocks_for(n, 256), 256, 0, n, notmin.p, w, d_labels);
+}
+
+void strength_from_pattern(Ctx& c, const Csr& s, Strength& g) {
+  if (s.n != s.m) throw InvalidArgument("StrengthGraph: pattern must be square");
+  g.n = s.n;
+  g.nnz = s.nnz;
+  g.rp.alloc(c, (size_t)s.n + 1);
+  g.ci.alloc(c, (size_t)s.nnz);
+  CUDA_CHECK(cudaMemcpyAsync(g.rp.p, s.rp.p, sizeof(int32_t) * (s.n + 1), cudaMemcpyDeviceToDevice, c.stream));
+  if (s.nnz) CUDA_CHECK(cudaMemcpyAsync(g.ci.p, s.ci.p, sizeof(int32_t) * s.nnz, cudaMemcpyDeviceToDevice, c.stream));
+  g.st_cnt.alloc(c, (size_t)s.n);
+  g.st_cnt.zero(c);
+  if (s.n) LAUNCH(c, in_degree, blocks_for(s.n, 256), 256, 0, s.n, g.rp.p, g.ci.p, g.st_cnt.p);
 }
 
 void build_label_map(Ctx& c, const uint8_t* d_labels, int32_t n, LabelMap& map) {

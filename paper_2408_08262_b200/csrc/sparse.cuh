@@ -31,6 +31,11 @@ void strength(Ctx& c, const Csr& a, double alpha, Strength& g);
 // PMISR labels (one-shot local minima, see cfsplit.cu) into d_labels.
 void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weight_mode,
            uint8_t* d_labels, double* d_weights);
+// pmisr_with_weights (coarsening.hpp:83-84) and a StrengthGraph from an
+// externally supplied S pattern (StrengthGraph::from_pattern).
+void pmisr_with_weights(Ctx& c, const Strength& g, int64_t max_loops, const double* d_w,
+                        uint8_t* d_labels);
+void strength_from_pattern(Ctx& c, const Csr& s, Strength& g);
 
 struct LabelMap {
   int32_t n = 0, nf = 0, nc = 0;
