@@ -176,6 +176,8 @@ int airg_csr_destroy(airg_csr* a);
 /* y = A x (sparse.cpp:185-201): sequential per-row accumulation in column
  * order without FMA, bit-identical to the reference. */
 int airg_spmv(airg_ctx* ctx, const airg_csr* a, const double* d_x, double* d_y);
+/* spmv with host vectors (the reference signature's value semantics). */
+int airg_spmv_host(airg_ctx* ctx, const airg_csr* a, const double* h_x, double* h_y);
 /* C = A B (sparse.cpp:203-242), cancellation zeros kept, contributions to
  * each entry accumulated in A-row order. */
 int airg_spgemm(airg_ctx* ctx, const airg_csr* a, const airg_csr* b,
@@ -213,6 +215,12 @@ int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha,
                   int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
                   uint8_t* d_labels, uint8_t* d_labels_pre,
                   airg_cf_report* report);
+/* airg_cf_split with the labels returned to host memory. */
+int airg_cf_split_host(airg_ctx* ctx, const airg_csr* a, double alpha,
+                       int64_t max_loops, uint64_t seed, int32_t weight_mode,
+                       int32_t ddc_enabled, double ddc_fraction,
+                       int64_t ddc_bins, uint8_t* h_labels,
+                       airg_cf_report* report);
 /* ddc on given labels (coarsening.cpp:252-330); selection 0 = histogram,
  * 2 = direct (alpha_diag given). Converts in place. */
 int airg_ddc(airg_ctx* ctx, const airg_csr* a, uint8_t* d_labels,

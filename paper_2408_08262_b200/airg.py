@@ -299,6 +299,13 @@ def _new(ctx, fn, *args) -> DeviceCSR:
     return DeviceCSR(ctx, out)
 
 
+def _new1(ctx, fn, d: DeviceCSR, *args) -> DeviceCSR:
+    """Like _new with one matrix operand, kept alive across the call."""
+    out = _VP()
+    _check(fn(ctx.h, d.h, *args, C.byref(out)))
+    return DeviceCSR(ctx, out)
+
+
 # ---- L0 (sparse.hpp:97-110) -------------------------------------------------
 def spmv(a, x, ctx: Context | None = None) -> np.ndarray:
     """y = A x (sparse.cpp:185-201); bit-identical to the reference."""
@@ -324,13 +331,13 @@ def spgemm(a, b, ctx: Context | None = None) -> SparseMatrix:
 def drop_entries(a, tol: float, keep_diagonal: bool = True, ctx: Context | None = None) -> SparseMatrix:
     """sparse.cpp:244-268."""
     ctx = ctx or default_context()
-    return _new(ctx, lib().airg_drop, _dev(a, ctx).h, float(tol), int(keep_diagonal)).download()
+    return _new1(ctx, lib().airg_drop, _dev(a, ctx), float(tol), int(keep_diagonal)).download()
 
 
 def with_full_diagonal(a, ctx: Context | None = None) -> SparseMatrix:
     """SparseMatrix::with_full_diagonal (sparse.cpp:132-160)."""
     ctx = ctx or default_context()
-    return _new(ctx, lib().airg_with_full_diagonal, _dev(a, ctx).h).download()
+    return _new1(ctx, lib().airg_with_full_diagonal, _dev(a, ctx)).download()
 
 
 def extract_blocks(a, labels, ctx: Context | None = None):
@@ -347,7 +354,7 @@ def extract_blocks(a, labels, ctx: Context | None = None):
 def strength(a, alpha: float, ctx: Context | None = None) -> SparseMatrix:
     """coarsening.cpp:83-105: S as a pattern matrix (values 1.0)."""
     ctx = ctx or default_context()
-    return _new(ctx, lib().airg_strength, _dev(a, ctx).h, float(alpha)).download()
+    return _new1(ctx, lib().airg_strength, _dev(a, ctx), float(alpha)).download()
 
 
 def pmisr(a, alpha: float, max_loops: int, seed: int, weight_mode: int = 0,
@@ -452,7 +459,7 @@ def assemble_fixed_sparsity(a, coeffs, effective_order: int, sparsity_order: int
     """gmres_poly.cpp:197-280."""
     ctx = ctx or default_context()
     c = np.ascontiguousarray(coeffs, np.float64)
-    return _new(ctx, lib().airg_poly_assemble, _dev(a, ctx).h, c.ctypes.data, len(c),
+    return _new1(ctx, lib().airg_poly_assemble, _dev(a, ctx), c.ctypes.data, len(c),
                 int(effective_order), int(sparsity_order)).download()
 
 

@@ -215,6 +215,36 @@ int airg_spmv(airg_ctx* ctx, const airg_csr* a, const double* x, double* y) {
   });
 }
 
+int airg_spmv_host(airg_ctx* ctx, const airg_csr* a, const double* hx, double* hy) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    bind(ctx->c);
+    Ctx& c = ctx->c;
+    DBuf<double> dx(c, (size_t)a->m.m), dy(c, (size_t)a->m.n);
+    to_device(c, dx.p, hx, (size_t)a->m.m);
+    spmv(c, a->m, dx.p, dy.p);
+    to_host(c, hy, dy.p, (size_t)a->m.n);
+  });
+}
+
+int airg_cf_split_host(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops,
+                       uint64_t seed, int32_t weight_mode, int32_t ddc_enabled, double ddc_fraction,
+                       int64_t ddc_bins, uint8_t* h_labels, airg_cf_report* rep) {
+  int rc = AIRG_OK;
+  int rc2 = guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(h_labels, "labels");
+    bind(ctx->c);
+    DBuf<uint8_t> d(ctx->c, (size_t)std::max(1, a->m.n));
+    rc = airg_cf_split(ctx, a, alpha, max_loops, seed, weight_mode, ddc_enabled, ddc_fraction,
+                       ddc_bins, d.p, nullptr, rep);
+    if (rc == AIRG_OK) to_host(ctx->c, h_labels, d.p, (size_t)a->m.n);
+  });
+  return rc != AIRG_OK ? rc : rc2;
+}
+
 int airg_spgemm(airg_ctx* ctx, const airg_csr* a, const airg_csr* b, airg_csr** out) {
   return guard([&] {
     need(ctx, "context");

@@ -77,6 +77,35 @@ struct Ctx {
     CUDA_CHECK(cudaGetLastError());                                                   \
   } while (0)
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// LAUNCH_PDL may start while its predecessor drains; it must call
+// pdl_wait() before touching anything the predecessor writes, and calls
+// pdl_trigger() to let its own successor launch early. Both are no-ops for
+// ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(Ctx& c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  c.launches++;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+#define LAUNCH_PDL(ctx, kernel, grid, block, smem, ...) \
+  ::airg::launch_pdl((ctx), kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__)
+
 inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   return (unsigned)(b < 1 ? 1 : b);
@@ -159,6 +188,9 @@ struct Csr {
   int64_t nnz = 0;
   DBuf<int32_t> rp, ci;
   DBuf<double> v;
+  DBuf<int32_t> tiles;  // row starts of the warp tiles (tiled.cuh), built on demand
+  int32_t ntiles = -1;
+  int8_t row_mode = 0;  // 0 unbuilt, 1 thread per row, 2 warp tiles
 
   Csr() = default;
   Csr(Csr&&) = default;

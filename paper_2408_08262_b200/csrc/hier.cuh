@@ -11,6 +11,7 @@ struct Level {
   LabelMap map;
   Csr aff, afc, acf;         // blocks (acf feeds Z; aff/afc are kept for download)
   Csr af;                    // F rows of A, global columns, bit 31 = C column
+  Csr affg;                  // A_FF with global column indices (later F-smooths)
   Csr ffinv, r, p;
   DBuf<int32_t> pmap;        // one-point P as a map (-1 = empty row)
   // report
@@ -21,6 +22,7 @@ struct Level {
   DBuf<double> b;            // level rhs (level 0 uses Hier::r)
   DBuf<double> x;            // level correction
   DBuf<double> rf;           // F residual
+  DBuf<double> sc;           // A_FC x_C kept from the first F-smooth
 };
 
 struct Hier {

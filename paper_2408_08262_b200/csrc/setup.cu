@@ -6,6 +6,7 @@
 #include <cstring>
 
 #include "hier.cuh"
+#include "tiled.cuh"
 
 namespace airg {
 
@@ -57,13 +58,23 @@ Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs
   return k;
 }
 
+// Solve-side structures: A_FF with global columns, the tile starts of every
+// matrix the V-cycle streams, and the per-level vectors (fixed pointers, so
+// the V-cycle can be captured into a CUDA graph).
 void alloc_workspace(Ctx& c, Hier& h) {
   for (size_t l = 0; l < h.levels.size(); ++l) {
     Level& L = h.levels[l];
     if (l > 0) L.b.alloc(c, (size_t)L.a.n);
     L.x.alloc(c, (size_t)L.a.n);
     L.rf.alloc(c, (size_t)std::max(1, L.map.nf));
+    L.sc.alloc(c, (size_t)std::max(1, L.map.nf));
+    map_columns(c, L.aff, L.map.f_to_fine.p, L.a.n, L.affg);
+    for (Csr* m : {&L.r, &L.af, &L.affg, &L.ffinv}) build_tiles(c, *m);
   }
+  build_tiles(c, h.coarse_a);
+  build_tiles(c, h.coarse_inv);
+  Csr& top = h.levels.empty() ? h.coarse_a : h.levels.front().a;
+  build_tiles(c, top);
   const size_t nc = (size_t)std::max(1, h.coarse_a.n);
   h.cb.alloc(c, nc);
   h.cx.alloc(c, nc);
@@ -72,7 +83,8 @@ void alloc_workspace(Ctx& c, Hier& h) {
   h.rhs.alloc(c, n);
   h.xsol.alloc(c, n);
   h.r.alloc(c, n);
-  h.part.alloc(c, kReduceBlocks + 8);
+  // one partial per residual block, either decomposition (tiled.cuh rows_grid)
+  h.part.alloc(c, (size_t)(kReduceBlocks + top.n / kTileThreads + std::max(0, top.ntiles) + 8));
   h.scal.alloc(c, 64);
 }
 

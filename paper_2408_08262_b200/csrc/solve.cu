@@ -17,119 +17,118 @@
 #include <cstring>
 
 #include "hier.cuh"
+#include "tiled.cuh"
 
 namespace airg {
 
 namespace {
 
-__global__ void k_spmv_into(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                            const double* __restrict__ v, const double* __restrict__ x,
-                            double* __restrict__ y) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double acc = 0.0;
-  for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k)
-    acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ci + k))));
-  y[i] = acc;
+// ---- epilogues of the tiled row kernels (tiled.cuh) --------------------------
+// first F-smooth: r_F = (b_F - A_FF x_F) - A_FC x_C, keeping A_FC x_C for the
+// following smooths (x_C is not changed by F-smoothing, solve.cpp:63-87)
+struct EpiFres1 {
+  const double* b;
+  const int32_t* f2f;
+  double* rf;
+  double* sc_keep;
+  __device__ void row2(int k, double sf, double sc) const {
+    sc_keep[k] = sc;
+    rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc);
+  }
+};
+// later F-smooths: only A_FF x_F is recomputed
+struct EpiFres2 {
+  const double* b;
+  const int32_t* f2f;
+  const double* sc_keep;
+  double* rf;
+  __device__ void row(int k, double sf) const {
+    rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc_keep[k]);
+  }
+  __device__ void finish() const {}
+};
+// x_F += Aff^-1 r_F
+struct EpiFupd {
+  const int32_t* f2f;
+  double* x;
+  __device__ void row(int k, double d) const {
+    const int i = __ldg(f2f + k);
+    x[i] = __dadd_rn(x[i], d);
+  }
+  __device__ void finish() const {}
+};
+// coarse residual r = rhs - A_c e
+struct EpiCres {
+  const double* rhs;
+  double* r;
+  __device__ void row(int i, double acc) const { r[i] = __dsub_rn(rhs[i], acc); }
+  __device__ void finish() const {}
+};
+// coarse update e += 1.0 * (Ac^-1 r)
+struct EpiCupd {
+  double* e;
+  int first;
+  __device__ void row(int i, double acc) const {
+    const double e0 = first ? 0.0 : e[i];
+    e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
+  }
+  __device__ void finish() const {}
+};
+// top residual r = b - A x with one partial sum of r^2 per block
+struct EpiResid {
+  const double* b;
+  double* r;
+  double* part;
+  mutable double s;
+  __device__ void row(int i, double acc) const {
+    const double ri = __dsub_rn(b[i], acc);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  __device__ void finish() const {
+    __shared__ double sm[kTileThreads / 32];
+    double v = s;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      v = threadIdx.x < kTileThreads / 32 ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+  }
+};
+
+inline TileView tv(const Csr& m) {
+  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n};
 }
 
 // x_l = 0 + P e_c  (solve.cpp:139-141: pe = spmv(P, ec); x += 1.0 * pe)
 __global__ void k_prolong(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
                           double* __restrict__ x) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = i < n ? __ldg(pmap + i) : -1;  // static data: before the dependency wait
+  pdl_wait();
+  pdl_trigger();
   if (i >= n) return;
-  const int j = pmap[i];
   const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
   x[i] = __dadd_rn(0.0, __dmul_rn(1.0, pe));
 }
 
-// r_F[k] = (b[i] - sum_F a x) - sum_C a x, i = f_to_fine[k] (solve.cpp:72-80)
-__global__ void k_fresid(int nf, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                         const double* __restrict__ v, const int32_t* __restrict__ f2f,
-                         const double* __restrict__ b, const double* __restrict__ x,
-                         double* __restrict__ rf) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nf) return;
-  double sf = 0.0, sc = 0.0;
-  for (int t = __ldg(rp + k); t < __ldg(rp + k + 1); ++t) {
-    const int c = __ldg(ci + t);
-    const double p = __dmul_rn(__ldg(v + t), __ldg(x + (c & 0x7fffffff)));
-    if (c >= 0)
-      sf = __dadd_rn(sf, p);
-    else
-      sc = __dadd_rn(sc, p);
-  }
-  rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc);
-}
-
-// x[f_to_fine[k]] += (Aff^-1 r_F)[k] (solve.cpp:81-84)
-__global__ void k_fupdate(int nf, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                          const double* __restrict__ v, const int32_t* __restrict__ f2f,
-                          const double* __restrict__ rf, double* __restrict__ x) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nf) return;
-  double acc = 0.0;
-  for (int t = __ldg(rp + k); t < __ldg(rp + k + 1); ++t)
-    acc = __dadd_rn(acc, __dmul_rn(__ldg(v + t), __ldg(rf + __ldg(ci + t))));
-  const int i = __ldg(f2f + k);
-  x[i] = __dadd_rn(x[i], acc);
-}
-
-// coarse Richardson pieces (solve.cpp:34-59)
-__global__ void k_cresid(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                         const double* __restrict__ v, const double* __restrict__ rhs,
-                         const double* __restrict__ e, double* __restrict__ r) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double acc = 0.0;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], e[ci[k]]));
-  r[i] = __dsub_rn(rhs[i], acc);
-}
-__global__ void k_cupdate(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                          const double* __restrict__ v, const double* __restrict__ r,
-                          double* __restrict__ e, int first) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double acc = 0.0;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], r[ci[k]]));
-  const double e0 = first ? 0.0 : e[i];
-  e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
-}
-
 // x += 1.0 * e (solve.cpp:224)
 __global__ void k_axpy1(int n, const double* __restrict__ e, double* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(1.0, e[i]));
 }
 
-// r = b - A x with block partial sums of r^2 (solve.cpp:202-207)
-__global__ void k_resid_partial(int n, const int32_t* __restrict__ rp,
-                                const int32_t* __restrict__ ci, const double* __restrict__ v,
-                                const double* __restrict__ b, const double* __restrict__ x,
-                                double* __restrict__ r, double* __restrict__ part) {
-  __shared__ double sm[32];
-  double s = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k)
-      acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ci + k))));
-    const double ri = __dsub_rn(b[i], acc);
-    r[i] = ri;
-    s = fma(ri, ri, s);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
-  }
-}
 __global__ void k_sum_partials(const double* __restrict__ part, int np, double* __restrict__ out) {
   __shared__ double sm[32];
+  pdl_wait();
+  pdl_trigger();
   double s = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
 #pragma unroll
@@ -221,8 +220,7 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     const double* bl = l == 0 ? b0 : lv.b.p;
     double* bn = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
     if (lv.r.n)
-      LAUNCH(c, k_spmv_into, blocks_for(lv.r.n, kT), kT, 0, lv.r.n, lv.r.rp.p, lv.r.ci.p, lv.r.v.p,
-             bl, bn);
+      LAUNCH_ROWS_P(c,EpiStore, tv(lv.r), bl, EpiStore{bn});
   }
   // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
   {
@@ -232,12 +230,10 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
       for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
         const double* r = rhs;
         if (it > 0) {
-          LAUNCH(c, k_cresid, blocks_for(n, kT), kT, 0, n, h.coarse_a.rp.p, h.coarse_a.ci.p,
-                 h.coarse_a.v.p, rhs, h.cx.p, h.cr.p);
+          LAUNCH_ROWS_P(c,EpiCres, tv(h.coarse_a), h.cx.p, (EpiCres{rhs, h.cr.p}));
           r = h.cr.p;
         }
-        LAUNCH(c, k_cupdate, blocks_for(n, kT), kT, 0, n, h.coarse_inv.rp.p, h.coarse_inv.ci.p,
-               h.coarse_inv.v.p, r, h.cx.p, it == 0 ? 1 : 0);
+        LAUNCH_ROWS_P(c,EpiCupd, tv(h.coarse_inv), r, (EpiCupd{h.cx.p, it == 0 ? 1 : 0}));
       }
       if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * n, c.stream));
     }
@@ -248,26 +244,28 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     const double* bl = l == 0 ? b0 : lv.b.p;
     const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
     const int n = lv.a.n, nf = lv.map.nf;
-    LAUNCH(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
+    LAUNCH_PDL(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
     for (int64_t s = 0; s < cfg.up_f_smooths && nf > 0; ++s) {
-      LAUNCH(c, k_fresid, blocks_for(nf, kT), kT, 0, nf, lv.af.rp.p, lv.af.ci.p, lv.af.v.p,
-             lv.map.f_to_fine.p, bl, lv.x.p, lv.rf.p);
-      LAUNCH(c, k_fupdate, blocks_for(nf, kT), kT, 0, nf, lv.ffinv.rp.p, lv.ffinv.ci.p,
-             lv.ffinv.v.p, lv.map.f_to_fine.p, lv.rf.p, lv.x.p);
+      if (s == 0)
+        LAUNCH_ROWS_FC_P(c,EpiFres1, tv(lv.af), lv.x.p,
+                       (EpiFres1{bl, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p}));
+      else
+        LAUNCH_ROWS_P(c,EpiFres2, tv(lv.affg), lv.x.p,
+                    (EpiFres2{bl, lv.map.f_to_fine.p, lv.sc.p, lv.rf.p}));
+      LAUNCH_ROWS_P(c,EpiFupd, tv(lv.ffinv), lv.rf.p, (EpiFupd{lv.map.f_to_fine.p, lv.x.p}));
     }
   }
 }
 
 double* vcycle_output(Hier& h) { return h.levels.empty() ? h.cx.p : h.levels[0].x.p; }
 
-int resid_blocks(int n) { return (int)std::min<int64_t>(kReduceBlocks, blocks_for(n, 256)); }
 
 // r = b - A x, ||r||^2 -> h.scal[0]
 void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double* r) {
   const Csr& a = h.top();
-  const int nb = resid_blocks(a.n);
-  LAUNCH(c, k_resid_partial, nb, 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, b, x, r, h.part.p);
-  LAUNCH(c, k_sum_partials, 1, 1024, 0, h.part.p, nb, h.scal.p);
+  const TileView v = tv(a);
+  LAUNCH_ROWS_P(c,EpiResid, v, x, (EpiResid{b, r, h.part.p, 0.0}));
+  LAUNCH_PDL(c, k_sum_partials, 1, 1024, 0, h.part.p, (int)rows_grid(v), h.scal.p);
 }
 
 int64_t graph_key(const airg_solve_config& cfg) {
@@ -373,7 +371,7 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
       h.g_rich_kernels = capture(c, &h.g_rich, [&] {
         enqueue_vcycle(c, h, cfg, h.r.p);
         const double* e = vcycle_output(h);
-        LAUNCH(c, k_axpy1, blocks_for(n, 256), 256, 0, n, e, h.xsol.p);
+        LAUNCH_PDL(c, k_axpy1, blocks_for(n, 256), 256, 0, n, e, h.xsol.p);
         enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
       });
       h.g_key_rich = key;

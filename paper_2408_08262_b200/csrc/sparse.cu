@@ -1,6 +1,7 @@
 // L0 sparse kernels: CSR upload/validation, SpMV, with_full_diagonal and
 // drop_entries (reference: proj/src/sparse.cpp).
 #include "sparse.cuh"
+#include "tiled.cuh"
 
 namespace airg {
 
@@ -47,10 +48,7 @@ __global__ void spmv_rows(int n, const int32_t* __restrict__ rp, const int32_t* 
                           double* __restrict__ y) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int s = __ldg(rp + i), e = __ldg(rp + i + 1);
-  double acc = 0.0;
-  for (int k = s; k < e; ++k) acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ci + k))));
-  y[i] = acc;
+  y[i] = dot_ordered(__ldg(rp + i), __ldg(rp + i + 1), ci, v, x);
 }
 
 // ---- with_full_diagonal, sparse.cpp:132-160
@@ -120,7 +118,67 @@ __global__ void drop_fill(int n, const int32_t* __restrict__ rp, const int32_t* 
     }
 }
 
+// ---- tiles (tiled.cuh): a row starts a tile when its first nonzero lies in a
+// different kWarpNnz chunk than its predecessor's.
+__global__ void tile_flags(int n, const int32_t* __restrict__ rp, int32_t* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = (i == 0) || (rp[i] / kWarpNnz != rp[i - 1] / kWarpNnz);
+}
+__global__ void tile_fill(int n, const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
+                          int32_t* __restrict__ tiles, int ntiles) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) tiles[pos[i]] = i;
+  if (i == 0) tiles[ntiles] = n;
+}
+
+__global__ void map_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci,
+                                const int32_t* __restrict__ map, int32_t* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nnz) out[k] = map[ci[k]];
+}
+
 }  // namespace
+
+// Row-kernel decomposition for this matrix: thread per row for short rows,
+// warp tiles otherwise (tiled.cuh). AIRG_ROWS=thread|tiles forces one.
+static int rows_override() {
+  static int v = [] {
+    const char* e = getenv("AIRG_ROWS");
+    if (!e) return 0;
+    if (!strcmp(e, "thread")) return 1;
+    if (!strcmp(e, "tiles")) return 2;
+    return 0;
+  }();
+  return v;
+}
+
+void build_tiles(Ctx& c, Csr& a) {
+  if (a.row_mode != 0) return;
+  const int ov = rows_override();
+  const bool short_rows = ov ? ov == 1 : (a.n == 0 || a.nnz <= (int64_t)kShortRow * a.n);
+  if (short_rows) {
+    a.row_mode = 1;
+    a.ntiles = 0;
+    return;
+  }
+  a.row_mode = 2;
+  DBuf<int32_t> flag(c, (size_t)a.n), pos(c, (size_t)a.n + 1);
+  LAUNCH(c, tile_flags, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, flag.p);
+  const int64_t nt = exclusive_scan(c, flag.p, pos.p, a.n);
+  a.tiles.alloc(c, (size_t)nt + 1);
+  LAUNCH(c, tile_fill, blocks_for(a.n, 256), 256, 0, a.n, flag.p, pos.p, a.tiles.p, (int)nt);
+  a.ntiles = (int32_t)nt;
+}
+
+void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out) {
+  out.alloc(c, a.n, new_ncols, a.nnz);
+  CUDA_CHECK(cudaMemcpyAsync(out.rp.p, a.rp.p, sizeof(int32_t) * (a.n + 1), cudaMemcpyDeviceToDevice, c.stream));
+  if (a.nnz) {
+    CUDA_CHECK(cudaMemcpyAsync(out.v.p, a.v.p, sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice, c.stream));
+    LAUNCH(c, map_cols_kernel, blocks_for(a.nnz, 256), 256, 0, a.nnz, a.ci.p, d_map, out.ci.p);
+  }
+}
 
 void csr_upload(Ctx& c, int64_t n, int64_t m, const int64_t* h_rp, const int64_t* h_ci,
                 const double* h_v, Csr& out) {
@@ -159,7 +217,18 @@ void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
+// y = A x: the tiled coalesced kernel (tiled.cuh); tiles are a per-matrix
+// cache built on first use (outside graph capture).
 void spmv(Ctx& c, const Csr& a, const double* x, double* y) {
+  if (a.n == 0) return;
+  Csr& m = const_cast<Csr&>(a);
+  build_tiles(c, m);
+  TileView tv{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n};
+  LAUNCH_ROWS(c, EpiStore, tv, x, EpiStore{y});
+}
+
+// reference-order thread-per-row SpMV (kept for A/B checks of the tiled path)
+void spmv_thread_rows(Ctx& c, const Csr& a, const double* x, double* y) {
   if (a.n == 0) return;
   LAUNCH(c, spmv_rows, blocks_for(a.n, 128), 128, 0, a.n, a.rp.p, a.ci.p, a.v.p, x, y);
 }

@@ -12,6 +12,10 @@ void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_
 void spmv(Ctx& c, const Csr& a, const double* x, double* y);
 void with_full_diagonal(Ctx& c, const Csr& a, Csr& out);
 void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
+// tile starts for the tiled row kernels (tiled.cuh); idempotent
+void build_tiles(Ctx& c, Csr& a);
+// out = a with every column j replaced by map[j] (order-preserving maps only)
+void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out);
 
 // spgemm.cu -------------------------------------------------------------------
 // C = A B with per-entry accumulation in A-row order (sparse.cpp:203-242).

@@ -1,0 +1,193 @@
+// Bit-exact CSR row kernels with two work decompositions, chosen per matrix
+// by its mean row length (Csr::ntiles / tiles are built once, build_tiles()).
+//
+// * short rows (mean <= kShortRow): thread per row, batched loads
+//   (rowdot.cuh). A warp's 32 consecutive rows are contiguous in memory,
+//   so the warp still touches whole cache lines.
+// * long rows: WARP TILES. A tile = the rows whose first nonzero falls in one
+//   kWarpNnz-entry chunk of the nnz arrays. Each warp owns one tile:
+//   phase 1 streams the tile's column indices and values with unit stride
+//   (fully coalesced), gathers x and stores every product a_ij * x_j --
+//   rounded exactly as the reference rounds it -- in the warp's slice of
+//   shared memory; phase 2 (after __syncwarp, no block barrier) has one lane
+//   per row add its products in column order (the reference's sequential
+//   order, sparse.cpp:193-198) and run the epilogue.
+// Both give the reference's bits. Tiles longer than the shared slice (rows
+// of more than ~kWarpCap - kWarpNnz entries) fall back to the batched
+// per-lane loop for that tile.
+#pragma once
+
+#include "rowdot.cuh"
+
+namespace airg {
+
+constexpr int kTileThreads = 256;           // 8 warps per block
+constexpr int kWarpsPerBlock = kTileThreads / 32;
+constexpr int kWarpNnz = 256;               // chunk size that cuts tiles
+constexpr int kWarpCap = 384;               // shared products per warp
+constexpr int kShortRow = 6;                // mean nnz/row below which rows win
+
+struct TileView {
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* v;
+  const int32_t* tiles;  // nullptr => thread-per-row mode
+  int ntiles;
+  int nrows;
+};
+
+// ---- thread per row -----------------------------------------------------------
+template <class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const double* __restrict__ x,
+                                                            Epi epi) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m.nrows) epi.row(i, dot_ordered(__ldg(m.rp + i), __ldg(m.rp + i + 1), m.ci, m.v, x));
+  epi.finish();
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_thread_fc(TileView m,
+                                                               const double* __restrict__ x, Epi epi) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.nrows) return;
+  double sf, sc;
+  dot_ordered_fc(__ldg(m.rp + i), __ldg(m.rp + i + 1), m.ci, m.v, x, sf, sc);
+  epi.row2(i, sf, sc);
+}
+
+// ---- warp tiles -----------------------------------------------------------------
+template <class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_warp_tiles(TileView m,
+                                                                const double* __restrict__ x,
+                                                                Epi epi) {
+  __shared__ double prod_all[kWarpsPerBlock][kWarpCap];
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * kWarpsPerBlock + w;
+  if (t < m.ntiles) {
+    double* prod = prod_all[w];
+    const int r0 = __ldg(m.tiles + t), r1 = __ldg(m.tiles + t + 1);
+    const int k0 = __ldg(m.rp + r0), k1 = __ldg(m.rp + r1);
+    const int cnt = k1 - k0;
+    if (cnt > kWarpCap) {
+      for (int r = r0 + lane; r < r1; r += 32)
+        epi.row(r, dot_ordered(__ldg(m.rp + r), __ldg(m.rp + r + 1), m.ci, m.v, x));
+    } else {
+#pragma unroll 4
+      for (int j = lane; j < cnt; j += 32) {
+        const int k = k0 + j;
+        prod[j] = __dmul_rn(__ldg(m.v + k), __ldg(x + __ldg(m.ci + k)));
+      }
+      __syncwarp();
+      for (int r = r0 + lane; r < r1; r += 32) {
+        const int s = __ldg(m.rp + r) - k0, e = __ldg(m.rp + r + 1) - k0;
+        double acc = 0.0;
+        for (int q = s; q < e; ++q) acc = __dadd_rn(acc, prod[q]);
+        epi.row(r, acc);
+      }
+    }
+  }
+  epi.finish();
+}
+
+// F-row variant: columns with bit 31 set are C columns; the F and C partial
+// sums are kept apart (solve.cpp:72-80). Epi::row2(r, sf, sc).
+template <class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_warp_tiles_fc(TileView m,
+                                                                   const double* __restrict__ x,
+                                                                   Epi epi) {
+  __shared__ double prod_all[kWarpsPerBlock][kWarpCap];
+  __shared__ uint8_t isc_all[kWarpsPerBlock][kWarpCap];
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * kWarpsPerBlock + w;
+  if (t >= m.ntiles) return;
+  double* prod = prod_all[w];
+  uint8_t* isc = isc_all[w];
+  const int r0 = __ldg(m.tiles + t), r1 = __ldg(m.tiles + t + 1);
+  const int k0 = __ldg(m.rp + r0), k1 = __ldg(m.rp + r1);
+  const int cnt = k1 - k0;
+  if (cnt > kWarpCap) {
+    for (int r = r0 + lane; r < r1; r += 32) {
+      double sf, sc;
+      dot_ordered_fc(__ldg(m.rp + r), __ldg(m.rp + r + 1), m.ci, m.v, x, sf, sc);
+      epi.row2(r, sf, sc);
+    }
+    return;
+  }
+#pragma unroll 4
+  for (int j = lane; j < cnt; j += 32) {
+    const int k = k0 + j;
+    const int c = __ldg(m.ci + k);
+    prod[j] = __dmul_rn(__ldg(m.v + k), __ldg(x + (c & 0x7fffffff)));
+    isc[j] = c < 0;
+  }
+  __syncwarp();
+  for (int r = r0 + lane; r < r1; r += 32) {
+    const int s = __ldg(m.rp + r) - k0, e = __ldg(m.rp + r + 1) - k0;
+    double sf = 0.0, sc = 0.0;
+    for (int q = s; q < e; ++q) {
+      if (isc[q])
+        sc = __dadd_rn(sc, prod[q]);
+      else
+        sf = __dadd_rn(sf, prod[q]);
+    }
+    epi.row2(r, sf, sc);
+  }
+}
+
+// grid size for either mode
+inline unsigned rows_grid(const TileView& m) {
+  if (m.tiles) return (unsigned)((m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock > 0
+                                     ? (m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock
+                                     : 1);
+  return (unsigned)((m.nrows + kTileThreads - 1) / kTileThreads > 0
+                        ? (m.nrows + kTileThreads - 1) / kTileThreads
+                        : 1);
+}
+
+// Launch helpers (used inside LAUNCH-counted wrappers).
+#define LAUNCH_ROWS(ctx, Epi, view, x, epi)                                          \
+  do {                                                                               \
+    if ((view).tiles)                                                                \
+      LAUNCH(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
+    else                                                                             \
+      LAUNCH(ctx, rows_thread<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
+  } while (0)
+// programmatic-dependent-launch variants (used inside the captured V-cycle)
+#define LAUNCH_ROWS_P(ctx, Epi, view, x, epi)                                                   \
+  do {                                                                                          \
+    if ((view).tiles)                                                                           \
+      LAUNCH_PDL(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);    \
+    else                                                                                        \
+      LAUNCH_PDL(ctx, rows_thread<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);        \
+  } while (0)
+#define LAUNCH_ROWS_FC_P(ctx, Epi, view, x, epi)                                                \
+  do {                                                                                          \
+    if ((view).tiles)                                                                           \
+      LAUNCH_PDL(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
+    else                                                                                        \
+      LAUNCH_PDL(ctx, rows_thread_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
+  } while (0)
+#define LAUNCH_ROWS_FC(ctx, Epi, view, x, epi)                                          \
+  do {                                                                                  \
+    if ((view).tiles)                                                                   \
+      LAUNCH(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
+    else                                                                                \
+      LAUNCH(ctx, rows_thread_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
+  } while (0)
+
+// ---- epilogues ---------------------------------------------------------------
+struct EpiStore {  // y = A x
+  double* y;
+  __device__ void row(int r, double acc) const { y[r] = acc; }
+  __device__ void finish() const {}
+};
+
+}  // namespace airg

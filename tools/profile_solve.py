@@ -1,0 +1,64 @@
+"""Profiling driver: build the C2 hierarchy, warm up, then run ONE solve
+between cudaProfilerStart/Stop so `ncu --profile-from-start off` captures
+exactly the kernels of one timed step (setup excluded).
+
+  python tools/profile_solve.py [--config 2] [--what solve|spmv|setup]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2408_08262_b200 import airg, problems  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--what", default="solve")
+    args = ap.parse_args()
+    ctx = airg.Context(0)
+    p = problems.make(args.config, args.scale)
+    prm = problems.setup_params(args.config)
+    a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
+    dA = airg.DeviceCSR.upload(a, ctx)
+    if args.what == "setup":
+        airg.setup(dA, ctx=ctx, **prm)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        h = airg.setup(dA, ctx=ctx, **prm)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return
+    h = airg.setup(dA, ctx=ctx, **prm)
+    tb = ctx.to_device(p.b)
+    tx = ctx.empty(p.n, torch.float64)
+    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    for _ in range(2):
+        st, _ = h.solve_device(tb, tx, **sk)
+    torch.cuda.synchronize()
+    if args.what == "spmv":
+        A0 = h.matrix_handle(0, 0)
+        x = torch.rand(p.n, dtype=torch.float64, device=ctx.tdev)
+        y = torch.empty_like(x)
+        airg.spmv_device(A0, x, y, ctx=ctx)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        for _ in range(3):
+            airg.spmv_device(A0, x, y, ctx=ctx)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return
+    torch.cuda.profiler.start()
+    st, _ = h.solve_device(tb, tx, **sk)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print("iterations", st.iterations, "levels", h.n_levels)
+
+
+if __name__ == "__main__":
+    main()
