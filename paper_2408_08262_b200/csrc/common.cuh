@@ -95,11 +95,15 @@ inline void launch_pdl(Ctx& c, void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c.stream;
+  static const bool enabled = [] {
+    const char* e = getenv("AIRG_PDL");
+    return !(e && e[0] == '0');
+  }();
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = enabled ? 1 : 0;
   c.launches++;
   CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
@@ -191,6 +195,11 @@ struct Csr {
   DBuf<int32_t> tiles;  // row starts of the warp tiles (tiled.cuh), built on demand
   int32_t ntiles = -1;
   int8_t row_mode = 0;  // 0 unbuilt, 1 thread per row, 2 warp tiles
+  // SELL-32-sigma copy for the solve (sell.cuh), built on demand
+  DBuf<int32_t> s_off, s_len, s_perm, s_ci;
+  DBuf<double> s_v;
+  int32_t s_nslices = -1;
+  int32_t s_g = 1;  // lanes per row
 
   Csr() = default;
   Csr(Csr&&) = default;

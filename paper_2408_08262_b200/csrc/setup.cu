@@ -69,12 +69,16 @@ void alloc_workspace(Ctx& c, Hier& h) {
     L.rf.alloc(c, (size_t)std::max(1, L.map.nf));
     L.sc.alloc(c, (size_t)std::max(1, L.map.nf));
     map_columns(c, L.aff, L.map.f_to_fine.p, L.a.n, L.affg);
-    for (Csr* m : {&L.r, &L.af, &L.affg, &L.ffinv}) build_tiles(c, *m);
+    for (Csr* m : {&L.r, &L.af, &L.affg, &L.ffinv}) {
+      build_tiles(c, *m);
+      if (solve_layout_sell()) build_sell(c, *m);
+    }
   }
-  build_tiles(c, h.coarse_a);
-  build_tiles(c, h.coarse_inv);
   Csr& top = h.levels.empty() ? h.coarse_a : h.levels.front().a;
-  build_tiles(c, top);
+  for (Csr* m : {&h.coarse_a, &h.coarse_inv, &top}) {
+    build_tiles(c, *m);
+    if (solve_layout_sell()) build_sell(c, *m);
+  }
   const size_t nc = (size_t)std::max(1, h.coarse_a.n);
   h.cb.alloc(c, nc);
   h.cx.alloc(c, nc);

@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include "hier.cuh"
+#include "sell.cuh"
 #include "tiled.cuh"
 
 namespace airg {
@@ -104,6 +105,25 @@ struct EpiResid {
 inline TileView tv(const Csr& m) {
   return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n};
 }
+inline SellView svw(const Csr& m) {
+  return SellView{m.s_off.p, m.s_len.p, m.s_perm.p, m.s_ci.p, m.s_v.p, m.n, m.s_nslices, m.s_g};
+}
+// solve layout: CSR row kernels (default) or SELL-32/G (AIRG_LAYOUT=sell)
+bool use_sell() { return solve_layout_sell(); }
+#define ROWS(Epi, M, x, epi)                                                          \
+  do {                                                                                \
+    if (use_sell())                                                                   \
+      LAUNCH_PDL(c, sell_rows<Epi>, sell_grid(svw(M)), 256, 0, svw(M), x, epi);       \
+    else                                                                              \
+      LAUNCH_ROWS_P(c, Epi, tv(M), x, epi);                                           \
+  } while (0)
+#define ROWS_FC(Epi, M, x, epi)                                                       \
+  do {                                                                                \
+    if (use_sell())                                                                   \
+      LAUNCH_PDL(c, sell_rows_fc<Epi>, sell_grid(svw(M)), 256, 0, svw(M), x, epi);    \
+    else                                                                              \
+      LAUNCH_ROWS_FC_P(c, Epi, tv(M), x, epi);                                        \
+  } while (0)
 
 // x_l = 0 + P e_c  (solve.cpp:139-141: pe = spmv(P, ec); x += 1.0 * pe)
 __global__ void k_prolong(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
@@ -220,7 +240,7 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     const double* bl = l == 0 ? b0 : lv.b.p;
     double* bn = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
     if (lv.r.n)
-      LAUNCH_ROWS_P(c,EpiStore, tv(lv.r), bl, EpiStore{bn});
+      ROWS(EpiStore, lv.r, bl, EpiStore{bn});
   }
   // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
   {
@@ -230,10 +250,10 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
       for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
         const double* r = rhs;
         if (it > 0) {
-          LAUNCH_ROWS_P(c,EpiCres, tv(h.coarse_a), h.cx.p, (EpiCres{rhs, h.cr.p}));
+          ROWS(EpiCres, h.coarse_a, h.cx.p, (EpiCres{rhs, h.cr.p}));
           r = h.cr.p;
         }
-        LAUNCH_ROWS_P(c,EpiCupd, tv(h.coarse_inv), r, (EpiCupd{h.cx.p, it == 0 ? 1 : 0}));
+        ROWS(EpiCupd, h.coarse_inv, r, (EpiCupd{h.cx.p, it == 0 ? 1 : 0}));
       }
       if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * n, c.stream));
     }
@@ -247,12 +267,12 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     LAUNCH_PDL(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
     for (int64_t s = 0; s < cfg.up_f_smooths && nf > 0; ++s) {
       if (s == 0)
-        LAUNCH_ROWS_FC_P(c,EpiFres1, tv(lv.af), lv.x.p,
+        ROWS_FC(EpiFres1, lv.af, lv.x.p,
                        (EpiFres1{bl, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p}));
       else
-        LAUNCH_ROWS_P(c,EpiFres2, tv(lv.affg), lv.x.p,
+        ROWS(EpiFres2, lv.affg, lv.x.p,
                     (EpiFres2{bl, lv.map.f_to_fine.p, lv.sc.p, lv.rf.p}));
-      LAUNCH_ROWS_P(c,EpiFupd, tv(lv.ffinv), lv.rf.p, (EpiFupd{lv.map.f_to_fine.p, lv.x.p}));
+      ROWS(EpiFupd, lv.ffinv, lv.rf.p, (EpiFupd{lv.map.f_to_fine.p, lv.x.p}));
     }
   }
 }
@@ -263,9 +283,9 @@ double* vcycle_output(Hier& h) { return h.levels.empty() ? h.cx.p : h.levels[0].
 // r = b - A x, ||r||^2 -> h.scal[0]
 void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double* r) {
   const Csr& a = h.top();
-  const TileView v = tv(a);
-  LAUNCH_ROWS_P(c,EpiResid, v, x, (EpiResid{b, r, h.part.p, 0.0}));
-  LAUNCH_PDL(c, k_sum_partials, 1, 1024, 0, h.part.p, (int)rows_grid(v), h.scal.p);
+  ROWS(EpiResid, a, x, (EpiResid{b, r, h.part.p, 0.0}));
+  const int nb = use_sell() ? (int)sell_grid(svw(a)) : (int)rows_grid(tv(a));
+  LAUNCH_PDL(c, k_sum_partials, 1, 1024, 0, h.part.p, nb, h.scal.p);
 }
 
 int64_t graph_key(const airg_solve_config& cfg) {

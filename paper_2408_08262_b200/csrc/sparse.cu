@@ -1,6 +1,7 @@
 // L0 sparse kernels: CSR upload/validation, SpMV, with_full_diagonal and
 // drop_entries (reference: proj/src/sparse.cpp).
 #include "sparse.cuh"
+#include "sell.cuh"
 #include "tiled.cuh"
 
 namespace airg {
@@ -132,6 +133,59 @@ __global__ void tile_fill(int n, const int32_t* __restrict__ flag, const int32_t
   if (i == 0) tiles[ntiles] = n;
 }
 
+// ---- SELL-32-sigma build (sell.cuh)
+// sort (len desc, row asc) inside each 256-row window with a bitonic sort
+__global__ void __launch_bounds__(kSellWindow) sell_sort(int n, const int32_t* __restrict__ rp,
+                                                         int32_t* __restrict__ perm,
+                                                         int32_t* __restrict__ slen) {
+  __shared__ int32_t klen[kSellWindow], kidx[kSellWindow];
+  const int t = threadIdx.x, r = blockIdx.x * kSellWindow + t;
+  klen[t] = r < n ? rp[r + 1] - rp[r] : -1;
+  kidx[t] = r;
+  __syncthreads();
+  for (int size = 2; size <= kSellWindow; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int p = t ^ stride;
+      if (p > t) {
+        // "a before b" in the target order: longer first, then lower row
+        const bool dir = (t & size) == 0;
+        const bool t_after_p = (klen[t] < klen[p]) || (klen[t] == klen[p] && kidx[t] > kidx[p]);
+        if (t_after_p == dir) {
+          int a = klen[t]; klen[t] = klen[p]; klen[p] = a;
+          a = kidx[t]; kidx[t] = kidx[p]; kidx[p] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (r < n) {
+    perm[r] = kidx[t];
+    slen[r] = klen[t];
+  }
+}
+// slice width in slots: chunks of its longest (first) row x 32
+__global__ void sell_width(int nslices, int rows_per_slice, int g, const int32_t* __restrict__ slen,
+                           int32_t* __restrict__ w) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nslices) w[s] = ((slen[s * rows_per_slice] + g - 1) / g) * 32;
+}
+__global__ void sell_fill(int n, int rows_per_slice, int g, const int32_t* __restrict__ rp,
+                          const int32_t* __restrict__ ci, const double* __restrict__ v,
+                          const int32_t* __restrict__ perm, const int32_t* __restrict__ slen,
+                          const int32_t* __restrict__ off, int32_t* __restrict__ sci,
+                          double* __restrict__ sv) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int o = perm[r], len = slen[r];
+  const int s = r / rows_per_slice, rl = r % rows_per_slice;
+  const int base = off[s] + rl * g;
+  for (int k = 0; k < len; ++k) {
+    const int slot = base + (k / g) * 32 + (k % g);
+    sci[slot] = ci[rp[o] + k];
+    sv[slot] = v[rp[o] + k];
+  }
+}
+
 __global__ void map_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci,
                                 const int32_t* __restrict__ map, int32_t* __restrict__ out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,13 +196,22 @@ __global__ void map_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci,
 
 // Row-kernel decomposition for this matrix: thread per row for short rows,
 // warp tiles otherwise (tiled.cuh). AIRG_ROWS=thread|tiles forces one.
+// Default: thread per row (measured fastest on the C2 hierarchy, see
+// profiles/); AIRG_ROWS=auto picks warp tiles for long rows, =tiles forces them.
 static int rows_override() {
   static int v = [] {
     const char* e = getenv("AIRG_ROWS");
-    if (!e) return 0;
-    if (!strcmp(e, "thread")) return 1;
+    if (!e || !strcmp(e, "thread")) return 1;
     if (!strcmp(e, "tiles")) return 2;
-    return 0;
+    return 0;  // auto
+  }();
+  return v;
+}
+
+bool solve_layout_sell() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_LAYOUT");
+    return e && !strcmp(e, "sell");
   }();
   return v;
 }
@@ -169,6 +232,41 @@ void build_tiles(Ctx& c, Csr& a) {
   a.tiles.alloc(c, (size_t)nt + 1);
   LAUNCH(c, tile_fill, blocks_for(a.n, 256), 256, 0, a.n, flag.p, pos.p, a.tiles.p, (int)nt);
   a.ntiles = (int32_t)nt;
+}
+
+void build_sell(Ctx& c, Csr& a) {
+  if (a.s_nslices >= 0) return;
+  const int n = a.n;
+  static const int g_override = [] {
+    const char* e = getenv("AIRG_SELL_G");
+    return e ? atoi(e) : 0;
+  }();
+  int g = g_override > 0 ? g_override : sell_lanes_for(n ? (double)a.nnz / n : 0.0);
+  if (g != 1 && g != 2 && g != 4 && g != 8) g = 1;
+  const int rps = 32 / g;
+  const int nslices = (n + rps - 1) / rps;
+  a.s_g = g;
+  a.s_perm.alloc(c, (size_t)std::max(1, n));
+  a.s_len.alloc(c, (size_t)std::max(1, n + kSellWindow));
+  a.s_len.zero(c);
+  a.s_off.alloc(c, (size_t)nslices + 1);
+  if (n == 0) {
+    a.s_off.zero(c);
+    a.s_nslices = 0;
+    return;
+  }
+  LAUNCH(c, sell_sort, (n + kSellWindow - 1) / kSellWindow, kSellWindow, 0, n, a.rp.p, a.s_perm.p,
+         a.s_len.p);
+  DBuf<int32_t> w(c, (size_t)nslices);
+  LAUNCH(c, sell_width, blocks_for(nslices, 256), 256, 0, nslices, rps, g, a.s_len.p, w.p);
+  const int64_t slots = exclusive_scan(c, w.p, a.s_off.p, nslices);
+  a.s_ci.alloc(c, (size_t)slots);
+  a.s_v.alloc(c, (size_t)slots);
+  a.s_ci.zero(c);
+  a.s_v.zero(c);
+  LAUNCH(c, sell_fill, blocks_for(n, 256), 256, 0, n, rps, g, a.rp.p, a.ci.p, a.v.p, a.s_perm.p,
+         a.s_len.p, a.s_off.p, a.s_ci.p, a.s_v.p);
+  a.s_nslices = nslices;
 }
 
 void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out) {
@@ -222,6 +320,11 @@ void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_
 void spmv(Ctx& c, const Csr& a, const double* x, double* y) {
   if (a.n == 0) return;
   Csr& m = const_cast<Csr&>(a);
+  if (m.s_nslices >= 0) {  // solve matrices carry a SELL copy (sell.cuh)
+    SellView sv{m.s_off.p, m.s_len.p, m.s_perm.p, m.s_ci.p, m.s_v.p, m.n, m.s_nslices, m.s_g};
+    LAUNCH(c, sell_rows<EpiStore>, sell_grid(sv), 256, 0, sv, x, EpiStore{y});
+    return;
+  }
   build_tiles(c, m);
   TileView tv{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n};
   LAUNCH_ROWS(c, EpiStore, tv, x, EpiStore{y});

@@ -14,6 +14,10 @@ void with_full_diagonal(Ctx& c, const Csr& a, Csr& out);
 void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
 // tile starts for the tiled row kernels (tiled.cuh); idempotent
 void build_tiles(Ctx& c, Csr& a);
+// SELL-32-sigma solve copy (sell.cuh); idempotent
+void build_sell(Ctx& c, Csr& a);
+// solve layout switch: SELL only with AIRG_LAYOUT=sell (CSR rows by default)
+bool solve_layout_sell();
 // out = a with every column j replaced by map[j] (order-preserving maps only)
 void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out);
 

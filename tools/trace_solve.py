@@ -23,20 +23,29 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--out", default="gpurun_out/trace_summary.txt")
+    ap.add_argument("--what", default="solve", choices=["solve", "setup"])
     args = ap.parse_args()
     ctx = airg.Context(0)
     p = problems.make(args.config, args.scale)
     prm = problems.setup_params(args.config)
     a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
-    h = airg.setup(airg.DeviceCSR.upload(a, ctx), ctx=ctx, **prm)
+    dA = airg.DeviceCSR.upload(a, ctx)
+    h = airg.setup(dA, ctx=ctx, **prm)
     tb = ctx.to_device(p.b)
     tx = ctx.empty(p.n, torch.float64)
     sk = dict(coarse_iterations=prm["coarse_iterations"])
     for _ in range(3):
         h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
+
+    class _St:
+        iterations = 0
+    st = _St()
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-        st, _ = h.solve_device(tb, tx, **sk)
+        if args.what == "setup":
+            h2 = airg.setup(dA, ctx=ctx, **prm)
+        else:
+            st, _ = h.solve_device(tb, tx, **sk)
         torch.cuda.synchronize()
     path = "/tmp/trace_solve.json"
     prof.export_chrome_trace(path)
@@ -44,8 +53,11 @@ def main():
     ev.sort(key=lambda e: e["ts"])
     tot = collections.defaultdict(float)
     cnt = collections.Counter()
+    import re
     for e in ev:
-        name = e["name"].split("(")[0].split("::")[-1][:48]
+        nm = e["name"].replace("(anonymous namespace)::", "")
+        mt = re.search(r"(\w+)(<[^()]*>)?\(", nm)
+        name = (mt.group(1) + (mt.group(2) or "")).replace("airg::", "")[:48] if mt else nm[:48]
         tot[name] += e["dur"]
         cnt[name] += 1
     span = (ev[-1]["ts"] + ev[-1]["dur"] - ev[0]["ts"]) if ev else 0.0
@@ -56,6 +68,33 @@ def main():
              if gaps else "no gaps"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"{k:48s} {cnt[k]:6d} {v:10.1f} us {100 * v / max(busy, 1e-9):5.1f}%  mean {v / cnt[k]:.2f}")
+    if args.what == "solve" and st.iterations > 2:
+        # per-level breakdown of one middle iteration (kernel order of
+        # enqueue_vcycle: R_0..R_{L-1}, coarse (2 ci - 1), then per level
+        # L-1..0: prolong, fres1, fupd, fres2, fupd, ..., then axpy, resid, sum)
+        L = h.n_levels
+        nco = 2 * prm["coarse_iterations"] - 1
+        per_it = L + nco + L * (1 + 2 * 2) + 3
+        first = 2  # dot_partials, reduce_partials (bnorm)
+        it = min(5, st.iterations - 1)
+        seq = ev[first + it * per_it: first + (it + 1) * per_it]
+        lines.append(f"-- iteration {it}: {len(seq)} kernels, span "
+                     f"{seq[-1]['ts'] + seq[-1]['dur'] - seq[0]['ts']:.1f} us")
+        lines.append(f"{'lvl':>3} {'n':>8} {'nnzR':>9} {'R us':>7} {'GB/s':>6} | {'nnzAF':>9} {'fres1':>7} {'GB/s':>6}"
+                     f" | {'nnzFF':>8} {'fres2':>6} | {'nnzQ':>8} {'fupd':>6} {'GB/s':>6} | {'prol':>5}")
+        asc = seq[L + nco: L + nco + 5 * L]
+        for l in range(L):
+            info = h.level(l)
+            r_us = seq[l]["dur"]
+            blk = asc[(L - 1 - l) * 5:(L - l) * 5]
+            nnz_af = info.nnz_ff + info.nnz_fc
+            br = 12 * info.nnz_r + 4 * info.n_c + 16 * info.n_c + 8 * info.n
+            baf = 12 * nnz_af + 4 * info.n_f + 8 * info.n + 32 * info.n_f
+            bq = 12 * info.nnz_ffinv + 4 * info.n_f + 24 * info.n_f
+            lines.append(f"{l:3d} {info.n:8d} {info.nnz_r:9d} {r_us:7.1f} {br / r_us / 1e3:6.0f} | {nnz_af:9d} "
+                         f"{blk[1]['dur']:7.1f} {baf / blk[1]['dur'] / 1e3:6.0f} | {info.nnz_ff:8d} "
+                         f"{blk[3]['dur']:6.1f} | {info.nnz_ffinv:8d} {blk[2]['dur']:6.1f} "
+                         f"{bq / blk[2]['dur'] / 1e3:6.0f} | {blk[0]['dur']:5.1f}")
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     open(args.out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
