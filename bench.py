@@ -197,15 +197,117 @@ def config_dict(args, p, par):
             "parallelism": par, "l2": "flushed (512 MiB write) before each timed step; hierarchy > L2"}
 
 
+def run_gpu_dist(args):
+    """N > 1 (torchrun, one process per GPU): weak scaling of the C2 family
+    (128 x 128 x 128N cells, one 128^3 z-slab = 2,097,152 unknowns per GPU).
+    Every rank builds the global hierarchy (replicated setup), keeps its row
+    slabs (z-slabs on level 0, the replay halving rule on coarser levels, the
+    coarsest grid gathered on rank 0) and runs the distributed Richardson
+    solve with NCCL halo exchanges and allreduced norms."""
+    import torch
+    import torch.distributed as dist
+    from paper_2408_08262_b200 import airg, problems
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = airg.Context(local)
+    stream = ctx.stream
+    p = problems.c2_structured_3d(128, nz_slabs=ws)
+    prm = problems.setup_params(2)
+    a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
+    dA = airg.DeviceCSR.upload(a, ctx)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h = airg.setup(dA, ctx=ctx, **prm)
+    e1.record(stream)
+    e1.synchronize()
+    setup_ms = e0.elapsed_time(e1)
+    uid = [airg.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = airg.NcclComm(ws, rank, uid[0])
+    slab = p.n // ws
+    starts = np.arange(ws + 1, dtype=np.int64) * slab
+    d = airg.Dist(h, ws, rank=rank, comm=comm, threshold=2.0, starts=starts)
+    lo, hi = starts[rank], starts[rank + 1]
+    with torch.cuda.stream(stream):
+        tb = torch.from_numpy(p.b[lo:hi].copy()).to(ctx.tdev)
+        tx = torch.empty(hi - lo, dtype=torch.float64, device=ctx.tdev)
+        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=ctx.tdev)
+    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    for _ in range(args.warmup):
+        st, _ = d.solve_device(tb, tx, **sk)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = []
+    l0 = ctx.launches()
+    clk = ClockSampler(local).__enter__()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        st, _ = d.solve_device(tb, tx, **sk)
+        s1.record(stream)
+        s1.synchronize()
+        times.append(s0.elapsed_time(s1))
+    launches = ctx.launches() - l0
+    # e2e: host slab in, host slab out
+    hb = torch.from_numpy(p.b[lo:hi].copy()).pin_memory()
+    hx = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        with torch.cuda.stream(stream):
+            tb.copy_(hb, non_blocking=True)
+        d.solve_device(tb, tx, **sk)
+        with torch.cuda.stream(stream):
+            hx.copy_(tx, non_blocking=True)
+        s1.record(stream)
+        s1.synchronize()
+        if k >= args.warmup:
+            e2e.append(s0.elapsed_time(s1))
+    clk.__exit__(None, None, None)
+    t = torch.tensor([sum(times), sum(e2e) / len(e2e)], device=ctx.tdev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms, e2e_ms = float(t[0]), float(t[1])
+    value = p.n * args.steps / (tot_ms / 1e3)
+    levels = [d.level_info(l) for l in range(h.n_levels + 1)]
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 family 128 x 128 x {128 * ws} (one 128^3 z-slab per GPU)",
+                   "unknowns": int(p.n), "nnz": int(p.nnz), "alpha": 0.5, "ddc_fraction": 0.1,
+                   "poly_order": 4, "parallelism": f"row slabs x{ws} (NCCL halos, replay halving, "
+                   "gathered coarse grid; setup replicated per GPU)",
+                   "l2": "flushed (512 MiB write) before each timed step"},
+        "iterations": int(st.iterations), "final_relative_residual": float(st.final_relative_residual),
+        "levels": int(h.n_levels), "setup_ms": setup_ms,
+        "active_ranks": [lv["active"] for lv in levels],
+        "e2e": {"value": p.n / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
+                "d2h_bytes_per_step": 8 * int(hi - lo), "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    del d, comm
+    dist.destroy_process_group()
+    return 0
+
+
 def run_gpu(args):
     import torch
     from paper_2408_08262_b200 import airg, problems
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if ws > 1 or args.force_dist:
+        return run_gpu_dist(args)
     dev = local
     ctx = airg.Context(dev)
     stream = ctx.stream
@@ -372,6 +474,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-nx", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the distributed (NCCL row-slab) path even on one rank")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "airg":
         args.warmup = 3

@@ -275,6 +275,41 @@ int airg_solve_host(airg_ctx* ctx, const airg_hier* h,
                     double* h_x, airg_solve_stats* stats, double* h_history,
                     int64_t history_cap);
 
+/* ---- multi-GPU: row-slab distributed solve ------------------ */
+typedef struct airg_dist airg_dist;
+/* NCCL bootstrap: rank 0 creates the 128-byte id, every rank passes it. */
+int airg_nccl_unique_id(void* h_id128);
+int airg_nccl_comm_create(int nranks, int rank, const void* h_id128, void** comm_out);
+int airg_nccl_comm_destroy(void* comm);
+/* Partition a built hierarchy into P contiguous row slabs per level with the
+ * reference's halving rule (partition_model.cpp:77-112, threshold on the
+ * local/non-local nnz ratio) and a gathered coarsest grid. rank = -1
+ * emulates all P ranks on this context's GPU (phase by phase; no kernel
+ * waits on another rank); rank >= 0 builds only that rank's slab and needs
+ * an NCCL communicator. h_level0_starts (P+1, nullable) fixes level 0's
+ * slabs (e.g. z-slabs). */
+int airg_dist_create(airg_ctx* ctx, const airg_hier* h, int32_t nranks,
+                     int32_t rank, void* nccl_comm, double halving_threshold,
+                     const int64_t* h_level0_starts, airg_dist** out);
+/* Richardson solve over the slabs: emulation takes/returns global device
+ * vectors; with NCCL d_b / d_x are this rank's level-0 slab. */
+int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg,
+                    const double* d_b, double* d_x, airg_solve_stats* stats,
+                    double* h_history, int64_t history_cap);
+/* Per level: active ranks, replay-rule ratios, total halo entries. */
+int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
+                         double* ratio_before, double* ratio_after,
+                         int32_t* triggered, int64_t* halo_entries,
+                         int64_t* h_starts /* P+1, nullable */);
+int airg_dist_destroy(airg_dist* d);
+/* Host-only halo plan of one rank (the rule the device build applies):
+ * sorted distinct referenced indices outside [starts[rank], starts[rank+1]),
+ * plus the per-owner receive counts. No GPU needed (CPU / gloo tests). */
+int airg_dist_plan_host(int32_t nranks, const int64_t* h_starts, int32_t rank,
+                        const int64_t* h_cols, int64_t ncols,
+                        int64_t* h_halo_out, int64_t halo_cap,
+                        int64_t* n_halo, int64_t* h_recv_counts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,20 @@ def lib() -> C.CDLL:
                             C.c_int64], C.c_int),
             "airg_solve_host": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                                  C.c_int64], C.c_int),
+            "airg_spmv_host": ([_VP, _VP, _VP, _VP], C.c_int),
+            "airg_cf_split_host": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, C.c_int32,
+                                    C.c_double, C.c_int64, _VP, _P(abi.CfReport)], C.c_int),
+            "airg_nccl_unique_id": ([_VP], C.c_int),
+            "airg_nccl_comm_create": ([C.c_int, C.c_int, _VP, _P(_VP)], C.c_int),
+            "airg_nccl_comm_destroy": ([_VP], C.c_int),
+            "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
+            "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
+                                 C.c_int64], C.c_int),
+            "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
+                                      _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
+            "airg_dist_destroy": ([_VP], C.c_int),
+            "airg_dist_plan_host": ([C.c_int32, _VP, C.c_int32, _VP, C.c_int64, _VP, C.c_int64,
+                                     _P(C.c_int64), _VP], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -596,3 +610,88 @@ def gmres_solve(h: Hierarchy, b, restart: int = 30, **solve_kw) -> SolveResult:
     """Right-preconditioned restarted GMRES with one AIRG V-cycle per
     iteration (BASELINE config 0's outer solver)."""
     return richardson_solve(h, b, outer=1, gmres_restart=restart, **solve_kw)
+
+
+# ---- multi-GPU: row-slab distributed solve (SURVEY §8e) ---------------------------
+def plan_host(starts, rank: int, cols):
+    """Host halo plan of one rank (no GPU): (sorted halo indices, recv counts per owner)."""
+    s = np.ascontiguousarray(starts, np.int64)
+    c = np.ascontiguousarray(cols, np.int64)
+    P = len(s) - 1
+    halo = np.zeros(max(1, len(c)), np.int64)
+    nh = C.c_int64()
+    rc = np.zeros(P, np.int64)
+    _check(lib().airg_dist_plan_host(P, s.ctypes.data, int(rank), c.ctypes.data, len(c), halo.ctypes.data,
+                                     len(halo), C.byref(nh), rc.ctypes.data))
+    return halo[: nh.value].copy(), rc
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().airg_nccl_unique_id(buf))
+    return buf.raw
+
+
+class NcclComm:
+    def __init__(self, nranks: int, rank: int, uid: bytes):
+        buf = C.create_string_buffer(uid, 128)
+        h = _VP()
+        _check(lib().airg_nccl_comm_create(int(nranks), int(rank), buf, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().airg_nccl_comm_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+
+class Dist:
+    """A hierarchy partitioned into row slabs (airg_dist)."""
+
+    def __init__(self, h: Hierarchy, nranks: int, rank: int = -1, comm: NcclComm | None = None,
+                 threshold: float = 2.0, starts=None):
+        self.h, self.ctx, self.P, self.rank = h, h.ctx, int(nranks), int(rank)
+        st = None if starts is None else np.ascontiguousarray(starts, np.int64)
+        self._starts = st
+        out = _VP()
+        _check(lib().airg_dist_create(self.ctx.h, h.h, self.P, self.rank, comm.h if comm else None,
+                                      float(threshold), st.ctypes.data if st is not None else None,
+                                      C.byref(out)))
+        self.d = out
+        self._comm = comm
+
+    def __del__(self):
+        if getattr(self, "d", None):
+            try:
+                lib().airg_dist_destroy(self.d)
+            except Exception:
+                pass
+            self.d = None
+
+    def level_info(self, l: int) -> dict:
+        a, t = C.c_int32(), C.c_int32()
+        rb, ra = C.c_double(), C.c_double()
+        halo = C.c_int64()
+        starts = np.zeros(self.P + 1, np.int64)
+        _check(lib().airg_dist_level_info(self.d, int(l), C.byref(a), C.byref(rb), C.byref(ra), C.byref(t),
+                                          C.byref(halo), starts.ctypes.data))
+        return dict(active=a.value, ratio_before=rb.value, ratio_after=ra.value, triggered=bool(t.value),
+                    halo=halo.value, starts=starts)
+
+    def solve_device(self, tb, tx, history_cap: int = 0, **solve_kw):
+        cfg = abi.solve_config(**solve_kw)
+        st = abi.SolveStats()
+        hist = np.zeros(max(history_cap, 1))
+        _check(lib().airg_dist_solve(self.ctx.h, self.d, C.byref(cfg), _ptr(tb), _ptr(tx), C.byref(st),
+                                     hist.ctypes.data if history_cap else None, int(history_cap)))
+        return st, hist[: min(history_cap, st.history_len)]
+
+    def solve(self, b, **solve_kw):
+        """Emulated (rank = -1): global host b -> global host x."""
+        tb = self.ctx.to_device(np.asarray(b, np.float64))
+        tx = self.ctx.empty(len(b), self.ctx.torch.float64)
+        st, hist = self.solve_device(tb, tx, history_cap=1024, **solve_kw)
+        return SolveResult(self.ctx.to_host(tx), st, hist)

@@ -4,7 +4,7 @@
 #include <cstring>
 #include <memory>
 
-#include "hier.cuh"
+#include "dist.cuh"
 
 using namespace airg;
 
@@ -611,6 +611,125 @@ int airg_solve_host(airg_ctx* ctx, const airg_hier* hp, const airg_solve_config*
     if (hist)
       for (int64_t k = 0; k < cap && k < (int64_t)hv.size(); ++k) hist[k] = hv[k];
     if (st) *st = s;
+  });
+}
+
+// ---- multi-GPU ----------------------------------------------------------------------
+struct airg_dist {
+  Ctx* c = nullptr;
+  DHier d;
+};
+
+int airg_nccl_unique_id(void* id) {
+  return guard([&] {
+    need(id, "id buffer");
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) throw CudaError("ncclGetUniqueId failed");
+    static_assert(sizeof(u) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id, &u, sizeof u);
+  });
+}
+
+int airg_nccl_comm_create(int nranks, int rank, const void* id, void** comm) {
+  return guard([&] {
+    need(id, "id");
+    need(comm, "comm out");
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    ncclComm_t cm;
+    const ncclResult_t r = ncclCommInitRank(&cm, nranks, u, rank);
+    if (r != ncclSuccess) throw CudaError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    *comm = cm;
+  });
+}
+
+int airg_nccl_comm_destroy(void* comm) {
+  return guard([&] {
+    if (comm) ncclCommDestroy((ncclComm_t)comm);
+  });
+}
+
+int airg_dist_create(airg_ctx* ctx, const airg_hier* h, int32_t nranks, int32_t rank, void* comm,
+                     double threshold, const int64_t* starts, airg_dist** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(h, "hierarchy");
+    need(out, "output handle");
+    bind(ctx->c);
+    auto d = std::make_unique<airg_dist>();
+    d->c = &ctx->c;
+    dist_create(ctx->c, const_cast<airg_hier*>(h)->h, nranks, rank, (ncclComm_t)comm, threshold, starts,
+                d->d);
+    *out = d.release();
+  });
+}
+
+int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg, const double* b,
+                    double* x, airg_solve_stats* st, double* hist, int64_t cap) {
+  return guard([&] {
+    need(ctx, "context");
+    need(d, "dist");
+    need(cfg, "config");
+    bind(ctx->c);
+    std::vector<double> hv;
+    airg_solve_stats s;
+    dist_solve(ctx->c, d->d, *cfg, b, x, s, hv);
+    if (hist)
+      for (int64_t k = 0; k < cap && k < (int64_t)hv.size(); ++k) hist[k] = hv[k];
+    if (st) *st = s;
+  });
+}
+
+int airg_dist_level_info(const airg_dist* dp, int64_t l, int32_t* active, double* rb, double* ra,
+                         int32_t* trig, int64_t* halo, int64_t* starts) {
+  return guard([&] {
+    need(dp, "dist");
+    const DHier& d = dp->d;
+    if (l < 0 || l > (int64_t)d.lv.size()) throw InvalidArgument("level out of range");
+    if (l == (int64_t)d.lv.size()) {  // coarsest: gathered
+      if (active) *active = 1;
+      if (rb) *rb = INFINITY;
+      if (ra) *ra = INFINITY;
+      if (trig) *trig = 0;
+      int64_t hs = 0;
+      for (const auto& R : d.CX.rk) hs += R.nhalo;
+      if (halo) *halo = hs;
+      if (starts) std::memcpy(starts, d.cpart.s.data(), sizeof(int64_t) * d.cpart.s.size());
+      return;
+    }
+    const DLevel& D = d.lv[l];
+    if (active) *active = D.active;
+    if (rb) *rb = D.ratio_before;
+    if (ra) *ra = D.ratio_after;
+    if (trig) *trig = D.triggered;
+    int64_t hs = 0;
+    for (const auto& R : D.X.rk) hs += R.nhalo;
+    if (halo) *halo = hs;
+    if (starts) std::memcpy(starts, D.fine.s.data(), sizeof(int64_t) * D.fine.s.size());
+  });
+}
+
+int airg_dist_destroy(airg_dist* d) {
+  return guard([&] {
+    if (!d) return;
+    if (d->c) bind(*d->c);
+    delete d;
+  });
+}
+
+int airg_dist_plan_host(int32_t nranks, const int64_t* starts, int32_t rank, const int64_t* cols,
+                        int64_t ncols, int64_t* halo_out, int64_t cap, int64_t* n_halo,
+                        int64_t* recv_counts) {
+  return guard([&] {
+    need(starts, "starts");
+    if (rank < 0 || rank >= nranks) throw InvalidArgument("dist: rank out of range");
+    std::vector<int64_t> s(starts, starts + nranks + 1), halo, rc;
+    halo_plan_host(s, rank, cols, ncols, halo, rc);
+    if (n_halo) *n_halo = (int64_t)halo.size();
+    if (halo_out)
+      for (int64_t k = 0; k < cap && k < (int64_t)halo.size(); ++k) halo_out[k] = halo[k];
+    if (recv_counts)
+      for (int q = 0; q < nranks; ++q) recv_counts[q] = rc[q];
   });
 }
 

@@ -1,0 +1,890 @@
+// Row-slab distributed AIRG solve (see dist.cuh).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "dist.cuh"
+#include "tiled.cuh"
+
+namespace airg {
+
+#define NCCL_CHECK(x)                                                          \
+  do {                                                                         \
+    ncclResult_t r__ = (x);                                                    \
+    if (r__ != ncclSuccess)                                                    \
+      throw CudaError(std::string("NCCL error: ") + ncclGetErrorString(r__)); \
+  } while (0)
+
+int Part::owner(int64_t g) const {
+  return (int)(std::upper_bound(s.begin(), s.end(), g) - s.begin()) - 1;
+}
+
+namespace {
+
+// ---- device helpers ---------------------------------------------------------
+__device__ __forceinline__ int owner_of(const int64_t* __restrict__ s, int P, int64_t g) {
+  int lo = 0, hi = P;  // largest r with s[r] <= g (and non-empty ranges win)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s[mid] <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void k_locality(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const int64_t* __restrict__ s, int P,
+                           unsigned long long* __restrict__ cnt) {  // [2P]: local, nonlocal
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = owner_of(s, P, i);
+  unsigned long long loc = 0, non = 0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) (owner_of(s, P, ci[k]) == r ? loc : non)++;
+  if (loc) atomicAdd(cnt + r, loc);
+  if (non) atomicAdd(cnt + P + r, non);
+}
+
+__global__ void k_slice(int n_local, int64_t row0, const int32_t* __restrict__ rp,
+                        const int32_t* __restrict__ ci, const double* __restrict__ v,
+                        int32_t* __restrict__ orp, int32_t* __restrict__ oci,
+                        double* __restrict__ ov) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n_local) return;
+  const int base = rp[row0];
+  orp[i] = rp[row0 + i] - base;
+  if (i == n_local) return;
+  for (int k = rp[row0 + i]; k < rp[row0 + i + 1]; ++k) {
+    oci[k - base] = ci[k];
+    ov[k - base] = v[k];
+  }
+}
+
+__global__ void k_mark_cols(int64_t nnz, const int32_t* __restrict__ ci, int64_t lo, int64_t hi,
+                            int32_t* __restrict__ mark) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  const int64_t c = ci[k] & 0x7fffffff;
+  if (c < lo || c >= hi) mark[c] = 1;
+}
+__global__ void k_mark_vals(int64_t n, const int32_t* __restrict__ idx, int64_t lo, int64_t hi,
+                            int32_t* __restrict__ mark) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t c = idx[k];
+  if (c >= 0 && (c < lo || c >= hi)) mark[c] = 1;
+}
+__global__ void k_compact(int64_t N, const int32_t* __restrict__ mark, const int32_t* __restrict__ pos,
+                          int32_t* __restrict__ out) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < N && mark[g]) out[pos[g]] = (int32_t)g;
+}
+__global__ void k_src(int64_t nh, const int32_t* __restrict__ halo, const int64_t* __restrict__ s, int P,
+                      int32_t* __restrict__ src_rank, int32_t* __restrict__ src_idx) {
+  const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= nh) return;
+  const int r = owner_of(s, P, halo[h]);
+  src_rank[h] = r;
+  src_idx[h] = (int32_t)(halo[h] - s[r]);
+}
+__device__ __forceinline__ int32_t remap_one(int64_t c, int64_t lo, int64_t hi, int64_t own,
+                                             const int32_t* __restrict__ halo, int64_t nh) {
+  if (c >= lo && c < hi) return (int32_t)(c - lo);
+  int64_t a = 0, b = nh;
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (halo[m] < c)
+      a = m + 1;
+    else
+      b = m;
+  }
+  return (int32_t)(own + a);
+}
+__global__ void k_remap_cols(int64_t nnz, int32_t* __restrict__ ci, int64_t lo, int64_t hi, int64_t own,
+                             const int32_t* __restrict__ halo, int64_t nh) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  const int32_t raw = ci[k];
+  const int32_t flag = raw & (int32_t)0x80000000;
+  ci[k] = remap_one(raw & 0x7fffffff, lo, hi, own, halo, nh) | flag;
+}
+__global__ void k_remap_vals(int64_t n, const int32_t* __restrict__ in, int32_t* __restrict__ out,
+                             int64_t lo, int64_t hi, int64_t own, const int32_t* __restrict__ halo,
+                             int64_t nh) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  out[k] = in[k] < 0 ? -1 : remap_one(in[k], lo, hi, own, halo, nh);
+}
+__global__ void k_shift(int64_t n, const int32_t* __restrict__ in, int64_t off, int32_t* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = (int32_t)(in[k] - off);
+}
+// count of sorted[] entries < bound[j]  (F points below each slab boundary)
+__global__ void k_count_below(const int32_t* __restrict__ sorted, int64_t n, const int64_t* __restrict__ bound,
+                              int nb, int64_t* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nb) return;
+  int64_t a = 0, b = n;
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (sorted[m] < bound[j])
+      a = m + 1;
+    else
+      b = m;
+  }
+  out[j] = a;
+}
+
+// halo exchange kernels
+__global__ void k_gather_halo(int64_t nh, const int32_t* __restrict__ src_rank,
+                              const int32_t* __restrict__ src_idx, double* const* __restrict__ bases,
+                              double* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < nh) dst[h] = bases[src_rank[h]][src_idx[h]];
+}
+__global__ void k_pack(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                       double* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) dst[k] = src[idx[k]];
+}
+
+// solve kernels (local versions of solve.cu's)
+__global__ void k_prolong_l(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
+                            double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = i < n ? __ldg(pmap + i) : -1;
+  pdl_wait();
+  pdl_trigger();
+  if (i >= n) return;
+  const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
+  x[i] = __dadd_rn(0.0, __dmul_rn(1.0, pe));
+}
+__global__ void k_axpy1_l(int n, const double* __restrict__ e, double* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(1.0, e[i]));
+}
+__global__ void k_sum(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double sm[32];
+  pdl_wait();
+  pdl_trigger();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *out = s;
+  }
+}
+
+// epilogues (local layouts)
+struct LStore {
+  double* y;
+  __device__ void row(int r, double acc) const { y[r] = acc; }
+  __device__ void finish() const {}
+};
+struct LFres1 {
+  const double* b;
+  const int32_t* f2f;
+  double* rf;
+  double* sc;
+  __device__ void row2(int k, double sf, double s) const {
+    sc[k] = s;
+    rf[k] = __dsub_rn(__dsub_rn(b[f2f[k]], sf), s);
+  }
+};
+struct LFres2 {
+  const double* b;
+  const int32_t* f2f;
+  const double* sc;
+  double* rf;
+  __device__ void row(int k, double sf) const { rf[k] = __dsub_rn(__dsub_rn(b[f2f[k]], sf), sc[k]); }
+  __device__ void finish() const {}
+};
+struct LFupd {
+  const int32_t* f2f;
+  double* x;
+  __device__ void row(int k, double d) const {
+    const int i = f2f[k];
+    x[i] = __dadd_rn(x[i], d);
+  }
+  __device__ void finish() const {}
+};
+struct LCres {
+  const double* rhs;
+  double* r;
+  __device__ void row(int i, double acc) const { r[i] = __dsub_rn(rhs[i], acc); }
+  __device__ void finish() const {}
+};
+struct LCupd {
+  double* e;
+  int first;
+  __device__ void row(int i, double acc) const {
+    const double e0 = first ? 0.0 : e[i];
+    e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
+  }
+  __device__ void finish() const {}
+};
+struct LResid {
+  const double* b;
+  double* r;
+  double* part;
+  mutable double s;
+  __device__ void row(int i, double acc) const {
+    const double ri = __dsub_rn(b[i], acc);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  __device__ void finish() const {
+    __shared__ double sm[kTileThreads / 32];
+    double v = s;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      v = threadIdx.x < kTileThreads / 32 ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+  }
+};
+
+inline TileView rows_of(const Csr& m) { return TileView{m.rp.p, m.ci.p, m.v.p, nullptr, 0, m.n}; }
+
+// ---- host helpers ---------------------------------------------------------------
+// partition_rows (partition_model.cpp:8-22) on `active` logical ranks, logical
+// rank k placed on physical rank k * stride
+Part balanced(int64_t n, int active, int P) {
+  const int ranks = (int)std::min<int64_t>(active, std::max<int64_t>(n, 1));
+  const int stride = std::max(1, P / std::max(1, active));
+  std::vector<int64_t> lstart(ranks + 1, 0);
+  const int64_t base = n / ranks, extra = n % ranks;
+  for (int k = 0; k < ranks; ++k) lstart[k + 1] = lstart[k] + base + (k < extra ? 1 : 0);
+  Part p;
+  p.s.assign(P + 1, n);
+  for (int q = 0; q <= P; ++q) {
+    // first logical block placed at a physical rank >= q
+    int k = (q + stride - 1) / stride;
+    p.s[q] = k < ranks ? lstart[k] : n;
+  }
+  p.s[0] = 0;
+  p.s[P] = n;
+  return p;
+}
+
+// merge adjacent logical pairs (r -> r / 2, partition_model.cpp:101-104)
+Part merged(const Part& p, int active, int new_active) {
+  const int P = p.P();
+  const int stride_old = std::max(1, P / std::max(1, active));
+  const int stride_new = std::max(1, P / std::max(1, new_active));
+  // logical block k of the old partition starts at p.s[k * stride_old]
+  std::vector<int64_t> lstart;
+  for (int k = 0; k < active; ++k) lstart.push_back(p.s[std::min(P, k * stride_old)]);
+  lstart.push_back(p.s[P]);
+  std::vector<int64_t> ns(new_active + 1);
+  for (int k = 0; k < new_active; ++k) ns[k] = lstart[std::min(active, 2 * k)];
+  ns[new_active] = p.s[P];
+  Part out;
+  out.s.assign(P + 1, p.s[P]);
+  for (int q = 0; q <= P; ++q) {
+    int k = (q + stride_new - 1) / stride_new;
+    out.s[q] = k < new_active ? ns[k] : p.s[P];
+  }
+  out.s[0] = 0;
+  return out;
+}
+
+Part gathered(int64_t n, int P) {
+  Part p;
+  p.s.assign(P + 1, n);
+  p.s[0] = 0;
+  return p;
+}
+
+// mean over ranks of local / non-local nnz (partition_model.cpp:53-64)
+double locality(Ctx& c, const Csr& a, const Part& p) {
+  const int P = p.P();
+  if (a.n == 0) return INFINITY;
+  DBuf<int64_t> ds(c, (size_t)P + 1);
+  to_device(c, ds.p, p.s.data(), (size_t)P + 1);
+  DBuf<unsigned long long> cnt(c, (size_t)2 * P);
+  cnt.zero(c);
+  LAUNCH(c, k_locality, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, ds.p, P, cnt.p);
+  std::vector<unsigned long long> h(2 * P);
+  to_host(c, h.data(), cnt.p, h.size());
+  double sum = 0.0;
+  int contributing = 0;
+  for (int r = 0; r < P; ++r) {
+    if (h[P + r] == 0) continue;
+    sum += (double)h[r] / (double)h[P + r];
+    ++contributing;
+  }
+  return contributing ? sum / contributing : INFINITY;
+}
+
+void slice(Ctx& c, const Csr& a, int64_t lo, int64_t hi, Csr& out) {
+  const int64_t n = hi - lo;
+  int32_t b[2] = {0, 0};
+  if (n > 0) {
+    to_host(c, &b[0], a.rp.p + lo, 1);
+    to_host(c, &b[1], a.rp.p + hi, 1);
+  }
+  out.alloc(c, n, a.m, b[1] - b[0]);
+  if (n > 0)
+    LAUNCH(c, k_slice, blocks_for(n + 1, 256), 256, 0, (int)n, lo, a.rp.p, a.ci.p, a.v.p, out.rp.p,
+           out.ci.p, out.v.p);
+  else
+    out.rp.zero(c);
+}
+
+// One rank's halo of a DVec from marks over the global index space.
+struct Marks {
+  DBuf<int32_t> m;
+  int64_t N = 0;
+  void init(Ctx& c, int64_t n) {
+    N = n;
+    m.alloc(c, (size_t)std::max<int64_t>(1, n));
+    m.zero(c);
+  }
+  void cols(Ctx& c, const Csr& a, int64_t lo, int64_t hi) {
+    if (a.nnz) LAUNCH(c, k_mark_cols, blocks_for(a.nnz, 256), 256, 0, a.nnz, a.ci.p, lo, hi, m.p);
+  }
+  void vals(Ctx& c, const int32_t* idx, int64_t n, int64_t lo, int64_t hi) {
+    if (n) LAUNCH(c, k_mark_vals, blocks_for(n, 256), 256, 0, n, idx, lo, hi, m.p);
+  }
+};
+
+void set_halo(Ctx& c, DVec& V, int r, Marks& mk) {
+  DVec::Rank& R = V.rk[r];
+  R.own = V.part.cnt(r);
+  R.lo = V.part.lo(r);
+  DBuf<int32_t> pos(c, (size_t)V.N + 1);
+  const int64_t nh = V.N ? exclusive_scan(c, mk.m.p, pos.p, V.N) : 0;
+  R.nhalo = nh;
+  R.halo.alloc(c, (size_t)std::max<int64_t>(1, nh));
+  if (V.N) LAUNCH(c, k_compact, blocks_for(V.N, 256), 256, 0, V.N, mk.m.p, pos.p, R.halo.p);
+  std::vector<int32_t> hh((size_t)nh);
+  to_host(c, hh.data(), R.halo.p, (size_t)nh);
+  R.halo_host.assign(hh.begin(), hh.end());
+}
+
+// After every rank's halo is known: buffers, emulation tables, NCCL lists.
+void finalize(Ctx& c, DVec& V, const DHier& d) {
+  const int P = V.part.P();
+  DBuf<int64_t> ds(c, (size_t)P + 1);
+  to_device(c, ds.p, V.part.s.data(), (size_t)P + 1);
+  std::vector<double*> bases(P, nullptr);
+  for (int r = 0; r < P; ++r) {
+    DVec::Rank& R = V.rk[r];
+    R.recv_off.assign(P, 0);
+    R.recv_cnt.assign(P, 0);
+    for (int64_t g : R.halo_host) R.recv_cnt[V.part.owner(g)]++;
+    for (int q = 1; q < P; ++q) R.recv_off[q] = R.recv_off[q - 1] + R.recv_cnt[q - 1];
+    if (!d.mine(r)) continue;
+    R.buf.alloc(c, (size_t)std::max<int64_t>(1, R.own + R.nhalo));
+    R.buf.zero(c);
+    bases[r] = R.buf.p;
+    if (d.me < 0 && R.nhalo) {
+      R.src_rank.alloc(c, (size_t)R.nhalo);
+      R.src_idx.alloc(c, (size_t)R.nhalo);
+      LAUNCH(c, k_src, blocks_for(R.nhalo, 256), 256, 0, R.nhalo, R.halo.p, ds.p, P, R.src_rank.p,
+             R.src_idx.p);
+    }
+  }
+  if (d.me >= 0) {  // my send lists: the entries of every peer's halo that I own
+    DVec::Rank& M = V.rk[d.me];
+    std::vector<int32_t> idx;
+    M.send_off.assign(P, 0);
+    M.send_cnt.assign(P, 0);
+    for (int q = 0; q < P; ++q) {
+      M.send_off[q] = (int64_t)idx.size();
+      if (q == d.me) continue;
+      for (int64_t g : V.rk[q].halo_host)
+        if (g >= M.lo && g < M.lo + M.own) idx.push_back((int32_t)(g - M.lo));
+      M.send_cnt[q] = (int64_t)idx.size() - M.send_off[q];
+    }
+    M.send_idx.alloc(c, std::max<size_t>(1, idx.size()));
+    to_device(c, M.send_idx.p, idx.data(), idx.size());
+    M.send_buf.alloc(c, std::max<size_t>(1, idx.size()));
+  } else {
+    V.bases.alloc(c, (size_t)P);
+    to_device(c, V.bases.p, bases.data(), (size_t)P);
+  }
+}
+
+void remap(Ctx& c, Csr& a, const DVec& V, int r) {
+  const DVec::Rank& R = V.rk[r];
+  if (a.nnz)
+    LAUNCH(c, k_remap_cols, blocks_for(a.nnz, 256), 256, 0, a.nnz, a.ci.p, R.lo, R.lo + R.own, R.own,
+           R.halo.p, R.nhalo);
+  a.m = (int32_t)(R.own + R.nhalo);
+}
+
+// halo exchange of one vector (all local ranks)
+void exchange(Ctx& c, DHier& d, DVec& V) {
+  const int P = V.part.P();
+  if (d.me < 0) {
+    for (int r = 0; r < P; ++r) {
+      DVec::Rank& R = V.rk[r];
+      if (R.nhalo)
+        LAUNCH_PDL(c, k_gather_halo, blocks_for(R.nhalo, 256), 256, 0, R.nhalo, R.src_rank.p,
+                   R.src_idx.p, (double* const*)V.bases.p, R.buf.p + R.own);
+    }
+    return;
+  }
+  DVec::Rank& M = V.rk[d.me];
+  const int64_t ns = M.send_off[P - 1] + M.send_cnt[P - 1];
+  if (ns) LAUNCH_PDL(c, k_pack, blocks_for(ns, 256), 256, 0, ns, M.send_idx.p, M.buf.p, M.send_buf.p);
+  bool any = ns > 0 || M.nhalo > 0;
+  for (int q = 0; q < P && !any; ++q) any = M.send_cnt[q] || M.recv_cnt[q];
+  NCCL_CHECK(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == d.me) continue;
+    if (M.send_cnt[q])
+      NCCL_CHECK(ncclSend(M.send_buf.p + M.send_off[q], (size_t)M.send_cnt[q], ncclDouble, q, d.comm, c.stream));
+    if (M.recv_cnt[q])
+      NCCL_CHECK(ncclRecv(M.buf.p + M.own + M.recv_off[q], (size_t)M.recv_cnt[q], ncclDouble, q, d.comm,
+                          c.stream));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+void halo_plan_host(const std::vector<int64_t>& starts, int rank, const int64_t* cols, int64_t ncols,
+                    std::vector<int64_t>& halo, std::vector<int64_t>& recv_cnt) {
+  Part p;
+  p.s = starts;
+  const int64_t lo = p.lo(rank), hi = lo + p.cnt(rank);
+  halo.clear();
+  for (int64_t k = 0; k < ncols; ++k) {
+    const int64_t g = cols[k] & 0x7fffffffLL;
+    if (g < lo || g >= hi) halo.push_back(g);
+  }
+  std::sort(halo.begin(), halo.end());
+  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+  recv_cnt.assign(p.P(), 0);
+  for (int64_t g : halo) recv_cnt[p.owner(g)]++;
+}
+
+void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double threshold,
+                 const int64_t* level0_starts, DHier& d) {
+  if (P < 1) throw InvalidArgument("dist: need at least one rank");
+  if (me >= P) throw InvalidArgument("dist: rank out of range");
+  if (me >= 0 && P > 1 && !comm) throw InvalidArgument("dist: a communicator is needed per rank");
+  d.P = P;
+  d.me = me;
+  d.comm = comm;
+  d.threshold = threshold;
+  const int L = (int)h.levels.size();
+  d.top_n = h.top_n();
+  // ---- partitions: the reference replay rule, then the coarse gather
+  d.lv.resize(L);
+  int active = P;
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    const Csr& A = h.levels[l].a;
+    Part p = (l == 0 && level0_starts) ? Part{std::vector<int64_t>(level0_starts, level0_starts + P + 1)}
+                                       : balanced(A.n, active, P);
+    D.ratio_before = locality(c, A, p);
+    D.ratio_after = D.ratio_before;
+    if (D.ratio_before < threshold && active > 1) {
+      const int na = (active + 1) / 2;
+      p = merged(p, active, na);
+      active = na;
+      D.triggered = true;
+      D.ratio_after = locality(c, A, p);
+    }
+    D.active = active;
+    D.fine = p;
+  }
+  d.cpart = gathered(h.coarse_a.n, P);
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    D.coarse_part = l + 1 < L ? d.lv[l + 1].fine : d.cpart;
+    // F partition: #F points below each fine boundary
+    const Level& Lv = h.levels[l];
+    DBuf<int64_t> bnd(c, (size_t)P + 1), cnt(c, (size_t)P + 1);
+    to_device(c, bnd.p, D.fine.s.data(), (size_t)P + 1);
+    LAUNCH(c, k_count_below, 1, 64, 0, Lv.map.f_to_fine.p, (int64_t)Lv.map.nf, bnd.p, P + 1, cnt.p);
+    D.fpart.s.resize(P + 1);
+    to_host(c, D.fpart.s.data(), cnt.p, (size_t)P + 1);
+    D.rk.resize(P);
+    D.B.part = D.fine;
+    D.B.N = Lv.a.n;
+    D.X.part = D.fine;
+    D.X.N = Lv.a.n;
+    D.RF.part = D.fpart;
+    D.RF.N = Lv.map.nf;
+    D.B.rk.resize(P);
+    D.X.rk.resize(P);
+    D.RF.rk.resize(P);
+  }
+  d.CB.part = d.cpart;
+  d.CX.part = d.cpart;
+  d.CR.part = d.cpart;
+  d.CB.N = d.CX.N = d.CR.N = h.coarse_a.n;
+  d.CB.rk.resize(P);
+  d.CX.rk.resize(P);
+  d.CR.rk.resize(P);
+  d.XS.part = L ? d.lv[0].fine : d.cpart;
+  d.XS.N = h.top_n();
+  d.XS.rk.resize(P);
+  d.rk.resize(P);
+
+  // ---- local slices with global columns (every rank: the halo lists of all
+  // ranks are needed to derive send lists; only my ranks keep matrices)
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    const Level& Lv = h.levels[l];
+    for (int r = 0; r < P; ++r) {
+      DLevel::Rank& R = D.rk[r];
+      const int64_t flo = D.fpart.lo(r), fhi = flo + D.fpart.cnt(r);
+      const int64_t clo = D.coarse_part.lo(r), chi = clo + D.coarse_part.cnt(r);
+      const int64_t lo = D.fine.lo(r), hi = lo + D.fine.cnt(r);
+      slice(c, Lv.r, clo, chi, R.R);
+      slice(c, Lv.af, flo, fhi, R.AF);
+      slice(c, Lv.affg, flo, fhi, R.AFFG);
+      slice(c, Lv.ffinv, flo, fhi, R.FINV);
+      R.nf_own = fhi - flo;
+      R.n_own = hi - lo;
+      R.pmap.alloc(c, (size_t)std::max<int64_t>(1, hi - lo));
+      if (hi > lo)
+        CUDA_CHECK(cudaMemcpyAsync(R.pmap.p, Lv.pmap.p + lo, sizeof(int32_t) * (hi - lo),
+                                   cudaMemcpyDeviceToDevice, c.stream));
+      R.f2f.alloc(c, (size_t)std::max<int64_t>(1, fhi - flo));
+      if (fhi > flo)
+        LAUNCH(c, k_shift, blocks_for(fhi - flo, 256), 256, 0, fhi - flo, Lv.map.f_to_fine.p + flo, lo,
+               R.f2f.p);
+      R.sc.alloc(c, (size_t)std::max<int64_t>(1, fhi - flo));
+      // halos: B_l <- R_l ; X_l <- AF, AFFG, P_{l-1} ; RF_l <- FINV
+      Marks mb, mx, mf;
+      mb.init(c, D.B.N);
+      mb.cols(c, R.R, lo, hi);
+      set_halo(c, D.B, r, mb);
+      mx.init(c, D.X.N);
+      mx.cols(c, R.AF, lo, hi);
+      mx.cols(c, R.AFFG, lo, hi);
+      if (l > 0) {
+        const DLevel::Rank& U = d.lv[l - 1].rk[r];
+        mx.vals(c, U.pmap.p, U.n_own, lo, hi);
+      }
+      set_halo(c, D.X, r, mx);
+      mf.init(c, D.RF.N);
+      mf.cols(c, R.FINV, flo, fhi);
+      set_halo(c, D.RF, r, mf);
+    }
+  }
+  // coarsest: A_c / Ac^-1 on their owner, CX halo also serves P_{L-1}
+  for (int r = 0; r < P; ++r) {
+    DHier::Rank& T = d.rk[r];
+    const int64_t lo = d.cpart.lo(r), hi = lo + d.cpart.cnt(r);
+    slice(c, h.coarse_a, lo, hi, T.AC);
+    slice(c, h.coarse_inv, lo, hi, T.ACI);
+    Marks mc, mb, mr;
+    mc.init(c, d.CX.N);
+    mc.cols(c, T.AC, lo, hi);
+    if (L) {
+      const DLevel::Rank& U = d.lv[L - 1].rk[r];
+      mc.vals(c, U.pmap.p, U.n_own, lo, hi);
+    }
+    set_halo(c, d.CX, r, mc);
+    mb.init(c, d.CB.N);
+    mb.cols(c, T.ACI, lo, hi);
+    set_halo(c, d.CB, r, mb);
+    mr.init(c, d.CR.N);
+    mr.cols(c, T.ACI, lo, hi);
+    set_halo(c, d.CR, r, mr);
+    // top operator for the residual
+    const Csr& A0 = L ? h.levels[0].a : h.coarse_a;
+    const int64_t tlo = d.XS.part.lo(r), thi = tlo + d.XS.part.cnt(r);
+    slice(c, A0, tlo, thi, T.A0);
+    Marks ms;
+    ms.init(c, d.XS.N);
+    ms.cols(c, T.A0, tlo, thi);
+    set_halo(c, d.XS, r, ms);
+    T.rhs.alloc(c, (size_t)std::max<int64_t>(1, thi - tlo));
+  }
+  // ---- buffers, tables, remapped columns
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    finalize(c, D.B, d);
+    finalize(c, D.X, d);
+    finalize(c, D.RF, d);
+  }
+  finalize(c, d.CB, d);
+  finalize(c, d.CX, d);
+  finalize(c, d.CR, d);
+  finalize(c, d.XS, d);
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    const DVec& Xn = l + 1 < L ? d.lv[l + 1].X : d.CX;
+    for (int r = 0; r < P; ++r) {
+      DLevel::Rank& R = D.rk[r];
+      if (!d.mine(r)) {
+        R = DLevel::Rank();
+        continue;
+      }
+      remap(c, R.R, D.B, r);
+      remap(c, R.AF, D.X, r);
+      remap(c, R.AFFG, D.X, r);
+      remap(c, R.FINV, D.RF, r);
+      const DVec::Rank& XR = Xn.rk[r];
+      if (R.n_own)
+        LAUNCH(c, k_remap_vals, blocks_for(R.n_own, 256), 256, 0, R.n_own, R.pmap.p, R.pmap.p, XR.lo,
+               XR.lo + XR.own, XR.own, XR.halo.p, XR.nhalo);
+    }
+  }
+  d.nparts = 0;
+  d.part_off.assign(P, 0);
+  for (int r = 0; r < P; ++r) {
+    DHier::Rank& T = d.rk[r];
+    if (!d.mine(r)) {
+      T = DHier::Rank();
+      continue;
+    }
+    remap(c, T.AC, d.CX, r);
+    remap(c, T.ACI, d.CR, r);  // CB and CR share the column space; CR's halo is used
+    remap(c, T.A0, d.XS, r);
+    d.part_off[r] = d.nparts;
+    d.nparts += (int)blocks_for(std::max(1, T.A0.n), kTileThreads);
+  }
+  d.part.alloc(c, (size_t)d.nparts + 8);
+  d.scal.alloc(c, 8);
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+namespace {
+
+void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
+  const int L = (int)d.lv.size();
+  const int P = d.P;
+  auto rank_loop = [&](auto&& f) {
+    for (int r = 0; r < P; ++r)
+      if (d.mine(r)) f(r);
+  };
+  // descent
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    exchange(c, d, D.B);
+    DVec& Bn = l + 1 < L ? d.lv[l + 1].B : d.CB;
+    rank_loop([&](int r) {
+      const Csr& R = D.rk[r].R;
+      if (R.n)
+        LAUNCH_PDL(c, rows_thread<LStore>, blocks_for(R.n, kTileThreads), kTileThreads, 0, rows_of(R),
+                   (const double*)D.B.rk[r].buf.p, LStore{Bn.rk[r].buf.p});
+    });
+  }
+  // coarse solve on the coarse owner(s); CB and CR feed Ac^-1 through CR's
+  // layout: copy the owned rhs into CR before the first application
+  for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
+    if (it == 0) {
+      rank_loop([&](int r) {
+        const int64_t own = d.CB.rk[r].own;
+        if (own)
+          CUDA_CHECK(cudaMemcpyAsync(d.CR.rk[r].buf.p, d.CB.rk[r].buf.p, sizeof(double) * own,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+      });
+    } else {
+      exchange(c, d, d.CX);
+      rank_loop([&](int r) {
+        const Csr& A = d.rk[r].AC;
+        if (A.n)
+          LAUNCH_PDL(c, rows_thread<LCres>, blocks_for(A.n, kTileThreads), kTileThreads, 0, rows_of(A),
+                     (const double*)d.CX.rk[r].buf.p, (LCres{d.CB.rk[r].buf.p, d.CR.rk[r].buf.p}));
+      });
+    }
+    exchange(c, d, d.CR);
+    rank_loop([&](int r) {
+      const Csr& A = d.rk[r].ACI;
+      if (A.n)
+        LAUNCH_PDL(c, rows_thread<LCupd>, blocks_for(A.n, kTileThreads), kTileThreads, 0, rows_of(A),
+                   (const double*)d.CR.rk[r].buf.p, (LCupd{d.CX.rk[r].buf.p, it == 0 ? 1 : 0}));
+    });
+  }
+  // ascent
+  for (int l = L - 1; l >= 0; --l) {
+    DLevel& D = d.lv[l];
+    DVec& Xn = l + 1 < L ? d.lv[l + 1].X : d.CX;
+    exchange(c, d, Xn);
+    rank_loop([&](int r) {
+      const DLevel::Rank& R = D.rk[r];
+      if (R.n_own)
+        LAUNCH_PDL(c, k_prolong_l, blocks_for(R.n_own, 128), 128, 0, (int)R.n_own, R.pmap.p,
+                   Xn.rk[r].buf.p, D.X.rk[r].buf.p);
+    });
+    for (int64_t s = 0; s < cfg.up_f_smooths; ++s) {
+      exchange(c, d, D.X);
+      rank_loop([&](int r) {
+        DLevel::Rank& R = D.rk[r];
+        if (!R.nf_own) return;
+        const double* bl = D.B.rk[r].buf.p;
+        if (s == 0)
+          LAUNCH_PDL(c, rows_thread_fc<LFres1>, blocks_for(R.AF.n, kTileThreads), kTileThreads, 0,
+                     rows_of(R.AF), (const double*)D.X.rk[r].buf.p,
+                     (LFres1{bl, R.f2f.p, D.RF.rk[r].buf.p, R.sc.p}));
+        else
+          LAUNCH_PDL(c, rows_thread<LFres2>, blocks_for(R.AFFG.n, kTileThreads), kTileThreads, 0,
+                     rows_of(R.AFFG), (const double*)D.X.rk[r].buf.p,
+                     (LFres2{bl, R.f2f.p, R.sc.p, D.RF.rk[r].buf.p}));
+      });
+      exchange(c, d, D.RF);
+      rank_loop([&](int r) {
+        DLevel::Rank& R = D.rk[r];
+        if (!R.nf_own) return;
+        LAUNCH_PDL(c, rows_thread<LFupd>, blocks_for(R.FINV.n, kTileThreads), kTileThreads, 0,
+                   rows_of(R.FINV), (const double*)D.RF.rk[r].buf.p, (LFupd{R.f2f.p, D.X.rk[r].buf.p}));
+      });
+    }
+  }
+}
+
+// x += e (owned), r = b - A x, ||r||^2 -> d.scal[0] (local sum under NCCL)
+void enqueue_update_residual(Ctx& c, DHier& d) {
+  const int L = (int)d.lv.size();
+  DVec& E = L ? d.lv[0].X : d.CX;
+  DVec& Rv = L ? d.lv[0].B : d.CB;
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const int64_t own = d.XS.rk[r].own;
+    if (own)
+      LAUNCH_PDL(c, k_axpy1_l, blocks_for(own, 256), 256, 0, (int)own, (const double*)E.rk[r].buf.p,
+                 d.XS.rk[r].buf.p);
+  }
+  exchange(c, d, d.XS);
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const Csr& A = d.rk[r].A0;
+    if (A.n)
+      LAUNCH_PDL(c, rows_thread<LResid>, blocks_for(A.n, kTileThreads), kTileThreads, 0, rows_of(A),
+                 (const double*)d.XS.rk[r].buf.p,
+                 (LResid{d.rk[r].rhs.p, Rv.rk[r].buf.p, d.part.p + d.part_off[r], 0.0}));
+    else
+      CUDA_CHECK(cudaMemsetAsync(d.part.p + d.part_off[r], 0, sizeof(double), c.stream));
+  }
+  LAUNCH_PDL(c, k_sum, 1, 1024, 0, (const double*)d.part.p, d.nparts, d.scal.p);
+}
+
+double read_norm2(Ctx& c, DHier& d, double* dev) {
+  if (d.me >= 0 && d.P > 1)
+    NCCL_CHECK(ncclAllReduce(dev, dev, 1, ncclDouble, ncclSum, d.comm, c.stream));
+  return read1(c, dev);
+}
+
+template <class F>
+uint64_t capture_graph(Ctx& c, cudaGraphExec_t* exec, F&& body) {
+  if (*exec) {
+    cudaGraphExecDestroy(*exec);
+    *exec = nullptr;
+  }
+  const uint64_t before = c.launches;
+  cudaGraph_t g;
+  CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(c.stream, &dummy);
+    if (dummy) cudaGraphDestroy(dummy);
+    throw;
+  }
+  CUDA_CHECK(cudaStreamEndCapture(c.stream, &g));
+  CUDA_CHECK(cudaGraphInstantiate(exec, g, 0));
+  CUDA_CHECK(cudaGraphDestroy(g));
+  const uint64_t k = c.launches - before;
+  c.launches = before;
+  return k;
+}
+
+}  // namespace
+
+void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
+                airg_solve_stats& st, std::vector<double>& hist) {
+  if (cfg.down_smooths != 0) throw InvalidArgument("solve: down_smooths > 0 is not offered by the GPU V-cycle");
+  if (cfg.rtol <= 0.0) throw InvalidArgument("richardson_solve: rtol must be positive");
+  if (cfg.outer != 0) throw InvalidArgument("dist: the distributed solve runs Richardson (outer = 0)");
+  std::memset(&st, 0, sizeof st);
+  const int L = (int)d.lv.size();
+  DVec& Rv = L ? d.lv[0].B : d.CB;
+  const auto t0 = std::chrono::steady_clock::now();
+  // scatter b (emulation: from the global vector; nccl: my slab)
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const int64_t own = d.XS.rk[r].own, lo = d.me < 0 ? d.XS.rk[r].lo : 0;
+    if (own) {
+      CUDA_CHECK(cudaMemcpyAsync(d.rk[r].rhs.p, d_b + lo, sizeof(double) * own, cudaMemcpyDeviceToDevice, c.stream));
+      CUDA_CHECK(cudaMemcpyAsync(Rv.rk[r].buf.p, d_b + lo, sizeof(double) * own, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    CUDA_CHECK(cudaMemsetAsync(d.XS.rk[r].buf.p, 0, sizeof(double) * std::max<int64_t>(1, own), c.stream));
+  }
+  // ||b||: sum of local squared norms
+  double bn2 = 0.0;
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const int64_t own = d.XS.rk[r].own;
+    if (!own) continue;
+    dot_async(c, d.rk[r].rhs.p, d.rk[r].rhs.p, own, d.scal.p + 1, d.part.p);
+    bn2 += read1(c, d.scal.p + 1);
+  }
+  if (d.me >= 0 && d.P > 1) {
+    to_device(c, d.scal.p + 2, &bn2, 1);
+    bn2 = read_norm2(c, d, d.scal.p + 2);
+  }
+  const double bnorm = std::sqrt(bn2);
+  if (bnorm == 0.0) {
+    st.converged = 1;
+    hist.push_back(0.0);
+  } else {
+    const int64_t key = cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31;
+    if (!d.graph || d.graph_key != key) {
+      d.graph_kernels = capture_graph(c, &d.graph, [&] {
+        enqueue_vcycle(c, d, cfg);
+        enqueue_update_residual(c, d);
+      });
+      d.graph_key = key;
+    }
+    for (int64_t it = 0;; ++it) {
+      const double rel = it == 0 ? 1.0 : std::sqrt(read_norm2(c, d, d.scal.p)) / bnorm;
+      hist.push_back(rel);
+      st.final_relative_residual = rel;
+      if (rel <= cfg.rtol) {
+        st.converged = 1;
+        st.iterations = it;
+        break;
+      }
+      if (it >= cfg.max_iterations) {
+        st.iterations = it;
+        break;
+      }
+      CUDA_CHECK(cudaGraphLaunch(d.graph, c.stream));
+      c.launches += d.graph_kernels;
+    }
+  }
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const int64_t own = d.XS.rk[r].own, lo = d.me < 0 ? d.XS.rk[r].lo : 0;
+    if (own)
+      CUDA_CHECK(cudaMemcpyAsync(d_x + lo, d.XS.rk[r].buf.p, sizeof(double) * own, cudaMemcpyDeviceToDevice,
+                                 c.stream));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  st.history_len = (int64_t)hist.size();
+}
+
+}  // namespace airg

@@ -1,0 +1,113 @@
+// Row-slab distributed AIRG solve.
+//
+// Every level's index spaces (fine rows, F points) are split into contiguous
+// slabs over the active ranks; each operator's rows live with the owner of
+// its output rows and read its input vector through a per-rank halo (the
+// remote entries its rows reference, grouped by owner). Row order and the
+// order of entries inside a row are untouched, only column indices are
+// remapped to the [owned | halo] local layout, so every row product is the
+// same sequential, separately rounded sum as on one GPU: the distributed
+// V-cycle is bit-identical to the single-GPU one (and to the reference).
+//
+// Active-GPU reduction follows the reference's replay rule
+// (partition_model.cpp:77-112): level by level, when the mean local /
+// non-local nnz ratio of the balanced partition drops below the threshold,
+// the active ranks halve by merging adjacent slabs (rank 2k keeps both). The
+// coarsest grid is gathered onto rank 0 for the polynomial coarse solve.
+//
+// Transport: kEmulate keeps all P ranks in one process on one GPU and runs
+// them phase by phase (no kernel ever waits on another rank); the halo
+// exchange is a gather kernel reading the owners' buffers. kNccl runs one
+// rank per process/GPU and exchanges halos with grouped ncclSend/ncclRecv
+// and reduces norms with ncclAllReduce.
+#pragma once
+
+#include <nccl.h>
+
+#include "hier.cuh"
+
+namespace airg {
+
+struct Part {
+  std::vector<int64_t> s;  // P + 1 starts
+  int P() const { return (int)s.size() - 1; }
+  int64_t lo(int r) const { return s[r]; }
+  int64_t cnt(int r) const { return s[r + 1] - s[r]; }
+  int owner(int64_t g) const;
+};
+
+// A vector over one partitioned index space, with a halo plan per rank.
+struct DVec {
+  Part part;
+  int64_t N = 0;
+  struct Rank {
+    int64_t own = 0, lo = 0, nhalo = 0;
+    DBuf<int32_t> halo;              // sorted global indices of the halo
+    std::vector<int64_t> halo_host;  // same, host copy (plan building)
+    DBuf<double> buf;                // [own | halo]
+    // emulation: owner rank and owner-local index per halo entry
+    DBuf<int32_t> src_rank, src_idx;
+    // nccl: per-peer receive segments and send lists
+    std::vector<int64_t> recv_off, recv_cnt, send_off, send_cnt;
+    DBuf<int32_t> send_idx;
+    DBuf<double> send_buf;
+  };
+  std::vector<Rank> rk;
+  DBuf<double*> bases;  // emulation: buf pointer per rank
+};
+
+struct DLevel {
+  Part fine, coarse_part, fpart;  // partitions of level l rows, level l+1 rows, F points
+  int active = 1;
+  double ratio_before = 0.0, ratio_after = 0.0;
+  bool triggered = false;
+  DVec B, X, RF;  // b_l (input of R_l), x_l (input of AF/AFFg and of P_{l-1}), r_F
+  struct Rank {
+    Csr R, AF, AFFG, FINV;    // local rows, remapped columns
+    DBuf<int32_t> pmap, f2f;  // prolongation map (-> X_{l+1} layout), F row -> local fine row
+    DBuf<double> sc;
+    int64_t nf_own = 0, n_own = 0;
+  };
+  std::vector<Rank> rk;
+};
+
+struct DHier {
+  int P = 1;
+  int me = -1;  // -1: emulate all ranks in this process
+  ncclComm_t comm = nullptr;
+  double threshold = 2.0;
+  std::vector<DLevel> lv;
+  Part cpart;            // coarsest rows (gathered on rank 0)
+  DVec CB, CX, CR, XS;   // coarse b / e / r and the top solution vector
+  struct Rank {
+    Csr A0, AC, ACI;     // top operator (residual), coarse operator and its inverse
+    DBuf<double> rhs;    // owned part of b
+  };
+  std::vector<Rank> rk;
+  DBuf<double> part;     // residual partial sums (all local ranks)
+  DBuf<double> scal;
+  std::vector<int> part_off;  // per local rank offset into part
+  int nparts = 0;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_key = -1;
+  uint64_t graph_kernels = 0;
+  int64_t top_n = 0;
+  ~DHier() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
+  bool mine(int r) const { return me < 0 || me == r; }
+};
+
+void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double threshold,
+                 const int64_t* level0_starts, DHier& d);
+// d_b / d_x: global vectors in emulation mode, this rank's slab with NCCL
+void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
+                airg_solve_stats& st, std::vector<double>& history);
+
+// Host-side halo plan of one rank (same rule as the device build): the
+// sorted distinct referenced indices outside the owned range, with the
+// per-owner receive counts. Used by the CPU (gloo) tests of the N > 1 path.
+void halo_plan_host(const std::vector<int64_t>& starts, int rank, const int64_t* cols,
+                    int64_t ncols, std::vector<int64_t>& halo, std::vector<int64_t>& recv_cnt);
+
+}  // namespace airg

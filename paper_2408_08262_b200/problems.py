@@ -110,10 +110,14 @@ def c0_structured_2d(nx: int = 128, angle: float = 0.3, sigma_t: float = 0.0,
     return _structured(nx, (ox, oy), h, np.full(nx * nx, sigma_t), seed, "C0", dims=2)
 
 
-def c2_structured_3d(nx: int = 128, seed: int = 0) -> Problem:
+def c2_structured_3d(nx: int = 128, seed: int = 0, nz_slabs: int = 1) -> Problem:
     """BASELINE config 2: 3D structured 7-point upwind, 128^3 cells, seed-random
     unit Omega, sigma_t piecewise constant over 8 random boxes in [0, 1e-2]
-    (the cube split by one random plane per axis, positions U[0.25, 0.75])."""
+    (the cube split by one random plane per axis, positions U[0.25, 0.75]).
+    nz_slabs > 1 stacks that many nx^3 cubes along z (nx x nx x nz_slabs*nx
+    cells, h = 1/nx): the weak-scaling family, one z-slab per GPU."""
+    if nz_slabs > 1:
+        return _c2_stacked(nx, seed, nz_slabs)
     s_om = stream(seed, TAG_OMEGA)
     g = np.array([_normal(s_om, k) for k in range(3)])
     om = g / np.linalg.norm(g)
@@ -129,6 +133,40 @@ def c2_structured_3d(nx: int = 128, seed: int = 0) -> Problem:
     p = _structured(nx, tuple(om), h, sig_box[box], seed, "C2", dims=3)
     p.meta.update(omega=om.tolist(), cuts=cuts.tolist(), sigma_boxes=sig_box.tolist())
     return p
+
+
+def _c2_stacked(nx: int, seed: int, slabs: int) -> Problem:
+    """C2 operator on nx x nx x (slabs*nx) cells: the same Omega and box
+    cross sections repeated per stacked cube (weak scaling in z)."""
+    s_om = stream(seed, TAG_OMEGA)
+    g = np.array([_normal(s_om, k) for k in range(3)])
+    om = g / np.linalg.norm(g)
+    s_box = stream(seed, TAG_BOXES)
+    cuts = 0.25 + 0.5 * uniform01(s_box, np.arange(3, dtype=np.uint64))
+    sig_box = 1e-2 * uniform01(stream(seed, TAG_SIGMA), np.arange(8, dtype=np.uint64))
+    h = 1.0 / nx
+    c = (np.arange(nx) + 0.5) * h
+    bx = (c >= cuts[0]).astype(np.int64)
+    by = (c >= cuts[1]).astype(np.int64)
+    bz = np.tile((c >= cuts[2]).astype(np.int64), slabs)
+    box = (bz[:, None, None] * 4 + by[None, :, None] * 2 + bx[None, None, :]).ravel()
+    nz = slabs * nx
+    n = nx * nx * nz
+    idx = np.arange(n, dtype=np.int64)
+    coord = [idx % nx, (idx // nx) % nx, idx // (nx * nx)]
+    dims_n = [nx, nx, nz]
+    strides = [1, nx, nx * nx]
+    rows, cols, vals = [idx], [idx], [sum(abs(o) for o in om) / h + sig_box[box]]
+    for d in range(3):
+        step = -1 if om[d] > 0 else 1
+        ok = (coord[d] + step >= 0) & (coord[d] + step < dims_n[d])
+        r = idx[ok]
+        rows.append(r)
+        cols.append(r + step * strides[d])
+        vals.append(np.full(r.size, -abs(om[d]) / h))
+    ro, co, va = _csr_from_coo(n, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
+    return Problem("C2x%d" % slabs, n, ro, co, va, _rhs(n, seed),
+                   dict(nx=nx, nz=nz, slabs=slabs, omega=om.tolist(), h=h))
 
 
 def _normal(seed, index: int) -> float:
