@@ -302,6 +302,19 @@ int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
                          int32_t* triggered, int64_t* halo_entries,
                          int64_t* h_starts /* P+1, nullable */);
 int airg_dist_destroy(airg_dist* d);
+/* The PMISR-DDC CF split (air.cpp:466-494) of a slab-partitioned operator:
+ * strength on own rows, |S^T| by a reverse halo sum, global-row-index
+ * weights, one forward halo exchange of weights, "not minimal" marks of
+ * remote endpoints returned to their owners, DDC with a global max and
+ * 1000-bin histogram (allreduce). Labels are bit-identical to airg_cf_split
+ * for every partition. rank = -1 emulates all ranks (d_labels global);
+ * rank >= 0 needs a communicator (d_labels = this rank's slab). */
+int airg_dist_cf_split(airg_ctx* ctx, const airg_csr* a, int32_t nranks,
+                       int32_t rank, void* nccl_comm, const int64_t* h_starts,
+                       double alpha, int64_t max_loops, uint64_t seed,
+                       int32_t ddc_enabled, double ddc_fraction,
+                       int64_t ddc_bins, uint8_t* d_labels,
+                       airg_cf_report* report);
 /* Host-only halo plan of one rank (the rule the device build applies):
  * sorted distinct referenced indices outside [starts[rank], starts[rank+1]),
  * plus the per-owner receive counts. No GPU needed (CPU / gloo tests). */

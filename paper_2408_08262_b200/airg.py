@@ -105,6 +105,9 @@ def lib() -> C.CDLL:
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
                                       _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
             "airg_dist_destroy": ([_VP], C.c_int),
+            "airg_dist_cf_split": ([_VP, _VP, C.c_int32, C.c_int32, _VP, _VP, C.c_double, C.c_int64,
+                                    C.c_uint64, C.c_int32, C.c_double, C.c_int64, _VP,
+                                    _P(abi.CfReport)], C.c_int),
             "airg_dist_plan_host": ([C.c_int32, _VP, C.c_int32, _VP, C.c_int64, _VP, C.c_int64,
                                      _P(C.c_int64), _VP], C.c_int),
         }
@@ -646,6 +649,40 @@ class NcclComm:
             except Exception:
                 pass
             self.h = None
+
+
+def dist_cf_split_device(d: DeviceCSR, starts, rank: int = -1, comm: NcclComm | None = None, alpha=0.5,
+                         max_loops=3, seed=0, ddc_enabled=True, ddc_fraction=0.1, ddc_bins=1000,
+                         labels=None, ctx: Context | None = None):
+    """Row-slab PMISR-DDC split (airg_dist_cf_split). rank = -1 emulates every
+    slab in this process and returns global labels; rank >= 0 (with a
+    communicator) returns this rank's slab. ``d`` is the global operator."""
+    ctx = ctx or d.ctx
+    s = np.ascontiguousarray(starts, np.int64)
+    P = len(s) - 1
+    n = d.dims()[0]
+    cnt = n if rank < 0 else int(s[rank + 1] - s[rank])
+    tl = labels if labels is not None else ctx.empty(max(cnt, 1), ctx.torch.uint8)
+    rep = abi.CfReport()
+    _check(lib().airg_dist_cf_split(ctx.h, d.h, P, int(rank), comm.h if comm else None, s.ctypes.data,
+                                    float(alpha), int(max_loops), int(seed) & (2**64 - 1), int(ddc_enabled),
+                                    float(ddc_fraction), int(ddc_bins), _ptr(tl), C.byref(rep)))
+    r = CfReport(rep.n_f_pre, rep.n_f, rep.n_c, rep.n_converted, rep.max_theta, rep.alpha_diag, rep.s_nnz)
+    return tl, r
+
+
+def dist_cf_split(a, nranks: int, starts=None, alpha=0.5, max_loops=3, seed=0, ddc_enabled=True,
+                  ddc_fraction=0.1, ddc_bins=1000, ctx: Context | None = None):
+    """Emulated row-slab split of a host matrix -> (labels, report); equal
+    slabs unless ``starts`` is given."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    n = d.dims()[0]
+    if starts is None:
+        starts = [n * r // nranks for r in range(nranks + 1)]
+    tl, r = dist_cf_split_device(d, starts, -1, None, alpha, max_loops, seed, ddc_enabled, ddc_fraction,
+                                 ddc_bins, ctx=ctx)
+    return ctx.to_host(tl)[:n], r
 
 
 class Dist:

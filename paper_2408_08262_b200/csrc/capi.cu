@@ -709,6 +709,35 @@ int airg_dist_level_info(const airg_dist* dp, int64_t l, int32_t* active, double
   });
 }
 
+int airg_dist_cf_split(airg_ctx* ctx, const airg_csr* a, int32_t nranks, int32_t rank, void* comm,
+                       const int64_t* starts, double alpha, int64_t max_loops, uint64_t seed,
+                       int32_t ddc_enabled, double fraction, int64_t bins, uint8_t* labels,
+                       airg_cf_report* rep) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(starts, "starts");
+    need(labels, "labels");
+    bind(ctx->c);
+    if (nranks < 1 || rank >= nranks) throw InvalidArgument("dist: rank out of range");
+    if (rank >= 0 && nranks > 1 && !comm) throw InvalidArgument("dist: a communicator is needed per rank");
+    CfReport r;
+    dist_cf_split(ctx->c, a->m, nranks, rank, (ncclComm_t)comm,
+                  std::vector<int64_t>(starts, starts + nranks + 1), alpha, max_loops, seed,
+                  ddc_enabled != 0, fraction, bins, labels, r);
+    if (rep) {
+      std::memset(rep, 0, sizeof *rep);
+      rep->n_f_pre = r.n_f_pre;
+      rep->n_f = r.n_f;
+      rep->n_c = a->m.n - r.n_f;
+      rep->n_converted = r.n_converted;
+      rep->max_theta = r.max_theta;
+      rep->alpha_diag = r.alpha_diag;
+      rep->s_nnz = r.s_nnz;
+    }
+  });
+}
+
 int airg_dist_destroy(airg_dist* d) {
   return guard([&] {
     if (!d) return;

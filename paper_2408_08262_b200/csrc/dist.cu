@@ -463,7 +463,387 @@ void exchange(Ctx& c, DHier& d, DVec& V) {
   NCCL_CHECK(ncclGroupEnd());
 }
 
+// ---- distributed CF split kernels (local column indices into [own | halo]) ----
+__device__ __forceinline__ uint64_t dsplitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ int64_t gidx(int32_t lc, int64_t lo, int64_t own, const int32_t* halo) {
+  return lc < own ? lo + lc : (int64_t)halo[lc - own];
+}
+// coarsening.cpp:83-105 on own rows; |S^T| contributions into stb ([own|halo])
+__global__ void k_dstrength(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, double alpha, int32_t* __restrict__ s_cnt,
+                            double* __restrict__ stb, const int32_t* __restrict__ srp,
+                            int32_t* __restrict__ sci) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double off_max = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k)
+    if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
+  const double thr = __dmul_rn(alpha, off_max);
+  int cnt = 0;
+  int o = srp ? srp[i] : 0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const double mag = fabs(v[k]);
+    if (ci[k] != i && mag > 0.0 && mag >= thr) {
+      ++cnt;
+      if (sci)
+        sci[o++] = ci[k];
+      else
+        atomicAdd(stb + ci[k], 1.0);
+    }
+  }
+  if (!sci) s_cnt[i] = cnt;
+}
+__global__ void k_dweights(int n, int64_t lo, const int32_t* __restrict__ s_cnt, const double* __restrict__ stb,
+                           uint64_t key, double* __restrict__ w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t deg = (int64_t)s_cnt[i] + (int64_t)stb[i];
+  const double u = (double)(dsplitmix(key ^ dsplitmix((uint64_t)(lo + i))) >> 11) * 0x1.0p-53;
+  w[i] = __dadd_rn((double)deg, u);
+}
+__global__ void k_dnotmin(int n, int64_t lo, int64_t own, const int32_t* __restrict__ halo,
+                          const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
+                          const double* __restrict__ w, double* __restrict__ nm) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double wi = w[i];
+  const int64_t gi = lo + i;
+  for (int k = srp[i]; k < srp[i + 1]; ++k) {
+    const int32_t lc = sci[k];
+    const double wj = w[lc];
+    const int64_t gj = gidx(lc, lo, own, halo);
+    const bool j_less = wj != wi ? wj < wi : gj < gi;  // weight_less(j, i)
+    nm[j_less ? i : lc] = 1.0;
+  }
+}
+__global__ void k_dlabels(int n, const double* __restrict__ w, const double* __restrict__ nm,
+                          double* __restrict__ lab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) lab[i] = (w[i] < 1.0 || nm[i] == 0.0) ? (double)AIRG_F : (double)AIRG_C;
+}
+// theta over own F rows, F columns in order (coarsening.cpp:219-250)
+__global__ void k_dtheta(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                         const double* __restrict__ v, const double* __restrict__ lab,
+                         const int32_t* __restrict__ fsub, double* __restrict__ theta,
+                         unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || lab[i] != (double)AIRG_F) return;
+  double off = 0.0, diag = 0.0;
+  bool seen = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const int32_t lc = ci[k];
+    if (lab[lc] != (double)AIRG_F) continue;
+    if (lc == i) {
+      diag = fabs(v[k]);
+      seen = true;
+    } else {
+      off = __dadd_rn(off, fabs(v[k]));
+    }
+  }
+  if (!seen || diag == 0.0) {
+    atomicMin(bad, (unsigned long long)fsub[i]);
+    theta[i] = 0.0;
+    return;
+  }
+  const double t = __ddiv_rn(off, diag);
+  theta[i] = t;
+  atomicMax(maxbits, (unsigned long long)__double_as_longlong(t));
+}
+__global__ void k_dfsub(int n, const double* __restrict__ lab, const int32_t* __restrict__ pos,
+                        int64_t base, int32_t* __restrict__ fsub) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) fsub[i] = (int32_t)(base + pos[i]);
+}
+__global__ void k_isf(int n, const double* __restrict__ lab, int32_t* __restrict__ f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = lab[i] == (double)AIRG_F;
+}
+__global__ void k_dhist(int n, const double* __restrict__ lab, const double* __restrict__ theta, double width,
+                        int64_t bins, double* __restrict__ hist) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || lab[i] != (double)AIRG_F) return;
+  int64_t b = (int64_t)__ddiv_rn(theta[i], width);
+  if (b > bins - 1) b = bins - 1;
+  atomicAdd(hist + b, 1.0);
+}
+__global__ void k_dconvert(int n, const double* __restrict__ theta, double alpha_diag,
+                           double* __restrict__ lab, unsigned long long* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || lab[i] != (double)AIRG_F) return;
+  const double t = theta[i];
+  if (t > alpha_diag && t != 0.0) {
+    lab[i] = (double)AIRG_C;
+    atomicAdd(count, 1ull);
+  }
+}
+__global__ void k_to_u8(int64_t n, const double* __restrict__ lab, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint8_t)lab[i];
+}
+__global__ void k_scatter_add(int64_t nh, const int32_t* __restrict__ src_rank,
+                              const int32_t* __restrict__ src_idx, double* const* __restrict__ bases,
+                              const double* __restrict__ halo_vals) {
+  const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < nh) atomicAdd(&bases[src_rank[h]][src_idx[h]], halo_vals[h]);
+}
+__global__ void k_unpack_add(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                             double* __restrict__ dst) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) atomicAdd(&dst[idx[k]], src[k]);
+}
+
+// reverse exchange: every halo entry is added into its owner's slot
+void reverse_add(Ctx& c, DHier& d, DVec& V) {
+  const int P = V.part.P();
+  if (d.me < 0) {
+    for (int r = 0; r < P; ++r) {
+      DVec::Rank& R = V.rk[r];
+      if (R.nhalo)
+        LAUNCH(c, k_scatter_add, blocks_for(R.nhalo, 256), 256, 0, R.nhalo, R.src_rank.p, R.src_idx.p,
+               (double* const*)V.bases.p, (const double*)(R.buf.p + R.own));
+    }
+    return;
+  }
+  DVec::Rank& M = V.rk[d.me];
+  NCCL_CHECK(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == d.me) continue;
+    if (M.recv_cnt[q])
+      NCCL_CHECK(ncclSend(M.buf.p + M.own + M.recv_off[q], (size_t)M.recv_cnt[q], ncclDouble, q, d.comm,
+                          c.stream));
+    if (M.send_cnt[q])
+      NCCL_CHECK(ncclRecv(M.send_buf.p + M.send_off[q], (size_t)M.send_cnt[q], ncclDouble, q, d.comm,
+                          c.stream));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  const int64_t ns = M.send_off[P - 1] + M.send_cnt[P - 1];
+  if (ns) LAUNCH(c, k_unpack_add, blocks_for(ns, 256), 256, 0, ns, M.send_idx.p, M.send_buf.p, M.buf.p);
+}
+
+// sum (or max) of a few host doubles over ranks
+void host_allreduce(Ctx& c, DHier& d, std::vector<double>& v, ncclRedOp_t op) {
+  if (d.me < 0 || d.P == 1 || v.empty()) return;
+  DBuf<double> t(c, v.size());
+  to_device(c, t.p, v.data(), v.size());
+  NCCL_CHECK(ncclAllReduce(t.p, t.p, v.size(), ncclDouble, op, d.comm, c.stream));
+  to_host(c, v.data(), t.p, v.size());
+}
+
 }  // namespace
+
+void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const std::vector<int64_t>& starts,
+                   double alpha, int64_t max_loops, uint64_t seed, bool ddc_enabled, double fraction,
+                   int64_t bins, uint8_t* d_labels, CfReport& rep) {
+  if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
+  if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
+  if ((int)starts.size() != P + 1 || starts[0] != 0 || starts[P] != a.n)
+    throw InvalidArgument("dist: slab starts must cover the matrix");
+  if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0)) throw InvalidArgument("ddc: fraction must be in (0, 1]");
+  DHier d;
+  d.P = P;
+  d.me = me;
+  d.comm = comm;
+  DVec V;  // [own | halo] payloads: |S^T| counts, weights, marks, labels
+  V.part.s = starts;
+  V.N = a.n;
+  V.rk.resize(P);
+  std::vector<Csr> loc(P);
+  for (int r = 0; r < P; ++r) {
+    slice(c, a, V.part.lo(r), V.part.lo(r) + V.part.cnt(r), loc[r]);
+    Marks mk;
+    mk.init(c, a.n);
+    mk.cols(c, loc[r], V.part.lo(r), V.part.lo(r) + V.part.cnt(r));
+    set_halo(c, V, r, mk);
+  }
+  finalize(c, V, d);
+  struct RS {
+    DBuf<int32_t> s_cnt, srp, sci, fsub;
+    DBuf<double> w, nm, lab, theta;
+    int64_t s_nnz = 0;
+  };
+  std::vector<RS> rs(P);
+  auto mine = [&](auto&& f) {
+    for (int r = 0; r < P; ++r)
+      if (d.mine(r)) f(r);
+  };
+  const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
+  // 1. strength, |S^T| by reverse sum
+  mine([&](int r) {
+    DVec::Rank& R = V.rk[r];
+    remap(c, loc[r], V, r);
+    R.buf.zero(c);
+    const int n = (int)R.own;
+    rs[r].s_cnt.alloc(c, (size_t)std::max(1, n));
+    if (n)
+      LAUNCH(c, k_dstrength, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, alpha,
+             rs[r].s_cnt.p, R.buf.p, (const int32_t*)nullptr, (int32_t*)nullptr);
+  });
+  reverse_add(c, d, V);
+  mine([&](int r) {
+    DVec::Rank& R = V.rk[r];
+    const int n = (int)R.own;
+    rs[r].srp.alloc(c, (size_t)n + 1);
+    rs[r].s_nnz = exclusive_scan(c, rs[r].s_cnt.p, rs[r].srp.p, n);
+    rs[r].sci.alloc(c, (size_t)std::max<int64_t>(1, rs[r].s_nnz));
+    if (n)
+      LAUNCH(c, k_dstrength, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, alpha,
+             rs[r].s_cnt.p, R.buf.p, rs[r].srp.p, rs[r].sci.p);
+    // 2. weights into the own part, then the halo weights
+    rs[r].w.alloc(c, (size_t)std::max<int64_t>(1, R.own + R.nhalo));
+    if (n) LAUNCH(c, k_dweights, blocks_for(n, 256), 256, 0, n, R.lo, rs[r].s_cnt.p, R.buf.p, key, rs[r].w.p);
+  });
+  // forward exchange of weights through V's buffers
+  mine([&](int r) {
+    if (V.rk[r].own)
+      CUDA_CHECK(cudaMemcpyAsync(V.rk[r].buf.p, rs[r].w.p, sizeof(double) * V.rk[r].own,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+  });
+  exchange(c, d, V);
+  // 3. "not minimal" marks, returned to the owners
+  mine([&](int r) {
+    DVec::Rank& R = V.rk[r];
+    const int64_t tot = R.own + R.nhalo;
+    if (tot) CUDA_CHECK(cudaMemcpyAsync(rs[r].w.p, R.buf.p, sizeof(double) * tot, cudaMemcpyDeviceToDevice, c.stream));
+    R.buf.zero(c);
+    const int n = (int)R.own;
+    if (n)
+      LAUNCH(c, k_dnotmin, blocks_for(n, 256), 256, 0, n, R.lo, R.own, R.halo.p, rs[r].srp.p, rs[r].sci.p,
+             rs[r].w.p, R.buf.p);
+  });
+  reverse_add(c, d, V);
+  // 4. PMISR labels on own rows, then the halo labels
+  std::vector<double> cnts(P, 0.0);
+  mine([&](int r) {
+    DVec::Rank& R = V.rk[r];
+    const int n = (int)R.own;
+    rs[r].lab.alloc(c, (size_t)std::max<int64_t>(1, R.own + R.nhalo));
+    if (n) LAUNCH(c, k_dlabels, blocks_for(n, 256), 256, 0, n, rs[r].w.p, R.buf.p, rs[r].lab.p);
+    if (n) CUDA_CHECK(cudaMemcpyAsync(R.buf.p, rs[r].lab.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  });
+  exchange(c, d, V);
+  double s_nnz = 0.0;
+  mine([&](int r) {
+    DVec::Rank& R = V.rk[r];
+    const int64_t tot = R.own + R.nhalo;
+    if (tot) CUDA_CHECK(cudaMemcpyAsync(rs[r].lab.p, R.buf.p, sizeof(double) * tot, cudaMemcpyDeviceToDevice, c.stream));
+    const int n = (int)R.own;
+    DBuf<int32_t> f(c, (size_t)std::max(1, n)), pos(c, (size_t)n + 1);
+    if (n) LAUNCH(c, k_isf, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, f.p);
+    cnts[r] = (double)exclusive_scan(c, f.p, pos.p, n);
+    rs[r].fsub.alloc(c, (size_t)std::max(1, n));
+    s_nnz += (double)rs[r].s_nnz;
+  });
+  // global F numbering (for the zero-diagonal row index) and totals
+  std::vector<double> allc(P, 0.0);
+  if (me < 0) {
+    allc = cnts;
+  } else {
+    allc[me] = cnts[me];
+    host_allreduce(c, d, allc, ncclSum);
+  }
+  std::vector<double> tot1{s_nnz};
+  host_allreduce(c, d, tot1, ncclSum);
+  int64_t nf_pre = 0;
+  std::vector<int64_t> fbase(P, 0);
+  for (int r = 0; r < P; ++r) {
+    fbase[r] = nf_pre;
+    nf_pre += (int64_t)allc[r];
+  }
+  rep = CfReport();
+  rep.n_f_pre = nf_pre;
+  rep.s_nnz = (int64_t)tot1[0];
+  if (ddc_enabled && nf_pre > 0) {
+    // 5. DDC with global max / histogram
+    DBuf<unsigned long long> u(c, 3);
+    std::vector<double> stats(2 * P, 0.0);  // per rank: max theta, bad row (as double, -1 none)
+    mine([&](int r) {
+      DVec::Rank& R = V.rk[r];
+      const int n = (int)R.own;
+      DBuf<int32_t> f(c, (size_t)std::max(1, n)), pos(c, (size_t)n + 1);
+      if (n) LAUNCH(c, k_isf, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, f.p);
+      exclusive_scan(c, f.p, pos.p, n);
+      if (n) LAUNCH(c, k_dfsub, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, pos.p, fbase[r], rs[r].fsub.p);
+      rs[r].theta.alloc(c, (size_t)std::max(1, n));
+      const unsigned long long init[3] = {0ull, ~0ull, 0ull};
+      to_device(c, u.p, init, 3);
+      if (n)
+        LAUNCH(c, k_dtheta, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, rs[r].lab.p,
+               rs[r].fsub.p, rs[r].theta.p, u.p, u.p + 1);
+      unsigned long long hu[3];
+      to_host(c, hu, u.p, 3);
+      double mx;
+      std::memcpy(&mx, &hu[0], sizeof mx);
+      stats[r] = mx;
+      stats[P + r] = hu[1] == ~0ull ? -1.0 : (double)hu[1];
+    });
+    double max_theta = 0.0;
+    int64_t bad = -1;
+    if (me >= 0) {
+      std::vector<double> m1{stats[me]};
+      host_allreduce(c, d, m1, ncclMax);
+      max_theta = m1[0];
+      std::vector<double> b1{stats[P + me] < 0 ? 1e300 : stats[P + me]};
+      host_allreduce(c, d, b1, ncclMin);
+      bad = b1[0] >= 1e300 ? -1 : (int64_t)b1[0];
+    } else {
+      for (int r = 0; r < P; ++r) {
+        max_theta = std::max(max_theta, stats[r]);
+        if (stats[P + r] >= 0 && (bad < 0 || (int64_t)stats[P + r] < bad)) bad = (int64_t)stats[P + r];
+      }
+    }
+    if (bad >= 0) throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(bad));
+    const double width = max_theta > 0.0 ? max_theta / (double)bins : 1.0;
+    std::vector<double> hist((size_t)bins, 0.0);
+    mine([&](int r) {
+      DBuf<double> hd(c, (size_t)bins);
+      hd.zero(c);
+      const int n = (int)V.rk[r].own;
+      if (n) LAUNCH(c, k_dhist, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, rs[r].theta.p, width, bins, hd.p);
+      std::vector<double> hh((size_t)bins);
+      to_host(c, hh.data(), hd.p, hh.size());
+      for (int64_t b = 0; b < bins; ++b) hist[b] += hh[b];
+    });
+    host_allreduce(c, d, hist, ncclSum);
+    // coarsening.cpp:290-315, identical arithmetic on every rank
+    double alpha_diag = 0.0;
+    if (max_theta != 0.0) {
+      const double target = fraction * (double)nf_pre;
+      int64_t above = 0, best_k = bins;
+      double best_err = std::fabs((double)above - target);
+      for (int64_t k = bins; k-- > 0;) {
+        above += (int64_t)hist[k];
+        const double err = std::fabs((double)above - target);
+        if (err < best_err) {
+          best_err = err;
+          best_k = k;
+        }
+      }
+      alpha_diag = (double)best_k * (max_theta / (double)bins);
+    }
+    std::vector<double> conv(1, 0.0);
+    mine([&](int r) {
+      const int n = (int)V.rk[r].own;
+      CUDA_CHECK(cudaMemsetAsync(u.p + 2, 0, sizeof(unsigned long long), c.stream));
+      if (n) LAUNCH(c, k_dconvert, blocks_for(n, 256), 256, 0, n, rs[r].theta.p, alpha_diag, rs[r].lab.p, u.p + 2);
+      conv[0] += (double)read1(c, u.p + 2);
+    });
+    host_allreduce(c, d, conv, ncclSum);
+    rep.max_theta = max_theta;
+    rep.alpha_diag = alpha_diag;
+    rep.n_converted = (int64_t)conv[0];
+  }
+  rep.n_f = rep.n_f_pre - rep.n_converted;
+  mine([&](int r) {
+    const int64_t n = V.rk[r].own, lo = me < 0 ? V.rk[r].lo : 0;
+    if (n) LAUNCH(c, k_to_u8, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, d_labels + lo);
+  });
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
 
 // ---------------------------------------------------------------------------
 void halo_plan_host(const std::vector<int64_t>& starts, int rank, const int64_t* cols, int64_t ncols,

@@ -104,6 +104,22 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
 void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
                 airg_solve_stats& st, std::vector<double>& history);
 
+// Distributed PMISR-DDC CF split of a slab-partitioned operator (the paper's
+// contribution at N GPUs): strength on own rows, |S^T| by a reverse halo sum,
+// weights on the global row index, one forward exchange of halo weights, the
+// "not minimal" marks of remote endpoints returned by a reverse exchange, and
+// DDC with a global max / histogram (allreduce). Labels are bit-identical to
+// the one-GPU split for every partition. d_labels: global (emulation) or
+// this rank's slab (NCCL).
+struct CfReport {
+  int64_t n_f_pre = 0, n_f = 0, n_converted = 0, s_nnz = 0;
+  double max_theta = 0.0, alpha_diag = 0.0;
+};
+void dist_cf_split(Ctx& c, const Csr& a_global, int P, int me, ncclComm_t comm,
+                   const std::vector<int64_t>& starts, double alpha, int64_t max_loops, uint64_t seed,
+                   bool ddc_enabled, double fraction, int64_t bins, uint8_t* d_labels,
+                   CfReport& rep);
+
 // Host-side halo plan of one rank (same rule as the device build): the
 // sorted distinct referenced indices outside the owned range, with the
 // per-owner receive counts. Used by the CPU (gloo) tests of the N > 1 path.

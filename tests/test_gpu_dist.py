@@ -81,3 +81,50 @@ def test_dist_c2_reduced_with_zslabs():
     res = d.solve(p.b, coarse_iterations=3)
     assert same_bits(res.x, ref.x)
     assert d.level_info(0)["halo"] > 0
+
+
+def _split_cases():
+    out = []
+    for path in GOLDEN[:4]:
+        g = np.load(path)
+        prm = _params(g)
+        n = len(g["rp"]) - 1
+        out.append((os.path.basename(path)[:-4], airg.SparseMatrix.from_arrays(n, n, g["rp"], g["ci"], g["v"]),
+                    prm.get("strength_alpha", 0.5)))
+    p = problems.c2_structured_3d(32)
+    out.append(("c2_32", airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), 0.5))
+    return out
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("ddc", [True, False])
+def test_dist_cf_split_matches_single_gpu(P, ddc):
+    """Row-slab PMISR-DDC (halo weights, reverse-summed |S^T| and 'not
+    minimal' marks, allreduced DDC histogram) == the one-GPU split, bitwise."""
+    rng = np.random.default_rng(P)
+    for name, a, alpha in _split_cases():
+        n = a.nrows
+        for seed in (0, 7):
+            lab, _, rep = airg.cf_split(a, alpha, 3, seed, ddc_enabled=ddc)
+            if P > 1 and seed == 7:  # ragged slabs, some empty
+                cuts = np.sort(rng.integers(0, n + 1, P - 1))
+                starts = np.concatenate([[0], cuts, [n]])
+            else:
+                starts = None
+            dl, drep = airg.dist_cf_split(a, P, starts=starts, alpha=alpha, seed=seed, ddc_enabled=ddc)
+            assert np.array_equal(dl, lab), f"{name} P={P} seed={seed}: labels differ"
+            assert (drep.n_f_pre, drep.n_f, drep.n_converted, drep.s_nnz) == \
+                (rep.n_f_pre, rep.n_f, rep.n_converted, rep.s_nnz), name
+            assert same_bits(np.float64([drep.max_theta, drep.alpha_diag]),
+                             np.float64([rep.max_theta, rep.alpha_diag])), name
+
+
+def test_dist_cf_split_nccl_single_rank():
+    p = problems.c2_structured_3d(24)
+    a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
+    lab, _, _ = airg.cf_split(a, 0.5, 3, 3)
+    ctx = airg.default_context()
+    d = airg.DeviceCSR.upload(a, ctx)
+    comm = airg.NcclComm(1, 0, airg.nccl_unique_id())
+    tl, _ = airg.dist_cf_split_device(d, [0, p.n], rank=0, comm=comm, seed=3)
+    assert np.array_equal(ctx.to_host(tl)[: p.n], lab)
