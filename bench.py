@@ -45,6 +45,74 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback"
 
 
+def spmv_bytes(rows, cols, nnz):
+    """int32 column + fp64 value per nonzero, int32 row
+    pointer, x read once, y written once."""
+    return 12 * nnz + 4 * (rows + 1) + 8 * cols + 8 * rows
+
+
+def solve_alg_bytes(h, iterations, coarse_iterations, up_smooths=2):
+    """Algorithmic HBM bytes of one solve: every operator the V-cycle applies
+    is read once per application (12 B per nonzero + 4 B per row pointer) and
+    every vector it needs is read or written once (8 B per entry, 4 B per
+    index map entry). Per level (solve.cpp:93-146): R b; the first F-smooth's
+    residual over A's F rows (A_ff and A_fc entries: nnz_ff + nnz_fc) with x,
+    b_F, r_F and the kept A_fc x_C; Aff^-1 r_F with the x_F update (twice);
+    the second residual over A_ff; the one-point prolongation. Per Richardson
+    iteration the top residual r = b - A x with its norm and x += e; the
+    coarse grid's polynomial iterations. The reference's unfused operator
+    sequence (separate gathers, A_ff / A_fc SpMVs, vector temporaries) moves
+    more; that count is reported separately (reference_op_bytes)."""
+    info = h.info()
+    per_cycle = 0
+    for l in range(info.n_levels):
+        lv = h.level(l)
+        n, nf, nc = lv.n, lv.n_f, lv.n_c
+        r = 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc
+        fres1 = 12 * (lv.nnz_ff + lv.nnz_fc) + 4 * (nf + 1) + 8 * n + nf * (4 + 8 + 8 + 8)
+        fupd = 12 * lv.nnz_ffinv + 4 * (nf + 1) + 8 * nf + nf * (4 + 16)
+        fres2 = 12 * lv.nnz_ff + 4 * (nf + 1) + 8 * nf + nf * (4 + 8 + 8 + 8)
+        prol = n * (4 + 8) + 8 * nc
+        smooths = fres1 + fupd + (up_smooths - 1) * (fres2 + fupd)
+        per_cycle += r + prol + smooths
+    cn = info.coarse_n
+    for it in range(coarse_iterations):
+        per_cycle += 12 * info.coarse_inv_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+        if it:
+            per_cycle += 12 * info.coarse_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+    top = h.level(0) if info.n_levels else None
+    n0 = top.n if top else cn
+    nnz0 = top.nnz if top else info.coarse_nnz
+    resid = spmv_bytes(n0, n0, nnz0) + 8 * n0  # + b
+    per_iter = per_cycle + resid + 24 * n0
+    return iterations * per_iter + resid
+
+
+def reference_op_bytes(h, iterations, coarse_iterations, up_smooths=2):
+    """The same solve counted over the reference's unfused operations
+    (every SpMV and vector op solve.cpp:34-259 issues,
+    separately: x_F / x_C gathers, A_ff and A_fc SpMVs, b_F - . - ., scatter)."""
+    info = h.info()
+    per_cycle = 0
+    for l in range(info.n_levels):
+        lv = h.level(l)
+        n, nf, nc = lv.n, lv.n_f, lv.n_c
+        b = spmv_bytes(nc, n, lv.nnz_r) + spmv_bytes(n, nc, lv.nnz_p) + 24 * n
+        smooth = (16 * nf + 16 * nc + spmv_bytes(nf, nf, lv.nnz_ff) + spmv_bytes(nf, nc, lv.nnz_fc)
+                  + 16 * nf + 32 * nf + spmv_bytes(nf, nf, lv.nnz_ffinv) + 28 * nf)
+        per_cycle += b + up_smooths * smooth
+    cn = info.coarse_n
+    for it in range(coarse_iterations):
+        per_cycle += spmv_bytes(cn, cn, info.coarse_inv_nnz) + 24 * cn
+        if it:
+            per_cycle += spmv_bytes(cn, cn, info.coarse_nnz) + 24 * cn
+    top = h.level(0) if info.n_levels else None
+    n0 = top.n if top else cn
+    nnz0 = top.nnz if top else info.coarse_nnz
+    per_iter = per_cycle + spmv_bytes(n0, n0, nnz0) + 24 * n0 + 8 * n0 + 24 * n0
+    return iterations * per_iter + spmv_bytes(n0, n0, nnz0) + 32 * n0
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -403,33 +471,45 @@ def run_gpu(args):
     e2e_ms = sum(e2e_times) / len(e2e_times)
     e2e_value = p.n * ws / (e2e_ms / 1e3)
 
-    # ---- roofline of the dominant kernel: the level-0 CSR SpMV (y = A x) ----
-    # algorithmic bytes = 12 nnz + 4 (n+1) + 8 n (x) + 8 n (y)
+    # ---- roofline. The unit is the whole solve step ("per
+    # V-cycle and per solve: sum over every SpMV and vector op"), whose
+    # kernels replay as one captured graph per Richardson iteration; no single
+    # kernel owns more than ~30% of it (profiles/r1_solve_launches.txt). The
+    # level-0 SpMV (the reference's top hot spot, sparse.cpp:185-201) is
+    # reported beside it, timed alone.
+    step_bytes = solve_alg_bytes(h, int(st.iterations), prm["coarse_iterations"])
+    peak, peak_kind = hbm_peak()
+    step_achieved = step_bytes / (ms_per_step / 1e3) / 1e9
     A0 = h.matrix_handle(0, 0) if info.n_levels else dA
     n0, _, nnz0 = A0.dims()
-    alg_bytes = 12 * nnz0 + 4 * (n0 + 1) + 8 * n0 + 8 * n0
+    alg_bytes = spmv_bytes(n0, n0, nnz0)
     with torch.cuda.stream(stream):
         xv = torch.rand(n0, dtype=torch.float64, device=ctx.tdev)
         yv = torch.empty(n0, dtype=torch.float64, device=ctx.tdev)
-    reps = 50
-    for _ in range(5):
+    reps = 20
+    for _ in range(3):
         airg.spmv_device(A0, xv, yv, ctx=ctx)
-    k0, k1 = ev(), ev()
-    k0.record(stream)
-    for _ in range(reps):
+    kt = []
+    for _ in range(reps):  # L2 flushed before each launch: HBM-resident operands
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        k0, k1 = ev(), ev()
+        k0.record(stream)
         airg.spmv_device(A0, xv, yv, ctx=ctx)
-    k1.record(stream)
-    k1.synchronize()
-    kern_ms = k0.elapsed_time(k1) / reps
-    peak, peak_kind = hbm_peak()
+        k1.record(stream)
+        k1.synchronize()
+        kt.append(k0.elapsed_time(k1))
+    kern_ms = statistics.median(kt)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    traffic = None
-    tf = os.path.join(REPO, "profiles", "spmv_dram_bytes.json")
-    if os.path.exists(tf):
+    prof = {}
+    pf = os.path.join(REPO, "profiles", "dram_bytes.json")
+    if os.path.exists(pf):
         try:
-            traffic = json.load(open(tf)).get("bytes_per_launch")
+            prof = json.load(open(pf))
         except Exception:
-            traffic = None
+            prof = {}
+    step_traffic = prof.get("solve_dram_bytes_per_step")
+    spmv_traffic = prof.get("spmv_dram_bytes_per_launch")
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -446,10 +526,16 @@ def run_gpu(args):
         "iterations": int(st.iterations), "final_relative_residual": float(rel),
         "levels": int(info.n_levels), "operator_complexity": info.operator_complexity,
         "setup_ms": setup_ms, "cf_split_ms": cf_ms,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "spmv_rows (level-0 A, thread-per-row exact CSR SpMV)",
-                     "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_ms, "peak_kind": peak_kind},
+        "roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
+                     "frac": step_achieved / peak, "traffic": step_traffic,
+                     "kernel": "one AIRG solve step: the captured V-cycle graph of all row kernels, "
+                               "replayed once per Richardson iteration",
+                     "alg_bytes_per_step": step_bytes, "avg_step_ms": ms_per_step, "peak_kind": peak_kind,
+                     "reference_op_bytes_per_step": reference_op_bytes(h, int(st.iterations),
+                                                                       prm["coarse_iterations"]),
+                     "top_spmv": {"kernel": "rows_thread<EpiStore> on level-0 A (exact CSR SpMV, y = A x)",
+                                  "achieved": achieved, "frac": achieved / peak, "traffic": spmv_traffic,
+                                  "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_ms}},
         "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 8 * p.n,
                 "d2h_bytes_per_step": 8 * p.n, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),

@@ -194,7 +194,8 @@ struct Csr {
   DBuf<double> v;
   DBuf<int32_t> tiles;  // row starts of the warp tiles (tiled.cuh), built on demand
   int32_t ntiles = -1;
-  int8_t row_mode = 0;  // 0 unbuilt, 1 thread per row, 2 warp tiles
+  int8_t row_mode = 0;  // 0 unbuilt, 1 thread (group) per row, 2 warp tiles
+  int8_t group = 1;     // lanes per row in row_mode 1 (tiled.cuh rows_group)
   // SELL-32-sigma copy for the solve (sell.cuh), built on demand
   DBuf<int32_t> s_off, s_len, s_perm, s_ci;
   DBuf<double> s_v;

@@ -194,18 +194,52 @@ __global__ void map_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci,
 
 }  // namespace
 
-// Row-kernel decomposition for this matrix: thread per row for short rows,
-// warp tiles otherwise (tiled.cuh). AIRG_ROWS=thread|tiles forces one.
-// Default: thread per row (measured fastest on the C2 hierarchy, see
-// profiles/); AIRG_ROWS=auto picks warp tiles for long rows, =tiles forces them.
+// Row-kernel decomposition for this matrix (tiled.cuh):
+//   default (AIRG_ROWS unset or =thread): thread per row everywhere;
+//   AIRG_ROWS=group: G lanes per row, G from the mean row length
+//     (AIRG_GROUP=G forces G);
+//   AIRG_ROWS=tiles: warp tiles everywhere; =auto: warp tiles for long rows.
 static int rows_override() {
   static int v = [] {
     const char* e = getenv("AIRG_ROWS");
     if (!e || !strcmp(e, "thread")) return 1;
+    if (!strcmp(e, "group")) return 3;
     if (!strcmp(e, "tiles")) return 2;
     return 0;  // auto
   }();
   return v;
+}
+
+// Aligned 8-entry vector batches pay off on long rows (the A_F rows of the
+// Galerkin levels, ~25-30 entries); short rows keep the scalar loop.
+// AIRG_VEC=0|4|8 forces one choice for every matrix.
+int row_vec(int64_t n, int64_t nnz) {
+  static const int forced = [] {
+    const char* e = getenv("AIRG_VEC");
+    return e ? atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced == 4 || forced == 8 ? forced : 0;
+  return n > 0 && nnz >= 12 * n ? 8 : 0;
+}
+
+static int forced_group() {
+  static const int forced = [] {
+    const char* e = getenv("AIRG_GROUP");
+    const int g = e ? atoi(e) : 0;
+    return g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 ? g : 0;
+  }();
+  return forced;
+}
+
+// lanes per row for a matrix of n rows and nnz entries
+int row_group_for(int64_t n, int64_t nnz) {
+  const int forced = forced_group();
+  if (forced) return forced;
+  if (n <= 0) return 1;
+  const double mean = (double)nnz / (double)n;
+  int g = 1;
+  while (g < 16 && mean >= 4.0 * g * 2) g *= 2;  // about 4+ entries per lane
+  return g;
 }
 
 bool solve_layout_sell() {
@@ -219,6 +253,12 @@ bool solve_layout_sell() {
 void build_tiles(Ctx& c, Csr& a) {
   if (a.row_mode != 0) return;
   const int ov = rows_override();
+  if (ov == 3 || ov == 1 || forced_group()) {
+    a.row_mode = 1;
+    a.ntiles = 0;
+    a.group = (int8_t)(ov == 3 || forced_group() ? row_group_for(a.n, a.nnz) : 1);
+    return;
+  }
   const bool short_rows = ov ? ov == 1 : (a.n == 0 || a.nnz <= (int64_t)kShortRow * a.n);
   if (short_rows) {
     a.row_mode = 1;
@@ -326,7 +366,7 @@ void spmv(Ctx& c, const Csr& a, const double* x, double* y) {
     return;
   }
   build_tiles(c, m);
-  TileView tv{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n};
+  TileView tv{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz)};
   LAUNCH_ROWS(c, EpiStore, tv, x, EpiStore{y});
 }
 

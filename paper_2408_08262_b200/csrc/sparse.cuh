@@ -14,6 +14,8 @@ void with_full_diagonal(Ctx& c, const Csr& a, Csr& out);
 void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
 // tile starts for the tiled row kernels (tiled.cuh); idempotent
 void build_tiles(Ctx& c, Csr& a);
+// entries per aligned vector batch of the thread-per-row kernels (AIRG_VEC=0|4|8)
+int row_vec(int64_t n, int64_t nnz);
 // SELL-32-sigma solve copy (sell.cuh); idempotent
 void build_sell(Ctx& c, Csr& a);
 // solve layout switch: SELL only with AIRG_LAYOUT=sell (CSR rows by default)

@@ -31,9 +31,12 @@ struct TileView {
   const int32_t* rp;
   const int32_t* ci;
   const double* v;
-  const int32_t* tiles;  // nullptr => thread-per-row mode
+  const int32_t* tiles;  // nullptr => thread-per-row (group <= 1) or group-per-row mode
   int ntiles;
   int nrows;
+  int group = 1;         // lanes per row of the group kernels (1, 2, 4, 8, 16, 32)
+  int nnz = 0;           // > 0: thread-per-row kernels use aligned vector loads (rowdot.cuh)
+  int vec = 0;           // entries per vector batch (4 or 8), 0 = scalar loop
 };
 
 // ---- thread per row -----------------------------------------------------------
@@ -43,7 +46,17 @@ __global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const do
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m.nrows) epi.row(i, dot_ordered(__ldg(m.rp + i), __ldg(m.rp + i + 1), m.ci, m.v, x));
+  if (i < m.nrows) {
+    const int s = __ldg(m.rp + i), e = __ldg(m.rp + i + 1);
+    double acc;
+    if (m.vec == 8)
+      acc = dot_ordered_vec<8>(s, e, m.nnz, m.ci, m.v, x);
+    else if (m.vec == 4)
+      acc = dot_ordered_vec<4>(s, e, m.nnz, m.ci, m.v, x);
+    else
+      acc = dot_ordered(s, e, m.ci, m.v, x);
+    epi.row(i, acc);
+  }
   epi.finish();
 }
 
@@ -55,7 +68,13 @@ __global__ void __launch_bounds__(kTileThreads) rows_thread_fc(TileView m,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m.nrows) return;
   double sf, sc;
-  dot_ordered_fc(__ldg(m.rp + i), __ldg(m.rp + i + 1), m.ci, m.v, x, sf, sc);
+  const int s = __ldg(m.rp + i), e = __ldg(m.rp + i + 1);
+  if (m.vec == 8)
+    dot_ordered_fc_vec<8>(s, e, m.nnz, m.ci, m.v, x, sf, sc);
+  else if (m.vec == 4)
+    dot_ordered_fc_vec<4>(s, e, m.nnz, m.ci, m.v, x, sf, sc);
+  else
+    dot_ordered_fc(s, e, m.ci, m.v, x, sf, sc);
   epi.row2(i, sf, sc);
 }
 
@@ -142,21 +161,110 @@ __global__ void __launch_bounds__(kTileThreads) rows_warp_tiles_fc(TileView m,
   }
 }
 
+// ---- lane groups: G lanes per row ------------------------------------------------
+// The G lanes of a row load G consecutive (column, value) pairs at a time
+// (unit stride across the group), gather x and form the products -- each
+// rounded exactly as the reference rounds it -- and lane 0 of the group adds
+// them in column order from the group's registers (G shuffles). Same bits as
+// thread per row; G times the memory parallelism per row, which is what the
+// long rows of the mid/coarse Galerkin levels need.
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  return G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+}
+
+template <int G, class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_group(TileView m, const double* __restrict__ x,
+                                                           Epi epi) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  const int lane = threadIdx.x & (G - 1);
+  if (r < m.nrows) {
+    const unsigned mask = group_mask<G>();
+    const int s = __ldg(m.rp + r), e = __ldg(m.rp + r + 1);
+    double acc = 0.0;
+    for (int k0 = s; k0 < e; k0 += 2 * G) {
+      const int ka = k0 + lane, kb = ka + G;
+      const int ca = ka < e ? __ldg(m.ci + ka) : 0, cb = kb < e ? __ldg(m.ci + kb) : 0;
+      const double va = ka < e ? __ldg(m.v + ka) : 0.0, vb = kb < e ? __ldg(m.v + kb) : 0.0;
+      const double pa = ka < e ? __dmul_rn(va, __ldg(x + ca)) : 0.0;
+      const double pb = kb < e ? __dmul_rn(vb, __ldg(x + cb)) : 0.0;
+      const int cnt = e - k0;
+      const int na = cnt < G ? cnt : G;
+      for (int j = 0; j < na; ++j) acc = __dadd_rn(acc, __shfl_sync(mask, pa, j, G));
+      const int nb = cnt - G < G ? cnt - G : G;
+      for (int j = 0; j < nb; ++j) acc = __dadd_rn(acc, __shfl_sync(mask, pb, j, G));
+    }
+    if (lane == 0) epi.row(r, acc);
+  }
+  epi.finish();
+}
+
+template <int G, class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_group_fc(TileView m, const double* __restrict__ x,
+                                                              Epi epi) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  const int lane = threadIdx.x & (G - 1);
+  if (r >= m.nrows) return;
+  const unsigned mask = group_mask<G>();
+  const int shift = (threadIdx.x & 31) & ~(G - 1);
+  const int s = __ldg(m.rp + r), e = __ldg(m.rp + r + 1);
+  double sf = 0.0, sc = 0.0;
+  for (int k0 = s; k0 < e; k0 += G) {
+    const int k = k0 + lane;
+    const int c = k < e ? __ldg(m.ci + k) : 0;
+    const double p = k < e ? __dmul_rn(__ldg(m.v + k), __ldg(x + (c & 0x7fffffff))) : 0.0;
+    const unsigned isc = __ballot_sync(mask, c < 0) >> shift;
+    const int cnt = e - k0 < G ? e - k0 : G;
+    for (int j = 0; j < cnt; ++j) {
+      const double q = __shfl_sync(mask, p, j, G);
+      if ((isc >> j) & 1u)
+        sc = __dadd_rn(sc, q);
+      else
+        sf = __dadd_rn(sf, q);
+    }
+  }
+  if (lane == 0) epi.row2(r, sf, sc);
+}
+
 // grid size for either mode
 inline unsigned rows_grid(const TileView& m) {
   if (m.tiles) return (unsigned)((m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock > 0
                                      ? (m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock
                                      : 1);
-  return (unsigned)((m.nrows + kTileThreads - 1) / kTileThreads > 0
-                        ? (m.nrows + kTileThreads - 1) / kTileThreads
-                        : 1);
+  const int64_t threads = (int64_t)m.nrows * (m.group > 1 ? m.group : 1);
+  const int64_t blocks = (threads + kTileThreads - 1) / kTileThreads;
+  return (unsigned)(blocks > 0 ? blocks : 1);
 }
+
+// dispatch a group kernel on the runtime lane count (G in {2,4,8,16,32}); the
+// kernel is bound to a pointer first so the template commas stay out of the
+// launch macros
+#define ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, G, Epi, view, x, epi)             \
+  case G: {                                                                     \
+    auto* kfn__ = &KERNEL<G, Epi>;                                              \
+    LAUNCHER(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);       \
+  } break;
+#define ROWS_GROUP_SWITCH(LAUNCHER, ctx, KERNEL, Epi, view, x, epi) \
+  switch ((view).group) {                                          \
+    ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, 2, Epi, view, x, epi)    \
+    ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, 4, Epi, view, x, epi)    \
+    ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, 8, Epi, view, x, epi)    \
+    ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, 16, Epi, view, x, epi)   \
+    default:                                                       \
+    ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, 32, Epi, view, x, epi)   \
+  }
 
 // Launch helpers (used inside LAUNCH-counted wrappers).
 #define LAUNCH_ROWS(ctx, Epi, view, x, epi)                                          \
   do {                                                                               \
     if ((view).tiles)                                                                \
       LAUNCH(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
+    else if ((view).group > 1)                                                              \
+      ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group, Epi, view, x, epi)                                  \
     else                                                                             \
       LAUNCH(ctx, rows_thread<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
   } while (0)
@@ -165,6 +273,8 @@ inline unsigned rows_grid(const TileView& m) {
   do {                                                                                          \
     if ((view).tiles)                                                                           \
       LAUNCH_PDL(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);    \
+    else if ((view).group > 1)                                                              \
+      ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
     else                                                                                        \
       LAUNCH_PDL(ctx, rows_thread<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);        \
   } while (0)
@@ -172,6 +282,8 @@ inline unsigned rows_grid(const TileView& m) {
   do {                                                                                          \
     if ((view).tiles)                                                                           \
       LAUNCH_PDL(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
+    else if ((view).group > 1)                                                              \
+      ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else                                                                                        \
       LAUNCH_PDL(ctx, rows_thread_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
   } while (0)
@@ -179,6 +291,8 @@ inline unsigned rows_grid(const TileView& m) {
   do {                                                                                  \
     if ((view).tiles)                                                                   \
       LAUNCH(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
+    else if ((view).group > 1)                                                              \
+      ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else                                                                                \
       LAUNCH(ctx, rows_thread_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
   } while (0)

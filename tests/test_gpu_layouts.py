@@ -1,0 +1,59 @@
+"""Every row-kernel decomposition gives the same bits (tiled.cuh): thread per
+row, G-lane groups (G = 2..32), warp tiles and SELL-32/G, selected by
+environment variables that are read once per process -- hence one
+subprocess per layout. Each prints the SHA-256 of the solution's bytes of a
+reduced C2 solve and of a level-0 SpMV."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+p = problems.c2_structured_3d(24)
+prm = dict(problems.setup_params(2), coarse_size_target=300)
+a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
+h = airg.setup(a, **prm)
+r = airg.richardson_solve(h, p.b, coarse_iterations=3)
+y = airg.spmv(h.matrix(1, 0), np.random.default_rng(0).random(h.level(1).n))
+print(r.stats.iterations, hashlib.sha256(r.x.tobytes()).hexdigest(), hashlib.sha256(y.tobytes()).hexdigest())
+""" % REPO
+
+LAYOUTS = {
+    "thread": {"AIRG_ROWS": "thread", "AIRG_VEC": "0"},
+    "vec4": {"AIRG_VEC": "4"},
+    "vec8": {"AIRG_VEC": "8"},
+    "group_auto": {"AIRG_ROWS": "group"},
+    "g2": {"AIRG_GROUP": "2"},
+    "g4": {"AIRG_GROUP": "4"},
+    "g8": {"AIRG_GROUP": "8"},
+    "g16": {"AIRG_GROUP": "16"},
+    "g32": {"AIRG_GROUP": "32"},
+    "tiles": {"AIRG_ROWS": "tiles"},
+    "sell": {"AIRG_LAYOUT": "sell"},
+    "nopdl": {"AIRG_PDL": "0"},
+}
+
+
+def _run(env_extra):
+    env = dict(os.environ)
+    for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC"):
+        env.pop(k, None)
+    env.update(env_extra)
+    out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return out.stdout.strip().split("\n")[-1]
+
+
+def test_all_layouts_bit_identical():
+    base = _run(LAYOUTS["thread"])
+    for name, env in LAYOUTS.items():
+        if name != "thread":
+            assert _run(env) == base, f"layout {name} differs from thread-per-row"
