@@ -40,6 +40,8 @@ struct Hier {
   // outer GMRES workspace (allocated on first use)
   int64_t gm_restart = 0;
   DBuf<double> V, Z, w, hbuf, ybuf;
+  // coarse-tail persistent kernel (tail.cuh): grid barrier words
+  DBuf<unsigned> tail_bar;
   // cached graphs
   cudaGraphExec_t g_rich = nullptr, g_vc = nullptr;
   int64_t g_key_rich = -1, g_key_vc = -1;

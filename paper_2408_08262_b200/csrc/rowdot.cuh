@@ -141,4 +141,77 @@ __device__ __forceinline__ void dot_ordered_fc_vec(int s, int e, int nnz, const 
   }
 }
 
+// ---- prefetching form (used by the PDL row kernels, tiled.cuh) -------------
+// The matrix is constant during a solve, so a row kernel may load its row
+// bounds and first batch of (column, value) pairs BEFORE griddepcontrol.wait
+// -- overlapping them with the tail of the kernel it depends on -- and only
+// the x gathers wait for the predecessor. VEC: batches start at the 16-byte
+// aligned group containing s and use vector loads (load_group).
+template <int VB, bool VEC>
+struct RowBatch {
+  int c[VB];
+  double a[VB];
+  __device__ __forceinline__ void load(int k0, int e, int nnz, const int32_t* __restrict__ ci,
+                                       const double* __restrict__ v) {
+    if (VEC) {
+      load_group<VB>(k0, nnz, ci, v, c, a);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VB; ++j) {
+        c[j] = k0 + j < e ? __ldg(ci + k0 + j) : 0;
+        a[j] = k0 + j < e ? __ldg(v + k0 + j) : 0.0;
+      }
+    }
+  }
+};
+
+template <int VB, bool VEC>
+__device__ __forceinline__ int batch_start(int s) {
+  return VEC ? (s & ~3) : s;
+}
+
+template <int VB, bool VEC>
+__device__ __forceinline__ double dot_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
+                                                 const double* __restrict__ v, const double* __restrict__ x,
+                                                 RowBatch<VB, VEC>& b) {
+  double acc = 0.0;
+  const int k00 = batch_start<VB, VEC>(s);
+  for (int k0 = k00; k0 < e; k0 += VB) {
+    if (k0 != k00) b.load(k0, e, nnz, ci, v);
+    double xv[VB];
+#pragma unroll
+    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + b.c[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < VB; ++j)
+      if (k0 + j >= s && k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(b.a[j], xv[j]));
+  }
+  return acc;
+}
+
+template <int VB, bool VEC>
+__device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
+                                                  const double* __restrict__ v, const double* __restrict__ x,
+                                                  RowBatch<VB, VEC>& b, double& sf, double& sc) {
+  sf = 0.0;
+  sc = 0.0;
+  const int k00 = batch_start<VB, VEC>(s);
+  for (int k0 = k00; k0 < e; k0 += VB) {
+    if (k0 != k00) b.load(k0, e, nnz, ci, v);
+    double xv[VB];
+#pragma unroll
+    for (int j = 0; j < VB; ++j)
+      xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + (b.c[j] & 0x7fffffff)) : 0.0;
+#pragma unroll
+    for (int j = 0; j < VB; ++j) {
+      if (k0 + j >= s && k0 + j < e) {
+        const double p = __dmul_rn(b.a[j], xv[j]);
+        if (b.c[j] >= 0)
+          sf = __dadd_rn(sf, p);
+        else
+          sc = __dadd_rn(sc, p);
+      }
+    }
+  }
+}
+
 }  // namespace airg

@@ -62,6 +62,8 @@ Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs
 // matrix the V-cycle streams, and the per-level vectors (fixed pointers, so
 // the V-cycle can be captured into a CUDA graph).
 void alloc_workspace(Ctx& c, Hier& h) {
+  h.tail_bar.alloc(c, 2);  // grid barrier of the coarse-tail kernel (solve.cu)
+  h.tail_bar.zero(c);
   for (size_t l = 0; l < h.levels.size(); ++l) {
     Level& L = h.levels[l];
     if (l > 0) L.b.alloc(c, (size_t)L.a.n);

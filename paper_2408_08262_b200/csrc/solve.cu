@@ -19,6 +19,7 @@
 #include "hier.cuh"
 #include "sell.cuh"
 #include "tiled.cuh"
+#include "tail.cuh"
 
 namespace airg {
 
@@ -230,20 +231,142 @@ __global__ void k_xupdate(int64_t n, int j, const double* __restrict__ Z, const 
 
 constexpr int kT = 128;
 
+// First fine level handled by the coarse-tail kernel (tail.cuh): the first
+// level with at most AIRG_TAIL_N rows. Off by default: on the C2 hierarchy a
+// barrier-separated phase costs ~6 us against ~3.5 us for a PDL-chained
+// kernel (profiles/r1_tail_ab.txt), so the per-phase kernels stay faster.
+int tail_start(const Hier& h, const airg_solve_config& cfg) {
+  static const int64_t tail_n = [] {
+    const char* e = getenv("AIRG_TAIL_N");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  const int L = (int)h.levels.size();
+  if (tail_n <= 0 || L == 0 || cfg.coarse_iterations <= 0 || h.coarse_a.n == 0) return L;
+  // phases: R + prolong + 2 per F-smooth per level, 2 per coarse iteration
+  const int64_t per_level = 2 + 2 * std::max<int64_t>(cfg.up_f_smooths, 0);
+  for (int l = 0; l < L; ++l)
+    if (h.levels[l].a.n <= tail_n && (L - l) * per_level + 2 * cfg.coarse_iterations <= kMaxTailPhases)
+      return l;
+  return L;
+}
+
+// Build the phase list of levels Lt..L-1 + the coarse grid and launch the
+// tail kernel (cooperative: every CTA resident, one per SM).
+void enqueue_tail(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* b0, int Lt) {
+  const int L = (int)h.levels.size();
+  std::vector<TailPhase> ph;
+  auto mat = [](TailPhase& p, const Csr& m) {
+    p.n = m.n;
+    p.rp = m.rp.p;
+    p.ci = m.ci.p;
+    p.v = m.v.p;
+  };
+  for (int l = Lt; l < L; ++l) {
+    Level& lv = h.levels[l];
+    if (!lv.r.n) continue;
+    TailPhase p{};
+    p.kind = kTailStore;
+    mat(p, lv.r);
+    p.x = l == 0 ? b0 : lv.b.p;
+    p.out = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
+    ph.push_back(p);
+  }
+  const double* rhs = h.cb.p;
+  for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
+    const double* r = rhs;
+    if (it > 0) {
+      TailPhase p{};
+      p.kind = kTailCres;
+      mat(p, h.coarse_a);
+      p.x = h.cx.p;
+      p.b = rhs;
+      p.out = h.cr.p;
+      ph.push_back(p);
+      r = h.cr.p;
+    }
+    TailPhase p{};
+    p.kind = kTailCupd;
+    mat(p, h.coarse_inv);
+    p.x = r;
+    p.out = h.cx.p;
+    p.first = it == 0 ? 1 : 0;
+    ph.push_back(p);
+  }
+  for (int l = L - 1; l >= Lt; --l) {
+    Level& lv = h.levels[l];
+    const double* bl = l == 0 ? b0 : lv.b.p;
+    TailPhase p{};
+    p.kind = kTailProlong;
+    p.n = lv.a.n;
+    p.idx = lv.pmap.p;
+    p.x = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
+    p.out = lv.x.p;
+    ph.push_back(p);
+    for (int64_t s = 0; s < cfg.up_f_smooths && lv.map.nf > 0; ++s) {
+      TailPhase q{};
+      if (s == 0) {
+        q.kind = kTailFres1;
+        mat(q, lv.af);
+        q.out2 = lv.sc.p;
+      } else {
+        q.kind = kTailFres2;
+        mat(q, lv.affg);
+        q.in2 = lv.sc.p;
+      }
+      q.x = lv.x.p;
+      q.b = bl;
+      q.idx = lv.map.f_to_fine.p;
+      q.out = lv.rf.p;
+      ph.push_back(q);
+      TailPhase u{};
+      u.kind = kTailFupd;
+      mat(u, lv.ffinv);
+      u.x = lv.rf.p;
+      u.idx = lv.map.f_to_fine.p;
+      u.out = lv.x.p;
+      ph.push_back(u);
+    }
+  }
+  static TailTable table;  // host staging of the parameter block (copied at launch)
+  table.nph = (int)ph.size();
+  std::copy(ph.begin(), ph.end(), table.ph);
+  if (!h.tail_bar.p) throw RuntimeError("tail kernel: barrier words not allocated");
+  static int per_sm = [] {
+    int nb = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tail, kTailThreads, 0));
+    return nb;
+  }();
+  if (per_sm < 1) throw RuntimeError("tail kernel: no resident CTA per SM");
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)c.num_sms);
+  lc.blockDim = dim3(kTailThreads);
+  lc.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  c.launches++;
+  CUDA_CHECK(cudaLaunchKernelEx(&lc, k_tail, table, h.tail_bar.p));
+}
+
 // Enqueue one V-cycle from level 0 rhs b0 into levels[0].x (or the coarse
 // x when there are no fine levels).
 void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* b0) {
   const int L = (int)h.levels.size();
+  const int Lt = tail_start(h, cfg);
   // descent: b_{l+1} = R_l b_l
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < Lt; ++l) {
     Level& lv = h.levels[l];
     const double* bl = l == 0 ? b0 : lv.b.p;
     double* bn = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
     if (lv.r.n)
       ROWS(EpiStore, lv.r, bl, EpiStore{bn});
   }
-  // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
-  {
+  if (Lt < L) {
+    enqueue_tail(c, h, cfg, b0, Lt);
+  } else {
+    // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
     const int n = h.coarse_a.n;
     const double* rhs = L == 0 ? b0 : h.cb.p;
     if (n) {
@@ -259,7 +382,7 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     }
   }
   // ascent: prolongate and F-smooth
-  for (int l = L - 1; l >= 0; --l) {
+  for (int l = std::min(L, Lt) - 1; l >= 0; --l) {
     Level& lv = h.levels[l];
     const double* bl = l == 0 ? b0 : lv.b.p;
     const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;

@@ -218,7 +218,7 @@ int row_vec(int64_t n, int64_t nnz) {
     const char* e = getenv("AIRG_VEC");
     return e ? atoi(e) : -1;
   }();
-  if (forced >= 0) return forced == 4 || forced == 8 ? forced : 0;
+  if (forced >= 0) return forced ? 8 : 0;
   return n > 0 && nnz >= 12 * n ? 8 : 0;
 }
 

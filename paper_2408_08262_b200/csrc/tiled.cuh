@@ -40,42 +40,61 @@ struct TileView {
 };
 
 // ---- thread per row -----------------------------------------------------------
+// Row bounds and the first batch of the row are loaded before the PDL wait
+// (static matrix data, rowdot.cuh RowBatch); m.vec selects aligned vector
+// batches for long-row matrices.
+template <int VB, bool VEC, class Epi>
+__device__ __forceinline__ void thread_row(const TileView& m, const double* __restrict__ x, Epi& epi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < m.nrows;
+  int s = 0, e = 0;
+  RowBatch<VB, VEC> b;
+  if (live) {
+    s = __ldg(m.rp + i);
+    e = __ldg(m.rp + i + 1);
+    if (s < e) b.load(batch_start<VB, VEC>(s), e, m.nnz, m.ci, m.v);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (live) epi.row(i, dot_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b));
+}
+
 template <class Epi>
 __global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const double* __restrict__ x,
                                                             Epi epi) {
+  if (m.vec)
+    thread_row<kRowBatch, true>(m, x, epi);
+  else
+    thread_row<kRowBatch, false>(m, x, epi);
+  epi.finish();
+}
+
+template <int VB, bool VEC, class Epi>
+__device__ __forceinline__ void thread_row_fc(const TileView& m, const double* __restrict__ x, Epi& epi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < m.nrows;
+  int s = 0, e = 0;
+  RowBatch<VB, VEC> b;
+  if (live) {
+    s = __ldg(m.rp + i);
+    e = __ldg(m.rp + i + 1);
+    if (s < e) b.load(batch_start<VB, VEC>(s), e, m.nnz, m.ci, m.v);
+  }
   pdl_wait();
   pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m.nrows) {
-    const int s = __ldg(m.rp + i), e = __ldg(m.rp + i + 1);
-    double acc;
-    if (m.vec == 8)
-      acc = dot_ordered_vec<8>(s, e, m.nnz, m.ci, m.v, x);
-    else if (m.vec == 4)
-      acc = dot_ordered_vec<4>(s, e, m.nnz, m.ci, m.v, x);
-    else
-      acc = dot_ordered(s, e, m.ci, m.v, x);
-    epi.row(i, acc);
-  }
-  epi.finish();
+  if (!live) return;
+  double sf, sc;
+  dot_fc_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b, sf, sc);
+  epi.row2(i, sf, sc);
 }
 
 template <class Epi>
 __global__ void __launch_bounds__(kTileThreads) rows_thread_fc(TileView m,
                                                                const double* __restrict__ x, Epi epi) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m.nrows) return;
-  double sf, sc;
-  const int s = __ldg(m.rp + i), e = __ldg(m.rp + i + 1);
-  if (m.vec == 8)
-    dot_ordered_fc_vec<8>(s, e, m.nnz, m.ci, m.v, x, sf, sc);
-  else if (m.vec == 4)
-    dot_ordered_fc_vec<4>(s, e, m.nnz, m.ci, m.v, x, sf, sc);
+  if (m.vec)
+    thread_row_fc<kRowBatch, true>(m, x, epi);
   else
-    dot_ordered_fc(s, e, m.ci, m.v, x, sf, sc);
-  epi.row2(i, sf, sc);
+    thread_row_fc<kRowBatch, false>(m, x, epi);
 }
 
 // ---- warp tiles -----------------------------------------------------------------

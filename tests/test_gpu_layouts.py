@@ -27,7 +27,7 @@ print(r.stats.iterations, hashlib.sha256(r.x.tobytes()).hexdigest(), hashlib.sha
 """ % REPO
 
 LAYOUTS = {
-    "thread": {"AIRG_ROWS": "thread", "AIRG_VEC": "0"},
+    "thread": {"AIRG_ROWS": "thread", "AIRG_VEC": "0", "AIRG_TAIL_N": "0"},
     "vec4": {"AIRG_VEC": "4"},
     "vec8": {"AIRG_VEC": "8"},
     "group_auto": {"AIRG_ROWS": "group"},
@@ -39,12 +39,14 @@ LAYOUTS = {
     "tiles": {"AIRG_ROWS": "tiles"},
     "sell": {"AIRG_LAYOUT": "sell"},
     "nopdl": {"AIRG_PDL": "0"},
+    "tail_off": {"AIRG_TAIL_N": "0"},
+    "tail_all": {"AIRG_TAIL_N": "100000000"},
 }
 
 
 def _run(env_extra):
     env = dict(os.environ)
-    for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC"):
+    for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N"):
         env.pop(k, None)
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
