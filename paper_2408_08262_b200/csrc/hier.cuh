@@ -42,6 +42,14 @@ struct Hier {
   DBuf<double> V, Z, w, hbuf, ybuf;
   // coarse-tail persistent kernel (tail.cuh): grid barrier words
   DBuf<unsigned> tail_bar;
+  // device-side Richardson loop (solve.cu): iteration count, residual
+  // history, [rtol, max_iterations] and the conditional-WHILE graph
+  DBuf<long long> loop_it;
+  DBuf<double> loop_hist, loop_par;
+  cudaGraphExec_t g_loop = nullptr;
+  int64_t g_key_loop = -1;
+  uint64_t g_loop_kernels = 0;
+  bool loop_broken = false;  // instantiation refused: host loop from then on
   // cached graphs
   cudaGraphExec_t g_rich = nullptr, g_vc = nullptr;
   int64_t g_key_rich = -1, g_key_vc = -1;
@@ -52,6 +60,7 @@ struct Hier {
   ~Hier() {
     if (g_rich) cudaGraphExecDestroy(g_rich);
     if (g_vc) cudaGraphExecDestroy(g_vc);
+    if (g_loop) cudaGraphExecDestroy(g_loop);
   }
 };
 

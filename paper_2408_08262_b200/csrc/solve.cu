@@ -164,6 +164,23 @@ __global__ void k_sum_partials(const double* __restrict__ part, int np, double* 
   }
 }
 
+// Device-side convergence test of the Richardson loop (solve.cpp:196-224):
+// it += 1; rel = sqrt(||r||^2) / sqrt(||b||^2) -- the same correctly rounded
+// sqrt and division the host loop performs -- appended to the history; the
+// WHILE condition stays 1 unless rel <= rtol or it >= max_iterations.
+__global__ void k_loop_check(cudaGraphConditionalHandle hnd, const double* __restrict__ scal,
+                             const double* __restrict__ par, long long* __restrict__ it,
+                             double* __restrict__ hist, long long cap) {
+  pdl_wait();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long k = *it + 1;
+  *it = k;
+  const double rel = sqrt(scal[0]) / sqrt(scal[1]);
+  if (k < cap) hist[k] = rel;
+  const bool stop = rel <= par[0] || (double)k >= par[1];
+  cudaGraphSetConditional(hnd, stop ? 0u : 1u);
+}
+
 // ---- GMRES helpers
 // partial dots of w with columns 0..j of V: grid (blocks, j+1)
 __global__ void k_multidot(int64_t n, const double* __restrict__ V, const double* __restrict__ w,
@@ -493,6 +510,80 @@ void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, do
 
 namespace {
 
+// The whole Richardson loop as ONE graph launch: a conditional WHILE node
+// whose body is the captured iteration (V-cycle, x += e, r = b - A x, ||r||^2)
+// followed by k_loop_check, which sets the loop condition on the device. No
+// host round trip between iterations. Returns false when the driver refuses
+// the conditional graph (the caller then runs the host loop).
+bool build_device_loop(Ctx& c, Hier& h, const airg_solve_config& cfg) {
+  const int64_t key = graph_key(cfg);
+  if (h.g_loop && h.g_key_loop == key) return true;
+  if (h.g_loop) {
+    cudaGraphExecDestroy(h.g_loop);
+    h.g_loop = nullptr;
+  }
+  const int n = h.top_n();
+  cudaGraph_t g = nullptr;
+  CUDA_CHECK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle hnd;
+  cudaGraphNode_t node;
+  cudaGraphNodeParams np = {};
+  if (cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    return false;
+  }
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = hnd;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &np) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    return false;
+  }
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  const uint64_t before = c.launches;
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_vcycle(c, h, cfg, h.r.p);
+    LAUNCH_PDL(c, k_axpy1, blocks_for(n, 256), 256, 0, n, vcycle_output(h), h.xsol.p);
+    enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
+    LAUNCH_PDL(c, k_loop_check, 1, 32, 0, hnd, (const double*)h.scal.p, (const double*)h.loop_par.p,
+               h.loop_it.p, h.loop_hist.p, (long long)h.loop_hist.n);
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(c.stream, &dummy);
+    cudaGraphDestroy(g);
+    c.launches = before;
+    throw;
+  }
+  cudaGraph_t captured;
+  CUDA_CHECK(cudaStreamEndCapture(c.stream, &captured));
+  const uint64_t k = c.launches - before;
+  c.launches = before;
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  h.g_loop = exec;
+  h.g_key_loop = key;
+  h.g_loop_kernels = k;
+  return true;
+}
+
+bool device_loop_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_DEVLOOP");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // richardson_solve (solve.cpp:167-259)
 void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
                 std::vector<double>& hist) {
@@ -520,6 +611,33 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
       h.g_key_rich = key;
     }
     CUDA_CHECK(cudaMemcpyAsync(h.r.p, h.rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    // device loop: the first test (rel = 1 at it = 0) on the host, the rest
+    // inside the graph
+    const int64_t cap = cfg.max_iterations + 1;
+    const bool first_stops = 1.0 <= cfg.rtol || cfg.max_iterations <= 0;
+    if (!first_stops && device_loop_enabled() && !h.loop_broken && cap <= (int64_t)1 << 20) {
+      if (h.loop_hist.n < (size_t)cap) h.loop_hist.alloc(c, (size_t)cap);
+      if (!h.loop_par.p) h.loop_par.alloc(c, 2);
+      if (!h.loop_it.p) h.loop_it.alloc(c, 1);
+      if (!build_device_loop(c, h, cfg)) h.loop_broken = true;
+    }
+    if (!first_stops && device_loop_enabled() && !h.loop_broken && h.g_loop) {
+      const double par[2] = {cfg.rtol, (double)cfg.max_iterations};
+      to_device(c, h.loop_par.p, par, 2);
+      CUDA_CHECK(cudaMemsetAsync(h.loop_it.p, 0, sizeof(long long), c.stream));
+      CUDA_CHECK(cudaGraphLaunch(h.g_loop, c.stream));
+      const long long its = read1(c, h.loop_it.p);
+      std::vector<double> hv((size_t)its + 1);
+      hv[0] = 1.0;
+      if (its > 0) to_host(c, hv.data() + 1, h.loop_hist.p + 1, (size_t)its);
+      for (double r : hv) hist.push_back(r);
+      c.launches += h.g_loop_kernels * (uint64_t)its;
+      fc += (uint64_t)its * (vflops + 2 * (uint64_t)n) +
+            (uint64_t)its * (2 * (uint64_t)a.nnz + 2 * (uint64_t)n + 2 * (uint64_t)n);
+      st.final_relative_residual = hv.back();
+      st.iterations = its;
+      st.converged = hv.back() <= cfg.rtol ? 1 : 0;
+    } else
     for (int64_t it = 0;; ++it) {
       double rel;
       if (it == 0) {

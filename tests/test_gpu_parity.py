@@ -44,7 +44,7 @@ def _injection(oh, prm):
                        info.coarse_effective_order)}
 
 
-CF_CASES = [(0, 1.0), (1, 0.25), (2, 0.25), (3, 0.125), (4, 0.25), (1, 1.0), (2, 1.0)]
+CF_CASES = [(0, 1.0), (1, 0.25), (2, 0.25), (3, 0.125), (4, 0.25), (1, 1.0), (2, 1.0), (3, 1.0), (4, 1.0)]
 
 
 @pytest.mark.parametrize("cfg,scale", CF_CASES, ids=[f"C{c}x{s}" for c, s in CF_CASES])
@@ -58,6 +58,12 @@ def test_p1_level0_cf_labels_bit_exact(port, cfg, scale):
     assert np.array_equal(lab, ol), "post-DDC labels differ"
     assert (rep.n_f_pre, rep.n_converted, rep.s_nnz) == (orep.n_f_pre, orep.n_converted, orep.s_nnz)
     assert same_bits([rep.max_theta, rep.alpha_diag], [orep.max_theta, orep.alpha_diag])
+    # ... and at 2/4/8 GPUs (row slabs, emulated ranks)
+    for P in (2, 4, 8):
+        dl, drep = airg.dist_cf_split(_sm(p), P, alpha=prm["strength_alpha"], max_loops=prm["max_loops"],
+                                      seed=seed)
+        assert np.array_equal(dl, ol), f"{P}-slab labels differ"
+        assert drep.n_converted == orep.n_converted
     # size-independent property: F independent in S u S^T
     s = airg.strength(_sm(p), prm["strength_alpha"])
     d = np.repeat(np.arange(p.n), np.diff(s.row_offsets))
@@ -167,6 +173,28 @@ def test_c2_full_native_solve(port):
     assert np.linalg.norm(r) / np.linalg.norm(p.b) <= TOL_RES * 1.01
     g = airg.gmres_solve(h, p.b, coarse_iterations=prm["coarse_iterations"])
     assert g.stats.converged and np.linalg.norm(g.x - res.x) / np.linalg.norm(res.x) <= 1e-8
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3, 4])
+def test_full_size_native_solves(cfg):
+    """Every BASELINE config at full size: native setup + solve converges to
+    rtol 1e-10, checked by a host scipy matvec independent of the GPU. C0
+    and C4 use the outer GMRES: C0's config names it, and on C4 the level-0
+    polynomial smoother misses the growth bound on every attempt (growth
+    2.33 at full size, 1.04 at half size -- the compiled reference reports
+    the same 1.0387 at half size) so plain Richardson stagnates there, in
+    the reference as here."""
+    import scipy.sparse as sp
+    p = problems.make(cfg)
+    prm = problems.setup_params(cfg)
+    h = airg.setup(_sm(p), **prm)
+    solve = airg.gmres_solve if cfg in (0, 4) else airg.richardson_solve
+    res = solve(h, p.b, coarse_iterations=prm["coarse_iterations"])
+    assert res.stats.converged and res.stats.final_relative_residual <= TOL_RES
+    A = sp.csr_matrix((p.vals, p.cols, p.row_offsets), shape=(p.n, p.n))
+    rel = np.linalg.norm(p.b - A @ res.x) / np.linalg.norm(p.b)
+    assert rel <= TOL_RES * 1.05
+    assert h.n_levels >= 1
 
 
 def test_edge_cases():

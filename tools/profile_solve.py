@@ -9,6 +9,10 @@ import os
 import sys
 
 import numpy as np
+
+# profilers see the kernels of the host-driven loop (conditional graph bodies are
+# opaque to CUPTI / ncu)
+os.environ.setdefault("AIRG_DEVLOOP", "0")
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

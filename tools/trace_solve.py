@@ -47,10 +47,14 @@ def main():
         else:
             st, _ = h.solve_device(tb, tx, **sk)
         torch.cuda.synchronize()
-    path = "/tmp/trace_solve.json"
+    path = os.path.splitext(args.out)[0] + ".json"
     prof.export_chrome_trace(path)
     ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") == "kernel"]
     ev.sort(key=lambda e: e["ts"])
+    # marginal cost of a kernel on the dependency chain: end(k) - end(k-1)
+    # (with PDL a kernel starts before its predecessor ends, so 'dur' overlaps)
+    for i, e in enumerate(ev):
+        e["marg"] = e["dur"] if i == 0 else (e["ts"] + e["dur"]) - (ev[i - 1]["ts"] + ev[i - 1]["dur"])
     tot = collections.defaultdict(float)
     cnt = collections.Counter()
     import re
@@ -75,6 +79,8 @@ def main():
         L = h.n_levels
         nco = 2 * prm["coarse_iterations"] - 1
         per_it = L + nco + L * (1 + 2 * 2) + 3
+        if any("k_loop_check" in e["name"] for e in ev):
+            per_it += 1  # device-side convergence test (AIRG_DEVLOOP)
         first = 2  # dot_partials, reduce_partials (bnorm)
         it = min(5, st.iterations - 1)
         seq = ev[first + it * per_it: first + (it + 1) * per_it]
@@ -85,16 +91,17 @@ def main():
         asc = seq[L + nco: L + nco + 5 * L]
         for l in range(L):
             info = h.level(l)
-            r_us = seq[l]["dur"]
+            r_us = seq[l]["marg"]
             blk = asc[(L - 1 - l) * 5:(L - l) * 5]
             nnz_af = info.nnz_ff + info.nnz_fc
             br = 12 * info.nnz_r + 4 * info.n_c + 16 * info.n_c + 8 * info.n
             baf = 12 * nnz_af + 4 * info.n_f + 8 * info.n + 32 * info.n_f
             bq = 12 * info.nnz_ffinv + 4 * info.n_f + 24 * info.n_f
             lines.append(f"{l:3d} {info.n:8d} {info.nnz_r:9d} {r_us:7.1f} {br / r_us / 1e3:6.0f} | {nnz_af:9d} "
-                         f"{blk[1]['dur']:7.1f} {baf / blk[1]['dur'] / 1e3:6.0f} | {info.nnz_ff:8d} "
-                         f"{blk[3]['dur']:6.1f} | {info.nnz_ffinv:8d} {blk[2]['dur']:6.1f} "
-                         f"{bq / blk[2]['dur'] / 1e3:6.0f} | {blk[0]['dur']:5.1f}")
+                         f"{blk[1]['marg']:7.1f} {baf / blk[1]['marg'] / 1e3:6.0f} | {info.nnz_ff:8d} "
+                         f"{blk[3]['marg']:6.1f} | {info.nnz_ffinv:8d} {blk[2]['marg']:6.1f} "
+                         f"{bq / blk[2]['marg'] / 1e3:6.0f} | {blk[0]['marg']:5.1f}")
+        lines.append("(per-kernel columns are marginal times on the chain: end(k) - end(k-1))")
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     open(args.out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
