@@ -298,6 +298,24 @@ def run_gpu_dist(args):
     starts = np.arange(ws + 1, dtype=np.int64) * slab
     d = airg.Dist(h, ws, rank=rank, comm=comm, threshold=2.0, starts=starts)
     lo, hi = starts[rank], starts[rank + 1]
+    # CF split at N GPUs: the row-slab PMISR-DDC (airg_dist_cf_split) on
+    # every level's operator with that level's slabs; max over ranks
+    cf_ms = 0.0
+    for l in range(h.n_levels):
+        Al = h.matrix_handle(l, 0)
+        sl = d.level_info(l)["starts"]
+        seed = int(problems.mix(np.uint64(0), np.uint64(l)))
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        airg.dist_cf_split_device(Al, sl, rank=rank, comm=comm, alpha=prm["strength_alpha"],
+                                  max_loops=prm["max_loops"], seed=seed, ctx=ctx)
+        c1.record(stream)
+        c1.synchronize()
+        cf_ms += c0.elapsed_time(c1)
+    tcf = torch.tensor([cf_ms], device=ctx.tdev, dtype=torch.float64)
+    dist.all_reduce(tcf, op=dist.ReduceOp.MAX)
+    cf_ms = float(tcf[0])
     with torch.cuda.stream(stream):
         tb = torch.from_numpy(p.b[lo:hi].copy()).to(ctx.tdev)
         tx = torch.empty(hi - lo, dtype=torch.float64, device=ctx.tdev)
@@ -359,8 +377,8 @@ def run_gpu_dist(args):
         "active_ranks": [lv["active"] for lv in levels],
         "e2e": {"value": p.n / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
                 "d2h_bytes_per_step": 8 * int(hi - lo), "ms_per_step": e2e_ms},
-        "gpu_launches": int(launches),
-        "gmres": gm, "clocks": clk.summary(), "cpu_baseline": None,
+        "gpu_launches": int(launches), "cf_split_ms": cf_ms,
+        "clocks": clk.summary(), "cpu_baseline": None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
