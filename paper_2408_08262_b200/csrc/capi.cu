@@ -124,6 +124,8 @@ int airg_ctx_destroy(airg_ctx* ctx) {
     if (!ctx) return;
     bind(ctx->c);
     cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.scratch) cudaFree(ctx->c.scratch);
+    if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
   });
@@ -328,6 +330,15 @@ int airg_pmisr_with_weights(airg_ctx* ctx, const airg_csr* s_pattern, int64_t ma
   });
 }
 
+// AIRG_CF=legacy: the step-by-step split (materialised S, label map, A_ff)
+static bool cf_split_legacy() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_CF");
+    return e && !strcmp(e, "legacy");
+  }();
+  return v;
+}
+
 int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops, uint64_t seed,
                   int32_t weight_mode, int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
                   uint8_t* labels, uint8_t* labels_pre, airg_cf_report* rep) {
@@ -337,6 +348,22 @@ int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_lo
     need(labels, "labels");
     bind(ctx->c);
     Ctx& c = ctx->c;
+    if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
+    if (weight_mode == 0 && !cf_split_legacy()) {
+      const CfFused f = cf_split_fused(c, a->m, alpha, seed, ddc_enabled != 0, ddc_fraction, ddc_bins,
+                                       labels, labels_pre);
+      airg_cf_report r;
+      std::memset(&r, 0, sizeof r);
+      r.n_f_pre = f.n_f_pre;
+      r.s_nnz = f.s_nnz;
+      r.max_theta = f.max_theta;
+      r.alpha_diag = f.alpha_diag;
+      r.n_converted = f.n_converted;
+      r.n_f = r.n_f_pre - r.n_converted;
+      r.n_c = a->m.n - r.n_f;
+      if (rep) *rep = r;
+      return;
+    }
     Strength g;
     strength(c, a->m, alpha, g);
     pmisr(c, g, max_loops, seed, weight_mode, labels, nullptr);

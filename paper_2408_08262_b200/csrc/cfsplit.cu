@@ -227,25 +227,28 @@ __global__ void theta_rows(int nf, const int32_t* __restrict__ rp, const int32_t
                            unsigned long long* __restrict__ maxbits,
                            unsigned long long* __restrict__ bad_row) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nf) return;
-  double off = 0.0, diag = 0.0;
-  bool seen = false;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) {
-    if (ci[k] == i) {
-      diag = fabs(v[k]);
-      seen = true;
+  unsigned long long tb = 0;
+  if (i < nf) {
+    double off = 0.0, diag = 0.0;
+    bool seen = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      if (ci[k] == i) {
+        diag = fabs(v[k]);
+        seen = true;
+      } else {
+        off = __dadd_rn(off, fabs(v[k]));
+      }
+    }
+    if (!seen || diag == 0.0) {
+      atomicMin(bad_row, (unsigned long long)i);
+      theta[i] = 0.0;
     } else {
-      off = __dadd_rn(off, fabs(v[k]));
+      const double t = __ddiv_rn(off, diag);
+      theta[i] = t;
+      tb = (unsigned long long)__double_as_longlong(t);
     }
   }
-  if (!seen || diag == 0.0) {
-    atomicMin(bad_row, (unsigned long long)i);
-    theta[i] = 0.0;
-    return;
-  }
-  const double t = __ddiv_rn(off, diag);
-  theta[i] = t;
-  atomicMax(maxbits, (unsigned long long)__double_as_longlong(t));
+  block_max(maxbits, tb);
 }
 
 __global__ void theta_hist(int nf, const double* __restrict__ theta,
@@ -272,19 +275,36 @@ __global__ void theta_hist(int nf, const double* __restrict__ theta,
       if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
 }
 
-// coarsening.cpp:290-315
-__global__ void select_alpha(int nf, const unsigned long long* __restrict__ hist, int64_t bins,
-                             double fraction, const unsigned long long* __restrict__ maxbits,
-                             int selection, double direct_alpha, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// coarsening.cpp:290-315 with n_f read from the device counter. The
+// reference scans k = bins-1 .. 0, accumulating above += hist[k] and keeping
+// k when |above - target| is STRICTLY smaller than the best so far (initially
+// k = bins, above = 0). That is the largest k among the minimisers of
+// err_k = |S_k - target| over k in [0, bins] (S_k = suffix sum, S_bins = 0):
+// one block computes the suffix sums in shared memory, every thread scores
+// its bins with the same rounded ops, and an (err, -k) min-reduction picks
+// the winner -- identical to the serial scan, without ~bins dependent
+// global loads on one thread. Falls back to the serial scan for bins > 8192.
+constexpr int kSelThreads = 1024;
+__global__ void __launch_bounds__(kSelThreads)
+fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
+           const unsigned long long* __restrict__ hist, int64_t bins, double fraction,
+           const unsigned long long* __restrict__ maxbits, int selection, double direct_alpha,
+           double* __restrict__ out) {
+  __shared__ unsigned suf[8192 + 1];  // counts <= n_f < 2^31
+  __shared__ double werr[kSelThreads / 32];
+  __shared__ int64_t wk[kSelThreads / 32];
   const double max_theta = __longlong_as_double((long long)*maxbits);
-  double alpha_diag;
-  if (selection == 2) {
-    alpha_diag = direct_alpha;
-  } else if (max_theta == 0.0) {
-    alpha_diag = 0.0;
-  } else {
-    const double target = __dmul_rn(fraction, (double)nf);
+  const int t = threadIdx.x;
+  if (selection == 2 || max_theta == 0.0) {  // direct alpha (DdcSelection::direct) / nothing dominant
+    if (t == 0) {
+      out[0] = selection == 2 ? direct_alpha : 0.0;
+      out[1] = max_theta;
+    }
+    return;
+  }
+  const double target = __dmul_rn(fraction, (double)(nfp ? (long long)*nfp : nf_val));
+  if (bins > 8192) {  // serial scan
+    if (t != 0) return;
     int64_t above = 0, best_k = bins;
     double best_err = fabs(__dsub_rn((double)above, target));
     for (int64_t k = bins; k-- > 0;) {
@@ -295,10 +315,87 @@ __global__ void select_alpha(int nf, const unsigned long long* __restrict__ hist
         best_k = k;
       }
     }
-    alpha_diag = __dmul_rn((double)best_k, __ddiv_rn(max_theta, (double)bins));
+    out[0] = __dmul_rn((double)best_k, __ddiv_rn(max_theta, (double)bins));
+    out[1] = max_theta;
+    return;
   }
-  out[0] = alpha_diag;
-  out[1] = max_theta;
+  const int nb = (int)bins;
+  for (int k = t; k < nb; k += kSelThreads) suf[k] = (unsigned)hist[k];
+  if (t == 0) suf[nb] = 0;
+  __syncthreads();
+  // suffix sums: each thread owns a contiguous chunk; serial within, scan of chunk totals
+  const int chunk = (nb + kSelThreads - 1) / kSelThreads;
+  const int lo = t * chunk, hi = min(nb, lo + chunk);
+  unsigned acc = 0;
+  for (int k = hi - 1; k >= lo; --k) acc += suf[k];
+  // exclusive suffix scan of the chunk totals across the block (integers: exact)
+  __shared__ unsigned wtot[kSelThreads / 32];
+  const int lane = t & 31, wid = t >> 5;
+  unsigned incl = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_down_sync(0xffffffffu, incl, o);
+    if (lane + o < 32) incl += y;
+  }
+  if (lane == 0) wtot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned wv = lane < kSelThreads / 32 ? wtot[lane] : 0u;
+    unsigned wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_down_sync(0xffffffffu, wi, o);
+      if (lane + o < 32) wi += y;
+    }
+    if (lane < kSelThreads / 32) wtot[lane] = wi - wv;  // sum over later warps
+  }
+  __syncthreads();
+  unsigned run = (incl - acc) + wtot[wid];
+  for (int k = hi - 1; k >= lo; --k) {
+    run += suf[k];
+    suf[k] = run;  // S_k
+  }
+  __syncthreads();
+  double best_err = INFINITY;
+  int64_t best_k = -1;
+  for (int k = t; k <= nb; k += kSelThreads) {
+    const double err = fabs(__dsub_rn((double)(int64_t)suf[k], target));
+    if (err < best_err || (err == best_err && k > best_k)) {
+      best_err = err;
+      best_k = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double e2 = __shfl_xor_sync(0xffffffffu, best_err, o);
+    const int64_t k2 = __shfl_xor_sync(0xffffffffu, best_k, o);
+    if (e2 < best_err || (e2 == best_err && k2 > best_k)) {
+      best_err = e2;
+      best_k = k2;
+    }
+  }
+  if ((t & 31) == 0) {
+    werr[t >> 5] = best_err;
+    wk[t >> 5] = best_k;
+  }
+  __syncthreads();
+  if (t < 32) {
+    best_err = werr[t];
+    best_k = wk[t];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double e2 = __shfl_xor_sync(0xffffffffu, best_err, o);
+      const int64_t k2 = __shfl_xor_sync(0xffffffffu, best_k, o);
+      if (e2 < best_err || (e2 == best_err && k2 > best_k)) {
+        best_err = e2;
+        best_k = k2;
+      }
+    }
+    if (t == 0) {
+      out[0] = __dmul_rn((double)best_k, __ddiv_rn(max_theta, (double)bins));
+      out[1] = max_theta;
+    }
+  }
 }
 
 __global__ void ddc_convert(int nf, const double* __restrict__ theta, const double* __restrict__ sel,
@@ -458,8 +555,8 @@ DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, do
     const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
     LAUNCH(c, theta_hist, blocks, 256, smem, nf, s.theta.p, s.u.p, bins, hist.p);
   }
-  LAUNCH(c, select_alpha, 1, 32, 0, nf, hist.p, bins, fraction, s.u.p, selection, direct_alpha,
-         sel.p);
+  LAUNCH(c, fcf_select, 1, kSelThreads, 0, (const unsigned long long*)nullptr, (long long)nf, hist.p, bins,
+         fraction, s.u.p, selection, direct_alpha, sel.p);
   if (convert && nf)
     LAUNCH(c, ddc_convert, blocks_for(nf, 256), 256, 0, nf, s.theta.p, sel.p, map.f_to_fine.p,
            d_labels, s.u.p + 2);
@@ -484,6 +581,226 @@ double dominance_max(Ctx& c, const Csr& aff) {
   double mx;
   memcpy(&mx, &u[0], sizeof mx);
   return mx;
+}
+
+// ---- fused, sync-free CF split (airg_cf_split, the CF-split metric) -------------
+// The labels need neither S nor A_ff as matrices: strength is a per-row
+// threshold (thr_i = alpha * off_max_i) that any later pass re-applies to A's
+// entries, and theta of an F row is its A row restricted to F columns in
+// column order -- exactly A_ff's row, since extract_blocks keeps the order.
+// So the split is seven passes over A with no scans, no allocations sized by
+// a count, and no host synchronisation until the single report readback:
+//   rows (thr, |S_i|, |S^T| atomics) -> weights -> not-minimal marks ->
+//   labels -> theta (+max) -> histogram -> alpha (1 thread) -> convert.
+// Same arithmetic as the kernels above, so the same labels bit for bit.
+namespace {
+
+__global__ void fcf_rows(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                         const double* __restrict__ v, double alpha, double* __restrict__ thr,
+                         int32_t* __restrict__ s_cnt, int32_t* __restrict__ st_cnt,
+                         unsigned long long* __restrict__ s_total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int cnt = 0;
+  if (i < n) {
+    const int s = rp[i], e = rp[i + 1];
+    double off_max = 0.0;
+    for (int k = s; k < e; ++k)
+      if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
+    const double t = __dmul_rn(alpha, off_max);
+    thr[i] = t;
+    for (int k = s; k < e; ++k) {
+      const double mag = fabs(v[k]);
+      const int c = ci[k];
+      if (c != i && mag > 0.0 && mag >= t) {
+        ++cnt;
+        atomicAdd(st_cnt + c, 1);
+      }
+    }
+    s_cnt[i] = cnt;
+  }
+  block_add(s_total, (unsigned long long)cnt);
+}
+
+__global__ void fcf_weights(int n, const int32_t* __restrict__ s_cnt, const int32_t* __restrict__ st_cnt,
+                            uint64_t stream_key, double* __restrict__ w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t deg = (int64_t)s_cnt[i] + st_cnt[i];
+  const double u = (double)(mix(stream_key, (uint64_t)i) >> 11) * 0x1.0p-53;
+  w[i] = __dadd_rn((double)deg, u);
+}
+
+__global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const double* __restrict__ thr,
+                          const double* __restrict__ w, uint8_t* __restrict__ notmin) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double t = thr[i];
+  bool mine = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const int j = ci[k];
+    const double mag = fabs(v[k]);
+    if (j == i || !(mag > 0.0) || !(mag >= t)) continue;
+    if (weight_less(w, j, i))
+      mine = true;
+    else
+      notmin[j] = 1;
+  }
+  if (mine) notmin[i] = 1;
+}
+
+__global__ void fcf_labels(int n, const uint8_t* __restrict__ notmin, const double* __restrict__ w,
+                           uint8_t* __restrict__ label, unsigned long long* __restrict__ nf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool f = false;
+  if (i < n) {
+    f = w[i] < 1.0 || !notmin[i];
+    label[i] = f ? AIRG_F : AIRG_C;
+  }
+  block_add(nf, f ? 1ull : 0ull);
+}
+
+// theta of an F row over A's F columns in column order (= its A_ff row)
+__global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const uint8_t* __restrict__ label,
+                          double* __restrict__ theta, unsigned long long* __restrict__ maxbits,
+                          unsigned long long* __restrict__ bad_row) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long tb = 0;
+  if (i < n && label[i] == AIRG_F) {
+    double off = 0.0, diag = 0.0;
+    bool seen = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      if (label[j] != AIRG_F) continue;
+      if (j == i) {
+        diag = fabs(v[k]);
+        seen = true;
+      } else {
+        off = __dadd_rn(off, fabs(v[k]));
+      }
+    }
+    if (!seen || diag == 0.0) {
+      atomicMin(bad_row, (unsigned long long)i);
+      theta[i] = 0.0;
+    } else {
+      const double t = __ddiv_rn(off, diag);
+      theta[i] = t;
+      tb = (unsigned long long)__double_as_longlong(t);  // t >= 0: bit order = value order
+    }
+  }
+  block_max(maxbits, tb);
+}
+
+__global__ void fcf_hist(int n, const uint8_t* __restrict__ label, const double* __restrict__ theta,
+                         const unsigned long long* __restrict__ maxbits, int64_t bins,
+                         unsigned long long* __restrict__ hist) {
+  extern __shared__ unsigned int sh[];
+  const bool priv = bins <= 8192;
+  if (priv)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const double mx = __longlong_as_double((long long)*maxbits);
+  const double width = mx > 0.0 ? __ddiv_rn(mx, (double)bins) : 1.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (label[i] != AIRG_F) continue;
+    int64_t b = (int64_t)__ddiv_rn(theta[i], width);
+    if (b > bins - 1) b = bins - 1;
+    if (priv)
+      atomicAdd(sh + b, 1u);
+    else
+      atomicAdd(hist + b, 1ull);
+  }
+  __syncthreads();
+  if (priv)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+      if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
+}
+
+__global__ void fcf_convert(int n, const double* __restrict__ theta, const double* __restrict__ sel,
+                            const unsigned long long* __restrict__ bad_row, uint8_t* __restrict__ label,
+                            unsigned long long* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool conv = false;
+  if (i < n && *bad_row == ~0ull && label[i] == AIRG_F) {
+    const double t = theta[i];
+    if (t > sel[0] && t != 0.0) {
+      label[i] = AIRG_C;
+      conv = true;
+    }
+  }
+  block_add(count, conv ? 1ull : 0ull);
+}
+
+}  // namespace
+
+CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
+                       double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre) {
+  if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
+  if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0))
+    throw InvalidArgument("ddc: fraction must be in (0, 1]");
+  if (ddc_enabled && bins < 1) throw InvalidArgument("dominance_report: bins >= 1");
+  CfFused r;
+  const int n = a.n;
+  if (n == 0) return r;
+  const unsigned g = blocks_for(n, 256);
+  // one scratch block: [u: 8 x u64 | hist: bins x u64 | thr | w | theta | sel(2)] doubles,
+  // then [s_cnt | st_cnt] int32, then notmin bytes
+  const size_t nb = ddc_enabled ? (size_t)bins : 0;
+  const size_t dbl = 8 + nb + 3 * (size_t)n + 2;
+  const size_t bytes = dbl * 8 + 2 * (size_t)n * 4 + (size_t)n + 16;
+  uint8_t* base = static_cast<uint8_t*>(ctx_scratch(c, bytes));
+  unsigned long long* u = reinterpret_cast<unsigned long long*>(base);
+  unsigned long long* hist = u + 8;
+  double* thr = reinterpret_cast<double*>(hist + nb);
+  double* w = thr + n;
+  double* theta = w + n;
+  double* sel = theta + n;
+  int32_t* cnt = reinterpret_cast<int32_t*>(sel + 2);
+  uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + 2 * (size_t)n);
+  // u: [0] |S| [1] n_f_pre [2] max theta bits [3] bad row [4] converted
+  //    [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
+  CUDA_CHECK(cudaMemsetAsync(u, 0, (8 + nb) * 8, c.stream));
+  CUDA_CHECK(cudaMemsetAsync(u + 3, 0xff, 8, c.stream));
+  CUDA_CHECK(cudaMemsetAsync(cnt + n, 0, sizeof(int32_t) * n, c.stream));
+  CUDA_CHECK(cudaMemsetAsync(notmin, 0, n, c.stream));
+  LAUNCH(c, fcf_rows, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, cnt + n, u);
+  const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
+  LAUNCH(c, fcf_weights, g, 256, 0, n, cnt, cnt + n, key, w);
+  LAUNCH(c, fcf_marks, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, w, notmin);
+  LAUNCH(c, fcf_labels, g, 256, 0, n, notmin, w, d_labels, u + 1);
+  if (d_labels_pre)
+    CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
+  if (ddc_enabled) {
+    LAUNCH(c, fcf_theta, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, d_labels, theta, u + 2, u + 3);
+    const unsigned hb = (unsigned)std::min<int64_t>(g, 4 * c.num_sms);
+    const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
+    LAUNCH(c, fcf_hist, hb, 256, smem, n, d_labels, theta, u + 2, bins, hist);
+    LAUNCH(c, fcf_select, 1, kSelThreads, 0, u + 1, 0ll, hist, bins, fraction, u + 2, 0, 0.0,
+           reinterpret_cast<double*>(u + 5));
+    LAUNCH(c, fcf_convert, g, 256, 0, n, theta, reinterpret_cast<const double*>(u + 5), u + 3, d_labels,
+           u + 4);
+  }
+  (void)sel;
+  unsigned long long hu[8];
+  to_host(c, hu, u, 8);
+  double hs[2];
+  std::memcpy(hs, hu + 5, sizeof hs);
+  if (ddc_enabled && hu[3] != ~0ull) {
+    // the reference names the A_ff row: the F sub-index of the fine row
+    // (fcf_convert leaves the labels untouched when a row was bad)
+    std::vector<uint8_t> lab((size_t)hu[3]);
+    if (!lab.empty()) to_host(c, lab.data(), d_labels, lab.size());
+    int64_t sub = 0;
+    for (uint8_t l : lab) sub += l == AIRG_F;
+    throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(sub));
+  }
+  r.s_nnz = (int64_t)hu[0];
+  r.n_f_pre = (int64_t)hu[1];
+  r.n_converted = (int64_t)hu[4];
+  r.alpha_diag = hs[0];
+  r.max_theta = hs[1];
+  return r;
 }
 
 }  // namespace airg

@@ -13,7 +13,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -63,10 +65,17 @@ struct Ctx {
   cudaStream_t own_stream = nullptr;
   uint64_t launches = 0;
   int num_sms = 148;
-  // pinned host staging for small readbacks
+  // pinned host staging for small readbacks (allocated on first use)
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // reusable device scratch (stream-ordered; grown on demand)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
 };
+
+// Device scratch of at least `bytes` (contents undefined), reused across
+// calls on the context's stream.
+inline void* ctx_scratch(Ctx& c, size_t bytes);
 
 // Launch helper: counts every kernel this library enqueues (bench.py reports
 // the delta as gpu_launches) and checks the launch.
@@ -109,6 +118,34 @@ inline void launch_pdl(Ctx& c, void (*kernel)(KArgs...), dim3 grid, dim3 block, 
 }
 #define LAUNCH_PDL(ctx, kernel, grid, block, smem, ...) \
   ::airg::launch_pdl((ctx), kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__)
+
+// one atomic per block: warp shuffles, then the block's warps through shared
+// memory (counters shared by all rows would otherwise serialise at L2)
+__device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long long v) {
+  __shared__ unsigned long long part[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    if (t) atomicAdd(dst, t);
+  }
+}
+__device__ __forceinline__ void block_max(unsigned long long* dst, unsigned long long v) {
+  __shared__ unsigned long long part[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = max(t, part[w]);
+    if (t) atomicMax(dst, t);
+  }
+}
+
 
 inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
@@ -166,11 +203,35 @@ struct DBuf {
   T* get() const { return p; }
 };
 
-// Read a few values back (synchronises the context stream).
+inline void* ctx_scratch(Ctx& c, size_t bytes) {
+  if (bytes > c.scratch_bytes) {
+    if (c.scratch) CUDA_CHECK(cudaFreeAsync(c.scratch, c.stream));
+    const size_t want = std::max(bytes, 2 * c.scratch_bytes);
+    CUDA_CHECK(cudaMallocAsync(&c.scratch, want, c.stream));
+    c.scratch_bytes = want;
+  }
+  return c.scratch;
+}
+
+// Read a few values back (synchronises the context stream). Small reads go
+// through a pinned staging buffer: a pageable D2H copy costs a staged,
+// synchronous transfer.
+constexpr size_t kPinnedBytes = 1 << 16;
 template <class T>
 inline void to_host(Ctx& c, T* h, const T* d, size_t count) {
   if (!count) return;
-  CUDA_CHECK(cudaMemcpyAsync(h, d, count * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  const size_t bytes = count * sizeof(T);
+  if (bytes <= kPinnedBytes) {
+    if (!c.pinned) {
+      CUDA_CHECK(cudaMallocHost(&c.pinned, kPinnedBytes));
+      c.pinned_bytes = kPinnedBytes;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(c.pinned, d, bytes, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    std::memcpy(h, c.pinned, bytes);
+    return;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c.stream));
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 template <class T>

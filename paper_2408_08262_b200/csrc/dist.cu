@@ -532,27 +532,30 @@ __global__ void k_dtheta(int n, const int32_t* __restrict__ rp, const int32_t* _
                          const int32_t* __restrict__ fsub, double* __restrict__ theta,
                          unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || lab[i] != (double)AIRG_F) return;
-  double off = 0.0, diag = 0.0;
-  bool seen = false;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) {
-    const int32_t lc = ci[k];
-    if (lab[lc] != (double)AIRG_F) continue;
-    if (lc == i) {
-      diag = fabs(v[k]);
-      seen = true;
+  unsigned long long tb = 0;
+  if (i < n && lab[i] == (double)AIRG_F) {
+    double off = 0.0, diag = 0.0;
+    bool seen = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int32_t lc = ci[k];
+      if (lab[lc] != (double)AIRG_F) continue;
+      if (lc == i) {
+        diag = fabs(v[k]);
+        seen = true;
+      } else {
+        off = __dadd_rn(off, fabs(v[k]));
+      }
+    }
+    if (!seen || diag == 0.0) {
+      atomicMin(bad, (unsigned long long)fsub[i]);
+      theta[i] = 0.0;
     } else {
-      off = __dadd_rn(off, fabs(v[k]));
+      const double t = __ddiv_rn(off, diag);
+      theta[i] = t;
+      tb = (unsigned long long)__double_as_longlong(t);
     }
   }
-  if (!seen || diag == 0.0) {
-    atomicMin(bad, (unsigned long long)fsub[i]);
-    theta[i] = 0.0;
-    return;
-  }
-  const double t = __ddiv_rn(off, diag);
-  theta[i] = t;
-  atomicMax(maxbits, (unsigned long long)__double_as_longlong(t));
+  block_max(maxbits, tb);
 }
 __global__ void k_dfsub(int n, const double* __restrict__ lab, const int32_t* __restrict__ pos,
                         int64_t base, int32_t* __restrict__ fsub) {

@@ -69,6 +69,14 @@ struct DdcResult {
 // 1 quickselect (unsupported on GPU), 2 direct.
 DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, double fraction,
               int64_t bins, int selection, double direct_alpha, bool convert);
+// The whole PMISR-DDC split (weight mode 0) in seven sync-free passes over A
+// (cfsplit.cu); labels bit-identical to strength -> pmisr -> extract -> ddc.
+struct CfFused {
+  int64_t s_nnz = 0, n_f_pre = 0, n_converted = 0;
+  double max_theta = 0.0, alpha_diag = 0.0;
+};
+CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
+                       double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre);
 // max theta only (theta_post, air.cpp:355); throws on a zero diagonal
 double dominance_max(Ctx& c, const Csr& aff);
 

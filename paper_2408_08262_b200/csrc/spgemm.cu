@@ -14,16 +14,43 @@ namespace airg {
 
 namespace {
 
-__global__ void spgemm_bound(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
-                             const int32_t* __restrict__ brp, int64_t* __restrict__ ub) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int64_t s = 0;
-  for (int k = arp[i]; k < arp[i + 1]; ++k) {
-    const int j = aci[k];
-    s += brp[j + 1] - brp[j];
+// warp-aggregated append of row i to list `cls` (one atomic per warp and class)
+__device__ __forceinline__ void append_row(int i, int cls, bool live, int32_t* __restrict__ lists,
+                                           int32_t* __restrict__ counts, int64_t stride) {
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned m = __ballot_sync(0xffffffffu, live && cls == k);
+    if (!m) continue;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if ((int)lane == leader) base = atomicAdd(counts + k, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (live && cls == k) lists[k * stride + base + __popc(m & ((1u << lane) - 1))] = i;
   }
-  ub[i] = s;
+}
+
+// products per row (upper bound of the row's length) and the row's class:
+// 0 thread per row (few products or more A entries than the warp prefix
+// holds), 1 warp hash. Lists: [0 | 1 | 2 | 3] x n, counts[4].
+constexpr int kThreadProducts = 32;
+constexpr int kWarpA = 64;
+__global__ void spgemm_bound(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                             const int32_t* __restrict__ brp, int64_t* __restrict__ ub,
+                             int32_t* __restrict__ lists, int32_t* __restrict__ counts, int classify) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  int64_t s = 0;
+  int cls = 0;
+  if (live) {
+    for (int k = arp[i]; k < arp[i + 1]; ++k) {
+      const int j = aci[k];
+      s += brp[j + 1] - brp[j];
+    }
+    ub[i] = s;
+    cls = (s <= kThreadProducts || arp[i + 1] - arp[i] > kWarpA) ? 0 : 1;
+  }
+  if (classify) append_row(i, cls, live, lists, counts, n);
 }
 
 // ---- warp-per-row accumulation with a shared-memory hash table ---------------
@@ -33,38 +60,165 @@ __global__ void spgemm_bound(int n, const int32_t* __restrict__ arp, const int32
 // one in lane order, so every entry still sees its contributions in the
 // reference's order, starting from 0.0. Occupied slots are then compacted,
 // bitonic-sorted by column and written to the row's scratch segment. Rows
-// with more than kWarpA A-entries or kHashCap distinct columns are flagged
-// and left to the thread-per-row kernel below.
-constexpr int kWarpA = 64;
+// with more than kHashCap distinct columns go to the next list (a bigger
+// table, then the thread-per-row kernel). Rows are taken from a device list
+// by a persistent grid (the list length never crosses to the host).
 
-// kHashCap distinct columns per row, kSpgWarps rows per block; `only`
-// (nullable) restricts the kernel to rows flagged by a previous pass.
-template <int kHashCap, int kSpgWarps>
-__global__ void __launch_bounds__(kSpgWarps * 32)
-spgemm_warp_rows(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
-                 const double* __restrict__ av, const int32_t* __restrict__ brp,
-                 const int32_t* __restrict__ bci, const double* __restrict__ bv,
-                 const int64_t* __restrict__ off, int32_t* __restrict__ scol,
-                 double* __restrict__ sval, int32_t* __restrict__ len, int32_t* __restrict__ kept,
-                 int32_t* __restrict__ fallback, double drop_tol, int square_keep_diag,
-                 const int32_t* __restrict__ only) {
-  __shared__ int32_t keys_all[kSpgWarps][kHashCap];
-  __shared__ double vals_all[kSpgWarps][kHashCap];
-  __shared__ int32_t pref_all[kSpgWarps][kWarpA + 1];
-  __shared__ double pbuf_all[kSpgWarps][32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kSpgWarps + w;
-  if (i >= n) return;
-  if (only && !only[i]) return;
-  int32_t* keys = keys_all[w];
-  double* vals = vals_all[w];
-  int32_t* pref = pref_all[w];
-  double* pbuf = pbuf_all[w];
-  const int s = arp[i], na = arp[i + 1] - s;
-  if (na > kWarpA) {
-    if (lane == 0) fallback[i] = 1;
-    return;
+// ---- sorted write-out of a warp's accumulated row ------------------------------
+// The drop rule (sparse.cpp:244-268) on the sorted row: keep the diagonal
+// (square products), else keep unless |v| < tol * rowmax and |v| < rowmax.
+__device__ __forceinline__ void row_counts(int cnt, double drop_tol, int lane, int32_t* __restrict__ len,
+                                           int32_t* __restrict__ kept, int i, int kc_lane) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) kc_lane += __shfl_xor_sync(0xffffffffu, kc_lane, o);
+  if (lane == 0) {
+    len[i] = cnt;
+    kept[i] = drop_tol < 0.0 ? cnt : kc_lane;
   }
+}
+
+// Bitonic sort of the compacted (column, value) pairs in registers: element
+// t = e * 32 + lane; strides >= 32 swap registers, smaller ones exchange with
+// __shfl_xor. Padding keys (INT_MAX) sort last. Replaces the shared-memory
+// sort (the bulk of the warp kernel's instructions) for rows of <= 256.
+template <int E>
+__device__ __forceinline__ void finish_reg(const int32_t* __restrict__ keys, const double* __restrict__ vals,
+                                           int cnt, int lane, int i, int32_t* __restrict__ oc,
+                                           double* __restrict__ ov, double drop_tol, int square_keep_diag,
+                                           int32_t* __restrict__ len, int32_t* __restrict__ kept) {
+  constexpr int S = 32 * E;
+  int k[E];
+  double v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int t = e * 32 + lane;
+    k[e] = t < cnt ? keys[t] : 0x7fffffff;
+    v[e] = t < cnt ? vals[t] : 0.0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int size = 2; size <= S; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int es = stride >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int e2 = e ^ es;
+          if (e2 > e) {
+            const bool asc = ((e * 32 + lane) & size) == 0;
+            if ((k[e] > k[e2]) == asc) {
+              const int tk = k[e];
+              k[e] = k[e2];
+              k[e2] = tk;
+              const double tv = v[e];
+              v[e] = v[e2];
+              v[e2] = tv;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int kp = __shfl_xor_sync(0xffffffffu, k[e], stride);
+          const double vp = __shfl_xor_sync(0xffffffffu, v[e], stride);
+          const bool asc = ((e * 32 + lane) & size) == 0;
+          const bool lower = (lane & stride) == 0;
+          const bool take = (lower == asc) ? (kp < k[e]) : (kp > k[e]);
+          if (take) {
+            k[e] = kp;
+            v[e] = vp;
+          }
+        }
+      }
+    }
+  }
+  double rmax = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int t = e * 32 + lane;
+    if (t < cnt) {
+      oc[t] = k[e];
+      ov[t] = v[e];
+      rmax = fmax(rmax, fabs(v[e]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  int kc = 0;
+  if (drop_tol >= 0.0) {
+    const double thr = __dmul_rn(drop_tol, rmax);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int t = e * 32 + lane;
+      if (t < cnt) {
+        const double mag = fabs(v[e]);
+        const bool diag = square_keep_diag && k[e] == i;
+        kc += diag || !(mag < thr && mag < rmax);
+      }
+    }
+  }
+  row_counts(cnt, drop_tol, lane, len, kept, i, kc);
+}
+
+// rows of more than 256 distinct columns (2048-slot tables): shared-memory sort
+__device__ __forceinline__ void finish_smem(int32_t* __restrict__ keys, double* __restrict__ vals, int cnt,
+                                            int lane, int i, int32_t* __restrict__ oc, double* __restrict__ ov,
+                                            double drop_tol, int square_keep_diag, int32_t* __restrict__ len,
+                                            int32_t* __restrict__ kept) {
+  int S = 1;
+  while (S < cnt) S <<= 1;
+  for (int q = cnt + lane; q < S; q += 32) keys[q] = 0x7fffffff;
+  __syncwarp();
+  for (int size = 2; size <= S; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < S; t += 32) {
+        const int p2 = t ^ stride;
+        if (p2 > t) {
+          const bool asc = (t & size) == 0;
+          const int kt = keys[t], kp = keys[p2];
+          if ((kt > kp) == asc) {
+            keys[t] = kp;
+            keys[p2] = kt;
+            const double vt = vals[t];
+            vals[t] = vals[p2];
+            vals[p2] = vt;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  double rmax = 0.0;
+  for (int q = lane; q < cnt; q += 32) {
+    oc[q] = keys[q];
+    ov[q] = vals[q];
+    rmax = fmax(rmax, fabs(vals[q]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  int kc = 0;
+  if (drop_tol >= 0.0) {
+    const double thr = __dmul_rn(drop_tol, rmax);
+    for (int q = lane; q < cnt; q += 32) {
+      const double mag = fabs(vals[q]);
+      const bool diag = square_keep_diag && keys[q] == i;
+      kc += diag || !(mag < thr && mag < rmax);
+    }
+  }
+  row_counts(cnt, drop_tol, lane, len, kept, i, kc);
+}
+
+template <int kHashCap>
+__device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ keys, double* __restrict__ vals,
+                                         int32_t* __restrict__ pref, double* __restrict__ pbuf,
+                                         const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                         const double* __restrict__ av, const int32_t* __restrict__ brp,
+                                         const int32_t* __restrict__ bci, const double* __restrict__ bv,
+                                         const int64_t* __restrict__ off, int32_t* __restrict__ scol,
+                                         double* __restrict__ sval, int32_t* __restrict__ len,
+                                         int32_t* __restrict__ kept, double drop_tol, int square_keep_diag) {
+  const int s = arp[i], na = arp[i + 1] - s;
+  if (na > kWarpA) return true;
   // prefix of the B-row lengths of this A row (warp scan); empty A rows
   // (e.g. a C point without F neighbours in A_cf) give total = 0
   if (lane == 0) pref[0] = 0;
@@ -139,10 +293,7 @@ spgemm_warp_rows(int n, const int32_t* __restrict__ arp, const int32_t* __restri
       }
     }
     __syncwarp();
-    if (__any_sync(0xffffffffu, overflow)) {
-      if (lane == 0) fallback[i] = 1;
-      return;
-    }
+    if (__any_sync(0xffffffffu, overflow)) return true;
   }
   // compact occupied slots to the front (keys/vals), then bitonic sort by column
   int cnt = 0;
@@ -159,70 +310,56 @@ spgemm_warp_rows(int n, const int32_t* __restrict__ arp, const int32_t* __restri
     __syncwarp();
     cnt += __popc(occ);
   }
-  int S = 1;
-  while (S < cnt) S <<= 1;
-  for (int q = cnt + lane; q < S; q += 32) keys[q] = 0x7fffffff;
-  __syncwarp();
-  for (int size = 2; size <= S; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = lane; t < S; t += 32) {
-        const int p2 = t ^ stride;
-        if (p2 > t) {
-          const bool asc = (t & size) == 0;
-          const int kt = keys[t], kp = keys[p2];
-          if ((kt > kp) == asc) {
-            keys[t] = kp;
-            keys[p2] = kt;
-            const double vt = vals[t];
-            vals[t] = vals[p2];
-            vals[p2] = vt;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  // write the row, drop count (sparse.cpp:244-268 rule)
   int32_t* oc = scol + off[i];
   double* ov = sval + off[i];
-  double rmax = 0.0;
-  for (int q = lane; q < cnt; q += 32) {
-    oc[q] = keys[q];
-    ov[q] = vals[q];
-    rmax = fmax(rmax, fabs(vals[q]));
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-  int kc = 0;
-  if (drop_tol < 0.0) {
-    kc = cnt;
+  if (cnt <= 32) {
+    finish_reg<1>(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
+  } else if (cnt <= 64) {
+    finish_reg<2>(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
+  } else if (cnt <= 128) {
+    finish_reg<4>(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
   } else {
-    const double thr = __dmul_rn(drop_tol, rmax);
-    for (int q = lane; q < cnt; q += 32) {
-      const double mag = fabs(vals[q]);
-      const bool diag = square_keep_diag && keys[q] == i;
-      kc += diag || !(mag < thr && mag < rmax);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
+    finish_smem(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
   }
-  if (lane == 0) {
-    len[i] = cnt;
-    kept[i] = kc;
-    fallback[i] = 0;
+  return false;
+}
+
+// kSpgWarps warps per block, one list row per warp at a time; rows that
+// overflow the table are appended to next_list
+template <int kHashCap, int kSpgWarps>
+__global__ void __launch_bounds__(kSpgWarps * 32, kSpgWarps == 8 ? 7 : 1)
+spgemm_warp_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                 int32_t* __restrict__ next_list, int32_t* __restrict__ next_count,
+                 const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                 const double* __restrict__ av, const int32_t* __restrict__ brp,
+                 const int32_t* __restrict__ bci, const double* __restrict__ bv,
+                 const int64_t* __restrict__ off, int32_t* __restrict__ scol, double* __restrict__ sval,
+                 int32_t* __restrict__ len, int32_t* __restrict__ kept, double drop_tol,
+                 int square_keep_diag) {
+  __shared__ int32_t keys_all[kSpgWarps][kHashCap];
+  __shared__ double vals_all[kSpgWarps][kHashCap];
+  __shared__ int32_t pref_all[kSpgWarps][kWarpA + 1];
+  __shared__ double pbuf_all[kSpgWarps][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nrows = *count;
+  for (int q = blockIdx.x * kSpgWarps + w; q < nrows; q += gridDim.x * kSpgWarps) {
+    const int i = list[q];
+    const bool ovf = warp_row<kHashCap>(i, lane, keys_all[w], vals_all[w], pref_all[w], pbuf_all[w], arp,
+                                        aci, av, brp, bci, bv, off, scol, sval, len, kept, drop_tol,
+                                        square_keep_diag);
+    if (ovf && lane == 0) next_list[atomicAdd(next_count, 1)] = i;
+    __syncwarp();
   }
 }
 
-__global__ void spgemm_accumulate(int n, const int32_t* __restrict__ arp,
-                                  const int32_t* __restrict__ aci, const double* __restrict__ av,
-                                  const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
-                                  const double* __restrict__ bv, const int64_t* __restrict__ off,
-                                  int32_t* __restrict__ scol, double* __restrict__ sval,
-                                  int32_t* __restrict__ len, int32_t* __restrict__ kept,
-                                  double drop_tol, int square_keep_diag,
-                                  const int32_t* __restrict__ only) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (only && !only[i]) return;  // rows the warp kernel already produced
+// thread per row: sorted insertion into the row's scratch segment
+__device__ __forceinline__ void thread_row(int i, const int32_t* __restrict__ arp,
+                                           const int32_t* __restrict__ aci, const double* __restrict__ av,
+                                           const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                           const double* __restrict__ bv, const int64_t* __restrict__ off,
+                                           int32_t* __restrict__ scol, double* __restrict__ sval,
+                                           int32_t* __restrict__ len, int32_t* __restrict__ kept,
+                                           double drop_tol, int square_keep_diag) {
   int32_t* cols = scol + off[i];
   double* vals = sval + off[i];
   int L = 0;
@@ -271,6 +408,20 @@ __global__ void spgemm_accumulate(int n, const int32_t* __restrict__ arp,
   kept[i] = kc;
 }
 
+// rows of `list` (or every row when list == nullptr), grid-stride
+__global__ void spgemm_accumulate(int n, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                                  const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                  const double* __restrict__ av, const int32_t* __restrict__ brp,
+                                  const int32_t* __restrict__ bci, const double* __restrict__ bv,
+                                  const int64_t* __restrict__ off, int32_t* __restrict__ scol,
+                                  double* __restrict__ sval, int32_t* __restrict__ len,
+                                  int32_t* __restrict__ kept, double drop_tol, int square_keep_diag) {
+  const int rows = list ? *count : n;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < rows; q += gridDim.x * blockDim.x)
+    thread_row(list ? list[q] : q, arp, aci, av, brp, bci, bv, off, scol, sval, len, kept, drop_tol,
+               square_keep_diag);
+}
+
 __global__ void spgemm_compact(int n, const int64_t* __restrict__ off,
                                const int32_t* __restrict__ scol, const double* __restrict__ sval,
                                const int32_t* __restrict__ len, const int32_t* __restrict__ orp,
@@ -316,32 +467,39 @@ void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol, bool 
     out = std::move(r);
     return;
   }
-  DBuf<int64_t> ub(c, (size_t)n), off(c, (size_t)n + 1);
-  LAUNCH(c, spgemm_bound, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, b.rp.p, ub.p);
-  const int64_t total = exclusive_scan64(c, ub.p, off.p, n);
-  DBuf<int32_t> scol(c, (size_t)total), len(c, (size_t)n), kept(c, (size_t)n);
-  DBuf<double> sval(c, (size_t)total);
-  const int sq = (keep_diag && a.n == b.m) ? 1 : 0;
   static const bool thread_only = [] {
     const char* e = getenv("AIRG_SPGEMM");
     return e && !strcmp(e, "thread");
   }();
+  DBuf<int64_t> ub(c, (size_t)n), off(c, (size_t)n + 1);
+  DBuf<int32_t> lists(c, thread_only ? 1 : 4 * (size_t)n), counts(c, 4);
+  counts.zero(c);
+  LAUNCH(c, spgemm_bound, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, b.rp.p, ub.p, lists.p, counts.p,
+         thread_only ? 0 : 1);
+  const int64_t total = exclusive_scan64(c, ub.p, off.p, n);
+  DBuf<int32_t> scol(c, (size_t)total), len(c, (size_t)n), kept(c, (size_t)n);
+  DBuf<double> sval(c, (size_t)total);
+  const int sq = (keep_diag && a.n == b.m) ? 1 : 0;
+  const unsigned tgrid = (unsigned)std::min<int64_t>(blocks_for(n, 128), 16 * c.num_sms);
   if (thread_only) {
-    LAUNCH(c, spgemm_accumulate, blocks_for(n, 128), 128, 0, n, a.rp.p, a.ci.p, a.v.p, b.rp.p,
-           b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, (const int32_t*)nullptr);
+    LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)nullptr, (const int32_t*)nullptr,
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
   } else {
-    // 256-slot tables, 8 rows per block; overflowing rows retry with
-    // 2048-slot tables (one row per block), then the thread-per-row kernel
-    DBuf<int32_t> fb(c, (size_t)n), fb2(c, (size_t)n);
-    fb.zero(c);
-    fb2.zero(c);
-    LAUNCH(c, (spgemm_warp_rows<256, 8>), (n + 7) / 8, 256, 0, n, a.rp.p, a.ci.p, a.v.p, b.rp.p,
-           b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, fb.p, drop_tol, sq,
-           (const int32_t*)nullptr);
-    LAUNCH(c, (spgemm_warp_rows<2048, 1>), n, 32, 0, n, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
-           off.p, scol.p, sval.p, len.p, kept.p, fb2.p, drop_tol, sq, (const int32_t*)fb.p);
-    LAUNCH(c, spgemm_accumulate, blocks_for(n, 128), 128, 0, n, a.rp.p, a.ci.p, a.v.p, b.rp.p,
-           b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, (const int32_t*)fb2.p);
+    // list 0: few products -> thread per row; list 1: warp + 256-slot table,
+    // overflow -> list 2: one warp per block + 2048-slot table, overflow ->
+    // list 3: thread per row. Persistent grids read the list lengths on device.
+    const int64_t N = n;
+    LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)lists.p, (const int32_t*)counts.p,
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+    LAUNCH(c, (spgemm_warp_list<256, 8>), (unsigned)std::min<int64_t>((N + 7) / 8, 8 * c.num_sms), 256, 0,
+           (const int32_t*)(lists.p + N), (const int32_t*)(counts.p + 1), lists.p + 2 * N, counts.p + 2,
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+    LAUNCH(c, (spgemm_warp_list<2048, 1>), (unsigned)std::min<int64_t>(N, 8 * c.num_sms), 32, 0,
+           (const int32_t*)(lists.p + 2 * N), (const int32_t*)(counts.p + 2), lists.p + 3 * N, counts.p + 3,
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+    LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)(lists.p + 3 * N),
+           (const int32_t*)(counts.p + 3), a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p,
+           sval.p, len.p, kept.p, drop_tol, sq);
   }
   const int64_t nnz = exclusive_scan(c, kept.p, r.rp.p, n);
   r.nnz = nnz;
