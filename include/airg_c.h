@@ -302,6 +302,21 @@ int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
                          int32_t* triggered, int64_t* halo_entries,
                          int64_t* h_starts /* P+1, nullable */);
 int airg_dist_destroy(airg_dist* d);
+/* ---- Matrix Market exchange (matrix_market.hpp:11-19) ---------------------
+ * Host-side, no GPU needed. airg_mm_read parses a "coordinate real general"
+ * file (1-based, duplicates summed as SparseMatrix::from_triplets,
+ * sparse.cpp:48-80); the result is read out with airg_mm_dims/airg_mm_copy
+ * (int64 CSR, the reference layout) and released with airg_mm_free.
+ * airg_mm_write writes the reference's format ("%.17g" values). Errors are
+ * AIRG_ERUNTIME with the reference's "matrix market: <path>: ..." text. */
+typedef struct airg_mm airg_mm;
+int airg_mm_read(const char* path, airg_mm** out);
+int airg_mm_dims(const airg_mm* h, int64_t* nrows, int64_t* ncols, int64_t* nnz);
+int airg_mm_copy(const airg_mm* h, int64_t* row_offsets, int64_t* col_indices, double* values);
+int airg_mm_free(airg_mm* h);
+int airg_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_offsets,
+                  const int64_t* col_indices, const double* values);
+
 /* The PMISR-DDC CF split (air.cpp:466-494) of a slab-partitioned operator:
  * strength on own rows, |S^T| by a reverse halo sum, global-row-index
  * weights, one forward halo exchange of weights, "not minimal" marks of

@@ -17,6 +17,7 @@
 #include "airgraph/air.hpp"
 #include "airgraph/coarsening.hpp"
 #include "airgraph/gmres_poly.hpp"
+#include "airgraph/matrix_market.hpp"
 #include "airgraph/partition_model.hpp"
 #include "airgraph/solve.hpp"
 #include "airgraph/sparse.hpp"
@@ -146,6 +147,13 @@ int ref_mat_copy(const void* h, int64_t* rp, int64_t* ci, double* v) {
 int ref_mat_free(void* h) {
   delete static_cast<SparseMatrix*>(h);
   return AIRG_OK;
+}
+// matrix_market.hpp:11-19 (read / write a coordinate real general file)
+int ref_mm_read(const char* path, void** out) {
+  return guard([&] { *out = new SparseMatrix(read_matrix_market(path)); });
+}
+int ref_mm_write(const void* h, const char* path) {
+  return guard([&] { write_matrix_market(*static_cast<const SparseMatrix*>(h), path); });
 }
 
 // ---- L0 -------------------------------------------------------------------

@@ -163,6 +163,80 @@ class Mat:
 class RefLib(_Lib):
     prefix = "ref_"
 
+    # matrix_market.hpp:11-19 (reference build only). The reference's reader
+    # crashes inside a process that has imported numpy (a C++ runtime clash
+    # around std::filesystem / iostreams in this image), so both calls run in
+    # a numpy-free child interpreter that exchanges raw arrays through files.
+    _MM_CHILD = r"""
+import ctypes as C, struct, sys
+L = C.CDLL(sys.argv[1])
+op, path, blob = sys.argv[2], sys.argv[3], sys.argv[4]
+buf = C.create_string_buffer(4096)
+def chk(rc):
+    if rc:
+        L.ref_last_error(buf, 4096)
+        sys.stderr.write(buf.value.decode()); sys.exit(3)
+h = C.c_void_p()
+if op == "read":
+    L.ref_mm_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    chk(L.ref_mm_read(path.encode(), C.byref(h)))
+    n, m, z = C.c_int64(), C.c_int64(), C.c_int64()
+    L.ref_mat_dims(h, C.byref(n), C.byref(m), C.byref(z))
+    rp = (C.c_int64 * (n.value + 1))(); ci = (C.c_int64 * max(z.value, 1))(); v = (C.c_double * max(z.value, 1))()
+    L.ref_mat_copy(h, rp, ci, v)
+    with open(blob, "wb") as f:
+        f.write(struct.pack("<3q", n.value, m.value, z.value))
+        f.write(bytes(rp)); f.write(bytes(ci)[: 8 * z.value]); f.write(bytes(v)[: 8 * z.value])
+else:
+    with open(blob, "rb") as f:
+        n, m, z = struct.unpack("<3q", f.read(24))
+        rp = (C.c_int64 * (n + 1)).from_buffer_copy(f.read(8 * (n + 1)))
+        ci = (C.c_int64 * max(z, 1)).from_buffer_copy(f.read(8 * z).ljust(8, b"\0"))
+        v = (C.c_double * max(z, 1)).from_buffer_copy(f.read(8 * z).ljust(8, b"\0"))
+    L.ref_mat_new.argtypes = [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+    chk(L.ref_mat_new(n, m, rp, ci, v, C.byref(h)))
+    L.ref_mm_write.argtypes = [C.c_void_p, C.c_char_p]
+    chk(L.ref_mm_write(h, path.encode()))
+"""
+
+    def _mm_child(self, op, path, blob):
+        import sys as _sys
+        r = subprocess.run([_sys.executable, "-c", self._MM_CHILD, self.path, op, str(path), str(blob)],
+                           capture_output=True, text=True)
+        if r.returncode == 3:
+            raise OracleError(r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"reference matrix-market child failed: {r.stderr[-500:]}")
+
+    def mm_read(self, path: str):
+        """-> (nrows, ncols, row_offsets, col_indices, values)"""
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            blob = os.path.join(d, "m.bin")
+            self._mm_child("read", path, blob)
+            raw = open(blob, "rb").read()
+        n, m, z = np.frombuffer(raw[:24], np.int64)
+        o = 24
+        rp = np.frombuffer(raw[o:o + 8 * (n + 1)], np.int64).copy()
+        o += 8 * (n + 1)
+        ci = np.frombuffer(raw[o:o + 8 * z], np.int64).copy()
+        o += 8 * z
+        v = np.frombuffer(raw[o:o + 8 * z], np.float64).copy()
+        return int(n), int(m), rp, ci, v
+
+    def mm_write(self, a: Mat, path: str) -> None:
+        import tempfile
+        n, m, z = a.dims()
+        rp, ci, v = a.arrays()
+        with tempfile.TemporaryDirectory() as d:
+            blob = os.path.join(d, "m.bin")
+            with open(blob, "wb") as f:
+                f.write(np.array([n, m, z], np.int64).tobytes())
+                f.write(rp.tobytes())
+                f.write(ci.tobytes())
+                f.write(v.tobytes())
+            self._mm_child("write", path, blob)
+
 
 class PortLib(_Lib):
     prefix = "orc_"

@@ -105,6 +105,11 @@ def lib() -> C.CDLL:
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
                                       _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
             "airg_dist_destroy": ([_VP], C.c_int),
+            "airg_mm_read": ([C.c_char_p, _P(_VP)], C.c_int),
+            "airg_mm_dims": ([_VP, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
+            "airg_mm_copy": ([_VP, _VP, _VP, _VP], C.c_int),
+            "airg_mm_free": ([_VP], C.c_int),
+            "airg_mm_write": ([C.c_char_p, C.c_int64, C.c_int64, _VP, _VP, _VP], C.c_int),
             "airg_dist_cf_split": ([_VP, _VP, C.c_int32, C.c_int32, _VP, _VP, C.c_double, C.c_int64,
                                     C.c_uint64, C.c_int32, C.c_double, C.c_int64, _VP,
                                     _P(abi.CfReport)], C.c_int),
@@ -613,6 +618,35 @@ def gmres_solve(h: Hierarchy, b, restart: int = 30, **solve_kw) -> SolveResult:
     """Right-preconditioned restarted GMRES with one AIRG V-cycle per
     iteration (BASELINE config 0's outer solver)."""
     return richardson_solve(h, b, outer=1, gmres_restart=restart, **solve_kw)
+
+
+# ---- Matrix Market exchange (matrix_market.hpp:11-19) ----------------------------
+def read_matrix_market(path) -> SparseMatrix:
+    """airgraph::read_matrix_market: coordinate real general, duplicates summed
+    exactly as the reference does (host code in the library; no GPU)."""
+    h = _VP()
+    _check(lib().airg_mm_read(os.fsencode(str(path)), C.byref(h)))
+    try:
+        n, m, z = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().airg_mm_dims(h, C.byref(n), C.byref(m), C.byref(z)))
+        rp = np.zeros(n.value + 1, np.int64)
+        ci = np.zeros(max(z.value, 1), np.int64)
+        v = np.zeros(max(z.value, 1), np.float64)
+        _check(lib().airg_mm_copy(h, rp.ctypes.data, ci.ctypes.data, v.ctypes.data))
+    finally:
+        lib().airg_mm_free(h)
+    return SparseMatrix(n.value, m.value, rp, ci[: z.value].copy(), v[: z.value].copy())
+
+
+def write_matrix_market(a, path) -> None:
+    """airgraph::write_matrix_market ("%.17g" values: exact round trip)."""
+    if isinstance(a, DeviceCSR):
+        a = a.download()
+    rp = np.ascontiguousarray(a.row_offsets, np.int64)
+    ci = np.ascontiguousarray(a.col_indices, np.int64)
+    v = np.ascontiguousarray(a.values, np.float64)
+    _check(lib().airg_mm_write(os.fsencode(str(path)), int(a.nrows), int(a.ncols), rp.ctypes.data,
+                               ci.ctypes.data, v.ctypes.data))
 
 
 # ---- multi-GPU: row-slab distributed solve (SURVEY §8e) ---------------------------

@@ -5,6 +5,7 @@
 #include <memory>
 
 #include "dist.cuh"
+#include "mmio.cuh"
 
 using namespace airg;
 
@@ -762,6 +763,53 @@ int airg_dist_cf_split(airg_ctx* ctx, const airg_csr* a, int32_t nranks, int32_t
       rep->alpha_diag = r.alpha_diag;
       rep->s_nnz = r.s_nnz;
     }
+  });
+}
+
+struct airg_mm {
+  MmHost m;
+};
+
+int airg_mm_read(const char* path, airg_mm** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "output handle");
+    auto h = std::make_unique<airg_mm>();
+    mm_read(path, h->m);
+    *out = h.release();
+  });
+}
+
+int airg_mm_dims(const airg_mm* h, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+  return guard([&] {
+    need(h, "matrix market handle");
+    if (nrows) *nrows = h->m.n;
+    if (ncols) *ncols = h->m.m;
+    if (nnz) *nnz = (int64_t)h->m.ci.size();
+  });
+}
+
+int airg_mm_copy(const airg_mm* h, int64_t* rp, int64_t* ci, double* v) {
+  return guard([&] {
+    need(h, "matrix market handle");
+    if (rp) std::memcpy(rp, h->m.rp.data(), sizeof(int64_t) * h->m.rp.size());
+    if (ci && !h->m.ci.empty()) std::memcpy(ci, h->m.ci.data(), sizeof(int64_t) * h->m.ci.size());
+    if (v && !h->m.v.empty()) std::memcpy(v, h->m.v.data(), sizeof(double) * h->m.v.size());
+  });
+}
+
+int airg_mm_free(airg_mm* h) {
+  delete h;
+  return AIRG_OK;
+}
+
+int airg_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* rp, const int64_t* ci,
+                  const double* v) {
+  return guard([&] {
+    need(path, "path");
+    if (nrows < 0 || ncols < 0) throw InvalidArgument("matrix market: negative dimensions");
+    if (nrows > 0) need(rp, "row offsets");
+    mm_write(path, nrows, ncols, rp, ci, v);
   });
 }
 

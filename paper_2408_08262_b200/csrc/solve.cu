@@ -248,21 +248,35 @@ __global__ void k_xupdate(int64_t n, int j, const double* __restrict__ Z, const 
 
 constexpr int kT = 128;
 
-// First fine level handled by the coarse-tail kernel (tail.cuh): the first
-// level with at most AIRG_TAIL_N rows. Off by default: on the C2 hierarchy a
-// barrier-separated phase costs ~6 us against ~3.5 us for a PDL-chained
-// kernel (profiles/r1_tail_ab.txt), so the per-phase kernels stay faster.
-int tail_start(const Hier& h, const airg_solve_config& cfg) {
-  static const int64_t tail_n = [] {
-    const char* e = getenv("AIRG_TAIL_N");
-    return e ? (int64_t)atoll(e) : (int64_t)0;
+// Coarse-tail kernels (tail.cuh). AIRG_TAIL=cluster runs the levels with at
+// most AIRG_TAIL_N rows (and the coarse grid) on one 16-CTA cluster;
+// AIRG_TAIL=grid on the whole GPU with a software grid barrier (measured
+// slower than PDL-chained kernels: profiles/r1_tail_ab.txt).
+struct TailCfg {
+  int mode = 0;  // 0 off, 1 cluster, 2 grid
+  int64_t rows = 0;
+};
+const TailCfg& tail_cfg() {
+  static const TailCfg v = [] {
+    TailCfg t;
+    const char* m = getenv("AIRG_TAIL");
+    const char* n = getenv("AIRG_TAIL_N");
+    t.mode = m && !strcmp(m, "grid") ? 2 : 1;
+    t.rows = n ? (int64_t)atoll(n) : (t.mode == 1 ? 0 : 0);
+    if (t.rows <= 0) t.mode = 0;
+    return t;
   }();
+  return v;
+}
+
+int tail_start(const Hier& h, const airg_solve_config& cfg) {
+  const TailCfg& tc = tail_cfg();
   const int L = (int)h.levels.size();
-  if (tail_n <= 0 || L == 0 || cfg.coarse_iterations <= 0 || h.coarse_a.n == 0) return L;
+  if (tc.mode == 0 || L == 0 || cfg.coarse_iterations <= 0 || h.coarse_a.n == 0) return L;
   // phases: R + prolong + 2 per F-smooth per level, 2 per coarse iteration
   const int64_t per_level = 2 + 2 * std::max<int64_t>(cfg.up_f_smooths, 0);
   for (int l = 0; l < L; ++l)
-    if (h.levels[l].a.n <= tail_n && (L - l) * per_level + 2 * cfg.coarse_iterations <= kMaxTailPhases)
+    if (h.levels[l].a.n <= tc.rows && (L - l) * per_level + 2 * cfg.coarse_iterations <= kMaxTailPhases)
       return l;
   return L;
 }
@@ -348,6 +362,38 @@ void enqueue_tail(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* b
   table.nph = (int)ph.size();
   std::copy(ph.begin(), ph.end(), table.ph);
   if (!h.tail_bar.p) throw RuntimeError("tail kernel: barrier words not allocated");
+  if (tail_cfg().mode == 1) {
+    static const int csize = [] {
+      CUDA_CHECK(cudaFuncSetAttribute(k_tail_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(kTailThreads);
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 16;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int mx = 0;
+      CUDA_CHECK(cudaOccupancyMaxPotentialClusterSize(&mx, k_tail_cluster, &q));
+      return std::max(1, std::min(16, mx));
+    }();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)csize);
+    lc.blockDim = dim3(kTailThreads);
+    lc.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    c.launches++;
+    CUDA_CHECK(cudaLaunchKernelEx(&lc, k_tail_cluster, table));
+    return;
+  }
   static int per_sm = [] {
     int nb = 0;
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tail, kTailThreads, 0));

@@ -12,9 +12,15 @@
 // so the result is bit-identical to the kernel-per-phase V-cycle.
 //
 // Vectors written by an earlier phase of the same launch are read with
-// ordinary (coherent) loads; only the matrices go through the read-only
-// path.
+// L2-coherent loads (ld.global.cg, never a stale L1 line); only the matrices
+// go through the read-only path.
+//
+// Two barriers: k_tail spans the whole GPU with a software grid barrier
+// (cooperative launch); k_tail_cluster runs the small levels on ONE thread-
+// block cluster (up to 16 SMs) with the hardware cluster barrier.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "rowdot.cuh"
 
@@ -86,7 +92,7 @@ __device__ __forceinline__ double tail_dot(int s, int e, const int32_t* __restri
       a[j] = k0 + j < e ? __ldg(v + k0 + j) : 0.0;
     }
 #pragma unroll
-    for (int j = 0; j < kRowBatch; ++j) xv[j] = (k0 + j < e) ? x[c[j]] : 0.0;
+    for (int j = 0; j < kRowBatch; ++j) xv[j] = (k0 + j < e) ? __ldcg(x + c[j]) : 0.0;
 #pragma unroll
     for (int j = 0; j < kRowBatch; ++j)
       if (k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(a[j], xv[j]));
@@ -108,7 +114,7 @@ __device__ __forceinline__ void tail_dot_fc(int s, int e, const int32_t* __restr
       a[j] = k0 + j < e ? __ldg(v + k0 + j) : 0.0;
     }
 #pragma unroll
-    for (int j = 0; j < kRowBatch; ++j) xv[j] = (k0 + j < e) ? x[c[j] & 0x7fffffff] : 0.0;
+    for (int j = 0; j < kRowBatch; ++j) xv[j] = (k0 + j < e) ? __ldcg(x + (c[j] & 0x7fffffff)) : 0.0;
 #pragma unroll
     for (int j = 0; j < kRowBatch; ++j) {
       if (k0 + j < e) {
@@ -126,7 +132,7 @@ __device__ __forceinline__ void tail_row(const TailPhase& P, int i) {
   switch (P.kind) {
     case kTailProlong: {
       const int j = __ldg(P.idx + i);
-      const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, P.x[j])) : 0.0;
+      const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, __ldcg(P.x + j))) : 0.0;
       P.out[i] = __dadd_rn(0.0, __dmul_rn(1.0, pe));
       return;
     }
@@ -134,7 +140,7 @@ __device__ __forceinline__ void tail_row(const TailPhase& P, int i) {
       double sf, sc;
       tail_dot_fc(__ldg(P.rp + i), __ldg(P.rp + i + 1), P.ci, P.v, P.x, sf, sc);
       P.out2[i] = sc;
-      P.out[i] = __dsub_rn(__dsub_rn(P.b[__ldg(P.idx + i)], sf), sc);
+      P.out[i] = __dsub_rn(__dsub_rn(__ldcg(P.b + __ldg(P.idx + i)), sf), sc);
       return;
     }
     default:
@@ -146,19 +152,19 @@ __device__ __forceinline__ void tail_row(const TailPhase& P, int i) {
       P.out[i] = acc;
       break;
     case kTailCres:
-      P.out[i] = __dsub_rn(P.b[i], acc);
+      P.out[i] = __dsub_rn(__ldcg(P.b + i), acc);
       break;
     case kTailCupd: {
-      const double e0 = P.first ? 0.0 : P.out[i];
+      const double e0 = P.first ? 0.0 : __ldcg(P.out + i);
       P.out[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
       break;
     }
     case kTailFres2:
-      P.out[i] = __dsub_rn(__dsub_rn(P.b[__ldg(P.idx + i)], acc), P.in2[i]);
+      P.out[i] = __dsub_rn(__dsub_rn(__ldcg(P.b + __ldg(P.idx + i)), acc), __ldcg(P.in2 + i));
       break;
     case kTailFupd: {
       const int r = __ldg(P.idx + i);
-      P.out[r] = __dadd_rn(P.out[r], acc);
+      P.out[r] = __dadd_rn(__ldcg(P.out + r), acc);
       break;
     }
     default:
@@ -183,6 +189,22 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const __grid_constant__ T
     const TailPhase& P = t.ph[p];
     for (int i = tid; i < P.n; i += nthreads) tail_row(P, i);
     if (p + 1 < nph) tail_grid_barrier(bar, gridDim.x);
+  }
+}
+
+// One cluster of CTAs walks the phase list; rows are spread over the
+// cluster's threads and consecutive phases are separated by the hardware
+// cluster barrier (release / acquire at cluster scope).
+__global__ void __launch_bounds__(kTailThreads) k_tail_cluster(const __grid_constant__ TailTable t) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int nthreads = (int)cl.num_blocks() * blockDim.x;
+  const int tid = (int)cl.block_rank() * blockDim.x + threadIdx.x;
+  const int nph = t.nph;
+  for (int p = 0; p < nph; ++p) {
+    const TailPhase& P = t.ph[p];
+    for (int i = tid; i < P.n; i += nthreads) tail_row(P, i);
+    if (p + 1 < nph) cl.sync();
   }
 }
 

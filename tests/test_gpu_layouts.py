@@ -40,13 +40,16 @@ LAYOUTS = {
     "sell": {"AIRG_LAYOUT": "sell"},
     "nopdl": {"AIRG_PDL": "0"},
     "tail_off": {"AIRG_TAIL_N": "0"},
-    "tail_all": {"AIRG_TAIL_N": "100000000"},
+    "tail_cluster_all": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "100000000"},
+    "tail_cluster_small": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "2000"},
+    "tail_grid_all": {"AIRG_TAIL": "grid", "AIRG_TAIL_N": "100000000"},
 }
 
 
 def _run(env_extra):
     env = dict(os.environ)
-    for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N"):
+    for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N", "AIRG_TAIL",
+              "AIRG_DEVLOOP"):
         env.pop(k, None)
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
