@@ -247,6 +247,16 @@ int airg_poly_assemble(airg_ctx* ctx, const airg_csr* a, const double* h_coeffs,
 /* setup (air.cpp:285-410). inj may be NULL (native coefficients). */
 int airg_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
                const airg_injection* inj, airg_hier** out);
+/* setup at N GPUs (SURVEY §8e setup collectives): every heavy row kernel of
+ * the setup (the CF split, the SpGEMMs of Z, A P and R (A P), the polynomial
+ * assembly, the power-basis and growth SpMVs) runs on one row slab per rank
+ * and the slabs are all-gathered over NCCL; every rank ends with the same
+ * hierarchy, bit-identical to airg_setup's (also in native mode). rank = -1
+ * emulates all ranks in this process; rank >= 0 needs a communicator and the
+ * same (replicated) input on every rank. Feed the result to airg_dist_create. */
+int airg_dist_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
+                    const airg_injection* inj, int32_t nranks, int32_t rank, void* nccl_comm,
+                    airg_hier** out);
 int airg_hier_info_get(const airg_hier* h, airg_hier_info* info);
 int airg_hier_level_info(const airg_hier* h, int64_t level,
                          airg_level_info* info);

@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
             "airg_poly_coefficients": ([_VP, _VP, C.c_int64, C.c_uint64, _VP, _P(C.c_int64)], C.c_int),
             "airg_poly_assemble": ([_VP, _VP, _VP, C.c_int64, C.c_int64, C.c_int64, _P(_VP)], C.c_int),
             "airg_setup": ([_VP, _VP, _P(abi.SetupConfig), _P(abi.Injection), _P(_VP)], C.c_int),
+            "airg_dist_setup": ([_VP, _VP, _P(abi.SetupConfig), _P(abi.Injection), C.c_int32, C.c_int32, _VP,
+                                 _P(_VP)], C.c_int),
             "airg_hier_info_get": ([_VP, _P(abi.HierInfo)], C.c_int),
             "airg_hier_level_info": ([_VP, C.c_int64, _P(abi.LevelInfo)], C.c_int),
             "airg_hier_matrix": ([_VP, C.c_int64, C.c_int32, _P(_VP)], C.c_int),
@@ -561,11 +563,14 @@ class Hierarchy:
         return st, hist[: min(history_cap, st.history_len)]
 
 
-def setup(a, injection: dict | None = None, ctx: Context | None = None, **cfg_kw) -> Hierarchy:
+def setup(a, injection: dict | None = None, ctx: Context | None = None, nranks: int = 0, rank: int = -1,
+          comm: "NcclComm | None" = None, **cfg_kw) -> Hierarchy:
     """airgraph::setup (air.cpp:285-410) on the GPU. `injection` (optional)
     = {"levels": [(coeffs, eff), ...], "coarse": (coeffs, eff)} takes the
     polynomial coefficients from the reference (coefficient-injection parity
-    mode)."""
+    mode). nranks > 0: the setup's row work split over that
+    many ranks (airg_dist_setup; rank = -1 emulates them all, rank >= 0 with
+    a communicator is one rank of a torchrun job)."""
     ctx = ctx or default_context()
     d = _dev(a, ctx)
     cfg = abi.setup_config(**cfg_kw)
@@ -587,7 +592,11 @@ def setup(a, injection: dict | None = None, ctx: Context | None = None, **cfg_kw
                             int(injection["coarse"][1]))
         inj_p = C.byref(inj)
     out = _VP()
-    _check(lib().airg_setup(ctx.h, d.h, C.byref(cfg), inj_p, C.byref(out)))
+    if nranks > 0:
+        _check(lib().airg_dist_setup(ctx.h, d.h, C.byref(cfg), inj_p, int(nranks), int(rank),
+                                     comm.h if comm else None, C.byref(out)))
+    else:
+        _check(lib().airg_setup(ctx.h, d.h, C.byref(cfg), inj_p, C.byref(out)))
     del keep
     return Hierarchy(ctx, out, d.dims()[0])
 

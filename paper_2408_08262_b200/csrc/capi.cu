@@ -6,6 +6,7 @@
 
 #include "dist.cuh"
 #include "mmio.cuh"
+#include "rowsplit.cuh"
 
 using namespace airg;
 
@@ -460,8 +461,9 @@ int airg_poly_assemble(airg_ctx* ctx, const airg_csr* a, const double* coeffs, i
 }
 
 // ---- setup --------------------------------------------------------------------------
-int airg_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
-               const airg_injection* inj, airg_hier** out) {
+namespace {
+int setup_impl(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg, const airg_injection* inj,
+               airg_hier** out, const RowSplit* rs) {
   return guard([&] {
     need(ctx, "context");
     need(a, "matrix");
@@ -482,9 +484,33 @@ int airg_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
       in->coarse_coeffs.assign(inj->coarse_coeffs, inj->coarse_coeffs + cfg->coarse_poly_order + 1);
       in->coarse_eff = inj->coarse_eff_order;
     }
-    setup(ctx->c, a->m, *cfg, in.get(), h->h);
+    setup(ctx->c, a->m, *cfg, in.get(), h->h, rs);
     *out = h.release();
   });
+}
+}  // namespace
+
+int airg_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
+               const airg_injection* inj, airg_hier** out) {
+  return setup_impl(ctx, a, cfg, inj, out, nullptr);
+}
+
+int airg_dist_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* cfg,
+                    const airg_injection* inj, int32_t nranks, int32_t rank, void* nccl_comm,
+                    airg_hier** out) {
+  if (nranks < 1 || rank >= nranks) {
+    g_err = "dist_setup: rank out of range";
+    return AIRG_EINVAL;
+  }
+  if (rank >= 0 && nranks > 1 && !nccl_comm) {
+    g_err = "dist_setup: a communicator is needed per rank";
+    return AIRG_EINVAL;
+  }
+  RowSplit rs;
+  rs.P = nranks;
+  rs.me = rank;
+  rs.comm = (ncclComm_t)nccl_comm;
+  return setup_impl(ctx, a, cfg, inj, out, &rs);
 }
 
 int airg_hier_info_get(const airg_hier* hp, airg_hier_info* info) {

@@ -38,10 +38,11 @@ __device__ __forceinline__ uint64_t mix(uint64_t seed, uint64_t key) {
 
 __global__ void strength_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                const double* __restrict__ v, double alpha,
-                               int32_t* __restrict__ s_cnt, int32_t* __restrict__ st_cnt) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int s = rp[i], e = rp[i + 1];
+                               int32_t* __restrict__ s_cnt, int32_t* __restrict__ st_cnt, int row_base) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = row_base + r;  // global row (rows of a slab carry global columns)
+  const int s = rp[r], e = rp[r + 1];
   double off_max = 0.0;
   for (int k = s; k < e; ++k)
     if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
@@ -55,20 +56,21 @@ __global__ void strength_count(int n, const int32_t* __restrict__ rp, const int3
       atomicAdd(st_cnt + c, 1);
     }
   }
-  s_cnt[i] = cnt;
+  s_cnt[r] = cnt;
 }
 
 __global__ void strength_fill(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                               const double* __restrict__ v, double alpha,
-                              const int32_t* __restrict__ srp, int32_t* __restrict__ sci) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int s = rp[i], e = rp[i + 1];
+                              const int32_t* __restrict__ srp, int32_t* __restrict__ sci, int row_base) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = row_base + r;
+  const int s = rp[r], e = rp[r + 1];
   double off_max = 0.0;
   for (int k = s; k < e; ++k)
     if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
   const double thr = __dmul_rn(alpha, off_max);
-  int o = srp[i];
+  int o = srp[r];
   for (int k = s; k < e; ++k) {
     const double mag = fabs(v[k]);
     const int c = ci[k];
@@ -162,15 +164,18 @@ __global__ void label_fill(int n, const uint8_t* __restrict__ label, const int32
 }
 
 // ---- extract_blocks (sparse.cpp:292-340)
+// Row slabs: local row r is global row rb + r; its F (C) sub-index is offset
+// by fb (cb), the number of F (C) points before the slab. Whole matrix: 0s.
 __global__ void blocks_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                              const uint8_t* __restrict__ label, const int32_t* __restrict__ f2s,
                              int32_t* __restrict__ ff, int32_t* __restrict__ fc,
-                             int32_t* __restrict__ cf, int32_t* __restrict__ af) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                             int32_t* __restrict__ cf, int32_t* __restrict__ af, int rb, int fb, int cb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
   int nF = 0, nC = 0;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) (label[ci[k]] == AIRG_F ? nF : nC)++;
-  const int sub = f2s[i];
+  for (int k = rp[r]; k < rp[r + 1]; ++k) (label[ci[k]] == AIRG_F ? nF : nC)++;
+  const int sub = f2s[i] - (label[i] == AIRG_F ? fb : cb);
   if (label[i] == AIRG_F) {
     ff[sub] = nF;
     fc[sub] = nC;
@@ -187,14 +192,15 @@ __global__ void blocks_fill(int n, const int32_t* __restrict__ rp, const int32_t
                             double* __restrict__ fcv, const int32_t* __restrict__ cfrp,
                             int32_t* __restrict__ cfci, double* __restrict__ cfv,
                             const int32_t* __restrict__ afrp, int32_t* __restrict__ afci,
-                            double* __restrict__ afv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int sub = f2s[i];
+                            double* __restrict__ afv, int rb, int fb, int cb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
+  const int sub = f2s[i] - (label[i] == AIRG_F ? fb : cb);
   if (label[i] == AIRG_F) {
     int of = ffrp[sub], oc = fcrp[sub];
     int oa = afci ? afrp[sub] : 0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
       const int j = ci[k];
       const bool jf = label[j] == AIRG_F;
       if (jf) {
@@ -211,7 +217,7 @@ __global__ void blocks_fill(int n, const int32_t* __restrict__ rp, const int32_t
     }
   } else {
     int o = cfrp[sub];
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
       const int j = ci[k];
       if (label[j] == AIRG_F) {
         cfci[o] = f2s[j];
@@ -225,14 +231,14 @@ __global__ void blocks_fill(int n, const int32_t* __restrict__ rp, const int32_t
 __global__ void theta_rows(int nf, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                            const double* __restrict__ v, double* __restrict__ theta,
                            unsigned long long* __restrict__ maxbits,
-                           unsigned long long* __restrict__ bad_row) {
+                           unsigned long long* __restrict__ bad_row, int rb) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long tb = 0;
   if (i < nf) {
     double off = 0.0, diag = 0.0;
     bool seen = false;
     for (int k = rp[i]; k < rp[i + 1]; ++k) {
-      if (ci[k] == i) {
+      if (ci[k] == rb + i) {
         diag = fabs(v[k]);
         seen = true;
       } else {
@@ -412,21 +418,21 @@ __global__ void ddc_convert(int nf, const double* __restrict__ theta, const doub
 
 }  // namespace
 
-void strength(Ctx& c, const Csr& a, double alpha, Strength& g) {
-  if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
+void strength(Ctx& c, const Csr& a, double alpha, Strength& g, int row_base) {
+  if (row_base == 0 && a.n != a.m) throw InvalidArgument("strength: matrix must be square");
   g.n = a.n;
   DBuf<int32_t> s_cnt(c, (size_t)a.n);
-  g.st_cnt.alloc(c, (size_t)a.n);
+  g.st_cnt.alloc(c, (size_t)std::max(a.n, a.m));
   g.st_cnt.zero(c);
   g.rp.alloc(c, (size_t)a.n + 1);
   if (a.n)
     LAUNCH(c, strength_count, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, alpha,
-           s_cnt.p, g.st_cnt.p);
+           s_cnt.p, g.st_cnt.p, row_base);
   g.nnz = exclusive_scan(c, s_cnt.p, g.rp.p, a.n);
   g.ci.alloc(c, (size_t)g.nnz);
   if (a.n)
     LAUNCH(c, strength_fill, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, alpha,
-           g.rp.p, g.ci.p);
+           g.rp.p, g.ci.p, row_base);
 }
 
 void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weight_mode,
@@ -494,11 +500,19 @@ void build_label_map(Ctx& c, const uint8_t* d_labels, int32_t n, LabelMap& map) 
 
 void extract_blocks(Ctx& c, const Csr& a, const LabelMap& map, Blocks& out, bool want_af) {
   if (a.n != a.m || a.n != map.n) throw InvalidArgument("extract_blocks: label length mismatch");
-  const int n = a.n, nf = map.nf, nc = map.nc;
+  extract_block_rows(c, a, 0, map, 0, map.nf, 0, map.nc, out, want_af);
+}
+
+// Rows [rb, rb + a.n) of the operator (global columns, global map): the F
+// rows of the slab are F sub-indices [fb, fe), its C rows [cb, ce); block
+// columns stay global sub-indices (af: global fine columns).
+void extract_block_rows(Ctx& c, const Csr& a, int rb, const LabelMap& map, int fb, int fe, int cb, int ce,
+                        Blocks& out, bool want_af) {
+  const int n = a.n, nf = fe - fb, nc = ce - cb;
   DBuf<int32_t> ffc(c, (size_t)nf), fcc(c, (size_t)nf), cfc(c, (size_t)nc), afc(c, want_af ? (size_t)nf : 0);
   if (n)
     LAUNCH(c, blocks_count, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, map.label.p,
-           map.fine_to_sub.p, ffc.p, fcc.p, cfc.p, want_af ? afc.p : nullptr);
+           map.fine_to_sub.p, ffc.p, fcc.p, cfc.p, want_af ? afc.p : nullptr, rb, fb, cb);
   auto finish = [&](Csr& m, int rows, int cols, const int32_t* cnt) {
     m.n = rows;
     m.m = cols;
@@ -507,16 +521,16 @@ void extract_blocks(Ctx& c, const Csr& a, const LabelMap& map, Blocks& out, bool
     m.ci.alloc(c, (size_t)m.nnz);
     m.v.alloc(c, (size_t)m.nnz);
   };
-  finish(out.aff, nf, nf, ffc.p);
-  finish(out.afc, nf, nc, fcc.p);
-  finish(out.acf, nc, nf, cfc.p);
-  if (want_af) finish(out.af, nf, n, afc.p);
+  finish(out.aff, nf, map.nf, ffc.p);
+  finish(out.afc, nf, map.nc, fcc.p);
+  finish(out.acf, nc, map.nf, cfc.p);
+  if (want_af) finish(out.af, nf, map.n, afc.p);
   if (n)
     LAUNCH(c, blocks_fill, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, a.v.p, map.label.p,
            map.fine_to_sub.p, out.aff.rp.p, out.aff.ci.p, out.aff.v.p, out.afc.rp.p, out.afc.ci.p,
            out.afc.v.p, out.acf.rp.p, out.acf.ci.p, out.acf.v.p,
            want_af ? out.af.rp.p : nullptr, want_af ? out.af.ci.p : nullptr,
-           want_af ? out.af.v.p : nullptr);
+           want_af ? out.af.v.p : nullptr, rb, fb, cb);
 }
 
 namespace {
@@ -524,14 +538,14 @@ struct ThetaScratch {
   DBuf<double> theta;
   DBuf<unsigned long long> u;  // [0] max bits, [1] bad row, [2] converted
 };
-void theta_pass(Ctx& c, const Csr& aff, ThetaScratch& s) {
+void theta_pass(Ctx& c, const Csr& aff, ThetaScratch& s, int rb = 0) {
   s.theta.alloc(c, (size_t)aff.n);
   s.u.alloc(c, 3);
   const unsigned long long init[3] = {0ull, ~0ull, 0ull};
   to_device(c, s.u.p, init, 3);
   if (aff.n)
     LAUNCH(c, theta_rows, blocks_for(aff.n, 256), 256, 0, aff.n, aff.rp.p, aff.ci.p, aff.v.p,
-           s.theta.p, s.u.p, s.u.p + 1);
+           s.theta.p, s.u.p, s.u.p + 1, rb);
 }
 void throw_zero_diag(unsigned long long row) {
   throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(row));
@@ -572,9 +586,9 @@ DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, do
   return r;
 }
 
-double dominance_max(Ctx& c, const Csr& aff) {
+double dominance_max(Ctx& c, const Csr& aff, int rb) {
   ThetaScratch s;
-  theta_pass(c, aff, s);
+  theta_pass(c, aff, s, rb);
   unsigned long long u[3];
   to_host(c, u, s.u.p, 3);
   if (u[1] != ~0ull) throw_zero_diag(u[1]);

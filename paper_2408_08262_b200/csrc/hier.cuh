@@ -72,7 +72,10 @@ struct Injection {
   int64_t coarse_eff = 0;
 };
 
-void setup(Ctx& c, const Csr& a, const airg_setup_config& cfg, const Injection* inj, Hier& h);
+struct RowSplit;
+// rs (nullable): split the setup's heavy row kernels over ranks (rowsplit.cuh)
+void setup(Ctx& c, const Csr& a, const airg_setup_config& cfg, const Injection* inj, Hier& h,
+           const RowSplit* rs = nullptr);
 void recompute_metrics(Hier& h);
 
 // solve.cu

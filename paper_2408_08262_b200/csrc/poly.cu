@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "dd.cuh"
+#include "rowsplit.cuh"
 #include "sparse.cuh"
 
 namespace airg {
@@ -84,24 +85,27 @@ __global__ void dd_gram(int64_t n, int ncols, const double* __restrict__ kh,
 }
 
 // ---- assemble_fixed_sparsity (gmres_poly.cpp:197-280)
+// rows r of a slab are global rows rb + r (rp/ci: the whole matrix)
 __global__ void pattern_count_s1(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                 int32_t* __restrict__ cnt) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                                 int32_t* __restrict__ cnt, int rb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
   bool seen = false;
   for (int k = rp[i]; k < rp[i + 1]; ++k) seen |= ci[k] == i;
-  cnt[i] = rp[i + 1] - rp[i] + (seen ? 0 : 1);
+  cnt[r] = rp[i + 1] - rp[i] + (seen ? 0 : 1);
 }
 // sorted union of row i of P, {i} and row i of A
 __global__ void pattern_union_count(int n, const int32_t* __restrict__ prp,
                                     const int32_t* __restrict__ pci, const int32_t* __restrict__ arp,
                                     const int32_t* __restrict__ aci, int32_t* __restrict__ cnt,
-                                    const int32_t* __restrict__ orp, int32_t* __restrict__ oci) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                                    const int32_t* __restrict__ orp, int32_t* __restrict__ oci, int rb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
   int p = prp ? prp[i] : 0, pe = prp ? prp[i + 1] : 0, q = arp[i], qe = arp[i + 1];
   bool diag = false;
-  int last = -1, c = 0, o = orp ? orp[i] : 0;
+  int last = -1, c = 0, o = orp ? orp[r] : 0;
   while (p < pe || q < qe || !diag) {
     int cand = INT32_MAX;
     if (p < pe) cand = pci[p];
@@ -116,7 +120,7 @@ __global__ void pattern_union_count(int n, const int32_t* __restrict__ prp,
     }
     last = cand;
   }
-  if (cnt) cnt[i] = c;
+  if (cnt) cnt[r] = c;
 }
 
 __device__ __forceinline__ int find_pos(const int32_t* __restrict__ cols, int w, int key) {
@@ -135,10 +139,11 @@ __global__ void assemble_rows(int n, const int32_t* __restrict__ arp, const int3
                               const double* __restrict__ av, const int32_t* __restrict__ orp,
                               const int32_t* __restrict__ oci, double* __restrict__ ov,
                               double* __restrict__ curb, double* __restrict__ nextb,
-                              const double* __restrict__ coeffs, int deg) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int o = orp[i], w = orp[i + 1] - o;
+                              const double* __restrict__ coeffs, int deg, int rb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
+  const int o = orp[r], w = orp[r + 1] - o;
   const int32_t* prow = oci + o;
   double* out = ov + o;
   double* cur = curb + o;
@@ -224,7 +229,7 @@ __global__ void scale_by(int n, double* __restrict__ v, const double* __restrict
 // host factors G (Cholesky == QR's R up to row signs), applies the same rank
 // cut (|R_kk| < 1e-12 on the normalised basis), the same candidate-degree
 // least-squares solves and scores each candidate's true residual from G.
-PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed) {
+PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const RowSplit* rs) {
   if (a.n != a.m) throw InvalidArgument("compute_coefficients: matrix must be square");
   if (m < 1) throw InvalidArgument("compute_coefficients: m must be >= 1");
   const int64_t n = a.n;
@@ -233,9 +238,24 @@ PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed) {
   DBuf<double> kh(c, (size_t)(n * nc)), kl(c, (size_t)(n * nc));
   const uint64_t rhs_seed = mix_host(seed, 0x504f4c59ull);
   LAUNCH(c, normal_fill, blocks_for(n, 256), 256, 0, n, rhs_seed, kh.p, kl.p);
-  for (int k = 1; k <= m; ++k)
-    LAUNCH(c, dd_spmv, blocks_for(n, 128), 128, 0, (int)n, a.rp.p, a.ci.p, a.v.p,
-           kh.p + (k - 1) * n, kl.p + (k - 1) * n, kh.p + k * n, kl.p + k * n);
+  if (rs) {  // row slabs per rank, gathered after every power (rowsplit.cuh)
+    RowSlices sl;
+    sl.build(c, *rs, a);
+    for (int k = 1; k <= m; ++k) {
+      for (int r = 0; r < rs->P; ++r) {
+        const Csr& p = sl.part[r];
+        if (!rs->mine(r) || !p.n) continue;
+        LAUNCH(c, dd_spmv, blocks_for(p.n, 128), 128, 0, p.n, p.rp.p, p.ci.p, p.v.p, kh.p + (k - 1) * n,
+               kl.p + (k - 1) * n, kh.p + k * n + sl.s[r], kl.p + k * n + sl.s[r]);
+      }
+      rs->gather_vec(c, kh.p + k * n, sl.s);
+      rs->gather_vec(c, kl.p + k * n, sl.s);
+    }
+  } else {
+    for (int k = 1; k <= m; ++k)
+      LAUNCH(c, dd_spmv, blocks_for(n, 128), 128, 0, (int)n, a.rp.p, a.ci.p, a.v.p,
+             kh.p + (k - 1) * n, kl.p + (k - 1) * n, kh.p + k * n, kl.p + k * n);
+  }
   std::vector<int2> pairs;
   for (int x = 0; x < nc; ++x)
     for (int y = x; y < nc; ++y) pairs.push_back(make_int2(x, y));
@@ -348,8 +368,38 @@ PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed) {
   return f;
 }
 
+namespace {
+// rows rb.. (n of them) of the sparsity-1 assembly, a local CSR with global columns
+void assemble_slab_s1(Ctx& c, const Csr& a, int rb, int n, const double* d_coeffs, int64_t deg, Csr& r) {
+  r.n = n;
+  r.m = a.n;
+  r.rp.alloc(c, (size_t)n + 1);
+  DBuf<int32_t> cnt(c, (size_t)std::max(1, n));
+  if (n) LAUNCH(c, pattern_count_s1, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, cnt.p, rb);
+  r.nnz = exclusive_scan(c, cnt.p, r.rp.p, n);
+  r.ci.alloc(c, (size_t)r.nnz);
+  r.v.alloc(c, (size_t)r.nnz);
+  if (!n) return;
+  LAUNCH(c, pattern_union_count, blocks_for(n, 256), 256, 0, n, (const int32_t*)nullptr,
+         (const int32_t*)nullptr, a.rp.p, a.ci.p, (int32_t*)nullptr, r.rp.p, r.ci.p, rb);
+  DBuf<double> cur(c, (size_t)std::max<int64_t>(1, r.nnz)), nxt(c, (size_t)std::max<int64_t>(1, r.nnz));
+  LAUNCH(c, assemble_rows, blocks_for(n, 128), 128, 0, n, a.rp.p, a.ci.p, a.v.p, r.rp.p, r.ci.p, r.v.p,
+         cur.p, nxt.p, d_coeffs, (int)deg, rb);
+}
+}  // namespace
+
 void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs, int64_t deg,
-                   int64_t sparsity_order, Csr& out) {
+                   int64_t sparsity_order, Csr& out, const RowSplit* rs) {
+  if (rs && sparsity_order == 1 && a.n == a.m && ncoeffs >= 1 && deg < ncoeffs) {
+    DBuf<double> coeffs(c, (size_t)ncoeffs);
+    to_device(c, coeffs.p, h_coeffs, (size_t)ncoeffs);
+    const std::vector<int64_t> s = rs->slabs(a.n);
+    std::vector<Csr> slab(rs->P);
+    for (int r = 0; r < rs->P; ++r)
+      if (rs->mine(r)) assemble_slab_s1(c, a, (int)s[r], (int)(s[r + 1] - s[r]), coeffs.p, deg, slab[r]);
+    gather_csr(c, *rs, s, slab, a.n, out);
+    return;
+  }
   if (a.n != a.m) throw InvalidArgument("assemble_fixed_sparsity: square matrix only");
   if (sparsity_order < 1) throw InvalidArgument("assemble_fixed_sparsity: sparsity_order >= 1");
   if (ncoeffs < 1) throw InvalidArgument("assemble_fixed_sparsity: empty polynomial");
@@ -372,9 +422,9 @@ void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs
   if (n) {
     if (sparsity_order >= 2)
       LAUNCH(c, pattern_union_count, blocks_for(n, 256), 256, 0, n, power.rp.p, power.ci.p, a.rp.p,
-             a.ci.p, cnt.p, (const int32_t*)nullptr, (int32_t*)nullptr);
+             a.ci.p, cnt.p, (const int32_t*)nullptr, (int32_t*)nullptr, 0);
     else
-      LAUNCH(c, pattern_count_s1, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, cnt.p);
+      LAUNCH(c, pattern_count_s1, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, cnt.p, 0);
   }
   r.nnz = exclusive_scan(c, cnt.p, r.rp.p, n);
   r.ci.alloc(c, (size_t)r.nnz);
@@ -383,11 +433,11 @@ void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs
     LAUNCH(c, pattern_union_count, blocks_for(n, 256), 256, 0, n,
            sparsity_order >= 2 ? power.rp.p : (const int32_t*)nullptr,
            sparsity_order >= 2 ? power.ci.p : (const int32_t*)nullptr, a.rp.p, a.ci.p,
-           (int32_t*)nullptr, r.rp.p, r.ci.p);
+           (int32_t*)nullptr, r.rp.p, r.ci.p, 0);
     DBuf<double> coeffs(c, (size_t)ncoeffs), cur(c, (size_t)r.nnz), nxt(c, (size_t)r.nnz);
     to_device(c, coeffs.p, h_coeffs, (size_t)ncoeffs);
     LAUNCH(c, assemble_rows, blocks_for(n, 128), 128, 0, n, a.rp.p, a.ci.p, a.v.p, r.rp.p, r.ci.p,
-           r.v.p, cur.p, nxt.p, coeffs.p, (int)deg);
+           r.v.p, cur.p, nxt.p, coeffs.p, (int)deg, 0);
   }
   out = std::move(r);
 }
@@ -397,7 +447,7 @@ void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs
 // steps are enqueued without a host round trip; the per-step norms come back
 // once at the end (parallel reductions: not bit-identical to the reference's
 // sequential sums, which only matters at the 0.5 acceptance boundary).
-double smoother_growth(Ctx& c, const Csr& a, const Csr& q) {
+double smoother_growth(Ctx& c, const Csr& a, const Csr& q, const RowSplit* rs) {
   const int n = a.n;
   if (n == 0) return 0.0;
   constexpr int kIters = 30, kTail = 15;
@@ -413,9 +463,19 @@ double smoother_growth(Ctx& c, const Csr& a, const Csr& q) {
   LAUNCH(c, sub_partial, blocks, threads, 0, n, v.p, zero.p, part.p);
   LAUNCH(c, finish_norm, 1, 1024, 0, part.p, blocks, g.p + kIters);
   LAUNCH(c, scale_by, blocks_for(n, 256), 256, 0, n, v.p, g.p + kIters);
+  RowSlices sa, sq;
+  if (rs) {
+    sa.build(c, *rs, a);
+    sq.build(c, *rs, q);
+  }
   for (int k = 0; k < kIters; ++k) {
-    spmv(c, a, v.p, av.p);
-    spmv(c, q, av.p, qav.p);
+    if (rs) {  // slab SpMVs, gathered: the norms below see the same full vectors
+      split_spmv(c, *rs, sa, v.p, av.p);
+      split_spmv(c, *rs, sq, av.p, qav.p);
+    } else {
+      spmv(c, a, v.p, av.p);
+      spmv(c, q, av.p, qav.p);
+    }
     LAUNCH(c, sub_partial, blocks, threads, 0, n, v.p, qav.p, part.p);
     LAUNCH(c, finish_norm, 1, 1024, 0, part.p, blocks, g.p + k);
     LAUNCH(c, scale_by, blocks_for(n, 256), 256, 0, n, v.p, g.p + k);

@@ -5,7 +5,9 @@
 #include <cmath>
 #include <cstring>
 
+#include "dist.cuh"
 #include "hier.cuh"
+#include "rowsplit.cuh"
 #include "tiled.cuh"
 
 namespace airg {
@@ -24,16 +26,16 @@ struct Checked {
 // make_checked_inverse (air.cpp:106-129): up to 6 seeded fits, keep the
 // least-growing, stop once growth <= 0.5.
 Checked make_checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsity,
-                             uint64_t seed) {
+                             uint64_t seed, const RowSplit* rs) {
   Checked best;
   double best_growth = INFINITY;
   for (int64_t attempt = 0; attempt < 6; ++attempt) {
     const uint64_t s = attempt == 0 ? seed : mix_host(seed, 0x52455452ull + (uint64_t)attempt);
-    PolyFit fit = poly_coefficients(c, a, order + 1, s);
+    PolyFit fit = poly_coefficients(c, a, order + 1, s, rs);
     Csr q;
     poly_assemble(c, a, fit.coeffs.data(), (int64_t)fit.coeffs.size(), fit.effective_order,
-                  sparsity, q);
-    const double growth = smoother_growth(c, a, q);
+                  sparsity, q, rs);
+    const double growth = smoother_growth(c, a, q, rs);
     if (growth < best_growth) {
       best.coeffs = fit.coeffs;
       best.eff = fit.effective_order;
@@ -49,11 +51,11 @@ Checked make_checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsi
 }
 
 Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs, int64_t eff,
-                         int64_t sparsity) {
+                         int64_t sparsity, const RowSplit* rs) {
   Checked k;
   k.coeffs = coeffs;
   k.eff = eff;
-  poly_assemble(c, a, coeffs.data(), (int64_t)coeffs.size(), eff, sparsity, k.q);
+  poly_assemble(c, a, coeffs.data(), (int64_t)coeffs.size(), eff, sparsity, k.q, rs);
   k.valid = true;
   return k;
 }
@@ -114,7 +116,8 @@ void recompute_metrics(Hier& h) {
   h.store_c = store / nnz0;
 }
 
-void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection* inj, Hier& h) {
+void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection* inj, Hier& h,
+           const RowSplit* rs) {
   if (a0.n != a0.m) throw InvalidArgument("setup: matrix must be square");
   if (cfg.poly_order < 1 || cfg.coarse_poly_order < 1)
     throw InvalidArgument("setup: polynomial orders must be >= 1");
@@ -141,12 +144,12 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
                         (cfg.max_levels > 0 && built + 1 >= cfg.max_levels);
     if (inj) {
       if (built >= inj->n_levels) {
-        coarse = injected_inverse(c, current, inj->coarse_coeffs, inj->coarse_eff, cfg.sparsity_order);
+        coarse = injected_inverse(c, current, inj->coarse_coeffs, inj->coarse_eff, cfg.sparsity_order, rs);
         break;
       }
     } else if (forced || current.n <= cfg.coarse_size_target) {  // air.cpp:309-320
       coarse = make_checked_inverse(c, current, cfg.coarse_poly_order, cfg.sparsity_order,
-                                    mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)built));
+                                    mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)built), rs);
       if (forced || coarse.growth <= kCoarseAccept) break;
       coarse = Checked();
     }
@@ -160,19 +163,38 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     Strength g;
     strength(c, L.a, cfg.strength_alpha, g);
     DBuf<uint8_t> labels(c, (size_t)n);
-    pmisr(c, g, cfg.max_loops, level_seed, cfg.weight_mode, labels.p, nullptr);
-    build_label_map(c, labels.p, n, L.map);
-    L.n_f_pre = L.map.nf;
     Blocks blk;
-    extract_blocks(c, L.a, L.map, blk, /*want_af=*/false);
-    if (cfg.ddc_enabled && L.map.nf > 0) {
-      DdcResult res = ddc(c, blk.aff, L.map, labels.p, cfg.ddc_fraction, cfg.ddc_bins, 0, 0.0, true);
-      L.max_theta_pre = res.max_theta;
-      L.alpha_diag = res.alpha_diag;
-      L.n_converted = res.converted;
-      if (res.converted > 0) build_label_map(c, labels.p, n, L.map);
+    if (rs && cfg.weight_mode == 0 && (cfg.ddc_enabled == 0 || cfg.ddc_fraction > 0.0)) {
+      // row slabs over the ranks (dist.cu): the labels, all-gathered
+      const std::vector<int64_t> sl = rs->slabs(n);
+      CfReport rep;
+      uint8_t* mine = rs->me < 0 ? labels.p : labels.p + sl[rs->me];
+      dist_cf_split(c, L.a, rs->P, rs->me, rs->comm, sl, cfg.strength_alpha, cfg.max_loops, level_seed,
+                    cfg.ddc_enabled != 0, cfg.ddc_fraction, cfg.ddc_bins, mine, rep);
+      rs->gather_vec(c, labels.p, sl);
+      build_label_map(c, labels.p, n, L.map);
+      L.n_f_pre = rep.n_f_pre;
+      L.n_converted = rep.n_converted;
+      L.alpha_diag = rep.alpha_diag;
+      L.max_theta_pre = rep.max_theta;
+      if (!cfg.ddc_enabled && L.map.nf > 0) {
+        extract_blocks(c, L.a, L.map, blk, /*want_af=*/false);
+        L.max_theta_pre = dominance_max(c, blk.aff);
+      }
     } else {
-      L.max_theta_pre = dominance_max(c, blk.aff);
+      pmisr(c, g, cfg.max_loops, level_seed, cfg.weight_mode, labels.p, nullptr);
+      build_label_map(c, labels.p, n, L.map);
+      L.n_f_pre = L.map.nf;
+      extract_blocks(c, L.a, L.map, blk, /*want_af=*/false);
+      if (cfg.ddc_enabled && L.map.nf > 0) {
+        DdcResult res = ddc(c, blk.aff, L.map, labels.p, cfg.ddc_fraction, cfg.ddc_bins, 0, 0.0, true);
+        L.max_theta_pre = res.max_theta;
+        L.alpha_diag = res.alpha_diag;
+        L.n_converted = res.converted;
+        if (res.converted > 0) build_label_map(c, labels.p, n, L.map);
+      } else {
+        L.max_theta_pre = dominance_max(c, blk.aff);
+      }
     }
     extract_blocks(c, L.a, L.map, blk, /*want_af=*/true);
     L.max_theta_post = dominance_max(c, blk.aff);
@@ -198,30 +220,35 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
 
     // --- approximate ideal restriction (air.cpp:378-381)
     Checked ff = inj ? injected_inverse(c, L.aff, inj->level_coeffs[built], inj->level_eff[built],
-                                        cfg.sparsity_order)
-                     : make_checked_inverse(c, L.aff, cfg.poly_order, cfg.sparsity_order, level_seed);
+                                        cfg.sparsity_order, rs)
+                     : make_checked_inverse(c, L.aff, cfg.poly_order, cfg.sparsity_order, level_seed, rs);
     L.ffinv = std::move(ff.q);
     L.coeffs = ff.coeffs;
     L.eff = ff.eff;
     L.growth = ff.growth;
     L.attempts = ff.attempts;
-    build_restriction(c, L.acf, L.ffinv, cfg.drop_restrict, L.map, L.r);
+    build_restriction(c, L.acf, L.ffinv, cfg.drop_restrict, L.map, L.r, nullptr, 0, rs);
     build_prolongation(c, L.map, g, L.a, L.pmap, L.p);
 
     // --- Galerkin coarse operator (air.cpp:268-271, :386-387)
     Csr ap, rap;
-    spgemm(c, L.a, L.p, ap);
-    spgemm(c, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
+    if (rs) {  // row slabs over the ranks, gathered (rowsplit.cuh)
+      split_spgemm(c, *rs, L.a, L.p, ap, -1.0, true);
+      split_spgemm(c, *rs, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
+    } else {
+      spgemm(c, L.a, L.p, ap);
+      spgemm(c, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
+    }
     with_full_diagonal(c, rap, current);
   }
   h.coarse_a = std::move(current);
   if (!coarse.valid) {
     // reached only through the all-F break (air.cpp:538-543)
     if (inj)
-      coarse = injected_inverse(c, h.coarse_a, inj->coarse_coeffs, inj->coarse_eff, cfg.sparsity_order);
+      coarse = injected_inverse(c, h.coarse_a, inj->coarse_coeffs, inj->coarse_eff, cfg.sparsity_order, rs);
     else
       coarse = make_checked_inverse(c, h.coarse_a, cfg.coarse_poly_order, cfg.sparsity_order,
-                                    mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)h.levels.size()));
+                                    mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)h.levels.size()), rs);
   }
   h.coarse_inv = std::move(coarse.q);
   h.coarse_coeffs = coarse.coeffs;

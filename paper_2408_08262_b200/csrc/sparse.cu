@@ -53,22 +53,25 @@ __global__ void spmv_rows(int n, const int32_t* __restrict__ rp, const int32_t* 
 }
 
 // ---- with_full_diagonal, sparse.cpp:132-160
+// rows r of a slab starting at global row rb: the diagonal is column rb + r
 __global__ void fulldiag_count(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                               int32_t* __restrict__ cnt) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                               int32_t* __restrict__ cnt, int rb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
   bool seen = false;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) seen |= ci[k] == i;
-  cnt[i] = rp[i + 1] - rp[i] + (seen ? 0 : 1);
+  for (int k = rp[r]; k < rp[r + 1]; ++k) seen |= ci[k] == i;
+  cnt[r] = rp[r + 1] - rp[r] + (seen ? 0 : 1);
 }
 __global__ void fulldiag_fill(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                               const double* __restrict__ v, const int32_t* __restrict__ orp,
-                              int32_t* __restrict__ oci, double* __restrict__ ov) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int o = orp[i];
+                              int32_t* __restrict__ oci, double* __restrict__ ov, int rb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
+  int o = orp[r];
   bool seen = false;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+  for (int k = rp[r]; k < rp[r + 1]; ++k) {
     const int c = ci[k];
     if (!seen && c > i) {
       oci[o] = i;
@@ -376,11 +379,12 @@ void spmv_thread_rows(Ctx& c, const Csr& a, const double* x, double* y) {
   LAUNCH(c, spmv_rows, blocks_for(a.n, 128), 128, 0, a.n, a.rp.p, a.ci.p, a.v.p, x, y);
 }
 
-void with_full_diagonal(Ctx& c, const Csr& a, Csr& out) {
-  if (a.n != a.m) throw InvalidArgument("SparseMatrix: with_full_diagonal requires a square matrix");
+void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base) {
+  if (row_base == 0 && a.n != a.m)
+    throw InvalidArgument("SparseMatrix: with_full_diagonal requires a square matrix");
   DBuf<int32_t> cnt(c, (size_t)a.n);
   Csr r;
-  if (a.n) LAUNCH(c, fulldiag_count, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, cnt.p);
+  if (a.n) LAUNCH(c, fulldiag_count, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, cnt.p, row_base);
   r.rp.alloc(c, (size_t)a.n + 1);
   const int64_t nnz = exclusive_scan(c, cnt.p, r.rp.p, a.n);
   r.n = a.n;
@@ -390,7 +394,7 @@ void with_full_diagonal(Ctx& c, const Csr& a, Csr& out) {
   r.v.alloc(c, (size_t)nnz);
   if (a.n)
     LAUNCH(c, fulldiag_fill, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.v.p, r.rp.p,
-           r.ci.p, r.v.p);
+           r.ci.p, r.v.p, row_base);
   out = std::move(r);
 }
 

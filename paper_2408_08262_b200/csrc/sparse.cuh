@@ -10,7 +10,7 @@ void csr_upload(Ctx& c, int64_t n, int64_t m, const int64_t* h_rp, const int64_t
                 const double* h_v, Csr& out);
 void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_v);
 void spmv(Ctx& c, const Csr& a, const double* x, double* y);
-void with_full_diagonal(Ctx& c, const Csr& a, Csr& out);
+void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base = 0);  // row_base: slab rows
 void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
 // tile starts for the tiled row kernels (tiled.cuh); idempotent
 void build_tiles(Ctx& c, Csr& a);
@@ -27,8 +27,13 @@ void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, 
 // C = A B with per-entry accumulation in A-row order (sparse.cpp:203-242).
 // drop_tol >= 0 fuses drop_entries(C, drop_tol, keep_diag) into the
 // compaction; drop_tol < 0 keeps everything.
+// bmap (device, nullable): B row of every A column -- B then holds gathered
+// rows of a distributed operator; row_base: the rows of `a` are global rows
+// row_base.. (diagonal of the drop rule); square_n: global row count of a
+// square product computed as a row slab (-1: a.n).
 void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol = -1.0,
-            bool keep_diag = true);
+            bool keep_diag = true, const int32_t* bmap = nullptr, int row_base = 0,
+            int64_t square_n = -1);
 
 // cfsplit.cu ------------------------------------------------------------------
 struct Strength {
@@ -37,7 +42,9 @@ struct Strength {
   DBuf<int32_t> rp, ci;     // S, sorted rows
   DBuf<int32_t> st_cnt;     // |S_i^T|
 };
-void strength(Ctx& c, const Csr& a, double alpha, Strength& g);
+// row_base: the rows of `a` are global rows row_base.. of a larger operator
+// (a row slab with global columns); 0 for a whole square matrix.
+void strength(Ctx& c, const Csr& a, double alpha, Strength& g, int row_base = 0);
 // PMISR labels (one-shot local minima, see cfsplit.cu) into d_labels.
 void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weight_mode,
            uint8_t* d_labels, double* d_weights);
@@ -59,6 +66,8 @@ struct Blocks {
   Csr af;  // A's F rows with global columns; bit 31 of a column flags a C column
 };
 void extract_blocks(Ctx& c, const Csr& a, const LabelMap& map, Blocks& out, bool want_af);
+void extract_block_rows(Ctx& c, const Csr& a, int rb, const LabelMap& map, int fb, int fe, int cb, int ce,
+                        Blocks& out, bool want_af);
 
 struct DdcResult {
   int64_t converted = 0;
@@ -78,22 +87,30 @@ struct CfFused {
 CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
                        double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre);
 // max theta only (theta_post, air.cpp:355); throws on a zero diagonal
-double dominance_max(Ctx& c, const Csr& aff);
+double dominance_max(Ctx& c, const Csr& aff, int rb = 0);  // rb: F rows of a slab
 
 // poly.cu ---------------------------------------------------------------------
 struct PolyFit {
   std::vector<double> coeffs;  // m values
   int64_t effective_order = 0;
 };
-PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed);
+struct RowSplit;  // rowsplit.cuh: row-partitioned setup work over ranks (nullable)
+PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const RowSplit* rs = nullptr);
 void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs, int64_t deg,
-                   int64_t sparsity_order, Csr& out);
-double smoother_growth(Ctx& c, const Csr& a, const Csr& q);
+                   int64_t sparsity_order, Csr& out, const RowSplit* rs = nullptr);
+double smoother_growth(Ctx& c, const Csr& a, const Csr& q, const RowSplit* rs = nullptr);
 
 // transfer.cu -----------------------------------------------------------------
+// R rows of the C points of acf (coarse rows cb..; whole operator: cb = 0);
+// bmap: row of ffinv holding each F column (gathered rows), null = identity
 void build_restriction(Ctx& c, const Csr& acf, const Csr& ffinv, double drop, const LabelMap& map,
-                       Csr& r);
+                       Csr& r, const int32_t* bmap = nullptr, int cb = 0, const RowSplit* rs = nullptr);
 // one-point P (air.cpp:191-238) as pmap[i] (coarse index or -1) and a CSR.
+// one-point P of the slab rows rb.. of `a` (S of the same rows, global map)
+void prolongation_map_rows(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a, int rb,
+                           int32_t* pmap);
+// the n x nc CSR of a one-point map (-1 = empty row)
+void prolongation_from_map(Ctx& c, const int32_t* pmap, int n, int nc, Csr& p);
 void build_prolongation(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a,
                         DBuf<int32_t>& pmap, Csr& p);
 

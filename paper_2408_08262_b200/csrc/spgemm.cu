@@ -35,16 +35,21 @@ __device__ __forceinline__ void append_row(int i, int cls, bool live, int32_t* _
 // holds), 1 warp hash. Lists: [0 | 1 | 2 | 3] x n, counts[4].
 constexpr int kThreadProducts = 32;
 constexpr int kWarpA = 64;
+// bmap (nullable): B row of each A column (B holds gathered rows of a
+// distributed operator); identity when null
+__device__ __forceinline__ int brow(const int32_t* __restrict__ bmap, int j) { return bmap ? bmap[j] : j; }
+
 __global__ void spgemm_bound(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
-                             const int32_t* __restrict__ brp, int64_t* __restrict__ ub,
-                             int32_t* __restrict__ lists, int32_t* __restrict__ counts, int classify) {
+                             const int32_t* __restrict__ brp, const int32_t* __restrict__ bmap,
+                             int64_t* __restrict__ ub, int32_t* __restrict__ lists, int32_t* __restrict__ counts,
+                             int classify) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < n;
   int64_t s = 0;
   int cls = 0;
   if (live) {
     for (int k = arp[i]; k < arp[i + 1]; ++k) {
-      const int j = aci[k];
+      const int j = brow(bmap, aci[k]);
       s += brp[j + 1] - brp[j];
     }
     ub[i] = s;
@@ -83,7 +88,7 @@ __device__ __forceinline__ void row_counts(int cnt, double drop_tol, int lane, i
 // sort (the bulk of the warp kernel's instructions) for rows of <= 256.
 template <int E>
 __device__ __forceinline__ void finish_reg(const int32_t* __restrict__ keys, const double* __restrict__ vals,
-                                           int cnt, int lane, int i, int32_t* __restrict__ oc,
+                                           int cnt, int lane, int i, int gi, int32_t* __restrict__ oc,
                                            double* __restrict__ ov, double drop_tol, int square_keep_diag,
                                            int32_t* __restrict__ len, int32_t* __restrict__ kept) {
   constexpr int S = 32 * E;
@@ -153,7 +158,7 @@ __device__ __forceinline__ void finish_reg(const int32_t* __restrict__ keys, con
       const int t = e * 32 + lane;
       if (t < cnt) {
         const double mag = fabs(v[e]);
-        const bool diag = square_keep_diag && k[e] == i;
+        const bool diag = square_keep_diag && k[e] == gi;
         kc += diag || !(mag < thr && mag < rmax);
       }
     }
@@ -163,7 +168,7 @@ __device__ __forceinline__ void finish_reg(const int32_t* __restrict__ keys, con
 
 // rows of more than 256 distinct columns (2048-slot tables): shared-memory sort
 __device__ __forceinline__ void finish_smem(int32_t* __restrict__ keys, double* __restrict__ vals, int cnt,
-                                            int lane, int i, int32_t* __restrict__ oc, double* __restrict__ ov,
+                                            int lane, int i, int gi, int32_t* __restrict__ oc, double* __restrict__ ov,
                                             double drop_tol, int square_keep_diag, int32_t* __restrict__ len,
                                             int32_t* __restrict__ kept) {
   int S = 1;
@@ -201,7 +206,7 @@ __device__ __forceinline__ void finish_smem(int32_t* __restrict__ keys, double* 
     const double thr = __dmul_rn(drop_tol, rmax);
     for (int q = lane; q < cnt; q += 32) {
       const double mag = fabs(vals[q]);
-      const bool diag = square_keep_diag && keys[q] == i;
+      const bool diag = square_keep_diag && keys[q] == gi;
       kc += diag || !(mag < thr && mag < rmax);
     }
   }
@@ -216,7 +221,8 @@ __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ 
                                          const int32_t* __restrict__ bci, const double* __restrict__ bv,
                                          const int64_t* __restrict__ off, int32_t* __restrict__ scol,
                                          double* __restrict__ sval, int32_t* __restrict__ len,
-                                         int32_t* __restrict__ kept, double drop_tol, int square_keep_diag) {
+                                         int32_t* __restrict__ kept, double drop_tol, int square_keep_diag,
+                                         const int32_t* __restrict__ bmap, int rb) {
   const int s = arp[i], na = arp[i + 1] - s;
   if (na > kWarpA) return true;
   // prefix of the B-row lengths of this A row (warp scan); empty A rows
@@ -227,7 +233,7 @@ __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ 
     const int k = k0 + lane;
     int l = 0;
     if (k < na) {
-      const int j = aci[s + k];
+      const int j = brow(bmap, aci[s + k]);
       l = brp[j + 1] - brp[j];
     }
     int incl = l;
@@ -258,7 +264,7 @@ __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ 
         else
           hi = mid - 1;
       }
-      const int j = aci[s + lo];
+      const int j = brow(bmap, aci[s + lo]);
       const int t = brp[j] + (q - pref[lo]);
       col = bci[t];
       p = __dmul_rn(av[s + lo], bv[t]);
@@ -313,13 +319,13 @@ __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ 
   int32_t* oc = scol + off[i];
   double* ov = sval + off[i];
   if (cnt <= 32) {
-    finish_reg<1>(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
+    finish_reg<1>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
   } else if (cnt <= 64) {
-    finish_reg<2>(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
+    finish_reg<2>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
   } else if (cnt <= 128) {
-    finish_reg<4>(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
+    finish_reg<4>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
   } else {
-    finish_smem(keys, vals, cnt, lane, i, oc, ov, drop_tol, square_keep_diag, len, kept);
+    finish_smem(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
   }
   return false;
 }
@@ -335,7 +341,7 @@ spgemm_warp_list(const int32_t* __restrict__ list, const int32_t* __restrict__ c
                  const int32_t* __restrict__ bci, const double* __restrict__ bv,
                  const int64_t* __restrict__ off, int32_t* __restrict__ scol, double* __restrict__ sval,
                  int32_t* __restrict__ len, int32_t* __restrict__ kept, double drop_tol,
-                 int square_keep_diag) {
+                 int square_keep_diag, const int32_t* __restrict__ bmap, int rb) {
   __shared__ int32_t keys_all[kSpgWarps][kHashCap];
   __shared__ double vals_all[kSpgWarps][kHashCap];
   __shared__ int32_t pref_all[kSpgWarps][kWarpA + 1];
@@ -346,7 +352,7 @@ spgemm_warp_list(const int32_t* __restrict__ list, const int32_t* __restrict__ c
     const int i = list[q];
     const bool ovf = warp_row<kHashCap>(i, lane, keys_all[w], vals_all[w], pref_all[w], pbuf_all[w], arp,
                                         aci, av, brp, bci, bv, off, scol, sval, len, kept, drop_tol,
-                                        square_keep_diag);
+                                        square_keep_diag, bmap, rb);
     if (ovf && lane == 0) next_list[atomicAdd(next_count, 1)] = i;
     __syncwarp();
   }
@@ -359,13 +365,14 @@ __device__ __forceinline__ void thread_row(int i, const int32_t* __restrict__ ar
                                            const double* __restrict__ bv, const int64_t* __restrict__ off,
                                            int32_t* __restrict__ scol, double* __restrict__ sval,
                                            int32_t* __restrict__ len, int32_t* __restrict__ kept,
-                                           double drop_tol, int square_keep_diag) {
+                                           double drop_tol, int square_keep_diag,
+                                           const int32_t* __restrict__ bmap, int rb) {
   int32_t* cols = scol + off[i];
   double* vals = sval + off[i];
   int L = 0;
   for (int k = arp[i]; k < arp[i + 1]; ++k) {
     const double a = av[k];
-    const int j = aci[k];
+    const int j = brow(bmap, aci[k]);
     for (int t = brp[j]; t < brp[j + 1]; ++t) {
       const int cc = bci[t];
       const double p = __dmul_rn(a, bv[t]);
@@ -402,7 +409,7 @@ __device__ __forceinline__ void thread_row(int i, const int32_t* __restrict__ ar
   int kc = 0;
   for (int q = 0; q < L; ++q) {
     const double mag = fabs(vals[q]);
-    const bool diag = square_keep_diag && cols[q] == i;
+    const bool diag = square_keep_diag && cols[q] == rb + i;
     kc += diag || !(mag < thr && mag < row_max);
   }
   kept[i] = kc;
@@ -415,18 +422,19 @@ __global__ void spgemm_accumulate(int n, const int32_t* __restrict__ list, const
                                   const int32_t* __restrict__ bci, const double* __restrict__ bv,
                                   const int64_t* __restrict__ off, int32_t* __restrict__ scol,
                                   double* __restrict__ sval, int32_t* __restrict__ len,
-                                  int32_t* __restrict__ kept, double drop_tol, int square_keep_diag) {
+                                  int32_t* __restrict__ kept, double drop_tol, int square_keep_diag,
+                                  const int32_t* __restrict__ bmap, int rb) {
   const int rows = list ? *count : n;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < rows; q += gridDim.x * blockDim.x)
     thread_row(list ? list[q] : q, arp, aci, av, brp, bci, bv, off, scol, sval, len, kept, drop_tol,
-               square_keep_diag);
+               square_keep_diag, bmap, rb);
 }
 
 __global__ void spgemm_compact(int n, const int64_t* __restrict__ off,
                                const int32_t* __restrict__ scol, const double* __restrict__ sval,
                                const int32_t* __restrict__ len, const int32_t* __restrict__ orp,
                                int32_t* __restrict__ oci, double* __restrict__ ov, double drop_tol,
-                               int square_keep_diag) {
+                               int square_keep_diag, int rb) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t* cols = scol + off[i];
@@ -445,7 +453,7 @@ __global__ void spgemm_compact(int n, const int64_t* __restrict__ off,
   const double thr = __dmul_rn(drop_tol, row_max);
   for (int q = 0; q < L; ++q) {
     const double mag = fabs(vals[q]);
-    const bool diag = square_keep_diag && cols[q] == i;
+    const bool diag = square_keep_diag && cols[q] == rb + i;
     if (diag || !(mag < thr && mag < row_max)) {
       oci[o] = cols[q];
       ov[o++] = vals[q];
@@ -455,8 +463,9 @@ __global__ void spgemm_compact(int n, const int64_t* __restrict__ off,
 
 }  // namespace
 
-void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol, bool keep_diag) {
-  if (a.m != b.n) throw InvalidArgument("spgemm: dimension mismatch");
+void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol, bool keep_diag,
+            const int32_t* bmap, int row_base, int64_t square_n) {
+  if (!bmap && a.m != b.n) throw InvalidArgument("spgemm: dimension mismatch");
   const int n = a.n;
   Csr r;
   r.n = a.n;
@@ -474,39 +483,45 @@ void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol, bool 
   DBuf<int64_t> ub(c, (size_t)n), off(c, (size_t)n + 1);
   DBuf<int32_t> lists(c, thread_only ? 1 : 4 * (size_t)n), counts(c, 4);
   counts.zero(c);
-  LAUNCH(c, spgemm_bound, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, b.rp.p, ub.p, lists.p, counts.p,
-         thread_only ? 0 : 1);
+  LAUNCH(c, spgemm_bound, blocks_for(n, 256), 256, 0, n, a.rp.p, a.ci.p, b.rp.p, bmap, ub.p, lists.p,
+         counts.p, thread_only ? 0 : 1);
   const int64_t total = exclusive_scan64(c, ub.p, off.p, n);
   DBuf<int32_t> scol(c, (size_t)total), len(c, (size_t)n), kept(c, (size_t)n);
   DBuf<double> sval(c, (size_t)total);
-  const int sq = (keep_diag && a.n == b.m) ? 1 : 0;
+  // square rule (keep the diagonal): the product is square -- for a row slab,
+  // square_n is the global row count
+  const int sq = (keep_diag && (square_n >= 0 ? square_n : (int64_t)a.n) == b.m) ? 1 : 0;
   const unsigned tgrid = (unsigned)std::min<int64_t>(blocks_for(n, 128), 16 * c.num_sms);
   if (thread_only) {
     LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)nullptr, (const int32_t*)nullptr,
-           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
+           off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
   } else {
     // list 0: few products -> thread per row; list 1: warp + 256-slot table,
     // overflow -> list 2: one warp per block + 2048-slot table, overflow ->
     // list 3: thread per row. Persistent grids read the list lengths on device.
     const int64_t N = n;
     LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)lists.p, (const int32_t*)counts.p,
-           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
+           off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
     LAUNCH(c, (spgemm_warp_list<256, 8>), (unsigned)std::min<int64_t>((N + 7) / 8, 8 * c.num_sms), 256, 0,
            (const int32_t*)(lists.p + N), (const int32_t*)(counts.p + 1), lists.p + 2 * N, counts.p + 2,
-           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
+           off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
     LAUNCH(c, (spgemm_warp_list<2048, 1>), (unsigned)std::min<int64_t>(N, 8 * c.num_sms), 32, 0,
            (const int32_t*)(lists.p + 2 * N), (const int32_t*)(counts.p + 2), lists.p + 3 * N, counts.p + 3,
-           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq);
+           a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
+           off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
     LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)(lists.p + 3 * N),
-           (const int32_t*)(counts.p + 3), a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, off.p, scol.p,
-           sval.p, len.p, kept.p, drop_tol, sq);
+           (const int32_t*)(counts.p + 3), a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
+           off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
   }
   const int64_t nnz = exclusive_scan(c, kept.p, r.rp.p, n);
   r.nnz = nnz;
   r.ci.alloc(c, (size_t)nnz);
   r.v.alloc(c, (size_t)nnz);
   LAUNCH(c, spgemm_compact, blocks_for(n, 256), 256, 0, n, off.p, scol.p, sval.p, len.p, r.rp.p,
-         r.ci.p, r.v.p, drop_tol, sq);
+         r.ci.p, r.v.p, drop_tol, sq, row_base);
   out = std::move(r);
 }
 

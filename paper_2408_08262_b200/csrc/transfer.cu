@@ -1,4 +1,5 @@
 // Grid-transfer operators (reference: proj/src/air.cpp:154-238).
+#include "rowsplit.cuh"
 #include "sparse.cuh"
 
 namespace airg {
@@ -39,22 +40,24 @@ __global__ void r_fill(int nc, const int32_t* __restrict__ zrp, const int32_t* _
 }
 
 // one-point prolongation (air.cpp:191-238)
+// rows of a slab: local row r is global row rb + r (label / f2s are global)
 __global__ void p_map(int n, const uint8_t* __restrict__ label, const int32_t* __restrict__ f2s,
                       const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
                       const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
-                      const double* __restrict__ av, int32_t* __restrict__ pmap) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                      const double* __restrict__ av, int32_t* __restrict__ pmap, int rb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int i = rb + r;
   if (label[i] == AIRG_C) {
-    pmap[i] = f2s[i];
+    pmap[r] = f2s[i];
     return;
   }
   int best = -1;
   double best_mag = -1.0;
   // strong C neighbours: S_i is a sorted subset of A's row -> merge walk
-  int k = arp[i];
-  const int ke = arp[i + 1];
-  for (int t = srp[i]; t < srp[i + 1]; ++t) {
+  int k = arp[r];
+  const int ke = arp[r + 1];
+  for (int t = srp[r]; t < srp[r + 1]; ++t) {
     const int j = sci[t];
     while (k < ke && aci[k] < j) ++k;
     if (label[j] != AIRG_C) continue;
@@ -65,7 +68,7 @@ __global__ void p_map(int n, const uint8_t* __restrict__ label, const int32_t* _
     }
   }
   if (best < 0) {
-    for (int q = arp[i]; q < ke; ++q) {
+    for (int q = arp[r]; q < ke; ++q) {
       const int cc = aci[q];
       if (cc == i || label[cc] != AIRG_C) continue;
       const double mag = fabs(av[q]);
@@ -75,7 +78,7 @@ __global__ void p_map(int n, const uint8_t* __restrict__ label, const int32_t* _
       }
     }
   }
-  pmap[i] = best >= 0 ? f2s[best] : -1;
+  pmap[r] = best >= 0 ? f2s[best] : -1;
 }
 
 __global__ void p_count(int n, const int32_t* __restrict__ pmap, int32_t* __restrict__ cnt) {
@@ -94,10 +97,13 @@ __global__ void p_fill(int n, const int32_t* __restrict__ pmap, const int32_t* _
 }  // namespace
 
 void build_restriction(Ctx& c, const Csr& acf, const Csr& ffinv, double drop, const LabelMap& map,
-                       Csr& r) {
+                       Csr& r, const int32_t* bmap, int cb, const RowSplit* rs) {
   Csr z;
-  spgemm(c, acf, ffinv, z, drop, /*keep_diag=*/false);  // air.cpp:298-299
-  const int nc = map.nc;
+  if (rs)
+    split_spgemm(c, *rs, acf, ffinv, z, drop, /*keep_diag=*/false);  // air.cpp:298-299
+  else
+    spgemm(c, acf, ffinv, z, drop, /*keep_diag=*/false, bmap);
+  const int nc = acf.n;  // the C rows of this slab: coarse rows cb..
   Csr out;
   out.n = nc;
   out.m = map.n;
@@ -109,28 +115,37 @@ void build_restriction(Ctx& c, const Csr& acf, const Csr& ffinv, double drop, co
   out.v.alloc(c, (size_t)out.nnz);
   if (nc)
     LAUNCH(c, r_fill, blocks_for(nc, 256), 256, 0, nc, z.rp.p, z.ci.p, z.v.p, map.f_to_fine.p,
-           map.c_to_fine.p, out.rp.p, out.ci.p, out.v.p);
+           map.c_to_fine.p + cb, out.rp.p, out.ci.p, out.v.p);
   r = std::move(out);
+}
+
+void prolongation_map_rows(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a, int rb,
+                           int32_t* pmap) {
+  if (a.n)
+    LAUNCH(c, p_map, blocks_for(a.n, 256), 256, 0, a.n, map.label.p, map.fine_to_sub.p, g.rp.p, g.ci.p,
+           a.rp.p, a.ci.p, a.v.p, pmap, rb);
+}
+
+void prolongation_from_map(Ctx& c, const int32_t* pmap, int n, int nc, Csr& p) {
+  Csr out;
+  out.n = n;
+  out.m = nc;
+  out.rp.alloc(c, (size_t)n + 1);
+  DBuf<int32_t> cnt(c, (size_t)std::max(1, n));
+  if (n) LAUNCH(c, p_count, blocks_for(n, 256), 256, 0, n, pmap, cnt.p);
+  out.nnz = exclusive_scan(c, cnt.p, out.rp.p, n);
+  out.ci.alloc(c, (size_t)out.nnz);
+  out.v.alloc(c, (size_t)out.nnz);
+  if (n) LAUNCH(c, p_fill, blocks_for(n, 256), 256, 0, n, pmap, out.rp.p, out.ci.p, out.v.p);
+  p = std::move(out);
 }
 
 void build_prolongation(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a,
                         DBuf<int32_t>& pmap, Csr& p) {
   const int n = map.n;
   pmap.alloc(c, (size_t)n);
-  if (n)
-    LAUNCH(c, p_map, blocks_for(n, 256), 256, 0, n, map.label.p, map.fine_to_sub.p, g.rp.p, g.ci.p,
-           a.rp.p, a.ci.p, a.v.p, pmap.p);
-  Csr out;
-  out.n = n;
-  out.m = map.nc;
-  out.rp.alloc(c, (size_t)n + 1);
-  DBuf<int32_t> cnt(c, (size_t)n);
-  if (n) LAUNCH(c, p_count, blocks_for(n, 256), 256, 0, n, pmap.p, cnt.p);
-  out.nnz = exclusive_scan(c, cnt.p, out.rp.p, n);
-  out.ci.alloc(c, (size_t)out.nnz);
-  out.v.alloc(c, (size_t)out.nnz);
-  if (n) LAUNCH(c, p_fill, blocks_for(n, 256), 256, 0, n, pmap.p, out.rp.p, out.ci.p, out.v.p);
-  p = std::move(out);
+  prolongation_map_rows(c, map, g, a, 0, pmap.p);
+  prolongation_from_map(c, pmap.p, n, map.nc, p);
 }
 
 }  // namespace airg
