@@ -59,13 +59,12 @@ __device__ __forceinline__ void thread_row(const TileView& m, const double* __re
   if (live) epi.row(i, dot_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b));
 }
 
-template <class Epi>
+// VEC (a separate instantiation per batch kind keeps each kernel's register
+// count at what its own loop needs)
+template <class Epi, bool VEC = false>
 __global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const double* __restrict__ x,
                                                             Epi epi) {
-  if (m.vec)
-    thread_row<kRowBatch, true>(m, x, epi);
-  else
-    thread_row<kRowBatch, false>(m, x, epi);
+  thread_row<kRowBatch, VEC>(m, x, epi);
   epi.finish();
 }
 
@@ -88,13 +87,16 @@ __device__ __forceinline__ void thread_row_fc(const TileView& m, const double* _
   epi.row2(i, sf, sc);
 }
 
-template <class Epi>
-__global__ void __launch_bounds__(kTileThreads) rows_thread_fc(TileView m,
-                                                               const double* __restrict__ x, Epi epi) {
-  if (m.vec)
-    thread_row_fc<kRowBatch, true>(m, x, epi);
-  else
-    thread_row_fc<kRowBatch, false>(m, x, epi);
+// AIRG_FC_MIN_BLOCKS=5 (<= 48 registers, one wave on the big levels) spills
+// and measured slower (18.56 vs 18.2 ms per C2 solve); kept as a build knob
+#ifndef AIRG_FC_MIN_BLOCKS
+#define AIRG_FC_MIN_BLOCKS 1
+#endif
+constexpr int kFcMinBlocks = AIRG_FC_MIN_BLOCKS;
+template <class Epi, bool VEC = false>
+__global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc(TileView m, const double* __restrict__ x,
+                                                               Epi epi) {
+  thread_row_fc<kRowBatch, VEC>(m, x, epi);
 }
 
 // ---- warp tiles -----------------------------------------------------------------
@@ -284,8 +286,10 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group, Epi, view, x, epi)                                  \
-    else                                                                             \
-      LAUNCH(ctx, rows_thread<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
+    else {                                                                           \
+      auto* kfn__ = (view).vec ? &rows_thread<Epi, true> : &rows_thread<Epi, false>;   \
+      LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);              \
+    }                                                                                \
   } while (0)
 // programmatic-dependent-launch variants (used inside the captured V-cycle)
 #define LAUNCH_ROWS_P(ctx, Epi, view, x, epi)                                                   \
@@ -294,8 +298,10 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);    \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
-    else                                                                                        \
-      LAUNCH_PDL(ctx, rows_thread<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);        \
+    else {                                                                                      \
+      auto* kfn__ = (view).vec ? &rows_thread<Epi, true> : &rows_thread<Epi, false>;              \
+      LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
+    }                                                                                           \
   } while (0)
 #define LAUNCH_ROWS_FC_P(ctx, Epi, view, x, epi)                                                \
   do {                                                                                          \
@@ -303,8 +309,10 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
-    else                                                                                        \
-      LAUNCH_PDL(ctx, rows_thread_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
+    else {                                                                                      \
+      auto* kfn__ = (view).vec ? &rows_thread_fc<Epi, true> : &rows_thread_fc<Epi, false>;        \
+      LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
+    }                                                                                           \
   } while (0)
 #define LAUNCH_ROWS_FC(ctx, Epi, view, x, epi)                                          \
   do {                                                                                  \
@@ -312,8 +320,10 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group_fc, Epi, view, x, epi)                                  \
-    else                                                                                \
-      LAUNCH(ctx, rows_thread_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);     \
+    else {                                                                              \
+      auto* kfn__ = (view).vec ? &rows_thread_fc<Epi, true> : &rows_thread_fc<Epi, false>;  \
+      LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                   \
+    }                                                                                   \
   } while (0)
 
 // ---- epilogues ---------------------------------------------------------------

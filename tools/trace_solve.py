@@ -12,6 +12,9 @@ import os
 import sys
 
 import numpy as np
+
+# CUPTI does not see the kernels of conditional graph bodies: host-driven loop
+os.environ.setdefault("AIRG_DEVLOOP", "0")
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
