@@ -748,6 +748,11 @@ __global__ void fcf_convert(int n, const double* __restrict__ theta, const doubl
 
 }  // namespace
 
+void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,
+                       double fraction, const unsigned long long* d_maxbits, double* d_out) {
+  LAUNCH(c, fcf_select, 1, kSelThreads, 0, d_nf, 0ll, d_hist, bins, fraction, d_maxbits, 0, 0.0, d_out);
+}
+
 CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
                        double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre) {
   if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");

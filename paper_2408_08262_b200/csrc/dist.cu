@@ -446,6 +446,7 @@ void exchange(Ctx& c, DHier& d, DVec& V) {
     }
     return;
   }
+  if (P == 1) return;  // a single rank has no halo
   DVec::Rank& M = V.rk[d.me];
   const int64_t ns = M.send_off[P - 1] + M.send_cnt[P - 1];
   if (ns) LAUNCH_PDL(c, k_pack, blocks_for(ns, 256), 256, 0, ns, M.send_idx.p, M.buf.p, M.send_buf.p);
@@ -473,31 +474,6 @@ __device__ __forceinline__ uint64_t dsplitmix(uint64_t x) {
 __device__ __forceinline__ int64_t gidx(int32_t lc, int64_t lo, int64_t own, const int32_t* halo) {
   return lc < own ? lo + lc : (int64_t)halo[lc - own];
 }
-// coarsening.cpp:83-105 on own rows; |S^T| contributions into stb ([own|halo])
-__global__ void k_dstrength(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                            const double* __restrict__ v, double alpha, int32_t* __restrict__ s_cnt,
-                            double* __restrict__ stb, const int32_t* __restrict__ srp,
-                            int32_t* __restrict__ sci) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double off_max = 0.0;
-  for (int k = rp[i]; k < rp[i + 1]; ++k)
-    if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
-  const double thr = __dmul_rn(alpha, off_max);
-  int cnt = 0;
-  int o = srp ? srp[i] : 0;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) {
-    const double mag = fabs(v[k]);
-    if (ci[k] != i && mag > 0.0 && mag >= thr) {
-      ++cnt;
-      if (sci)
-        sci[o++] = ci[k];
-      else
-        atomicAdd(stb + ci[k], 1.0);
-    }
-  }
-  if (!sci) s_cnt[i] = cnt;
-}
 __global__ void k_dweights(int n, int64_t lo, const int32_t* __restrict__ s_cnt, const double* __restrict__ stb,
                            uint64_t key, double* __restrict__ w) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -505,84 +481,6 @@ __global__ void k_dweights(int n, int64_t lo, const int32_t* __restrict__ s_cnt,
   const int64_t deg = (int64_t)s_cnt[i] + (int64_t)stb[i];
   const double u = (double)(dsplitmix(key ^ dsplitmix((uint64_t)(lo + i))) >> 11) * 0x1.0p-53;
   w[i] = __dadd_rn((double)deg, u);
-}
-__global__ void k_dnotmin(int n, int64_t lo, int64_t own, const int32_t* __restrict__ halo,
-                          const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
-                          const double* __restrict__ w, double* __restrict__ nm) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double wi = w[i];
-  const int64_t gi = lo + i;
-  for (int k = srp[i]; k < srp[i + 1]; ++k) {
-    const int32_t lc = sci[k];
-    const double wj = w[lc];
-    const int64_t gj = gidx(lc, lo, own, halo);
-    const bool j_less = wj != wi ? wj < wi : gj < gi;  // weight_less(j, i)
-    nm[j_less ? i : lc] = 1.0;
-  }
-}
-__global__ void k_dlabels(int n, const double* __restrict__ w, const double* __restrict__ nm,
-                          double* __restrict__ lab) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) lab[i] = (w[i] < 1.0 || nm[i] == 0.0) ? (double)AIRG_F : (double)AIRG_C;
-}
-// theta over own F rows, F columns in order (coarsening.cpp:219-250)
-__global__ void k_dtheta(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                         const double* __restrict__ v, const double* __restrict__ lab,
-                         const int32_t* __restrict__ fsub, double* __restrict__ theta,
-                         unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long tb = 0;
-  if (i < n && lab[i] == (double)AIRG_F) {
-    double off = 0.0, diag = 0.0;
-    bool seen = false;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
-      const int32_t lc = ci[k];
-      if (lab[lc] != (double)AIRG_F) continue;
-      if (lc == i) {
-        diag = fabs(v[k]);
-        seen = true;
-      } else {
-        off = __dadd_rn(off, fabs(v[k]));
-      }
-    }
-    if (!seen || diag == 0.0) {
-      atomicMin(bad, (unsigned long long)fsub[i]);
-      theta[i] = 0.0;
-    } else {
-      const double t = __ddiv_rn(off, diag);
-      theta[i] = t;
-      tb = (unsigned long long)__double_as_longlong(t);
-    }
-  }
-  block_max(maxbits, tb);
-}
-__global__ void k_dfsub(int n, const double* __restrict__ lab, const int32_t* __restrict__ pos,
-                        int64_t base, int32_t* __restrict__ fsub) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) fsub[i] = (int32_t)(base + pos[i]);
-}
-__global__ void k_isf(int n, const double* __restrict__ lab, int32_t* __restrict__ f) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) f[i] = lab[i] == (double)AIRG_F;
-}
-__global__ void k_dhist(int n, const double* __restrict__ lab, const double* __restrict__ theta, double width,
-                        int64_t bins, double* __restrict__ hist) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || lab[i] != (double)AIRG_F) return;
-  int64_t b = (int64_t)__ddiv_rn(theta[i], width);
-  if (b > bins - 1) b = bins - 1;
-  atomicAdd(hist + b, 1.0);
-}
-__global__ void k_dconvert(int n, const double* __restrict__ theta, double alpha_diag,
-                           double* __restrict__ lab, unsigned long long* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || lab[i] != (double)AIRG_F) return;
-  const double t = theta[i];
-  if (t > alpha_diag && t != 0.0) {
-    lab[i] = (double)AIRG_C;
-    atomicAdd(count, 1ull);
-  }
 }
 __global__ void k_to_u8(int64_t n, const double* __restrict__ lab, uint8_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -600,6 +498,137 @@ __global__ void k_unpack_add(int64_t n, const int32_t* __restrict__ idx, const d
   if (k < n) atomicAdd(&dst[idx[k]], src[k]);
 }
 
+// ---- fused distributed split (same passes as cfsplit.cu's cf_split_fused) ----
+__global__ void k_frows(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                        const double* __restrict__ v, double alpha, double* __restrict__ thr,
+                        int32_t* __restrict__ s_cnt, double* __restrict__ stb,
+                        unsigned long long* __restrict__ s_total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int cnt = 0;
+  if (i < n) {
+    double off_max = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
+    const double t = __dmul_rn(alpha, off_max);
+    thr[i] = t;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const double mag = fabs(v[k]);
+      if (ci[k] != i && mag > 0.0 && mag >= t) {
+        ++cnt;
+        atomicAdd(stb + ci[k], 1.0);
+      }
+    }
+    s_cnt[i] = cnt;
+  }
+  block_add(s_total, (unsigned long long)cnt);
+}
+__global__ void k_fmarks(int n, int64_t lo, int64_t own, const int32_t* __restrict__ halo,
+                         const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                         const double* __restrict__ v, const double* __restrict__ thr,
+                         const double* __restrict__ w, double* __restrict__ nm) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double wi = w[i], t = thr[i];
+  const int64_t gi = lo + i;
+  bool mine = false;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const int32_t lc = ci[k];
+    const double mag = fabs(v[k]);
+    if (lc == i || !(mag > 0.0) || !(mag >= t)) continue;
+    const double wj = w[lc];
+    const int64_t gj = gidx(lc, lo, own, halo);
+    if (wj != wi ? wj < wi : gj < gi)  // weight_less(j, i)
+      mine = true;
+    else
+      nm[lc] = 1.0;
+  }
+  if (mine) nm[i] = 1.0;
+}
+__global__ void k_flabels(int n, const double* __restrict__ w, const double* __restrict__ nm,
+                          double* __restrict__ lab, unsigned long long* __restrict__ nf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool f = false;
+  if (i < n) {
+    f = w[i] < 1.0 || nm[i] == 0.0;
+    lab[i] = f ? (double)AIRG_F : (double)AIRG_C;
+  }
+  block_add(nf, f ? 1ull : 0ull);
+}
+__global__ void k_ftheta(int n, int64_t lo, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                         const double* __restrict__ v, const double* __restrict__ lab, double* __restrict__ theta,
+                         unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long tb = 0;
+  if (i < n && lab[i] == (double)AIRG_F) {
+    double off = 0.0, diag = 0.0;
+    bool seen = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int32_t lc = ci[k];
+      if (lab[lc] != (double)AIRG_F) continue;
+      if (lc == i) {
+        diag = fabs(v[k]);
+        seen = true;
+      } else {
+        off = __dadd_rn(off, fabs(v[k]));
+      }
+    }
+    if (!seen || diag == 0.0) {
+      atomicMin(bad, (unsigned long long)(lo + i));  // global fine row; F sub-index on the host
+      theta[i] = 0.0;
+    } else {
+      const double t = __ddiv_rn(off, diag);
+      theta[i] = t;
+      tb = (unsigned long long)__double_as_longlong(t);
+    }
+  }
+  block_max(maxbits, tb);
+}
+__global__ void k_fhist(int n, const double* __restrict__ lab, const double* __restrict__ theta,
+                        const unsigned long long* __restrict__ maxbits, int64_t bins,
+                        unsigned long long* __restrict__ hist) {
+  extern __shared__ unsigned int sh[];
+  const bool priv = bins <= 8192;
+  if (priv)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const double mx = __longlong_as_double((long long)*maxbits);
+  const double width = mx > 0.0 ? __ddiv_rn(mx, (double)bins) : 1.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (lab[i] != (double)AIRG_F) continue;
+    int64_t b = (int64_t)__ddiv_rn(theta[i], width);
+    if (b > bins - 1) b = bins - 1;
+    if (priv)
+      atomicAdd(sh + b, 1u);
+    else
+      atomicAdd(hist + b, 1ull);
+  }
+  __syncthreads();
+  if (priv)
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+      if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
+}
+__global__ void k_fconvert(int n, const double* __restrict__ theta, const double* __restrict__ sel,
+                           const unsigned long long* __restrict__ bad, double* __restrict__ lab,
+                           unsigned long long* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool conv = false;
+  if (i < n && *bad == ~0ull && lab[i] == (double)AIRG_F) {
+    const double t = theta[i];
+    if (t > sel[0] && t != 0.0) {
+      lab[i] = (double)AIRG_C;
+      conv = true;
+    }
+  }
+  block_add(count, conv ? 1ull : 0ull);
+}
+// F points of this slab below global fine row `limit` (zero-diagonal message)
+__global__ void k_f_below(int n, int64_t lo, const double* __restrict__ lab, unsigned long long limit,
+                          unsigned long long* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool f = i < n && (unsigned long long)(lo + i) < limit && lab[i] == (double)AIRG_F;
+  block_add(cnt, f ? 1ull : 0ull);
+}
+
 // reverse exchange: every halo entry is added into its owner's slot
 void reverse_add(Ctx& c, DHier& d, DVec& V) {
   const int P = V.part.P();
@@ -612,6 +641,7 @@ void reverse_add(Ctx& c, DHier& d, DVec& V) {
     }
     return;
   }
+  if (P == 1) return;
   DVec::Rank& M = V.rk[d.me];
   NCCL_CHECK(ncclGroupStart());
   for (int q = 0; q < P; ++q) {
@@ -626,15 +656,6 @@ void reverse_add(Ctx& c, DHier& d, DVec& V) {
   NCCL_CHECK(ncclGroupEnd());
   const int64_t ns = M.send_off[P - 1] + M.send_cnt[P - 1];
   if (ns) LAUNCH(c, k_unpack_add, blocks_for(ns, 256), 256, 0, ns, M.send_idx.p, M.send_buf.p, M.buf.p);
-}
-
-// sum (or max) of a few host doubles over ranks
-void host_allreduce(Ctx& c, DHier& d, std::vector<double>& v, ncclRedOp_t op) {
-  if (d.me < 0 || d.P == 1 || v.empty()) return;
-  DBuf<double> t(c, v.size());
-  to_device(c, t.p, v.data(), v.size());
-  NCCL_CHECK(ncclAllReduce(t.p, t.p, v.size(), ncclDouble, op, d.comm, c.stream));
-  to_host(c, v.data(), t.p, v.size());
 }
 
 }  // namespace
@@ -664,50 +685,53 @@ void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const s
     set_halo(c, V, r, mk);
   }
   finalize(c, V, d);
+  // Per rank: thr, |S_i|, w, theta (own rows); labels / marks travel in V's
+  // [own | halo] buffers. Global counters: one shared block in emulation, one
+  // per process + NCCL allreduces otherwise.
+  // u: [0] |S| [1] n_f_pre [2] max theta bits [3] bad row [4] converted
   struct RS {
-    DBuf<int32_t> s_cnt, srp, sci, fsub;
-    DBuf<double> w, nm, lab, theta;
-    int64_t s_nnz = 0;
+    DBuf<int32_t> s_cnt;
+    DBuf<double> thr, w, lab, theta;
   };
   std::vector<RS> rs(P);
   auto mine = [&](auto&& f) {
     for (int r = 0; r < P; ++r)
       if (d.mine(r)) f(r);
   };
+  const bool nccl = me >= 0 && P > 1;
+  DBuf<unsigned long long> u(c, 8), hist(c, ddc_enabled ? (size_t)std::max<int64_t>(1, bins) : 1);
+  DBuf<double> sel(c, 2);
+  CUDA_CHECK(cudaMemsetAsync(u.p, 0, 8 * sizeof(unsigned long long), c.stream));
+  CUDA_CHECK(cudaMemsetAsync(u.p + 3, 0xff, sizeof(unsigned long long), c.stream));
+  hist.zero(c);
+  sel.zero(c);
+  auto allreduce = [&](unsigned long long* p, size_t cnt, ncclRedOp_t op) {
+    if (nccl) NCCL_CHECK(ncclAllReduce(p, p, cnt, ncclUint64, op, comm, c.stream));
+  };
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
-  // 1. strength, |S^T| by reverse sum
+  // 1. thresholds, |S_i|, |S^T| contributions, then the reverse sum of the counts
   mine([&](int r) {
     DVec::Rank& R = V.rk[r];
     remap(c, loc[r], V, r);
     R.buf.zero(c);
     const int n = (int)R.own;
     rs[r].s_cnt.alloc(c, (size_t)std::max(1, n));
+    rs[r].thr.alloc(c, (size_t)std::max(1, n));
     if (n)
-      LAUNCH(c, k_dstrength, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, alpha,
-             rs[r].s_cnt.p, R.buf.p, (const int32_t*)nullptr, (int32_t*)nullptr);
+      LAUNCH(c, k_frows, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, alpha,
+             rs[r].thr.p, rs[r].s_cnt.p, R.buf.p, u.p);
   });
   reverse_add(c, d, V);
+  // 2. weights (own), forward exchange
   mine([&](int r) {
     DVec::Rank& R = V.rk[r];
     const int n = (int)R.own;
-    rs[r].srp.alloc(c, (size_t)n + 1);
-    rs[r].s_nnz = exclusive_scan(c, rs[r].s_cnt.p, rs[r].srp.p, n);
-    rs[r].sci.alloc(c, (size_t)std::max<int64_t>(1, rs[r].s_nnz));
-    if (n)
-      LAUNCH(c, k_dstrength, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, alpha,
-             rs[r].s_cnt.p, R.buf.p, rs[r].srp.p, rs[r].sci.p);
-    // 2. weights into the own part, then the halo weights
     rs[r].w.alloc(c, (size_t)std::max<int64_t>(1, R.own + R.nhalo));
     if (n) LAUNCH(c, k_dweights, blocks_for(n, 256), 256, 0, n, R.lo, rs[r].s_cnt.p, R.buf.p, key, rs[r].w.p);
-  });
-  // forward exchange of weights through V's buffers
-  mine([&](int r) {
-    if (V.rk[r].own)
-      CUDA_CHECK(cudaMemcpyAsync(V.rk[r].buf.p, rs[r].w.p, sizeof(double) * V.rk[r].own,
-                                 cudaMemcpyDeviceToDevice, c.stream));
+    if (n) CUDA_CHECK(cudaMemcpyAsync(R.buf.p, rs[r].w.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   });
   exchange(c, d, V);
-  // 3. "not minimal" marks, returned to the owners
+  // 3. not-minimal marks from the strong entries (thresholds re-applied), reverse sum
   mine([&](int r) {
     DVec::Rank& R = V.rk[r];
     const int64_t tot = R.own + R.nhalo;
@@ -715,132 +739,71 @@ void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const s
     R.buf.zero(c);
     const int n = (int)R.own;
     if (n)
-      LAUNCH(c, k_dnotmin, blocks_for(n, 256), 256, 0, n, R.lo, R.own, R.halo.p, rs[r].srp.p, rs[r].sci.p,
-             rs[r].w.p, R.buf.p);
+      LAUNCH(c, k_fmarks, blocks_for(n, 256), 256, 0, n, R.lo, R.own, R.halo.p, loc[r].rp.p, loc[r].ci.p,
+             loc[r].v.p, rs[r].thr.p, rs[r].w.p, R.buf.p);
   });
   reverse_add(c, d, V);
-  // 4. PMISR labels on own rows, then the halo labels
-  std::vector<double> cnts(P, 0.0);
+  // 4. labels (own), n_f; forward exchange of the labels
   mine([&](int r) {
     DVec::Rank& R = V.rk[r];
     const int n = (int)R.own;
     rs[r].lab.alloc(c, (size_t)std::max<int64_t>(1, R.own + R.nhalo));
-    if (n) LAUNCH(c, k_dlabels, blocks_for(n, 256), 256, 0, n, rs[r].w.p, R.buf.p, rs[r].lab.p);
+    if (n) LAUNCH(c, k_flabels, blocks_for(n, 256), 256, 0, n, rs[r].w.p, R.buf.p, rs[r].lab.p, u.p + 1);
     if (n) CUDA_CHECK(cudaMemcpyAsync(R.buf.p, rs[r].lab.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   });
+  allreduce(u.p, 2, ncclSum);
   exchange(c, d, V);
-  double s_nnz = 0.0;
-  mine([&](int r) {
-    DVec::Rank& R = V.rk[r];
-    const int64_t tot = R.own + R.nhalo;
-    if (tot) CUDA_CHECK(cudaMemcpyAsync(rs[r].lab.p, R.buf.p, sizeof(double) * tot, cudaMemcpyDeviceToDevice, c.stream));
-    const int n = (int)R.own;
-    DBuf<int32_t> f(c, (size_t)std::max(1, n)), pos(c, (size_t)n + 1);
-    if (n) LAUNCH(c, k_isf, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, f.p);
-    cnts[r] = (double)exclusive_scan(c, f.p, pos.p, n);
-    rs[r].fsub.alloc(c, (size_t)std::max(1, n));
-    s_nnz += (double)rs[r].s_nnz;
-  });
-  // global F numbering (for the zero-diagonal row index) and totals
-  std::vector<double> allc(P, 0.0);
-  if (me < 0) {
-    allc = cnts;
-  } else {
-    allc[me] = cnts[me];
-    host_allreduce(c, d, allc, ncclSum);
-  }
-  std::vector<double> tot1{s_nnz};
-  host_allreduce(c, d, tot1, ncclSum);
-  int64_t nf_pre = 0;
-  std::vector<int64_t> fbase(P, 0);
-  for (int r = 0; r < P; ++r) {
-    fbase[r] = nf_pre;
-    nf_pre += (int64_t)allc[r];
-  }
-  rep = CfReport();
-  rep.n_f_pre = nf_pre;
-  rep.s_nnz = (int64_t)tot1[0];
-  if (ddc_enabled && nf_pre > 0) {
-    // 5. DDC with global max / histogram
-    DBuf<unsigned long long> u(c, 3);
-    std::vector<double> stats(2 * P, 0.0);  // per rank: max theta, bad row (as double, -1 none)
+  if (ddc_enabled) {
+    // 5. theta (own F rows) -> global max / bad row -> histogram -> alpha -> convert
     mine([&](int r) {
       DVec::Rank& R = V.rk[r];
+      const int64_t tot = R.own + R.nhalo;
+      if (tot) CUDA_CHECK(cudaMemcpyAsync(rs[r].lab.p, R.buf.p, sizeof(double) * tot, cudaMemcpyDeviceToDevice, c.stream));
       const int n = (int)R.own;
-      DBuf<int32_t> f(c, (size_t)std::max(1, n)), pos(c, (size_t)n + 1);
-      if (n) LAUNCH(c, k_isf, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, f.p);
-      exclusive_scan(c, f.p, pos.p, n);
-      if (n) LAUNCH(c, k_dfsub, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, pos.p, fbase[r], rs[r].fsub.p);
       rs[r].theta.alloc(c, (size_t)std::max(1, n));
-      const unsigned long long init[3] = {0ull, ~0ull, 0ull};
-      to_device(c, u.p, init, 3);
       if (n)
-        LAUNCH(c, k_dtheta, blocks_for(n, 256), 256, 0, n, loc[r].rp.p, loc[r].ci.p, loc[r].v.p, rs[r].lab.p,
-               rs[r].fsub.p, rs[r].theta.p, u.p, u.p + 1);
-      unsigned long long hu[3];
-      to_host(c, hu, u.p, 3);
-      double mx;
-      std::memcpy(&mx, &hu[0], sizeof mx);
-      stats[r] = mx;
-      stats[P + r] = hu[1] == ~0ull ? -1.0 : (double)hu[1];
+        LAUNCH(c, k_ftheta, blocks_for(n, 256), 256, 0, n, R.lo, loc[r].rp.p, loc[r].ci.p, loc[r].v.p,
+               rs[r].lab.p, rs[r].theta.p, u.p + 2, u.p + 3);
     });
-    double max_theta = 0.0;
-    int64_t bad = -1;
-    if (me >= 0) {
-      std::vector<double> m1{stats[me]};
-      host_allreduce(c, d, m1, ncclMax);
-      max_theta = m1[0];
-      std::vector<double> b1{stats[P + me] < 0 ? 1e300 : stats[P + me]};
-      host_allreduce(c, d, b1, ncclMin);
-      bad = b1[0] >= 1e300 ? -1 : (int64_t)b1[0];
-    } else {
-      for (int r = 0; r < P; ++r) {
-        max_theta = std::max(max_theta, stats[r]);
-        if (stats[P + r] >= 0 && (bad < 0 || (int64_t)stats[P + r] < bad)) bad = (int64_t)stats[P + r];
-      }
-    }
-    if (bad >= 0) throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(bad));
-    const double width = max_theta > 0.0 ? max_theta / (double)bins : 1.0;
-    std::vector<double> hist((size_t)bins, 0.0);
-    mine([&](int r) {
-      DBuf<double> hd(c, (size_t)bins);
-      hd.zero(c);
-      const int n = (int)V.rk[r].own;
-      if (n) LAUNCH(c, k_dhist, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, rs[r].theta.p, width, bins, hd.p);
-      std::vector<double> hh((size_t)bins);
-      to_host(c, hh.data(), hd.p, hh.size());
-      for (int64_t b = 0; b < bins; ++b) hist[b] += hh[b];
-    });
-    host_allreduce(c, d, hist, ncclSum);
-    // coarsening.cpp:290-315, identical arithmetic on every rank
-    double alpha_diag = 0.0;
-    if (max_theta != 0.0) {
-      const double target = fraction * (double)nf_pre;
-      int64_t above = 0, best_k = bins;
-      double best_err = std::fabs((double)above - target);
-      for (int64_t k = bins; k-- > 0;) {
-        above += (int64_t)hist[k];
-        const double err = std::fabs((double)above - target);
-        if (err < best_err) {
-          best_err = err;
-          best_k = k;
-        }
-      }
-      alpha_diag = (double)best_k * (max_theta / (double)bins);
-    }
-    std::vector<double> conv(1, 0.0);
+    allreduce(u.p + 2, 1, ncclMax);
+    allreduce(u.p + 3, 1, ncclMin);
     mine([&](int r) {
       const int n = (int)V.rk[r].own;
-      CUDA_CHECK(cudaMemsetAsync(u.p + 2, 0, sizeof(unsigned long long), c.stream));
-      if (n) LAUNCH(c, k_dconvert, blocks_for(n, 256), 256, 0, n, rs[r].theta.p, alpha_diag, rs[r].lab.p, u.p + 2);
-      conv[0] += (double)read1(c, u.p + 2);
+      const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
+      if (n)
+        LAUNCH(c, k_fhist, (unsigned)std::min<int64_t>(blocks_for(n, 256), 4 * c.num_sms), 256, smem, n,
+               rs[r].lab.p, rs[r].theta.p, u.p + 2, bins, hist.p);
     });
-    host_allreduce(c, d, conv, ncclSum);
-    rep.max_theta = max_theta;
-    rep.alpha_diag = alpha_diag;
-    rep.n_converted = (int64_t)conv[0];
+    allreduce(hist.p, (size_t)bins, ncclSum);
+    launch_ddc_select(c, u.p + 1, hist.p, bins, fraction, u.p + 2, sel.p);
+    mine([&](int r) {
+      const int n = (int)V.rk[r].own;
+      if (n) LAUNCH(c, k_fconvert, blocks_for(n, 256), 256, 0, n, rs[r].theta.p, sel.p, u.p + 3, rs[r].lab.p, u.p + 4);
+    });
+    allreduce(u.p + 4, 1, ncclSum);
   }
+  unsigned long long hu[8];
+  to_host(c, hu, u.p, 8);
+  double hs[2];
+  to_host(c, hs, sel.p, 2);
+  if (ddc_enabled && hu[3] != ~0ull) {
+    // the reference names the A_ff row: #F points before the global fine row
+    DBuf<unsigned long long> cnt(c, 1);
+    cnt.zero(c);
+    mine([&](int r) {
+      const int n = (int)V.rk[r].own;
+      if (n) LAUNCH(c, k_f_below, blocks_for(n, 256), 256, 0, n, V.rk[r].lo, rs[r].lab.p, hu[3], cnt.p);
+    });
+    allreduce(cnt.p, 1, ncclSum);
+    throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(read1(c, cnt.p)));
+  }
+  rep = CfReport();
+  rep.s_nnz = (int64_t)hu[0];
+  rep.n_f_pre = (int64_t)hu[1];
+  rep.n_converted = (int64_t)hu[4];
   rep.n_f = rep.n_f_pre - rep.n_converted;
+  rep.alpha_diag = hs[0];
+  rep.max_theta = hs[1];
   mine([&](int r) {
     const int64_t n = V.rk[r].own, lo = me < 0 ? V.rk[r].lo : 0;
     if (n) LAUNCH(c, k_to_u8, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, d_labels + lo);

@@ -86,6 +86,9 @@ struct CfFused {
 };
 CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
                        double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre);
+// coarsening.cpp:290-315 on device counters: d_out = {alpha_diag, max_theta}
+void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,
+                       double fraction, const unsigned long long* d_maxbits, double* d_out);
 // max theta only (theta_post, air.cpp:355); throws on a zero diagonal
 double dominance_max(Ctx& c, const Csr& aff, int rb = 0);  // rb: F rows of a slab
 
