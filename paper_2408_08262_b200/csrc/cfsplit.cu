@@ -296,6 +296,8 @@ fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
            const unsigned long long* __restrict__ hist, int64_t bins, double fraction,
            const unsigned long long* __restrict__ maxbits, int selection, double direct_alpha,
            double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned suf[8192 + 1];  // counts <= n_f < 2^31
   __shared__ double werr[kSelThreads / 32];
   __shared__ int64_t wk[kSelThreads / 32];
@@ -613,6 +615,8 @@ __global__ void fcf_rows(int n, const int32_t* __restrict__ rp, const int32_t* _
                          const double* __restrict__ v, double alpha, double* __restrict__ thr,
                          int32_t* __restrict__ s_cnt, int32_t* __restrict__ st_cnt,
                          unsigned long long* __restrict__ s_total) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int cnt = 0;
   if (i < n) {
@@ -637,6 +641,8 @@ __global__ void fcf_rows(int n, const int32_t* __restrict__ rp, const int32_t* _
 
 __global__ void fcf_weights(int n, const int32_t* __restrict__ s_cnt, const int32_t* __restrict__ st_cnt,
                             uint64_t stream_key, double* __restrict__ w) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t deg = (int64_t)s_cnt[i] + st_cnt[i];
@@ -647,6 +653,8 @@ __global__ void fcf_weights(int n, const int32_t* __restrict__ s_cnt, const int3
 __global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ v, const double* __restrict__ thr,
                           const double* __restrict__ w, uint8_t* __restrict__ notmin) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double t = thr[i];
@@ -665,6 +673,8 @@ __global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* 
 
 __global__ void fcf_labels(int n, const uint8_t* __restrict__ notmin, const double* __restrict__ w,
                            uint8_t* __restrict__ label, unsigned long long* __restrict__ nf) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool f = false;
   if (i < n) {
@@ -679,6 +689,8 @@ __global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* 
                           const double* __restrict__ v, const uint8_t* __restrict__ label,
                           double* __restrict__ theta, unsigned long long* __restrict__ maxbits,
                           unsigned long long* __restrict__ bad_row) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long tb = 0;
   if (i < n && label[i] == AIRG_F) {
@@ -709,6 +721,8 @@ __global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* 
 __global__ void fcf_hist(int n, const uint8_t* __restrict__ label, const double* __restrict__ theta,
                          const unsigned long long* __restrict__ maxbits, int64_t bins,
                          unsigned long long* __restrict__ hist) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ unsigned int sh[];
   const bool priv = bins <= 8192;
   if (priv)
@@ -734,6 +748,8 @@ __global__ void fcf_hist(int n, const uint8_t* __restrict__ label, const double*
 __global__ void fcf_convert(int n, const double* __restrict__ theta, const double* __restrict__ sel,
                             const unsigned long long* __restrict__ bad_row, uint8_t* __restrict__ label,
                             unsigned long long* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool conv = false;
   if (i < n && *bad_row == ~0ull && label[i] == AIRG_F) {
@@ -783,21 +799,21 @@ CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool d
   CUDA_CHECK(cudaMemsetAsync(u + 3, 0xff, 8, c.stream));
   CUDA_CHECK(cudaMemsetAsync(cnt + n, 0, sizeof(int32_t) * n, c.stream));
   CUDA_CHECK(cudaMemsetAsync(notmin, 0, n, c.stream));
-  LAUNCH(c, fcf_rows, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, cnt + n, u);
+  LAUNCH_PDL(c, fcf_rows, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, cnt + n, u);
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
-  LAUNCH(c, fcf_weights, g, 256, 0, n, cnt, cnt + n, key, w);
-  LAUNCH(c, fcf_marks, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, w, notmin);
-  LAUNCH(c, fcf_labels, g, 256, 0, n, notmin, w, d_labels, u + 1);
+  LAUNCH_PDL(c, fcf_weights, g, 256, 0, n, cnt, cnt + n, key, w);
+  LAUNCH_PDL(c, fcf_marks, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, w, notmin);
+  LAUNCH_PDL(c, fcf_labels, g, 256, 0, n, notmin, w, d_labels, u + 1);
   if (d_labels_pre)
     CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
   if (ddc_enabled) {
-    LAUNCH(c, fcf_theta, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, d_labels, theta, u + 2, u + 3);
+    LAUNCH_PDL(c, fcf_theta, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, d_labels, theta, u + 2, u + 3);
     const unsigned hb = (unsigned)std::min<int64_t>(g, 4 * c.num_sms);
     const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
-    LAUNCH(c, fcf_hist, hb, 256, smem, n, d_labels, theta, u + 2, bins, hist);
-    LAUNCH(c, fcf_select, 1, kSelThreads, 0, u + 1, 0ll, hist, bins, fraction, u + 2, 0, 0.0,
+    LAUNCH_PDL(c, fcf_hist, hb, 256, smem, n, d_labels, theta, u + 2, bins, hist);
+    LAUNCH_PDL(c, fcf_select, 1, kSelThreads, 0, u + 1, 0ll, hist, bins, fraction, u + 2, 0, 0.0,
            reinterpret_cast<double*>(u + 5));
-    LAUNCH(c, fcf_convert, g, 256, 0, n, theta, reinterpret_cast<const double*>(u + 5), u + 3, d_labels,
+    LAUNCH_PDL(c, fcf_convert, g, 256, 0, n, theta, reinterpret_cast<const double*>(u + 5), u + 3, d_labels,
            u + 4);
   }
   (void)sel;
