@@ -126,7 +126,13 @@ bool use_sell() { return solve_layout_sell(); }
       LAUNCH_ROWS_FC_P(c, Epi, tv(M), x, epi);                                        \
   } while (0)
 
-// x_l = 0 + P e_c  (solve.cpp:139-141: pe = spmv(P, ec); x += 1.0 * pe)
+// x_l = 0 + P e_c  (solve.cpp:139-141: pe = spmv(P, ec); x += 1.0 * pe).
+// Four rows per thread (int4 map load, two double2 stores; the level vectors
+// come from the pool, 16-byte aligned); the last thread takes the n % 4 tail.
+__device__ __forceinline__ double prolong_one(int j, const double* __restrict__ ec) {
+  const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
+  return __dadd_rn(0.0, __dmul_rn(1.0, pe));
+}
 __global__ void k_prolong(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
                           double* __restrict__ x) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -134,8 +140,26 @@ __global__ void k_prolong(int n, const int32_t* __restrict__ pmap, const double*
   pdl_wait();
   pdl_trigger();
   if (i >= n) return;
-  const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
-  x[i] = __dadd_rn(0.0, __dmul_rn(1.0, pe));
+  x[i] = prolong_one(j, ec);
+}
+__global__ void k_prolong4(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
+                           double* __restrict__ x) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n4 = n >> 2;
+  int4 j = make_int4(-1, -1, -1, -1);
+  if (q < n4) j = __ldg(reinterpret_cast<const int4*>(pmap) + q);
+  pdl_wait();
+  pdl_trigger();
+  if (q == n4) {
+    for (int i = 4 * n4; i < n; ++i) x[i] = prolong_one(__ldg(pmap + i), ec);
+    return;
+  }
+  if (q > n4) return;
+  const double a = prolong_one(j.x, ec), b = prolong_one(j.y, ec);
+  const double c = prolong_one(j.z, ec), d = prolong_one(j.w, ec);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  x2[2 * q] = make_double2(a, b);
+  x2[2 * q + 1] = make_double2(c, d);
 }
 
 // x += 1.0 * e (solve.cpp:224)
@@ -450,7 +474,10 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     const double* bl = l == 0 ? b0 : lv.b.p;
     const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
     const int n = lv.a.n, nf = lv.map.nf;
-    LAUNCH_PDL(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
+    if (n >= 4096)
+      LAUNCH_PDL(c, k_prolong4, blocks_for(n / 4 + 1, 256), 256, 0, n, lv.pmap.p, ec, lv.x.p);
+    else
+      LAUNCH_PDL(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
     for (int64_t s = 0; s < cfg.up_f_smooths && nf > 0; ++s) {
       if (s == 0)
         ROWS_FC(EpiFres1, lv.af, lv.x.p,
