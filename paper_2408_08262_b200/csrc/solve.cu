@@ -162,20 +162,40 @@ __global__ void k_prolong4(int n, const int32_t* __restrict__ pmap, const double
   x2[2 * q + 1] = make_double2(c, d);
 }
 
-// x += 1.0 * e (solve.cpp:224)
+// x += 1.0 * e (solve.cpp:224), two entries per thread (pool vectors are
+// 16-byte aligned; the last thread takes an odd tail)
 __global__ void k_axpy1(int n, const double* __restrict__ e, double* __restrict__ x) {
   pdl_wait();
   pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(1.0, e[i]));
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n2 = n >> 1;
+  if (q < n2) {
+    const double2 ev = reinterpret_cast<const double2*>(e)[q];
+    double2 xv = reinterpret_cast<double2*>(x)[q];
+    xv.x = __dadd_rn(xv.x, __dmul_rn(1.0, ev.x));
+    xv.y = __dadd_rn(xv.y, __dmul_rn(1.0, ev.y));
+    reinterpret_cast<double2*>(x)[q] = xv;
+  } else if (q == n2 && (n & 1)) {
+    x[n - 1] = __dadd_rn(x[n - 1], __dmul_rn(1.0, e[n - 1]));
+  }
 }
 
 __global__ void k_sum_partials(const double* __restrict__ part, int np, double* __restrict__ out) {
   __shared__ double sm[32];
   pdl_wait();
   pdl_trigger();
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  // four independent accumulators: the partial loads are issued together
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const int step = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + 3 * step < np; i += 4 * step) {
+    s0 += part[i];
+    s1 += part[i + step];
+    s2 += part[i + 2 * step];
+    s3 += part[i + 3 * step];
+  }
+  for (; i < np; i += step) s0 += part[i];
+  double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
@@ -621,7 +641,7 @@ bool build_device_loop(Ctx& c, Hier& h, const airg_solve_config& cfg) {
                                            cudaStreamCaptureModeThreadLocal));
   try {
     enqueue_vcycle(c, h, cfg, h.r.p);
-    LAUNCH_PDL(c, k_axpy1, blocks_for(n, 256), 256, 0, n, vcycle_output(h), h.xsol.p);
+    LAUNCH_PDL(c, k_axpy1, blocks_for(n / 2 + 1, 256), 256, 0, n, vcycle_output(h), h.xsol.p);
     enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
     LAUNCH_PDL(c, k_loop_check, 1, 32, 0, hnd, (const double*)h.scal.p, (const double*)h.loop_par.p,
                h.loop_it.p, h.loop_hist.p, (long long)h.loop_hist.n);
@@ -678,7 +698,7 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
       h.g_rich_kernels = capture(c, &h.g_rich, [&] {
         enqueue_vcycle(c, h, cfg, h.r.p);
         const double* e = vcycle_output(h);
-        LAUNCH_PDL(c, k_axpy1, blocks_for(n, 256), 256, 0, n, e, h.xsol.p);
+        LAUNCH_PDL(c, k_axpy1, blocks_for(n / 2 + 1, 256), 256, 0, n, e, h.xsol.p);
         enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
       });
       h.g_key_rich = key;
