@@ -37,6 +37,15 @@ struct EpiFres1 {
     sc_keep[k] = sc;
     rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc);
   }
+  // b_l comes from the descent (long complete): prefetched before the wait
+  struct Pre {
+    double bb;
+  };
+  __device__ Pre pre(int k) const { return Pre{b[__ldg(f2f + k)]}; }
+  __device__ void row2_pre(int k, double sf, double sc, const Pre& p) const {
+    sc_keep[k] = sc;
+    rf[k] = __dsub_rn(__dsub_rn(p.bb, sf), sc);
+  }
 };
 // later F-smooths: only A_FF x_F is recomputed
 struct EpiFres2 {
@@ -48,6 +57,14 @@ struct EpiFres2 {
     rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc_keep[k]);
   }
   __device__ void finish() const {}
+  // b_l and A_FC x_C (from the first residual, three kernels back)
+  struct Pre {
+    double bb, sc;
+  };
+  __device__ Pre pre(int k) const { return Pre{b[__ldg(f2f + k)], sc_keep[k]}; }
+  __device__ void row_pre(int k, double sf, const Pre& p) const {
+    rf[k] = __dsub_rn(__dsub_rn(p.bb, sf), p.sc);
+  }
 };
 // x_F += Aff^-1 r_F
 struct EpiFupd {
@@ -58,6 +75,17 @@ struct EpiFupd {
     x[i] = __dadd_rn(x[i], d);
   }
   __device__ void finish() const {}
+  // x_F was last written two kernels back (prolongation or the previous
+  // update; the residual in between only reads it)
+  struct Pre {
+    int i;
+    double x0;
+  };
+  __device__ Pre pre(int k) const {
+    const int i = __ldg(f2f + k);
+    return Pre{i, x[i]};
+  }
+  __device__ void row_pre(int, double d, const Pre& p) const { x[p.i] = __dadd_rn(p.x0, d); }
 };
 // coarse residual r = rhs - A_c e
 struct EpiCres {
@@ -84,6 +112,15 @@ struct EpiResid {
   mutable double s;
   __device__ void row(int i, double acc) const {
     const double ri = __dsub_rn(b[i], acc);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  struct Pre {  // the right-hand side is constant during the solve
+    double bb;
+  };
+  __device__ Pre pre(int i) const { return Pre{b[i]}; }
+  __device__ void row_pre(int i, double acc, const Pre& p) const {
+    const double ri = __dsub_rn(p.bb, acc);
     r[i] = ri;
     s = fma(ri, ri, s);
   }

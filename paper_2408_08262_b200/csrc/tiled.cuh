@@ -17,6 +17,8 @@
 // per-lane loop for that tile.
 #pragma once
 
+#include <type_traits>
+
 #include "rowdot.cuh"
 
 namespace airg {
@@ -43,6 +45,16 @@ struct TileView {
 // Row bounds and the first batch of the row are loaded before the PDL wait
 // (static matrix data, rowdot.cuh RowBatch); m.vec selects aligned vector
 // batches for long-row matrices.
+// Epilogues may expose `Pre pre(int row)`: operands the epilogue reads that
+// were produced two or more kernels earlier (when this kernel launches under
+// PDL its predecessor has passed its own dependency wait, so everything
+// before the predecessor is complete). They are loaded with the row's
+// static data, before the wait, and handed to row_pre / row2_pre.
+template <class E, class = void>
+struct has_pre : std::false_type {};
+template <class E>
+struct has_pre<E, std::void_t<typename E::Pre>> : std::true_type {};
+
 template <int VB, bool VEC, class Epi>
 __device__ __forceinline__ void thread_row(const TileView& m, const double* __restrict__ x, Epi& epi) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -54,9 +66,17 @@ __device__ __forceinline__ void thread_row(const TileView& m, const double* __re
     e = __ldg(m.rp + i + 1);
     if (s < e) b.load(batch_start<VB, VEC>(s), e, m.nnz, m.ci, m.v);
   }
-  pdl_wait();
-  pdl_trigger();
-  if (live) epi.row(i, dot_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b));
+  if constexpr (has_pre<Epi>::value) {
+    typename Epi::Pre pre{};
+    if (live) pre = epi.pre(i);
+    pdl_wait();
+    pdl_trigger();
+    if (live) epi.row_pre(i, dot_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b), pre);
+  } else {
+    pdl_wait();
+    pdl_trigger();
+    if (live) epi.row(i, dot_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b));
+  }
 }
 
 // VEC (a separate instantiation per batch kind keeps each kernel's register
@@ -79,12 +99,23 @@ __device__ __forceinline__ void thread_row_fc(const TileView& m, const double* _
     e = __ldg(m.rp + i + 1);
     if (s < e) b.load(batch_start<VB, VEC>(s), e, m.nnz, m.ci, m.v);
   }
-  pdl_wait();
-  pdl_trigger();
-  if (!live) return;
-  double sf, sc;
-  dot_fc_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b, sf, sc);
-  epi.row2(i, sf, sc);
+  if constexpr (has_pre<Epi>::value) {
+    typename Epi::Pre pre{};
+    if (live) pre = epi.pre(i);
+    pdl_wait();
+    pdl_trigger();
+    if (!live) return;
+    double sf, sc;
+    dot_fc_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b, sf, sc);
+    epi.row2_pre(i, sf, sc, pre);
+  } else {
+    pdl_wait();
+    pdl_trigger();
+    if (!live) return;
+    double sf, sc;
+    dot_fc_prefetched<VB, VEC>(s, e, m.nnz, m.ci, m.v, x, b, sf, sc);
+    epi.row2(i, sf, sc);
+  }
 }
 
 // AIRG_FC_MIN_BLOCKS=5 (<= 48 registers, one wave on the big levels) spills
