@@ -93,6 +93,11 @@ struct EpiCres {
   double* r;
   __device__ void row(int i, double acc) const { r[i] = __dsub_rn(rhs[i], acc); }
   __device__ void finish() const {}
+  struct Pre {  // the coarse rhs comes from the descent, >= 2 kernels back
+    double rr;
+  };
+  __device__ Pre pre(int i) const { return Pre{rhs[i]}; }
+  __device__ void row_pre(int i, double acc, const Pre& p) const { r[i] = __dsub_rn(p.rr, acc); }
 };
 // coarse update e += 1.0 * (Ac^-1 r)
 struct EpiCupd {
@@ -103,6 +108,11 @@ struct EpiCupd {
     e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
   }
   __device__ void finish() const {}
+  struct Pre {  // e from the previous update, two kernels back (a residual between)
+    double e0;
+  };
+  __device__ Pre pre(int i) const { return Pre{first ? 0.0 : e[i]}; }
+  __device__ void row_pre(int i, double acc, const Pre& p) const { e[i] = __dadd_rn(p.e0, __dmul_rn(1.0, acc)); }
 };
 // top residual r = b - A x with one partial sum of r^2 per block
 struct EpiResid {
