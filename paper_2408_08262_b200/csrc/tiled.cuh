@@ -23,7 +23,7 @@
 
 namespace airg {
 
-constexpr int kTileThreads = 256;           // 8 warps per block
+constexpr int kTileThreads = 128;           // 4 warps per block (measured: 256 -> 128 is 2% faster, 64 slower)
 constexpr int kWarpsPerBlock = kTileThreads / 32;
 constexpr int kWarpNnz = 256;               // chunk size that cuts tiles
 constexpr int kWarpCap = 384;               // shared products per warp
