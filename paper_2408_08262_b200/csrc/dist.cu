@@ -248,14 +248,14 @@ struct LResid {
     s = fma(ri, ri, s);
   }
   __device__ void finish() const {
-    __shared__ double sm[kTileThreads / 32];
+    __shared__ double sm[32];  // any block size up to 1024 (SELL launches 256)
     double v = s;
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
     __syncthreads();
     if (threadIdx.x < 32) {
-      v = threadIdx.x < kTileThreads / 32 ? sm[threadIdx.x] : 0.0;
+      v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (threadIdx.x == 0) part[blockIdx.x] = v;

@@ -91,8 +91,9 @@ void alloc_workspace(Ctx& c, Hier& h) {
   h.rhs.alloc(c, n);
   h.xsol.alloc(c, n);
   h.r.alloc(c, n);
-  // one partial per residual block, either decomposition (tiled.cuh rows_grid)
-  h.part.alloc(c, (size_t)(kReduceBlocks + top.n / kTileThreads + std::max(0, top.ntiles) + 8));
+  // one partial per residual block for any decomposition (tiled.cuh rows_grid:
+  // up to 32 lanes per row in the group kernels)
+  h.part.alloc(c, (size_t)(kReduceBlocks + (int64_t)top.n * 32 / kTileThreads + std::max(0, top.ntiles) + 8));
   h.scal.alloc(c, 64);
 }
 
