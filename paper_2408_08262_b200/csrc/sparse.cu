@@ -214,15 +214,19 @@ static int rows_override() {
 }
 
 // Aligned 8-entry vector batches pay off on long rows (the A_F rows of the
-// Galerkin levels, ~25-30 entries); short rows keep the scalar loop.
-// AIRG_VEC=0|4|8 forces one choice for every matrix.
+// Galerkin levels, ~25-30 entries); rows of <= 5 entries on average (the
+// fine levels' A, R, A_FF, Aff^-1) use 4-entry batches; the rest the 8-entry
+// scalar loop. AIRG_VEC=0|4|8 forces one choice for every matrix.
 int row_vec(int64_t n, int64_t nnz) {
   static const int forced = [] {
     const char* e = getenv("AIRG_VEC");
     return e ? atoi(e) : -1;
   }();
-  if (forced >= 0) return forced ? 8 : 0;
-  return n > 0 && nnz >= 12 * n ? 8 : 0;
+  if (forced >= 0) return forced == 8 || forced == 4 ? forced : 0;
+  if (n <= 0) return 0;
+  if (nnz >= 12 * n) return 8;  // long rows: aligned vector batches
+  if (nnz <= 5 * n) return 4;   // short rows: 4-entry scalar batches
+  return 0;
 }
 
 static int forced_group() {

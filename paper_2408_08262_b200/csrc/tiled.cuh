@@ -81,10 +81,12 @@ __device__ __forceinline__ void thread_row(const TileView& m, const double* __re
 
 // VEC (a separate instantiation per batch kind keeps each kernel's register
 // count at what its own loop needs)
-template <class Epi, bool VEC = false>
+// batch kinds (TileView::vec): 0 = 8-entry scalar batches, 8 = aligned 8-entry
+// vector batches (long rows), 4 = 4-entry scalar batches (short rows)
+template <class Epi, bool VEC = false, int VB = kRowBatch>
 __global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const double* __restrict__ x,
                                                             Epi epi) {
-  thread_row<kRowBatch, VEC>(m, x, epi);
+  thread_row<VB, VEC>(m, x, epi);
   epi.finish();
 }
 
@@ -124,10 +126,10 @@ __device__ __forceinline__ void thread_row_fc(const TileView& m, const double* _
 #define AIRG_FC_MIN_BLOCKS 1
 #endif
 constexpr int kFcMinBlocks = AIRG_FC_MIN_BLOCKS;
-template <class Epi, bool VEC = false>
+template <class Epi, bool VEC = false, int VB = kRowBatch>
 __global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc(TileView m, const double* __restrict__ x,
                                                                Epi epi) {
-  thread_row_fc<kRowBatch, VEC>(m, x, epi);
+  thread_row_fc<VB, VEC>(m, x, epi);
 }
 
 // ---- warp tiles -----------------------------------------------------------------
@@ -318,7 +320,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group, Epi, view, x, epi)                                  \
     else {                                                                           \
-      auto* kfn__ = (view).vec ? &rows_thread<Epi, true> : &rows_thread<Epi, false>;   \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;   \
       LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);              \
     }                                                                                \
   } while (0)
@@ -330,7 +332,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
     else {                                                                                      \
-      auto* kfn__ = (view).vec ? &rows_thread<Epi, true> : &rows_thread<Epi, false>;              \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;              \
       LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
     }                                                                                           \
   } while (0)
@@ -341,7 +343,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else {                                                                                      \
-      auto* kfn__ = (view).vec ? &rows_thread_fc<Epi, true> : &rows_thread_fc<Epi, false>;        \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;        \
       LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
     }                                                                                           \
   } while (0)
@@ -352,7 +354,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else {                                                                              \
-      auto* kfn__ = (view).vec ? &rows_thread_fc<Epi, true> : &rows_thread_fc<Epi, false>;  \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;  \
       LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                   \
     }                                                                                   \
   } while (0)

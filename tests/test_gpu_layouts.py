@@ -30,6 +30,7 @@ LAYOUTS = {
     "thread": {"AIRG_ROWS": "thread", "AIRG_VEC": "0", "AIRG_TAIL_N": "0"},
     "vec4": {"AIRG_VEC": "4"},
     "vec8": {"AIRG_VEC": "8"},
+    "short4": {"AIRG_VEC": "4"},
     "group_auto": {"AIRG_ROWS": "group"},
     "g2": {"AIRG_GROUP": "2"},
     "g4": {"AIRG_GROUP": "4"},
