@@ -45,7 +45,7 @@ struct Hier {
   // device-side Richardson loop (solve.cu): iteration count, residual
   // history, [rtol, max_iterations] and the conditional-WHILE graph
   DBuf<long long> loop_it;
-  DBuf<double> loop_hist, loop_par;
+  DBuf<double> loop_hist, loop_par, loop_stamps;
   cudaGraphExec_t g_loop = nullptr;
   int64_t g_key_loop = -1;
   uint64_t g_loop_kernels = 0;

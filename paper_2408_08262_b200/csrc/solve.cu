@@ -272,6 +272,15 @@ __global__ void k_loop_check(cudaGraphConditionalHandle hnd, const double* __res
   cudaGraphSetConditional(hnd, stop ? 0u : 1u);
 }
 
+__global__ void k_stamp(const long long* __restrict__ it, double* __restrict__ hist, long long cap, int which) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const long long k = *it;
+  const long long slot = 2 * k + which;
+  if (slot < cap) hist[slot] = (double)t;
+}
+
 // ---- GMRES helpers
 // partial dots of w with columns 0..j of V: grid (blocks, j+1)
 __global__ void k_multidot(int64_t n, const double* __restrict__ V, const double* __restrict__ w,
@@ -686,10 +695,18 @@ bool build_device_loop(Ctx& c, Hier& h, const airg_solve_config& cfg) {
   const uint64_t before = c.launches;
   CUDA_CHECK(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
+  // AIRG_STAMPS=1 (diagnostic): %globaltimer at the start and the end of
+  // every body iteration into loop_stamps (printed after the solve)
+  static const bool stamps = [] {
+    const char* e = getenv("AIRG_STAMPS");
+    return e && e[0] == '1';
+  }();
   try {
+    if (stamps) LAUNCH(c, k_stamp, 1, 32, 0, h.loop_it.p, h.loop_stamps.p, (long long)h.loop_stamps.n, 0);
     enqueue_vcycle(c, h, cfg, h.r.p);
     LAUNCH_PDL(c, k_axpy1, blocks_for(n / 2 + 1, 256), 256, 0, n, vcycle_output(h), h.xsol.p);
     enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
+    if (stamps) LAUNCH(c, k_stamp, 1, 32, 0, h.loop_it.p, h.loop_stamps.p, (long long)h.loop_stamps.n, 1);
     LAUNCH_PDL(c, k_loop_check, 1, 32, 0, hnd, (const double*)h.scal.p, (const double*)h.loop_par.p,
                h.loop_it.p, h.loop_hist.p, (long long)h.loop_hist.n);
   } catch (...) {
@@ -759,6 +776,7 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
       if (h.loop_hist.n < (size_t)cap) h.loop_hist.alloc(c, (size_t)cap);
       if (!h.loop_par.p) h.loop_par.alloc(c, 2);
       if (!h.loop_it.p) h.loop_it.alloc(c, 1);
+      if (!h.loop_stamps.p) h.loop_stamps.alloc(c, 4096);
       if (!build_device_loop(c, h, cfg)) h.loop_broken = true;
     }
     if (!first_stops && device_loop_enabled() && !h.loop_broken && h.g_loop) {
@@ -767,10 +785,18 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
       CUDA_CHECK(cudaMemsetAsync(h.loop_it.p, 0, sizeof(long long), c.stream));
       CUDA_CHECK(cudaGraphLaunch(h.g_loop, c.stream));
       const long long its = read1(c, h.loop_it.p);
-      std::vector<double> hv((size_t)its + 1);
+      const long long kept = std::min<long long>(its, (long long)h.loop_hist.n - 1);
+      std::vector<double> hv((size_t)kept + 1);
       hv[0] = 1.0;
-      if (its > 0) to_host(c, hv.data() + 1, h.loop_hist.p + 1, (size_t)its);
+      if (kept > 0) to_host(c, hv.data() + 1, h.loop_hist.p + 1, (size_t)kept);
       for (double r : hv) hist.push_back(r);
+      if (getenv("AIRG_STAMPS") && getenv("AIRG_STAMPS")[0] == '1') {  // diagnostic print
+        std::vector<double> ts(h.loop_stamps.n);
+        to_host(c, ts.data(), h.loop_stamps.p, ts.size());
+        for (long long k = 0; k + 1 < its && 2 * k + 2 < (long long)ts.size(); ++k)
+          fprintf(stderr, "iter %lld body %.1f us gap-to-next %.1f us\n", k, (ts[2 * k + 1] - ts[2 * k]) / 1e3,
+                  (ts[2 * k + 2] - ts[2 * k + 1]) / 1e3);
+      }
       c.launches += h.g_loop_kernels * (uint64_t)its;
       fc += (uint64_t)its * (vflops + 2 * (uint64_t)n) +
             (uint64_t)its * (2 * (uint64_t)a.nnz + 2 * (uint64_t)n + 2 * (uint64_t)n);
