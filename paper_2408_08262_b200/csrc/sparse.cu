@@ -218,14 +218,23 @@ static int rows_override() {
 // fine levels' A, R, A_FF, Aff^-1) use 4-entry batches; the rest the 8-entry
 // scalar loop. AIRG_VEC=0|4|8 forces one choice for every matrix.
 int row_vec(int64_t n, int64_t nnz) {
+  // mean row length from which vector batches pay (AIRG_VEC_ROWS overrides)
+  static const int64_t kVecRows = [] {
+    const char* e = getenv("AIRG_VEC_ROWS");
+    return e ? (int64_t)atoi(e) : (int64_t)12;
+  }();
+  static const int64_t kShortRows = [] {
+    const char* e = getenv("AIRG_SHORT_ROWS");
+    return e ? (int64_t)atoi(e) : (int64_t)5;
+  }();
   static const int forced = [] {
     const char* e = getenv("AIRG_VEC");
     return e ? atoi(e) : -1;
   }();
   if (forced >= 0) return forced == 8 || forced == 4 ? forced : 0;
   if (n <= 0) return 0;
-  if (nnz >= 12 * n) return 8;  // long rows: aligned vector batches
-  if (nnz <= 5 * n) return 4;   // short rows: 4-entry scalar batches
+  if (nnz >= kVecRows * n) return 8;  // long rows: aligned vector batches
+  if (nnz <= kShortRows * n) return 4;  // short rows: 4-entry scalar batches
   return 0;
 }
 

@@ -126,6 +126,11 @@ __device__ __forceinline__ void thread_row_fc(const TileView& m, const double* _
 #define AIRG_FC_MIN_BLOCKS 1
 #endif
 constexpr int kFcMinBlocks = AIRG_FC_MIN_BLOCKS;
+// entries per aligned vector batch of the long-row first F residual
+#ifndef AIRG_FC_VEC_BATCH
+#define AIRG_FC_VEC_BATCH 8
+#endif
+constexpr int kFcVecBatch = AIRG_FC_VEC_BATCH;
 template <class Epi, bool VEC = false, int VB = kRowBatch>
 __global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc(TileView m, const double* __restrict__ x,
                                                                Epi epi) {
@@ -343,7 +348,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else {                                                                                      \
-      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;        \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true, kFcVecBatch> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;        \
       LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
     }                                                                                           \
   } while (0)
@@ -354,7 +359,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else {                                                                              \
-      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;  \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true, kFcVecBatch> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;  \
       LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                   \
     }                                                                                   \
   } while (0)
