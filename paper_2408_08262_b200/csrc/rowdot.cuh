@@ -188,10 +188,17 @@ __device__ __forceinline__ double dot_prefetched(int s, int e, int nnz, const in
   return acc;
 }
 
-template <int VB, bool VEC>
-__device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
-                                                  const double* __restrict__ v, const double* __restrict__ x,
-                                                  RowBatch<VB, VEC>& b, double& sf, double& sc) {
+// x source of the row dots: a plain vector (read-only path) or any gather
+// functor (e.g. the prolongation of a coarse vector, solve.cu XProlong)
+struct XDirect {
+  const double* __restrict__ x;
+  __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+};
+
+template <int VB, bool VEC, class XS>
+__device__ __forceinline__ void dot_fc_src(int s, int e, int nnz, const int32_t* __restrict__ ci,
+                                           const double* __restrict__ v, const XS& xs, RowBatch<VB, VEC>& b,
+                                           double& sf, double& sc) {
   sf = 0.0;
   sc = 0.0;
   const int k00 = batch_start<VB, VEC>(s);
@@ -199,8 +206,7 @@ __device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const i
     if (k0 != k00) b.load(k0, e, nnz, ci, v);
     double xv[VB];
 #pragma unroll
-    for (int j = 0; j < VB; ++j)
-      xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + (b.c[j] & 0x7fffffff)) : 0.0;
+    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? xs(b.c[j] & 0x7fffffff) : 0.0;
 #pragma unroll
     for (int j = 0; j < VB; ++j) {
       if (k0 + j >= s && k0 + j < e) {
@@ -212,6 +218,13 @@ __device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const i
       }
     }
   }
+}
+
+template <int VB, bool VEC>
+__device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
+                                                  const double* __restrict__ v, const double* __restrict__ x,
+                                                  RowBatch<VB, VEC>& b, double& sf, double& sc) {
+  dot_fc_src<VB, VEC>(s, e, nnz, ci, v, XDirect{x}, b, sf, sc);
 }
 
 }  // namespace airg

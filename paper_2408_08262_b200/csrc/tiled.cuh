@@ -137,6 +137,27 @@ __global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc(Til
   thread_row_fc<VB, VEC>(m, x, epi);
 }
 
+// First F residual computed from data complete before its predecessor
+// started: with XS = the prolongation of the coarse correction (solve.cu
+// XProlong), its inputs come from two kernels back, so it runs concurrently
+// with the prolongation kernel and waits for it only at its end (keeping the
+// completion order the following kernels rely on).
+template <class Epi, class XS, bool VEC = false, int VB = kRowBatch>
+__global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc_early(TileView m, XS xs, Epi epi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m.nrows) {
+    const int s = __ldg(m.rp + i), e = __ldg(m.rp + i + 1);
+    RowBatch<VB, VEC> b;
+    if (s < e) b.load(batch_start<VB, VEC>(s), e, m.nnz, m.ci, m.v);
+    const typename Epi::Pre pre = epi.pre(i);
+    double sf, sc;
+    dot_fc_src<VB, VEC>(s, e, m.nnz, m.ci, m.v, xs, b, sf, sc);
+    epi.row2_pre(i, sf, sc, pre);
+  }
+  pdl_wait();
+  pdl_trigger();
+}
+
 // ---- warp tiles -----------------------------------------------------------------
 template <class Epi>
 __global__ void __launch_bounds__(kTileThreads) rows_warp_tiles(TileView m,
