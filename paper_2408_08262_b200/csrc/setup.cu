@@ -73,7 +73,7 @@ void alloc_workspace(Ctx& c, Hier& h) {
     L.rf.alloc(c, (size_t)std::max(1, L.map.nf));
     L.sc.alloc(c, (size_t)std::max(1, L.map.nf));
     map_columns(c, L.aff, L.map.f_to_fine.p, L.a.n, L.affg);
-    for (Csr* m : {&L.r, &L.af, &L.affg, &L.ffinv}) {
+    for (Csr* m : {&L.r, &L.af, &L.affg, &L.afc, &L.ffinv}) {
       build_tiles(c, *m);
       if (solve_layout_sell()) build_sell(c, *m);
     }

@@ -385,6 +385,17 @@ const TailCfg& tail_cfg() {
 // prolongation map, concurrent with the prolongation kernel. Bit-identical,
 // but measured slower (1.31 vs 0.95 ms per C2 iteration): the extra dependent
 // map load per gathered entry costs more than the hidden prolongation.
+// AIRG_SPLIT=1: the first F residual as A_FF / A_FC dots with the C part
+// computed before the wait (overlapping the prolongation). Bit-identical;
+// measured 0.963 vs 0.952 ms per C2 iteration, so off by default.
+bool split_fres1() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_SPLIT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 bool early_fres1() {
   static const bool v = [] {
     const char* e = getenv("AIRG_EARLY");
@@ -582,7 +593,13 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
       if (s == 0) {
         const TileView v = tv(lv.af);
         const EpiFres1 ep{bl, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p};
-        if (early_fres1() && !use_sell() && !v.tiles && v.group <= 1) {
+        const TileView vf = tv(lv.affg), vc = tv(lv.afc);
+        if (split_fres1() && !use_sell() && !vf.tiles && vf.group <= 1 && !vc.tiles && vc.group <= 1) {
+          auto* k = vf.vec == 8   ? &rows_fres_split<EpiFres1, true, kFcVecBatch>
+                    : vf.vec == 4 ? &rows_fres_split<EpiFres1, false, 4>
+                                  : &rows_fres_split<EpiFres1, false>;
+          LAUNCH_PDL(c, k, rows_grid(vf), kTileThreads, 0, vf, vc, (const double*)lv.x.p, ec, ep);
+        } else if (early_fres1() && !use_sell() && !v.tiles && v.group <= 1) {
           const XProlong xs{lv.pmap.p, ec};
           auto* k = v.vec == 8   ? &rows_thread_fc_early<EpiFres1, XProlong, true, kFcVecBatch>
                     : v.vec == 4 ? &rows_thread_fc_early<EpiFres1, XProlong, false, 4>

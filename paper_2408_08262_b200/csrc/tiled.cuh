@@ -158,6 +158,38 @@ __global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc_ear
   pdl_trigger();
 }
 
+// First F residual as two ordered row dots over A_FF (global fine columns)
+// and A_FC (coarse columns): the C part reads x_C = e_c, the coarse
+// correction, which is complete before this kernel launches (two kernels
+// back), so A_FC x_C is computed BEFORE the dependency wait -- overlapping
+// the prolongation kernel -- and only A_FF x_F waits for it. Each partial
+// sum keeps its column order, so (b_F - A_FF x_F) - A_FC x_C has the same
+// bits as the single-pass kernel (x_C = 0 + 1.0 * (0 + 1.0 * e_c) equals e_c
+// up to the sign of a zero, which cannot change a sum that starts at +0.0).
+template <class Epi, bool VEC = false, int VB = kRowBatch>
+__global__ void __launch_bounds__(kTileThreads, kFcMinBlocks)
+rows_fres_split(TileView ff, TileView fc, const double* __restrict__ x, const double* __restrict__ ec, Epi epi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < ff.nrows;
+  int s = 0, e = 0;
+  double sc = 0.0;
+  RowBatch<VB, VEC> b;
+  typename Epi::Pre pre{};
+  if (live) {
+    const int cs = __ldg(fc.rp + i), ce = __ldg(fc.rp + i + 1);
+    RowBatch<VB, VEC> bc;
+    if (cs < ce) bc.load(batch_start<VB, VEC>(cs), ce, fc.nnz, fc.ci, fc.v);
+    sc = dot_prefetched<VB, VEC>(cs, ce, fc.nnz, fc.ci, fc.v, ec, bc);
+    s = __ldg(ff.rp + i);
+    e = __ldg(ff.rp + i + 1);
+    if (s < e) b.load(batch_start<VB, VEC>(s), e, ff.nnz, ff.ci, ff.v);
+    pre = epi.pre(i);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (live) epi.row2_pre(i, dot_prefetched<VB, VEC>(s, e, ff.nnz, ff.ci, ff.v, x, b), sc, pre);
+}
+
 // ---- warp tiles -----------------------------------------------------------------
 template <class Epi>
 __global__ void __launch_bounds__(kTileThreads) rows_warp_tiles(TileView m,

@@ -27,7 +27,7 @@ print(r.stats.iterations, hashlib.sha256(r.x.tobytes()).hexdigest(), hashlib.sha
 """ % REPO
 
 LAYOUTS = {
-    "thread": {"AIRG_ROWS": "thread", "AIRG_VEC": "0", "AIRG_TAIL_N": "0", "AIRG_EARLY": "0"},
+    "thread": {"AIRG_ROWS": "thread", "AIRG_VEC": "0", "AIRG_TAIL_N": "0"},
     "vec4": {"AIRG_VEC": "4"},
     "vec8": {"AIRG_VEC": "8"},
     "short4": {"AIRG_VEC": "4"},
@@ -41,6 +41,7 @@ LAYOUTS = {
     "sell": {"AIRG_LAYOUT": "sell"},
     "nopdl": {"AIRG_PDL": "0"},
     "early_fres1": {"AIRG_EARLY": "1"},
+    "split_fres1": {"AIRG_SPLIT": "1"},
     "tail_off": {"AIRG_TAIL_N": "0"},
     "tail_cluster_all": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "100000000"},
     "tail_cluster_small": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "2000"},
@@ -51,7 +52,7 @@ LAYOUTS = {
 def _run(env_extra):
     env = dict(os.environ)
     for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N", "AIRG_TAIL",
-              "AIRG_DEVLOOP", "AIRG_EARLY"):
+              "AIRG_DEVLOOP", "AIRG_EARLY", "AIRG_SPLIT"):
         env.pop(k, None)
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
