@@ -122,6 +122,34 @@ __global__ void drop_fill(int n, const int32_t* __restrict__ rp, const int32_t* 
     }
 }
 
+// ---- per-block row order: rows of one kTileThreads window sorted by length
+// (descending, ties by index) so a warp's rows have similar lengths
+__global__ void k_window_sort(int n, const int32_t* __restrict__ rp, int32_t* __restrict__ perm) {
+  __shared__ int len[kTileThreads], idx[kTileThreads];
+  const int base = blockIdx.x * kTileThreads, t = threadIdx.x;
+  const int i = base + t;
+  len[t] = i < n ? rp[i + 1] - rp[i] : -1;
+  idx[t] = i;
+  __syncthreads();
+  for (int size = 2; size <= kTileThreads; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int p = t ^ stride;
+      if (p > t) {
+        const bool desc = (t & size) == 0;
+        const bool t_first = len[t] != len[p] ? len[t] > len[p] : idx[t] < idx[p];
+        if (t_first != desc) {
+          const int l0 = len[t], i0 = idx[t];
+          len[t] = len[p];
+          idx[t] = idx[p];
+          len[p] = l0;
+          idx[p] = i0;
+        }
+      }
+      __syncthreads();
+    }
+  if (i < n) perm[i] = idx[t];
+}
+
 // ---- tiles (tiled.cuh): a row starts a tile when its first nonzero lies in a
 // different kWarpNnz chunk than its predecessor's.
 __global__ void tile_flags(int n, const int32_t* __restrict__ rp, int32_t* __restrict__ flag) {
@@ -273,6 +301,16 @@ void build_tiles(Ctx& c, Csr& a) {
     a.row_mode = 1;
     a.ntiles = 0;
     a.group = (int8_t)(ov == 3 || forced_group() ? row_group_for(a.n, a.nnz) : 1);
+    // AIRG_SORT=1: rows of a block sorted by length (less divergence in a
+    // warp) -- bit-identical, measured 11 % slower on C2 (row locality lost)
+    static const bool sort_rows = [] {
+      const char* e = getenv("AIRG_SORT");
+      return e && e[0] == '1';
+    }();
+    if (sort_rows && a.group <= 1 && a.n > 0) {  // rows of a block sorted by length
+      a.perm.alloc(c, (size_t)a.n);
+      LAUNCH(c, k_window_sort, blocks_for(a.n, kTileThreads), kTileThreads, 0, a.n, a.rp.p, a.perm.p);
+    }
     return;
   }
   const bool short_rows = ov ? ov == 1 : (a.n == 0 || a.nnz <= (int64_t)kShortRow * a.n);
@@ -382,7 +420,7 @@ void spmv(Ctx& c, const Csr& a, const double* x, double* y) {
     return;
   }
   build_tiles(c, m);
-  TileView tv{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz)};
+  TileView tv{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p};
   LAUNCH_ROWS(c, EpiStore, tv, x, EpiStore{y});
 }
 

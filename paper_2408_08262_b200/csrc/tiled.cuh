@@ -39,6 +39,7 @@ struct TileView {
   int group = 1;         // lanes per row of the group kernels (1, 2, 4, 8, 16, 32)
   int nnz = 0;           // > 0: thread-per-row kernels use aligned vector loads (rowdot.cuh)
   int vec = 0;           // entries per vector batch (4 or 8), 0 = scalar loop
+  const int32_t* perm = nullptr;  // thread -> row (rows sorted by length per block), null = identity
 };
 
 // ---- thread per row -----------------------------------------------------------
@@ -57,8 +58,9 @@ struct has_pre<E, std::void_t<typename E::Pre>> : std::true_type {};
 
 template <int VB, bool VEC, class Epi>
 __device__ __forceinline__ void thread_row(const TileView& m, const double* __restrict__ x, Epi& epi) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < m.nrows;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = t < m.nrows;
+  const int i = live && m.perm ? __ldg(m.perm + t) : t;
   int s = 0, e = 0;
   RowBatch<VB, VEC> b;
   if (live) {
@@ -92,8 +94,9 @@ __global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const do
 
 template <int VB, bool VEC, class Epi>
 __device__ __forceinline__ void thread_row_fc(const TileView& m, const double* __restrict__ x, Epi& epi) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < m.nrows;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = t < m.nrows;
+  const int i = live && m.perm ? __ldg(m.perm + t) : t;
   int s = 0, e = 0;
   RowBatch<VB, VEC> b;
   if (live) {
