@@ -550,20 +550,30 @@ def run_gpu(args):
     with torch.cuda.stream(stream):
         xv = torch.rand(n0, dtype=torch.float64, device=ctx.tdev)
         yv = torch.empty(n0, dtype=torch.float64, device=ctx.tdev)
-    reps = 20
+    # (a) back to back: A + x + y = alg_bytes > the 126 MB L2, so the
+    # operands stream from HBM; (b) one launch after an L2 flush (includes
+    # the launch latency of a ~30 us kernel)
     for _ in range(3):
         airg.spmv_device(A0, xv, yv, ctx=ctx)
+    k0, k1 = ev(), ev()
+    reps = 50
+    k0.record(stream)
+    for _ in range(reps):
+        airg.spmv_device(A0, xv, yv, ctx=ctx)
+    k1.record(stream)
+    k1.synchronize()
+    kern_ms = k0.elapsed_time(k1) / reps
     kt = []
-    for _ in range(reps):  # L2 flushed before each launch: HBM-resident operands
+    for _ in range(10):
         with torch.cuda.stream(stream):
             flush.fill_(1.0)
-        k0, k1 = ev(), ev()
-        k0.record(stream)
+        f0, f1 = ev(), ev()
+        f0.record(stream)
         airg.spmv_device(A0, xv, yv, ctx=ctx)
-        k1.record(stream)
-        k1.synchronize()
-        kt.append(k0.elapsed_time(k1))
-    kern_ms = statistics.median(kt)
+        f1.record(stream)
+        f1.synchronize()
+        kt.append(f0.elapsed_time(f1))
+    flushed_ms = statistics.median(kt)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     prof = {}
     pf = os.path.join(REPO, "profiles", "dram_bytes.json")
@@ -597,9 +607,12 @@ def run_gpu(args):
                      "alg_bytes_per_step": step_bytes, "avg_step_ms": ms_per_step, "peak_kind": peak_kind,
                      "reference_op_bytes_per_step": reference_op_bytes(h, int(st.iterations),
                                                                        prm["coarse_iterations"]),
-                     "top_spmv": {"kernel": "rows_thread<EpiStore> on level-0 A (exact CSR SpMV, y = A x)",
+                     "top_spmv": {"kernel": "rows_thread on level-0 A (exact CSR SpMV, y = A x)",
                                   "achieved": achieved, "frac": achieved / peak, "traffic": spmv_traffic,
-                                  "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_ms}},
+                                  "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_ms,
+                                  "timing": "50 back-to-back launches; A + x + y exceed the 126 MB L2",
+                                  "flushed_single_launch_ms": flushed_ms,
+                                  "flushed_single_launch_frac": alg_bytes / (flushed_ms / 1e3) / 1e9 / peak}},
         "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 8 * p.n,
                 "d2h_bytes_per_step": 8 * p.n, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
