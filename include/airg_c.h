@@ -197,6 +197,11 @@ int airg_strength(airg_ctx* ctx, const airg_csr* a, double alpha,
 int airg_pmisr(airg_ctx* ctx, const airg_csr* a, double alpha,
                int64_t max_loops, uint64_t seed, int32_t weight_mode,
                uint8_t* d_labels, double* d_weights);
+/* pmis(strength(a, alpha), swap, seed) (coarsening.cpp:169-217): the
+ * classical PMIS rounds on S u S^T, the paper's comparison splitting; swap
+ * exchanges C and F (PMIS-swap). Labels F = 0, C = 1. */
+int airg_pmis(airg_ctx* ctx, const airg_csr* a, double alpha, int32_t swap, uint64_t seed,
+              uint8_t* d_labels);
 /* pmisr_with_weights (coarsening.hpp:83-84) on a caller-supplied strength
  * pattern S (StrengthGraph::from_pattern) and caller weights (device). */
 int airg_pmisr_with_weights(airg_ctx* ctx, const airg_csr* s_pattern,

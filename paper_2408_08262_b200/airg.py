@@ -75,6 +75,7 @@ def lib() -> C.CDLL:
             "airg_strength": ([_VP, _VP, C.c_double, _P(_VP)], C.c_int),
             "airg_pmisr": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, _VP, _VP], C.c_int),
             "airg_pmisr_with_weights": ([_VP, _VP, C.c_int64, _VP, _VP], C.c_int),
+            "airg_pmis": ([_VP, _VP, C.c_double, C.c_int32, C.c_uint64, _VP], C.c_int),
             "airg_cf_split": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, C.c_int32,
                                C.c_double, C.c_int64, _VP, _VP, _P(abi.CfReport)], C.c_int),
             "airg_ddc": ([_VP, _VP, _VP, C.c_double, C.c_int64, C.c_int32, C.c_double,
@@ -404,6 +405,17 @@ def pmisr_with_weights(s_pattern: SparseMatrix, max_loops: int, weights,
     tw = ctx.to_device(np.asarray(weights, np.float64))
     tl = ctx.empty(max(n, 1), ctx.torch.uint8)
     _check(lib().airg_pmisr_with_weights(ctx.h, d.h, int(max_loops), _ptr(tw), _ptr(tl)))
+    return ctx.to_host(tl)[:n]
+
+
+def pmis(a, alpha=0.5, swap=False, seed=0, ctx: Context | None = None) -> np.ndarray:
+    """pmis(strength(a, alpha), swap, seed) (coarsening.cpp:169-217): the
+    classical PMIS / PMIS-swap baselines of the paper."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    n = d.dims()[0]
+    tl = ctx.empty(max(n, 1), ctx.torch.uint8)
+    _check(lib().airg_pmis(ctx.h, d.h, float(alpha), int(bool(swap)), int(seed) & (2**64 - 1), _ptr(tl)))
     return ctx.to_host(tl)[:n]
 
 

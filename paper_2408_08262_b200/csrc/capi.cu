@@ -319,6 +319,19 @@ int airg_pmisr(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_loops
   });
 }
 
+int airg_pmis(airg_ctx* ctx, const airg_csr* a, double alpha, int32_t swap, uint64_t seed, uint8_t* labels) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(labels, "labels");
+    bind(ctx->c);
+    Strength g;
+    strength(ctx->c, a->m, alpha, g);
+    pmis(ctx->c, g, swap != 0, seed, labels);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
 int airg_pmisr_with_weights(airg_ctx* ctx, const airg_csr* s_pattern, int64_t max_loops,
                             const double* weights, uint8_t* labels) {
   return guard([&] {

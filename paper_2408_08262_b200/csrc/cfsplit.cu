@@ -418,6 +418,56 @@ __global__ void ddc_convert(int nf, const double* __restrict__ theta, const doub
   }
 }
 
+// ---- PMIS / PMIS-swap (coarsening.cpp:169-217; the paper's baselines) -------
+// Rounds over the unassigned nodes: i joins D (-> C) when no unassigned
+// S u S^T neighbour is (w, i)-larger; D's unassigned neighbours -> F. Each
+// round is two passes over S's edges (every edge serves both directions)
+// plus a labelling pass; the set semantics make the rounds order-free.
+constexpr uint8_t kUnassigned = 2;
+__global__ void pmis_marks(int n, const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
+                           const double* __restrict__ w, const uint8_t* __restrict__ label,
+                           uint8_t* __restrict__ notmax) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || label[i] != kUnassigned) return;
+  for (int k = srp[i]; k < srp[i + 1]; ++k) {
+    const int j = sci[k];
+    if (label[j] != kUnassigned) continue;
+    if (weight_less(w, i, j))
+      notmax[i] = 1;
+    else
+      notmax[j] = 1;
+  }
+}
+__global__ void pmis_select(int n, const uint8_t* __restrict__ notmax, uint8_t* __restrict__ label,
+                            uint8_t* __restrict__ in_d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool d = label[i] == kUnassigned && !notmax[i];
+  in_d[i] = d;
+  if (d) label[i] = AIRG_C;
+}
+__global__ void pmis_neighbours(int n, const int32_t* __restrict__ srp, const int32_t* __restrict__ sci,
+                                const uint8_t* __restrict__ in_d, uint8_t* __restrict__ label) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool di = in_d[i];
+  for (int k = srp[i]; k < srp[i + 1]; ++k) {
+    const int j = sci[k];
+    if (di && label[j] == kUnassigned) label[j] = AIRG_F;
+    if (in_d[j] && label[i] == kUnassigned) label[i] = AIRG_F;
+  }
+}
+__global__ void pmis_count(int n, const uint8_t* __restrict__ label, unsigned long long* __restrict__ cnt,
+                           int swap, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool u = false;
+  if (i < n) {
+    u = label[i] == kUnassigned;
+    if (out) out[i] = swap ? (label[i] == AIRG_C ? AIRG_F : AIRG_C) : label[i];
+  }
+  block_add(cnt, u ? 1ull : 0ull);
+}
+
 }  // namespace
 
 void strength(Ctx& c, const Csr& a, double alpha, Strength& g, int row_base) {
@@ -452,6 +502,29 @@ void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weig
   LAUNCH(c, make_weights, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, g.st_cnt.p, key,
          weight_mode, w);
   pmisr_with_weights(c, g, max_loops, w, d_labels);
+}
+
+void pmis(Ctx& c, const Strength& g, bool swap, uint64_t seed, uint8_t* d_labels) {
+  const int n = g.n;
+  if (n == 0) return;
+  DBuf<double> w(c, (size_t)n);
+  const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
+  LAUNCH(c, make_weights, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, g.st_cnt.p, key, 0, w.p);
+  DBuf<uint8_t> label(c, (size_t)n), notmax(c, (size_t)n), in_d(c, (size_t)n);
+  DBuf<unsigned long long> cnt(c, 1);
+  CUDA_CHECK(cudaMemsetAsync(label.p, kUnassigned, n, c.stream));
+  for (int64_t round = 0;; ++round) {
+    if (round > n) throw RuntimeError("pmis: no progress");
+    notmax.zero(c);
+    LAUNCH(c, pmis_marks, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, w.p, label.p, notmax.p);
+    LAUNCH(c, pmis_select, blocks_for(n, 256), 256, 0, n, notmax.p, label.p, in_d.p);
+    LAUNCH(c, pmis_neighbours, blocks_for(n, 256), 256, 0, n, g.rp.p, g.ci.p, in_d.p, label.p);
+    cnt.zero(c);
+    LAUNCH(c, pmis_count, blocks_for(n, 256), 256, 0, n, label.p, cnt.p, 0, (uint8_t*)nullptr);
+    if (read1(c, cnt.p) == 0) break;
+  }
+  cnt.zero(c);
+  LAUNCH(c, pmis_count, blocks_for(n, 256), 256, 0, n, label.p, cnt.p, swap ? 1 : 0, d_labels);
 }
 
 void pmisr_with_weights(Ctx& c, const Strength& g, int64_t max_loops, const double* w,

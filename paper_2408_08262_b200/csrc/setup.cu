@@ -127,8 +127,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     throw InvalidArgument("setup: drop tolerances must be >= 0");
   if (cfg.strength_alpha < 0.0 || cfg.strength_alpha > 1.0)
     throw InvalidArgument("setup: strength_alpha must lie in [0, 1]");
-  if (cfg.cf != 0)
-    throw InvalidArgument("setup: the GPU path implements PMISR splitting (cf = 0) only");
+  if (cfg.cf < 0 || cfg.cf > 2) throw InvalidArgument("setup: cf must be pmisr (0), pmis (1) or pmis-swap (2)");
   if (cfg.prolongation != 0)
     throw InvalidArgument("setup: the GPU path implements one-point prolongation only");
   if (cfg.poly_order + 1 > 32 || cfg.coarse_poly_order + 1 > 32)
@@ -165,7 +164,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     strength(c, L.a, cfg.strength_alpha, g);
     DBuf<uint8_t> labels(c, (size_t)n);
     Blocks blk;
-    if (rs && cfg.weight_mode == 0 && (cfg.ddc_enabled == 0 || cfg.ddc_fraction > 0.0)) {
+    if (rs && cfg.cf == 0 && cfg.weight_mode == 0 && (cfg.ddc_enabled == 0 || cfg.ddc_fraction > 0.0)) {
       // row slabs over the ranks (dist.cu): the labels, all-gathered
       const std::vector<int64_t> sl = rs->slabs(n);
       CfReport rep;
@@ -183,7 +182,10 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
         L.max_theta_pre = dominance_max(c, blk.aff);
       }
     } else {
-      pmisr(c, g, cfg.max_loops, level_seed, cfg.weight_mode, labels.p, nullptr);
+      if (cfg.cf == 0)  // air.cpp:328-338
+        pmisr(c, g, cfg.max_loops, level_seed, cfg.weight_mode, labels.p, nullptr);
+      else
+        pmis(c, g, cfg.cf == 2, level_seed, labels.p);
       build_label_map(c, labels.p, n, L.map);
       L.n_f_pre = L.map.nf;
       extract_blocks(c, L.a, L.map, blk, /*want_af=*/false);

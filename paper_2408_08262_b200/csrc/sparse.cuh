@@ -53,6 +53,9 @@ void pmisr(Ctx& c, const Strength& g, int64_t max_loops, uint64_t seed, int weig
 void pmisr_with_weights(Ctx& c, const Strength& g, int64_t max_loops, const double* d_w,
                         uint8_t* d_labels);
 void strength_from_pattern(Ctx& c, const Csr& s, Strength& g);
+// PMIS / PMIS-swap (coarsening.cpp:169-217): MIS rounds on S u S^T with the
+// (|S_i| + |S_i^T|) + uniform weights; swap exchanges C and F at the end
+void pmis(Ctx& c, const Strength& g, bool swap, uint64_t seed, uint8_t* d_labels);
 
 struct LabelMap {
   int32_t n = 0, nf = 0, nc = 0;

@@ -120,6 +120,39 @@ def test_p4_injected_hierarchy_bit_identical(port, path):
     np.testing.assert_allclose(res.residual_history, g["history"], rtol=1e-9, atol=1e-15)
 
 
+@pytest.mark.parametrize("cf", [1, 2])
+@pytest.mark.parametrize("path", GOLDEN[:4], ids=lambda p: os.path.basename(p)[:-4])
+def test_pmis_baselines_injected_hierarchy(port, path, cf):
+    """The paper's comparison splittings (cli.cpp:141-147: PMIS and PMIS-swap,
+    DDC off): every level's labels and operators bit-identical to the oracle
+    with injected coefficients, and the V-cycle too."""
+    g = np.load(path)
+    prm = dict(_params(g), cf=cf, ddc_enabled=0)
+    n = len(g["rp"]) - 1
+    try:
+        oh = refpy.setup(port, port.mat(n, n, g["rp"], g["ci"], g["v"]), **prm)
+    except RuntimeError as e:  # the baseline may stall; the GPU must stall the same way
+        with pytest.raises(airg.AirgRuntimeError, match="stall"):
+            airg.setup(airg.SparseMatrix.from_arrays(n, n, g["rp"], g["ci"], g["v"]), **prm)
+        return
+    a = airg.SparseMatrix.from_arrays(n, n, g["rp"], g["ci"], g["v"])
+    h = airg.setup(a, injection=_injection(oh, prm), **prm)
+    assert h.n_levels == oh.info().n_levels
+    for l in range(h.n_levels):
+        assert np.array_equal(h.labels(l), oh.labels(l)), l
+        for w in range(7):
+            got = h.matrix(l, w)
+            exp = oh.matrix(l, w).arrays()
+            assert np.array_equal(got.col_indices, exp[1]) and same_bits(got.values, exp[2]), (l, w)
+    ci = prm.get("coarse_iterations", 3)
+    xo = oh.vcycle(g["b"], refpy.abi.solve_config(coarse_iterations=ci))
+    assert same_bits(h.vcycle(g["b"], coarse_iterations=ci), xo)
+    # the bare splitting through the C-ABI (DDC off: the level-0 labels)
+    seed = int(problems.mix(np.uint64(prm.get("seed", 0)), np.uint64(0)))
+    lab = airg.pmis(a, prm["strength_alpha"], swap=cf == 2, seed=seed)
+    assert np.array_equal(lab, oh.labels(0))
+
+
 @pytest.mark.parametrize("path", GOLDEN, ids=lambda p: os.path.basename(p)[:-4])
 def test_p5_native_solve_within_tolerance(port, path):
     g = np.load(path)
@@ -209,7 +242,9 @@ def test_edge_cases():
     with pytest.raises(airg.InvalidArgument):
         airg.DeviceCSR.upload(airg.SparseMatrix(1, 1, np.array([0, 1]), np.array([0]), np.array([np.nan])))
     with pytest.raises(airg.InvalidArgument):
-        airg.setup(a, cf=1)  # PMIS baselines are out of the GPU scope
+        airg.setup(a, cf=3)
+    with pytest.raises(airg.AirgRuntimeError, match="stall"):  # test_air.cpp:280-291
+        airg.setup(airg.SparseMatrix.identity(50), cf=1, ddc_enabled=0, coarse_size_target=5, poly_order=2)
     z = airg.SparseMatrix.from_triplets(3, 3, [(0, 0, 1.0), (0, 1, 2.0), (1, 0, 3.0), (2, 2, 1.0)])
     lab, _, _ = airg.cf_split(z, 0.5, 3, 0, ddc_enabled=True)
     assert set(np.unique(lab)) <= {0, 1}
