@@ -6,6 +6,7 @@
 // airgraph:: entry points through ctypes with the same plain-pointer shapes
 // as include/airg_c.h. Nothing here is product code; the product never
 // loads oracle/_ref.
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -19,6 +20,7 @@
 #include "airgraph/gmres_poly.hpp"
 #include "airgraph/matrix_market.hpp"
 #include "airgraph/partition_model.hpp"
+#include "airgraph/reports.hpp"
 #include "airgraph/solve.hpp"
 #include "airgraph/sparse.hpp"
 #include "airgraph/transport.hpp"
@@ -339,6 +341,33 @@ int ref_hier_info(const void* hp, airg_hier_info* info) {
     info->operator_complexity = h.metrics.operator_complexity;
     info->storage_complexity = h.metrics.storage_complexity;
   });
+}
+// reports.hpp: hierarchy_report(h).dump() and csv_row(h, stats, ...) for the
+// report-schema tests (the solve statistics come from the caller)
+int ref_hier_report(const void* hp, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    const std::string js = hierarchy_report(h).dump();
+    *len = static_cast<int64_t>(js.size());
+    if (out && cap > 0) std::snprintf(out, (size_t)cap, "%s", js.c_str());
+  });
+}
+int ref_csv_row(const void* hp, int64_t iterations, double work_units, int32_t converged, double final_relres,
+                double alpha, const char* cf_name, uint64_t seed, char* out, int64_t cap) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    SolveStats st;
+    st.iterations = iterations;
+    st.work_units = work_units;
+    st.converged = converged != 0;
+    st.final_relative_residual = final_relres;
+    const std::string row = csv_row(h, st, alpha, cf_name, seed);
+    std::snprintf(out, (size_t)cap, "%s", row.c_str());
+  });
+}
+int ref_csv_header(char* out, int64_t cap) {
+  std::snprintf(out, (size_t)cap, "%s", csv_header().c_str());
+  return AIRG_OK;
 }
 int ref_level_info(const void* hp, int64_t l, airg_level_info* info) {
   return guard([&] {

@@ -329,6 +329,25 @@ class Hier:
         m._keep = self
         return m
 
+    def report(self) -> str:
+        """reports.cpp hierarchy_report(h).dump() (reference build only)."""
+        f = self.lib.lib.ref_hier_report
+        f.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+        n = C.c_int64()
+        self.lib._chk(f(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.lib._chk(f(self.h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def csv_row(self, st, alpha, cf_name, seed) -> str:
+        f = self.lib.lib.ref_csv_row
+        f.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_char_p,
+                      C.c_uint64, C.c_char_p, C.c_int64]
+        buf = C.create_string_buffer(1024)
+        self.lib._chk(f(self.h, int(st.iterations), float(st.work_units), int(bool(st.converged)),
+                        float(st.final_relative_residual), float(alpha), cf_name.encode(), int(seed), buf, 1024))
+        return buf.value.decode()
+
     def labels(self, l):
         n = self.level(l).n
         out = np.zeros(n, np.uint8)

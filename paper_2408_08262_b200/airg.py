@@ -506,8 +506,11 @@ MATRICES = {"a": 0, "a_ff": 1, "a_fc": 2, "a_cf": 3, "ff_inv": 4, "r": 5, "p": 6
 class Hierarchy:
     """A device-resident airgraph::Hierarchy (air.hpp:76-91)."""
 
-    def __init__(self, ctx: Context, h, top_n: int):
+    def __init__(self, ctx: Context, h, top_n: int, cfg: "abi.SetupConfig | None" = None):
         self.ctx, self.h, self.top_n = ctx, h, top_n
+        cfg = cfg or abi.setup_config()
+        self.coarse_poly_order = int(cfg.coarse_poly_order)  # GmresPolynomial::order of the coarse solver
+        self.coarse_iterations = int(cfg.coarse_iterations)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -610,7 +613,7 @@ def setup(a, injection: dict | None = None, ctx: Context | None = None, nranks: 
     else:
         _check(lib().airg_setup(ctx.h, d.h, C.byref(cfg), inj_p, C.byref(out)))
     del keep
-    return Hierarchy(ctx, out, d.dims()[0])
+    return Hierarchy(ctx, out, d.dims()[0], cfg)
 
 
 @dataclass
