@@ -258,6 +258,8 @@ struct Csr {
   int8_t row_mode = 0;  // 0 unbuilt, 1 thread (group) per row, 2 warp tiles
   int8_t group = 1;     // lanes per row in row_mode 1 (tiled.cuh rows_group)
   DBuf<int32_t> perm;   // thread -> row, rows sorted by length within each block (AIRG_SORT)
+  DBuf<uint16_t> c16;   // 16-bit column deltas from cbase (AIRG_C16), built on demand
+  DBuf<int32_t> cbase;
   // SELL-32-sigma copy for the solve (sell.cuh), built on demand
   DBuf<int32_t> s_off, s_len, s_perm, s_ci;
   DBuf<double> s_v;

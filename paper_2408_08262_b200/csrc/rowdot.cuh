@@ -227,4 +227,52 @@ __device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const i
   dot_fc_src<VB, VEC>(s, e, nnz, ci, v, XDirect{x}, b, sf, sc);
 }
 
+// ---- 16-bit column deltas (AIRG_C16): col = cbase[row] + c16[k], cbase the
+// row's first column; rows of a matrix must span < 65536 columns. 10 B per
+// entry instead of 12; the arithmetic is unchanged. Groups of 8 entries are
+// 16-byte aligned (one int4 of deltas, four double2 of values).
+struct RowBatch16 {
+  unsigned short c[8];
+  double a[8];
+  __device__ __forceinline__ void load(int k0, int e, int nnz, const uint16_t* __restrict__ c16,
+                                       const double* __restrict__ v) {
+    if (k0 + 8 <= nnz) {
+      const int4 u = __ldg(reinterpret_cast<const int4*>(c16 + k0));
+      const unsigned w[4] = {(unsigned)u.x, (unsigned)u.y, (unsigned)u.z, (unsigned)u.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        c[2 * q] = (unsigned short)(w[q] & 0xffffu);
+        c[2 * q + 1] = (unsigned short)(w[q] >> 16);
+        const double2 p = __ldg(reinterpret_cast<const double2*>(v + k0 + 2 * q));
+        a[2 * q] = p.x;
+        a[2 * q + 1] = p.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = k0 + j < nnz ? __ldg(c16 + k0 + j) : (unsigned short)0;
+        a[j] = k0 + j < nnz ? __ldg(v + k0 + j) : 0.0;
+      }
+    }
+    (void)e;
+  }
+};
+
+__device__ __forceinline__ double dot16(int s, int e, int base, int nnz, const uint16_t* __restrict__ c16,
+                                        const double* __restrict__ v, const double* __restrict__ x,
+                                        RowBatch16& b) {
+  double acc = 0.0;
+  const int k00 = s & ~7;
+  for (int k0 = k00; k0 < e; k0 += 8) {
+    if (k0 != k00) b.load(k0, e, nnz, c16, v);
+    double xv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + base + b.c[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (k0 + j >= s && k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(b.a[j], xv[j]));
+  }
+  return acc;
+}
+
 }  // namespace airg

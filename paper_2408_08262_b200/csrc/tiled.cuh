@@ -40,6 +40,8 @@ struct TileView {
   int nnz = 0;           // > 0: thread-per-row kernels use aligned vector loads (rowdot.cuh)
   int vec = 0;           // entries per vector batch (4 or 8), 0 = scalar loop
   const int32_t* perm = nullptr;  // thread -> row (rows sorted by length per block), null = identity
+  const uint16_t* c16 = nullptr;  // 16-bit column deltas (rowdot.cuh dot16), null = int32 columns
+  const int32_t* cbase = nullptr;
 };
 
 // ---- thread per row -----------------------------------------------------------
@@ -89,6 +91,33 @@ template <class Epi, bool VEC = false, int VB = kRowBatch>
 __global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const double* __restrict__ x,
                                                             Epi epi) {
   thread_row<VB, VEC>(m, x, epi);
+  epi.finish();
+}
+
+// the same row kernel over 16-bit column deltas
+template <class Epi>
+__global__ void __launch_bounds__(kTileThreads) rows_thread16(TileView m, const double* __restrict__ x, Epi epi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < m.nrows;
+  int s = 0, e = 0, base = 0;
+  RowBatch16 b;
+  if (live) {
+    s = __ldg(m.rp + i);
+    e = __ldg(m.rp + i + 1);
+    base = __ldg(m.cbase + i);
+    if (s < e) b.load(s & ~7, e, m.nnz, m.c16, m.v);
+  }
+  if constexpr (has_pre<Epi>::value) {
+    typename Epi::Pre pre{};
+    if (live) pre = epi.pre(i);
+    pdl_wait();
+    pdl_trigger();
+    if (live) epi.row_pre(i, dot16(s, e, base, m.nnz, m.c16, m.v, x, b), pre);
+  } else {
+    pdl_wait();
+    pdl_trigger();
+    if (live) epi.row(i, dot16(s, e, base, m.nnz, m.c16, m.v, x, b));
+  }
   epi.finish();
 }
 
@@ -381,7 +410,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group, Epi, view, x, epi)                                  \
     else {                                                                           \
-      auto* kfn__ = (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;   \
+      auto* kfn__ = (view).c16 ? &rows_thread16<Epi> : (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;   \
       LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);              \
     }                                                                                \
   } while (0)
@@ -393,7 +422,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
     else {                                                                                      \
-      auto* kfn__ = (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;              \
+      auto* kfn__ = (view).c16 ? &rows_thread16<Epi> : (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;              \
       LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
     }                                                                                           \
   } while (0)

@@ -43,6 +43,7 @@ LAYOUTS = {
     "early_fres1": {"AIRG_EARLY": "1"},
     "split_fres1": {"AIRG_SPLIT": "1"},
     "sorted_rows": {"AIRG_SORT": "1"},
+    "c16": {"AIRG_C16": "1"},
     "tail_off": {"AIRG_TAIL_N": "0"},
     "tail_cluster_all": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "100000000"},
     "tail_cluster_small": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "2000"},
@@ -53,7 +54,8 @@ LAYOUTS = {
 def _run(env_extra):
     env = dict(os.environ)
     for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N", "AIRG_TAIL",
-              "AIRG_DEVLOOP", "AIRG_EARLY", "AIRG_SPLIT", "AIRG_SORT"):
+              "AIRG_DEVLOOP", "AIRG_EARLY", "AIRG_SPLIT", "AIRG_SORT",
+              "AIRG_C16"):
         env.pop(k, None)
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
