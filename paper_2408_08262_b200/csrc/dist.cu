@@ -155,21 +155,43 @@ __global__ void k_pack(int64_t n, const int32_t* __restrict__ idx, const double*
 }
 
 // solve kernels (local versions of solve.cu's)
-__global__ void k_prolong_l(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
-                            double* __restrict__ x) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = i < n ? __ldg(pmap + i) : -1;
+// four rows per thread (int4 map load, double2 stores); the owned slices
+// start at the buffers' bases, 16-byte aligned
+__device__ __forceinline__ double prolong_one_l(int j, const double* __restrict__ ec) {
+  const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
+  return __dadd_rn(0.0, __dmul_rn(1.0, pe));
+}
+__global__ void k_prolong4_l(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
+                             double* __restrict__ x) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n4 = n >> 2;
+  int4 j = make_int4(-1, -1, -1, -1);
+  if (q < n4) j = __ldg(reinterpret_cast<const int4*>(pmap) + q);
   pdl_wait();
   pdl_trigger();
-  if (i >= n) return;
-  const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
-  x[i] = __dadd_rn(0.0, __dmul_rn(1.0, pe));
+  if (q == n4) {
+    for (int i = 4 * n4; i < n; ++i) x[i] = prolong_one_l(__ldg(pmap + i), ec);
+    return;
+  }
+  if (q > n4) return;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  x2[2 * q] = make_double2(prolong_one_l(j.x, ec), prolong_one_l(j.y, ec));
+  x2[2 * q + 1] = make_double2(prolong_one_l(j.z, ec), prolong_one_l(j.w, ec));
 }
 __global__ void k_axpy1_l(int n, const double* __restrict__ e, double* __restrict__ x) {
   pdl_wait();
   pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(1.0, e[i]));
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;  // two entries per thread
+  const int n2 = n >> 1;
+  if (q < n2) {
+    const double2 ev = reinterpret_cast<const double2*>(e)[q];
+    double2 xv = reinterpret_cast<double2*>(x)[q];
+    xv.x = __dadd_rn(xv.x, __dmul_rn(1.0, ev.x));
+    xv.y = __dadd_rn(xv.y, __dmul_rn(1.0, ev.y));
+    reinterpret_cast<double2*>(x)[q] = xv;
+  } else if (q == n2 && (n & 1)) {
+    x[n - 1] = __dadd_rn(x[n - 1], __dmul_rn(1.0, e[n - 1]));
+  }
 }
 __global__ void k_sum(const double* __restrict__ part, int np, double* __restrict__ out) {
   __shared__ double sm[32];
@@ -200,9 +222,15 @@ struct LFres1 {
   const int32_t* f2f;
   double* rf;
   double* sc;
-  __device__ void row2(int k, double sf, double s) const {
+  // operands written two or more kernels back, loaded before the PDL wait
+  // (solve.cu explains the rule; halo exchanges in between only add order)
+  struct Pre {
+    double bb;
+  };
+  __device__ Pre pre(int k) const { return Pre{b[f2f[k]]}; }
+  __device__ void row2_pre(int k, double sf, double s, const Pre& p) const {
     sc[k] = s;
-    rf[k] = __dsub_rn(__dsub_rn(b[f2f[k]], sf), s);
+    rf[k] = __dsub_rn(__dsub_rn(p.bb, sf), s);
   }
 };
 struct LFres2 {
@@ -210,40 +238,58 @@ struct LFres2 {
   const int32_t* f2f;
   const double* sc;
   double* rf;
-  __device__ void row(int k, double sf) const { rf[k] = __dsub_rn(__dsub_rn(b[f2f[k]], sf), sc[k]); }
   __device__ void finish() const {}
+  struct Pre {
+    double bb, s;
+  };
+  __device__ Pre pre(int k) const { return Pre{b[f2f[k]], sc[k]}; }
+  __device__ void row_pre(int k, double sf, const Pre& p) const { rf[k] = __dsub_rn(__dsub_rn(p.bb, sf), p.s); }
 };
 struct LFupd {
   const int32_t* f2f;
   double* x;
-  __device__ void row(int k, double d) const {
-    const int i = f2f[k];
-    x[i] = __dadd_rn(x[i], d);
-  }
   __device__ void finish() const {}
+  struct Pre {
+    int i;
+    double x0;
+  };
+  __device__ Pre pre(int k) const {
+    const int i = f2f[k];
+    return Pre{i, x[i]};
+  }
+  __device__ void row_pre(int, double d, const Pre& p) const { x[p.i] = __dadd_rn(p.x0, d); }
 };
 struct LCres {
   const double* rhs;
   double* r;
-  __device__ void row(int i, double acc) const { r[i] = __dsub_rn(rhs[i], acc); }
   __device__ void finish() const {}
+  struct Pre {
+    double rr;
+  };
+  __device__ Pre pre(int i) const { return Pre{rhs[i]}; }
+  __device__ void row_pre(int i, double acc, const Pre& p) const { r[i] = __dsub_rn(p.rr, acc); }
 };
 struct LCupd {
   double* e;
   int first;
-  __device__ void row(int i, double acc) const {
-    const double e0 = first ? 0.0 : e[i];
-    e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
-  }
   __device__ void finish() const {}
+  struct Pre {
+    double e0;
+  };
+  __device__ Pre pre(int i) const { return Pre{first ? 0.0 : e[i]}; }
+  __device__ void row_pre(int i, double acc, const Pre& p) const { e[i] = __dadd_rn(p.e0, __dmul_rn(1.0, acc)); }
 };
 struct LResid {
   const double* b;
   double* r;
   double* part;
   mutable double s;
-  __device__ void row(int i, double acc) const {
-    const double ri = __dsub_rn(b[i], acc);
+  struct Pre {  // the right-hand side is constant during the solve
+    double bb;
+  };
+  __device__ Pre pre(int i) const { return Pre{b[i]}; }
+  __device__ void row_pre(int i, double acc, const Pre& p) const {
+    const double ri = __dsub_rn(p.bb, acc);
     r[i] = ri;
     s = fma(ri, ri, s);
   }
@@ -263,7 +309,24 @@ struct LResid {
   }
 };
 
-inline TileView rows_of(const Csr& m) { return TileView{m.rp.p, m.ci.p, m.v.p, nullptr, 0, m.n}; }
+inline TileView rows_of(const Csr& m) {
+  return TileView{m.rp.p, m.ci.p, m.v.p, nullptr, 0, m.n, 1, (int)m.nnz, row_vec(m.n, m.nnz)};
+}
+// thread-per-row kernels in the batch kind of the matrix (tiled.cuh)
+template <class Epi>
+void launch_rows(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
+  const TileView v = rows_of(m);
+  auto* k = v.vec == 8 ? &rows_thread<Epi, true> : v.vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;
+  LAUNCH_PDL(c, k, blocks_for(m.n, kTileThreads), kTileThreads, 0, v, x, epi);
+}
+template <class Epi>
+void launch_rows_fc(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
+  const TileView v = rows_of(m);
+  auto* k = v.vec == 8   ? &rows_thread_fc<Epi, true, kFcVecBatch>
+            : v.vec == 4 ? &rows_thread_fc<Epi, false, 4>
+                         : &rows_thread_fc<Epi, false>;
+  LAUNCH_PDL(c, k, blocks_for(m.n, kTileThreads), kTileThreads, 0, v, x, epi);
+}
 
 // ---- host helpers ---------------------------------------------------------------
 // partition_rows (partition_model.cpp:8-22) on `active` logical ranks, logical
@@ -1032,8 +1095,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
     rank_loop([&](int r) {
       const Csr& R = D.rk[r].R;
       if (R.n)
-        LAUNCH_PDL(c, rows_thread<LStore>, blocks_for(R.n, kTileThreads), kTileThreads, 0, rows_of(R),
-                   (const double*)D.B.rk[r].buf.p, LStore{Bn.rk[r].buf.p});
+        launch_rows(c, R, (const double*)D.B.rk[r].buf.p, LStore{Bn.rk[r].buf.p});
     });
   }
   // coarse solve on the coarse owner(s); CB and CR feed Ac^-1 through CR's
@@ -1051,16 +1113,14 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
       rank_loop([&](int r) {
         const Csr& A = d.rk[r].AC;
         if (A.n)
-          LAUNCH_PDL(c, rows_thread<LCres>, blocks_for(A.n, kTileThreads), kTileThreads, 0, rows_of(A),
-                     (const double*)d.CX.rk[r].buf.p, (LCres{d.CB.rk[r].buf.p, d.CR.rk[r].buf.p}));
+          launch_rows(c, A, (const double*)d.CX.rk[r].buf.p, LCres{d.CB.rk[r].buf.p, d.CR.rk[r].buf.p});
       });
     }
     exchange(c, d, d.CR);
     rank_loop([&](int r) {
       const Csr& A = d.rk[r].ACI;
       if (A.n)
-        LAUNCH_PDL(c, rows_thread<LCupd>, blocks_for(A.n, kTileThreads), kTileThreads, 0, rows_of(A),
-                   (const double*)d.CR.rk[r].buf.p, (LCupd{d.CX.rk[r].buf.p, it == 0 ? 1 : 0}));
+        launch_rows(c, A, (const double*)d.CR.rk[r].buf.p, LCupd{d.CX.rk[r].buf.p, it == 0 ? 1 : 0});
     });
   }
   // ascent
@@ -1071,7 +1131,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
     rank_loop([&](int r) {
       const DLevel::Rank& R = D.rk[r];
       if (R.n_own)
-        LAUNCH_PDL(c, k_prolong_l, blocks_for(R.n_own, 128), 128, 0, (int)R.n_own, R.pmap.p,
+        LAUNCH_PDL(c, k_prolong4_l, blocks_for(R.n_own / 4 + 1, 256), 256, 0, (int)R.n_own, R.pmap.p,
                    Xn.rk[r].buf.p, D.X.rk[r].buf.p);
     });
     for (int64_t s = 0; s < cfg.up_f_smooths; ++s) {
@@ -1081,20 +1141,15 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
         if (!R.nf_own) return;
         const double* bl = D.B.rk[r].buf.p;
         if (s == 0)
-          LAUNCH_PDL(c, rows_thread_fc<LFres1>, blocks_for(R.AF.n, kTileThreads), kTileThreads, 0,
-                     rows_of(R.AF), (const double*)D.X.rk[r].buf.p,
-                     (LFres1{bl, R.f2f.p, D.RF.rk[r].buf.p, R.sc.p}));
+          launch_rows_fc(c, R.AF, (const double*)D.X.rk[r].buf.p, LFres1{bl, R.f2f.p, D.RF.rk[r].buf.p, R.sc.p});
         else
-          LAUNCH_PDL(c, rows_thread<LFres2>, blocks_for(R.AFFG.n, kTileThreads), kTileThreads, 0,
-                     rows_of(R.AFFG), (const double*)D.X.rk[r].buf.p,
-                     (LFres2{bl, R.f2f.p, R.sc.p, D.RF.rk[r].buf.p}));
+          launch_rows(c, R.AFFG, (const double*)D.X.rk[r].buf.p, LFres2{bl, R.f2f.p, R.sc.p, D.RF.rk[r].buf.p});
       });
       exchange(c, d, D.RF);
       rank_loop([&](int r) {
         DLevel::Rank& R = D.rk[r];
         if (!R.nf_own) return;
-        LAUNCH_PDL(c, rows_thread<LFupd>, blocks_for(R.FINV.n, kTileThreads), kTileThreads, 0,
-                   rows_of(R.FINV), (const double*)D.RF.rk[r].buf.p, (LFupd{R.f2f.p, D.X.rk[r].buf.p}));
+        launch_rows(c, R.FINV, (const double*)D.RF.rk[r].buf.p, LFupd{R.f2f.p, D.X.rk[r].buf.p});
       });
     }
   }
@@ -1109,7 +1164,7 @@ void enqueue_update_residual(Ctx& c, DHier& d) {
     if (!d.mine(r)) continue;
     const int64_t own = d.XS.rk[r].own;
     if (own)
-      LAUNCH_PDL(c, k_axpy1_l, blocks_for(own, 256), 256, 0, (int)own, (const double*)E.rk[r].buf.p,
+      LAUNCH_PDL(c, k_axpy1_l, blocks_for(own / 2 + 1, 256), 256, 0, (int)own, (const double*)E.rk[r].buf.p,
                  d.XS.rk[r].buf.p);
   }
   exchange(c, d, d.XS);
@@ -1117,9 +1172,8 @@ void enqueue_update_residual(Ctx& c, DHier& d) {
     if (!d.mine(r)) continue;
     const Csr& A = d.rk[r].A0;
     if (A.n)
-      LAUNCH_PDL(c, rows_thread<LResid>, blocks_for(A.n, kTileThreads), kTileThreads, 0, rows_of(A),
-                 (const double*)d.XS.rk[r].buf.p,
-                 (LResid{d.rk[r].rhs.p, Rv.rk[r].buf.p, d.part.p + d.part_off[r], 0.0}));
+      launch_rows(c, A, (const double*)d.XS.rk[r].buf.p,
+                  LResid{d.rk[r].rhs.p, Rv.rk[r].buf.p, d.part.p + d.part_off[r], 0.0});
     else
       CUDA_CHECK(cudaMemsetAsync(d.part.p + d.part_off[r], 0, sizeof(double), c.stream));
   }
