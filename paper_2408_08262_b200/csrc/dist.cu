@@ -731,6 +731,18 @@ void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const s
   if ((int)starts.size() != P + 1 || starts[0] != 0 || starts[P] != a.n)
     throw InvalidArgument("dist: slab starts must cover the matrix");
   if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0)) throw InvalidArgument("ddc: fraction must be in (0, 1]");
+  if (P == 1) {  // one slab: no halo -- the fused one-GPU split (cfsplit.cu)
+    const CfFused f = cf_split_fused(c, a, alpha, seed, ddc_enabled, fraction, bins, d_labels, nullptr);
+    rep = CfReport();
+    rep.s_nnz = f.s_nnz;
+    rep.n_f_pre = f.n_f_pre;
+    rep.n_converted = f.n_converted;
+    rep.n_f = f.n_f_pre - f.n_converted;
+    rep.max_theta = f.max_theta;
+    rep.alpha_diag = f.alpha_diag;
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return;
+  }
   DHier d;
   d.P = P;
   d.me = me;
