@@ -515,6 +515,9 @@ void exchange(Ctx& c, DHier& d, DVec& V) {
   if (ns) LAUNCH_PDL(c, k_pack, blocks_for(ns, 256), 256, 0, ns, M.send_idx.p, M.buf.p, M.send_buf.p);
   bool any = ns > 0 || M.nhalo > 0;
   for (int q = 0; q < P && !any; ++q) any = M.send_cnt[q] || M.recv_cnt[q];
+  // no traffic of mine: no peer sends to or receives from me either (a send
+  // list is the owner's view of a peer's receive list), so no NCCL call
+  if (!any) return;
   NCCL_CHECK(ncclGroupStart());
   for (int q = 0; q < P; ++q) {
     if (q == d.me) continue;
@@ -706,6 +709,9 @@ void reverse_add(Ctx& c, DHier& d, DVec& V) {
   }
   if (P == 1) return;
   DVec::Rank& M = V.rk[d.me];
+  bool any = M.nhalo > 0;
+  for (int q = 0; q < P && !any; ++q) any = M.send_cnt[q] || M.recv_cnt[q];
+  if (!any) return;  // no traffic of mine in either direction
   NCCL_CHECK(ncclGroupStart());
   for (int q = 0; q < P; ++q) {
     if (q == d.me) continue;
