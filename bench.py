@@ -385,6 +385,14 @@ def run_gpu_dist(args):
     tot_ms, e2e_ms = float(t[0]), float(t[1])
     value = p.n * args.steps / (tot_ms / 1e3)
     levels = [d.level_info(l) for l in range(h.n_levels + 1)]
+    # roofline of the whole distributed solve step against the N GPUs' HBM
+    peak, peak_kind = hbm_peak()
+    step_bytes = solve_alg_bytes(h, int(st.iterations), prm["coarse_iterations"])
+    step_ach = step_bytes / (tot_ms / args.steps / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": step_ach, "peak": peak * ws, "unit": "GB/s",
+            "frac": step_ach / (peak * ws), "traffic": None, "peak_kind": peak_kind,
+            "kernel": f"one distributed AIRG solve step over {ws} GPUs (all row kernels + halo exchanges)",
+            "alg_bytes_per_step": step_bytes, "avg_step_ms": tot_ms / args.steps}
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -400,6 +408,7 @@ def run_gpu_dist(args):
         "e2e": {"value": p.n / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
                 "d2h_bytes_per_step": 8 * int(hi - lo), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches), "cf_split_ms": cf_ms,
+        "roofline": roof,
         "clocks": clk.summary(), "cpu_baseline": None,
     }
     if rank == 0:
