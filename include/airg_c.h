@@ -220,6 +220,18 @@ int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha,
                   int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
                   uint8_t* d_labels, uint8_t* d_labels_pre,
                   airg_cf_report* report);
+/* airg_cf_split (weight_mode 0) on `count` matrices with one
+ * synchronisation: the splits are enqueued back to back on the context
+ * stream and their reports read once at the end (e.g. re-splitting every
+ * level of a hierarchy, or many independent systems). seeds[i], d_labels[i]
+ * and reports[i] belong to mats[i]; labels are identical to one
+ * airg_cf_split call per matrix. No reference counterpart (batching of
+ * air.cpp:466-494 over matrices). */
+int airg_cf_split_batch(airg_ctx* ctx, const airg_csr* const* mats,
+                        int64_t count, const uint64_t* seeds, double alpha,
+                        int64_t max_loops, int32_t ddc_enabled,
+                        double ddc_fraction, int64_t ddc_bins,
+                        uint8_t* const* d_labels, airg_cf_report* reports);
 /* airg_cf_split with the labels returned to host memory. */
 int airg_cf_split_host(airg_ctx* ctx, const airg_csr* a, double alpha,
                        int64_t max_loops, uint64_t seed, int32_t weight_mode,

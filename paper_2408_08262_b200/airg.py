@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
             "airg_pmis": ([_VP, _VP, C.c_double, C.c_int32, C.c_uint64, _VP], C.c_int),
             "airg_cf_split": ([_VP, _VP, C.c_double, C.c_int64, C.c_uint64, C.c_int32, C.c_int32,
                                C.c_double, C.c_int64, _VP, _VP, _P(abi.CfReport)], C.c_int),
+            "airg_cf_split_batch": ([_VP, _VP, C.c_int64, _VP, C.c_double, C.c_int64, C.c_int32,
+                                     C.c_double, C.c_int64, _VP, _P(abi.CfReport)], C.c_int),
             "airg_ddc": ([_VP, _VP, _VP, C.c_double, C.c_int64, C.c_int32, C.c_double,
                           _P(abi.CfReport)], C.c_int),
             "airg_extract_blocks": ([_VP, _VP, _VP, _P(_VP), _P(_VP), _P(_VP)], C.c_int),
@@ -457,6 +459,26 @@ def cf_split_device(d: DeviceCSR, alpha=0.5, max_loops=3, seed=0, weight_mode=0,
                                int(weight_mode), int(ddc_enabled), float(ddc_fraction), int(ddc_bins),
                                _ptr(tl), None, C.byref(rep)))
     return tl, rep
+
+
+def cf_split_batch_device(mats, seeds, alpha=0.5, max_loops=3, ddc_enabled=True, ddc_fraction=0.1,
+                          ddc_bins=1000, labels=None, ctx: Context | None = None):
+    """airg_cf_split_batch: cf_split (weight mode 0) of several device
+    matrices with one synchronisation -> (device label tensors, reports)."""
+    mats = list(mats)
+    ctx = ctx or (mats[0].ctx if mats else default_context())
+    k = len(mats)
+    if labels is None:
+        labels = [ctx.empty(max(m.dims()[0], 1), ctx.torch.uint8) for m in mats]
+    hs = (_VP * max(k, 1))(*[m.h for m in mats])
+    sd = np.asarray([int(x) & (2**64 - 1) for x in seeds], dtype=np.uint64)
+    if len(sd) != k:
+        raise ValueError("cf_split_batch: one seed per matrix")
+    lp = (_VP * max(k, 1))(*[_ptr(t) for t in labels])
+    reps = (abi.CfReport * max(k, 1))()
+    _check(lib().airg_cf_split_batch(ctx.h, hs, k, sd.ctypes.data, float(alpha), int(max_loops),
+                                     int(ddc_enabled), float(ddc_fraction), int(ddc_bins), lp, reps))
+    return labels, [reps[i] for i in range(k)]
 
 
 def spmv_device(d: DeviceCSR, tx, ty, ctx: Context | None = None) -> None:

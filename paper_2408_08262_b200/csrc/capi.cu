@@ -405,6 +405,46 @@ int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha, int64_t max_lo
   });
 }
 
+int airg_cf_split_batch(airg_ctx* ctx, const airg_csr* const* mats, int64_t count, const uint64_t* seeds,
+                        double alpha, int64_t max_loops, int32_t ddc_enabled, double ddc_fraction,
+                        int64_t ddc_bins, uint8_t* const* labels, airg_cf_report* reps) {
+  return guard([&] {
+    need(ctx, "context");
+    if (count < 0) throw InvalidArgument("cf_split_batch: count must be >= 0");
+    if (count == 0) return;
+    need(mats, "matrices");
+    need(seeds, "seeds");
+    need(labels, "labels");
+    need(reps, "reports");
+    if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
+    for (int64_t i = 0; i < count; ++i) {
+      need(mats[i], "matrix");
+      if (mats[i]->m.n) need(labels[i], "labels");
+    }
+    bind(ctx->c);
+    Ctx& c = ctx->c;
+    DBuf<unsigned long long> u(c, 8 * (size_t)count);
+    for (int64_t i = 0; i < count; ++i)
+      cf_split_fused_enqueue(c, mats[i]->m, alpha, seeds[i], ddc_enabled != 0, ddc_fraction, ddc_bins, labels[i],
+                             nullptr, u.p + 8 * i);
+    std::vector<unsigned long long> hu(8 * (size_t)count);
+    to_host(c, hu.data(), u.p, hu.size());
+    for (int64_t i = 0; i < count; ++i) {
+      const CfFused f = cf_split_fused_finish(c, hu.data() + 8 * i, ddc_enabled != 0, labels[i]);
+      airg_cf_report r;
+      std::memset(&r, 0, sizeof r);
+      r.n_f_pre = f.n_f_pre;
+      r.s_nnz = f.s_nnz;
+      r.max_theta = f.max_theta;
+      r.alpha_diag = f.alpha_diag;
+      r.n_converted = f.n_converted;
+      r.n_f = r.n_f_pre - r.n_converted;
+      r.n_c = mats[i]->m.n - r.n_f;
+      reps[i] = r;
+    }
+  });
+}
+
 int airg_ddc(airg_ctx* ctx, const airg_csr* a, uint8_t* labels, double fraction, int64_t bins,
              int32_t selection, double direct_alpha, airg_cf_report* rep) {
   return guard([&] {

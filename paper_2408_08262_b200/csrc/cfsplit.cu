@@ -842,15 +842,22 @@ void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned lo
   LAUNCH(c, fcf_select, 1, kSelThreads, 0, d_nf, 0ll, d_hist, bins, fraction, d_maxbits, 0, 0.0, d_out);
 }
 
-CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
-                       double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre) {
+const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double alpha, uint64_t seed,
+                                                 bool ddc_enabled, double fraction, int64_t bins,
+                                                 uint8_t* d_labels, uint8_t* d_labels_pre,
+                                                 unsigned long long* d_u_out) {
   if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
   if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0))
     throw InvalidArgument("ddc: fraction must be in (0, 1]");
   if (ddc_enabled && bins < 1) throw InvalidArgument("dominance_report: bins >= 1");
-  CfFused r;
   const int n = a.n;
-  if (n == 0) return r;
+  if (n == 0) {
+    if (d_u_out) {
+      CUDA_CHECK(cudaMemsetAsync(d_u_out, 0, 8 * sizeof(unsigned long long), c.stream));
+      CUDA_CHECK(cudaMemsetAsync(d_u_out + 3, 0xff, 8, c.stream));
+    }
+    return d_u_out;
+  }
   const unsigned g = blocks_for(n, 256);
   // one scratch block: [u: 8 x u64 | hist: bins x u64 | thr | w | theta | sel(2)] doubles,
   // then [s_cnt | st_cnt] int32, then notmin bytes
@@ -890,8 +897,13 @@ CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool d
            u + 4);
   }
   (void)sel;
-  unsigned long long hu[8];
-  to_host(c, hu, u, 8);
+  if (!d_u_out) return u;
+  CUDA_CHECK(cudaMemcpyAsync(d_u_out, u, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c.stream));
+  return d_u_out;
+}
+
+CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_enabled, const uint8_t* d_labels) {
+  CfFused r;
   double hs[2];
   std::memcpy(hs, hu + 5, sizeof hs);
   if (ddc_enabled && hu[3] != ~0ull) {
@@ -909,6 +921,16 @@ CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool d
   r.alpha_diag = hs[0];
   r.max_theta = hs[1];
   return r;
+}
+
+CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
+                       double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre) {
+  const unsigned long long* u =
+      cf_split_fused_enqueue(c, a, alpha, seed, ddc_enabled, fraction, bins, d_labels, d_labels_pre, nullptr);
+  if (!u) return CfFused{};
+  unsigned long long hu[8];
+  to_host(c, hu, u, 8);
+  return cf_split_fused_finish(c, hu, ddc_enabled, d_labels);
 }
 
 }  // namespace airg

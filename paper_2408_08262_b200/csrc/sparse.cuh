@@ -89,6 +89,16 @@ struct CfFused {
 };
 CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
                        double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre);
+// The same split without the readback: the 8 report counters land in
+// d_u_out (or stay in the context scratch when d_u_out is null; the pointer
+// used is returned, null for an empty matrix without d_u_out); the finish
+// step turns the host copy of the counters into the report and raises the
+// zero-diagonal error. Lets several splits share one synchronisation.
+const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double alpha, uint64_t seed,
+                                                 bool ddc_enabled, double fraction, int64_t bins,
+                                                 uint8_t* d_labels, uint8_t* d_labels_pre,
+                                                 unsigned long long* d_u_out);
+CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_enabled, const uint8_t* d_labels);
 // coarsening.cpp:290-315 on device counters: d_out = {alpha_diag, max_theta}
 void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,
                        double fraction, const unsigned long long* d_maxbits, double* d_out);

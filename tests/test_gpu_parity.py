@@ -76,13 +76,25 @@ def test_p2_every_level_cf_split(port, path):
     prm = _params(g)
     n = len(g["rp"]) - 1
     oh = refpy.setup(port, port.mat(n, n, g["rp"], g["ci"], g["v"]), **prm)
+    mats, seeds, reps = [], [], []
     for l in range(oh.info().n_levels):
         rp, ci, v = oh.matrix(l, 0).arrays()
         a = airg.SparseMatrix.from_arrays(len(rp) - 1, len(rp) - 1, rp, ci, v)
         seed = int(problems.mix(np.uint64(prm.get("seed", 0)), np.uint64(l)))
-        lab, _, _ = airg.cf_split(a, prm["strength_alpha"], prm.get("max_loops", 3), seed,
-                                  ddc_fraction=prm.get("ddc_fraction", 0.1))
+        lab, _, rep = airg.cf_split(a, prm["strength_alpha"], prm.get("max_loops", 3), seed,
+                                    ddc_fraction=prm.get("ddc_fraction", 0.1))
         assert np.array_equal(lab, oh.labels(l)), f"level {l}"
+        mats.append(airg.DeviceCSR.upload(a))
+        seeds.append(seed)
+        reps.append(rep)
+    # every level in one batched call (one synchronisation): same labels and reports
+    bl, br = airg.cf_split_batch_device(mats, seeds, prm["strength_alpha"], prm.get("max_loops", 3),
+                                        ddc_fraction=prm.get("ddc_fraction", 0.1))
+    for l, (t, r) in enumerate(zip(bl, br)):
+        assert np.array_equal(t.cpu().numpy()[: len(oh.labels(l))], oh.labels(l)), f"batched level {l}"
+        assert (r.n_f, r.n_f_pre, r.n_converted, r.s_nnz) == \
+            (reps[l].n_f, reps[l].n_f_pre, reps[l].n_converted, reps[l].s_nnz)
+        assert same_bits([r.max_theta, r.alpha_diag], [reps[l].max_theta, reps[l].alpha_diag])
 
 
 @pytest.mark.parametrize("path", GOLDEN, ids=lambda p: os.path.basename(p)[:-4])
@@ -248,6 +260,13 @@ def test_edge_cases():
     z = airg.SparseMatrix.from_triplets(3, 3, [(0, 0, 1.0), (0, 1, 2.0), (1, 0, 3.0), (2, 2, 1.0)])
     lab, _, _ = airg.cf_split(z, 0.5, 3, 0, ddc_enabled=True)
     assert set(np.unique(lab)) <= {0, 1}
+    # batched split: empty batch, an empty matrix, and the same labels as one call
+    assert airg.cf_split_batch_device([], [], ctx=h.ctx) == ([], [])
+    e = airg.DeviceCSR.upload(airg.SparseMatrix(0, 0, np.array([0]), np.array([], np.int64), np.array([])))
+    bl, br = airg.cf_split_batch_device([airg.DeviceCSR.upload(z), e], [0, 0])
+    assert np.array_equal(bl[0].cpu().numpy()[:3], lab) and br[1].n_f == 0 and br[1].n_c == 0
+    with pytest.raises(airg.InvalidArgument):
+        airg.cf_split_batch_device([airg.DeviceCSR.upload(z)], [0], max_loops=0)
 
 
 def test_solve_device_api_matches_host_api():
