@@ -684,103 +684,139 @@ double dominance_max(Ctx& c, const Csr& aff, int rb) {
 // Same arithmetic as the kernels above, so the same labels bit for bit.
 namespace {
 
+// Visit the entries k = s..e-1 of one row in order, f(ci[k], v[k]). VEC:
+// the aligned body as 16-byte loads (4 column indices, 2 x 2 values) --
+// fewer, wider loads per thread for long rows; same order, same results.
+template <bool VEC, class F>
+__device__ __forceinline__ void for_row(const int32_t* __restrict__ ci, const double* __restrict__ v, int s,
+                                        int e, F&& f) {
+  int k = s;
+  if (VEC) {
+    for (; k < e && (k & 3); ++k) f(__ldg(ci + k), __ldg(v + k));
+    for (; k + 4 <= e; k += 4) {
+      const int4 c = __ldg(reinterpret_cast<const int4*>(ci + k));
+      const double2 a = __ldg(reinterpret_cast<const double2*>(v + k));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(v + k + 2));
+      f(c.x, a.x);
+      f(c.y, a.y);
+      f(c.z, b.x);
+      f(c.w, b.y);
+    }
+  }
+  for (; k < e; ++k) f(__ldg(ci + k), __ldg(v + k));
+}
+
+// long rows (mean >= AIRG_CF_VEC, default 6) take the 16-byte path
+int cf_vec_rows() {
+  static const int v = [] {
+    const char* e = getenv("AIRG_CF_VEC");
+    return e ? atoi(e) : 6;
+  }();
+  return v;
+}
+
+// lanes per row of the three row passes: AIRG_CF_GROUP = 4, 8 or 16
+// (otherwise thread per row, the measured default)
+int cf_group() {
+  static const int g = [] {
+    const char* e = getenv("AIRG_CF_GROUP");
+    const int v = e ? atoi(e) : 0;
+    return v == 4 || v == 8 || v == 16 ? v : 0;
+  }();
+  return g;
+}
+
+// The PMISR weight of row j (coarsening.cpp:50-63): |S_j| + |S^T_j| plus
+// the seeded hash fraction, rebuilt from the counts wherever it is needed
+// (no weight array, no weight pass). cnt[j] = {|S_j|, |S^T_j|}.
+__device__ __forceinline__ double fcf_weight(const int2* __restrict__ cnt, uint64_t key, int j) {
+  const int2 c = cnt[j];
+  const double u = (double)(mix(key, (uint64_t)j) >> 11) * 0x1.0p-53;
+  return __dadd_rn((double)((int64_t)c.x + c.y), u);
+}
+
+// Labels without a label pass: a row with no strong connection (weight < 1)
+// is never marked "not minimal", so the PMISR label is F exactly when
+// notmin == 0 -- the mark array IS the pre-DDC label array.
+
+template <bool VEC>
 __global__ void fcf_rows(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                          const double* __restrict__ v, double alpha, double* __restrict__ thr,
-                         int32_t* __restrict__ s_cnt, int32_t* __restrict__ st_cnt,
-                         unsigned long long* __restrict__ s_total) {
+                         int2* __restrict__ cnt, unsigned long long* __restrict__ s_total) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int cnt = 0;
+  int c_i = 0;
   if (i < n) {
     const int s = rp[i], e = rp[i + 1];
     double off_max = 0.0;
-    for (int k = s; k < e; ++k)
-      if (ci[k] != i) off_max = fmax(off_max, fabs(v[k]));
+    for_row<VEC>(ci, v, s, e, [&](int c, double x) {
+      if (c != i) off_max = fmax(off_max, fabs(x));
+    });
     const double t = __dmul_rn(alpha, off_max);
     thr[i] = t;
-    for (int k = s; k < e; ++k) {
-      const double mag = fabs(v[k]);
-      const int c = ci[k];
+    for_row<VEC>(ci, v, s, e, [&](int c, double x) {
+      const double mag = fabs(x);
       if (c != i && mag > 0.0 && mag >= t) {
-        ++cnt;
-        atomicAdd(st_cnt + c, 1);
+        ++c_i;
+        atomicAdd(&cnt[c].y, 1);
       }
-    }
-    s_cnt[i] = cnt;
+    });
+    cnt[i].x = c_i;
   }
-  block_add(s_total, (unsigned long long)cnt);
+  block_add(s_total, (unsigned long long)c_i);
 }
 
-__global__ void fcf_weights(int n, const int32_t* __restrict__ s_cnt, const int32_t* __restrict__ st_cnt,
-                            uint64_t stream_key, double* __restrict__ w) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t deg = (int64_t)s_cnt[i] + st_cnt[i];
-  const double u = (double)(mix(stream_key, (uint64_t)i) >> 11) * 0x1.0p-53;
-  w[i] = __dadd_rn((double)deg, u);
-}
-
+template <bool VEC>
 __global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ v, const double* __restrict__ thr,
-                          const double* __restrict__ w, uint8_t* __restrict__ notmin) {
+                          const int2* __restrict__ cnt, uint64_t key, uint8_t* __restrict__ notmin) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double t = thr[i];
+  const double wi = fcf_weight(cnt, key, i);
   bool mine = false;
-  for (int k = rp[i]; k < rp[i + 1]; ++k) {
-    const int j = ci[k];
-    const double mag = fabs(v[k]);
-    if (j == i || !(mag > 0.0) || !(mag >= t)) continue;
-    if (weight_less(w, j, i))
+  for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
+    const double mag = fabs(x);
+    if (j == i || !(mag > 0.0) || !(mag >= t)) return;
+    const double wj = fcf_weight(cnt, key, j);
+    if (wj != wi ? wj < wi : j < i)  // weight_less(w, j, i)
       mine = true;
     else
       notmin[j] = 1;
-  }
+  });
   if (mine) notmin[i] = 1;
 }
 
-__global__ void fcf_labels(int n, const uint8_t* __restrict__ notmin, const double* __restrict__ w,
-                           uint8_t* __restrict__ label, unsigned long long* __restrict__ nf) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  bool f = false;
-  if (i < n) {
-    f = w[i] < 1.0 || !notmin[i];
-    label[i] = f ? AIRG_F : AIRG_C;
-  }
-  block_add(nf, f ? 1ull : 0ull);
-}
-
-// theta of an F row over A's F columns in column order (= its A_ff row)
+// theta of an F row over A's F columns in column order (= its A_ff row);
+// also the optional copy of the PMISR labels
+template <bool VEC>
 __global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                          const double* __restrict__ v, const uint8_t* __restrict__ label,
-                          double* __restrict__ theta, unsigned long long* __restrict__ maxbits,
-                          unsigned long long* __restrict__ bad_row) {
+                          const double* __restrict__ v, const uint8_t* __restrict__ notmin,
+                          double* __restrict__ theta, uint8_t* __restrict__ label_pre,
+                          unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad_row) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long tb = 0;
-  if (i < n && label[i] == AIRG_F) {
+  const bool fr = i < n && !notmin[i];
+  if (label_pre && i < n) label_pre[i] = fr ? AIRG_F : AIRG_C;
+  if (fr) {
     double off = 0.0, diag = 0.0;
     bool seen = false;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
-      const int j = ci[k];
-      if (label[j] != AIRG_F) continue;
+    for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
+      if (notmin[j]) return;
       if (j == i) {
-        diag = fabs(v[k]);
+        diag = fabs(x);
         seen = true;
       } else {
-        off = __dadd_rn(off, fabs(v[k]));
+        off = __dadd_rn(off, fabs(x));
       }
-    }
+    });
     if (!seen || diag == 0.0) {
-      atomicMin(bad_row, (unsigned long long)i);
+      atomicMax(bad_row, ~(unsigned long long)i);  // ~i: the max is the first bad row
       theta[i] = 0.0;
     } else {
       const double t = __ddiv_rn(off, diag);
@@ -791,9 +827,159 @@ __global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* 
   block_max(maxbits, tb);
 }
 
-__global__ void fcf_hist(int n, const uint8_t* __restrict__ label, const double* __restrict__ theta,
+// ---- G lanes per row (coalesced: lane l reads entries s+l, s+l+G, ...) ----
+// Max, counts and marks are order-free; theta's off-diagonal sum keeps the
+// column order with a shuffle chain (skipped entries add +0.0, an identity
+// on a sum of magnitudes), so every variant gives the same bits.
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int G>
+__global__ void fcf_rows_g(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, double alpha, double* __restrict__ thr,
+                           int2* __restrict__ cnt, unsigned long long* __restrict__ s_total) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & (G - 1);
+  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  int s = 0, e = 0;
+  if (i < n) {
+    s = rp[i];
+    e = rp[i + 1];
+  }
+  double om = 0.0;
+  for (int k = s + lane; k < e; k += G)
+    if (__ldg(ci + k) != i) om = fmax(om, fabs(__ldg(v + k)));
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) om = fmax(om, __shfl_xor_sync(kFull, om, o, G));
+  const double t = __dmul_rn(alpha, om);
+  int c_i = 0;
+  for (int k = s + lane; k < e; k += G) {
+    const int c = __ldg(ci + k);
+    const double mag = fabs(__ldg(v + k));
+    if (c != i && mag > 0.0 && mag >= t) {
+      ++c_i;
+      atomicAdd(&cnt[c].y, 1);
+    }
+  }
+  block_add(s_total, (unsigned long long)c_i);
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) c_i += __shfl_xor_sync(kFull, c_i, o, G);
+  if (lane == 0 && i < n) {
+    thr[i] = t;
+    cnt[i].x = c_i;
+  }
+}
+
+template <int G>
+__global__ void fcf_marks_g(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ thr,
+                            const int2* __restrict__ cnt, uint64_t key, uint8_t* __restrict__ notmin) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & (G - 1);
+  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  int s = 0, e = 0;
+  double t = 0.0, wi = 0.0;
+  if (i < n) {
+    s = rp[i];
+    e = rp[i + 1];
+    t = thr[i];
+    wi = fcf_weight(cnt, key, i);
+  }
+  int mine = 0;
+  for (int k = s + lane; k < e; k += G) {
+    const int j = __ldg(ci + k);
+    const double mag = fabs(__ldg(v + k));
+    if (j == i || !(mag > 0.0) || !(mag >= t)) continue;
+    const double wj = fcf_weight(cnt, key, j);
+    if (wj != wi ? wj < wi : j < i)
+      mine = 1;
+    else
+      notmin[j] = 1;
+  }
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) mine |= __shfl_xor_sync(kFull, mine, o, G);
+  if (mine && lane == 0 && i < n) notmin[i] = 1;
+}
+
+template <int G>
+__global__ void fcf_theta_g(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const uint8_t* __restrict__ notmin,
+                            double* __restrict__ theta, uint8_t* __restrict__ label_pre,
+                            unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad_row) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & (G - 1);
+  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  const bool fr = i < n && !notmin[i];
+  if (label_pre && i < n && lane == 0) label_pre[i] = fr ? AIRG_F : AIRG_C;
+  int s = 0, e = 0;
+  if (fr) {
+    s = rp[i];
+    e = rp[i + 1];
+  }
+  double off = 0.0, diag = 0.0;
+  int seen = 0;
+  // the trip count is uniform per group, not per warp: shuffle within the group
+  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << ((threadIdx.x & 31) & ~(G - 1));
+  for (int base = s; base < e; base += G) {
+    const int k = base + lane;
+    double val = 0.0;
+    if (k < e) {
+      const int j = __ldg(ci + k);
+      if (!notmin[j]) {
+        const double mag = fabs(__ldg(v + k));
+        if (j == i) {
+          diag = mag;
+          seen = 1;
+        } else {
+          val = mag;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) off = __dadd_rn(off, __shfl_sync(gmask, val, q, G));
+  }
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) {
+    diag = fmax(diag, __shfl_xor_sync(kFull, diag, o, G));
+    seen |= __shfl_xor_sync(kFull, seen, o, G);
+  }
+  unsigned long long tb = 0;
+  if (fr && lane == 0) {
+    if (!seen || diag == 0.0) {
+      atomicMax(bad_row, ~(unsigned long long)i);
+      theta[i] = 0.0;
+    } else {
+      const double q = __ddiv_rn(off, diag);
+      theta[i] = q;
+      tb = (unsigned long long)__double_as_longlong(q);
+    }
+  }
+  block_max(maxbits, tb);
+}
+
+// no DDC: write the PMISR labels and count F
+__global__ void fcf_labels(int n, const uint8_t* __restrict__ notmin, uint8_t* __restrict__ label,
+                           unsigned long long* __restrict__ nf) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool f = false;
+  if (i < n) {
+    f = !notmin[i];
+    label[i] = f ? AIRG_F : AIRG_C;
+  }
+  block_add(nf, f ? 1ull : 0ull);
+}
+
+// histogram of theta over the F rows (coarsening.cpp:290-315) and the F
+// count. Rows of equal theta are common (structured operators), so lanes
+// of a warp that hit the same bin add once (match + popc) instead of
+// serialising on one shared-memory address.
+__global__ void fcf_hist(int n, const uint8_t* __restrict__ notmin, const double* __restrict__ theta,
                          const unsigned long long* __restrict__ maxbits, int64_t bins,
-                         unsigned long long* __restrict__ hist) {
+                         unsigned long long* __restrict__ hist, unsigned long long* __restrict__ nf) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ unsigned int sh[];
@@ -803,34 +989,47 @@ __global__ void fcf_hist(int n, const uint8_t* __restrict__ label, const double*
   __syncthreads();
   const double mx = __longlong_as_double((long long)*maxbits);
   const double width = mx > 0.0 ? __ddiv_rn(mx, (double)bins) : 1.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (label[i] != AIRG_F) continue;
-    int64_t b = (int64_t)__ddiv_rn(theta[i], width);
-    if (b > bins - 1) b = bins - 1;
-    if (priv)
-      atomicAdd(sh + b, 1u);
-    else
-      atomicAdd(hist + b, 1ull);
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {  // uniform trip count
+    const int64_t i = base + threadIdx.x;
+    long long b = -1;
+    if (i < n && !notmin[i]) {
+      b = (long long)__ddiv_rn(theta[i], width);
+      if (b > bins - 1) b = bins - 1;
+      ++cnt;
+    }
+    const unsigned peers = __match_any_sync(kFull, b);
+    if (b >= 0 && lane == __ffs(peers) - 1) {
+      if (priv)
+        atomicAdd(sh + b, (unsigned)__popc(peers));
+      else
+        atomicAdd(hist + b, (unsigned long long)__popc(peers));
+    }
   }
-  __syncthreads();
+  block_add(nf, cnt);
   if (priv)
     for (int b = threadIdx.x; b < bins; b += blockDim.x)
       if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
 }
 
-__global__ void fcf_convert(int n, const double* __restrict__ theta, const double* __restrict__ sel,
-                            const unsigned long long* __restrict__ bad_row, uint8_t* __restrict__ label,
-                            unsigned long long* __restrict__ count) {
+// the one-shot conversion (coarsening.cpp:322-328) writing the final labels
+// (the PMISR labels when a row had a zero diagonal: the split then fails)
+__global__ void fcf_convert(int n, const uint8_t* __restrict__ notmin, const double* __restrict__ theta,
+                            const double* __restrict__ sel, const unsigned long long* __restrict__ bad_row,
+                            uint8_t* __restrict__ label, unsigned long long* __restrict__ count) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool conv = false;
-  if (i < n && *bad_row == ~0ull && label[i] == AIRG_F) {
-    const double t = theta[i];
-    if (t > sel[0] && t != 0.0) {
-      label[i] = AIRG_C;
-      conv = true;
+  if (i < n) {
+    const bool f = !notmin[i];
+    if (f && *bad_row == 0) {
+      const double t = theta[i];
+      conv = t > sel[0] && t != 0.0;
     }
+    label[i] = f && !conv ? AIRG_F : AIRG_C;
   }
   block_add(count, conv ? 1ull : 0ull);
 }
@@ -852,51 +1051,56 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   if (ddc_enabled && bins < 1) throw InvalidArgument("dominance_report: bins >= 1");
   const int n = a.n;
   if (n == 0) {
-    if (d_u_out) {
-      CUDA_CHECK(cudaMemsetAsync(d_u_out, 0, 8 * sizeof(unsigned long long), c.stream));
-      CUDA_CHECK(cudaMemsetAsync(d_u_out + 3, 0xff, 8, c.stream));
-    }
+    if (d_u_out) CUDA_CHECK(cudaMemsetAsync(d_u_out, 0, 8 * sizeof(unsigned long long), c.stream));
     return d_u_out;
   }
   const unsigned g = blocks_for(n, 256);
-  // one scratch block: [u: 8 x u64 | hist: bins x u64 | thr | w | theta | sel(2)] doubles,
-  // then [s_cnt | st_cnt] int32, then notmin bytes
+  // one scratch block, zeroed by ONE memset up to notmin:
+  //   [u: 8 x u64 | hist: bins x u64 | cnt: n x {|S_i|, |S^T_i|} | notmin: n bytes | pad]
+  //   [thr: n doubles | theta: n doubles]
   const size_t nb = ddc_enabled ? (size_t)bins : 0;
-  const size_t dbl = 8 + nb + 3 * (size_t)n + 2;
-  const size_t bytes = dbl * 8 + 2 * (size_t)n * 4 + (size_t)n + 16;
+  const size_t zero_bytes = (8 + nb) * 8 + (size_t)n * 8 + (size_t)n;
+  const size_t head = (zero_bytes + 15) & ~(size_t)15;
+  const size_t bytes = head + 2 * (size_t)n * 8;
   uint8_t* base = static_cast<uint8_t*>(ctx_scratch(c, bytes));
   unsigned long long* u = reinterpret_cast<unsigned long long*>(base);
   unsigned long long* hist = u + 8;
-  double* thr = reinterpret_cast<double*>(hist + nb);
-  double* w = thr + n;
-  double* theta = w + n;
-  double* sel = theta + n;
-  int32_t* cnt = reinterpret_cast<int32_t*>(sel + 2);
-  uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + 2 * (size_t)n);
-  // u: [0] |S| [1] n_f_pre [2] max theta bits [3] bad row [4] converted
-  //    [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
-  CUDA_CHECK(cudaMemsetAsync(u, 0, (8 + nb) * 8, c.stream));
-  CUDA_CHECK(cudaMemsetAsync(u + 3, 0xff, 8, c.stream));
-  CUDA_CHECK(cudaMemsetAsync(cnt + n, 0, sizeof(int32_t) * n, c.stream));
-  CUDA_CHECK(cudaMemsetAsync(notmin, 0, n, c.stream));
-  LAUNCH_PDL(c, fcf_rows, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, cnt + n, u);
+  int2* cnt = reinterpret_cast<int2*>(hist + nb);
+  uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + n);
+  double* thr = reinterpret_cast<double*>(base + head);
+  double* theta = thr + n;
+  // u: [0] |S| [1] n_f_pre [2] max theta bits [3] ~(first bad row), 0 = none
+  //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
+  CUDA_CHECK(cudaMemsetAsync(base, 0, zero_bytes, c.stream));
+  const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
+  auto* k_rows = vec ? fcf_rows<true> : fcf_rows<false>;
+  auto* k_marks = vec ? fcf_marks<true> : fcf_marks<false>;
+  auto* k_theta = vec ? fcf_theta<true> : fcf_theta<false>;
+  unsigned gr = g;  // grid of the three row passes
+  const int G = cf_group();
+  if (G > 1) {
+    gr = blocks_for((int64_t)n * G, 256);
+    k_rows = G == 4 ? fcf_rows_g<4> : G == 8 ? fcf_rows_g<8> : fcf_rows_g<16>;
+    k_marks = G == 4 ? fcf_marks_g<4> : G == 8 ? fcf_marks_g<8> : fcf_marks_g<16>;
+    k_theta = G == 4 ? fcf_theta_g<4> : G == 8 ? fcf_theta_g<8> : fcf_theta_g<16>;
+  }
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
-  LAUNCH_PDL(c, fcf_weights, g, 256, 0, n, cnt, cnt + n, key, w);
-  LAUNCH_PDL(c, fcf_marks, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, w, notmin);
-  LAUNCH_PDL(c, fcf_labels, g, 256, 0, n, notmin, w, d_labels, u + 1);
-  if (d_labels_pre)
-    CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
+  LAUNCH_PDL(c, k_rows, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, u);
+  LAUNCH_PDL(c, k_marks, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, cnt, key, notmin);
   if (ddc_enabled) {
-    LAUNCH_PDL(c, fcf_theta, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, d_labels, theta, u + 2, u + 3);
+    LAUNCH_PDL(c, k_theta, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, notmin, theta, d_labels_pre, u + 2, u + 3);
     const unsigned hb = (unsigned)std::min<int64_t>(g, 4 * c.num_sms);
     const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
-    LAUNCH_PDL(c, fcf_hist, hb, 256, smem, n, d_labels, theta, u + 2, bins, hist);
+    LAUNCH_PDL(c, fcf_hist, hb, 256, smem, n, notmin, theta, u + 2, bins, hist, u + 1);
     LAUNCH_PDL(c, fcf_select, 1, kSelThreads, 0, u + 1, 0ll, hist, bins, fraction, u + 2, 0, 0.0,
-           reinterpret_cast<double*>(u + 5));
-    LAUNCH_PDL(c, fcf_convert, g, 256, 0, n, theta, reinterpret_cast<const double*>(u + 5), u + 3, d_labels,
-           u + 4);
+               reinterpret_cast<double*>(u + 5));
+    LAUNCH_PDL(c, fcf_convert, g, 256, 0, n, notmin, theta, reinterpret_cast<const double*>(u + 5), u + 3,
+               d_labels, u + 4);
+  } else {
+    LAUNCH_PDL(c, fcf_labels, g, 256, 0, n, notmin, d_labels, u + 1);
+    if (d_labels_pre)
+      CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
   }
-  (void)sel;
   if (!d_u_out) return u;
   CUDA_CHECK(cudaMemcpyAsync(d_u_out, u, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c.stream));
   return d_u_out;
@@ -906,10 +1110,10 @@ CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_ena
   CfFused r;
   double hs[2];
   std::memcpy(hs, hu + 5, sizeof hs);
-  if (ddc_enabled && hu[3] != ~0ull) {
+  if (ddc_enabled && hu[3] != 0) {
     // the reference names the A_ff row: the F sub-index of the fine row
-    // (fcf_convert leaves the labels untouched when a row was bad)
-    std::vector<uint8_t> lab((size_t)hu[3]);
+    // (fcf_convert writes the PMISR labels when a row was bad)
+    std::vector<uint8_t> lab((size_t)~hu[3]);
     if (!lab.empty()) to_host(c, lab.data(), d_labels, lab.size());
     int64_t sub = 0;
     for (uint8_t l : lab) sub += l == AIRG_F;

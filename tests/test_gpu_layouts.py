@@ -68,3 +68,49 @@ def test_all_layouts_bit_identical():
     for name, env in LAYOUTS.items():
         if name != "thread":
             assert _run(env) == base, f"layout {name} differs from thread-per-row"
+
+
+CF_SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+out = []
+for cfg, scale in ((2, 0.1875), (3, 0.125), (4, 0.25)):
+    p = problems.make(cfg, scale)
+    prm = dict(problems.setup_params(cfg), coarse_size_target=300)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    lab = np.concatenate([h.labels(l) for l in range(h.n_levels)])
+    reps = [(h.level(l).max_theta_pre, h.level(l).alpha_diag, h.level(l).ddc_converted) for l in range(h.n_levels)]
+    out.append(hashlib.sha256(lab.tobytes() + repr(reps).encode()).hexdigest()[:16])
+print(" ".join(out))
+""" % REPO
+
+CF_VARIANTS = {
+    "legacy": {"AIRG_CF": "legacy"},
+    "fused_scalar": {"AIRG_CF_VEC": "100000"},
+    "fused_vec": {"AIRG_CF_VEC": "1"},
+    "fused_g4": {"AIRG_CF_GROUP": "4"},
+    "fused_g8": {"AIRG_CF_GROUP": "8"},
+    "fused_g16": {"AIRG_CF_GROUP": "16"},
+    "fused_default": {},
+}
+
+
+def test_cf_split_variants_bit_identical():
+    """The fused split's row-pass variants (scalar, 16-byte loads, G lanes
+    per row) and the step-by-step split give the same hierarchy labels and
+    DDC reports on every level (C2/C3/C4, reduced)."""
+    def run(extra):
+        env = dict(os.environ)
+        for k in ("AIRG_CF", "AIRG_CF_VEC", "AIRG_CF_GROUP"):
+            env.pop(k, None)
+        env.update(extra)
+        out = subprocess.run([sys.executable, "-c", CF_SCRIPT], env=env, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr[-3000:]
+        return out.stdout.strip().split("\n")[-1]
+    base = run(CF_VARIANTS["legacy"])
+    for name, env in CF_VARIANTS.items():
+        if name != "legacy":
+            assert run(env) == base, f"CF variant {name} differs from the step-by-step split"
