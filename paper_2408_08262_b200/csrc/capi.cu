@@ -127,6 +127,7 @@ int airg_ctx_destroy(airg_ctx* ctx) {
     bind(ctx->c);
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.scratch) cudaFree(ctx->c.scratch);
+    if (ctx->c.grid_bar) cudaFree(ctx->c.grid_bar);
     if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;

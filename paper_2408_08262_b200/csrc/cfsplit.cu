@@ -291,17 +291,16 @@ __global__ void theta_hist(int nf, const double* __restrict__ theta,
 // the winner -- identical to the serial scan, without ~bins dependent
 // global loads on one thread. Falls back to the serial scan for bins > 8192.
 constexpr int kSelThreads = 1024;
-__global__ void __launch_bounds__(kSelThreads)
-fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
-           const unsigned long long* __restrict__ hist, int64_t bins, double fraction,
-           const unsigned long long* __restrict__ maxbits, int selection, double direct_alpha,
-           double* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
+// one block of kSelThreads threads (the kernel below, or block 0 of the
+// persistent small-level split)
+__device__ __forceinline__ void ddc_select_block(const unsigned long long* __restrict__ nfp, long long nf_val,
+                                                 const unsigned long long* __restrict__ hist, int64_t bins,
+                                                 double fraction, const unsigned long long* __restrict__ maxbits,
+                                                 int selection, double direct_alpha, double* __restrict__ out) {
   __shared__ unsigned suf[8192 + 1];  // counts <= n_f < 2^31
   __shared__ double werr[kSelThreads / 32];
   __shared__ int64_t wk[kSelThreads / 32];
-  const double max_theta = __longlong_as_double((long long)*maxbits);
+  const double max_theta = __longlong_as_double((long long)__ldcg(maxbits));
   const int t = threadIdx.x;
   if (selection == 2 || max_theta == 0.0) {  // direct alpha (DdcSelection::direct) / nothing dominant
     if (t == 0) {
@@ -310,13 +309,13 @@ fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
     }
     return;
   }
-  const double target = __dmul_rn(fraction, (double)(nfp ? (long long)*nfp : nf_val));
+  const double target = __dmul_rn(fraction, (double)(nfp ? (long long)__ldcg(nfp) : nf_val));
   if (bins > 8192) {  // serial scan
     if (t != 0) return;
     int64_t above = 0, best_k = bins;
     double best_err = fabs(__dsub_rn((double)above, target));
     for (int64_t k = bins; k-- > 0;) {
-      above += (int64_t)hist[k];
+      above += (int64_t)__ldcg(hist + k);
       const double err = fabs(__dsub_rn((double)above, target));
       if (err < best_err) {
         best_err = err;
@@ -328,7 +327,7 @@ fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
     return;
   }
   const int nb = (int)bins;
-  for (int k = t; k < nb; k += kSelThreads) suf[k] = (unsigned)hist[k];
+  for (int k = t; k < nb; k += kSelThreads) suf[k] = (unsigned)__ldcg(hist + k);
   if (t == 0) suf[nb] = 0;
   __syncthreads();
   // suffix sums: each thread owns a contiguous chunk; serial within, scan of chunk totals
@@ -404,6 +403,16 @@ fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
       out[1] = max_theta;
     }
   }
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+fcf_select(const unsigned long long* __restrict__ nfp, long long nf_val,
+           const unsigned long long* __restrict__ hist, int64_t bins, double fraction,
+           const unsigned long long* __restrict__ maxbits, int selection, double direct_alpha,
+           double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  ddc_select_block(nfp, nf_val, hist, bins, fraction, maxbits, selection, direct_alpha, out);
 }
 
 __global__ void ddc_convert(int nf, const double* __restrict__ theta, const double* __restrict__ sel,
@@ -739,6 +748,95 @@ __device__ __forceinline__ double fcf_weight(const int2* __restrict__ cnt, uint6
 // is never marked "not minimal", so the PMISR label is F exactly when
 // notmin == 0 -- the mark array IS the pre-DDC label array.
 
+// Loads of data written earlier in the same launch (the persistent
+// small-level split) bypass L1: COH = true -> ld.global.cg.
+template <bool COH, class T>
+__device__ __forceinline__ T ldc(const T* p) {
+  if constexpr (COH)
+    return __ldcg(p);
+  else
+    return *p;
+}
+
+template <bool COH>
+__device__ __forceinline__ double fcf_weight_c(const int2* cnt, uint64_t key, int j) {
+  const int2 c = ldc<COH>(cnt + j);
+  const double u = (double)(mix(key, (uint64_t)j) >> 11) * 0x1.0p-53;
+  return __dadd_rn((double)((int64_t)c.x + c.y), u);
+}
+
+// ---- one row of each pass (thread per row) ----
+// strength: thr_i = alpha * max off-diagonal |a_ij|, |S_i|, |S^T| atomics
+template <bool VEC>
+__device__ __forceinline__ int fcf_row_strength(int i, const int32_t* __restrict__ rp,
+                                                const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                                double alpha, double* thr, int2* cnt) {
+  const int s = rp[i], e = rp[i + 1];
+  double off_max = 0.0;
+  for_row<VEC>(ci, v, s, e, [&](int c, double x) {
+    if (c != i) off_max = fmax(off_max, fabs(x));
+  });
+  const double t = __dmul_rn(alpha, off_max);
+  thr[i] = t;
+  int c_i = 0;
+  for_row<VEC>(ci, v, s, e, [&](int c, double x) {
+    const double mag = fabs(x);
+    if (c != i && mag > 0.0 && mag >= t) {
+      ++c_i;
+      atomicAdd(&cnt[c].y, 1);
+    }
+  });
+  cnt[i].x = c_i;
+  return c_i;
+}
+
+// not-minimal marks over the strong entries of row i
+template <bool VEC, bool COH>
+__device__ __forceinline__ void fcf_row_marks(int i, const int32_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                              const double* thr, const int2* cnt, uint64_t key, uint8_t* notmin) {
+  const double t = ldc<COH>(thr + i);
+  const double wi = fcf_weight_c<COH>(cnt, key, i);
+  bool mine = false;
+  for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
+    const double mag = fabs(x);
+    if (j == i || !(mag > 0.0) || !(mag >= t)) return;
+    const double wj = fcf_weight_c<COH>(cnt, key, j);
+    if (wj != wi ? wj < wi : j < i)  // weight_less(w, j, i)
+      mine = true;
+    else
+      notmin[j] = 1;
+  });
+  if (mine) notmin[i] = 1;
+}
+
+// theta of F row i (its A_ff row); returns the bits for the max
+template <bool VEC, bool COH>
+__device__ __forceinline__ unsigned long long fcf_row_theta(int i, const int32_t* __restrict__ rp,
+                                                            const int32_t* __restrict__ ci,
+                                                            const double* __restrict__ v, const uint8_t* notmin,
+                                                            double* theta, unsigned long long* bad_row) {
+  double off = 0.0, diag = 0.0;
+  bool seen = false;
+  for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
+    if (ldc<COH>(notmin + j)) return;
+    if (j == i) {
+      diag = fabs(x);
+      seen = true;
+    } else {
+      off = __dadd_rn(off, fabs(x));
+    }
+  });
+  if (!seen || diag == 0.0) {
+    atomicMax(bad_row, ~(unsigned long long)i);  // ~i: the max is the first bad row
+    theta[i] = 0.0;
+    return 0;
+  }
+  const double t = __ddiv_rn(off, diag);
+  theta[i] = t;
+  return (unsigned long long)__double_as_longlong(t);  // t >= 0: bit order = value order
+}
+
 template <bool VEC>
 __global__ void fcf_rows(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                          const double* __restrict__ v, double alpha, double* __restrict__ thr,
@@ -746,24 +844,7 @@ __global__ void fcf_rows(int n, const int32_t* __restrict__ rp, const int32_t* _
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int c_i = 0;
-  if (i < n) {
-    const int s = rp[i], e = rp[i + 1];
-    double off_max = 0.0;
-    for_row<VEC>(ci, v, s, e, [&](int c, double x) {
-      if (c != i) off_max = fmax(off_max, fabs(x));
-    });
-    const double t = __dmul_rn(alpha, off_max);
-    thr[i] = t;
-    for_row<VEC>(ci, v, s, e, [&](int c, double x) {
-      const double mag = fabs(x);
-      if (c != i && mag > 0.0 && mag >= t) {
-        ++c_i;
-        atomicAdd(&cnt[c].y, 1);
-      }
-    });
-    cnt[i].x = c_i;
-  }
+  const int c_i = i < n ? fcf_row_strength<VEC>(i, rp, ci, v, alpha, thr, cnt) : 0;
   block_add(s_total, (unsigned long long)c_i);
 }
 
@@ -774,20 +855,7 @@ __global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* 
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double t = thr[i];
-  const double wi = fcf_weight(cnt, key, i);
-  bool mine = false;
-  for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
-    const double mag = fabs(x);
-    if (j == i || !(mag > 0.0) || !(mag >= t)) return;
-    const double wj = fcf_weight(cnt, key, j);
-    if (wj != wi ? wj < wi : j < i)  // weight_less(w, j, i)
-      mine = true;
-    else
-      notmin[j] = 1;
-  });
-  if (mine) notmin[i] = 1;
+  if (i < n) fcf_row_marks<VEC, false>(i, rp, ci, v, thr, cnt, key, notmin);
 }
 
 // theta of an F row over A's F columns in column order (= its A_ff row);
@@ -803,27 +871,7 @@ __global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* 
   unsigned long long tb = 0;
   const bool fr = i < n && !notmin[i];
   if (label_pre && i < n) label_pre[i] = fr ? AIRG_F : AIRG_C;
-  if (fr) {
-    double off = 0.0, diag = 0.0;
-    bool seen = false;
-    for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
-      if (notmin[j]) return;
-      if (j == i) {
-        diag = fabs(x);
-        seen = true;
-      } else {
-        off = __dadd_rn(off, fabs(x));
-      }
-    });
-    if (!seen || diag == 0.0) {
-      atomicMax(bad_row, ~(unsigned long long)i);  // ~i: the max is the first bad row
-      theta[i] = 0.0;
-    } else {
-      const double t = __ddiv_rn(off, diag);
-      theta[i] = t;
-      tb = (unsigned long long)__double_as_longlong(t);  // t >= 0: bit order = value order
-    }
-  }
+  if (fr) tb = fcf_row_theta<VEC, false>(i, rp, ci, v, notmin, theta, bad_row);
   block_max(maxbits, tb);
 }
 
@@ -1034,6 +1082,134 @@ __global__ void fcf_convert(int n, const uint8_t* __restrict__ notmin, const dou
   block_add(count, conv ? 1ull : 0ull);
 }
 
+// ---- the whole split of a small level in ONE launch ----
+// Small levels are launch- and latency-bound as six kernels (~30 us a
+// level whatever n is). One cooperative launch of up to one 1024-thread CTA
+// per SM runs the same passes with the same row functions, separated by
+// the software grid barrier; loads of data written inside the launch go
+// through L2 (ld.global.cg). Scratch zeroing is its first phase.
+struct FcfSmall {
+  int n;
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* v;
+  double alpha;
+  uint64_t key;
+  int ddc;
+  double fraction;
+  int64_t bins;
+  unsigned long long* u;     // report counters (8)
+  unsigned long long* hist;  // bins
+  int2* cnt;
+  uint8_t* notmin;
+  double* thr;
+  double* theta;
+  uint8_t* labels;
+  uint8_t* label_pre;  // nullable
+  unsigned* bar;       // grid barrier words (self-resetting)
+};
+constexpr int kSmallThreads = 1024;
+
+template <bool VEC>
+__global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_constant__ FcfSmall P) {
+  extern __shared__ unsigned sh[];
+  const int n = P.n;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  const unsigned nblk = gridDim.x;
+  // 0: zero the counters, the histogram, the counts and the marks
+  for (int k = tid; k < 8; k += stride) P.u[k] = 0;
+  for (int64_t k = tid; k < (P.ddc ? P.bins : 0); k += stride) P.hist[k] = 0;
+  for (int k = tid; k < n; k += stride) {
+    P.cnt[k] = make_int2(0, 0);
+    P.notmin[k] = 0;
+  }
+  grid_barrier(P.bar, nblk);
+  // 1: strength, |S_i|, |S^T| counts
+  unsigned long long acc = 0;
+  for (int i = tid; i < n; i += stride) acc += fcf_row_strength<VEC>(i, P.rp, P.ci, P.v, P.alpha, P.thr, P.cnt);
+  block_add(P.u, acc);
+  grid_barrier(P.bar, nblk);
+  // 2: not-minimal marks
+  for (int i = tid; i < n; i += stride) fcf_row_marks<VEC, true>(i, P.rp, P.ci, P.v, P.thr, P.cnt, P.key, P.notmin);
+  grid_barrier(P.bar, nblk);
+  if (!P.ddc) {
+    unsigned long long nf = 0;
+    for (int i = tid; i < n; i += stride) {
+      const bool f = !__ldcg(P.notmin + i);
+      P.labels[i] = f ? AIRG_F : AIRG_C;
+      nf += f;
+    }
+    block_add(P.u + 1, nf);
+    return;
+  }
+  // 3: theta of the F rows (+ the PMISR labels when asked)
+  unsigned long long tb = 0;
+  for (int i = tid; i < n; i += stride) {
+    const bool fr = !__ldcg(P.notmin + i);
+    if (P.label_pre) P.label_pre[i] = fr ? AIRG_F : AIRG_C;
+    if (fr) tb = max(tb, fcf_row_theta<VEC, true>(i, P.rp, P.ci, P.v, P.notmin, P.theta, P.u + 3));
+  }
+  block_max(P.u + 2, tb);
+  grid_barrier(P.bar, nblk);
+  // 4: histogram + F count (bins <= 8192 on this path: CTA-private bins)
+  {
+    const int64_t bins = P.bins;
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const double mx = __longlong_as_double((long long)__ldcg(P.u + 2));
+    const double width = mx > 0.0 ? __ddiv_rn(mx, (double)bins) : 1.0;
+    const int lane = threadIdx.x & 31;
+    unsigned long long nf = 0;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+      const int i = base + threadIdx.x;
+      long long b = -1;
+      if (i < n && !__ldcg(P.notmin + i)) {
+        b = (long long)__ddiv_rn(__ldcg(P.theta + i), width);
+        if (b > bins - 1) b = bins - 1;
+        ++nf;
+      }
+      const unsigned peers = __match_any_sync(kFull, b);
+      if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(sh + b, (unsigned)__popc(peers));
+    }
+    block_add(P.u + 1, nf);
+    __syncthreads();
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+      if (sh[b]) atomicAdd(P.hist + b, (unsigned long long)sh[b]);
+  }
+  grid_barrier(P.bar, nblk);
+  // 5: alpha_diag (one CTA)
+  if (blockIdx.x == 0)
+    ddc_select_block(P.u + 1, 0, P.hist, P.bins, P.fraction, P.u + 2, 0, 0.0, reinterpret_cast<double*>(P.u + 5));
+  grid_barrier(P.bar, nblk);
+  // 6: conversion and the final labels
+  const double sel = __ldcg(reinterpret_cast<const double*>(P.u + 5));
+  const bool ok = __ldcg(P.u + 3) == 0;
+  unsigned long long conv = 0;
+  for (int i = tid; i < n; i += stride) {
+    const bool f = !__ldcg(P.notmin + i);
+    bool c = false;
+    if (f && ok) {
+      const double t = __ldcg(P.theta + i);
+      c = t > sel && t != 0.0;
+    }
+    P.labels[i] = f && !c ? AIRG_F : AIRG_C;
+    conv += c;
+  }
+  block_add(P.u + 4, conv);
+}
+
+// levels up to AIRG_CF_SMALL rows take the one-launch split (default 0 = off:
+// measured slower than the PDL-chained passes on every C2 level, 2.67 -> 2.93 ms
+// at 131072; the passes are dependent-latency bound either way)
+int64_t cf_small_rows() {
+  static const int64_t v = [] {
+    const char* e = getenv("AIRG_CF_SMALL");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  return v;
+}
+
 }  // namespace
 
 void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,
@@ -1071,8 +1247,34 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   double* theta = thr + n;
   // u: [0] |S| [1] n_f_pre [2] max theta bits [3] ~(first bad row), 0 = none
   //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
-  CUDA_CHECK(cudaMemsetAsync(base, 0, zero_bytes, c.stream));
   const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
+  const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
+  if (n <= cf_small_rows() && (!ddc_enabled || bins <= 8192) && cf_group() == 0) {
+    if (!c.grid_bar) {
+      CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.grid_bar), 2 * sizeof(unsigned), c.stream));
+      CUDA_CHECK(cudaMemsetAsync(c.grid_bar, 0, 2 * sizeof(unsigned), c.stream));
+    }
+    FcfSmall P{n, a.rp.p, a.ci.p, a.v.p, alpha, key, ddc_enabled ? 1 : 0, fraction, bins,
+               d_u_out ? d_u_out : u, hist, cnt, notmin, thr, theta, d_labels, d_labels_pre, c.grid_bar};
+    if (!ddc_enabled && d_labels_pre) P.label_pre = nullptr;
+    const unsigned nblk = (unsigned)std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (n + 511) / 512));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = ddc_enabled ? (size_t)bins * sizeof(unsigned) : 0;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    c.launches++;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, vec ? fcf_small<true> : fcf_small<false>, P));
+    if (!ddc_enabled && d_labels_pre)
+      CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
+    return d_u_out ? d_u_out : u;
+  }
+  CUDA_CHECK(cudaMemsetAsync(base, 0, zero_bytes, c.stream));
   auto* k_rows = vec ? fcf_rows<true> : fcf_rows<false>;
   auto* k_marks = vec ? fcf_marks<true> : fcf_marks<false>;
   auto* k_theta = vec ? fcf_theta<true> : fcf_theta<false>;
@@ -1084,7 +1286,6 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
     k_marks = G == 4 ? fcf_marks_g<4> : G == 8 ? fcf_marks_g<8> : fcf_marks_g<16>;
     k_theta = G == 4 ? fcf_theta_g<4> : G == 8 ? fcf_theta_g<8> : fcf_theta_g<16>;
   }
-  const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
   LAUNCH_PDL(c, k_rows, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, u);
   LAUNCH_PDL(c, k_marks, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, cnt, key, notmin);
   if (ddc_enabled) {

@@ -71,6 +71,8 @@ struct Ctx {
   // reusable device scratch (stream-ordered; grown on demand)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // software grid-barrier words of persistent kernels (self-resetting)
+  unsigned* grid_bar = nullptr;
 };
 
 // Device scratch of at least `bytes` (contents undefined), reused across
@@ -144,6 +146,32 @@ __device__ __forceinline__ void block_max(unsigned long long* dst, unsigned long
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = max(t, part[w]);
     if (t) atomicMax(dst, t);
   }
+}
+
+
+// Sense-free grid barrier over co-resident CTAs: bar[0] arrivals, bar[1]
+// generation. The last CTA to arrive resets the count and bumps the
+// generation; the others spin on it (bounded: a lost CTA traps instead of
+// hanging the device).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      unsigned spins = 0;
+      while (*gen == g) {
+        if (++spins > (1u << 30)) __trap();
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 

@@ -53,30 +53,8 @@ struct TailPhase {
 
 constexpr int kTailThreads = 1024;  // one CTA per SM: few barrier arrivals
 
-// Sense-free grid barrier over co-resident CTAs: bar[0] arrivals, bar[1]
-// generation. The last CTA to arrive resets the count and bumps the
-// generation; the others spin on it (bounded: a lost CTA traps instead of
-// hanging the device).
-__device__ __forceinline__ void tail_grid_barrier(unsigned* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      unsigned spins = 0;
-      while (*gen == g) {
-        if (++spins > (1u << 30)) __trap();
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
+// the software grid barrier lives in common.cuh (grid_barrier)
+__device__ __forceinline__ void tail_grid_barrier(unsigned* bar, unsigned nblocks) { grid_barrier(bar, nblocks); }
 
 // ordered row sums with coherent x loads (x may have been written earlier in
 // this launch)

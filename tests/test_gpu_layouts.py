@@ -94,16 +94,20 @@ CF_VARIANTS = {
     "fused_g8": {"AIRG_CF_GROUP": "8"},
     "fused_g16": {"AIRG_CF_GROUP": "16"},
     "fused_default": {},
+    "fused_no_small": {"AIRG_CF_SMALL": "0"},
+    "fused_all_small": {"AIRG_CF_SMALL": "1000000000"},
+    "fused_all_small_scalar": {"AIRG_CF_SMALL": "1000000000", "AIRG_CF_VEC": "100000"},
 }
 
 
 def test_cf_split_variants_bit_identical():
-    """The fused split's row-pass variants (scalar, 16-byte loads, G lanes
-    per row) and the step-by-step split give the same hierarchy labels and
+    """The fused split's variants (scalar, 16-byte loads, G lanes per row,
+    the one-launch small-level split on no / every level) and the
+    step-by-step split give the same hierarchy labels and
     DDC reports on every level (C2/C3/C4, reduced)."""
     def run(extra):
         env = dict(os.environ)
-        for k in ("AIRG_CF", "AIRG_CF_VEC", "AIRG_CF_GROUP"):
+        for k in ("AIRG_CF", "AIRG_CF_VEC", "AIRG_CF_GROUP", "AIRG_CF_SMALL"):
             env.pop(k, None)
         env.update(extra)
         out = subprocess.run([sys.executable, "-c", CF_SCRIPT], env=env, capture_output=True, text=True,

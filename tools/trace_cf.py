@@ -32,9 +32,10 @@ def main():
     mats = [h.matrix_handle(l, 0) for l in range(L)]
     seeds = [int(problems.mix(np.uint64(0), np.uint64(l))) for l in range(L)]
 
-    def run():
-        for l in range(L):
-            airg.cf_split_device(mats[l], prm["strength_alpha"], prm["max_loops"], seeds[l], ctx=ctx)
+    labs = [ctx.empty(max(m.dims()[0], 1), torch.uint8) for m in mats]
+
+    def run():  # all levels back to back, one synchronisation (the bench's cf_split_ms)
+        airg.cf_split_batch_device(mats, seeds, prm["strength_alpha"], prm["max_loops"], labels=labs, ctx=ctx)
     run()
     torch.cuda.synchronize()
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA,
@@ -60,7 +61,7 @@ def main():
              f"kernel busy {sum(tot.values()):.1f} us"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"{k:40s} {cnt[k]:5d} {v:9.1f} us  mean {v / cnt[k]:.2f}")
-    # per level: first kernel start to last kernel end of each call (8 kernels / level)
+    # per level: first kernel start to last kernel end of each level's kernels
     per = len(ev) // L
     lines.append(f"per level ({per} kernels each): n, nnz, GPU span us, kernel busy us")
     for l in range(L):
