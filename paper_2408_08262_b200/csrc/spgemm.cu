@@ -166,6 +166,65 @@ __device__ __forceinline__ void finish_reg(const int32_t* __restrict__ keys, con
   row_counts(cnt, drop_tol, lane, len, kept, i, kc);
 }
 
+// Rank placement instead of a sort network: the keys are distinct, so each
+// compacted entry's position in the sorted row is the number of smaller
+// keys, counted against 16-byte broadcast reads of the compacted keys
+// (padded with INT_MAX). ~cnt/4 shared loads per lane instead of the
+// bitonic network's log^2 shuffle stages (40% of the warp kernel's issue
+// slots on the C2 Galerkin products). keys must be 16-byte aligned with
+// room for cnt + 4 entries.
+template <int E>
+__device__ __forceinline__ void finish_rank(int32_t* __restrict__ keys, const double* __restrict__ vals, int cnt,
+                                            int lane, int i, int gi, int32_t* __restrict__ oc,
+                                            double* __restrict__ ov, double drop_tol, int square_keep_diag,
+                                            int32_t* __restrict__ len, int32_t* __restrict__ kept) {
+  int k[E];
+  double v[E];
+  int r[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int t = e * 32 + lane;
+    k[e] = t < cnt ? keys[t] : 0x7fffffff;
+    v[e] = t < cnt ? vals[t] : 0.0;
+    r[e] = 0;
+  }
+  if (lane < 4) keys[cnt + lane] = 0x7fffffff;
+  __syncwarp();
+  const int4* k4 = reinterpret_cast<const int4*>(keys);
+  for (int t = 0; t < cnt; t += 4) {
+    const int4 q = k4[t >> 2];
+#pragma unroll
+    for (int e = 0; e < E; ++e) r[e] += (q.x < k[e]) + (q.y < k[e]) + (q.z < k[e]) + (q.w < k[e]);
+  }
+  double rmax = 0.0;
+  int kc = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int t = e * 32 + lane;
+    if (t < cnt) {
+      oc[r[e]] = k[e];
+      ov[r[e]] = v[e];
+      rmax = fmax(rmax, fabs(v[e]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if (drop_tol >= 0.0) {
+    const double thr = __dmul_rn(drop_tol, rmax);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int t = e * 32 + lane;
+      if (t < cnt) {
+        const double mag = fabs(v[e]);
+        const bool diag = square_keep_diag && k[e] == gi;
+        kc += diag || !(mag < thr && mag < rmax);
+      }
+    }
+  }
+  __syncwarp();  // the keys are read before the table is reused
+  row_counts(cnt, drop_tol, lane, len, kept, i, kc);
+}
+
 // rows of more than 256 distinct columns (2048-slot tables): shared-memory sort
 __device__ __forceinline__ void finish_smem(int32_t* __restrict__ keys, double* __restrict__ vals, int cnt,
                                             int lane, int i, int gi, int32_t* __restrict__ oc, double* __restrict__ ov,
@@ -213,7 +272,7 @@ __device__ __forceinline__ void finish_smem(int32_t* __restrict__ keys, double* 
   row_counts(cnt, drop_tol, lane, len, kept, i, kc);
 }
 
-template <int kHashCap>
+template <int kHashCap, bool RANK>
 __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ keys, double* __restrict__ vals,
                                          int32_t* __restrict__ pref, double* __restrict__ pbuf,
                                          const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
@@ -318,7 +377,13 @@ __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ 
   }
   int32_t* oc = scol + off[i];
   double* ov = sval + off[i];
-  if (cnt <= 32) {
+  if (RANK && cnt <= 32) {
+    finish_rank<1>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
+  } else if (RANK && cnt <= 64) {
+    finish_rank<2>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
+  } else if (RANK && cnt <= 128) {
+    finish_rank<4>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
+  } else if (cnt <= 32) {
     finish_reg<1>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
   } else if (cnt <= 64) {
     finish_reg<2>(keys, vals, cnt, lane, i, rb + i, oc, ov, drop_tol, square_keep_diag, len, kept);
@@ -332,7 +397,7 @@ __device__ __forceinline__ bool warp_row(int i, int lane, int32_t* __restrict__ 
 
 // kSpgWarps warps per block, one list row per warp at a time; rows that
 // overflow the table are appended to next_list
-template <int kHashCap, int kSpgWarps>
+template <int kHashCap, int kSpgWarps, bool RANK>
 __global__ void __launch_bounds__(kSpgWarps * 32, kSpgWarps == 8 ? 7 : 1)
 spgemm_warp_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
                  int32_t* __restrict__ next_list, int32_t* __restrict__ next_count,
@@ -342,7 +407,7 @@ spgemm_warp_list(const int32_t* __restrict__ list, const int32_t* __restrict__ c
                  const int64_t* __restrict__ off, int32_t* __restrict__ scol, double* __restrict__ sval,
                  int32_t* __restrict__ len, int32_t* __restrict__ kept, double drop_tol,
                  int square_keep_diag, const int32_t* __restrict__ bmap, int rb) {
-  __shared__ int32_t keys_all[kSpgWarps][kHashCap];
+  __shared__ __align__(16) int32_t keys_all[kSpgWarps][kHashCap];
   __shared__ double vals_all[kSpgWarps][kHashCap];
   __shared__ int32_t pref_all[kSpgWarps][kWarpA + 1];
   __shared__ double pbuf_all[kSpgWarps][32];
@@ -350,7 +415,7 @@ spgemm_warp_list(const int32_t* __restrict__ list, const int32_t* __restrict__ c
   const int nrows = *count;
   for (int q = blockIdx.x * kSpgWarps + w; q < nrows; q += gridDim.x * kSpgWarps) {
     const int i = list[q];
-    const bool ovf = warp_row<kHashCap>(i, lane, keys_all[w], vals_all[w], pref_all[w], pbuf_all[w], arp,
+    const bool ovf = warp_row<kHashCap, RANK>(i, lane, keys_all[w], vals_all[w], pref_all[w], pbuf_all[w], arp,
                                         aci, av, brp, bci, bv, off, scol, sval, len, kept, drop_tol,
                                         square_keep_diag, bmap, rb);
     if (ovf && lane == 0) next_list[atomicAdd(next_count, 1)] = i;
@@ -501,14 +566,28 @@ void spgemm(Ctx& c, const Csr& a, const Csr& b, Csr& out, double drop_tol, bool 
     // overflow -> list 2: one warp per block + 2048-slot table, overflow ->
     // list 3: thread per row. Persistent grids read the list lengths on device.
     const int64_t N = n;
+    // AIRG_SPGEMM_SORT=bitonic: the register sort network instead of rank placement
+    static const bool rank = [] {
+      const char* e = getenv("AIRG_SPGEMM_SORT");
+      return !(e && !strcmp(e, "bitonic"));
+    }();
+    auto* k256 = rank ? spgemm_warp_list<256, 8, true> : spgemm_warp_list<256, 8, false>;
+    auto* k2048 = rank ? spgemm_warp_list<2048, 1, true> : spgemm_warp_list<2048, 1, false>;
+    // the persistent grid is ONE wave: more CTAs than fit would run their
+    // statically assigned rows after the first wave drains
+    static int per_sm = 0;
+    if (!per_sm) {
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k256, 256, 0));
+      per_sm = std::max(per_sm, 1);
+    }
     LAUNCH(c, spgemm_accumulate, tgrid, 128, 0, n, (const int32_t*)lists.p, (const int32_t*)counts.p,
            a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
            off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
-    LAUNCH(c, (spgemm_warp_list<256, 8>), (unsigned)std::min<int64_t>((N + 7) / 8, 8 * c.num_sms), 256, 0,
+    LAUNCH(c, k256, (unsigned)std::min<int64_t>((N + 7) / 8, (int64_t)per_sm * c.num_sms), 256, 0,
            (const int32_t*)(lists.p + N), (const int32_t*)(counts.p + 1), lists.p + 2 * N, counts.p + 2,
            a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
            off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);
-    LAUNCH(c, (spgemm_warp_list<2048, 1>), (unsigned)std::min<int64_t>(N, 8 * c.num_sms), 32, 0,
+    LAUNCH(c, k2048, (unsigned)std::min<int64_t>(N, 8 * c.num_sms), 32, 0,
            (const int32_t*)(lists.p + 2 * N), (const int32_t*)(counts.p + 2), lists.p + 3 * N, counts.p + 3,
            a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p,
            off.p, scol.p, sval.p, len.p, kept.p, drop_tol, sq, bmap, row_base);

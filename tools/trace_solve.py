@@ -105,6 +105,21 @@ def main():
                          f"{blk[3]['marg']:6.1f} | {info.nnz_ffinv:8d} {blk[2]['marg']:6.1f} "
                          f"{bq / blk[2]['marg'] / 1e3:6.0f} | {blk[0]['marg']:5.1f}")
         lines.append("(per-kernel columns are marginal times on the chain: end(k) - end(k-1))")
+    if args.what == "setup":
+        # one line per SpGEMM call: rows (grid of spgemm_bound x 256) and the
+        # device time of each of its kernels, in call order
+        calls = []
+        for e in ev:
+            nm = e["name"]
+            if "spgemm_bound" in nm:
+                calls.append({"rows~": e.get("args", {}).get("grid", [0])[0] * 256, "ts": e["ts"], "k": []})
+            elif "spgemm" in nm and calls:
+                mt = re.search(r"(spgemm_\w+)(<[^()]*>)?\(", nm.replace("(anonymous namespace)::", ""))
+                calls[-1]["k"].append((mt.group(1) + (mt.group(2) or "") if mt else nm[:30], e["dur"]))
+        lines.append("-- SpGEMM calls: rows~, total us, kernels")
+        for i, c_ in enumerate(calls):
+            tot_us = sum(d for _, d in c_["k"])
+            lines.append(f"{i:3d} {c_['rows~']:9d} {tot_us:9.1f}  " + " ".join(f"{k}={d:.0f}" for k, d in c_["k"]))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     open(args.out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
