@@ -328,6 +328,10 @@ int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
                          double* ratio_before, double* ratio_after,
                          int32_t* triggered, int64_t* halo_entries,
                          int64_t* h_starts /* P+1, nullable */);
+/* Halo transport of the solve: 0 = emulation gather kernel, 1 = NCCL
+ * send/recv, 2 = NVLink peer stores (AIRG_TRANSPORT=p2p; emulated or one
+ * process per GPU). */
+int airg_dist_transport(const airg_dist* d, int32_t* transport);
 int airg_dist_destroy(airg_dist* d);
 /* ---- Matrix Market exchange (matrix_market.hpp:11-19) ---------------------
  * Host-side, no GPU needed. airg_mm_read parses a "coordinate real general"

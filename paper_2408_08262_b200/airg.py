@@ -109,6 +109,7 @@ def lib() -> C.CDLL:
                                  C.c_int64], C.c_int),
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
                                       _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
+            "airg_dist_transport": ([_VP, _P(C.c_int32)], C.c_int),
             "airg_dist_destroy": ([_VP], C.c_int),
             "airg_mm_read": ([C.c_char_p, _P(_VP)], C.c_int),
             "airg_mm_dims": ([_VP, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
@@ -787,6 +788,13 @@ class Dist:
             except Exception:
                 pass
             self.d = None
+
+    @property
+    def transport(self) -> str:
+        """Halo transport of the solve: "gather" (emulation), "nccl" or "p2p"."""
+        t = C.c_int32()
+        _check(lib().airg_dist_transport(self.d, C.byref(t)))
+        return ("gather", "nccl", "p2p")[t.value]
 
     def level_info(self, l: int) -> dict:
         a, t = C.c_int32(), C.c_int32()

@@ -893,6 +893,15 @@ int airg_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t*
   });
 }
 
+int airg_dist_transport(const airg_dist* dp, int32_t* transport) {
+  return guard([&] {
+    need(dp, "dist");
+    need(transport, "transport");
+    const DHier& d = dp->d;
+    *transport = d.p2p.on ? 2 : (d.me >= 0 && d.P > 1 ? 1 : 0);
+  });
+}
+
 int airg_dist_destroy(airg_dist* d) {
   return guard([&] {
     if (!d) return;

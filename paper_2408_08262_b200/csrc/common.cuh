@@ -188,19 +188,30 @@ struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool borrowed = false;  // a view into memory owned elsewhere (never freed here)
 
   DBuf() = default;
   DBuf(Ctx& c, size_t count) { alloc(c, count); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), borrowed(o.borrowed) {
+    o.p = nullptr;
+    o.n = 0;
+    o.borrowed = false;
+  }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; s = o.s; borrowed = o.borrowed;
+      o.p = nullptr; o.n = 0; o.borrowed = false;
     }
     return *this;
+  }
+  void view(T* ptr, size_t count) {
+    release();
+    p = ptr;
+    n = count;
+    borrowed = true;
   }
   ~DBuf() { release(); }
 
@@ -221,9 +232,10 @@ struct DBuf {
     }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !borrowed) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    borrowed = false;
   }
   void zero(Ctx& c) {
     if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), c.stream));

@@ -499,6 +499,10 @@ void remap(Ctx& c, Csr& a, const DVec& V, int r) {
 
 // halo exchange of one vector (all local ranks)
 void exchange(Ctx& c, DHier& d, DVec& V) {
+  if (d.p2p.on && V.slot >= 0) {
+    p2p_exchange(c, d, V);
+    return;
+  }
   const int P = V.part.P();
   if (d.me < 0) {
     for (int r = 0; r < P; ++r) {
@@ -528,6 +532,12 @@ void exchange(Ctx& c, DHier& d, DVec& V) {
                           c.stream));
   }
   NCCL_CHECK(ncclGroupEnd());
+}
+
+// the kernels that read V's halo since exchange(V) have been enqueued: the
+// p2p transport hands the halo slots back to their owners (no-op otherwise)
+void release(Ctx& c, DHier& d, DVec& V) {
+  if (d.p2p.on && V.slot >= 0) p2p_release(c, d, V);
 }
 
 // ---- distributed CF split kernels (local column indices into [own | halo]) ----
@@ -1058,6 +1068,18 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
   finalize(c, d.CX, d);
   finalize(c, d.CR, d);
   finalize(c, d.XS, d);
+  if (p2p_requested() && P > 1) {  // the solve's exchanged vectors move to the p2p arenas
+    std::vector<DVec*> vecs;
+    for (int l = 0; l < L; ++l) {
+      vecs.push_back(&d.lv[l].B);
+      vecs.push_back(&d.lv[l].X);
+      vecs.push_back(&d.lv[l].RF);
+    }
+    vecs.push_back(&d.CX);
+    vecs.push_back(&d.CR);
+    vecs.push_back(&d.XS);
+    p2p_setup(c, d, vecs);
+  }
   for (int l = 0; l < L; ++l) {
     DLevel& D = d.lv[l];
     const DVec& Xn = l + 1 < L ? d.lv[l + 1].X : d.CX;
@@ -1115,6 +1137,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
       if (R.n)
         launch_rows(c, R, (const double*)D.B.rk[r].buf.p, LStore{Bn.rk[r].buf.p});
     });
+    release(c, d, D.B);
   }
   // coarse solve on the coarse owner(s); CB and CR feed Ac^-1 through CR's
   // layout: copy the owned rhs into CR before the first application
@@ -1133,6 +1156,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
         if (A.n)
           launch_rows(c, A, (const double*)d.CX.rk[r].buf.p, LCres{d.CB.rk[r].buf.p, d.CR.rk[r].buf.p});
       });
+      release(c, d, d.CX);
     }
     exchange(c, d, d.CR);
     rank_loop([&](int r) {
@@ -1140,6 +1164,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
       if (A.n)
         launch_rows(c, A, (const double*)d.CR.rk[r].buf.p, LCupd{d.CX.rk[r].buf.p, it == 0 ? 1 : 0});
     });
+    release(c, d, d.CR);
   }
   // ascent
   for (int l = L - 1; l >= 0; --l) {
@@ -1152,6 +1177,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
         LAUNCH_PDL(c, k_prolong4_l, blocks_for(R.n_own / 4 + 1, 256), 256, 0, (int)R.n_own, R.pmap.p,
                    Xn.rk[r].buf.p, D.X.rk[r].buf.p);
     });
+    release(c, d, Xn);
     for (int64_t s = 0; s < cfg.up_f_smooths; ++s) {
       exchange(c, d, D.X);
       rank_loop([&](int r) {
@@ -1163,12 +1189,14 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
         else
           launch_rows(c, R.AFFG, (const double*)D.X.rk[r].buf.p, LFres2{bl, R.f2f.p, R.sc.p, D.RF.rk[r].buf.p});
       });
+      release(c, d, D.X);
       exchange(c, d, D.RF);
       rank_loop([&](int r) {
         DLevel::Rank& R = D.rk[r];
         if (!R.nf_own) return;
         launch_rows(c, R.FINV, (const double*)D.RF.rk[r].buf.p, LFupd{R.f2f.p, D.X.rk[r].buf.p});
       });
+      release(c, d, D.RF);
     }
   }
 }
@@ -1195,6 +1223,7 @@ void enqueue_update_residual(Ctx& c, DHier& d) {
     else
       CUDA_CHECK(cudaMemsetAsync(d.part.p + d.part_off[r], 0, sizeof(double), c.stream));
   }
+  release(c, d, d.XS);
   LAUNCH_PDL(c, k_sum, 1, 1024, 0, (const double*)d.part.p, d.nparts, d.scal.p);
 }
 

@@ -19,7 +19,11 @@
 // them phase by phase (no kernel ever waits on another rank); the halo
 // exchange is a gather kernel reading the owners' buffers. kNccl runs one
 // rank per process/GPU and exchanges halos with grouped ncclSend/ncclRecv
-// and reduces norms with ncclAllReduce.
+// and reduces norms with ncclAllReduce. AIRG_TRANSPORT=p2p replaces the
+// solve's halo exchanges by NVLink peer stores (halo_p2p.cuh): every rank's
+// vector buffers live in one IPC-shared arena, owners push halo entries
+// straight into the consumers' halo slots and signal per-slot counters; the
+// same protocol runs in emulation with the "peers" on one GPU.
 #pragma once
 
 #include <nccl.h>
@@ -27,6 +31,29 @@
 #include "hier.cuh"
 
 namespace airg {
+
+// ---- NVLink peer-store halo exchange (parameter blocks of halo_p2p.cu) ----
+constexpr int kP2PMaxPeers = 32;
+struct P2PSend {  // owner side: push my entries of the peers' halos, then signal
+  int64_t ns = 0;
+  const int32_t* idx = nullptr;  // owned local index per pushed entry
+  double* const* dst = nullptr;  // destination per entry (a peer's halo slot)
+  const double* src = nullptr;   // my [own | halo] buffer
+  int npeer = 0;
+  unsigned long long* remote_flag[kP2PMaxPeers] = {};  // "delivered" counter in each receiver's arena
+  const unsigned long long* ack[kP2PMaxPeers] = {};    // "consumed" counter per receiver in my arena
+  unsigned long long* sends = nullptr;                 // completed pushes of this slot
+  unsigned* blocks = nullptr;                          // CTA arrivals (self-resetting)
+};
+struct P2PWait {  // consumer side: wait for every sender's delivery
+  int nsrc = 0;
+  const unsigned long long* flag[kP2PMaxPeers] = {};
+  unsigned long long* recvs = nullptr;  // deliveries consumed so far
+};
+struct P2PAck {  // consumer side, after the consuming kernel: free the slots
+  int nsrc = 0;
+  unsigned long long* remote_ack[kP2PMaxPeers] = {};
+};
 
 struct Part {
   std::vector<int64_t> s;  // P + 1 starts
@@ -51,9 +78,16 @@ struct DVec {
     std::vector<int64_t> recv_off, recv_cnt, send_off, send_cnt;
     DBuf<int32_t> send_idx;
     DBuf<double> send_buf;
+    // p2p: pushed entries (index, destination) and the three parameter blocks
+    DBuf<int32_t> p2p_idx;
+    DBuf<double*> p2p_dst;
+    P2PSend push;
+    P2PWait wait;
+    P2PAck ack;
   };
   std::vector<Rank> rk;
   DBuf<double*> bases;  // emulation: buf pointer per rank
+  int slot = -1;        // p2p: index of this vector's counters (-1: not exchanged by p2p)
 };
 
 struct DLevel {
@@ -92,11 +126,27 @@ struct DHier {
   int64_t graph_key = -1;
   uint64_t graph_kernels = 0;
   int64_t top_n = 0;
-  ~DHier() {
-    if (graph) cudaGraphExecDestroy(graph);
-  }
+  // p2p transport: one arena per rank (emulation: all allocated here; NCCL
+  // ranks: mine allocated, the peers' opened from their IPC handles)
+  struct P2PState {
+    bool on = false;
+    int nslots = 0;
+    std::vector<void*> base;
+    std::vector<char> owned;
+    DBuf<unsigned long long> ctr;  // per local rank: [slot] sends | [slot] receives
+    DBuf<unsigned> blocks;         // per local rank and slot: push CTA arrivals
+  } p2p;
+  ~DHier();
   bool mine(int r) const { return me < 0 || me == r; }
 };
+
+// p2p transport (halo_p2p.cu): arenas, slot counters and parameter blocks for
+// the solve's vectors; exchange / release of one vector
+void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs);
+void p2p_exchange(Ctx& c, DHier& d, DVec& V);
+void p2p_release(Ctx& c, DHier& d, DVec& V);
+void p2p_free(DHier& d);
+bool p2p_requested();
 
 void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double threshold,
                  const int64_t* level0_starts, DHier& d);

@@ -1,0 +1,270 @@
+// Halo exchange by NVLink peer stores (AIRG_TRANSPORT=p2p; see dist.cuh).
+//
+// Each rank keeps ALL its exchanged vectors ([own | halo] buffers) and two
+// counter tables in one cudaMalloc'd arena whose IPC handle the other ranks
+// open, so every rank can address every peer's halo slots directly. The
+// arena layout is a pure function of the halo plans, which every rank holds
+// for every rank, so no address tables are exchanged -- only the handles.
+//
+// Per vector ("slot") and ordered pair (owner o -> consumer q):
+//   F[slot][o] in q's arena  -- deliveries from o (o increments it remotely)
+//   A[slot][q] in o's arena  -- deliveries q has consumed (q increments it)
+// exchange(V): o's push kernel waits until A[slot][q] == pushes so far (q is
+//   done reading the previous contents), stores its entries of q's halo into
+//   q's buffer, fences at system scope, and its last CTA bumps F[slot][o]
+//   with a release add; q's wait kernel spins (acquire) until F[slot][o]
+//   reaches its receive count + 1 for every sender o.
+// release(V), after q's consuming kernel: q bumps A[slot][o] at every sender.
+// Every rank issues the same exchange/release sequence, so a wait only ever
+// depends on pushes and acks its peers issued earlier in their own streams:
+// no circular wait. In emulation all "ranks" share one GPU and one stream;
+// their pushes are enqueued before any of their waits, so no wait blocks.
+// The values moved are copies: the V-cycle stays bit-identical to 1 GPU.
+#include <cstring>
+
+#include "dist.cuh"
+
+namespace airg {
+
+#define P2P_NCCL(x)                                                            \
+  do {                                                                         \
+    ncclResult_t r__ = (x);                                                    \
+    if (r__ != ncclSuccess)                                                    \
+      throw CudaError(std::string("NCCL error: ") + ncclGetErrorString(r__)); \
+  } while (0)
+
+namespace {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// bounded spin (a lost peer traps instead of hanging the device)
+__device__ __forceinline__ void spin_geq(const unsigned long long* p, unsigned long long target) {
+  unsigned ns = 32;
+  unsigned long long it = 0;
+  while (ld_acquire_sys(p) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (++it > (1ull << 26)) __trap();
+  }
+}
+
+__global__ void k_p2p_push(const __grid_constant__ P2PSend S) {
+  pdl_wait();
+  const unsigned long long done = *S.sends;  // pushes completed before this one
+  if ((int)threadIdx.x < S.npeer) spin_geq(S.ack[threadIdx.x], done);
+  __syncthreads();
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S.ns; k += (int64_t)gridDim.x * blockDim.x)
+    *S.dst[k] = S.src[S.idx[k]];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(S.blocks, 1u) == gridDim.x - 1) {  // last CTA
+    __threadfence_system();
+    *S.blocks = 0;
+    for (int p = 0; p < S.npeer; ++p) red_release_sys_add(S.remote_flag[p], 1ull);
+    *S.sends = done + 1;
+  }
+  pdl_trigger();
+}
+
+__global__ void k_p2p_wait(const __grid_constant__ P2PWait W) {
+  pdl_wait();
+  const unsigned long long target = *W.recvs + 1;
+  if ((int)threadIdx.x < W.nsrc) spin_geq(W.flag[threadIdx.x], target);
+  __syncthreads();
+  if (threadIdx.x == 0) *W.recvs = target;
+  pdl_trigger();
+}
+
+__global__ void k_p2p_ack(const __grid_constant__ P2PAck A) {
+  pdl_wait();  // the consuming kernel has finished reading the halo
+  if ((int)threadIdx.x < A.nsrc) red_release_sys_add(A.remote_ack[threadIdx.x], 1ull);
+  pdl_trigger();
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// arena of rank r: every vector's [own | halo] buffer, then F and A tables
+struct Layout {
+  std::vector<size_t> buf;
+  size_t f = 0, a = 0, bytes = 0;
+};
+Layout layout(const std::vector<DVec*>& vecs, int r, int P) {
+  Layout L;
+  size_t cur = 0;
+  for (const DVec* V : vecs) {
+    cur = align_up(cur);
+    L.buf.push_back(cur);
+    const DVec::Rank& R = V->rk[r];
+    cur += sizeof(double) * (size_t)std::max<int64_t>(1, R.own + R.nhalo);
+  }
+  L.f = align_up(cur);
+  L.a = L.f + sizeof(unsigned long long) * vecs.size() * (size_t)P;
+  L.bytes = align_up(L.a + sizeof(unsigned long long) * vecs.size() * (size_t)P);
+  return L;
+}
+
+}  // namespace
+
+bool p2p_requested() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_TRANSPORT");
+    return e && !strcmp(e, "p2p");
+  }();
+  return v;
+}
+
+void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs) {
+  const int P = d.P;
+  if (P > kP2PMaxPeers) throw InvalidArgument("dist: the p2p transport handles at most 32 ranks");
+  DHier::P2PState& S = d.p2p;
+  S.on = true;
+  S.nslots = (int)vecs.size();
+  for (int i = 0; i < S.nslots; ++i) vecs[i]->slot = i;
+  std::vector<Layout> lay;
+  for (int r = 0; r < P; ++r) lay.push_back(layout(vecs, r, P));
+  S.base.assign(P, nullptr);
+  S.owned.assign(P, 0);
+  for (int r = 0; r < P; ++r) {
+    if (!d.mine(r)) continue;
+    CUDA_CHECK(cudaMalloc(&S.base[r], lay[r].bytes));  // plain cudaMalloc: IPC-exportable
+    S.owned[r] = 1;
+    CUDA_CHECK(cudaMemsetAsync(S.base[r], 0, lay[r].bytes, c.stream));
+  }
+  if (d.me >= 0) {  // one process per GPU: exchange the arena handles, open the peers'
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    cudaIpcMemHandle_t mine;
+    CUDA_CHECK(cudaIpcGetMemHandle(&mine, S.base[d.me]));
+    DBuf<char> all(c, sizeof(cudaIpcMemHandle_t) * (size_t)P);
+    to_device(c, all.p + sizeof(cudaIpcMemHandle_t) * d.me, reinterpret_cast<const char*>(&mine), sizeof mine);
+    P2P_NCCL(ncclAllGather(all.p + sizeof(cudaIpcMemHandle_t) * d.me, all.p, sizeof(cudaIpcMemHandle_t),
+                           ncclChar, d.comm, c.stream));
+    std::vector<cudaIpcMemHandle_t> hs(P);
+    to_host(c, reinterpret_cast<char*>(hs.data()), all.p, sizeof(cudaIpcMemHandle_t) * (size_t)P);
+    for (int q = 0; q < P; ++q) {
+      if (q == d.me) continue;
+      CUDA_CHECK(cudaIpcOpenMemHandle(&S.base[q], hs[q], cudaIpcMemLazyEnablePeerAccess));
+    }
+  }  // emulation: every arena is local
+  auto at = [&](int r, size_t off) { return static_cast<char*>(S.base[r]) + off; };
+  auto F = [&](int r, int slot, int from) {
+    return reinterpret_cast<unsigned long long*>(at(r, lay[r].f)) + (size_t)slot * P + from;
+  };
+  auto A = [&](int r, int slot, int by) {
+    return reinterpret_cast<unsigned long long*>(at(r, lay[r].a)) + (size_t)slot * P + by;
+  };
+  // per local rank: [slot] sends then [slot] receives; CTA counters per slot
+  S.ctr.alloc(c, (size_t)2 * S.nslots * P);
+  S.ctr.zero(c);
+  S.blocks.alloc(c, (size_t)S.nslots * P);
+  S.blocks.zero(c);
+  for (DVec* Vp : vecs) {
+    DVec& V = *Vp;
+    const int slot = V.slot;
+    std::vector<double*> bases(P, nullptr);
+    for (int r = 0; r < P; ++r) {
+      DVec::Rank& R = V.rk[r];
+      if (d.mine(r)) {
+        R.buf.view(reinterpret_cast<double*>(at(r, lay[r].buf[slot])), (size_t)std::max<int64_t>(1, R.own + R.nhalo));
+        bases[r] = R.buf.p;
+      }
+    }
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r)) continue;
+      DVec::Rank& R = V.rk[r];
+      // sender side: my entries of every peer's halo, in the peer's halo order
+      std::vector<int32_t> idx;
+      std::vector<double*> dst;
+      R.push = P2PSend();
+      for (int q = 0; q < P; ++q) {
+        if (q == r) continue;
+        const DVec::Rank& Q = V.rk[q];
+        const int64_t cnt = Q.recv_cnt.empty() ? 0 : Q.recv_cnt[r];
+        if (!cnt) continue;
+        double* qbuf = reinterpret_cast<double*>(at(q, lay[q].buf[slot]));
+        int64_t k = 0;
+        for (int64_t g : Q.halo_host) {
+          if (g < R.lo || g >= R.lo + R.own) continue;
+          idx.push_back((int32_t)(g - R.lo));
+          dst.push_back(qbuf + Q.own + Q.recv_off[r] + k);
+          ++k;
+        }
+        if (k != cnt) throw RuntimeError("p2p: send list does not match the receiver's halo plan");
+        R.push.remote_flag[R.push.npeer] = F(q, slot, r);
+        R.push.ack[R.push.npeer] = A(r, slot, q);
+        R.push.npeer++;
+      }
+      R.p2p_idx.alloc(c, std::max<size_t>(1, idx.size()));
+      R.p2p_dst.alloc(c, std::max<size_t>(1, dst.size()));
+      to_device(c, R.p2p_idx.p, idx.data(), idx.size());
+      to_device(c, R.p2p_dst.p, dst.data(), dst.size());
+      R.push.ns = (int64_t)idx.size();
+      R.push.idx = R.p2p_idx.p;
+      R.push.dst = R.p2p_dst.p;
+      R.push.src = R.buf.p;
+      R.push.sends = S.ctr.p + (size_t)2 * S.nslots * r + slot;
+      R.push.blocks = S.blocks.p + (size_t)S.nslots * r + slot;
+      // consumer side: every owner I receive from
+      R.wait = P2PWait();
+      R.ack = P2PAck();
+      for (int o = 0; o < P; ++o) {
+        if (o == r || R.recv_cnt.empty() || !R.recv_cnt[o]) continue;
+        R.wait.flag[R.wait.nsrc++] = F(r, slot, o);
+        R.ack.remote_ack[R.ack.nsrc++] = A(o, slot, r);
+      }
+      R.wait.recvs = S.ctr.p + (size_t)2 * S.nslots * r + S.nslots + slot;
+    }
+    if (d.me < 0) {
+      V.bases.alloc(c, (size_t)P);
+      to_device(c, V.bases.p, bases.data(), (size_t)P);
+    }
+  }
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+void p2p_exchange(Ctx& c, DHier& d, DVec& V) {
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const P2PSend& S = V.rk[r].push;
+    if (S.ns)
+      LAUNCH_PDL(c, k_p2p_push, (unsigned)std::min<int64_t>(blocks_for(S.ns, 256), 2 * c.num_sms), 256, 0, S);
+  }
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const P2PWait& W = V.rk[r].wait;
+    if (W.nsrc) LAUNCH_PDL(c, k_p2p_wait, 1, 32, 0, W);
+  }
+}
+
+void p2p_release(Ctx& c, DHier& d, DVec& V) {
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    const P2PAck& A = V.rk[r].ack;
+    if (A.nsrc) LAUNCH_PDL(c, k_p2p_ack, 1, 32, 0, A);
+  }
+}
+
+void p2p_free(DHier& d) {
+  DHier::P2PState& S = d.p2p;
+  for (size_t r = 0; r < S.base.size(); ++r) {
+    if (!S.base[r]) continue;
+    if (S.owned[r])
+      cudaFree(S.base[r]);
+    else
+      cudaIpcCloseMemHandle(S.base[r]);
+    S.base[r] = nullptr;
+  }
+}
+
+DHier::~DHier() {
+  if (graph) cudaGraphExecDestroy(graph);
+  p2p_free(*this);
+}
+
+}  // namespace airg

@@ -78,6 +78,7 @@ def test_dist_c2_reduced_with_zslabs():
     ref = airg.richardson_solve(h, p.b, coarse_iterations=3)
     starts = np.linspace(0, p.n, 5).astype(np.int64)  # z-slabs of 8 planes
     d = airg.Dist(h, 4, threshold=2.0, starts=starts)
+    assert d.transport == ("p2p" if os.environ.get("AIRG_TRANSPORT") == "p2p" else "gather")
     res = d.solve(p.b, coarse_iterations=3)
     assert same_bits(res.x, ref.x)
     assert d.level_info(0)["halo"] > 0
@@ -181,3 +182,48 @@ def test_dist_setup_nccl_single_rank_then_solve():
     st, _ = d.solve_device(tb, tx, coarse_iterations=3)
     r0 = airg.richardson_solve(ref, p.b, coarse_iterations=3)
     assert st.iterations == r0.stats.iterations and same_bits(h.ctx.to_host(tx), r0.x)
+
+
+P2P_SCRIPT = r"""
+import glob, os, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+gold = sorted(glob.glob(os.path.join(%r, "golden", "*.npz")))[:4]
+cases = []
+for path in gold:
+    g = np.load(path)
+    prm = eval(str(g["params"][0]))
+    n = len(g["rp"]) - 1
+    cases.append((airg.SparseMatrix.from_arrays(n, n, g["rp"], g["ci"], g["v"]), prm, g["b"], None))
+p = problems.c2_structured_3d(32)
+cases.append((airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals),
+              dict(problems.setup_params(2), coarse_size_target=500), p.b, np.linspace(0, p.n, 5).astype(np.int64)))
+for a, prm, b, starts in cases:
+    h = airg.setup(a, **prm)
+    ci = prm.get("coarse_iterations", 3)
+    ref = airg.richardson_solve(h, b, coarse_iterations=ci)
+    for P, thr in ((2, 2.0), (3, 2.0), (4, 0.0), (8, 1e9)):
+        if starts is not None and P != 4:
+            continue
+        d = airg.Dist(h, P, threshold=thr, starts=starts)
+        assert d.transport == "p2p"
+        for rep in range(2):  # the slot counters carry over between solves
+            res = d.solve(b, coarse_iterations=ci)
+            assert res.stats.iterations == ref.stats.iterations, (P, rep)
+            assert res.x.tobytes() == ref.x.tobytes(), (P, rep)
+print("p2p ok")
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_dist_p2p_transport_emulated_bit_identical():
+    """AIRG_TRANSPORT=p2p: halo entries pushed into the consumers' halo slots
+    of the per-rank arenas with delivery / consumption counters (the NVLink
+    peer-store protocol, halo_p2p.cu), all ranks emulated on one GPU: same
+    bits as one GPU, twice in a row on the same distribution."""
+    import subprocess
+    import sys
+    env = dict(os.environ, AIRG_TRANSPORT="p2p")
+    out = subprocess.run([sys.executable, "-c", P2P_SCRIPT], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "p2p ok" in out.stdout
