@@ -1224,6 +1224,7 @@ void enqueue_update_residual(Ctx& c, DHier& d) {
       CUDA_CHECK(cudaMemsetAsync(d.part.p + d.part_off[r], 0, sizeof(double), c.stream));
   }
   release(c, d, d.XS);
+  p2p_flush(c, d);  // the captured body hands back every slot it read
   LAUNCH_PDL(c, k_sum, 1, 1024, 0, (const double*)d.part.p, d.nparts, d.scal.p);
 }
 

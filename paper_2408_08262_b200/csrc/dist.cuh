@@ -32,9 +32,21 @@
 
 namespace airg {
 
-// ---- NVLink peer-store halo exchange (parameter blocks of halo_p2p.cu) ----
+// ---- NVLink peer-store halo exchange (parameter block of halo_p2p.cu) ----
 constexpr int kP2PMaxPeers = 32;
-struct P2PSend {  // owner side: push my entries of the peers' halos, then signal
+constexpr int kP2PMaxAcks = 64;
+// One exchange of one vector on one rank, as ONE kernel: (1) hand back the
+// halo slots this rank has finished reading since its last exchange
+// ("consumed" acks to their owners), (2) wait until every receiver has
+// consumed my previous push of this vector, store my entries of their halos
+// into their buffers and signal "delivered", (3) wait for every owner's
+// delivery into my halo. Emulation runs the phases as separate launches
+// (all ranks share one stream).
+struct P2PExch {
+  int phases = 0;  // 1 acks, 2 push, 4 wait
+  int nack = 0;
+  unsigned long long* ack_out[kP2PMaxAcks] = {};
+  // push
   int64_t ns = 0;
   const int32_t* idx = nullptr;  // owned local index per pushed entry
   double* const* dst = nullptr;  // destination per entry (a peer's halo slot)
@@ -42,17 +54,12 @@ struct P2PSend {  // owner side: push my entries of the peers' halos, then signa
   int npeer = 0;
   unsigned long long* remote_flag[kP2PMaxPeers] = {};  // "delivered" counter in each receiver's arena
   const unsigned long long* ack[kP2PMaxPeers] = {};    // "consumed" counter per receiver in my arena
-  unsigned long long* sends = nullptr;                 // completed pushes of this slot
+  unsigned long long* sends = nullptr;                 // completed pushes of this vector
   unsigned* blocks = nullptr;                          // CTA arrivals (self-resetting)
-};
-struct P2PWait {  // consumer side: wait for every sender's delivery
+  // wait
   int nsrc = 0;
-  const unsigned long long* flag[kP2PMaxPeers] = {};
-  unsigned long long* recvs = nullptr;  // deliveries consumed so far
-};
-struct P2PAck {  // consumer side, after the consuming kernel: free the slots
-  int nsrc = 0;
-  unsigned long long* remote_ack[kP2PMaxPeers] = {};
+  const unsigned long long* flag[kP2PMaxPeers] = {};   // "delivered" counters in my arena
+  unsigned long long* recvs = nullptr;                 // deliveries consumed so far
 };
 
 struct Part {
@@ -78,12 +85,12 @@ struct DVec {
     std::vector<int64_t> recv_off, recv_cnt, send_off, send_cnt;
     DBuf<int32_t> send_idx;
     DBuf<double> send_buf;
-    // p2p: pushed entries (index, destination) and the three parameter blocks
+    // p2p: pushed entries (index, destination), the exchange parameter block
+    // and the "consumed" counters of my owners to bump after reading
     DBuf<int32_t> p2p_idx;
     DBuf<double*> p2p_dst;
-    P2PSend push;
-    P2PWait wait;
-    P2PAck ack;
+    P2PExch exch;
+    std::vector<unsigned long long*> release_to;
   };
   std::vector<Rank> rk;
   DBuf<double*> bases;  // emulation: buf pointer per rank
@@ -135,6 +142,8 @@ struct DHier {
     std::vector<char> owned;
     DBuf<unsigned long long> ctr;  // per local rank: [slot] sends | [slot] receives
     DBuf<unsigned> blocks;         // per local rank and slot: push CTA arrivals
+    // per rank: acks recorded by release() and not yet emitted (enqueue time)
+    std::vector<std::vector<unsigned long long*>> pending;
   } p2p;
   ~DHier();
   bool mine(int r) const { return me < 0 || me == r; }
@@ -145,6 +154,7 @@ struct DHier {
 void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs);
 void p2p_exchange(Ctx& c, DHier& d, DVec& V);
 void p2p_release(Ctx& c, DHier& d, DVec& V);
+void p2p_flush(Ctx& c, DHier& d);  // emit every pending ack (end of a captured body)
 void p2p_free(DHier& d);
 bool p2p_requested();
 

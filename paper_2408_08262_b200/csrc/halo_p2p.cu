@@ -9,17 +9,22 @@
 // Per vector ("slot") and ordered pair (owner o -> consumer q):
 //   F[slot][o] in q's arena  -- deliveries from o (o increments it remotely)
 //   A[slot][q] in o's arena  -- deliveries q has consumed (q increments it)
-// exchange(V): o's push kernel waits until A[slot][q] == pushes so far (q is
-//   done reading the previous contents), stores its entries of q's halo into
-//   q's buffer, fences at system scope, and its last CTA bumps F[slot][o]
-//   with a release add; q's wait kernel spins (acquire) until F[slot][o]
-//   reaches its receive count + 1 for every sender o.
-// release(V), after q's consuming kernel: q bumps A[slot][o] at every sender.
-// Every rank issues the same exchange/release sequence, so a wait only ever
-// depends on pushes and acks its peers issued earlier in their own streams:
-// no circular wait. In emulation all "ranks" share one GPU and one stream;
-// their pushes are enqueued before any of their waits, so no wait blocks.
-// The values moved are copies: the V-cycle stays bit-identical to 1 GPU.
+// exchange(V) is ONE kernel per rank (k_p2p_exchange):
+//   1. the acks this rank owes (slots it finished reading since its last
+//      exchange) go out as release adds on the owners' A counters;
+//   2. wait until A[slot][q] == my pushes of V so far for every receiver q
+//      (q is done with the previous contents), store my entries of q's halo
+//      into q's buffer, fence at system scope, and the last CTA bumps
+//      F[slot][me] at every receiver with a release add;
+//   3. CTA 0 spins (acquire) until F[slot][o] reaches its receive count + 1
+//      for every owner o; the consuming kernel runs after this grid.
+// release(V), after the consuming kernel, only records the acks; the next
+// exchange (or the flush closing a captured body) emits them. Every rank
+// issues the same exchange sequence and phase 1 never waits, so a wait only
+// depends on pushes and acks its peers issue earlier in their own streams:
+// no circular wait. Emulation (all ranks on one GPU, one stream) launches the
+// phases separately: all acks, then all pushes, then all waits, so no wait
+// ever blocks. The values moved are copies: the V-cycle stays bit-identical.
 #include <cstring>
 
 #include "dist.cuh"
@@ -54,37 +59,51 @@ __device__ __forceinline__ void spin_geq(const unsigned long long* p, unsigned l
   }
 }
 
-__global__ void k_p2p_push(const __grid_constant__ P2PSend S) {
+__global__ void k_p2p_exchange(const __grid_constant__ P2PExch E) {
   pdl_wait();
-  const unsigned long long done = *S.sends;  // pushes completed before this one
-  if ((int)threadIdx.x < S.npeer) spin_geq(S.ack[threadIdx.x], done);
-  __syncthreads();
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S.ns; k += (int64_t)gridDim.x * blockDim.x)
-    *S.dst[k] = S.src[S.idx[k]];
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(S.blocks, 1u) == gridDim.x - 1) {  // last CTA
+  if ((E.phases & 1) && blockIdx.x == 0)
+    for (int t = threadIdx.x; t < E.nack; t += blockDim.x) red_release_sys_add(E.ack_out[t], 1ull);
+  if (E.phases & 2) {
+    const unsigned long long done = *E.sends;  // my pushes of this vector so far
+    if ((int)threadIdx.x < E.npeer) spin_geq(E.ack[threadIdx.x], done);
+    __syncthreads();
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < E.ns;
+         k += (int64_t)gridDim.x * blockDim.x)
+      *E.dst[k] = E.src[E.idx[k]];
     __threadfence_system();
-    *S.blocks = 0;
-    for (int p = 0; p < S.npeer; ++p) red_release_sys_add(S.remote_flag[p], 1ull);
-    *S.sends = done + 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(E.blocks, 1u) == gridDim.x - 1) {  // last CTA
+      __threadfence_system();
+      *E.blocks = 0;
+      for (int p = 0; p < E.npeer; ++p) red_release_sys_add(E.remote_flag[p], 1ull);
+      *E.sends = done + 1;
+    }
+  }
+  if ((E.phases & 4) && blockIdx.x == 0) {
+    const unsigned long long target = *E.recvs + 1;
+    if ((int)threadIdx.x < E.nsrc) spin_geq(E.flag[threadIdx.x], target);
+    __syncthreads();
+    if (threadIdx.x == 0) *E.recvs = target;
   }
   pdl_trigger();
 }
 
-__global__ void k_p2p_wait(const __grid_constant__ P2PWait W) {
-  pdl_wait();
-  const unsigned long long target = *W.recvs + 1;
-  if ((int)threadIdx.x < W.nsrc) spin_geq(W.flag[threadIdx.x], target);
-  __syncthreads();
-  if (threadIdx.x == 0) *W.recvs = target;
-  pdl_trigger();
+void launch_exchange(Ctx& c, const P2PExch& E) {
+  const unsigned grid =
+      (E.phases & 2) ? (unsigned)std::min<int64_t>(blocks_for(E.ns, 256), 2 * c.num_sms) : 1u;
+  LAUNCH_PDL(c, k_p2p_exchange, grid, 256, 0, E);
 }
 
-__global__ void k_p2p_ack(const __grid_constant__ P2PAck A) {
-  pdl_wait();  // the consuming kernel has finished reading the halo
-  if ((int)threadIdx.x < A.nsrc) red_release_sys_add(A.remote_ack[threadIdx.x], 1ull);
-  pdl_trigger();
+// phase-1 launches for the acks of rank r (in chunks of kP2PMaxAcks)
+void emit_acks(Ctx& c, std::vector<unsigned long long*>& acks) {
+  for (size_t i = 0; i < acks.size(); i += kP2PMaxAcks) {
+    P2PExch E;
+    E.phases = 1;
+    E.nack = (int)std::min<size_t>(kP2PMaxAcks, acks.size() - i);
+    for (int k = 0; k < E.nack; ++k) E.ack_out[k] = acks[i + k];
+    launch_exchange(c, E);
+  }
+  acks.clear();
 }
 
 constexpr size_t kAlign = 256;
@@ -160,6 +179,7 @@ void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs) {
     return reinterpret_cast<unsigned long long*>(at(r, lay[r].a)) + (size_t)slot * P + by;
   };
   // per local rank: [slot] sends then [slot] receives; CTA counters per slot
+  S.pending.assign(P, {});
   S.ctr.alloc(c, (size_t)2 * S.nslots * P);
   S.ctr.zero(c);
   S.blocks.alloc(c, (size_t)S.nslots * P);
@@ -181,7 +201,8 @@ void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs) {
       // sender side: my entries of every peer's halo, in the peer's halo order
       std::vector<int32_t> idx;
       std::vector<double*> dst;
-      R.push = P2PSend();
+      P2PExch& E = R.exch;
+      E = P2PExch();
       for (int q = 0; q < P; ++q) {
         if (q == r) continue;
         const DVec::Rank& Q = V.rk[q];
@@ -196,29 +217,30 @@ void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs) {
           ++k;
         }
         if (k != cnt) throw RuntimeError("p2p: send list does not match the receiver's halo plan");
-        R.push.remote_flag[R.push.npeer] = F(q, slot, r);
-        R.push.ack[R.push.npeer] = A(r, slot, q);
-        R.push.npeer++;
+        E.remote_flag[E.npeer] = F(q, slot, r);
+        E.ack[E.npeer] = A(r, slot, q);
+        E.npeer++;
       }
       R.p2p_idx.alloc(c, std::max<size_t>(1, idx.size()));
       R.p2p_dst.alloc(c, std::max<size_t>(1, dst.size()));
       to_device(c, R.p2p_idx.p, idx.data(), idx.size());
       to_device(c, R.p2p_dst.p, dst.data(), dst.size());
-      R.push.ns = (int64_t)idx.size();
-      R.push.idx = R.p2p_idx.p;
-      R.push.dst = R.p2p_dst.p;
-      R.push.src = R.buf.p;
-      R.push.sends = S.ctr.p + (size_t)2 * S.nslots * r + slot;
-      R.push.blocks = S.blocks.p + (size_t)S.nslots * r + slot;
+      E.ns = (int64_t)idx.size();
+      E.idx = R.p2p_idx.p;
+      E.dst = R.p2p_dst.p;
+      E.src = R.buf.p;
+      E.sends = S.ctr.p + (size_t)2 * S.nslots * r + slot;
+      E.blocks = S.blocks.p + (size_t)S.nslots * r + slot;
+      E.phases = (E.ns ? 2 : 0);
       // consumer side: every owner I receive from
-      R.wait = P2PWait();
-      R.ack = P2PAck();
+      R.release_to.clear();
       for (int o = 0; o < P; ++o) {
         if (o == r || R.recv_cnt.empty() || !R.recv_cnt[o]) continue;
-        R.wait.flag[R.wait.nsrc++] = F(r, slot, o);
-        R.ack.remote_ack[R.ack.nsrc++] = A(o, slot, r);
+        E.flag[E.nsrc++] = F(r, slot, o);
+        R.release_to.push_back(A(o, slot, r));
       }
-      R.wait.recvs = S.ctr.p + (size_t)2 * S.nslots * r + S.nslots + slot;
+      if (E.nsrc) E.phases |= 4;
+      E.recvs = S.ctr.p + (size_t)2 * S.nslots * r + S.nslots + slot;
     }
     if (d.me < 0) {
       V.bases.alloc(c, (size_t)P);
@@ -229,25 +251,45 @@ void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs) {
 }
 
 void p2p_exchange(Ctx& c, DHier& d, DVec& V) {
+  DHier::P2PState& S = d.p2p;
+  if (d.me >= 0) {  // one process per GPU: the three phases in one kernel
+    P2PExch E = V.rk[d.me].exch;
+    std::vector<unsigned long long*>& acks = S.pending[d.me];
+    if (acks.size() > (size_t)kP2PMaxAcks) emit_acks(c, acks);  // rare: many slots released
+    E.nack = (int)acks.size();
+    for (int k = 0; k < E.nack; ++k) E.ack_out[k] = acks[k];
+    if (E.nack) E.phases |= 1;
+    acks.clear();
+    if (E.phases) launch_exchange(c, E);
+    return;
+  }
+  // emulation: all acks, then all pushes, then all waits
+  for (int r = 0; r < d.P; ++r) emit_acks(c, S.pending[r]);
   for (int r = 0; r < d.P; ++r) {
-    if (!d.mine(r)) continue;
-    const P2PSend& S = V.rk[r].push;
-    if (S.ns)
-      LAUNCH_PDL(c, k_p2p_push, (unsigned)std::min<int64_t>(blocks_for(S.ns, 256), 2 * c.num_sms), 256, 0, S);
+    P2PExch E = V.rk[r].exch;
+    E.phases &= 2;
+    if (E.phases) launch_exchange(c, E);
   }
   for (int r = 0; r < d.P; ++r) {
-    if (!d.mine(r)) continue;
-    const P2PWait& W = V.rk[r].wait;
-    if (W.nsrc) LAUNCH_PDL(c, k_p2p_wait, 1, 32, 0, W);
+    P2PExch E = V.rk[r].exch;
+    E.phases &= 4;
+    if (E.phases) launch_exchange(c, E);
   }
 }
 
 void p2p_release(Ctx& c, DHier& d, DVec& V) {
-  for (int r = 0; r < d.P; ++r) {
-    if (!d.mine(r)) continue;
-    const P2PAck& A = V.rk[r].ack;
-    if (A.nsrc) LAUNCH_PDL(c, k_p2p_ack, 1, 32, 0, A);
-  }
+  (void)c;
+  for (int r = 0; r < d.P; ++r)
+    if (d.mine(r)) {
+      const std::vector<unsigned long long*>& to = V.rk[r].release_to;
+      d.p2p.pending[r].insert(d.p2p.pending[r].end(), to.begin(), to.end());
+    }
+}
+
+void p2p_flush(Ctx& c, DHier& d) {
+  if (!d.p2p.on) return;
+  for (int r = 0; r < d.P; ++r)
+    if (d.mine(r)) emit_acks(c, d.p2p.pending[r]);
 }
 
 void p2p_free(DHier& d) {
