@@ -332,6 +332,14 @@ int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
  * send/recv, 2 = NVLink peer stores (AIRG_TRANSPORT=p2p; emulated or one
  * process per GPU). */
 int airg_dist_transport(const airg_dist* d, int32_t* transport);
+/* Host-only rule of the p2p push (no GPU; CPU / gloo tests): the entries of
+ * the receiver's sorted halo that `sender` owns, as the sender's local index
+ * and the position in the receiver's [own | halo] buffer they are stored to. */
+int airg_p2p_push_plan_host(int32_t nranks, const int64_t* h_starts,
+                            int32_t sender, const int64_t* recv_halo,
+                            int64_t n_recv_halo, int32_t receiver,
+                            int32_t* src_idx, int64_t* dst_pos, int64_t cap,
+                            int64_t* n_push);
 int airg_dist_destroy(airg_dist* d);
 /* ---- Matrix Market exchange (matrix_market.hpp:11-19) ---------------------
  * Host-side, no GPU needed. airg_mm_read parses a "coordinate real general"

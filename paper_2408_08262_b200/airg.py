@@ -110,6 +110,8 @@ def lib() -> C.CDLL:
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
                                       _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
             "airg_dist_transport": ([_VP, _P(C.c_int32)], C.c_int),
+            "airg_p2p_push_plan_host": ([C.c_int32, _VP, C.c_int32, _VP, C.c_int64, C.c_int32, _VP, _VP,
+                                         C.c_int64, _P(C.c_int64)], C.c_int),
             "airg_dist_destroy": ([_VP], C.c_int),
             "airg_mm_read": ([C.c_char_p, _P(_VP)], C.c_int),
             "airg_mm_dims": ([_VP, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
@@ -708,6 +710,21 @@ def plan_host(starts, rank: int, cols):
     _check(lib().airg_dist_plan_host(P, s.ctypes.data, int(rank), c.ctypes.data, len(c), halo.ctypes.data,
                                      len(halo), C.byref(nh), rc.ctypes.data))
     return halo[: nh.value].copy(), rc
+
+
+def p2p_push_plan_host(starts, sender: int, recv_halo, receiver: int):
+    """Host rule of the p2p push (no GPU): the entries of `receiver`'s sorted
+    halo owned by `sender` -> (sender-local indices, positions in the
+    receiver's [own | halo] buffer)."""
+    s = np.ascontiguousarray(starts, np.int64)
+    h = np.ascontiguousarray(recv_halo, np.int64)
+    cap = max(1, len(h))
+    si = np.zeros(cap, np.int32)
+    pos = np.zeros(cap, np.int64)
+    n = C.c_int64()
+    _check(lib().airg_p2p_push_plan_host(len(s) - 1, s.ctypes.data, int(sender), h.ctypes.data, len(h),
+                                         int(receiver), si.ctypes.data, pos.ctypes.data, cap, C.byref(n)))
+    return si[: n.value].copy(), pos[: n.value].copy()
 
 
 def nccl_unique_id() -> bytes:

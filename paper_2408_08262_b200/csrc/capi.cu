@@ -926,4 +926,27 @@ int airg_dist_plan_host(int32_t nranks, const int64_t* starts, int32_t rank, con
   });
 }
 
+int airg_p2p_push_plan_host(int32_t nranks, const int64_t* starts, int32_t sender, const int64_t* recv_halo,
+                            int64_t n_recv_halo, int32_t receiver, int32_t* src_idx, int64_t* dst_pos,
+                            int64_t cap, int64_t* n_push) {
+  return guard([&] {
+    need(starts, "starts");
+    if (sender < 0 || sender >= nranks || receiver < 0 || receiver >= nranks)
+      throw InvalidArgument("dist: rank out of range");
+    std::vector<int64_t> halo(recv_halo, recv_halo + n_recv_halo);
+    const int64_t recv_own = starts[receiver + 1] - starts[receiver];
+    int64_t recv_off = 0;  // the receiver's halo entries owned by lower ranks come first
+    for (int64_t g : halo)
+      if (g < starts[sender]) ++recv_off;
+    std::vector<int32_t> si;
+    std::vector<int64_t> pos;
+    p2p_push_plan(halo, recv_own, recv_off, starts[sender], starts[sender + 1] - starts[sender], si, pos);
+    if (n_push) *n_push = (int64_t)si.size();
+    for (int64_t k = 0; k < cap && k < (int64_t)si.size(); ++k) {
+      if (src_idx) src_idx[k] = si[k];
+      if (dst_pos) dst_pos[k] = pos[k];
+    }
+  });
+}
+
 }  // extern "C"

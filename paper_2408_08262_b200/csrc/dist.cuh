@@ -157,6 +157,13 @@ void p2p_release(Ctx& c, DHier& d, DVec& V);
 void p2p_flush(Ctx& c, DHier& d);  // emit every pending ack (end of a captured body)
 void p2p_free(DHier& d);
 bool p2p_requested();
+// Host rule of the p2p push (also behind airg_p2p_push_plan_host for the CPU
+// tests): the sender's entries of one receiver's sorted halo -- the sender's
+// local index of each, and its position in the receiver's [own | halo]
+// buffer (receiver own count + receive offset of the sender + k).
+void p2p_push_plan(const std::vector<int64_t>& recv_halo, int64_t recv_own, int64_t recv_off,
+                   int64_t send_lo, int64_t send_own, std::vector<int32_t>& src_idx,
+                   std::vector<int64_t>& dst_pos);
 
 void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double threshold,
                  const int64_t* level0_starts, DHier& d);

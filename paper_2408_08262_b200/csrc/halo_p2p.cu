@@ -131,6 +131,20 @@ Layout layout(const std::vector<DVec*>& vecs, int r, int P) {
 
 }  // namespace
 
+void p2p_push_plan(const std::vector<int64_t>& recv_halo, int64_t recv_own, int64_t recv_off,
+                   int64_t send_lo, int64_t send_own, std::vector<int32_t>& src_idx,
+                   std::vector<int64_t>& dst_pos) {
+  src_idx.clear();
+  dst_pos.clear();
+  // the receiver's halo is sorted and the owners' slabs are contiguous, so my
+  // entries form one run starting at its receive offset for me
+  for (int64_t g : recv_halo) {
+    if (g < send_lo || g >= send_lo + send_own) continue;
+    dst_pos.push_back(recv_own + recv_off + (int64_t)src_idx.size());
+    src_idx.push_back((int32_t)(g - send_lo));
+  }
+}
+
 bool p2p_requested() {
   static const bool v = [] {
     const char* e = getenv("AIRG_TRANSPORT");
@@ -209,14 +223,14 @@ void p2p_setup(Ctx& c, DHier& d, const std::vector<DVec*>& vecs) {
         const int64_t cnt = Q.recv_cnt.empty() ? 0 : Q.recv_cnt[r];
         if (!cnt) continue;
         double* qbuf = reinterpret_cast<double*>(at(q, lay[q].buf[slot]));
-        int64_t k = 0;
-        for (int64_t g : Q.halo_host) {
-          if (g < R.lo || g >= R.lo + R.own) continue;
-          idx.push_back((int32_t)(g - R.lo));
-          dst.push_back(qbuf + Q.own + Q.recv_off[r] + k);
-          ++k;
+        std::vector<int32_t> si;
+        std::vector<int64_t> pos;
+        p2p_push_plan(Q.halo_host, Q.own, Q.recv_off[r], R.lo, R.own, si, pos);
+        if ((int64_t)si.size() != cnt) throw RuntimeError("p2p: send list does not match the receiver's halo plan");
+        for (size_t k = 0; k < si.size(); ++k) {
+          idx.push_back(si[k]);
+          dst.push_back(qbuf + pos[k]);
         }
-        if (k != cnt) throw RuntimeError("p2p: send list does not match the receiver's halo plan");
         E.remote_flag[E.npeer] = F(q, slot, r);
         E.ack[E.npeer] = A(r, slot, q);
         E.npeer++;

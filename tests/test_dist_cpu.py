@@ -30,6 +30,19 @@ def test_plan_host_rule():
         assert np.array_equal(np.bincount(owners, minlength=3), rc)
     with pytest.raises(airg.InvalidArgument):
         airg.plan_host(starts, 3, a.cols[:4])
+    # the p2p push rule: every receiver's halo entry is pushed by its owner,
+    # once, to slot own + (its position in the receiver's sorted halo)
+    for q in range(3):
+        lo, hi = starts[q], starts[q + 1]
+        halo, _ = airg.plan_host(starts, q, a.cols[a.row_offsets[lo]:a.row_offsets[hi]])
+        filled = np.zeros(len(halo), int)
+        for r in range(3):
+            if r == q:
+                continue
+            si, pos = airg.p2p_push_plan_host(starts, r, halo, q)
+            assert np.array_equal(starts[r] + si, halo[pos - (hi - lo)])
+            filled[pos - (hi - lo)] += 1
+        assert (filled == 1).all()
 
 
 def _free_port():
@@ -88,7 +101,25 @@ def _worker(rank, world, port, result_q):
         g = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(g, t)
         ratio = np.mean([int(x[0]) / int(x[1]) for x in g if int(x[1]) > 0])
-        result_q.put((rank, bool(ok), len(halo), float(ratio)))
+        # the p2p transport's addressing (airg_p2p_push_plan_host): the peer
+        # computes where each of its values lands in MY [own | halo] buffer
+        # from my plan alone; ship (position, value) pairs and place them
+        my_push_idx, my_push_pos = airg.p2p_push_plan_host(starts, rank, np.array(lists[peer], np.int64), peer)
+        pair = torch.from_numpy(np.stack([my_push_pos.astype(np.float64), x_own[my_push_idx]]).copy())
+        n_in = torch.tensor([pair.shape[1]], dtype=torch.int64)
+        n_peer = torch.zeros(1, dtype=torch.int64)
+        reqs = [dist.isend(n_in, peer), dist.irecv(n_peer, peer)]
+        for q in reqs:
+            q.wait()
+        got = torch.zeros((2, int(n_peer[0])), dtype=torch.float64)
+        reqs = [dist.isend(pair, peer), dist.irecv(got, peer)]
+        for q in reqs:
+            q.wait()
+        x_p2p = np.full(hi - lo + len(halo), np.nan)
+        x_p2p[: hi - lo] = x_own
+        x_p2p[got[0].numpy().astype(np.int64)] = got[1].numpy()
+        ok_p2p = not np.isnan(x_p2p).any() and np.array_equal(x_p2p.view(np.uint64), x_local.view(np.uint64))
+        result_q.put((rank, bool(ok and ok_p2p), len(halo), float(ratio)))
     finally:
         dist.destroy_process_group()
 
