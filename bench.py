@@ -461,7 +461,8 @@ def run_gpu(args):
     for rep in range(2):
         s0, s1 = ev(), ev()
         s0.record(stream)
-        airg.cf_split_batch_device(mats, seeds, prm["strength_alpha"], prm["max_loops"], labels=cf_lab, ctx=ctx)
+        _, cf_reps = airg.cf_split_batch_device(mats, seeds, prm["strength_alpha"], prm["max_loops"],
+                                                labels=cf_lab, ctx=ctx)
         s1.record(stream)
         s1.synchronize()
         cf_ms = s0.elapsed_time(s1)
@@ -474,6 +475,11 @@ def run_gpu(args):
             s1.synchronize()
             tot += s0.elapsed_time(s1)
         cf_ms_each = tot
+    # SURVEY 8(d) CF-split bytes per level: 2(12 nnz + 4n) + 16|S| + 26n
+    cf_bytes = 0
+    for Al, rp in zip(mats, cf_reps):
+        n_l, _, z_l = Al.dims()
+        cf_bytes += 2 * (12 * z_l + 4 * n_l) + 16 * int(rp.s_nnz) + 26 * n_l
     for l in range(info.n_levels):  # the split re-derives the setup's labels (untimed check)
         if not np.array_equal(cf_lab[l][: mats[l].dims()[0]].cpu().numpy(), h.labels(l)):
             raise RuntimeError(f"CF split of level {l} differs from the hierarchy's labels")
@@ -622,6 +628,10 @@ def run_gpu(args):
         "iterations": int(st.iterations), "final_relative_residual": float(rel),
         "levels": int(info.n_levels), "operator_complexity": info.operator_complexity,
         "setup_ms": setup_ms, "cf_split_ms": cf_ms, "cf_split_ms_sync_each_level": cf_ms_each,
+        "cf_split_roofline": {"bound": "hbm", "achieved": cf_bytes / (cf_ms / 1e3) / 1e9, "peak": peak,
+                              "unit": "GB/s", "frac": cf_bytes / (cf_ms / 1e3) / 1e9 / peak,
+                              "alg_bytes_all_levels": cf_bytes,
+                              "bytes_rule": "sum over levels of 2(12 nnz + 4n) + 16|S| + 26n (SURVEY 8d)"},
         "roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
                      "frac": step_achieved / peak, "traffic": step_traffic,
                      "kernel": "one AIRG solve step: the captured V-cycle graph of all row kernels, "
