@@ -24,7 +24,9 @@ import numpy as np
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libairg_b200.so")
+# AIRG_LIB: an alternative build of the same engine (A/B variants built by
+# `make -C csrc variant V=<tag> XFLAGS=...`, tools/ab_variants.sh); default in-tree
+LIB_PATH = os.environ.get("AIRG_LIB") or os.path.join(HERE, "libairg_b200.so")
 
 
 class InvalidArgument(ValueError):

@@ -316,7 +316,7 @@ inline TileView rows_of(const Csr& m) {
 template <class Epi>
 void launch_rows(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
   const TileView v = rows_of(m);
-  auto* k = v.vec == 8 ? &rows_thread<Epi, true> : v.vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;
+  auto* k = v.vec == 8 ? &rows_thread<Epi, true, kVecBatch> : v.vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false, kScalarBatch>;
   LAUNCH_PDL(c, k, blocks_for(m.n, kTileThreads), kTileThreads, 0, v, x, epi);
 }
 template <class Epi>
@@ -324,7 +324,7 @@ void launch_rows_fc(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
   const TileView v = rows_of(m);
   auto* k = v.vec == 8   ? &rows_thread_fc<Epi, true, kFcVecBatch>
             : v.vec == 4 ? &rows_thread_fc<Epi, false, 4>
-                         : &rows_thread_fc<Epi, false>;
+                         : &rows_thread_fc<Epi, false, kScalarBatch>;
   LAUNCH_PDL(c, k, blocks_for(m.n, kTileThreads), kTileThreads, 0, v, x, epi);
 }
 

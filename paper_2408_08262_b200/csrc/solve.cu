@@ -151,7 +151,7 @@ struct EpiResid {
 };
 
 inline TileView tv(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p};
+  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p, m.stage};
 }
 inline SellView svw(const Csr& m) {
   return SellView{m.s_off.p, m.s_len.p, m.s_perm.p, m.s_ci.p, m.s_v.p, m.n, m.s_nslices, m.s_g};

@@ -316,6 +316,52 @@ bool solve_layout_sell() {
   return v;
 }
 
+// widest 128-row block slice [rp[r0] & ~3, rp[r1]) of a matrix (staged.cuh)
+__global__ void k_block_span(int n, const int32_t* __restrict__ rp, unsigned* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = b * kTileThreads;
+  if (r0 >= n) return;
+  const int r1 = min(r0 + kTileThreads, n);
+  atomicMax(out, (unsigned)(rp[r1] - (rp[r0] & ~3)));
+}
+
+// AIRG_STAGE=1: row kernels of the captured V-cycle stage each block's
+// (column, value) slice in shared memory by bulk copies (staged.cuh) for
+// every matrix that is not short-row; capacity = the widest block slice,
+// capped at AIRG_STAGE_CAP entries (default 4000: 48 KB; wider blocks walk
+// global memory)
+static bool stage_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_STAGE");
+#if defined(AIRG_STAGE_DEFAULT) && AIRG_STAGE_DEFAULT
+    return !(e && e[0] == '0');
+#else
+    return e && e[0] == '1';
+#endif
+  }();
+  return v;
+}
+
+static void build_stage(Ctx& c, Csr& a) {
+  static const int cap = [] {
+    const char* e = getenv("AIRG_STAGE_CAP");
+    const int v = e ? atoi(e) : 4000;
+    return v < 4 ? 4 : v > 4000 ? 4000 : v;
+  }();
+  a.stage = 0;
+  if (!stage_enabled() || a.n <= 0 || a.group > 1 || a.perm.p || a.c16.p) return;
+  if (row_vec(a.n, a.nnz) == 4) return;  // short rows: per-thread loads already touch whole lines
+  if (((uintptr_t)a.ci.p & 15) || ((uintptr_t)a.v.p & 15)) return;
+  DBuf<unsigned> sp(c, 1);
+  sp.zero(c);
+  const int nb = (a.n + kTileThreads - 1) / kTileThreads;
+  LAUNCH(c, k_block_span, blocks_for(nb, 256), 256, 0, a.n, a.rp.p, sp.p);
+  unsigned h = 0;
+  to_host(c, &h, sp.p, 1);
+  const int need = ((int)h + 3) & ~3;
+  a.stage = need < cap ? need : (cap & ~3);
+}
+
 void build_tiles(Ctx& c, Csr& a) {
   if (a.row_mode != 0) return;
   const int ov = rows_override();
@@ -352,6 +398,7 @@ void build_tiles(Ctx& c, Csr& a) {
         LAUNCH(c, k_make_c16, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, a.c16.p, a.cbase.p);
       }
     }
+    build_stage(c, a);
     return;
   }
   const bool short_rows = ov ? ov == 1 : (a.n == 0 || a.nnz <= (int64_t)kShortRow * a.n);

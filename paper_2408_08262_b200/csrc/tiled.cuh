@@ -42,6 +42,7 @@ struct TileView {
   const int32_t* perm = nullptr;  // thread -> row (rows sorted by length per block), null = identity
   const uint16_t* c16 = nullptr;  // 16-bit column deltas (rowdot.cuh dot16), null = int32 columns
   const int32_t* cbase = nullptr;
+  int stage = 0;         // > 0: staged row kernels (staged.cuh), shared slice capacity in entries
 };
 
 // ---- thread per row -----------------------------------------------------------
@@ -163,6 +164,16 @@ constexpr int kFcMinBlocks = AIRG_FC_MIN_BLOCKS;
 #define AIRG_FC_VEC_BATCH 8
 #endif
 constexpr int kFcVecBatch = AIRG_FC_VEC_BATCH;
+// entries per batch of the other long-row kernels (aligned vector batches)
+// and of the mid-length scalar kernels
+#ifndef AIRG_VEC_BATCH
+#define AIRG_VEC_BATCH 8
+#endif
+#ifndef AIRG_SCALAR_BATCH
+#define AIRG_SCALAR_BATCH 8
+#endif
+constexpr int kVecBatch = AIRG_VEC_BATCH;
+constexpr int kScalarBatch = AIRG_SCALAR_BATCH;
 template <class Epi, bool VEC = false, int VB = kRowBatch>
 __global__ void __launch_bounds__(kTileThreads, kFcMinBlocks) rows_thread_fc(TileView m, const double* __restrict__ x,
                                                                Epi epi) {
@@ -374,6 +385,10 @@ __global__ void __launch_bounds__(kTileThreads) rows_group_fc(TileView m, const 
   if (lane == 0) epi.row2(r, sf, sc);
 }
 
+}  // namespace airg
+#include "staged.cuh"
+namespace airg {
+
 // grid size for either mode
 inline unsigned rows_grid(const TileView& m) {
   if (m.tiles) return (unsigned)((m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock > 0
@@ -410,7 +425,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group, Epi, view, x, epi)                                  \
     else {                                                                           \
-      auto* kfn__ = (view).c16 ? &rows_thread16<Epi> : (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;   \
+      auto* kfn__ = (view).c16 ? &rows_thread16<Epi> : (view).vec == 8 ? &rows_thread<Epi, true, kVecBatch> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false, kScalarBatch>;   \
       LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);              \
     }                                                                                \
   } while (0)
@@ -421,8 +436,10 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);    \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
+    else if ((view).stage > 0)                                                                  \
+      LAUNCH_PDL(ctx, (rows_staged<Epi, false>), rows_grid(view), kTileThreads, stage_smem(view), view, x, epi); \
     else {                                                                                      \
-      auto* kfn__ = (view).c16 ? &rows_thread16<Epi> : (view).vec == 8 ? &rows_thread<Epi, true> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false>;              \
+      auto* kfn__ = (view).c16 ? &rows_thread16<Epi> : (view).vec == 8 ? &rows_thread<Epi, true, kVecBatch> : (view).vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false, kScalarBatch>;              \
       LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
     }                                                                                           \
   } while (0)
@@ -432,8 +449,10 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
+    else if ((view).stage > 0)                                                                  \
+      LAUNCH_PDL(ctx, (rows_staged<Epi, true>), rows_grid(view), kTileThreads, stage_smem(view), view, x, epi); \
     else {                                                                                      \
-      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true, kFcVecBatch> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;        \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true, kFcVecBatch> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false, kScalarBatch>;        \
       LAUNCH_PDL(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                     \
     }                                                                                           \
   } while (0)
@@ -444,7 +463,7 @@ inline unsigned rows_grid(const TileView& m) {
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH, ctx, rows_group_fc, Epi, view, x, epi)                                  \
     else {                                                                              \
-      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true, kFcVecBatch> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false>;  \
+      auto* kfn__ = (view).vec == 8 ? &rows_thread_fc<Epi, true, kFcVecBatch> : (view).vec == 4 ? &rows_thread_fc<Epi, false, 4> : &rows_thread_fc<Epi, false, kScalarBatch>;  \
       LAUNCH(ctx, kfn__, rows_grid(view), kTileThreads, 0, view, x, epi);                   \
     }                                                                                   \
   } while (0)
