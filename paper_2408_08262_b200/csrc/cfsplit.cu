@@ -693,6 +693,19 @@ double dominance_max(Ctx& c, const Csr& aff, int rb) {
 // Same arithmetic as the kernels above, so the same labels bit for bit.
 namespace {
 
+// build knobs: AIRG_CF_UNROLL = unroll of the 16-byte row loop; AIRG_CF_WARR:
+// the PMISR weights are written once per level by fcf_wfill after the counts
+// are complete, and the marks pass reads w[j] instead of rebuilding each
+// neighbour's weight from its counts and the hash (the rebuilt-weight marks
+// pass is issue bound: ncu 63 % issue at C2 level 3)
+#ifndef AIRG_CF_UNROLL
+#define AIRG_CF_UNROLL 1
+#endif
+#ifndef AIRG_CF_WARR
+#define AIRG_CF_WARR 0
+#endif
+constexpr int kCfUnroll = AIRG_CF_UNROLL;
+
 // Visit the entries k = s..e-1 of one row in order, f(ci[k], v[k]). VEC:
 // the aligned body as 16-byte loads (4 column indices, 2 x 2 values) --
 // fewer, wider loads per thread for long rows; same order, same results.
@@ -702,6 +715,7 @@ __device__ __forceinline__ void for_row(const int32_t* __restrict__ ci, const do
   int k = s;
   if (VEC) {
     for (; k < e && (k & 3); ++k) f(__ldg(ci + k), __ldg(v + k));
+#pragma unroll (kCfUnroll)
     for (; k + 4 <= e; k += 4) {
       const int4 c = __ldg(reinterpret_cast<const int4*>(ci + k));
       const double2 a = __ldg(reinterpret_cast<const double2*>(v + k));
@@ -856,6 +870,39 @@ __global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* 
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) fcf_row_marks<VEC, false>(i, rp, ci, v, thr, cnt, key, notmin);
+}
+
+// the PMISR weight of every row, once the counts are complete
+__global__ void fcf_wfill(int n, const int2* __restrict__ cnt, uint64_t key, double* __restrict__ w) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] = fcf_weight(cnt, key, i);
+}
+
+// not-minimal marks with the weights read from w (same decisions as
+// fcf_row_marks: weight_less(w, j, i) of coarsening.cpp:46-48)
+template <bool VEC>
+__global__ void fcf_marks_w(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ thr,
+                            const double* __restrict__ w, uint8_t* __restrict__ notmin) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double t = thr[i];
+  const double wi = w[i];
+  bool mine = false;
+  for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
+    const double mag = fabs(x);
+    if (j == i || !(mag > 0.0) || !(mag >= t)) return;
+    const double wj = w[j];
+    if (wj != wi ? wj < wi : j < i)
+      mine = true;
+    else
+      notmin[j] = 1;
+  });
+  if (mine) notmin[i] = 1;
 }
 
 // theta of an F row over A's F columns in column order (= its A_ff row);
@@ -1237,7 +1284,7 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   const size_t nb = ddc_enabled ? (size_t)bins : 0;
   const size_t zero_bytes = (8 + nb) * 8 + (size_t)n * 8 + (size_t)n;
   const size_t head = (zero_bytes + 15) & ~(size_t)15;
-  const size_t bytes = head + 2 * (size_t)n * 8;
+  const size_t bytes = head + (AIRG_CF_WARR ? 3 : 2) * (size_t)n * 8;
   uint8_t* base = static_cast<uint8_t*>(ctx_scratch(c, bytes));
   unsigned long long* u = reinterpret_cast<unsigned long long*>(base);
   unsigned long long* hist = u + 8;
@@ -1245,6 +1292,7 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + n);
   double* thr = reinterpret_cast<double*>(base + head);
   double* theta = thr + n;
+  double* wts = theta + n;  // AIRG_CF_WARR only
   // u: [0] |S| [1] n_f_pre [2] max theta bits [3] ~(first bad row), 0 = none
   //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
   const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
@@ -1287,7 +1335,13 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
     k_theta = G == 4 ? fcf_theta_g<4> : G == 8 ? fcf_theta_g<8> : fcf_theta_g<16>;
   }
   LAUNCH_PDL(c, k_rows, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, u);
-  LAUNCH_PDL(c, k_marks, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, cnt, key, notmin);
+  if (AIRG_CF_WARR && G <= 1) {
+    LAUNCH_PDL(c, fcf_wfill, g, 256, 0, n, (const int2*)cnt, key, wts);
+    LAUNCH_PDL(c, vec ? fcf_marks_w<true> : fcf_marks_w<false>, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p,
+               (const double*)thr, (const double*)wts, notmin);
+  } else {
+    LAUNCH_PDL(c, k_marks, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, cnt, key, notmin);
+  }
   if (ddc_enabled) {
     LAUNCH_PDL(c, k_theta, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, notmin, theta, d_labels_pre, u + 2, u + 3);
     const unsigned hb = (unsigned)std::min<int64_t>(g, 4 * c.num_sms);

@@ -150,8 +150,24 @@ struct EpiResid {
   }
 };
 
+// AIRG_WG=4|8|16: matrices whose mean row length is >= AIRG_WG_ROWS (default
+// 12) run the long-row group kernels (wgroup.cuh) in the captured V-cycle
+inline int wg_lanes(const Csr& m) {
+  static const int g = [] {
+    const char* e = getenv("AIRG_WG");
+    const int v = e ? atoi(e) : 0;
+    return v == 4 || v == 8 || v == 16 ? v : 0;
+  }();
+  static const int64_t rows = [] {
+    const char* e = getenv("AIRG_WG_ROWS");
+    return e ? (int64_t)atoi(e) : (int64_t)12;
+  }();
+  if (!g || m.n <= 0 || m.row_mode != 1 || m.group > 1 || m.perm.p || m.c16.p) return 0;
+  return m.nnz >= rows * (int64_t)m.n ? g : 0;
+}
+
 inline TileView tv(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p, m.stage};
+  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p, m.stage, wg_lanes(m)};
 }
 inline SellView svw(const Csr& m) {
   return SellView{m.s_off.p, m.s_len.p, m.s_perm.p, m.s_ci.p, m.s_v.p, m.n, m.s_nslices, m.s_g};

@@ -43,6 +43,7 @@ struct TileView {
   const uint16_t* c16 = nullptr;  // 16-bit column deltas (rowdot.cuh dot16), null = int32 columns
   const int32_t* cbase = nullptr;
   int stage = 0;         // > 0: staged row kernels (staged.cuh), shared slice capacity in entries
+  int wg = 0;            // > 0: lanes per row of the long-row group kernels (wgroup.cuh)
 };
 
 // ---- thread per row -----------------------------------------------------------
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(kTileThreads) rows_group_fc(TileView m, const 
 
 }  // namespace airg
 #include "staged.cuh"
+#include "wgroup.cuh"
 namespace airg {
 
 // grid size for either mode
@@ -394,7 +396,7 @@ inline unsigned rows_grid(const TileView& m) {
   if (m.tiles) return (unsigned)((m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock > 0
                                      ? (m.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock
                                      : 1);
-  const int64_t threads = (int64_t)m.nrows * (m.group > 1 ? m.group : 1);
+  const int64_t threads = (int64_t)m.nrows * (m.wg > 0 ? m.wg : m.group > 1 ? m.group : 1);
   const int64_t blocks = (threads + kTileThreads - 1) / kTileThreads;
   return (unsigned)(blocks > 0 ? blocks : 1);
 }
@@ -417,6 +419,19 @@ inline unsigned rows_grid(const TileView& m) {
     ROWS_GROUP_CASE(LAUNCHER, ctx, KERNEL, 32, Epi, view, x, epi)   \
   }
 
+// long-row group kernels on the view's lane count (wgroup.cuh)
+#define WG_SWITCH(ctx, FC, Epi, view, x, epi)                                                   \
+  switch ((view).wg) {                                                                          \
+    case 4:                                                                                     \
+      LAUNCH_PDL(ctx, (rows_wgroup<4, kWgB * 2, FC, Epi>), rows_grid(view), kTileThreads, 0, view, x, epi); \
+      break;                                                                                    \
+    case 16:                                                                                    \
+      LAUNCH_PDL(ctx, (rows_wgroup<16, 2, FC, Epi>), rows_grid(view), kTileThreads, 0, view, x, epi); \
+      break;                                                                                    \
+    default:                                                                                    \
+      LAUNCH_PDL(ctx, (rows_wgroup<8, kWgB, FC, Epi>), rows_grid(view), kTileThreads, 0, view, x, epi); \
+  }
+
 // Launch helpers (used inside LAUNCH-counted wrappers).
 #define LAUNCH_ROWS(ctx, Epi, view, x, epi)                                          \
   do {                                                                               \
@@ -436,6 +451,8 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);    \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
+    else if ((view).wg > 0)                                                                     \
+      WG_SWITCH(ctx, false, Epi, view, x, epi)                                                  \
     else if ((view).stage > 0)                                                                  \
       LAUNCH_PDL(ctx, (rows_staged<Epi, false>), rows_grid(view), kTileThreads, stage_smem(view), view, x, epi); \
     else {                                                                                      \
@@ -449,6 +466,8 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
+    else if ((view).wg > 0)                                                                     \
+      WG_SWITCH(ctx, true, Epi, view, x, epi)                                                   \
     else if ((view).stage > 0)                                                                  \
       LAUNCH_PDL(ctx, (rows_staged<Epi, true>), rows_grid(view), kTileThreads, stage_smem(view), view, x, epi); \
     else {                                                                                      \

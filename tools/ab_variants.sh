@@ -15,7 +15,7 @@ run() {  # tag envlist
   [ "$1" != base ] && lib=$PWD/paper_2408_08262_b200/variants/libairg_$1.so
   ( [ -n "$lib" ] && export AIRG_LIB=$lib
     IFS=, ; for kv in $2; do [ -n "$kv" ] && export "$kv"; done
-    timeout 300 python tools/iter_cost.py ) >> $out 2>&1
+    timeout 300 python ${AB_CMD:-tools/iter_cost.py} ) >> $out 2>&1
 }
 for rep in 1 2; do
   echo "== base" >> $out; run base ""
