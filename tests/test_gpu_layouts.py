@@ -1,5 +1,6 @@
 """Every row-kernel decomposition gives the same bits (tiled.cuh): thread per
-row, G-lane groups (G = 2..32), warp tiles and SELL-32/G, selected by
+row, G-lane groups (G = 2..32), warp tiles, SELL-32/G, shared-memory staged
+slices and long-row lane groups, selected by
 environment variables that are read once per process -- hence one
 subprocess per layout. Each prints the SHA-256 of the solution's bytes of a
 reduced C2 solve and of a level-0 SpMV."""
@@ -48,6 +49,11 @@ LAYOUTS = {
     "tail_cluster_all": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "100000000"},
     "tail_cluster_small": {"AIRG_TAIL": "cluster", "AIRG_TAIL_N": "2000"},
     "tail_grid_all": {"AIRG_TAIL": "grid", "AIRG_TAIL_N": "100000000"},
+    "staged": {"AIRG_STAGE": "1"},
+    "staged_small_cap": {"AIRG_STAGE": "1", "AIRG_STAGE_CAP": "64"},
+    "wg4_all": {"AIRG_WG": "4", "AIRG_WG_ROWS": "1"},
+    "wg8": {"AIRG_WG": "8"},
+    "wg16_all": {"AIRG_WG": "16", "AIRG_WG_ROWS": "1"},
 }
 
 
@@ -55,7 +61,7 @@ def _run(env_extra):
     env = dict(os.environ)
     for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N", "AIRG_TAIL",
               "AIRG_DEVLOOP", "AIRG_EARLY", "AIRG_SPLIT", "AIRG_SORT",
-              "AIRG_C16"):
+              "AIRG_C16", "AIRG_STAGE", "AIRG_STAGE_CAP", "AIRG_WG", "AIRG_WG_ROWS"):
         env.pop(k, None)
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
