@@ -172,6 +172,14 @@ int airg_csr_device_ptrs(const airg_csr* a, const int32_t** d_row_offsets,
                          const int32_t** d_cols, const double** d_vals);
 int airg_csr_destroy(airg_csr* a);
 
+/* ---- device buffers (for C / C++ / FFI hosts that do not link CUDA) ------- */
+/* Stream-ordered allocation on the context's device (synchronised). */
+int airg_device_alloc(airg_ctx* ctx, size_t bytes, void** d_out);
+int airg_device_free(airg_ctx* ctx, void* d_ptr);
+/* to_device != 0: host -> device, else device -> host (synchronised). */
+int airg_memcpy(airg_ctx* ctx, void* dst, const void* src, size_t bytes,
+                int32_t to_device);
+
 /* ---- L0 kernels ---------------------------------------------------------- */
 /* y = A x (sparse.cpp:185-201): sequential per-row accumulation in column
  * order without FMA, bit-identical to the reference. */
@@ -243,6 +251,18 @@ int airg_cf_split_host(airg_ctx* ctx, const airg_csr* a, double alpha,
 int airg_ddc(airg_ctx* ctx, const airg_csr* a, uint8_t* d_labels,
              double fraction, int64_t bins, int32_t selection,
              double direct_alpha_diag, airg_cf_report* report);
+/* dominance_report (coarsening.cpp:219-250; coarsening.hpp:106) of an A_ff
+ * block: theta per row into d_theta (device, nullable), the bins-bin
+ * histogram over [0, max theta] into h_hist (host int64[bins], nullable),
+ * max theta. Zero diagonal: AIRG_ERUNTIME "... zero diagonal in A_ff row i". */
+int airg_dominance_report(airg_ctx* ctx, const airg_csr* a_ff, int64_t bins,
+                          double* d_theta, int64_t* h_hist, double* max_theta);
+/* build_label_map (sparse.cpp:270-290; sparse.hpp:133): stable F-then-C
+ * sub-indexing of device labels; host int64 outputs (each nullable):
+ * fine_to_sub[n], f_to_fine[n_f], c_to_fine[n - n_f]. */
+int airg_build_label_map(airg_ctx* ctx, const uint8_t* d_labels, int64_t n,
+                         int64_t* h_fine_to_sub, int64_t* h_f_to_fine,
+                         int64_t* h_c_to_fine, int64_t* n_f);
 /* extract_blocks (sparse.cpp:292-340): A_ff, A_fc, A_cf (A_cc unused). */
 int airg_extract_blocks(airg_ctx* ctx, const airg_csr* a,
                         const uint8_t* d_labels, airg_csr** aff,
@@ -286,7 +306,34 @@ int airg_hier_labels(airg_ctx* ctx, const airg_hier* h, int64_t level,
                      uint8_t* h_labels);
 int airg_hier_destroy(airg_hier* h);
 
+/* ---- transfer operators (air.hpp:96-116) ----------------------------------- */
+/* build_restriction(a_cf, aff_inv, drop_restrict, map) (air.cpp:154-189):
+ * R = [-drop(A_cf Aff_inv, drop, keep_diagonal=false) | I] in fine columns;
+ * the map is built from the n device labels. */
+int airg_build_restriction(airg_ctx* ctx, const airg_csr* a_cf,
+                           const airg_csr* aff_inv, double drop_restrict,
+                           const uint8_t* d_labels, int64_t n, airg_csr** out);
+/* build_prolongation(labels, map, g, a) (air.cpp:191-238): one-point P from
+ * the strength pattern s (airg_strength of a) and a. */
+int airg_build_prolongation(airg_ctx* ctx, const airg_csr* a, const airg_csr* s,
+                            const uint8_t* d_labels, airg_csr** out);
+/* coarse_matrix(r, a, p, drop_coarse) (air.cpp:268-271):
+ * drop_entries(R (A P), drop_coarse). */
+int airg_coarse_matrix(airg_ctx* ctx, const airg_csr* r, const airg_csr* a,
+                       const airg_csr* p, double drop_coarse, airg_csr** out);
+/* apply_polynomial(a, p, b) (gmres_poly.cpp:173-195; gmres_poly.hpp:40-43):
+ * d_y = q(A) d_b by Horner over coefficients[0..effective_order] (host),
+ * effective_order matvecs, products and sums rounded separately. */
+int airg_apply_polynomial(airg_ctx* ctx, const airg_csr* a, const double* coeffs,
+                          int64_t ncoeffs, int64_t effective_order,
+                          const double* d_b, double* d_y);
+
 /* ---- L3 solve (solve.hpp) -------------------------------------------------- */
+/* f_smooth(level, b, x) (solve.cpp:63-87; solve.hpp:43-46) on level `level`
+ * of a built hierarchy: x_F += Aff_inv ((b_F - A_FF x_F) - A_FC x_C) in
+ * place on the device vector d_x (the level's size); C entries untouched. */
+int airg_f_smooth(airg_ctx* ctx, const airg_hier* h, int64_t level,
+                  const double* d_b, double* d_x);
 /* vcycle (solve.cpp:150-165) from x = 0 (x_is_zero): d_x = V(d_b). */
 int airg_vcycle(airg_ctx* ctx, const airg_hier* h, const airg_solve_config* cfg,
                 const double* d_b, double* d_x);

@@ -2021,6 +2021,90 @@ int orc_hier_labels(const void* hp, int64_t l, uint8_t* labels) {
   memcpy(labels, h->lev[l].map.label, (size_t)h->lev[l].a->n);
   API_END
 }
+/* ---- single operations of the reference API (dominance_report, label map,
+ * transfer operators, polynomial application, one F-smooth) ---- */
+int orc_dominance_report(const void* aff, int64_t bins, double* theta, int64_t* hist, double* max_theta) {
+  API_BEGIN
+  domrep r = dominance_report((const csr*)aff, bins);
+  if (theta) memcpy(theta, r.theta, sizeof(double) * (size_t)r.n);
+  if (hist) memcpy(hist, r.hist, sizeof(int64_t) * (size_t)bins);
+  if (max_theta) *max_theta = r.max_theta;
+  domrep_free(&r);
+  API_END
+}
+int orc_build_label_map(const uint8_t* labels, int64_t n, int64_t* fine_to_sub, int64_t* f_to_fine,
+                        int64_t* c_to_fine, int64_t* n_f) {
+  API_BEGIN
+  labelmap m = build_label_map(labels, n);
+  if (fine_to_sub) memcpy(fine_to_sub, m.fine_to_sub, sizeof(int64_t) * (size_t)n);
+  if (f_to_fine) memcpy(f_to_fine, m.f_to_fine, sizeof(int64_t) * (size_t)m.nf);
+  if (c_to_fine) memcpy(c_to_fine, m.c_to_fine, sizeof(int64_t) * (size_t)m.nc);
+  if (n_f) *n_f = m.nf;
+  map_free(&m);
+  API_END
+}
+int orc_build_restriction(const void* acf, const void* ffinv, double drop, const uint8_t* labels, int64_t n,
+                          void** out) {
+  API_BEGIN
+  labelmap m = build_label_map(labels, n);
+  *out = build_restriction((const csr*)acf, (const csr*)ffinv, drop, &m);
+  map_free(&m);
+  API_END
+}
+int orc_build_prolongation(const void* ap, const void* s_pattern, const uint8_t* labels, void** out) {
+  API_BEGIN
+  const csr* a = (const csr*)ap;
+  const csr* s = (const csr*)s_pattern;
+  sgraph g;
+  memset(&g, 0, sizeof g);
+  g.n = s->n;
+  g.s_rp = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)(s->n + 1));
+  g.s_ci = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)(nnz_of(s) + 1));
+  memcpy(g.s_rp, s->rp, sizeof(int64_t) * (size_t)(s->n + 1));
+  memcpy(g.s_ci, s->ci, sizeof(int64_t) * (size_t)nnz_of(s));
+  finish_graph(&g);
+  labelmap m = build_label_map(labels, a->n);
+  *out = build_prolongation(labels, &m, &g, a);
+  map_free(&m);
+  graph_free(&g);
+  API_END
+}
+int orc_coarse_matrix(const void* r, const void* a, const void* p, double drop, void** out) {
+  API_BEGIN
+  *out = coarse_matrix((const csr*)r, (const csr*)a, (const csr*)p, drop);
+  API_END
+}
+/* apply_polynomial gmres_poly.cpp:173-195: Horner, acc = c[deg] b, then
+ * deg times acc = A acc; acc[i] += c[k] b[i] */
+int orc_apply_polynomial(const void* ap, const double* coeffs, int64_t ncoeffs, int64_t deg, const double* b,
+                         double* y) {
+  API_BEGIN
+  const csr* a = (const csr*)ap;
+  if (ncoeffs < 1) EINV("apply_polynomial: empty polynomial");
+  if (deg < 0 || deg >= ncoeffs) EINV("apply_polynomial: effective_order out of range");
+  const int64_t n = a->n;
+  double* acc = (double*)xmalloc(sizeof(double) * (size_t)(n ? n : 1));
+  double* t = (double*)xmalloc(sizeof(double) * (size_t)(n ? n : 1));
+  for (int64_t i = 0; i < n; ++i) acc[i] = coeffs[deg] * b[i];
+  for (int64_t k = deg; k-- > 0;) {
+    spmv_into(a, acc, t);
+    const double alpha = coeffs[k];
+    for (int64_t i = 0; i < n; ++i) acc[i] = t[i] + alpha * b[i];
+  }
+  memcpy(y, acc, sizeof(double) * (size_t)n);
+  free(acc);
+  free(t);
+  API_END
+}
+int orc_f_smooth(const void* hp, int64_t l, const double* b, double* x) {
+  API_BEGIN
+  const hier_t* h = (const hier_t*)hp;
+  if (l < 0 || l >= h->nlev) EINV("f_smooth: level out of range");
+  counters c = {0, 0};
+  f_smooth(&h->lev[l], b, x, &c);
+  API_END
+}
+
 int orc_vcycle(const void* hp, const airg_solve_config* cfg, const double* b, double* x) {
   API_BEGIN
   const hier_t* h = (const hier_t*)hp;

@@ -64,6 +64,36 @@ int main() {
   report(same, "PMISR-DDC labels bit-identical");
   report(rep.n_converted == (int64_t)d.converted.size(), "DDC conversion count");
 
+  // the single operations of air.hpp / coarsening.hpp / gmres_poly.hpp
+  {
+    DominanceReport dr = dominance_report(s.a_ff, 1000);
+    airgraph_gpu::DominanceReport gd = airgraph_gpu::dominance_report(ctx, s.a_ff, 1000);
+    bool hist_ok = gd.histogram.size() == dr.histogram.size();
+    for (size_t k = 0; hist_ok && k < dr.histogram.size(); ++k) hist_ok = gd.histogram[k] == dr.histogram[k];
+    report(same_bits(dr.theta, gd.theta) && dr.max_theta == gd.max_theta && hist_ok,
+           "dominance_report bit-identical");
+    GmresPolynomial q = compute_coefficients(s.a_ff, 4, 5);
+    std::vector<double> bf(s.a_ff.ncols());
+    for (index_t i = 0; i < s.a_ff.ncols(); ++i) bf[i] = rng::uniform01(13, i);
+    report(same_bits(apply_polynomial(s.a_ff, q, bf),
+                     airgraph_gpu::apply_polynomial(ctx, s.a_ff, q.coefficients, q.effective_order, bf)),
+           "apply_polynomial bit-identical");
+    const SparseMatrix qa = assemble_fixed_sparsity(s.a_ff, q, 1);
+    std::vector<uint8_t> lab8(l.label.size());
+    for (size_t i = 0; i < lab8.size(); ++i) lab8[i] = static_cast<uint8_t>(l.label[i]);
+    LabelMap map = build_label_map(l.label);
+    const SparseMatrix r = build_restriction(s.a_cf, qa, 0.01, map);
+    report(r == airgraph_gpu::build_restriction(ctx, s.a_cf, qa, 0.01, lab8), "build_restriction ==");
+    const SparseMatrix pp = build_prolongation(l, map, g, af);
+    std::vector<Triplet> st;
+    for (index_t i = 0; i < g.n; ++i)
+      for (index_t j : g.s_row(i)) st.push_back({i, j, 1.0});
+    const SparseMatrix sp = SparseMatrix::from_triplets(g.n, g.n, st);
+    report(pp == airgraph_gpu::build_prolongation(ctx, af, sp, lab8), "build_prolongation ==");
+    report(coarse_matrix(r, af, pp, 0.001) == airgraph_gpu::coarse_matrix(ctx, r, af, pp, 0.001),
+           "coarse_matrix ==");
+  }
+
   // hierarchy with injected coefficients, then the Richardson solve
   SetupConfig cfg;
   cfg.poly_order = 3;

@@ -412,6 +412,89 @@ int ref_hier_labels(const void* hp, int64_t l, uint8_t* labels) {
   });
 }
 
+// ---- single operations (dominance_report, label map, transfer operators,
+// polynomial application, one F-smooth), each calling the reference itself
+int ref_dominance_report(const void* aff, int64_t bins, double* theta, int64_t* hist, double* max_theta) {
+  return guard([&] {
+    DominanceReport r = dominance_report(*static_cast<const SparseMatrix*>(aff), bins);
+    if (theta) std::memcpy(theta, r.theta.data(), sizeof(double) * r.theta.size());
+    if (hist)
+      for (size_t b = 0; b < r.histogram.size(); ++b) hist[b] = r.histogram[b];
+    if (max_theta) *max_theta = r.max_theta;
+  });
+}
+static std::vector<CfLabel> to_labels(const uint8_t* labels, int64_t n) {
+  std::vector<CfLabel> l((size_t)n);
+  for (int64_t i = 0; i < n; ++i) l[(size_t)i] = static_cast<CfLabel>(labels[i]);
+  return l;
+}
+int ref_build_label_map(const uint8_t* labels, int64_t n, int64_t* fine_to_sub, int64_t* f_to_fine,
+                        int64_t* c_to_fine, int64_t* n_f) {
+  return guard([&] {
+    const std::vector<CfLabel> l = to_labels(labels, n);
+    LabelMap m = build_label_map(l);
+    if (fine_to_sub) std::copy(m.fine_to_sub.begin(), m.fine_to_sub.end(), fine_to_sub);
+    if (f_to_fine) std::copy(m.f_to_fine.begin(), m.f_to_fine.end(), f_to_fine);
+    if (c_to_fine) std::copy(m.c_to_fine.begin(), m.c_to_fine.end(), c_to_fine);
+    if (n_f) *n_f = m.n_f();
+  });
+}
+int ref_build_restriction(const void* acf, const void* ffinv, double drop, const uint8_t* labels, int64_t n,
+                          void** out) {
+  return guard([&] {
+    const std::vector<CfLabel> l = to_labels(labels, n);
+    LabelMap m = build_label_map(l);
+    *out = new SparseMatrix(build_restriction(*static_cast<const SparseMatrix*>(acf),
+                                              *static_cast<const SparseMatrix*>(ffinv), drop, m));
+  });
+}
+int ref_build_prolongation(const void* a, const void* s_pattern, const uint8_t* labels, void** out) {
+  return guard([&] {
+    auto* am = static_cast<const SparseMatrix*>(a);
+    auto* s = static_cast<const SparseMatrix*>(s_pattern);
+    std::vector<std::vector<index_t>> rows(s->nrows());
+    for (index_t i = 0; i < s->nrows(); ++i) {
+      auto c = s->row_cols(i);
+      rows[i].assign(c.begin(), c.end());
+    }
+    StrengthGraph g = StrengthGraph::from_pattern(s->nrows(), rows);
+    CfLabels cl;
+    cl.label = to_labels(labels, am->nrows());
+    cl.weight.assign(am->nrows(), 0.5);
+    LabelMap m = build_label_map(cl.label);
+    *out = new SparseMatrix(build_prolongation(cl, m, g, *am));
+  });
+}
+int ref_coarse_matrix(const void* r, const void* a, const void* p, double drop, void** out) {
+  return guard([&] {
+    *out = new SparseMatrix(coarse_matrix(*static_cast<const SparseMatrix*>(r),
+                                          *static_cast<const SparseMatrix*>(a),
+                                          *static_cast<const SparseMatrix*>(p), drop));
+  });
+}
+int ref_apply_polynomial(const void* a, const double* coeffs, int64_t ncoeffs, int64_t deg, const double* b,
+                         double* y) {
+  return guard([&] {
+    auto* m = static_cast<const SparseMatrix*>(a);
+    GmresPolynomial p;
+    p.order = ncoeffs - 1;
+    p.coefficients.assign(coeffs, coeffs + ncoeffs);
+    p.effective_order = deg;
+    auto r = apply_polynomial(*m, p, std::span<const double>(b, (size_t)m->ncols()));
+    std::memcpy(y, r.data(), sizeof(double) * r.size());
+  });
+}
+int ref_f_smooth(const void* hp, int64_t l, const double* b, double* x) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    const Level& lv = h.levels.at(l);
+    const index_t n = lv.a.nrows();
+    std::vector<double> xv(x, x + n);
+    f_smooth(lv, std::span<const double>(b, (size_t)n), xv);
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+  });
+}
+
 // ---- L3: solve -------------------------------------------------------------------
 int ref_vcycle(const void* hp, const airg_solve_config* cfg, const double* b,
                double* x) {

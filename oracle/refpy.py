@@ -88,6 +88,13 @@ class _Lib:
             ("hier_labels", [C.c_void_p, C.c_int64, u8p]),
             ("vcycle", [C.c_void_p, C.POINTER(abi.SolveConfig), f64p, f64p]),
             ("solve", [C.c_void_p, C.POINTER(abi.SolveConfig), f64p, f64p, C.POINTER(abi.SolveStats), f64p, C.c_int64]),
+            ("dominance_report", [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
+            ("build_label_map", [u8p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+            ("build_restriction", [C.c_void_p, C.c_void_p, C.c_double, u8p, C.c_int64, C.POINTER(C.c_void_p)]),
+            ("build_prolongation", [C.c_void_p, C.c_void_p, u8p, C.POINTER(C.c_void_p)]),
+            ("coarse_matrix", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(C.c_void_p)]),
+            ("apply_polynomial", [C.c_void_p, f64p, C.c_int64, C.c_int64, f64p, f64p]),
+            ("f_smooth", [C.c_void_p, C.c_int64, f64p, f64p]),
         ]:
             fn = getattr(L, p + name, None)
             if fn is None:
@@ -354,6 +361,12 @@ class Hier:
         self.lib.call("hier_labels", self.h, l, out)
         return out
 
+    def f_smooth(self, level, b, x):
+        """One F-smooth on `level` (solve.cpp:63-87) -> the smoothed x."""
+        xx = np.ascontiguousarray(x, np.float64).copy()
+        self.lib.call("f_smooth", self.h, int(level), np.ascontiguousarray(b, np.float64), xx)
+        return xx
+
     def vcycle(self, b, scfg=None):
         scfg = scfg or abi.solve_config()
         x = np.zeros_like(b)
@@ -375,3 +388,33 @@ def setup(lib, A: Mat, **params) -> Hier:
     out = C.c_void_p()
     lib.call("setup", A.h, C.byref(cfg), C.byref(out))
     return Hier(lib, out)
+
+
+# ---- single reference operations (both libraries, same shapes) -------------
+def dominance_report(lib, A: Mat, bins: int):
+    n = A.dims()[0]
+    theta = np.zeros(max(n, 1))
+    hist = np.zeros(bins, np.int64)
+    mx = C.c_double()
+    lib.call("dominance_report", A.h, int(bins), theta.ctypes.data, hist.ctypes.data, C.byref(mx))
+    return theta[:n], hist, mx.value
+
+
+def build_label_map(lib, labels):
+    lab = np.ascontiguousarray(labels, np.uint8)
+    n = len(lab)
+    nf = int(np.count_nonzero(lab == 0))
+    f2s = np.zeros(max(n, 1), np.int64)
+    f2f = np.zeros(max(nf, 1), np.int64)
+    c2f = np.zeros(max(n - nf, 1), np.int64)
+    out_nf = C.c_int64()
+    lib.call("build_label_map", lab, n, f2s.ctypes.data, f2f.ctypes.data, c2f.ctypes.data, C.byref(out_nf))
+    return f2s[:n], f2f[:nf], c2f[: n - nf]
+
+
+def apply_polynomial(lib, A: Mat, coeffs, eff: int, b):
+    c = np.ascontiguousarray(coeffs, np.float64)
+    bb = np.ascontiguousarray(b, np.float64)
+    y = np.zeros(max(A.dims()[0], 1))
+    lib.call("apply_polynomial", A.h, c, len(c), int(eff), bb, y)
+    return y[: A.dims()[0]]

@@ -96,6 +96,13 @@ def lib() -> C.CDLL:
             "airg_hier_labels": ([_VP, _VP, C.c_int64, _VP], C.c_int),
             "airg_hier_destroy": ([_VP], C.c_int),
             "airg_vcycle": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP], C.c_int),
+            "airg_f_smooth": ([_VP, _VP, C.c_int64, _VP, _VP], C.c_int),
+            "airg_dominance_report": ([_VP, _VP, C.c_int64, _VP, _VP, _P(C.c_double)], C.c_int),
+            "airg_build_label_map": ([_VP, _VP, C.c_int64, _VP, _VP, _VP, _P(C.c_int64)], C.c_int),
+            "airg_build_restriction": ([_VP, _VP, _VP, C.c_double, _VP, C.c_int64, _P(_VP)], C.c_int),
+            "airg_build_prolongation": ([_VP, _VP, _VP, _VP, _P(_VP)], C.c_int),
+            "airg_coarse_matrix": ([_VP, _VP, _VP, _VP, C.c_double, _P(_VP)], C.c_int),
+            "airg_apply_polynomial": ([_VP, _VP, _VP, C.c_int64, C.c_int64, _VP, _VP], C.c_int),
             "airg_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                             C.c_int64], C.c_int),
             "airg_solve_host": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
@@ -505,7 +512,79 @@ def ddc(a, labels, fraction=0.1, bins=1000, selection=0, direct_alpha_diag=0.0,
     return ctx.to_host(tl), rep
 
 
+def dominance_report(a_ff, bins: int = 1000, ctx: Context | None = None):
+    """coarsening.cpp:219-250 -> (theta, histogram (int64), max_theta)."""
+    ctx = ctx or default_context()
+    d = _dev(a_ff, ctx)
+    n = d.dims()[0]
+    tt = ctx.empty(max(n, 1), ctx.torch.float64)
+    hist = np.zeros(max(int(bins), 1), np.int64)
+    mx = C.c_double()
+    _check(lib().airg_dominance_report(ctx.h, d.h, int(bins), _ptr(tt), hist.ctypes.data, C.byref(mx)))
+    return ctx.to_host(tt)[:n], hist[: max(int(bins), 0)], mx.value
+
+
+def build_label_map(labels, ctx: Context | None = None):
+    """sparse.cpp:270-290 -> (fine_to_sub, f_to_fine, c_to_fine), int64."""
+    ctx = ctx or default_context()
+    lab = np.ascontiguousarray(labels, np.uint8)
+    n = len(lab)
+    tl = ctx.to_device(lab)
+    nf = int(np.count_nonzero(lab == 0))
+    f2s = np.zeros(max(n, 1), np.int64)
+    f2f = np.zeros(max(nf, 1), np.int64)
+    c2f = np.zeros(max(n - nf, 1), np.int64)
+    out_nf = C.c_int64()
+    _check(lib().airg_build_label_map(ctx.h, _ptr(tl), n, f2s.ctypes.data, f2f.ctypes.data, c2f.ctypes.data,
+                                      C.byref(out_nf)))
+    return f2s[:n], f2f[:nf], c2f[: n - nf]
+
+
+def build_restriction(a_cf, aff_inv, drop_restrict: float, labels, ctx: Context | None = None) -> SparseMatrix:
+    """air.cpp:154-189: R = [-drop(A_cf Aff_inv) | I] in fine columns."""
+    ctx = ctx or default_context()
+    dcf, dinv = _dev(a_cf, ctx), _dev(aff_inv, ctx)
+    lab = np.ascontiguousarray(labels, np.uint8)
+    tl = ctx.to_device(lab)
+    out = _VP()
+    _check(lib().airg_build_restriction(ctx.h, dcf.h, dinv.h, float(drop_restrict), _ptr(tl), len(lab),
+                                        C.byref(out)))
+    return DeviceCSR(ctx, out).download()
+
+
+def build_prolongation(a, s_pattern, labels, ctx: Context | None = None) -> SparseMatrix:
+    """air.cpp:191-238: one-point P from the strength pattern (strength(a, alpha))."""
+    ctx = ctx or default_context()
+    da, ds = _dev(a, ctx), _dev(s_pattern, ctx)
+    tl = ctx.to_device(np.ascontiguousarray(labels, np.uint8))
+    out = _VP()
+    _check(lib().airg_build_prolongation(ctx.h, da.h, ds.h, _ptr(tl), C.byref(out)))
+    return DeviceCSR(ctx, out).download()
+
+
+def coarse_matrix(r, a, p, drop_coarse: float, ctx: Context | None = None) -> SparseMatrix:
+    """air.cpp:268-271: drop_entries(R (A P), drop_coarse)."""
+    ctx = ctx or default_context()
+    dr, da, dp = _dev(r, ctx), _dev(a, ctx), _dev(p, ctx)
+    out = _VP()
+    _check(lib().airg_coarse_matrix(ctx.h, dr.h, da.h, dp.h, float(drop_coarse), C.byref(out)))
+    return DeviceCSR(ctx, out).download()
+
+
 # ---- L1b (gmres_poly.hpp) -----------------------------------------------------------
+def apply_polynomial(a, coeffs, effective_order: int, b, ctx: Context | None = None) -> np.ndarray:
+    """gmres_poly.cpp:173-195: q(A) b by Horner (effective_order matvecs)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    c = np.ascontiguousarray(coeffs, np.float64)
+    n = d.dims()[0]
+    tb = ctx.to_device(np.asarray(b, np.float64))
+    ty = ctx.empty(max(n, 1), ctx.torch.float64)
+    _check(lib().airg_apply_polynomial(ctx.h, d.h, c.ctypes.data, len(c), int(effective_order), _ptr(tb),
+                                       _ptr(ty)))
+    return ctx.to_host(ty)[:n]
+
+
 def compute_coefficients(a, m: int, seed: int, ctx: Context | None = None):
     """gmres_poly.cpp:63-171 (double-double on the GPU) -> (coeffs, effective_order)."""
     ctx = ctx or default_context()
@@ -586,6 +665,13 @@ class Hierarchy:
         out = np.zeros(n, np.uint8)
         _check(lib().airg_hier_labels(self.ctx.h, self.h, int(l), out.ctypes.data))
         return out
+
+    def f_smooth(self, level: int, b, x) -> np.ndarray:
+        """f_smooth(level, b, x) (solve.cpp:63-87) -> the smoothed x."""
+        tb = self.ctx.to_device(np.asarray(b, np.float64))
+        tx = self.ctx.to_device(np.asarray(x, np.float64))
+        _check(lib().airg_f_smooth(self.ctx.h, self.h, int(level), _ptr(tb), _ptr(tx)))
+        return self.ctx.to_host(tx)
 
     def vcycle(self, b, **solve_kw) -> np.ndarray:
         """vcycle(h, b, x = 0) (solve.cpp:150-165)."""

@@ -137,6 +137,92 @@ std::vector<uint8_t> cf_split(Context& ctx, const SM& a, double alpha, int64_t m
   return labels;
 }
 
+// device scratch through the C-ABI (no CUDA runtime needed on this side)
+class DeviceBuffer {
+ public:
+  DeviceBuffer(Context& ctx, size_t bytes) : ctx_(&ctx) { check(airg_device_alloc(ctx.get(), bytes, &p_)); }
+  ~DeviceBuffer() {
+    if (p_) airg_device_free(ctx_->get(), p_);
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  template <class T>
+  T* as() const { return static_cast<T*>(p_); }
+  void upload(const void* h, size_t bytes) { check(airg_memcpy(ctx_->get(), p_, h, bytes, 1)); }
+  void download(void* h, size_t bytes) const { check(airg_memcpy(ctx_->get(), h, p_, bytes, 0)); }
+
+ private:
+  Context* ctx_;
+  void* p_ = nullptr;
+};
+
+// dominance_report (coarsening.hpp:106): theta per A_ff row, histogram, max
+struct DominanceReport {
+  std::vector<double> theta;
+  double max_theta = 0.0;
+  std::vector<int64_t> histogram;
+};
+template <class SM>
+DominanceReport dominance_report(Context& ctx, const SM& a_ff, int64_t bins = 1000) {
+  Matrix d = upload(ctx, a_ff);
+  DominanceReport r;
+  r.theta.resize(a_ff.nrows());
+  r.histogram.assign(bins > 0 ? bins : 0, 0);
+  DeviceBuffer dt(ctx, sizeof(double) * r.theta.size());
+  check(airg_dominance_report(ctx.get(), d.get(), bins, dt.as<double>(), r.histogram.data(), &r.max_theta));
+  dt.download(r.theta.data(), sizeof(double) * r.theta.size());
+  return r;
+}
+
+// apply_polynomial (gmres_poly.hpp:40-43): q(A) b, coefficients[0..eff]
+template <class SM>
+std::vector<double> apply_polynomial(Context& ctx, const SM& a, std::span<const double> coeffs, int64_t eff,
+                                     std::span<const double> b) {
+  if ((int64_t)b.size() != a.ncols()) throw std::invalid_argument("apply_polynomial: dimension mismatch");
+  Matrix d = upload(ctx, a);
+  const size_t n = a.nrows();
+  DeviceBuffer db(ctx, sizeof(double) * b.size()), dy(ctx, sizeof(double) * n);
+  db.upload(b.data(), sizeof(double) * b.size());
+  check(airg_apply_polynomial(ctx.get(), d.get(), coeffs.data(), (int64_t)coeffs.size(), eff, db.as<double>(),
+                              dy.as<double>()));
+  std::vector<double> y(n);
+  dy.download(y.data(), sizeof(double) * n);
+  return y;
+}
+
+// build_restriction (air.hpp:96-98); labels as airgraph::CfLabel values (F = 0, C = 1)
+template <class SM>
+SM build_restriction(Context& ctx, const SM& a_cf, const SM& aff_inv, double drop_restrict,
+                     const std::vector<uint8_t>& labels) {
+  Matrix dcf = upload(ctx, a_cf), dinv = upload(ctx, aff_inv);
+  DeviceBuffer dl(ctx, labels.size());
+  dl.upload(labels.data(), labels.size());
+  airg_csr* out = nullptr;
+  check(airg_build_restriction(ctx.get(), dcf.get(), dinv.get(), drop_restrict, dl.as<uint8_t>(),
+                               (int64_t)labels.size(), &out));
+  return download<SM>(ctx, Matrix(out));
+}
+
+// build_prolongation (air.hpp:104-105) with g given as the strength pattern S
+template <class SM>
+SM build_prolongation(Context& ctx, const SM& a, const SM& s_pattern, const std::vector<uint8_t>& labels) {
+  Matrix da = upload(ctx, a), ds = upload(ctx, s_pattern);
+  DeviceBuffer dl(ctx, labels.size());
+  dl.upload(labels.data(), labels.size());
+  airg_csr* out = nullptr;
+  check(airg_build_prolongation(ctx.get(), da.get(), ds.get(), dl.as<uint8_t>(), &out));
+  return download<SM>(ctx, Matrix(out));
+}
+
+// coarse_matrix (air.hpp:113-114): drop_entries(R (A P), drop_coarse)
+template <class SM>
+SM coarse_matrix(Context& ctx, const SM& r, const SM& a, const SM& p, double drop_coarse) {
+  Matrix dr = upload(ctx, r), da = upload(ctx, a), dp = upload(ctx, p);
+  airg_csr* out = nullptr;
+  check(airg_coarse_matrix(ctx.get(), dr.get(), da.get(), dp.get(), drop_coarse, &out));
+  return download<SM>(ctx, Matrix(out));
+}
+
 // airgraph::setup (air.hpp:126) -> a device-resident hierarchy
 class Hierarchy {
  public:

@@ -220,6 +220,35 @@ int airg_spmv(airg_ctx* ctx, const airg_csr* a, const double* x, double* y) {
   });
 }
 
+// ---- device buffers for hosts without the CUDA runtime (C / C++ / FFI) -----------
+int airg_device_alloc(airg_ctx* ctx, size_t bytes, void** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "output pointer");
+    bind(ctx->c);
+    *out = nullptr;
+    CUDA_CHECK(cudaMallocAsync(out, bytes ? bytes : 16, ctx->c.stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+int airg_device_free(airg_ctx* ctx, void* p) {
+  return guard([&] {
+    need(ctx, "context");
+    bind(ctx->c);
+    if (p) CUDA_CHECK(cudaFreeAsync(p, ctx->c.stream));
+  });
+}
+int airg_memcpy(airg_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t to_device) {
+  return guard([&] {
+    need(ctx, "context");
+    bind(ctx->c);
+    if (!bytes) return;
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                               ctx->c.stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
 int airg_spmv_host(airg_ctx* ctx, const airg_csr* a, const double* hx, double* hy) {
   return guard([&] {
     need(ctx, "context");
@@ -488,7 +517,110 @@ int airg_extract_blocks(airg_ctx* ctx, const airg_csr* a, const uint8_t* labels,
   });
 }
 
+// dominance_report (coarsening.cpp:219-250) of an A_ff block
+int airg_dominance_report(airg_ctx* ctx, const airg_csr* a_ff, int64_t bins, double* d_theta,
+                          int64_t* h_hist, double* max_theta) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a_ff, "matrix");
+    bind(ctx->c);
+    const double mx = dominance_report(ctx->c, a_ff->m, bins, d_theta, h_hist);
+    if (max_theta) *max_theta = mx;
+  });
+}
+
+// build_label_map (sparse.cpp:270-290): F-then-C sub-indexing, host outputs
+int airg_build_label_map(airg_ctx* ctx, const uint8_t* d_labels, int64_t n, int64_t* h_fine_to_sub,
+                         int64_t* h_f_to_fine, int64_t* h_c_to_fine, int64_t* n_f) {
+  return guard([&] {
+    need(ctx, "context");
+    bind(ctx->c);
+    if (n < 0 || n > INT32_MAX) throw InvalidArgument("build_label_map: length out of range");
+    LabelMap map;
+    build_label_map(ctx->c, d_labels, (int32_t)n, map);
+    auto out = [&](const DBuf<int32_t>& d, int64_t len, int64_t* h) {
+      if (!h || len == 0) return;
+      std::vector<int32_t> t((size_t)len);
+      to_host(ctx->c, t.data(), d.p, t.size());
+      for (int64_t k = 0; k < len; ++k) h[k] = t[(size_t)k];
+    };
+    out(map.fine_to_sub, n, h_fine_to_sub);
+    out(map.f_to_fine, map.nf, h_f_to_fine);
+    out(map.c_to_fine, map.nc, h_c_to_fine);
+    if (n_f) *n_f = map.nf;
+  });
+}
+
+// ---- transfer operators (air.hpp:96-116) ------------------------------------------
+int airg_build_restriction(airg_ctx* ctx, const airg_csr* a_cf, const airg_csr* aff_inv, double drop_restrict,
+                           const uint8_t* d_labels, int64_t n, airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a_cf, "matrix");
+    need(aff_inv, "matrix");
+    need(out, "output handle");
+    bind(ctx->c);
+    LabelMap map;
+    build_label_map(ctx->c, d_labels, (int32_t)n, map);
+    if (a_cf->m.n != map.nc || a_cf->m.m != map.nf || aff_inv->m.n != map.nf || aff_inv->m.m != map.nf)
+      throw InvalidArgument("build_restriction: block shapes do not match the label map");
+    Csr r;
+    build_restriction(ctx->c, a_cf->m, aff_inv->m, drop_restrict, map, r);
+    *out = wrap(ctx->c, std::move(r));
+  });
+}
+
+// one-point prolongation from the strength pattern S (airg_strength) and A
+int airg_build_prolongation(airg_ctx* ctx, const airg_csr* a, const airg_csr* s, const uint8_t* d_labels,
+                            airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(s, "strength pattern");
+    need(out, "output handle");
+    bind(ctx->c);
+    if (s->m.n != a->m.n || a->m.n != a->m.m) throw InvalidArgument("build_prolongation: shape mismatch");
+    LabelMap map;
+    build_label_map(ctx->c, d_labels, a->m.n, map);
+    Strength g;
+    strength_from_pattern(ctx->c, s->m, g);
+    DBuf<int32_t> pmap;
+    Csr p;
+    build_prolongation(ctx->c, map, g, a->m, pmap, p);
+    *out = wrap(ctx->c, std::move(p));
+  });
+}
+
+// coarse_matrix (air.cpp:268-271): drop_entries(R (A P), drop_coarse)
+int airg_coarse_matrix(airg_ctx* ctx, const airg_csr* r, const airg_csr* a, const airg_csr* p, double drop_coarse,
+                       airg_csr** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(r, "matrix");
+    need(a, "matrix");
+    need(p, "matrix");
+    need(out, "output handle");
+    bind(ctx->c);
+    Csr ap, rap, res;
+    spgemm(ctx->c, a->m, p->m, ap);
+    spgemm(ctx->c, r->m, ap, rap);
+    drop_entries(ctx->c, rap, drop_coarse, true, res);
+    *out = wrap(ctx->c, std::move(res));
+  });
+}
+
 // ---- polynomials ----------------------------------------------------------------
+// apply_polynomial (gmres_poly.cpp:173-195): d_y = q(A) d_b, Horner
+int airg_apply_polynomial(airg_ctx* ctx, const airg_csr* a, const double* coeffs, int64_t ncoeffs,
+                          int64_t effective_order, const double* d_b, double* d_y) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(coeffs, "coefficients");
+    bind(ctx->c);
+    apply_polynomial(ctx->c, const_cast<airg_csr*>(a)->m, coeffs, ncoeffs, effective_order, d_b, d_y);  // row-layout cache only
+  });
+}
 int airg_poly_coefficients(airg_ctx* ctx, const airg_csr* a, int64_t m, uint64_t seed,
                            double* coeffs, int64_t* eff) {
   return guard([&] {
@@ -672,6 +804,15 @@ int airg_hier_destroy(airg_hier* h) {
 }
 
 // ---- solve --------------------------------------------------------------------------
+int airg_f_smooth(airg_ctx* ctx, const airg_hier* hp, int64_t level, const double* d_b, double* d_x) {
+  return guard([&] {
+    need(ctx, "context");
+    need(hp, "hierarchy");
+    bind(ctx->c);
+    f_smooth_level(ctx->c, const_cast<airg_hier*>(hp)->h, level, d_b, d_x);
+  });
+}
+
 int airg_vcycle(airg_ctx* ctx, const airg_hier* hp, const airg_solve_config* cfg, const double* b,
                 double* x) {
   return guard([&] {

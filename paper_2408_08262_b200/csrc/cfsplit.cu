@@ -670,6 +670,35 @@ DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, do
   return r;
 }
 
+// dominance_report (coarsening.cpp:219-250): theta per F row, max, and the
+// bins-bin histogram over [0, max] (width max/bins, 1 when max == 0)
+double dominance_report(Ctx& c, const Csr& aff, int64_t bins, double* d_theta, int64_t* h_hist) {
+  if (bins < 1) throw InvalidArgument("dominance_report: bins >= 1");
+  ThetaScratch s;
+  theta_pass(c, aff, s);
+  const int nf = aff.n;
+  DBuf<unsigned long long> hist(c, (size_t)bins);
+  hist.zero(c);
+  if (nf) {
+    const int blocks = (int)std::min<int64_t>(blocks_for(nf, 256), 4 * c.num_sms);
+    const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
+    LAUNCH(c, theta_hist, blocks, 256, smem, nf, s.theta.p, s.u.p, bins, hist.p);
+    if (d_theta)
+      CUDA_CHECK(cudaMemcpyAsync(d_theta, s.theta.p, sizeof(double) * nf, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  unsigned long long u[3];
+  to_host(c, u, s.u.p, 3);
+  if (u[1] != ~0ull) throw_zero_diag(u[1]);
+  if (h_hist) {
+    std::vector<unsigned long long> hh((size_t)bins);
+    to_host(c, hh.data(), hist.p, hh.size());
+    for (int64_t b = 0; b < bins; ++b) h_hist[b] = (int64_t)hh[(size_t)b];
+  }
+  double mx;
+  memcpy(&mx, &u[0], sizeof mx);
+  return mx;
+}
+
 double dominance_max(Ctx& c, const Csr& aff, int rb) {
   ThetaScratch s;
   theta_pass(c, aff, s, rb);

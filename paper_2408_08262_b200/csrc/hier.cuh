@@ -80,6 +80,9 @@ void recompute_metrics(Hier& h);
 
 // solve.cu
 void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x);
+void f_smooth_level(Ctx& c, Hier& h, int64_t l, const double* d_b, double* d_x);
+void apply_polynomial(Ctx& c, Csr& a, const double* coeffs, int64_t ncoeffs, int64_t deg, const double* d_b,
+                      double* d_y);
 void solve(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x,
            airg_solve_stats& st, std::vector<double>& history);
 

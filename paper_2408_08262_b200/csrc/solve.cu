@@ -708,6 +708,53 @@ using Clock = std::chrono::steady_clock;
 
 }  // namespace
 
+// ---- single operations of the reference's solve / polynomial API ----------
+namespace {
+// Horner step (gmres_poly.cpp:188-193): acc = A acc, then acc += alpha * b
+struct EpiHorner {
+  const double* b;
+  double alpha;
+  double* y;
+  __device__ void row(int i, double acc) const { y[i] = __dadd_rn(acc, __dmul_rn(alpha, b[i])); }
+  __device__ void finish() const {}
+};
+__global__ void k_scale(int n, double a, const double* __restrict__ b, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __dmul_rn(a, b[i]);
+}
+}  // namespace
+
+// apply_polynomial (gmres_poly.cpp:173-195): q(A) b by Horner with
+// effective_order matvecs, each product and sum rounded separately
+void apply_polynomial(Ctx& c, Csr& a, const double* coeffs, int64_t ncoeffs, int64_t deg, const double* d_b,
+                      double* d_y) {
+  if (ncoeffs < 1) throw InvalidArgument("apply_polynomial: empty polynomial");
+  if (deg < 0 || deg >= ncoeffs) throw InvalidArgument("apply_polynomial: effective_order out of range");
+  if (deg > 0 && a.n != a.m) throw InvalidArgument("apply_polynomial: dimension mismatch");
+  const int n = a.n;
+  if (n == 0) return;
+  build_tiles(c, a);
+  DBuf<double> t(c, deg > 0 ? (size_t)n : 1);
+  // ping-pong so that the last step lands in d_y
+  double* cur = (deg % 2 == 0) ? d_y : t.p;
+  double* nxt = (deg % 2 == 0) ? t.p : d_y;
+  LAUNCH(c, k_scale, blocks_for(n, 256), 256, 0, n, coeffs[deg], d_b, cur);
+  for (int64_t k = deg; k-- > 0;) {
+    LAUNCH_ROWS(c, EpiHorner, tv(a), cur, (EpiHorner{d_b, coeffs[k], nxt}));
+    std::swap(cur, nxt);
+  }
+}
+
+// f_smooth (solve.cpp:63-87) on level l of a built hierarchy: x_F += Aff^-1
+// ((b_F - A_FF x_F) - A_FC x_C), x of the level's size, C entries untouched
+void f_smooth_level(Ctx& c, Hier& h, int64_t l, const double* d_b, double* d_x) {
+  if (l < 0 || l >= (int64_t)h.levels.size()) throw InvalidArgument("f_smooth: level out of range");
+  Level& lv = h.levels[(size_t)l];
+  if (lv.map.nf == 0) return;
+  ROWS_FC(EpiFres1, lv.af, d_x, (EpiFres1{d_b, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p}));
+  ROWS(EpiFupd, lv.ffinv, lv.rf.p, (EpiFupd{lv.map.f_to_fine.p, d_x}));
+}
+
 void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x) {
   check_cfg(cfg);
   const int n = h.top_n();

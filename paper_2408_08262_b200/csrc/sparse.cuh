@@ -103,7 +103,8 @@ CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_ena
 void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,
                        double fraction, const unsigned long long* d_maxbits, double* d_out);
 // max theta only (theta_post, air.cpp:355); throws on a zero diagonal
-double dominance_max(Ctx& c, const Csr& aff, int rb = 0);  // rb: F rows of a slab
+double dominance_max(Ctx& c, const Csr& aff, int rb = 0);
+double dominance_report(Ctx& c, const Csr& aff, int64_t bins, double* d_theta, int64_t* h_hist);  // rb: F rows of a slab
 
 // poly.cu ---------------------------------------------------------------------
 struct PolyFit {

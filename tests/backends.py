@@ -156,6 +156,29 @@ class PortBackend:
     def setup(self, a, **prm):
         return refpy.setup(self.lib, self._m(a), **prm)
 
+    # single operations (air.hpp:96-116, coarsening.hpp:106, gmres_poly.hpp:40-43, sparse.hpp:133)
+    def dominance_report(self, a_ff, bins):
+        return refpy.dominance_report(self.lib, self._m(a_ff), bins)
+
+    def label_map(self, labels):
+        return refpy.build_label_map(self.lib, labels)
+
+    def restriction(self, a_cf, aff_inv, drop, labels):
+        A, B = self._m(a_cf), self._m(aff_inv)
+        return self._t(refpy.binop(self.lib, "build_restriction", A.h, B.h, float(drop),
+                                   np.ascontiguousarray(labels, np.uint8), len(labels)))
+
+    def prolongation(self, a, s_pattern, labels):
+        A, S = self._m(a), self._m(s_pattern)
+        return self._t(refpy.binop(self.lib, "build_prolongation", A.h, S.h, np.ascontiguousarray(labels, np.uint8)))
+
+    def coarse_matrix(self, r, a, p, drop):
+        R, A, P = self._m(r), self._m(a), self._m(p)
+        return self._t(refpy.binop(self.lib, "coarse_matrix", R.h, A.h, P.h, float(drop)))
+
+    def apply_polynomial(self, a, coeffs, eff, b):
+        return refpy.apply_polynomial(self.lib, self._m(a), coeffs, eff, b)
+
 
 class GpuBackend:
     name = "gpu"
@@ -215,6 +238,24 @@ class GpuBackend:
 
     def setup(self, a, **prm):
         return self.airg.setup(self._s(a), **prm)
+
+    def dominance_report(self, a_ff, bins):
+        return self.airg.dominance_report(self._s(a_ff), bins)
+
+    def label_map(self, labels):
+        return self.airg.build_label_map(labels)
+
+    def restriction(self, a_cf, aff_inv, drop, labels):
+        return self._t(self.airg.build_restriction(self._s(a_cf), self._s(aff_inv), drop, labels))
+
+    def prolongation(self, a, s_pattern, labels):
+        return self._t(self.airg.build_prolongation(self._s(a), self._s(s_pattern), labels))
+
+    def coarse_matrix(self, r, a, p, drop):
+        return self._t(self.airg.coarse_matrix(self._s(r), self._s(a), self._s(p), drop))
+
+    def apply_polynomial(self, a, coeffs, eff, b):
+        return self.airg.apply_polynomial(self._s(a), coeffs, eff, b)
 
 
 def same_bits(x, y) -> bool:

@@ -14,6 +14,7 @@ import pytest
 
 import refpy
 from backends import random_sparse, same_bits
+from paper_2408_08262_b200 import abi
 
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
 
@@ -144,3 +145,60 @@ def test_port_setup_matches_reference_c2_small(port, reflib):
     s1 = h1.solve(p.b, refpy.abi.solve_config())
     s2 = h2.solve(p.b, refpy.abi.solve_config())
     assert same_bits(s1[0], s2[0]) and same_bits(s1[2], s2[2])
+
+
+def _same_mat(x, y):
+    (a, b, c), (d, e, f) = x.arrays(), y.arrays()
+    return x.dims() == y.dims() and np.array_equal(a, d) and np.array_equal(b, e) and same_bits(c, f)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_port_single_ops_match_reference(port, reflib, seed):
+    """dominance_report, build_label_map, build_restriction /
+    build_prolongation / coarse_matrix, apply_polynomial and f_smooth of the
+    C restatement against the reference build, bit for bit."""
+    import ctypes as C
+    a = random_sparse(80, 0.08, 300 + seed)
+    A, R = port.mat(*a), reflib.mat(*a)
+    lab = np.zeros(80, np.uint8)
+    rep = abi.CfReport()
+    port.call("cf_split", A.h, 0.5, 3, seed, 0, 1, 0.1, 1000, lab, None, C.byref(rep))
+    lm_p, lm_r = refpy.build_label_map(port, lab), refpy.build_label_map(reflib, lab)
+    assert all(np.array_equal(u, v) for u, v in zip(lm_p, lm_r))
+    blocks = []
+    for lib, M in ((port, A), (reflib, R)):
+        o = [C.c_void_p(), C.c_void_p(), C.c_void_p()]
+        lib.call("extract_blocks", M.h, lab, *[C.byref(x) for x in o])
+        blocks.append([refpy.Mat(lib, x, True) for x in o])
+    (pff, pfc, pcf), (rff, rfc, rcf) = blocks
+    for bins in (1, 9, 1000):
+        x, y = refpy.dominance_report(port, pff, bins), refpy.dominance_report(reflib, rff, bins)
+        assert same_bits(x[0], y[0]) and np.array_equal(x[1], y[1]) and x[2] == y[2]
+    co = np.zeros(4)
+    eff = C.c_int64()
+    reflib.call("poly_coefficients", rff.h, 4, seed, co, C.byref(eff))
+    qp = refpy.binop(port, "poly_assemble", pff.h, co, 4, eff.value, 1)
+    qr = refpy.binop(reflib, "poly_assemble", rff.h, co, 4, eff.value, 1)
+    rp_ = refpy.binop(port, "build_restriction", pcf.h, qp.h, 0.01, lab, 80)
+    rr_ = refpy.binop(reflib, "build_restriction", rcf.h, qr.h, 0.01, lab, 80)
+    assert _same_mat(rp_, rr_)
+    sp, sr = C.c_void_p(), C.c_void_p()
+    port.call("strength", A.h, 0.5, C.byref(sp), None)
+    reflib.call("strength", R.h, 0.5, C.byref(sr), None)
+    SP, SR = refpy.Mat(port, sp, True), refpy.Mat(reflib, sr, True)
+    pp = refpy.binop(port, "build_prolongation", A.h, SP.h, lab)
+    pr = refpy.binop(reflib, "build_prolongation", R.h, SR.h, lab)
+    assert _same_mat(pp, pr)
+    cp = refpy.binop(port, "coarse_matrix", rp_.h, A.h, pp.h, 0.001)
+    cr = refpy.binop(reflib, "coarse_matrix", rr_.h, R.h, pr.h, 0.001)
+    assert _same_mat(cp, cr)
+    b = np.random.default_rng(seed).random(80)
+    assert same_bits(refpy.apply_polynomial(port, A, co, eff.value, b),
+                     refpy.apply_polynomial(reflib, R, co, eff.value, b))
+    from paper_2408_08262_b200 import problems
+    pb = problems.c2_structured_3d(10)
+    prm = dict(problems.setup_params(2), coarse_size_target=150)
+    hp = refpy.setup(port, port.mat_from_problem(pb), **prm)
+    hr = refpy.setup(reflib, reflib.mat_from_problem(pb), **prm)
+    x0 = np.random.default_rng(seed + 7).random(pb.n)
+    assert same_bits(hp.f_smooth(0, pb.b, x0), hr.f_smooth(0, pb.b, x0))
