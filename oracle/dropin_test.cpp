@@ -35,6 +35,7 @@ static bool same_bits(const std::vector<double>& a, const std::vector<double>& b
 }
 
 int main() {
+  std::setvbuf(stdout, nullptr, _IONBF, 0);  // progress survives a crash
   airgraph_gpu::Context ctx(0);
   // the reference's own desk operator (transport.cpp), 4 SUPG angle blocks
   StreamingProblem p = assemble_streaming(generate_mesh(20, 3, 0.25));
@@ -64,8 +65,10 @@ int main() {
   report(same, "PMISR-DDC labels bit-identical");
   report(rep.n_converted == (int64_t)d.converted.size(), "DDC conversion count");
 
-  // the single operations of air.hpp / coarsening.hpp / gmres_poly.hpp
+  // the single operations of air.hpp / coarsening.hpp / gmres_poly.hpp, on
+  // the blocks of the final (post-DDC) labels
   {
+    const BlockSplit s = extract_blocks(af, l.label);
     DominanceReport dr = dominance_report(s.a_ff, 1000);
     airgraph_gpu::DominanceReport gd = airgraph_gpu::dominance_report(ctx, s.a_ff, 1000);
     bool hist_ok = gd.histogram.size() == dr.histogram.size();
