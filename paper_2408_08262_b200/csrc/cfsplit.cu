@@ -734,6 +734,14 @@ namespace {
 #define AIRG_CF_WARR 0
 #endif
 constexpr int kCfUnroll = AIRG_CF_UNROLL;
+#ifndef AIRG_CF_PIPE
+#define AIRG_CF_PIPE 1
+#endif
+#if AIRG_CF_PIPE
+#define CF_RESTRICT __restrict__
+#else
+#define CF_RESTRICT
+#endif
 
 // Visit the entries k = s..e-1 of one row in order, f(ci[k], v[k]). VEC:
 // the aligned body as 16-byte loads (4 column indices, 2 x 2 values) --
@@ -742,7 +750,31 @@ template <bool VEC, class F>
 __device__ __forceinline__ void for_row(const int32_t* __restrict__ ci, const double* __restrict__ v, int s,
                                         int e, F&& f) {
   int k = s;
-  if (VEC) {
+  if (VEC && AIRG_CF_PIPE) {
+    // software-pipelined: group k+4's loads are issued before group k is used
+    for (; k < e && (k & 3); ++k) f(__ldg(ci + k), __ldg(v + k));
+    if (k + 4 <= e) {
+      int4 c = __ldg(reinterpret_cast<const int4*>(ci + k));
+      double2 a = __ldg(reinterpret_cast<const double2*>(v + k));
+      double2 b = __ldg(reinterpret_cast<const double2*>(v + k + 2));
+      for (; k + 4 <= e; k += 4) {
+        int4 cn = c;
+        double2 an = a, bn = b;
+        if (k + 8 <= e) {
+          cn = __ldg(reinterpret_cast<const int4*>(ci + k + 4));
+          an = __ldg(reinterpret_cast<const double2*>(v + k + 4));
+          bn = __ldg(reinterpret_cast<const double2*>(v + k + 6));
+        }
+        f(c.x, a.x);
+        f(c.y, a.y);
+        f(c.z, b.x);
+        f(c.w, b.y);
+        c = cn;
+        a = an;
+        b = bn;
+      }
+    }
+  } else if (VEC) {
     for (; k < e && (k & 3); ++k) f(__ldg(ci + k), __ldg(v + k));
 #pragma unroll (kCfUnroll)
     for (; k + 4 <= e; k += 4) {
@@ -837,7 +869,8 @@ __device__ __forceinline__ int fcf_row_strength(int i, const int32_t* __restrict
 template <bool VEC, bool COH>
 __device__ __forceinline__ void fcf_row_marks(int i, const int32_t* __restrict__ rp,
                                               const int32_t* __restrict__ ci, const double* __restrict__ v,
-                                              const double* thr, const int2* cnt, uint64_t key, uint8_t* notmin) {
+                                              const double* thr, const int2* CF_RESTRICT cnt, uint64_t key,
+                                              uint8_t* CF_RESTRICT notmin) {
   const double t = ldc<COH>(thr + i);
   const double wi = fcf_weight_c<COH>(cnt, key, i);
   bool mine = false;
