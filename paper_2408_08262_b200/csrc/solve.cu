@@ -166,8 +166,27 @@ inline int wg_lanes(const Csr& m) {
   return m.nnz >= rows * (int64_t)m.n ? g : 0;
 }
 
+// AIRG_W32=1: matrices whose mean row length is >= AIRG_W32_ROWS (default 12)
+// run the warp-staged product kernels (w32.cuh) in the captured V-cycle
+inline int w32_on(const Csr& m) {
+  static const bool on = [] {
+    const char* e = getenv("AIRG_W32");
+    return e && e[0] == '1';
+  }();
+  static const int64_t rows = [] {
+    const char* e = getenv("AIRG_W32_ROWS");
+    return e ? (int64_t)atoi(e) : (int64_t)12;
+  }();
+  static const int64_t rows_max = [] {
+    const char* e = getenv("AIRG_W32_MAX");
+    return e ? (int64_t)atoi(e) : (int64_t)1 << 30;
+  }();
+  if (!on || m.n <= 0 || m.row_mode != 1 || m.group > 1 || m.perm.p || m.c16.p) return 0;
+  return m.nnz >= rows * (int64_t)m.n && m.nnz < rows_max * (int64_t)m.n ? 1 : 0;
+}
+
 inline TileView tv(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p, m.stage, wg_lanes(m)};
+  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p, m.stage, wg_lanes(m), w32_on(m)};
 }
 inline SellView svw(const Csr& m) {
   return SellView{m.s_off.p, m.s_len.p, m.s_perm.p, m.s_ci.p, m.s_v.p, m.n, m.s_nslices, m.s_g};

@@ -44,6 +44,7 @@ struct TileView {
   const int32_t* cbase = nullptr;
   int stage = 0;         // > 0: staged row kernels (staged.cuh), shared slice capacity in entries
   int wg = 0;            // > 0: lanes per row of the long-row group kernels (wgroup.cuh)
+  int w32 = 0;           // 1: warp-staged product kernels (w32.cuh)
 };
 
 // ---- thread per row -----------------------------------------------------------
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(kTileThreads) rows_group_fc(TileView m, const 
 }  // namespace airg
 #include "staged.cuh"
 #include "wgroup.cuh"
+#include "w32.cuh"
 namespace airg {
 
 // grid size for either mode
@@ -451,6 +453,8 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi);    \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group, Epi, view, x, epi)                                  \
+    else if ((view).w32)                                                                        \
+      LAUNCH_PDL(ctx, (rows_w32<Epi, false>), rows_grid(view), kTileThreads, (w32_smem_checked<Epi, false>()), view, x, epi); \
     else if ((view).wg > 0)                                                                     \
       WG_SWITCH(ctx, false, Epi, view, x, epi)                                                  \
     else if ((view).stage > 0)                                                                  \
@@ -466,6 +470,8 @@ inline unsigned rows_grid(const TileView& m) {
       LAUNCH_PDL(ctx, rows_warp_tiles_fc<Epi>, rows_grid(view), kTileThreads, 0, view, x, epi); \
     else if ((view).group > 1)                                                              \
       ROWS_GROUP_SWITCH(LAUNCH_PDL, ctx, rows_group_fc, Epi, view, x, epi)                                  \
+    else if ((view).w32)                                                                        \
+      LAUNCH_PDL(ctx, (rows_w32<Epi, true>), rows_grid(view), kTileThreads, (w32_smem_checked<Epi, true>()), view, x, epi); \
     else if ((view).wg > 0)                                                                     \
       WG_SWITCH(ctx, true, Epi, view, x, epi)                                                   \
     else if ((view).stage > 0)                                                                  \

@@ -54,6 +54,8 @@ LAYOUTS = {
     "wg4_all": {"AIRG_WG": "4", "AIRG_WG_ROWS": "1"},
     "wg8": {"AIRG_WG": "8"},
     "wg16_all": {"AIRG_WG": "16", "AIRG_WG_ROWS": "1"},
+    "w32": {"AIRG_W32": "1"},
+    "w32_all": {"AIRG_W32": "1", "AIRG_W32_ROWS": "1"},
 }
 
 
@@ -61,7 +63,7 @@ def _run(env_extra):
     env = dict(os.environ)
     for k in ("AIRG_ROWS", "AIRG_GROUP", "AIRG_LAYOUT", "AIRG_PDL", "AIRG_VEC", "AIRG_TAIL_N", "AIRG_TAIL",
               "AIRG_DEVLOOP", "AIRG_EARLY", "AIRG_SPLIT", "AIRG_SORT",
-              "AIRG_C16", "AIRG_STAGE", "AIRG_STAGE_CAP", "AIRG_WG", "AIRG_WG_ROWS"):
+              "AIRG_C16", "AIRG_STAGE", "AIRG_STAGE_CAP", "AIRG_WG", "AIRG_WG_ROWS", "AIRG_W32", "AIRG_W32_ROWS"):
         env.pop(k, None)
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
