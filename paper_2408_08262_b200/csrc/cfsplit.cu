@@ -22,6 +22,8 @@
 //   reference's strict '<', one-shot conversion theta > alpha && theta != 0.
 #include "sparse.cuh"
 
+#include <cooperative_groups.h>
+
 namespace airg {
 
 namespace {
@@ -1219,7 +1221,19 @@ struct FcfSmall {
 };
 constexpr int kSmallThreads = 1024;
 
-template <bool VEC>
+// barrier between the phases of the one-launch split: the software grid
+// barrier (cooperative launch over up to one CTA per SM) or, CL, the
+// hardware barrier of ONE thread-block cluster (<= 16 CTAs; release/acquire
+// at cluster scope orders the global-memory phases as well)
+template <bool CL>
+__device__ __forceinline__ void small_barrier(unsigned* bar, unsigned nblk) {
+  if constexpr (CL)
+    cooperative_groups::this_cluster().sync();
+  else
+    grid_barrier(bar, nblk);
+}
+
+template <bool VEC, bool CL = false>
 __global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_constant__ FcfSmall P) {
   extern __shared__ unsigned sh[];
   const int n = P.n;
@@ -1233,15 +1247,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_const
     P.cnt[k] = make_int2(0, 0);
     P.notmin[k] = 0;
   }
-  grid_barrier(P.bar, nblk);
+  small_barrier<CL>(P.bar, nblk);
   // 1: strength, |S_i|, |S^T| counts
   unsigned long long acc = 0;
   for (int i = tid; i < n; i += stride) acc += fcf_row_strength<VEC>(i, P.rp, P.ci, P.v, P.alpha, P.thr, P.cnt);
   block_add(P.u, acc);
-  grid_barrier(P.bar, nblk);
+  small_barrier<CL>(P.bar, nblk);
   // 2: not-minimal marks
   for (int i = tid; i < n; i += stride) fcf_row_marks<VEC, true>(i, P.rp, P.ci, P.v, P.thr, P.cnt, P.key, P.notmin);
-  grid_barrier(P.bar, nblk);
+  small_barrier<CL>(P.bar, nblk);
   if (!P.ddc) {
     unsigned long long nf = 0;
     for (int i = tid; i < n; i += stride) {
@@ -1260,7 +1274,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_const
     if (fr) tb = max(tb, fcf_row_theta<VEC, true>(i, P.rp, P.ci, P.v, P.notmin, P.theta, P.u + 3));
   }
   block_max(P.u + 2, tb);
-  grid_barrier(P.bar, nblk);
+  small_barrier<CL>(P.bar, nblk);
   // 4: histogram + F count (bins <= 8192 on this path: CTA-private bins)
   {
     const int64_t bins = P.bins;
@@ -1286,11 +1300,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_const
     for (int b = threadIdx.x; b < bins; b += blockDim.x)
       if (sh[b]) atomicAdd(P.hist + b, (unsigned long long)sh[b]);
   }
-  grid_barrier(P.bar, nblk);
+  small_barrier<CL>(P.bar, nblk);
   // 5: alpha_diag (one CTA)
   if (blockIdx.x == 0)
     ddc_select_block(P.u + 1, 0, P.hist, P.bins, P.fraction, P.u + 2, 0, 0.0, reinterpret_cast<double*>(P.u + 5));
-  grid_barrier(P.bar, nblk);
+  small_barrier<CL>(P.bar, nblk);
   // 6: conversion and the final labels
   const double sel = __ldcg(reinterpret_cast<const double*>(P.u + 5));
   const bool ok = __ldcg(P.u + 3) == 0;
@@ -1311,6 +1325,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_const
 // levels up to AIRG_CF_SMALL rows take the one-launch split (default 0 = off:
 // measured slower than the PDL-chained passes on every C2 level, 2.67 -> 2.93 ms
 // at 131072; the passes are dependent-latency bound either way)
+// levels up to AIRG_CF_CLUSTER rows take the one-launch split on one
+// 16-CTA thread-block cluster (hardware barrier between the phases)
+int64_t cf_cluster_rows() {
+  static const int64_t v = [] {
+    const char* e = getenv("AIRG_CF_CLUSTER");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  return v;
+}
+
 int64_t cf_small_rows() {
   static const int64_t v = [] {
     const char* e = getenv("AIRG_CF_SMALL");
@@ -1359,6 +1383,36 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
   const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
+  if (n <= cf_cluster_rows() && (!ddc_enabled || bins <= 8192) && cf_group() == 0) {
+    FcfSmall P{n, a.rp.p, a.ci.p, a.v.p, alpha, key, ddc_enabled ? 1 : 0, fraction, bins,
+               d_u_out ? d_u_out : u, hist, cnt, notmin, thr, theta, d_labels, d_labels_pre, nullptr};
+    if (!ddc_enabled && d_labels_pre) P.label_pre = nullptr;
+    auto* k = vec ? fcf_small<true, true> : fcf_small<false, true>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[vec]) {
+      CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(unsigned)));
+      attr_set[vec] = true;
+    }
+    const unsigned nblk = (unsigned)std::min<int64_t>(16, std::max<int64_t>(1, (n + 1023) / 1024));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = ddc_enabled ? (size_t)bins * sizeof(unsigned) : 0;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nblk;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    c.launches++;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, P));
+    if (!ddc_enabled && d_labels_pre)
+      CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
+    return d_u_out ? d_u_out : u;
+  }
   if (n <= cf_small_rows() && (!ddc_enabled || bins <= 8192) && cf_group() == 0) {
     if (!c.grid_bar) {
       CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.grid_bar), 2 * sizeof(unsigned), c.stream));
