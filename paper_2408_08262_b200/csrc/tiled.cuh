@@ -90,8 +90,13 @@ __device__ __forceinline__ void thread_row(const TileView& m, const double* __re
 // count at what its own loop needs)
 // batch kinds (TileView::vec): 0 = 8-entry scalar batches, 8 = aligned 8-entry
 // vector batches (long rows), 4 = 4-entry scalar batches (short rows)
+// minimum resident blocks per SM of the row kernels (build knob; 1 = the
+// compiler's register choice)
+#ifndef AIRG_ROWS_MIN_BLOCKS
+#define AIRG_ROWS_MIN_BLOCKS 1
+#endif
 template <class Epi, bool VEC = false, int VB = kRowBatch>
-__global__ void __launch_bounds__(kTileThreads) rows_thread(TileView m, const double* __restrict__ x,
+__global__ void __launch_bounds__(kTileThreads, AIRG_ROWS_MIN_BLOCKS) rows_thread(TileView m, const double* __restrict__ x,
                                                             Epi epi) {
   thread_row<VB, VEC>(m, x, epi);
   epi.finish();
