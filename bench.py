@@ -631,6 +631,7 @@ def run_gpu(args):
         "cf_split_roofline": {"bound": "hbm", "achieved": cf_bytes / (cf_ms / 1e3) / 1e9, "peak": peak,
                               "unit": "GB/s", "frac": cf_bytes / (cf_ms / 1e3) / 1e9 / peak,
                               "alg_bytes_all_levels": cf_bytes,
+                              "traffic": prof.get("cf_split_dram_bytes_all_levels"),
                               "bytes_rule": "sum over levels of 2(12 nnz + 4n) + 16|S| + 26n (SURVEY 8d)"},
         "roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
                      "frac": step_achieved / peak, "traffic": step_traffic,

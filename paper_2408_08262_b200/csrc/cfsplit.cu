@@ -1193,6 +1193,47 @@ __global__ void fcf_convert(int n, const uint8_t* __restrict__ notmin, const dou
   block_add(count, conv ? 1ull : 0ull);
 }
 
+// alpha_diag and the conversion in ONE launch: every CTA (<= one per SM)
+// runs the selection block on the histogram (8 KB from L2 each) into shared
+// memory -- the same value in every CTA -- and converts its grid-stride share
+// of the rows; CTA 0 also writes alpha_diag / max theta for the report.
+__global__ void __launch_bounds__(kSelThreads)
+fcf_select_convert(int n, const unsigned long long* __restrict__ nfp, const unsigned long long* __restrict__ hist,
+                   int64_t bins, double fraction, const unsigned long long* __restrict__ maxbits,
+                   double* __restrict__ sel_out, const uint8_t* __restrict__ notmin,
+                   const double* __restrict__ theta, const unsigned long long* __restrict__ bad_row,
+                   uint8_t* __restrict__ label, unsigned long long* __restrict__ count) {
+  __shared__ double ssel[2];
+  pdl_wait();
+  pdl_trigger();
+  ddc_select_block(nfp, 0, hist, bins, fraction, maxbits, 0, 0.0, ssel);
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < 2) sel_out[threadIdx.x] = ssel[threadIdx.x];
+  const double sel = ssel[0];
+  const bool ok = *bad_row == 0;
+  unsigned long long conv = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const bool f = !notmin[i];
+    bool c = false;
+    if (f && ok) {
+      const double t = theta[i];
+      c = t > sel && t != 0.0;
+    }
+    label[i] = f && !c ? AIRG_F : AIRG_C;
+    conv += c;
+  }
+  block_add(count, conv);
+}
+
+// AIRG_CF_SELCONV=0 restores the separate selection and conversion kernels
+bool cf_selconv() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_CF_SELCONV");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // ---- the whole split of a small level in ONE launch ----
 // Small levels are launch- and latency-bound as six kernels (~30 us a
 // level whatever n is). One cooperative launch of up to one 1024-thread CTA
@@ -1463,10 +1504,16 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
     const unsigned hb = (unsigned)std::min<int64_t>(g, 4 * c.num_sms);
     const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
     LAUNCH_PDL(c, fcf_hist, hb, 256, smem, n, notmin, theta, u + 2, bins, hist, u + 1);
-    LAUNCH_PDL(c, fcf_select, 1, kSelThreads, 0, u + 1, 0ll, hist, bins, fraction, u + 2, 0, 0.0,
-               reinterpret_cast<double*>(u + 5));
-    LAUNCH_PDL(c, fcf_convert, g, 256, 0, n, notmin, theta, reinterpret_cast<const double*>(u + 5), u + 3,
-               d_labels, u + 4);
+    if (cf_selconv() && bins <= 8192) {
+      const unsigned gs = (unsigned)std::min<int64_t>(c.num_sms, (n + kSelThreads - 1) / kSelThreads);
+      LAUNCH_PDL(c, fcf_select_convert, gs, kSelThreads, 0, n, u + 1, hist, bins, fraction, u + 2,
+                 reinterpret_cast<double*>(u + 5), notmin, theta, u + 3, d_labels, u + 4);
+    } else {
+      LAUNCH_PDL(c, fcf_select, 1, kSelThreads, 0, u + 1, 0ll, hist, bins, fraction, u + 2, 0, 0.0,
+                 reinterpret_cast<double*>(u + 5));
+      LAUNCH_PDL(c, fcf_convert, g, 256, 0, n, notmin, theta, reinterpret_cast<const double*>(u + 5), u + 3,
+                 d_labels, u + 4);
+    }
   } else {
     LAUNCH_PDL(c, fcf_labels, g, 256, 0, n, notmin, d_labels, u + 1);
     if (d_labels_pre)

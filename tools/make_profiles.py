@@ -71,6 +71,29 @@ def main(tag="r1"):
                         val = float(f[1]) * BYTES.get(f[2], 1)
                         rd, wr = (val, wr) if f[0] == "dram_rd" else (rd, val)
                 res["spmv_dram_bytes_per_launch"] = rd + wr
+    # CF split of all C2 levels (tools/ncu_cf.py): launch list + level-3 captures
+    cfl = os.path.join(out, f"{tag}_cf_launches.csv")
+    if os.path.exists(cfl):
+        L = launches(cfl)
+        t = collections.defaultdict(float)
+        b = collections.defaultdict(float)
+        n = collections.Counter()
+        for d in L:
+            t[d["name"]] += d.get("us", 0.0)
+            b[d["name"]] += d.get("dram", 0.0)
+            n[d["name"]] += 1
+        tot, totb = sum(t.values()), sum(b.values())
+        lines = [f"ncu launch list of one batched CF split of all C2 levels (tools/ncu_cf.py): {len(L)} launches,",
+                 f"serialised cold-cache kernel time {tot:.1f} us, DRAM bytes {totb / 1e6:.1f} MB",
+                 f"{'us':>10} {'share':>6} {'count':>6} {'DRAM MB':>9}  kernel"]
+        for k, v in sorted(t.items(), key=lambda x: -x[1]):
+            lines.append(f"{v:10.1f} {100 * v / tot:5.1f}% {n[k]:6d} {b[k] / 1e6:9.1f}  {k}")
+        rep = os.path.join(out, f"{tag}_cf_l3.ncu-rep")
+        if os.path.exists(rep):
+            lines += ["", "--set full of the three row passes at level 3 (n = 947,182, nnz = 16,719,437):",
+                      summary(rep)]
+        open(os.path.join(prof, f"{tag}_cf_ncu.txt"), "w").write("\n".join(lines) + "\n")
+        res["cf_split_dram_bytes_all_levels"] = totb
     json.dump(res, open(os.path.join(prof, "dram_bytes.json"), "w"), indent=1)
     print(json.dumps(res))
 
