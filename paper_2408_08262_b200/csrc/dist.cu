@@ -933,6 +933,18 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
   // ---- partitions: the reference replay rule, then the coarse gather
   d.lv.resize(L);
   int active = P;
+  // AIRG_DIST_MIN_ROWS (default 0 = off): beside the reference's locality
+  // rule, halve the active ranks while a level has fewer rows per active rank
+  // than this. Over NVLink the halo bytes of the slab partitions are
+  // negligible (tools/dist_model.py: < 30 MB per V-cycle at 8 ranks, ~4 us
+  // of link time) while every exchange costs a latency; below ~10^5 rows per
+  // rank the row kernels sit at their launch floor, so fewer, fuller ranks
+  // remove exchanges without adding kernel time. Any partition gives the
+  // same bits.
+  const int64_t min_rows = [] {
+    const char* e = getenv("AIRG_DIST_MIN_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
   for (int l = 0; l < L; ++l) {
     DLevel& D = d.lv[l];
     const Csr& A = h.levels[l].a;
@@ -941,6 +953,13 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
     D.ratio_before = locality(c, A, p);
     D.ratio_after = D.ratio_before;
     if (D.ratio_before < threshold && active > 1) {
+      const int na = (active + 1) / 2;
+      p = merged(p, active, na);
+      active = na;
+      D.triggered = true;
+      D.ratio_after = locality(c, A, p);
+    }
+    while (min_rows > 0 && active > 1 && (int64_t)A.n < min_rows * (int64_t)active) {
       const int na = (active + 1) / 2;
       p = merged(p, active, na);
       active = na;

@@ -84,6 +84,24 @@ def test_dist_c2_reduced_with_zslabs():
     assert d.level_info(0)["halo"] > 0
 
 
+@pytest.mark.parametrize("min_rows", [1000, 6000])
+def test_dist_min_rows_rule_bit_identical(min_rows, monkeypatch):
+    """AIRG_DIST_MIN_ROWS (the latency rule for NVLink, dist.cu) halves the
+    active ranks on the small levels; the solve keeps the one-GPU bits."""
+    monkeypatch.setenv("AIRG_DIST_MIN_ROWS", str(min_rows))
+    p = problems.c2_structured_3d(32)
+    prm = dict(problems.setup_params(2), coarse_size_target=500)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    ref = airg.richardson_solve(h, p.b, coarse_iterations=3)
+    d = airg.Dist(h, 8, threshold=2.0, starts=np.linspace(0, p.n, 9).astype(np.int64))
+    act = [d.level_info(l)["active"] for l in range(h.n_levels)]
+    assert act == sorted(act, reverse=True) and act[-1] < 8
+    for l in range(h.n_levels):
+        assert h.level(l).n >= min_rows * d.level_info(l)["active"] or d.level_info(l)["active"] == 1
+    res = d.solve(p.b, coarse_iterations=3)
+    assert same_bits(res.x, ref.x)
+
+
 def _split_cases():
     out = []
     for path in GOLDEN[:4]:
