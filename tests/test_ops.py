@@ -180,3 +180,26 @@ def test_f_smooth(be):
     exp[f2f] = exp[f2f] + d
     assert same_bits(got, exp)
     assert same_bits(got[c2f], x[c2f])
+
+
+@pytest.mark.gpu
+def test_device_buffer_helpers_round_trip():
+    """airg_device_alloc / airg_memcpy / airg_device_free (the buffers the
+    C++ adapter uses without linking CUDA)."""
+    import ctypes as C
+    from paper_2408_08262_b200 import airg
+    L = airg.lib()
+    for name, args in (("airg_device_alloc", [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+                       ("airg_device_free", [C.c_void_p, C.c_void_p]),
+                       ("airg_memcpy", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32])):
+        getattr(L, name).argtypes = args
+        getattr(L, name).restype = C.c_int
+    ctx = airg.default_context()
+    src = np.random.default_rng(0).random(1000)
+    dst = np.zeros_like(src)
+    p = C.c_void_p()
+    assert L.airg_device_alloc(ctx.h, src.nbytes, C.byref(p)) == 0 and p.value
+    assert L.airg_memcpy(ctx.h, p, src.ctypes.data, src.nbytes, 1) == 0
+    assert L.airg_memcpy(ctx.h, dst.ctypes.data, p, src.nbytes, 0) == 0
+    assert L.airg_device_free(ctx.h, p) == 0
+    assert same_bits(src, dst)
