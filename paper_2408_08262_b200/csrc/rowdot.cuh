@@ -151,6 +151,44 @@ template <int VB, bool VEC>
 struct RowBatch {
   int c[VB];
   double a[VB];
+  // column / value halves of load() (AIRG_PIPE == 2)
+  __device__ __forceinline__ void load_cols(int k0, int e, int nnz, const int32_t* __restrict__ ci, int* cc) const {
+    if (VEC) {
+#pragma unroll
+      for (int g = 0; g < VB; g += 4) {
+        const int k = k0 + g;
+        if (k + 4 <= nnz) {
+          const int4 q = __ldg(reinterpret_cast<const int4*>(ci + k));
+          cc[g] = q.x; cc[g + 1] = q.y; cc[g + 2] = q.z; cc[g + 3] = q.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cc[g + j] = k + j < nnz ? __ldg(ci + k + j) : 0;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < VB; ++j) cc[j] = k0 + j < e ? __ldg(ci + k0 + j) : 0;
+    }
+  }
+  __device__ __forceinline__ void load_vals(int k0, int e, int nnz, const double* __restrict__ v) {
+    if (VEC) {
+#pragma unroll
+      for (int g = 0; g < VB; g += 4) {
+        const int k = k0 + g;
+        if (k + 4 <= nnz) {
+          const double2 p = __ldg(reinterpret_cast<const double2*>(v + k));
+          const double2 q = __ldg(reinterpret_cast<const double2*>(v + k + 2));
+          a[g] = p.x; a[g + 1] = p.y; a[g + 2] = q.x; a[g + 3] = q.y;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a[g + j] = k + j < nnz ? __ldg(v + k + j) : 0.0;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < VB; ++j) a[j] = k0 + j < e ? __ldg(v + k0 + j) : 0.0;
+    }
+  }
   __device__ __forceinline__ void load(int k0, int e, int nnz, const int32_t* __restrict__ ci,
                                        const double* __restrict__ v) {
     if (VEC) {
@@ -183,7 +221,25 @@ __device__ __forceinline__ double dot_prefetched(int s, int e, int nnz, const in
                                                  RowBatch<VB, VEC>& b) {
   double acc = 0.0;
   const int k00 = batch_start<VB, VEC>(s);
-#if AIRG_PIPE
+#if AIRG_PIPE == 2
+  for (int k0 = k00; k0 < e; k0 += VB) {
+    double xv[VB];
+#pragma unroll
+    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + b.c[j]) : 0.0;
+    int cn[VB];
+    const bool more = k0 + VB < e;
+    if (more) b.load_cols(k0 + VB, e, nnz, ci, cn);
+#pragma unroll
+    for (int j = 0; j < VB; ++j)
+      if (k0 + j >= s && k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(b.a[j], xv[j]));
+    if (more) {
+#pragma unroll
+      for (int j = 0; j < VB; ++j) b.c[j] = cn[j];
+      b.load_vals(k0 + VB, e, nnz, v);
+    }
+  }
+  return acc;
+#elif AIRG_PIPE
   for (int k0 = k00; k0 < e; k0 += VB) {
     double xv[VB];
 #pragma unroll
@@ -224,7 +280,30 @@ __device__ __forceinline__ void dot_fc_src(int s, int e, int nnz, const int32_t*
   sc = 0.0;
   const int k00 = batch_start<VB, VEC>(s);
   for (int k0 = k00; k0 < e; k0 += VB) {
-#if AIRG_PIPE
+#if AIRG_PIPE == 2
+    double xv[VB];
+#pragma unroll
+    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? xs(b.c[j] & 0x7fffffff) : 0.0;
+    int cn[VB];
+    const bool more = k0 + VB < e;
+    if (more) b.load_cols(k0 + VB, e, nnz, ci, cn);
+#pragma unroll
+    for (int j = 0; j < VB; ++j) {
+      if (k0 + j >= s && k0 + j < e) {
+        const double p = __dmul_rn(b.a[j], xv[j]);
+        if (b.c[j] >= 0)
+          sf = __dadd_rn(sf, p);
+        else
+          sc = __dadd_rn(sc, p);
+      }
+    }
+    if (more) {
+#pragma unroll
+      for (int j = 0; j < VB; ++j) b.c[j] = cn[j];
+      b.load_vals(k0 + VB, e, nnz, v);
+    }
+    continue;
+#elif AIRG_PIPE
     double xv[VB];
 #pragma unroll
     for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? xs(b.c[j] & 0x7fffffff) : 0.0;
