@@ -203,3 +203,41 @@ def test_device_buffer_helpers_round_trip():
     assert L.airg_memcpy(ctx.h, dst.ctypes.data, p, src.nbytes, 0) == 0
     assert L.airg_device_free(ctx.h, p) == 0
     assert same_bits(src, dst)
+
+
+_CF_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+from backends import PortBackend
+port = PortBackend()
+for nx in (12, 20):
+    p = problems.c2_structured_3d(nx)
+    a = (p.n, p.n, p.row_offsets, p.cols, p.vals)
+    for seed in (0, 3):
+        lab, pre, rep = airg.cf_split(airg.SparseMatrix.from_arrays(*a), 0.5, 3, seed)
+        exp, exp_pre, _ = port.cf_split(a, seed=seed)
+        assert np.array_equal(lab, exp) and np.array_equal(pre, exp_pre), (nx, seed)
+print("ok")
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"AIRG_CF_CLUSTER": "100000000"}, {"AIRG_CF_SMALL": "100000000"},
+                                 {"AIRG_CF_SELCONV": "0"}, {"AIRG_CF_GROUP": "8"}],
+                         ids=["one_cluster", "one_cooperative_launch", "separate_select", "lane_groups"])
+def test_fused_cf_split_schedules_match_oracle(env):
+    """The fused split's alternative schedules (read once per process, hence a
+    subprocess each) give the oracle's labels bit for bit."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _CF_SCRIPT % (repo, os.path.join(repo, "tests"), os.path.join(repo, "oracle"))
+    full = dict(os.environ)
+    full.update(env)
+    out = subprocess.run([sys.executable, "-c", script], env=full, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
