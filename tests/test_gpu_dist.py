@@ -241,7 +241,9 @@ def test_dist_p2p_transport_emulated_bit_identical():
     bits as one GPU, twice in a row on the same distribution."""
     import subprocess
     import sys
-    env = dict(os.environ, AIRG_TRANSPORT="p2p")
-    out = subprocess.run([sys.executable, "-c", P2P_SCRIPT], env=env, capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0, out.stderr[-3000:]
-    assert "p2p ok" in out.stdout
+    for extra in ({}, {"AIRG_DIST_MIN_ROWS": "3000"}):  # slabs as given / merged on the small levels
+        env = dict(os.environ, AIRG_TRANSPORT="p2p", **extra)
+        out = subprocess.run([sys.executable, "-c", P2P_SCRIPT], env=env, capture_output=True, text=True,
+                             timeout=900)
+        assert out.returncode == 0, out.stderr[-3000:]
+        assert "p2p ok" in out.stdout
