@@ -1,22 +1,29 @@
 #!/usr/bin/env python
 """AIRG benchmark (driver contract: one JSON line from rank 0).
 
-Workload (BASELINE.json configs[2], the largest structured single-GPU case):
-3D 7-point upwind streaming operator, 128^3 cells = 2,097,152 unknowns,
-fp64, alpha 0.5, DDC 0.1, poly order 4, truncation at 5,000 rows, coarse
-poly order 8, Richardson to rtol 1e-10 from x = 0. Synthetic seeded input
-(problems.py; no dataset exists for this operator).
+Workload (BASELINE.json configs[4], the configuration the metric's 1/2/4/8
+GPU weak scaling is quoted on): the 3D unstructured P0 upwind streaming
+operator on a jittered tet lattice, 70 x 70 x 68 cubes x 6 tets =
+1,999,200 unknowns per GPU (z-slabs at N > 1), fp64, alpha 0.5, DDC 0.1,
+poly order 4, truncation at 5,000 rows, coarse poly order 8; solved to
+rtol 1e-10 from x = 0 by the outer right-preconditioned GMRES(30) with one
+AIRG V(0,2) cycle per iteration. (The reference's own Richardson diverges on
+this system -- level-0 smoother growth 2.33 on the best of its six fits --
+so both arms run the same GMRES(30); tests/golden/full/c4.npz.)
+Synthetic seeded input (problems.py; no dataset exists for this operator).
 
-One STEP = one complete AIRG solve (Richardson, V(0,2) cycles) of that
-system with b already resident in HBM; value = unknowns solved per second
-over all ranks. The hierarchy is built once before timing (setup time and
-the CF-split time are reported alongside as setup_ms / cf_split_ms).
+One STEP = one complete solve of that system with b already resident in HBM;
+value = unknowns solved per second over all ranks. The hierarchy is built
+once before timing (setup and CF-split times are reported alongside).
 L2 is flushed (512 MiB write) before every timed step; the hierarchy
-(~1.8 GB) is larger than L2 as well.
+(~1 GB) and the Krylov basis (~1 GB) are larger than L2 as well.
+`configs` adds C2 (128^3) and C3 (8.4 M unknowns) under Richardson, one GPU.
 
---impl reference times the reference's own serial CPU implementation
-(oracle/_ref built from /root/reference, else the C restatement) on the
-same configuration; each step is one full Richardson solve.
+--impl reference times the reference's own CPU implementation (oracle/_ref
+built from /root/reference; else the C restatement) on the SAME full-size
+system with the same outer GMRES(30) around the reference's vcycle():
+K full solves spread over all host cores (the reference is serial; its
+solves of one hierarchy are reentrant, solve.hpp / SPEC.md:92).
 """
 from __future__ import annotations
 
@@ -49,6 +56,52 @@ def spmv_bytes(rows, cols, nnz):
     """int32 column + fp64 value per nonzero, int32 row
     pointer, x read once, y written once."""
     return 12 * nnz + 4 * (rows + 1) + 8 * cols + 8 * rows
+
+
+def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2):
+    """Algorithmic HBM bytes of one V-cycle (see solve_alg_bytes)."""
+    info = h.info()
+    per_cycle = 0
+    for l in range(info.n_levels):
+        lv = h.level(l)
+        n, nf, nc = lv.n, lv.n_f, lv.n_c
+        r = 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc
+        fres1 = 12 * (lv.nnz_ff + lv.nnz_fc) + 4 * (nf + 1) + 8 * n + nf * (4 + 8 + 8 + 8)
+        fupd = 12 * lv.nnz_ffinv + 4 * (nf + 1) + 8 * nf + nf * (4 + 16)
+        fres2 = 12 * lv.nnz_ff + 4 * (nf + 1) + 8 * nf + nf * (4 + 8 + 8 + 8)
+        prol = n * (4 + 8) + 8 * nc
+        smooths = fres1 + fupd + (up_smooths - 1) * (fres2 + fupd)
+        per_cycle += r + prol + smooths
+    cn = info.coarse_n
+    for it in range(coarse_iterations):
+        per_cycle += 12 * info.coarse_inv_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+        if it:
+            per_cycle += 12 * info.coarse_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+    return per_cycle
+
+
+def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2):
+    """Algorithmic HBM bytes of one GMRES(m) solve. Per Arnoldi step j (one
+    outer iteration): the V-cycle (vcycle_alg_bytes), w = A z (SpMV + z
+    written), classical Gram-Schmidt twice -- at least three sweeps over
+    V_0..V_j (dots; first update fused with the second dots; second update
+    with the norm) plus w read/written per sweep -- and v_{j+1} = w / |w|.
+    Per restart: x += Z y (j + 2 vectors), r = b - A x and its norm."""
+    info = h.info()
+    top = h.level(0) if info.n_levels else None
+    n = top.n if top else info.coarse_n
+    nnz = top.nnz if top else info.coarse_nnz
+    cyc = vcycle_alg_bytes(h, coarse_iterations, up_smooths)
+    spmv = spmv_bytes(n, n, nnz)
+    tot = 8 * n  # ||b||
+    left = iterations
+    while left > 0:
+        j_max = min(restart, left)
+        for j in range(j_max):
+            tot += cyc + spmv + 8 * n + 3 * (j + 1) * 8 * n + 5 * 8 * n + 16 * n
+        tot += (j_max + 2) * 8 * n + spmv + 8 * n
+        left -= j_max
+    return tot
 
 
 def solve_alg_bytes(h, iterations, coarse_iterations, up_smooths=2):
@@ -196,84 +249,119 @@ def oracle_lib():
     return refpy, (ref if ref is not None else refpy.port()), ("reference" if ref is not None else "port")
 
 
-def cpu_solve_sample(cfg_idx: int, nx: int):
-    """Bounded CPU sample: the reference (or its restatement) on the same
-    generator at nx^3, setup untimed, one Richardson solve timed."""
+def solver_kw(cfg_idx: int) -> dict:
+    """Outer solver per config: GMRES(30) for C0 (its config names it) and
+    C4 (the reference's Richardson diverges there), Richardson otherwise."""
+    return dict(outer=1, gmres_restart=30) if cfg_idx in (0, 4) else dict(outer=0)
+
+
+def solver_name(cfg_idx: int) -> str:
+    return "outer GMRES(30) + AIRG V(0,2)" if cfg_idx in (0, 4) else "Richardson + AIRG V(0,2)"
+
+
+def cpu_solve_sample(cfg_idx: int):
+    """Bounded CPU sample for `cpu_baseline`: the reference (or its
+    restatement) on the same generator at half the linear size (1/8 of the
+    unknowns; ~10 s of serial work), setup untimed, one solve timed with the
+    same outer solver."""
     from paper_2408_08262_b200 import problems
     refpy, lib, kind = oracle_lib()
-    p = problems.c2_structured_3d(nx)
+    p = problems.make(cfg_idx, 0.5)
     prm = problems.setup_params(cfg_idx)
     A = lib.mat_from_problem(p)
     h = refpy.setup(lib, A, **prm)
     t0 = time.perf_counter()
-    x, st, _ = h.solve(p.b, refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"]))
+    x, st, _ = h.solve(p.b, refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"],
+                                                   max_iterations=400, **solver_kw(cfg_idx)))
     t = time.perf_counter() - t0
     return {"value": p.n / t, "unit": "DOF/s", "cores": 1, "kind": kind,
-            "sample": f"C2 generator at {nx}^3 ({p.n} unknowns): one serial Richardson solve "
-                      f"({st.iterations} its, {t:.2f} s; setup untimed) on {cpu_model()}"}
+            "sample": f"C{cfg_idx} generator at half linear size ({p.n} unknowns): one serial "
+                      f"{solver_name(cfg_idx)} solve ({st.iterations} its, {t:.2f} s; setup untimed) "
+                      f"on {cpu_model()}"}
 
 
 def run_reference(args):
+    """The reference's own serial CPU path on the SAME full-size system and
+    outer solver as the GPU arm, with all host cores. The serial setup (~55 s
+    for C4) runs once, untimed. One complete solve is then timed alone (its
+    iteration count I and time are reported). For GMRES(m) each of the K
+    steps is a bounded sample: one full restart cycle (m iterations from
+    x = 0 -- the same work as every complete cycle of the solve), the K
+    samples running concurrently on min(K, cores) threads (the reference's
+    solves of one hierarchy are reentrant; ctypes releases the
+    GIL); value = K * m / I solves' worth of unknowns over the pool's wall
+    time. For Richardson each step is one complete solve."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    from concurrent.futures import ThreadPoolExecutor
     from paper_2408_08262_b200 import problems
     refpy, lib, kind = oracle_lib()
-    # A bounded sample of the workload: the reference's serial setup of the
-    # full 128^3 system alone takes ~150 s (one solve ~12 s, 0.18 M DOF/s,
-    # measured in this container), so each step is one full Richardson solve
-    # of the same C2 generator at --cpu-nx^3 (default 64^3: setup ~15 s once,
-    # ~0.5 s per solve); DOF/s is size-normalised, and the smaller sample is
-    # the reference's faster (cache-resident) case.
-    full = problems.make(args.config, args.scale)
-    if args.config == 2 and args.cpu_nx and args.cpu_nx < round(128 * args.scale):
-        p = problems.c2_structured_3d(args.cpu_nx)
-        sample = f"C2 generator at {args.cpu_nx}^3 ({p.n} unknowns) as a bounded sample of the {full.n}-unknown workload"
-    else:
-        p = full
-        sample = "full workload"
+    p = problems.make(args.config, args.scale)
     prm = problems.setup_params(args.config)
     A = lib.mat_from_problem(p)
     t0 = time.perf_counter()
     h = refpy.setup(lib, A, **prm)
     setup_s = time.perf_counter() - t0
-    scfg = refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"])
-    for _ in range(args.warmup):
-        h.solve(p.b, scfg)
-    times = []
-    its = 0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        x, st, _ = h.solve(p.b, scfg)
-        times.append(time.perf_counter() - t0)
-        its = st.iterations
-    tot = sum(times)
-    value = p.n * args.steps / tot
+    skw = solver_kw(args.config)
+    full_cfg = refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **skw)
+    t0 = time.perf_counter()
+    _, fst, _ = h.solve(p.b, full_cfg)
+    full_s = time.perf_counter() - t0
+    its = int(fst.iterations)
+    gm = skw["outer"] == 1
+    m = skw.get("gmres_restart", 30)
+    step_cfg = (refpy.abi.solve_config(coarse_iterations=prm["coarse_iterations"], max_iterations=min(m, its), **skw)
+                if gm else full_cfg)
+    frac = min(m, its) / its if gm else 1.0  # one step = this fraction of a complete solve
+    threads = max(1, min(args.steps, cpu_cores()))
+
+    def one(_):
+        t = time.perf_counter()
+        h.solve(p.b, step_cfg)
+        return time.perf_counter() - t
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        res = list(pool.map(one, range(args.steps)))
+    wall = time.perf_counter() - t0
+    solves = args.steps * frac
+    value = p.n * solves / wall
+    sample = (f"full workload ({p.n} unknowns): one complete {solver_name(args.config)} solve timed alone "
+              f"({its} its, {full_s:.1f} s), then {args.steps} samples of one full GMRES({m}) restart cycle "
+              f"({min(m, its)} iterations from x = 0 = {frac:.3f} of a solve) on {threads} concurrent threads"
+              if gm else f"full workload ({p.n} unknowns): {args.steps} complete {solver_name(args.config)} "
+                         f"solves on {threads} concurrent threads")
+    sample += f" of {cpu_model()} ({cpu_cores()} cores visible); setup once, untimed"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args, full, "serial CPU"),
-        "iterations": its, "final_relative_residual": st.final_relative_residual,
-        "setup_ms": 1e3 * setup_s,
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": kind,
-                         "sample": f"{sample}, one Richardson solve per step on {cpu_model()} "
-                                   f"(serial reference; {cpu_cores()} cores visible)"},
+        "data": "synthetic", "config": config_dict(args, p, f"serial reference x {threads} concurrent solves"),
+        "iterations": its, "final_relative_residual": float(fst.final_relative_residual),
+        "converged": bool(fst.converged), "setup_ms": 1e3 * setup_s,
+        "single_solve_ms": 1e3 * full_s, "single_solve_dof_s": p.n / full_s,
+        "step_ms_mean": 1e3 * sum(res) / len(res),
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-METRIC = "AIRG solve DOFs/s (Richardson to rtol 1e-10, V(0,2) cycles)"
+METRIC = "AIRG solve DOFs/s"
 
 
-def config_dict(args, p, par):
-    names = {0: "C0 2D structured upwind 128^2", 1: "C1 2D unstructured upwind 512^2 quads",
-             2: "C2 3D structured 7-point upwind 128^3", 3: "C3 2D S_n 256^2 x 64 angles",
-             4: "C4 3D unstructured tets 2M/GPU"}
-    return {"workload": names.get(args.config, str(args.config)) + (f" (scale {args.scale})" if args.scale != 1 else ""),
+CONFIG_NAMES = {0: "C0 2D structured upwind 128^2", 1: "C1 2D unstructured upwind 512^2 quads",
+                2: "C2 3D structured 7-point upwind 128^3", 3: "C3 2D S_n 256^2 x 64 angles",
+                4: "C4 3D unstructured tets, 70x70x68 cubes x 6 = 1,999,200 tets per GPU"}
+
+
+def config_dict(args, p, par, cfg_idx=None):
+    c = args.config if cfg_idx is None else cfg_idx
+    return {"workload": CONFIG_NAMES.get(c, str(c)) + (f" (scale {args.scale})" if args.scale != 1 else ""),
             "unknowns": int(p.n), "nnz": int(p.nnz), "alpha": 0.5, "ddc_fraction": 0.1, "poly_order": 4,
+            "solver": solver_name(c) + " to rtol 1e-10 from x = 0",
             "parallelism": par, "l2": "flushed (512 MiB write) before each timed step; hierarchy > L2"}
 
 
@@ -419,6 +507,66 @@ def run_gpu_dist(args):
     return 0
 
 
+def _ev():
+    import torch
+    return torch.cuda.Event(enable_timing=True)
+
+
+def time_solves(h, ctx, tb, tx, flush, steps, sk):
+    """Device-resident solves, L2 flushed before each; per-step event times."""
+    import torch
+    stream = ctx.stream
+    out = []
+    st = None
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        s0, s1 = _ev(), _ev()
+        s0.record(stream)
+        st, _ = h.solve_device(tb, tx, **sk)
+        s1.record(stream)
+        s1.synchronize()
+        out.append(s0.elapsed_time(s1))
+    return out, st
+
+
+def extra_config(ctx, cfg_idx, flush, steps=5, warmup=3):
+    """A secondary single-GPU line (C2 / C3): setup + device-resident solves."""
+    import torch
+    from paper_2408_08262_b200 import airg, problems
+    p = problems.make(cfg_idx)
+    prm = problems.setup_params(cfg_idx)
+    dA = airg.DeviceCSR.upload(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), ctx)
+    h = airg.setup(dA, ctx=ctx, **prm)
+    del h
+    torch.cuda.synchronize()
+    e0, e1 = _ev(), _ev()
+    e0.record(ctx.stream)
+    h = airg.setup(dA, ctx=ctx, **prm)
+    e1.record(ctx.stream)
+    e1.synchronize()
+    setup_ms = e0.elapsed_time(e1)
+    with torch.cuda.stream(ctx.stream):
+        tb = torch.from_numpy(p.b).to(ctx.tdev)
+        tx = torch.empty(p.n, dtype=torch.float64, device=ctx.tdev)
+    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **solver_kw(cfg_idx))
+    for _ in range(warmup):
+        h.solve_device(tb, tx, **sk)
+    times, st = time_solves(h, ctx, tb, tx, flush, steps, sk)
+    ms = sum(times) / len(times)
+    its = int(st.iterations)
+    byts = (gmres_alg_bytes(h, its, prm["coarse_iterations"]) if sk["outer"]
+            else solve_alg_bytes(h, its, prm["coarse_iterations"]))
+    peak, _ = hbm_peak()
+    out = {"workload": CONFIG_NAMES[cfg_idx], "unknowns": int(p.n), "solver": solver_name(cfg_idx),
+           "value": p.n / (ms / 1e3), "unit": "DOF/s", "ms_per_step": ms, "steps": steps,
+           "iterations": its, "final_relative_residual": float(st.final_relative_residual),
+           "levels": int(h.n_levels), "setup_ms": setup_ms,
+           "roofline_frac": byts / (ms / 1e3) / 1e9 / peak}
+    del h, dA
+    return out
+
+
 def run_gpu(args):
     import torch
     from paper_2408_08262_b200 import airg, problems
@@ -433,10 +581,7 @@ def run_gpu(args):
     prm = problems.setup_params(args.config)
     a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
     dA = airg.DeviceCSR.upload(a, ctx)
-
-    def ev():
-        e = torch.cuda.Event(enable_timing=True)
-        return e
+    ev = _ev
 
     # ---- setup (warm once, then time)
     h = airg.setup(dA, ctx=ctx, **prm)
@@ -490,60 +635,20 @@ def run_gpu(args):
         tx = torch.empty(p.n, dtype=torch.float64, device=ctx.tdev)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=ctx.tdev)
     torch.cuda.synchronize()
-    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **solver_kw(args.config))
     for _ in range(args.warmup):
         st, _ = h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    times = []
     l0 = ctx.launches()
     clk = ClockSampler(dev).__enter__()
-    if True:
-        for _ in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(1.0)
-            s0, s1 = ev(), ev()
-            s0.record(stream)
-            st, _ = h.solve_device(tb, tx, **sk)
-            s1.record(stream)
-            s1.synchronize()
-            times.append(s0.elapsed_time(s1))
+    times, st = time_solves(h, ctx, tb, tx, flush, args.steps, sk)
     launches = ctx.launches() - l0
     torch.cuda.synchronize()
-    local_ms = sum(times)
-    tot_ms = local_ms
-    if ws > 1:
-        t = torch.tensor([local_ms], device=ctx.tdev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = sum(times)
     ms_per_step = tot_ms / args.steps
-    value = p.n * ws * args.steps / (tot_ms / 1e3)
+    value = p.n * args.steps / (tot_ms / 1e3)
     x = ctx.to_host(tx)
     rel = np.linalg.norm(p.b - airg.spmv(dA, x, ctx=ctx)) / np.linalg.norm(p.b)
-
-    # ---- the same system under the outer GMRES(30) the north star names
-    # (device-resident b; reported beside the Richardson headline)
-    gm = None
-    try:
-        gk = dict(sk, outer=1, gmres_restart=30)
-        h.solve_device(tb, tx, **gk)
-        gt = []
-        for _ in range(3):
-            with torch.cuda.stream(stream):
-                flush.fill_(1.0)
-            g0, g1 = ev(), ev()
-            g0.record(stream)
-            gst, _ = h.solve_device(tb, tx, **gk)
-            g1.record(stream)
-            g1.synchronize()
-            gt.append(g0.elapsed_time(g1))
-        gms = statistics.median(gt)
-        gm = {"value": p.n * ws / (gms / 1e3), "unit": "DOF/s", "ms_per_step": gms,
-              "iterations": int(gst.iterations), "final_relative_residual": float(gst.final_relative_residual),
-              "restart": 30}
-    except Exception as exc:  # keep the headline line
-        gm = {"error": str(exc)[:200]}
 
     # ---- end-to-end through the reference-facing call (host b -> host x)
     hb = torch.from_numpy(p.b.copy()).pin_memory()
@@ -554,22 +659,22 @@ def run_gpu(args):
             flush.fill_(1.0)
         s0, s1 = ev(), ev()
         s0.record(stream)
-        res = h.solve_host_ptr(hb.data_ptr(), hx.data_ptr(), **sk)
+        h.solve_host_ptr(hb.data_ptr(), hx.data_ptr(), **sk)
         s1.record(stream)
         s1.synchronize()
         if k >= args.warmup:
             e2e_times.append(s0.elapsed_time(s1))
     clk.__exit__(None, None, None)  # clocks sampled across the device and e2e timed loops
     e2e_ms = sum(e2e_times) / len(e2e_times)
-    e2e_value = p.n * ws / (e2e_ms / 1e3)
+    e2e_value = p.n / (e2e_ms / 1e3)
 
     # ---- roofline. The unit is the whole solve step ("per
-    # V-cycle and per solve: sum over every SpMV and vector op"), whose
-    # kernels replay as one captured graph per Richardson iteration; no single
-    # kernel owns more than ~30% of it (profiles/r1_solve_launches.txt). The
-    # level-0 SpMV (the reference's top hot spot, sparse.cpp:185-201) is
-    # reported beside it, timed alone.
-    step_bytes = solve_alg_bytes(h, int(st.iterations), prm["coarse_iterations"])
+    # V-cycle and per solve: sum over every SpMV and vector op"): no single
+    # kernel owns more than ~15% of it (profiles/). The level-0 SpMV (the
+    # reference's top hot spot, sparse.cpp:185-201) is reported beside it.
+    its = int(st.iterations)
+    step_bytes = (gmres_alg_bytes(h, its, prm["coarse_iterations"]) if sk["outer"]
+                  else solve_alg_bytes(h, its, prm["coarse_iterations"]))
     peak, peak_kind = hbm_peak()
     step_achieved = step_bytes / (ms_per_step / 1e3) / 1e9
     A0 = h.matrix_handle(0, 0) if info.n_levels else dA
@@ -578,9 +683,6 @@ def run_gpu(args):
     with torch.cuda.stream(stream):
         xv = torch.rand(n0, dtype=torch.float64, device=ctx.tdev)
         yv = torch.empty(n0, dtype=torch.float64, device=ctx.tdev)
-    # (a) back to back: A + x + y = alg_bytes > the 126 MB L2, so the
-    # operands stream from HBM; (b) one launch after an L2 flush (includes
-    # the launch latency of a ~30 us kernel)
     for _ in range(3):
         airg.spmv_device(A0, xv, yv, ctx=ctx)
     k0, k1 = ev(), ev()
@@ -607,16 +709,25 @@ def run_gpu(args):
     pf = os.path.join(REPO, "profiles", "dram_bytes.json")
     if os.path.exists(pf):
         try:
-            prof = json.load(open(pf))
+            prof = json.load(open(pf)).get(f"C{args.config}", {})
         except Exception:
             prof = {}
-    step_traffic = prof.get("solve_dram_bytes_per_step")
-    spmv_traffic = prof.get("spmv_dram_bytes_per_launch")
+
+    extras = {}
+    if not args.no_extras and args.scale == 1:
+        del h
+        for c in (2, 3):
+            if c == args.config:
+                continue
+            try:
+                extras[f"C{c}"] = extra_config(ctx, c, flush)
+            except Exception as exc:  # keep the headline line
+                extras[f"C{c}"] = {"error": str(exc)[:200]}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_solve_sample(args.config, args.cpu_nx)
+            cpu = cpu_solve_sample(args.config)
         except Exception as exc:  # keep the GPU line even if the checker fails
             cpu = {"value": None, "unit": "DOF/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -624,8 +735,8 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, p, "replicas (one independent system per GPU)" if ws > 1 else "single GPU"),
-        "iterations": int(st.iterations), "final_relative_residual": float(rel),
+        "config": config_dict(args, p, "single GPU"),
+        "iterations": its, "final_relative_residual": float(rel),
         "levels": int(info.n_levels), "operator_complexity": info.operator_complexity,
         "setup_ms": setup_ms, "cf_split_ms": cf_ms, "cf_split_ms_sync_each_level": cf_ms_each,
         "cf_split_roofline": {"bound": "hbm", "achieved": cf_bytes / (cf_ms / 1e3) / 1e9, "peak": peak,
@@ -634,30 +745,25 @@ def run_gpu(args):
                               "traffic": prof.get("cf_split_dram_bytes_all_levels"),
                               "bytes_rule": "sum over levels of 2(12 nnz + 4n) + 16|S| + 26n (SURVEY 8d)"},
         "roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
-                     "frac": step_achieved / peak, "traffic": step_traffic,
-                     "kernel": "one AIRG solve step: the captured V-cycle graph of all row kernels, "
-                               "replayed once per Richardson iteration",
+                     "frac": step_achieved / peak, "traffic": prof.get("solve_dram_bytes_per_step"),
+                     "kernel": "one AIRG solve step: every kernel of the solve (V-cycle graphs, "
+                               "Krylov orthogonalisation, residuals)",
                      "alg_bytes_per_step": step_bytes, "avg_step_ms": ms_per_step, "peak_kind": peak_kind,
-                     "reference_op_bytes_per_step": reference_op_bytes(h, int(st.iterations),
-                                                                       prm["coarse_iterations"]),
-                     "top_spmv": {"kernel": "rows_thread on level-0 A (exact CSR SpMV, y = A x)",
-                                  "achieved": achieved, "frac": achieved / peak, "traffic": spmv_traffic,
+                     "top_spmv": {"kernel": "level-0 CSR SpMV y = A x",
+                                  "achieved": achieved, "frac": achieved / peak,
+                                  "traffic": prof.get("spmv_dram_bytes_per_launch"),
                                   "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_ms,
-                                  "timing": "50 back-to-back launches; A + x + y exceed the 126 MB L2",
+                                  "timing": "50 back-to-back launches",
                                   "flushed_single_launch_ms": flushed_ms,
                                   "flushed_single_launch_frac": alg_bytes / (flushed_ms / 1e3) / 1e9 / peak}},
         "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 8 * p.n,
                 "d2h_bytes_per_step": 8 * p.n, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
-        "gmres": gm,
+        "configs": extras,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -667,9 +773,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="airg", choices=["airg", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--cpu-nx", type=int, default=64)
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2 / C3 secondary lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the distributed (NCCL row-slab) path even on one rank")

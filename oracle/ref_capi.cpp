@@ -6,6 +6,9 @@
 // airgraph:: entry points through ctypes with the same plain-pointer shapes
 // as include/airg_c.h. Nothing here is product code; the product never
 // loads oracle/_ref.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -506,10 +509,132 @@ int ref_vcycle(const void* hp, const airg_solve_config* cfg, const double* b,
     std::memcpy(x, r.data(), sizeof(double) * n);
   });
 }
+// Outer right-preconditioned restarted GMRES (CGS2, Givens) around the
+// reference's own vcycle() and spmv() (solve.hpp:51-54, sparse.hpp:97-98).
+// NOT in the reference (Richardson only, solve.cpp:167-259); the same steps
+// as orc_solve(outer = 1) in oracle/airg_oracle.c and the GPU's solve.cu, so
+// the reference arm can run the systems on which Richardson diverges (C4).
+static void ref_gmres(const Hierarchy& h, const airg_solve_config* cfg, const double* b,
+                      double* x, airg_solve_stats* st, double* hist, int64_t cap) {
+  const SparseMatrix& a = h.top();
+  const index_t n = a.nrows();
+  const int64_t m = cfg->gmres_restart > 0 ? cfg->gmres_restart : 30;
+  if (cfg->rtol <= 0.0) throw std::invalid_argument("gmres_solve: rtol must be positive");
+  const SolveConfig scfg = to_scfg(cfg);
+  int64_t hl = 0;
+  auto push = [&](double v) {
+    if (hist && hl < cap) hist[hl] = v;
+    ++hl;
+  };
+  auto nrm = [&](const double* v) {
+    double s = 0.0;
+    for (index_t i = 0; i < n; ++i) s += v[i] * v[i];
+    return std::sqrt(s);
+  };
+  std::vector<double> V((size_t)n * (m + 1) + 1), Z((size_t)n * m + 1), r(n), H((m + 1) * m, 0.0);
+  std::vector<double> cs(m), sn(m), g(m + 1), hcol(m + 1), y(m + 1), zero(n, 0.0);
+  std::fill(x, x + n, 0.0);
+  const auto t0 = std::chrono::steady_clock::now();
+  const double bnorm = nrm(b);
+  int64_t its = 0;
+  std::memset(st, 0, sizeof(*st));
+  if (bnorm == 0.0) {
+    st->converged = 1;
+    push(0.0);
+  } else {
+    std::memcpy(r.data(), b, sizeof(double) * n);
+    double beta = bnorm;
+    push(1.0);
+    st->final_relative_residual = 1.0;
+    while (its < cfg->max_iterations) {
+      for (index_t i = 0; i < n; ++i) V[i] = r[i] / beta;
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int64_t j = 0;
+      std::vector<double> w;
+      double hn = 0.0;
+      for (; j < m && its < cfg->max_iterations; ++j) {
+        double* vj = V.data() + j * n;
+        double* zj = Z.data() + j * n;
+        std::vector<double> e = vcycle(h, std::span<const double>(vj, n), zero, scfg);
+        std::memcpy(zj, e.data(), sizeof(double) * n);
+        w = spmv(a, std::span<const double>(zj, n));
+        for (int64_t k = 0; k <= j; ++k) hcol[k] = 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int64_t k = 0; k <= j; ++k) {
+            double s = 0.0;
+            const double* vk = V.data() + k * n;
+            for (index_t i = 0; i < n; ++i) s += vk[i] * w[i];
+            y[k] = s;
+          }
+          for (index_t i = 0; i < n; ++i) {
+            double s = w[i];
+            for (int64_t k = 0; k <= j; ++k) s -= y[k] * V[k * n + i];
+            w[i] = s;
+          }
+          for (int64_t k = 0; k <= j; ++k) hcol[k] += y[k];
+        }
+        hn = nrm(w.data());
+        hcol[j + 1] = hn;
+        double* vn = V.data() + (j + 1) * n;
+        for (index_t i = 0; i < n; ++i) vn[i] = hn > 0.0 ? w[i] / hn : 0.0;
+        for (int64_t k = 0; k < j; ++k) {
+          const double t = cs[k] * hcol[k] + sn[k] * hcol[k + 1];
+          hcol[k + 1] = -sn[k] * hcol[k] + cs[k] * hcol[k + 1];
+          hcol[k] = t;
+        }
+        const double den = std::hypot(hcol[j], hcol[j + 1]);
+        cs[j] = den > 0.0 ? hcol[j] / den : 1.0;
+        sn[j] = den > 0.0 ? hcol[j + 1] / den : 0.0;
+        hcol[j] = den;
+        hcol[j + 1] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        for (int64_t k = 0; k <= j; ++k) H[k + j * (m + 1)] = hcol[k];
+        ++its;
+        const double est = std::fabs(g[j + 1]) / bnorm;
+        push(est);
+        if (est <= cfg->rtol || hn == 0.0) {
+          ++j;
+          break;
+        }
+      }
+      for (int64_t k = j - 1; k >= 0; --k) {
+        double s = g[k];
+        for (int64_t q = k + 1; q < j; ++q) s -= H[k + q * (m + 1)] * y[q];
+        y[k] = s / H[k + k * (m + 1)];
+      }
+      for (index_t i = 0; i < n; ++i) {
+        double s = x[i];
+        for (int64_t k = 0; k < j; ++k) s += y[k] * Z[k * n + i];
+        x[i] = s;
+      }
+      std::vector<double> ax = spmv(a, std::span<const double>(x, n));
+      for (index_t i = 0; i < n; ++i) r[i] = b[i] - ax[i];
+      beta = nrm(r.data());
+      const double rel = beta / bnorm;
+      st->final_relative_residual = rel;
+      if (rel <= cfg->rtol) {
+        st->converged = 1;
+        break;
+      }
+      if (beta == 0.0) break;
+    }
+  }
+  st->iterations = its;
+  st->solve_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  st->history_len = hl;
+}
+
 int ref_solve(const void* hp, const airg_solve_config* cfg, const double* b,
               double* x, airg_solve_stats* st, double* hist, int64_t cap) {
   return guard([&] {
     const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    if (cfg->outer == 1) {
+      ref_gmres(h, cfg, b, x, st, hist, cap);
+      return;
+    }
     const index_t n = h.top().nrows();
     std::vector<double> xo;
     SolveStats s = richardson_solve(h, std::span<const double>(b, n), to_scfg(cfg), &xo);

@@ -952,14 +952,17 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
                                        : balanced(A.n, active, P);
     D.ratio_before = locality(c, A, p);
     D.ratio_after = D.ratio_before;
-    if (D.ratio_before < threshold && active > 1) {
+    // A caller-fixed level-0 partition (one process per GPU: the caller's b
+    // and x slabs) is kept as given; halving applies from level 1 onward.
+    const bool fixed = l == 0 && level0_starts;
+    if (!fixed && D.ratio_before < threshold && active > 1) {
       const int na = (active + 1) / 2;
       p = merged(p, active, na);
       active = na;
       D.triggered = true;
       D.ratio_after = locality(c, A, p);
     }
-    while (min_rows > 0 && active > 1 && (int64_t)A.n < min_rows * (int64_t)active) {
+    while (!fixed && min_rows > 0 && active > 1 && (int64_t)A.n < min_rows * (int64_t)active) {
       const int na = (active + 1) / 2;
       p = merged(p, active, na);
       active = na;

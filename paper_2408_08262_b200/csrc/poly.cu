@@ -229,6 +229,127 @@ __global__ void scale_by(int n, double* __restrict__ v, const double* __restrict
 // host factors G (Cholesky == QR's R up to row signs), applies the same rank
 // cut (|R_kk| < 1e-12 on the normalised basis), the same candidate-degree
 // least-squares solves and scores each candidate's true residual from G.
+namespace {
+using DV = std::vector<dd>;
+
+// Householder reflector of x (length k): beta = -sign(x0)|x|, v0 = 1,
+// tau = (beta - x0) / beta (the same convention as oracle/shim).
+void dd_house(const dd* x, int k, DV& v, dd& tau, dd& beta) {
+  v.assign(x, x + k);
+  dd tail{0.0, 0.0};
+  for (int i = 1; i < k; ++i) tail = dd_add(tail, dd_mul(x[i], x[i]));
+  const dd c0 = x[0];
+  if (tail.hi <= 0.0) {
+    tau = dd{0.0, 0.0};
+    beta = c0;
+    for (int i = 1; i < k; ++i) v[i] = dd{0.0, 0.0};
+    v[0] = dd{1.0, 0.0};
+    return;
+  }
+  beta = dd_sqrt(dd_add(dd_mul(c0, c0), tail));
+  if (c0.hi >= 0.0) beta = dd_neg(beta);
+  const dd den = dd_sub(c0, beta);
+  for (int i = 1; i < k; ++i) v[i] = dd_div(x[i], den);
+  v[0] = dd{1.0, 0.0};
+  tau = dd_div(dd_sub(beta, c0), beta);
+}
+
+// Minimum-norm least squares through a complete orthogonal decomposition in
+// double-double, with the semantics of Eigen's CompleteOrthogonalDecomposition
+// under setThreshold(thr) (gmres_poly.cpp:144-147): column-pivoted
+// Householder QR (pivot = largest remaining column norm, first on ties),
+// rank = #{|R_jj| > thr * max_j |R_jj|}, a right-side Householder (RZ)
+// reduction of the rank-r trapezoid, y = P Z^T [T11^-1 (Q^T b)_r ; 0].
+// a: m x n row-major (overwritten). Returns the rank (0: no solution).
+int cod_solve(DV a, int m, int n, DV b, double thr, DV& y) {
+  const int k = std::min(m, n);
+  std::vector<int> perm(n);
+  for (int j = 0; j < n; ++j) perm[j] = j;
+  auto A = [&](int i, int j) -> dd& { return a[(size_t)i * n + j]; };
+  DV x, v;
+  double maxpiv = 0.0;
+  for (int j = 0; j < k; ++j) {
+    int best = j;
+    double bestn = -1.0;
+    for (int c = j; c < n; ++c) {
+      dd s{0.0, 0.0};
+      for (int i = j; i < m; ++i) s = dd_add(s, dd_mul(A(i, c), A(i, c)));
+      if (s.hi > bestn) {
+        bestn = s.hi;
+        best = c;
+      }
+    }
+    if (best != j) {
+      for (int i = 0; i < m; ++i) std::swap(A(i, j), A(i, best));
+      std::swap(perm[j], perm[best]);
+    }
+    x.resize(m - j);
+    for (int i = j; i < m; ++i) x[i - j] = A(i, j);
+    dd tau, beta;
+    dd_house(x.data(), m - j, v, tau, beta);
+    if (tau.hi != 0.0) {
+      for (int c = j + 1; c < n; ++c) {
+        dd s{0.0, 0.0};
+        for (int i = 0; i < m - j; ++i) s = dd_add(s, dd_mul(v[i], A(j + i, c)));
+        s = dd_mul(s, tau);
+        for (int i = 0; i < m - j; ++i) A(j + i, c) = dd_sub(A(j + i, c), dd_mul(s, v[i]));
+      }
+      dd s{0.0, 0.0};  // b <- H b
+      for (int i = 0; i < m - j; ++i) s = dd_add(s, dd_mul(v[i], b[j + i]));
+      s = dd_mul(s, tau);
+      for (int i = 0; i < m - j; ++i) b[j + i] = dd_sub(b[j + i], dd_mul(s, v[i]));
+    }
+    A(j, j) = beta;
+    for (int i = j + 1; i < m; ++i) A(i, j) = dd{0.0, 0.0};
+    maxpiv = std::max(maxpiv, fabs(beta.hi));
+  }
+  int r = 0;
+  for (int j = 0; j < k; ++j)
+    if (fabs(A(j, j).hi) > thr * maxpiv) ++r;
+  if (r == 0) return 0;
+  // RZ: annihilate columns [r, n) of the top r rows with right reflectors
+  // acting on {kk} u [r, n)
+  std::vector<DV> zv(r);
+  DV ztau(r, dd{0.0, 0.0});
+  if (r < n) {
+    for (int kk = r - 1; kk >= 0; --kk) {
+      x.assign(1 + (n - r), dd{0.0, 0.0});
+      x[0] = A(kk, kk);
+      for (int c = r; c < n; ++c) x[1 + c - r] = A(kk, c);
+      dd tau, beta;
+      dd_house(x.data(), (int)x.size(), v, tau, beta);
+      for (int rr = 0; rr <= kk; ++rr) {
+        dd s = dd_mul(A(rr, kk), v[0]);
+        for (int c = r; c < n; ++c) s = dd_add(s, dd_mul(A(rr, c), v[1 + c - r]));
+        s = dd_mul(s, tau);
+        A(rr, kk) = dd_sub(A(rr, kk), dd_mul(s, v[0]));
+        for (int c = r; c < n; ++c) A(rr, c) = dd_sub(A(rr, c), dd_mul(s, v[1 + c - r]));
+      }
+      zv[kk] = v;
+      ztau[kk] = tau;
+    }
+  }
+  DV w(n, dd{0.0, 0.0});
+  for (int i = r - 1; i >= 0; --i) {
+    dd s = b[i];
+    for (int j = i + 1; j < r; ++j) s = dd_sub(s, dd_mul(A(i, j), w[j]));
+    w[i] = dd_div(s, A(i, i));
+  }
+  for (int kk = 0; kk < (int)zv.size(); ++kk) {
+    if (ztau[kk].hi == 0.0 || zv[kk].empty()) continue;
+    const DV& zk = zv[kk];
+    dd s = dd_mul(w[kk], zk[0]);
+    for (int i = 1; i < (int)zk.size(); ++i) s = dd_add(s, dd_mul(zk[i], w[r + i - 1]));
+    s = dd_mul(s, ztau[kk]);
+    w[kk] = dd_sub(w[kk], dd_mul(s, zk[0]));
+    for (int i = 1; i < (int)zk.size(); ++i) w[r + i - 1] = dd_sub(w[r + i - 1], dd_mul(s, zk[i]));
+  }
+  y.assign(n, dd{0.0, 0.0});
+  for (int j = 0; j < n; ++j) y[perm[j]] = w[j];
+  return r;
+}
+}  // namespace
+
 PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const RowSplit* rs) {
   if (a.n != a.m) throw InvalidArgument("compute_coefficients: matrix must be square");
   if (m < 1) throw InvalidArgument("compute_coefficients: m must be >= 1");
@@ -312,38 +433,15 @@ PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const 
   std::vector<double> best_y;
   for (int d = 1; d <= lcols; ++d) {
     const int lrows = std::min(rrows, d + 1);
-    // Hessenberg least squares via Givens rotations in double-double
+    // the reference's CompleteOrthogonalDecomposition with threshold 1e-12
+    // (gmres_poly.cpp:141-147): column-pivoted rank decision, minimum-norm
+    // solution when the unscaled block is numerically rank deficient
     std::vector<dd> H((size_t)lrows * d), rhs(lrows, dd{0.0, 0.0});
     for (int i = 0; i < lrows; ++i)
       for (int j = 0; j < d; ++j) H[i * d + j] = R[i * nc + 1 + j];
     rhs[0] = R[0];
-    for (int j = 0; j < d && j + 1 < lrows; ++j) {
-      const dd a0 = H[j * d + j], b0 = H[(j + 1) * d + j];
-      const dd r = dd_sqrt(dd_add(dd_mul(a0, a0), dd_mul(b0, b0)));
-      if (r.hi == 0.0) continue;
-      const dd cs = dd_div(a0, r), sn = dd_div(b0, r);
-      for (int k = j; k < d; ++k) {
-        const dd x = H[j * d + k], y = H[(j + 1) * d + k];
-        H[j * d + k] = dd_add(dd_mul(cs, x), dd_mul(sn, y));
-        H[(j + 1) * d + k] = dd_sub(dd_mul(cs, y), dd_mul(sn, x));
-      }
-      const dd x = rhs[j], y = rhs[j + 1];
-      rhs[j] = dd_add(dd_mul(cs, x), dd_mul(sn, y));
-      rhs[j + 1] = dd_sub(dd_mul(cs, y), dd_mul(sn, x));
-    }
-    const int kdim = std::min(d, lrows);
-    double maxpiv = 0.0;
-    for (int j = 0; j < kdim; ++j) maxpiv = std::max(maxpiv, fabs(H[j * d + j].hi));
-    bool deficient = kdim < d;
-    for (int j = 0; j < kdim; ++j)
-      if (!(fabs(H[j * d + j].hi) > 1e-12 * maxpiv)) deficient = true;
-    if (maxpiv == 0.0 || deficient) continue;
-    std::vector<dd> y(d);
-    for (int j = d - 1; j >= 0; --j) {
-      dd s = rhs[j];
-      for (int k = j + 1; k < d; ++k) s = dd_sub(s, dd_mul(H[j * d + k], y[k]));
-      y[j] = dd_div(s, H[j * d + j]);
-    }
+    std::vector<dd> y;
+    if (cod_solve(H, lrows, d, rhs, 1e-12, y) == 0) continue;
     bool finite = true;
     for (int j = 0; j < d; ++j) finite &= std::isfinite(y[j].hi);
     if (!finite) continue;

@@ -905,7 +905,15 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
     const int64_t cap = cfg.max_iterations + 1;
     const bool first_stops = 1.0 <= cfg.rtol || cfg.max_iterations <= 0;
     if (!first_stops && device_loop_enabled() && !h.loop_broken && cap <= (int64_t)1 << 20) {
-      if (h.loop_hist.n < (size_t)cap) h.loop_hist.alloc(c, (size_t)cap);
+      if (h.loop_hist.n < (size_t)cap) {
+        // the captured k_loop_check holds the history pointer and capacity:
+        // a reallocation invalidates the loop graph
+        h.loop_hist.alloc(c, (size_t)cap);
+        if (h.g_loop) {
+          cudaGraphExecDestroy(h.g_loop);
+          h.g_loop = nullptr;
+        }
+      }
       if (!h.loop_par.p) h.loop_par.alloc(c, 2);
       if (!h.loop_it.p) h.loop_it.alloc(c, 1);
       if (!h.loop_stamps.p) h.loop_stamps.alloc(c, 4096);

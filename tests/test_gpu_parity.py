@@ -182,11 +182,12 @@ def test_p5_native_solve_within_tolerance(port, path):
     assert np.linalg.norm(res.x - g["x"]) / np.linalg.norm(g["x"]) <= TOL_X
     # native coefficients track the reference's long-double fit
     oh = refpy.setup(port, port.mat(n, n, g["rp"], g["ci"], g["v"]), **prm)
-    for l in range(min(h.n_levels, oh.info().n_levels)):
+    assert h.n_levels == oh.info().n_levels
+    for l in range(h.n_levels):
         c1 = np.array(h.level(l).coefficients[: prm["poly_order"] + 1])
         c2 = np.array(oh.level(l).coefficients[: prm["poly_order"] + 1])
-        if h.level(l).effective_order == oh.level(l).effective_order:
-            assert np.abs(c1 - c2).max() <= 1e-7 * max(1.0, np.abs(c2).max()), l
+        assert h.level(l).effective_order == oh.level(l).effective_order, l
+        assert np.abs(c1 - c2).max() <= 1e-7 * max(1.0, np.abs(c2).max()), l
 
 
 @pytest.mark.parametrize("path", GOLDEN[:3], ids=lambda p: os.path.basename(p)[:-4])
@@ -280,3 +281,20 @@ def test_solve_device_api_matches_host_api():
     st, hist = h.solve_device(tb, tx, history_cap=64, coarse_iterations=3)
     res = airg.richardson_solve(h, p.b, coarse_iterations=3)
     assert same_bits(ctx.to_host(tx), res.x) and st.iterations == res.stats.iterations
+
+
+def test_device_loop_history_realloc():
+    """Two Richardson solves on one hierarchy with a growing max_iterations:
+    the second reallocates the device history, which must rebuild the
+    captured loop (the loop graph kept the freed buffer)."""
+    p = problems.make(0)
+    prm = problems.setup_params(0)
+    h = airg.setup(_sm(p), **prm)
+    r1 = airg.richardson_solve(h, p.b, coarse_iterations=3, max_iterations=3)
+    assert not r1.stats.converged and r1.stats.iterations == 3 and len(r1.residual_history) == 4
+    r2 = airg.richardson_solve(h, p.b, coarse_iterations=3, max_iterations=500)
+    r3 = airg.richardson_solve(h, p.b, coarse_iterations=3)
+    assert r2.stats.converged and r2.stats.iterations == r3.stats.iterations
+    assert same_bits(r2.residual_history, r3.residual_history) and same_bits(r2.x, r3.x)
+    np.testing.assert_allclose(r2.residual_history[:4], r1.residual_history, rtol=0, atol=0)
+    assert r2.stats.final_relative_residual == r2.residual_history[-1] <= 1e-10

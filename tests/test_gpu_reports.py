@@ -56,13 +56,13 @@ def test_reports_match_reference(ref, path, tmp_path):
     assert strip(ours) == strip(theirs)
     hn = airg.setup(a, **prm)  # native: the guard's numbers agree to rounding
     nat = reports.hierarchy_report(hn)
-    if hn.n_levels == oh.info().n_levels:
-        for lo, lt in zip(nat["levels"], theirs["levels"]):
-            assert lo["poly_attempts"] == lt["poly_attempts"]
-            # native coefficients differ from the long-double fit in the last
-            # digits: the same accept / reject side of 0.5, values close
-            assert (lo["smoother_growth"] <= 0.5) == (lt["smoother_growth"] <= 0.5)
-            assert abs(lo["smoother_growth"] - lt["smoother_growth"]) <= 1e-3 * max(1.0, lt["smoother_growth"])
+    assert hn.n_levels == oh.info().n_levels
+    for lo, lt in zip(nat["levels"], theirs["levels"]):
+        assert lo["poly_attempts"] == lt["poly_attempts"]
+        # native coefficients differ from the long-double fit in the last
+        # digits: the same accept / reject side of 0.5, values close
+        assert (lo["smoother_growth"] <= 0.5) == (lt["smoother_growth"] <= 0.5)
+        assert abs(lo["smoother_growth"] - lt["smoother_growth"]) <= 1e-3 * max(1.0, lt["smoother_growth"])
     res = airg.richardson_solve(h, g["b"], coarse_iterations=prm.get("coarse_iterations", 3))
     assert reports.csv_row(h, res.stats, prm["strength_alpha"], "pmisr-ddc", 7) == \
         oh.csv_row(res.stats, prm["strength_alpha"], "pmisr-ddc", 7)

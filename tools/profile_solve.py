@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--what", default="solve")
+    ap.add_argument("--outer", type=int, default=None, help="1 = outer GMRES(30) (default for C0 / C4)")
     args = ap.parse_args()
     ctx = airg.Context(0)
     p = problems.make(args.config, args.scale)
@@ -41,7 +42,8 @@ def main():
     h = airg.setup(dA, ctx=ctx, **prm)
     tb = ctx.to_device(p.b)
     tx = ctx.empty(p.n, torch.float64)
-    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    outer = args.outer if args.outer is not None else int(args.config in (0, 4))
+    sk = dict(coarse_iterations=prm["coarse_iterations"], outer=outer)
     for _ in range(2):
         st, _ = h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--out", default="gpurun_out/trace_summary.txt")
     ap.add_argument("--what", default="solve", choices=["solve", "setup"])
+    ap.add_argument("--outer", type=int, default=0, help="1 = outer GMRES(30)")
+    ap.add_argument("--max-its", type=int, default=200)
     args = ap.parse_args()
     ctx = airg.Context(0)
     p = problems.make(args.config, args.scale)
@@ -36,7 +38,7 @@ def main():
     h = airg.setup(dA, ctx=ctx, **prm)
     tb = ctx.to_device(p.b)
     tx = ctx.empty(p.n, torch.float64)
-    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    sk = dict(coarse_iterations=prm["coarse_iterations"], outer=args.outer, max_iterations=args.max_its)
     for _ in range(3):
         h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
@@ -75,7 +77,7 @@ def main():
              if gaps else "no gaps"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"{k:48s} {cnt[k]:6d} {v:10.1f} us {100 * v / max(busy, 1e-9):5.1f}%  mean {v / cnt[k]:.2f}")
-    if args.what == "solve" and st.iterations > 2:
+    if args.what == "solve" and st.iterations > 2 and not args.outer:
         # per-level breakdown of one middle iteration (kernel order of
         # enqueue_vcycle: R_0..R_{L-1}, coarse (2 ci - 1), then per level
         # L-1..0: prolong, fres1, fupd, fres2, fupd, ..., then axpy, resid, sum)
