@@ -77,6 +77,10 @@ typedef struct airg_solve_config {
   int32_t outer;              /* 0 = Richardson (reference), 1 = right-preconditioned GMRES */
   int64_t nddofs;             /* 0 */
   int64_t gmres_restart;      /* 30 */
+  int32_t fast;               /* 0 = the reference's bits (thread-per-row ordered sums, no FMA);
+                                 1 = lane groups per row, FMA, tree reductions (solve within
+                                 rounding of the reference: rtol, +-1 iteration, 1e-8 in x) */
+  int32_t _pad2;
 } airg_solve_config;
 
 /* Mirrors airgraph::SolveStats (solve.hpp:21-39). */

@@ -43,6 +43,8 @@ class SolveConfig(C.Structure):
         ("outer", C.c_int32),
         ("nddofs", C.c_int64),
         ("gmres_restart", C.c_int64),
+        ("fast", C.c_int32),
+        ("_pad2", C.c_int32),
     ]
 
 
@@ -121,7 +123,7 @@ SETUP_DEFAULTS = dict(
 
 SOLVE_DEFAULTS = dict(
     rtol=1e-10, max_iterations=200, up_f_smooths=2, down_smooths=0,
-    coarse_iterations=3, collect_timing=1, outer=0, nddofs=0, gmres_restart=30)
+    coarse_iterations=3, collect_timing=1, outer=0, nddofs=0, gmres_restart=30, fast=0, _pad2=0)
 
 
 def setup_config(**kw) -> SetupConfig:

@@ -99,6 +99,8 @@ void airg_solve_config_default(airg_solve_config* c) {
   c->outer = 0;
   c->nddofs = 0;
   c->gmres_restart = 30;
+  c->fast = 0;
+  c->_pad2 = 0;
 }
 
 int airg_ctx_create(int device, airg_ctx** out) {

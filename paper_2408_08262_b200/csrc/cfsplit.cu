@@ -724,16 +724,9 @@ double dominance_max(Ctx& c, const Csr& aff, int rb) {
 // Same arithmetic as the kernels above, so the same labels bit for bit.
 namespace {
 
-// build knobs: AIRG_CF_UNROLL = unroll of the 16-byte row loop; AIRG_CF_WARR:
-// the PMISR weights are written once per level by fcf_wfill after the counts
-// are complete, and the marks pass reads w[j] instead of rebuilding each
-// neighbour's weight from its counts and the hash (the rebuilt-weight marks
-// pass is issue bound: ncu 63 % issue at C2 level 3)
+// build knob: AIRG_CF_UNROLL = unroll of the 16-byte row loop
 #ifndef AIRG_CF_UNROLL
 #define AIRG_CF_UNROLL 1
-#endif
-#ifndef AIRG_CF_WARR
-#define AIRG_CF_WARR 0
 #endif
 constexpr int kCfUnroll = AIRG_CF_UNROLL;
 #ifndef AIRG_CF_PIPE
@@ -799,17 +792,6 @@ int cf_vec_rows() {
     return e ? atoi(e) : 6;
   }();
   return v;
-}
-
-// lanes per row of the three row passes: AIRG_CF_GROUP = 4, 8 or 16
-// (otherwise thread per row, the measured default)
-int cf_group() {
-  static const int g = [] {
-    const char* e = getenv("AIRG_CF_GROUP");
-    const int v = e ? atoi(e) : 0;
-    return v == 4 || v == 8 || v == 16 ? v : 0;
-  }();
-  return g;
 }
 
 // The PMISR weight of row j (coarsening.cpp:50-63): |S_j| + |S^T_j| plus
@@ -936,39 +918,6 @@ __global__ void fcf_marks(int n, const int32_t* __restrict__ rp, const int32_t* 
   if (i < n) fcf_row_marks<VEC, false>(i, rp, ci, v, thr, cnt, key, notmin);
 }
 
-// the PMISR weight of every row, once the counts are complete
-__global__ void fcf_wfill(int n, const int2* __restrict__ cnt, uint64_t key, double* __restrict__ w) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) w[i] = fcf_weight(cnt, key, i);
-}
-
-// not-minimal marks with the weights read from w (same decisions as
-// fcf_row_marks: weight_less(w, j, i) of coarsening.cpp:46-48)
-template <bool VEC>
-__global__ void fcf_marks_w(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                            const double* __restrict__ v, const double* __restrict__ thr,
-                            const double* __restrict__ w, uint8_t* __restrict__ notmin) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double t = thr[i];
-  const double wi = w[i];
-  bool mine = false;
-  for_row<VEC>(ci, v, rp[i], rp[i + 1], [&](int j, double x) {
-    const double mag = fabs(x);
-    if (j == i || !(mag > 0.0) || !(mag >= t)) return;
-    const double wj = w[j];
-    if (wj != wi ? wj < wi : j < i)
-      mine = true;
-    else
-      notmin[j] = 1;
-  });
-  if (mine) notmin[i] = 1;
-}
-
 // theta of an F row over A's F columns in column order (= its A_ff row);
 // also the optional copy of the PMISR labels
 template <bool VEC>
@@ -986,139 +935,8 @@ __global__ void fcf_theta(int n, const int32_t* __restrict__ rp, const int32_t* 
   block_max(maxbits, tb);
 }
 
-// ---- G lanes per row (coalesced: lane l reads entries s+l, s+l+G, ...) ----
-// Max, counts and marks are order-free; theta's off-diagonal sum keeps the
-// column order with a shuffle chain (skipped entries add +0.0, an identity
-// on a sum of magnitudes), so every variant gives the same bits.
 constexpr unsigned kFull = 0xffffffffu;
 
-template <int G>
-__global__ void fcf_rows_g(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                           const double* __restrict__ v, double alpha, double* __restrict__ thr,
-                           int2* __restrict__ cnt, unsigned long long* __restrict__ s_total) {
-  pdl_wait();
-  pdl_trigger();
-  const int lane = threadIdx.x & (G - 1);
-  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
-  int s = 0, e = 0;
-  if (i < n) {
-    s = rp[i];
-    e = rp[i + 1];
-  }
-  double om = 0.0;
-  for (int k = s + lane; k < e; k += G)
-    if (__ldg(ci + k) != i) om = fmax(om, fabs(__ldg(v + k)));
-#pragma unroll
-  for (int o = G / 2; o; o >>= 1) om = fmax(om, __shfl_xor_sync(kFull, om, o, G));
-  const double t = __dmul_rn(alpha, om);
-  int c_i = 0;
-  for (int k = s + lane; k < e; k += G) {
-    const int c = __ldg(ci + k);
-    const double mag = fabs(__ldg(v + k));
-    if (c != i && mag > 0.0 && mag >= t) {
-      ++c_i;
-      atomicAdd(&cnt[c].y, 1);
-    }
-  }
-  block_add(s_total, (unsigned long long)c_i);
-#pragma unroll
-  for (int o = G / 2; o; o >>= 1) c_i += __shfl_xor_sync(kFull, c_i, o, G);
-  if (lane == 0 && i < n) {
-    thr[i] = t;
-    cnt[i].x = c_i;
-  }
-}
-
-template <int G>
-__global__ void fcf_marks_g(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                            const double* __restrict__ v, const double* __restrict__ thr,
-                            const int2* __restrict__ cnt, uint64_t key, uint8_t* __restrict__ notmin) {
-  pdl_wait();
-  pdl_trigger();
-  const int lane = threadIdx.x & (G - 1);
-  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
-  int s = 0, e = 0;
-  double t = 0.0, wi = 0.0;
-  if (i < n) {
-    s = rp[i];
-    e = rp[i + 1];
-    t = thr[i];
-    wi = fcf_weight(cnt, key, i);
-  }
-  int mine = 0;
-  for (int k = s + lane; k < e; k += G) {
-    const int j = __ldg(ci + k);
-    const double mag = fabs(__ldg(v + k));
-    if (j == i || !(mag > 0.0) || !(mag >= t)) continue;
-    const double wj = fcf_weight(cnt, key, j);
-    if (wj != wi ? wj < wi : j < i)
-      mine = 1;
-    else
-      notmin[j] = 1;
-  }
-#pragma unroll
-  for (int o = G / 2; o; o >>= 1) mine |= __shfl_xor_sync(kFull, mine, o, G);
-  if (mine && lane == 0 && i < n) notmin[i] = 1;
-}
-
-template <int G>
-__global__ void fcf_theta_g(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                            const double* __restrict__ v, const uint8_t* __restrict__ notmin,
-                            double* __restrict__ theta, uint8_t* __restrict__ label_pre,
-                            unsigned long long* __restrict__ maxbits, unsigned long long* __restrict__ bad_row) {
-  pdl_wait();
-  pdl_trigger();
-  const int lane = threadIdx.x & (G - 1);
-  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
-  const bool fr = i < n && !notmin[i];
-  if (label_pre && i < n && lane == 0) label_pre[i] = fr ? AIRG_F : AIRG_C;
-  int s = 0, e = 0;
-  if (fr) {
-    s = rp[i];
-    e = rp[i + 1];
-  }
-  double off = 0.0, diag = 0.0;
-  int seen = 0;
-  // the trip count is uniform per group, not per warp: shuffle within the group
-  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << ((threadIdx.x & 31) & ~(G - 1));
-  for (int base = s; base < e; base += G) {
-    const int k = base + lane;
-    double val = 0.0;
-    if (k < e) {
-      const int j = __ldg(ci + k);
-      if (!notmin[j]) {
-        const double mag = fabs(__ldg(v + k));
-        if (j == i) {
-          diag = mag;
-          seen = 1;
-        } else {
-          val = mag;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < G; ++q) off = __dadd_rn(off, __shfl_sync(gmask, val, q, G));
-  }
-#pragma unroll
-  for (int o = G / 2; o; o >>= 1) {
-    diag = fmax(diag, __shfl_xor_sync(kFull, diag, o, G));
-    seen |= __shfl_xor_sync(kFull, seen, o, G);
-  }
-  unsigned long long tb = 0;
-  if (fr && lane == 0) {
-    if (!seen || diag == 0.0) {
-      atomicMax(bad_row, ~(unsigned long long)i);
-      theta[i] = 0.0;
-    } else {
-      const double q = __ddiv_rn(off, diag);
-      theta[i] = q;
-      tb = (unsigned long long)__double_as_longlong(q);
-    }
-  }
-  block_max(maxbits, tb);
-}
-
-// no DDC: write the PMISR labels and count F
 __global__ void fcf_labels(int n, const uint8_t* __restrict__ notmin, uint8_t* __restrict__ label,
                            unsigned long long* __restrict__ nf) {
   pdl_wait();
@@ -1225,165 +1043,6 @@ fcf_select_convert(int n, const unsigned long long* __restrict__ nfp, const unsi
   block_add(count, conv);
 }
 
-// AIRG_CF_SELCONV=0 restores the separate selection and conversion kernels
-bool cf_selconv() {
-  static const bool v = [] {
-    const char* e = getenv("AIRG_CF_SELCONV");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
-// ---- the whole split of a small level in ONE launch ----
-// Small levels are launch- and latency-bound as six kernels (~30 us a
-// level whatever n is). One cooperative launch of up to one 1024-thread CTA
-// per SM runs the same passes with the same row functions, separated by
-// the software grid barrier; loads of data written inside the launch go
-// through L2 (ld.global.cg). Scratch zeroing is its first phase.
-struct FcfSmall {
-  int n;
-  const int32_t* rp;
-  const int32_t* ci;
-  const double* v;
-  double alpha;
-  uint64_t key;
-  int ddc;
-  double fraction;
-  int64_t bins;
-  unsigned long long* u;     // report counters (8)
-  unsigned long long* hist;  // bins
-  int2* cnt;
-  uint8_t* notmin;
-  double* thr;
-  double* theta;
-  uint8_t* labels;
-  uint8_t* label_pre;  // nullable
-  unsigned* bar;       // grid barrier words (self-resetting)
-};
-constexpr int kSmallThreads = 1024;
-
-// barrier between the phases of the one-launch split: the software grid
-// barrier (cooperative launch over up to one CTA per SM) or, CL, the
-// hardware barrier of ONE thread-block cluster (<= 16 CTAs; release/acquire
-// at cluster scope orders the global-memory phases as well)
-template <bool CL>
-__device__ __forceinline__ void small_barrier(unsigned* bar, unsigned nblk) {
-  if constexpr (CL)
-    cooperative_groups::this_cluster().sync();
-  else
-    grid_barrier(bar, nblk);
-}
-
-template <bool VEC, bool CL = false>
-__global__ void __launch_bounds__(kSmallThreads, 1) fcf_small(const __grid_constant__ FcfSmall P) {
-  extern __shared__ unsigned sh[];
-  const int n = P.n;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int stride = gridDim.x * blockDim.x;
-  const unsigned nblk = gridDim.x;
-  // 0: zero the counters, the histogram, the counts and the marks
-  for (int k = tid; k < 8; k += stride) P.u[k] = 0;
-  for (int64_t k = tid; k < (P.ddc ? P.bins : 0); k += stride) P.hist[k] = 0;
-  for (int k = tid; k < n; k += stride) {
-    P.cnt[k] = make_int2(0, 0);
-    P.notmin[k] = 0;
-  }
-  small_barrier<CL>(P.bar, nblk);
-  // 1: strength, |S_i|, |S^T| counts
-  unsigned long long acc = 0;
-  for (int i = tid; i < n; i += stride) acc += fcf_row_strength<VEC>(i, P.rp, P.ci, P.v, P.alpha, P.thr, P.cnt);
-  block_add(P.u, acc);
-  small_barrier<CL>(P.bar, nblk);
-  // 2: not-minimal marks
-  for (int i = tid; i < n; i += stride) fcf_row_marks<VEC, true>(i, P.rp, P.ci, P.v, P.thr, P.cnt, P.key, P.notmin);
-  small_barrier<CL>(P.bar, nblk);
-  if (!P.ddc) {
-    unsigned long long nf = 0;
-    for (int i = tid; i < n; i += stride) {
-      const bool f = !__ldcg(P.notmin + i);
-      P.labels[i] = f ? AIRG_F : AIRG_C;
-      nf += f;
-    }
-    block_add(P.u + 1, nf);
-    return;
-  }
-  // 3: theta of the F rows (+ the PMISR labels when asked)
-  unsigned long long tb = 0;
-  for (int i = tid; i < n; i += stride) {
-    const bool fr = !__ldcg(P.notmin + i);
-    if (P.label_pre) P.label_pre[i] = fr ? AIRG_F : AIRG_C;
-    if (fr) tb = max(tb, fcf_row_theta<VEC, true>(i, P.rp, P.ci, P.v, P.notmin, P.theta, P.u + 3));
-  }
-  block_max(P.u + 2, tb);
-  small_barrier<CL>(P.bar, nblk);
-  // 4: histogram + F count (bins <= 8192 on this path: CTA-private bins)
-  {
-    const int64_t bins = P.bins;
-    for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
-    __syncthreads();
-    const double mx = __longlong_as_double((long long)__ldcg(P.u + 2));
-    const double width = mx > 0.0 ? __ddiv_rn(mx, (double)bins) : 1.0;
-    const int lane = threadIdx.x & 31;
-    unsigned long long nf = 0;
-    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-      const int i = base + threadIdx.x;
-      long long b = -1;
-      if (i < n && !__ldcg(P.notmin + i)) {
-        b = (long long)__ddiv_rn(__ldcg(P.theta + i), width);
-        if (b > bins - 1) b = bins - 1;
-        ++nf;
-      }
-      const unsigned peers = __match_any_sync(kFull, b);
-      if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(sh + b, (unsigned)__popc(peers));
-    }
-    block_add(P.u + 1, nf);
-    __syncthreads();
-    for (int b = threadIdx.x; b < bins; b += blockDim.x)
-      if (sh[b]) atomicAdd(P.hist + b, (unsigned long long)sh[b]);
-  }
-  small_barrier<CL>(P.bar, nblk);
-  // 5: alpha_diag (one CTA)
-  if (blockIdx.x == 0)
-    ddc_select_block(P.u + 1, 0, P.hist, P.bins, P.fraction, P.u + 2, 0, 0.0, reinterpret_cast<double*>(P.u + 5));
-  small_barrier<CL>(P.bar, nblk);
-  // 6: conversion and the final labels
-  const double sel = __ldcg(reinterpret_cast<const double*>(P.u + 5));
-  const bool ok = __ldcg(P.u + 3) == 0;
-  unsigned long long conv = 0;
-  for (int i = tid; i < n; i += stride) {
-    const bool f = !__ldcg(P.notmin + i);
-    bool c = false;
-    if (f && ok) {
-      const double t = __ldcg(P.theta + i);
-      c = t > sel && t != 0.0;
-    }
-    P.labels[i] = f && !c ? AIRG_F : AIRG_C;
-    conv += c;
-  }
-  block_add(P.u + 4, conv);
-}
-
-// levels up to AIRG_CF_SMALL rows take the one-launch split (default 0 = off:
-// measured slower than the PDL-chained passes on every C2 level, 2.67 -> 2.93 ms
-// at 131072; the passes are dependent-latency bound either way)
-// levels up to AIRG_CF_CLUSTER rows take the one-launch split on one
-// 16-CTA thread-block cluster (hardware barrier between the phases)
-int64_t cf_cluster_rows() {
-  static const int64_t v = [] {
-    const char* e = getenv("AIRG_CF_CLUSTER");
-    return e ? (int64_t)atoll(e) : (int64_t)0;
-  }();
-  return v;
-}
-
-int64_t cf_small_rows() {
-  static const int64_t v = [] {
-    const char* e = getenv("AIRG_CF_SMALL");
-    return e ? (int64_t)atoll(e) : (int64_t)0;
-  }();
-  return v;
-}
-
 }  // namespace
 
 void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,
@@ -1411,7 +1070,7 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   const size_t nb = ddc_enabled ? (size_t)bins : 0;
   const size_t zero_bytes = (8 + nb) * 8 + (size_t)n * 8 + (size_t)n;
   const size_t head = (zero_bytes + 15) & ~(size_t)15;
-  const size_t bytes = head + (AIRG_CF_WARR ? 3 : 2) * (size_t)n * 8;
+  const size_t bytes = head + 2 * (size_t)n * 8;
   uint8_t* base = static_cast<uint8_t*>(ctx_scratch(c, bytes));
   unsigned long long* u = reinterpret_cast<unsigned long long*>(base);
   unsigned long long* hist = u + 8;
@@ -1419,92 +1078,22 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + n);
   double* thr = reinterpret_cast<double*>(base + head);
   double* theta = thr + n;
-  double* wts = theta + n;  // AIRG_CF_WARR only
   // u: [0] |S| [1] n_f_pre [2] max theta bits [3] ~(first bad row), 0 = none
   //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
   const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
-  if (n <= cf_cluster_rows() && (!ddc_enabled || bins <= 8192) && cf_group() == 0) {
-    FcfSmall P{n, a.rp.p, a.ci.p, a.v.p, alpha, key, ddc_enabled ? 1 : 0, fraction, bins,
-               d_u_out ? d_u_out : u, hist, cnt, notmin, thr, theta, d_labels, d_labels_pre, nullptr};
-    if (!ddc_enabled && d_labels_pre) P.label_pre = nullptr;
-    auto* k = vec ? fcf_small<true, true> : fcf_small<false, true>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[vec]) {
-      CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(unsigned)));
-      attr_set[vec] = true;
-    }
-    const unsigned nblk = (unsigned)std::min<int64_t>(16, std::max<int64_t>(1, (n + 1023) / 1024));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nblk);
-    cfg.blockDim = dim3(kSmallThreads);
-    cfg.dynamicSmemBytes = ddc_enabled ? (size_t)bins * sizeof(unsigned) : 0;
-    cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = nblk;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    c.launches++;
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, P));
-    if (!ddc_enabled && d_labels_pre)
-      CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
-    return d_u_out ? d_u_out : u;
-  }
-  if (n <= cf_small_rows() && (!ddc_enabled || bins <= 8192) && cf_group() == 0) {
-    if (!c.grid_bar) {
-      CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.grid_bar), 2 * sizeof(unsigned), c.stream));
-      CUDA_CHECK(cudaMemsetAsync(c.grid_bar, 0, 2 * sizeof(unsigned), c.stream));
-    }
-    FcfSmall P{n, a.rp.p, a.ci.p, a.v.p, alpha, key, ddc_enabled ? 1 : 0, fraction, bins,
-               d_u_out ? d_u_out : u, hist, cnt, notmin, thr, theta, d_labels, d_labels_pre, c.grid_bar};
-    if (!ddc_enabled && d_labels_pre) P.label_pre = nullptr;
-    const unsigned nblk = (unsigned)std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (n + 511) / 512));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nblk);
-    cfg.blockDim = dim3(kSmallThreads);
-    cfg.dynamicSmemBytes = ddc_enabled ? (size_t)bins * sizeof(unsigned) : 0;
-    cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    c.launches++;
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, vec ? fcf_small<true> : fcf_small<false>, P));
-    if (!ddc_enabled && d_labels_pre)
-      CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
-    return d_u_out ? d_u_out : u;
-  }
   CUDA_CHECK(cudaMemsetAsync(base, 0, zero_bytes, c.stream));
   auto* k_rows = vec ? fcf_rows<true> : fcf_rows<false>;
   auto* k_marks = vec ? fcf_marks<true> : fcf_marks<false>;
   auto* k_theta = vec ? fcf_theta<true> : fcf_theta<false>;
-  unsigned gr = g;  // grid of the three row passes
-  const int G = cf_group();
-  if (G > 1) {
-    gr = blocks_for((int64_t)n * G, 256);
-    k_rows = G == 4 ? fcf_rows_g<4> : G == 8 ? fcf_rows_g<8> : fcf_rows_g<16>;
-    k_marks = G == 4 ? fcf_marks_g<4> : G == 8 ? fcf_marks_g<8> : fcf_marks_g<16>;
-    k_theta = G == 4 ? fcf_theta_g<4> : G == 8 ? fcf_theta_g<8> : fcf_theta_g<16>;
-  }
-  LAUNCH_PDL(c, k_rows, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, u);
-  if (AIRG_CF_WARR && G <= 1) {
-    LAUNCH_PDL(c, fcf_wfill, g, 256, 0, n, (const int2*)cnt, key, wts);
-    LAUNCH_PDL(c, vec ? fcf_marks_w<true> : fcf_marks_w<false>, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p,
-               (const double*)thr, (const double*)wts, notmin);
-  } else {
-    LAUNCH_PDL(c, k_marks, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, cnt, key, notmin);
-  }
+  LAUNCH_PDL(c, k_rows, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, alpha, thr, cnt, u);
+  LAUNCH_PDL(c, k_marks, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, thr, cnt, key, notmin);
   if (ddc_enabled) {
-    LAUNCH_PDL(c, k_theta, gr, 256, 0, n, a.rp.p, a.ci.p, a.v.p, notmin, theta, d_labels_pre, u + 2, u + 3);
+    LAUNCH_PDL(c, k_theta, g, 256, 0, n, a.rp.p, a.ci.p, a.v.p, notmin, theta, d_labels_pre, u + 2, u + 3);
     const unsigned hb = (unsigned)std::min<int64_t>(g, 4 * c.num_sms);
     const size_t smem = bins <= 8192 ? (size_t)bins * sizeof(unsigned) : 0;
     LAUNCH_PDL(c, fcf_hist, hb, 256, smem, n, notmin, theta, u + 2, bins, hist, u + 1);
-    if (cf_selconv() && bins <= 8192) {
+    if (bins <= 8192) {
       const unsigned gs = (unsigned)std::min<int64_t>(c.num_sms, (n + kSelThreads - 1) / kSelThreads);
       LAUNCH_PDL(c, fcf_select_convert, gs, kSelThreads, 0, n, u + 1, hist, bins, fraction, u + 2,
                  reinterpret_cast<double*>(u + 5), notmin, theta, u + 3, d_labels, u + 4);

@@ -293,19 +293,6 @@ struct Csr {
   int64_t nnz = 0;
   DBuf<int32_t> rp, ci;
   DBuf<double> v;
-  DBuf<int32_t> tiles;  // row starts of the warp tiles (tiled.cuh), built on demand
-  int32_t ntiles = -1;
-  int8_t row_mode = 0;  // 0 unbuilt, 1 thread (group) per row, 2 warp tiles
-  int8_t group = 1;     // lanes per row in row_mode 1 (tiled.cuh rows_group)
-  int32_t stage = 0;    // > 0: staged row kernels, shared slice capacity in entries (staged.cuh)
-  DBuf<int32_t> perm;   // thread -> row, rows sorted by length within each block (AIRG_SORT)
-  DBuf<uint16_t> c16;   // 16-bit column deltas from cbase (AIRG_C16), built on demand
-  DBuf<int32_t> cbase;
-  // SELL-32-sigma copy for the solve (sell.cuh), built on demand
-  DBuf<int32_t> s_off, s_len, s_perm, s_ci;
-  DBuf<double> s_v;
-  int32_t s_nslices = -1;
-  int32_t s_g = 1;  // lanes per row
 
   Csr() = default;
   Csr(Csr&&) = default;

@@ -309,23 +309,14 @@ struct LResid {
   }
 };
 
-inline TileView rows_of(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, nullptr, 0, m.n, 1, (int)m.nnz, row_vec(m.n, m.nnz)};
-}
-// thread-per-row kernels in the batch kind of the matrix (tiled.cuh)
+// exact thread-per-row kernels in the batch kind of the matrix (tiled.cuh)
 template <class Epi>
 void launch_rows(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
-  const TileView v = rows_of(m);
-  auto* k = v.vec == 8 ? &rows_thread<Epi, true, kVecBatch> : v.vec == 4 ? &rows_thread<Epi, false, 4> : &rows_thread<Epi, false, kScalarBatch>;
-  LAUNCH_PDL(c, k, blocks_for(m.n, kTileThreads), kTileThreads, 0, v, x, epi);
+  LAUNCH_ROWS(c, Epi, tview(m), x, epi);
 }
 template <class Epi>
 void launch_rows_fc(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
-  const TileView v = rows_of(m);
-  auto* k = v.vec == 8   ? &rows_thread_fc<Epi, true, kFcVecBatch>
-            : v.vec == 4 ? &rows_thread_fc<Epi, false, 4>
-                         : &rows_thread_fc<Epi, false, kScalarBatch>;
-  LAUNCH_PDL(c, k, blocks_for(m.n, kTileThreads), kTileThreads, 0, v, x, epi);
+  LAUNCH_ROWS_FC_MODE(c, Epi, tview(m), x, epi, false);
 }
 
 // ---- host helpers ---------------------------------------------------------------

@@ -40,8 +40,6 @@ struct Hier {
   // outer GMRES workspace (allocated on first use)
   int64_t gm_restart = 0;
   DBuf<double> V, Z, w, hbuf, ybuf;
-  // coarse-tail persistent kernel (tail.cuh): grid barrier words
-  DBuf<unsigned> tail_bar;
   // device-side Richardson loop (solve.cu): iteration count, residual
   // history, [rtol, max_iterations] and the conditional-WHILE graph
   DBuf<long long> loop_it;

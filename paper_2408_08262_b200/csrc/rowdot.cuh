@@ -151,44 +151,6 @@ template <int VB, bool VEC>
 struct RowBatch {
   int c[VB];
   double a[VB];
-  // column / value halves of load() (AIRG_PIPE == 2)
-  __device__ __forceinline__ void load_cols(int k0, int e, int nnz, const int32_t* __restrict__ ci, int* cc) const {
-    if (VEC) {
-#pragma unroll
-      for (int g = 0; g < VB; g += 4) {
-        const int k = k0 + g;
-        if (k + 4 <= nnz) {
-          const int4 q = __ldg(reinterpret_cast<const int4*>(ci + k));
-          cc[g] = q.x; cc[g + 1] = q.y; cc[g + 2] = q.z; cc[g + 3] = q.w;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) cc[g + j] = k + j < nnz ? __ldg(ci + k + j) : 0;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < VB; ++j) cc[j] = k0 + j < e ? __ldg(ci + k0 + j) : 0;
-    }
-  }
-  __device__ __forceinline__ void load_vals(int k0, int e, int nnz, const double* __restrict__ v) {
-    if (VEC) {
-#pragma unroll
-      for (int g = 0; g < VB; g += 4) {
-        const int k = k0 + g;
-        if (k + 4 <= nnz) {
-          const double2 p = __ldg(reinterpret_cast<const double2*>(v + k));
-          const double2 q = __ldg(reinterpret_cast<const double2*>(v + k + 2));
-          a[g] = p.x; a[g + 1] = p.y; a[g + 2] = q.x; a[g + 3] = q.y;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) a[g + j] = k + j < nnz ? __ldg(v + k + j) : 0.0;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < VB; ++j) a[j] = k0 + j < e ? __ldg(v + k0 + j) : 0.0;
-    }
-  }
   __device__ __forceinline__ void load(int k0, int e, int nnz, const int32_t* __restrict__ ci,
                                        const double* __restrict__ v) {
     if (VEC) {
@@ -208,39 +170,16 @@ __device__ __forceinline__ int batch_start(int s) {
   return VEC ? (s & ~3) : s;
 }
 
-// AIRG_PIPE (default 1; measured 0.953 -> 0.868 ms per C2 iteration): software-pipelined batches -- batch k+1's (column, value)
-// loads are issued together with batch k's x gathers, so a row costs one
-// dependent memory round trip per batch instead of two (more registers).
-#ifndef AIRG_PIPE
-#define AIRG_PIPE 1
-#endif
-
+// Software-pipelined batches (measured 0.953 -> 0.868 ms per C2 iteration):
+// batch k+1's (column, value) loads are issued together with batch k's x
+// gathers, so a row costs one dependent memory round trip per batch instead
+// of two. The adds stay one left-to-right chain per row.
 template <int VB, bool VEC>
 __device__ __forceinline__ double dot_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
                                                  const double* __restrict__ v, const double* __restrict__ x,
                                                  RowBatch<VB, VEC>& b) {
   double acc = 0.0;
-  const int k00 = batch_start<VB, VEC>(s);
-#if AIRG_PIPE == 2
-  for (int k0 = k00; k0 < e; k0 += VB) {
-    double xv[VB];
-#pragma unroll
-    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + b.c[j]) : 0.0;
-    int cn[VB];
-    const bool more = k0 + VB < e;
-    if (more) b.load_cols(k0 + VB, e, nnz, ci, cn);
-#pragma unroll
-    for (int j = 0; j < VB; ++j)
-      if (k0 + j >= s && k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(b.a[j], xv[j]));
-    if (more) {
-#pragma unroll
-      for (int j = 0; j < VB; ++j) b.c[j] = cn[j];
-      b.load_vals(k0 + VB, e, nnz, v);
-    }
-  }
-  return acc;
-#elif AIRG_PIPE
-  for (int k0 = k00; k0 < e; k0 += VB) {
+  for (int k0 = batch_start<VB, VEC>(s); k0 < e; k0 += VB) {
     double xv[VB];
 #pragma unroll
     for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + b.c[j]) : 0.0;
@@ -252,67 +191,27 @@ __device__ __forceinline__ double dot_prefetched(int s, int e, int nnz, const in
     b = nb;
   }
   return acc;
-#endif
-  for (int k0 = k00; k0 < e; k0 += VB) {
-    if (k0 != k00) b.load(k0, e, nnz, ci, v);
-    double xv[VB];
-#pragma unroll
-    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + b.c[j]) : 0.0;
-#pragma unroll
-    for (int j = 0; j < VB; ++j)
-      if (k0 + j >= s && k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(b.a[j], xv[j]));
-  }
-  return acc;
 }
 
-// x source of the row dots: a plain vector (read-only path) or any gather
-// functor (e.g. the prolongation of a coarse vector, solve.cu XProlong)
-struct XDirect {
-  const double* __restrict__ x;
-  __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
-};
-
-template <int VB, bool VEC, class XS>
-__device__ __forceinline__ void dot_fc_src(int s, int e, int nnz, const int32_t* __restrict__ ci,
-                                           const double* __restrict__ v, const XS& xs, RowBatch<VB, VEC>& b,
-                                           double& sf, double& sc) {
+// F-row variant: columns with bit 31 set are C columns; the F and C partial
+// sums are kept apart (solve.cpp:72-80).
+template <int VB, bool VEC>
+__device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
+                                                  const double* __restrict__ v, const double* __restrict__ x,
+                                                  RowBatch<VB, VEC>& b, double& sf, double& sc) {
   sf = 0.0;
   sc = 0.0;
-  const int k00 = batch_start<VB, VEC>(s);
-  for (int k0 = k00; k0 < e; k0 += VB) {
-#if AIRG_PIPE == 2
+  for (int k0 = batch_start<VB, VEC>(s); k0 < e; k0 += VB) {
     double xv[VB];
 #pragma unroll
-    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? xs(b.c[j] & 0x7fffffff) : 0.0;
-    int cn[VB];
-    const bool more = k0 + VB < e;
-    if (more) b.load_cols(k0 + VB, e, nnz, ci, cn);
-#pragma unroll
-    for (int j = 0; j < VB; ++j) {
-      if (k0 + j >= s && k0 + j < e) {
-        const double p = __dmul_rn(b.a[j], xv[j]);
-        if (b.c[j] >= 0)
-          sf = __dadd_rn(sf, p);
-        else
-          sc = __dadd_rn(sc, p);
-      }
-    }
-    if (more) {
-#pragma unroll
-      for (int j = 0; j < VB; ++j) b.c[j] = cn[j];
-      b.load_vals(k0 + VB, e, nnz, v);
-    }
-    continue;
-#elif AIRG_PIPE
-    double xv[VB];
-#pragma unroll
-    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? xs(b.c[j] & 0x7fffffff) : 0.0;
+    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + (b.c[j] & 0x7fffffff)) : 0.0;
     int cc[VB];
-#pragma unroll
-    for (int j = 0; j < VB; ++j) cc[j] = b.c[j];
     double aa[VB];
 #pragma unroll
-    for (int j = 0; j < VB; ++j) aa[j] = b.a[j];
+    for (int j = 0; j < VB; ++j) {
+      cc[j] = b.c[j];
+      aa[j] = b.a[j];
+    }
     if (k0 + VB < e) b.load(k0 + VB, e, nnz, ci, v);
 #pragma unroll
     for (int j = 0; j < VB; ++j) {
@@ -324,79 +223,7 @@ __device__ __forceinline__ void dot_fc_src(int s, int e, int nnz, const int32_t*
           sc = __dadd_rn(sc, p);
       }
     }
-    continue;
-#else
-    if (k0 != k00) b.load(k0, e, nnz, ci, v);
-    double xv[VB];
-#pragma unroll
-    for (int j = 0; j < VB; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? xs(b.c[j] & 0x7fffffff) : 0.0;
-#endif
-#pragma unroll
-    for (int j = 0; j < VB; ++j) {
-      if (k0 + j >= s && k0 + j < e) {
-        const double p = __dmul_rn(b.a[j], xv[j]);
-        if (b.c[j] >= 0)
-          sf = __dadd_rn(sf, p);
-        else
-          sc = __dadd_rn(sc, p);
-      }
-    }
   }
-}
-
-template <int VB, bool VEC>
-__device__ __forceinline__ void dot_fc_prefetched(int s, int e, int nnz, const int32_t* __restrict__ ci,
-                                                  const double* __restrict__ v, const double* __restrict__ x,
-                                                  RowBatch<VB, VEC>& b, double& sf, double& sc) {
-  dot_fc_src<VB, VEC>(s, e, nnz, ci, v, XDirect{x}, b, sf, sc);
-}
-
-// ---- 16-bit column deltas (AIRG_C16): col = cbase[row] + c16[k], cbase the
-// row's first column; rows of a matrix must span < 65536 columns. 10 B per
-// entry instead of 12; the arithmetic is unchanged. Groups of 8 entries are
-// 16-byte aligned (one int4 of deltas, four double2 of values).
-struct RowBatch16 {
-  unsigned short c[8];
-  double a[8];
-  __device__ __forceinline__ void load(int k0, int e, int nnz, const uint16_t* __restrict__ c16,
-                                       const double* __restrict__ v) {
-    if (k0 + 8 <= nnz) {
-      const int4 u = __ldg(reinterpret_cast<const int4*>(c16 + k0));
-      const unsigned w[4] = {(unsigned)u.x, (unsigned)u.y, (unsigned)u.z, (unsigned)u.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        c[2 * q] = (unsigned short)(w[q] & 0xffffu);
-        c[2 * q + 1] = (unsigned short)(w[q] >> 16);
-        const double2 p = __ldg(reinterpret_cast<const double2*>(v + k0 + 2 * q));
-        a[2 * q] = p.x;
-        a[2 * q + 1] = p.y;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = k0 + j < nnz ? __ldg(c16 + k0 + j) : (unsigned short)0;
-        a[j] = k0 + j < nnz ? __ldg(v + k0 + j) : 0.0;
-      }
-    }
-    (void)e;
-  }
-};
-
-__device__ __forceinline__ double dot16(int s, int e, int base, int nnz, const uint16_t* __restrict__ c16,
-                                        const double* __restrict__ v, const double* __restrict__ x,
-                                        RowBatch16& b) {
-  double acc = 0.0;
-  const int k00 = s & ~7;
-  for (int k0 = k00; k0 < e; k0 += 8) {
-    if (k0 != k00) b.load(k0, e, nnz, c16, v);
-    double xv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) xv[j] = (k0 + j >= s && k0 + j < e) ? __ldg(x + base + b.c[j]) : 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (k0 + j >= s && k0 + j < e) acc = __dadd_rn(acc, __dmul_rn(b.a[j], xv[j]));
-  }
-  return acc;
 }
 
 }  // namespace airg

@@ -64,8 +64,6 @@ Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs
 // matrix the V-cycle streams, and the per-level vectors (fixed pointers, so
 // the V-cycle can be captured into a CUDA graph).
 void alloc_workspace(Ctx& c, Hier& h) {
-  h.tail_bar.alloc(c, 2);  // grid barrier of the coarse-tail kernel (solve.cu)
-  h.tail_bar.zero(c);
   for (size_t l = 0; l < h.levels.size(); ++l) {
     Level& L = h.levels[l];
     if (l > 0) L.b.alloc(c, (size_t)L.a.n);
@@ -73,16 +71,8 @@ void alloc_workspace(Ctx& c, Hier& h) {
     L.rf.alloc(c, (size_t)std::max(1, L.map.nf));
     L.sc.alloc(c, (size_t)std::max(1, L.map.nf));
     map_columns(c, L.aff, L.map.f_to_fine.p, L.a.n, L.affg);
-    for (Csr* m : {&L.r, &L.af, &L.affg, &L.afc, &L.ffinv}) {
-      build_tiles(c, *m);
-      if (solve_layout_sell()) build_sell(c, *m);
-    }
   }
   Csr& top = h.levels.empty() ? h.coarse_a : h.levels.front().a;
-  for (Csr* m : {&h.coarse_a, &h.coarse_inv, &top}) {
-    build_tiles(c, *m);
-    if (solve_layout_sell()) build_sell(c, *m);
-  }
   const size_t nc = (size_t)std::max(1, h.coarse_a.n);
   h.cb.alloc(c, nc);
   h.cx.alloc(c, nc);
@@ -93,7 +83,7 @@ void alloc_workspace(Ctx& c, Hier& h) {
   h.r.alloc(c, n);
   // one partial per residual block for any decomposition (tiled.cuh rows_grid:
   // up to 32 lanes per row in the group kernels)
-  h.part.alloc(c, (size_t)(kReduceBlocks + (int64_t)top.n * 32 / kTileThreads + std::max(0, top.ntiles) + 8));
+  h.part.alloc(c, (size_t)(kReduceBlocks + (int64_t)top.n * 32 / kTileThreads + 8));
   h.scal.alloc(c, 64);
 }
 

@@ -17,9 +17,7 @@
 #include <cstring>
 
 #include "hier.cuh"
-#include "sell.cuh"
 #include "tiled.cuh"
-#include "tail.cuh"
 
 namespace airg {
 
@@ -150,63 +148,10 @@ struct EpiResid {
   }
 };
 
-// AIRG_WG=4|8|16: matrices whose mean row length is >= AIRG_WG_ROWS (default
-// 12) run the long-row group kernels (wgroup.cuh) in the captured V-cycle
-inline int wg_lanes(const Csr& m) {
-  static const int g = [] {
-    const char* e = getenv("AIRG_WG");
-    const int v = e ? atoi(e) : 0;
-    return v == 4 || v == 8 || v == 16 ? v : 0;
-  }();
-  static const int64_t rows = [] {
-    const char* e = getenv("AIRG_WG_ROWS");
-    return e ? (int64_t)atoi(e) : (int64_t)12;
-  }();
-  if (!g || m.n <= 0 || m.row_mode != 1 || m.group > 1 || m.perm.p || m.c16.p) return 0;
-  return m.nnz >= rows * (int64_t)m.n ? g : 0;
-}
-
-// AIRG_W32=1: matrices whose mean row length is >= AIRG_W32_ROWS (default 12)
-// run the warp-staged product kernels (w32.cuh) in the captured V-cycle
-inline int w32_on(const Csr& m) {
-  static const bool on = [] {
-    const char* e = getenv("AIRG_W32");
-    return e && e[0] == '1';
-  }();
-  static const int64_t rows = [] {
-    const char* e = getenv("AIRG_W32_ROWS");
-    return e ? (int64_t)atoi(e) : (int64_t)12;
-  }();
-  static const int64_t rows_max = [] {
-    const char* e = getenv("AIRG_W32_MAX");
-    return e ? (int64_t)atoi(e) : (int64_t)1 << 30;
-  }();
-  if (!on || m.n <= 0 || m.row_mode != 1 || m.group > 1 || m.perm.p || m.c16.p) return 0;
-  return m.nnz >= rows * (int64_t)m.n && m.nnz < rows_max * (int64_t)m.n ? 1 : 0;
-}
-
-inline TileView tv(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, m.row_mode == 2 ? m.tiles.p : nullptr, m.ntiles, m.n, m.group, (int)m.nnz, row_vec(m.n, m.nnz), m.perm.p, m.c16.p, m.cbase.p, m.stage, wg_lanes(m), w32_on(m)};
-}
-inline SellView svw(const Csr& m) {
-  return SellView{m.s_off.p, m.s_len.p, m.s_perm.p, m.s_ci.p, m.s_v.p, m.n, m.s_nslices, m.s_g};
-}
-// solve layout: CSR row kernels (default) or SELL-32/G (AIRG_LAYOUT=sell)
-bool use_sell() { return solve_layout_sell(); }
-#define ROWS(Epi, M, x, epi)                                                          \
-  do {                                                                                \
-    if (use_sell())                                                                   \
-      LAUNCH_PDL(c, sell_rows<Epi>, sell_grid(svw(M)), 256, 0, svw(M), x, epi);       \
-    else                                                                              \
-      LAUNCH_ROWS_P(c, Epi, tv(M), x, epi);                                           \
-  } while (0)
-#define ROWS_FC(Epi, M, x, epi)                                                       \
-  do {                                                                                \
-    if (use_sell())                                                                   \
-      LAUNCH_PDL(c, sell_rows_fc<Epi>, sell_grid(svw(M)), 256, 0, svw(M), x, epi);    \
-    else                                                                              \
-      LAUNCH_ROWS_FC_P(c, Epi, tv(M), x, epi);                                        \
-  } while (0)
+// Row kernels of the solve in the configured arithmetic mode (tiled.cuh);
+// `fast` must be in scope.
+#define ROWS(Epi, M, x, epi) LAUNCH_ROWS_MODE(c, Epi, tview(M), x, epi, fast)
+#define ROWS_FC(Epi, M, x, epi) LAUNCH_ROWS_FC_MODE(c, Epi, tview(M), x, epi, fast)
 
 // x_l = 0 + P e_c  (solve.cpp:139-141: pe = spmv(P, ec); x += 1.0 * pe).
 // Four rows per thread (int4 map load, two double2 stores; the level vectors
@@ -215,18 +160,6 @@ __device__ __forceinline__ double prolong_one(int j, const double* __restrict__ 
   const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, ec[j])) : 0.0;
   return __dadd_rn(0.0, __dmul_rn(1.0, pe));
 }
-// x_l[c] without reading x_l: the prolongation of the coarse correction
-// (written two kernels back, complete before this kernel launched)
-struct XProlong {
-  const int32_t* __restrict__ pmap;
-  const double* __restrict__ ec;
-  __device__ __forceinline__ double operator()(int c) const {
-    const int j = __ldg(pmap + c);
-    const double pe = j >= 0 ? __dadd_rn(0.0, __dmul_rn(1.0, __ldg(ec + j))) : 0.0;
-    return __dadd_rn(0.0, __dmul_rn(1.0, pe));
-  }
-};
-
 __global__ void k_prolong(int n, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
                           double* __restrict__ x) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -395,227 +328,34 @@ __global__ void k_xupdate(int64_t n, int j, const double* __restrict__ Z, const 
 
 constexpr int kT = 128;
 
-// Coarse-tail kernels (tail.cuh). AIRG_TAIL=cluster runs the levels with at
-// most AIRG_TAIL_N rows (and the coarse grid) on one 16-CTA cluster;
-// AIRG_TAIL=grid on the whole GPU with a software grid barrier (measured
-// slower than PDL-chained kernels: profiles/r1_tail_ab.txt).
-struct TailCfg {
-  int mode = 0;  // 0 off, 1 cluster, 2 grid
-  int64_t rows = 0;
-};
-const TailCfg& tail_cfg() {
-  static const TailCfg v = [] {
-    TailCfg t;
-    const char* m = getenv("AIRG_TAIL");
-    const char* n = getenv("AIRG_TAIL_N");
-    t.mode = m && !strcmp(m, "grid") ? 2 : 1;
-    t.rows = n ? (int64_t)atoll(n) : (t.mode == 1 ? 0 : 0);
-    if (t.rows <= 0) t.mode = 0;
-    return t;
-  }();
-  return v;
-}
-
-// AIRG_EARLY=1: the first F residual from the coarse correction through the
-// prolongation map, concurrent with the prolongation kernel. Bit-identical,
-// but measured slower (1.31 vs 0.95 ms per C2 iteration): the extra dependent
-// map load per gathered entry costs more than the hidden prolongation.
-// AIRG_SPLIT=1: the first F residual as A_FF / A_FC dots with the C part
-// computed before the wait (overlapping the prolongation). Bit-identical;
-// measured 0.963 vs 0.952 ms per C2 iteration, so off by default.
-bool split_fres1() {
-  static const bool v = [] {
-    const char* e = getenv("AIRG_SPLIT");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-bool early_fres1() {
-  static const bool v = [] {
-    const char* e = getenv("AIRG_EARLY");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-int tail_start(const Hier& h, const airg_solve_config& cfg) {
-  const TailCfg& tc = tail_cfg();
-  const int L = (int)h.levels.size();
-  if (tc.mode == 0 || L == 0 || cfg.coarse_iterations <= 0 || h.coarse_a.n == 0) return L;
-  // phases: R + prolong + 2 per F-smooth per level, 2 per coarse iteration
-  const int64_t per_level = 2 + 2 * std::max<int64_t>(cfg.up_f_smooths, 0);
-  for (int l = 0; l < L; ++l)
-    if (h.levels[l].a.n <= tc.rows && (L - l) * per_level + 2 * cfg.coarse_iterations <= kMaxTailPhases)
-      return l;
-  return L;
-}
-
-// Build the phase list of levels Lt..L-1 + the coarse grid and launch the
-// tail kernel (cooperative: every CTA resident, one per SM).
-void enqueue_tail(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* b0, int Lt) {
-  const int L = (int)h.levels.size();
-  std::vector<TailPhase> ph;
-  auto mat = [](TailPhase& p, const Csr& m) {
-    p.n = m.n;
-    p.rp = m.rp.p;
-    p.ci = m.ci.p;
-    p.v = m.v.p;
-  };
-  for (int l = Lt; l < L; ++l) {
-    Level& lv = h.levels[l];
-    if (!lv.r.n) continue;
-    TailPhase p{};
-    p.kind = kTailStore;
-    mat(p, lv.r);
-    p.x = l == 0 ? b0 : lv.b.p;
-    p.out = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
-    ph.push_back(p);
-  }
-  const double* rhs = h.cb.p;
-  for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
-    const double* r = rhs;
-    if (it > 0) {
-      TailPhase p{};
-      p.kind = kTailCres;
-      mat(p, h.coarse_a);
-      p.x = h.cx.p;
-      p.b = rhs;
-      p.out = h.cr.p;
-      ph.push_back(p);
-      r = h.cr.p;
-    }
-    TailPhase p{};
-    p.kind = kTailCupd;
-    mat(p, h.coarse_inv);
-    p.x = r;
-    p.out = h.cx.p;
-    p.first = it == 0 ? 1 : 0;
-    ph.push_back(p);
-  }
-  for (int l = L - 1; l >= Lt; --l) {
-    Level& lv = h.levels[l];
-    const double* bl = l == 0 ? b0 : lv.b.p;
-    TailPhase p{};
-    p.kind = kTailProlong;
-    p.n = lv.a.n;
-    p.idx = lv.pmap.p;
-    p.x = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
-    p.out = lv.x.p;
-    ph.push_back(p);
-    for (int64_t s = 0; s < cfg.up_f_smooths && lv.map.nf > 0; ++s) {
-      TailPhase q{};
-      if (s == 0) {
-        q.kind = kTailFres1;
-        mat(q, lv.af);
-        q.out2 = lv.sc.p;
-      } else {
-        q.kind = kTailFres2;
-        mat(q, lv.affg);
-        q.in2 = lv.sc.p;
-      }
-      q.x = lv.x.p;
-      q.b = bl;
-      q.idx = lv.map.f_to_fine.p;
-      q.out = lv.rf.p;
-      ph.push_back(q);
-      TailPhase u{};
-      u.kind = kTailFupd;
-      mat(u, lv.ffinv);
-      u.x = lv.rf.p;
-      u.idx = lv.map.f_to_fine.p;
-      u.out = lv.x.p;
-      ph.push_back(u);
-    }
-  }
-  static TailTable table;  // host staging of the parameter block (copied at launch)
-  table.nph = (int)ph.size();
-  std::copy(ph.begin(), ph.end(), table.ph);
-  if (!h.tail_bar.p) throw RuntimeError("tail kernel: barrier words not allocated");
-  if (tail_cfg().mode == 1) {
-    static const int csize = [] {
-      CUDA_CHECK(cudaFuncSetAttribute(k_tail_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3(16);
-      q.blockDim = dim3(kTailThreads);
-      cudaLaunchAttribute qa[1];
-      qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = 16;
-      qa[0].val.clusterDim.y = 1;
-      qa[0].val.clusterDim.z = 1;
-      q.attrs = qa;
-      q.numAttrs = 1;
-      int mx = 0;
-      CUDA_CHECK(cudaOccupancyMaxPotentialClusterSize(&mx, k_tail_cluster, &q));
-      return std::max(1, std::min(16, mx));
-    }();
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)csize);
-    lc.blockDim = dim3(kTailThreads);
-    lc.stream = c.stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)csize;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    c.launches++;
-    CUDA_CHECK(cudaLaunchKernelEx(&lc, k_tail_cluster, table));
-    return;
-  }
-  static int per_sm = [] {
-    int nb = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tail, kTailThreads, 0));
-    return nb;
-  }();
-  if (per_sm < 1) throw RuntimeError("tail kernel: no resident CTA per SM");
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)c.num_sms);
-  lc.blockDim = dim3(kTailThreads);
-  lc.stream = c.stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  c.launches++;
-  CUDA_CHECK(cudaLaunchKernelEx(&lc, k_tail, table, h.tail_bar.p));
-}
-
 // Enqueue one V-cycle from level 0 rhs b0 into levels[0].x (or the coarse
 // x when there are no fine levels).
 void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* b0) {
+  const bool fast = cfg.fast != 0;
   const int L = (int)h.levels.size();
-  const int Lt = tail_start(h, cfg);
   // descent: b_{l+1} = R_l b_l
-  for (int l = 0; l < Lt; ++l) {
+  for (int l = 0; l < L; ++l) {
     Level& lv = h.levels[l];
     const double* bl = l == 0 ? b0 : lv.b.p;
     double* bn = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
-    if (lv.r.n)
-      ROWS(EpiStore, lv.r, bl, EpiStore{bn});
+    if (lv.r.n) ROWS(EpiStore, lv.r, bl, EpiStore{bn});
   }
-  if (Lt < L) {
-    enqueue_tail(c, h, cfg, b0, Lt);
-  } else {
-    // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
-    const int n = h.coarse_a.n;
-    const double* rhs = L == 0 ? b0 : h.cb.p;
-    if (n) {
-      for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
-        const double* r = rhs;
-        if (it > 0) {
-          ROWS(EpiCres, h.coarse_a, h.cx.p, (EpiCres{rhs, h.cr.p}));
-          r = h.cr.p;
-        }
-        ROWS(EpiCupd, h.coarse_inv, r, (EpiCupd{h.cx.p, it == 0 ? 1 : 0}));
+  // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
+  const int nco = h.coarse_a.n;
+  const double* rhs = L == 0 ? b0 : h.cb.p;
+  if (nco) {
+    for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
+      const double* r = rhs;
+      if (it > 0) {
+        ROWS(EpiCres, h.coarse_a, h.cx.p, (EpiCres{rhs, h.cr.p}));
+        r = h.cr.p;
       }
-      if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * n, c.stream));
+      ROWS(EpiCupd, h.coarse_inv, r, (EpiCupd{h.cx.p, it == 0 ? 1 : 0}));
     }
+    if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * nco, c.stream));
   }
   // ascent: prolongate and F-smooth
-  for (int l = std::min(L, Lt) - 1; l >= 0; --l) {
+  for (int l = L - 1; l >= 0; --l) {
     Level& lv = h.levels[l];
     const double* bl = l == 0 ? b0 : lv.b.p;
     const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
@@ -625,27 +365,10 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     else
       LAUNCH_PDL(c, k_prolong, blocks_for(n, kT), kT, 0, n, lv.pmap.p, ec, lv.x.p);
     for (int64_t s = 0; s < cfg.up_f_smooths && nf > 0; ++s) {
-      if (s == 0) {
-        const TileView v = tv(lv.af);
-        const EpiFres1 ep{bl, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p};
-        const TileView vf = tv(lv.affg), vc = tv(lv.afc);
-        if (split_fres1() && !use_sell() && !vf.tiles && vf.group <= 1 && !vc.tiles && vc.group <= 1) {
-          auto* k = vf.vec == 8   ? &rows_fres_split<EpiFres1, true, kFcVecBatch>
-                    : vf.vec == 4 ? &rows_fres_split<EpiFres1, false, 4>
-                                  : &rows_fres_split<EpiFres1, false>;
-          LAUNCH_PDL(c, k, rows_grid(vf), kTileThreads, 0, vf, vc, (const double*)lv.x.p, ec, ep);
-        } else if (early_fres1() && !use_sell() && !v.tiles && v.group <= 1) {
-          const XProlong xs{lv.pmap.p, ec};
-          auto* k = v.vec == 8   ? &rows_thread_fc_early<EpiFres1, XProlong, true, kFcVecBatch>
-                    : v.vec == 4 ? &rows_thread_fc_early<EpiFres1, XProlong, false, 4>
-                                 : &rows_thread_fc_early<EpiFres1, XProlong, false>;
-          LAUNCH_PDL(c, k, rows_grid(v), kTileThreads, 0, v, xs, ep);
-        } else {
-          ROWS_FC(EpiFres1, lv.af, lv.x.p, ep);
-        }
-      } else
-        ROWS(EpiFres2, lv.affg, lv.x.p,
-                    (EpiFres2{bl, lv.map.f_to_fine.p, lv.sc.p, lv.rf.p}));
+      if (s == 0)
+        ROWS_FC(EpiFres1, lv.af, lv.x.p, (EpiFres1{bl, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p}));
+      else
+        ROWS(EpiFres2, lv.affg, lv.x.p, (EpiFres2{bl, lv.map.f_to_fine.p, lv.sc.p, lv.rf.p}));
       ROWS(EpiFupd, lv.ffinv, lv.rf.p, (EpiFupd{lv.map.f_to_fine.p, lv.x.p}));
     }
   }
@@ -655,15 +378,15 @@ double* vcycle_output(Hier& h) { return h.levels.empty() ? h.cx.p : h.levels[0].
 
 
 // r = b - A x, ||r||^2 -> h.scal[0]
-void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double* r) {
+void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double* r, bool fast) {
   const Csr& a = h.top();
   ROWS(EpiResid, a, x, (EpiResid{b, r, h.part.p, 0.0}));
-  const int nb = use_sell() ? (int)sell_grid(svw(a)) : (int)rows_grid(tv(a));
+  const int nb = (int)rows_grid(tview(a), fast);
   LAUNCH_PDL(c, k_sum_partials, 1, 1024, 0, h.part.p, nb, h.scal.p);
 }
 
 int64_t graph_key(const airg_solve_config& cfg) {
-  return cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths;
+  return (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths) * 2 + (cfg.fast != 0);
 }
 
 // Capture `body` into a graph executable; returns the number of kernels.
@@ -752,14 +475,13 @@ void apply_polynomial(Ctx& c, Csr& a, const double* coeffs, int64_t ncoeffs, int
   if (deg > 0 && a.n != a.m) throw InvalidArgument("apply_polynomial: dimension mismatch");
   const int n = a.n;
   if (n == 0) return;
-  build_tiles(c, a);
   DBuf<double> t(c, deg > 0 ? (size_t)n : 1);
   // ping-pong so that the last step lands in d_y
   double* cur = (deg % 2 == 0) ? d_y : t.p;
   double* nxt = (deg % 2 == 0) ? t.p : d_y;
   LAUNCH(c, k_scale, blocks_for(n, 256), 256, 0, n, coeffs[deg], d_b, cur);
   for (int64_t k = deg; k-- > 0;) {
-    LAUNCH_ROWS(c, EpiHorner, tv(a), cur, (EpiHorner{d_b, coeffs[k], nxt}));
+    LAUNCH_ROWS(c, EpiHorner, tview(a), cur, (EpiHorner{d_b, coeffs[k], nxt}));
     std::swap(cur, nxt);
   }
 }
@@ -770,6 +492,7 @@ void f_smooth_level(Ctx& c, Hier& h, int64_t l, const double* d_b, double* d_x) 
   if (l < 0 || l >= (int64_t)h.levels.size()) throw InvalidArgument("f_smooth: level out of range");
   Level& lv = h.levels[(size_t)l];
   if (lv.map.nf == 0) return;
+  const bool fast = false;
   ROWS_FC(EpiFres1, lv.af, d_x, (EpiFres1{d_b, lv.map.f_to_fine.p, lv.rf.p, lv.sc.p}));
   ROWS(EpiFupd, lv.ffinv, lv.rf.p, (EpiFupd{lv.map.f_to_fine.p, d_x}));
 }
@@ -837,7 +560,7 @@ bool build_device_loop(Ctx& c, Hier& h, const airg_solve_config& cfg) {
     if (stamps) LAUNCH(c, k_stamp, 1, 32, 0, h.loop_it.p, h.loop_stamps.p, (long long)h.loop_stamps.n, 0);
     enqueue_vcycle(c, h, cfg, h.r.p);
     LAUNCH_PDL(c, k_axpy1, blocks_for(n / 2 + 1, 256), 256, 0, n, vcycle_output(h), h.xsol.p);
-    enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
+    enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p, cfg.fast != 0);
     if (stamps) LAUNCH(c, k_stamp, 1, 32, 0, h.loop_it.p, h.loop_stamps.p, (long long)h.loop_stamps.n, 1);
     LAUNCH_PDL(c, k_loop_check, 1, 32, 0, hnd, (const double*)h.scal.p, (const double*)h.loop_par.p,
                h.loop_it.p, h.loop_hist.p, (long long)h.loop_hist.n);
@@ -895,7 +618,7 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
         enqueue_vcycle(c, h, cfg, h.r.p);
         const double* e = vcycle_output(h);
         LAUNCH_PDL(c, k_axpy1, blocks_for(n / 2 + 1, 256), 256, 0, n, e, h.xsol.p);
-        enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p);
+        enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r.p, cfg.fast != 0);
       });
       h.g_key_rich = key;
     }
@@ -1078,7 +801,7 @@ void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
       }
       to_device(c, h.ybuf.p, y.data(), (size_t)j);
       LAUNCH(c, k_xupdate, blocks_for(n, 256), 256, 0, n, j, h.Z.p, h.ybuf.p, h.xsol.p);
-      enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.w.p);
+      enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.w.p, cfg.fast != 0);
       fc += 2 * (uint64_t)a.nnz + 2 * (uint64_t)n;
       beta = std::sqrt(read1(c, h.scal.p));
       const double rel = beta / bnorm;

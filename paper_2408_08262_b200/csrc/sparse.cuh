@@ -12,14 +12,11 @@ void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_
 void spmv(Ctx& c, const Csr& a, const double* x, double* y);
 void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base = 0);  // row_base: slab rows
 void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
-// tile starts for the tiled row kernels (tiled.cuh); idempotent
-void build_tiles(Ctx& c, Csr& a);
-// entries per aligned vector batch of the thread-per-row kernels (AIRG_VEC=0|4|8)
+// entries per batch of the thread-per-row kernels for a matrix of n rows and
+// nnz entries: 8 = aligned vector batches, 4 / 0 = 4- / 8-entry scalar batches
 int row_vec(int64_t n, int64_t nnz);
-// SELL-32-sigma solve copy (sell.cuh); idempotent
-void build_sell(Ctx& c, Csr& a);
-// solve layout switch: SELL only with AIRG_LAYOUT=sell (CSR rows by default)
-bool solve_layout_sell();
+// lanes per row of the fast-mode row kernels (tiled.cuh rows_lanes)
+int row_lanes(int64_t n, int64_t nnz);
 // out = a with every column j replaced by map[j] (order-preserving maps only)
 void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out);
 

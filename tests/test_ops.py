@@ -226,12 +226,12 @@ print("ok")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"AIRG_CF_CLUSTER": "100000000"}, {"AIRG_CF_SMALL": "100000000"},
-                                 {"AIRG_CF_SELCONV": "0"}, {"AIRG_CF_GROUP": "8"}],
-                         ids=["one_cluster", "one_cooperative_launch", "separate_select", "lane_groups"])
+@pytest.mark.parametrize("env", [{}, {"AIRG_CF_VEC": "1"}, {"AIRG_CF_VEC": "100000"}, {"AIRG_PDL": "0"}],
+                         ids=["default", "vector_rows", "scalar_rows", "no_pdl"])
 def test_fused_cf_split_schedules_match_oracle(env):
-    """The fused split's alternative schedules (read once per process, hence a
-    subprocess each) give the oracle's labels bit for bit."""
+    """The fused split with 16-byte / scalar row loads and without PDL (read
+    once per process, hence a subprocess each) gives the oracle's labels bit
+    for bit."""
     import os
     import subprocess
     import sys

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--what", default="solve", choices=["solve", "setup"])
     ap.add_argument("--outer", type=int, default=0, help="1 = outer GMRES(30)")
     ap.add_argument("--max-its", type=int, default=200)
+    ap.add_argument("--fast", type=int, default=0, help="1 = fast arithmetic mode (lane groups, FMA)")
     args = ap.parse_args()
     ctx = airg.Context(0)
     p = problems.make(args.config, args.scale)
@@ -38,7 +39,7 @@ def main():
     h = airg.setup(dA, ctx=ctx, **prm)
     tb = ctx.to_device(p.b)
     tx = ctx.empty(p.n, torch.float64)
-    sk = dict(coarse_iterations=prm["coarse_iterations"], outer=args.outer, max_iterations=args.max_its)
+    sk = dict(coarse_iterations=prm["coarse_iterations"], outer=args.outer, max_iterations=args.max_its, fast=args.fast)
     for _ in range(3):
         h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
