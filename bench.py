@@ -58,11 +58,26 @@ def spmv_bytes(rows, cols, nnz):
     return 12 * nnz + 4 * (rows + 1) + 8 * cols + 8 * rows
 
 
-def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2):
-    """Algorithmic HBM bytes of one V-cycle (see solve_alg_bytes)."""
+def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2, fast=False):
+    """Algorithmic HBM bytes of one V-cycle (see solve_alg_bytes). fast: the
+    fused ascent (fused.cu) -- per level R b, r1 = b_F - (A_F P) e_c and
+    x = P e_c + W r1 (W rows on the F points, the C points prolongated)."""
     info = h.info()
     per_cycle = 0
-    for l in range(info.n_levels):
+    if fast:
+        for l in range(info.n_levels):
+            lv = h.level(l)
+            n, nf, nc = lv.n, lv.n_f, lv.n_c
+            afp, wx = h.fused_nnz(l)
+            r = 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc
+            fres = 12 * afp + 4 * (nf + 1) + 8 * nc + nf * (4 + 8 + 8)
+            xw = 12 * wx + 4 * (nf + 1) + 8 * nf + n * (4 + 4 + 8) + 8 * nc
+            per_cycle += r + fres + xw
+    # exact (reference-structured) V-cycle, per level (solve.cpp:93-146): R b;
+    # the first F-smooth's residual over A's F rows (nnz_ff + nnz_fc) with x,
+    # b_F, r_F and the kept A_fc x_C; Aff^-1 r_F with the x_F update (twice);
+    # the second residual over A_ff; the one-point prolongation
+    for l in range(0 if fast else info.n_levels):
         lv = h.level(l)
         n, nf, nc = lv.n, lv.n_f, lv.n_c
         r = 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc
@@ -80,7 +95,7 @@ def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2):
     return per_cycle
 
 
-def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2):
+def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, fast=False):
     """Algorithmic HBM bytes of one GMRES(m) solve. Per Arnoldi step j (one
     outer iteration): the V-cycle (vcycle_alg_bytes), w = A z (SpMV + z
     written), classical Gram-Schmidt twice -- at least three sweeps over
@@ -91,7 +106,7 @@ def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2):
     top = h.level(0) if info.n_levels else None
     n = top.n if top else info.coarse_n
     nnz = top.nnz if top else info.coarse_nnz
-    cyc = vcycle_alg_bytes(h, coarse_iterations, up_smooths)
+    cyc = vcycle_alg_bytes(h, coarse_iterations, up_smooths, fast)
     spmv = spmv_bytes(n, n, nnz)
     tot = 8 * n  # ||b||
     left = iterations
@@ -104,37 +119,16 @@ def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2):
     return tot
 
 
-def solve_alg_bytes(h, iterations, coarse_iterations, up_smooths=2):
-    """Algorithmic HBM bytes of one solve: every operator the V-cycle applies
-    is read once per application (12 B per nonzero + 4 B per row pointer) and
-    every vector it needs is read or written once (8 B per entry, 4 B per
-    index map entry). Per level (solve.cpp:93-146): R b; the first F-smooth's
-    residual over A's F rows (A_ff and A_fc entries: nnz_ff + nnz_fc) with x,
-    b_F, r_F and the kept A_fc x_C; Aff^-1 r_F with the x_F update (twice);
-    the second residual over A_ff; the one-point prolongation. Per Richardson
-    iteration the top residual r = b - A x with its norm and x += e; the
-    coarse grid's polynomial iterations. The reference's unfused operator
-    sequence (separate gathers, A_ff / A_fc SpMVs, vector temporaries) moves
-    more; that count is reported separately (reference_op_bytes)."""
+def solve_alg_bytes(h, iterations, coarse_iterations, up_smooths=2, fast=False):
+    """Algorithmic HBM bytes of one Richardson solve: every operator the
+    V-cycle applies is read once per application (12 B per nonzero + 4 B per
+    row pointer) and every vector it needs is read or written once (8 B per
+    entry, 4 B per index map entry) -- vcycle_alg_bytes; per iteration the top
+    residual r = b - A x with its norm and x += e."""
     info = h.info()
-    per_cycle = 0
-    for l in range(info.n_levels):
-        lv = h.level(l)
-        n, nf, nc = lv.n, lv.n_f, lv.n_c
-        r = 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc
-        fres1 = 12 * (lv.nnz_ff + lv.nnz_fc) + 4 * (nf + 1) + 8 * n + nf * (4 + 8 + 8 + 8)
-        fupd = 12 * lv.nnz_ffinv + 4 * (nf + 1) + 8 * nf + nf * (4 + 16)
-        fres2 = 12 * lv.nnz_ff + 4 * (nf + 1) + 8 * nf + nf * (4 + 8 + 8 + 8)
-        prol = n * (4 + 8) + 8 * nc
-        smooths = fres1 + fupd + (up_smooths - 1) * (fres2 + fupd)
-        per_cycle += r + prol + smooths
-    cn = info.coarse_n
-    for it in range(coarse_iterations):
-        per_cycle += 12 * info.coarse_inv_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
-        if it:
-            per_cycle += 12 * info.coarse_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+    per_cycle = vcycle_alg_bytes(h, coarse_iterations, up_smooths, fast)
     top = h.level(0) if info.n_levels else None
-    n0 = top.n if top else cn
+    n0 = top.n if top else info.coarse_n
     nnz0 = top.nnz if top else info.coarse_nnz
     resid = spmv_bytes(n0, n0, nnz0) + 8 * n0  # + b
     per_iter = per_cycle + resid + 24 * n0
@@ -530,12 +524,12 @@ def time_solves(h, ctx, tb, tx, flush, steps, sk):
     return out, st
 
 
-def extra_config(ctx, cfg_idx, flush, steps=5, warmup=3):
+def extra_config(ctx, cfg_idx, flush, fast, steps=5, warmup=3):
     """A secondary single-GPU line (C2 / C3): setup + device-resident solves."""
     import torch
     from paper_2408_08262_b200 import airg, problems
     p = problems.make(cfg_idx)
-    prm = problems.setup_params(cfg_idx)
+    prm = dict(problems.setup_params(cfg_idx), fused_smooths=2 if fast else -1)
     dA = airg.DeviceCSR.upload(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), ctx)
     h = airg.setup(dA, ctx=ctx, **prm)
     del h
@@ -549,16 +543,17 @@ def extra_config(ctx, cfg_idx, flush, steps=5, warmup=3):
     with torch.cuda.stream(ctx.stream):
         tb = torch.from_numpy(p.b).to(ctx.tdev)
         tx = torch.empty(p.n, dtype=torch.float64, device=ctx.tdev)
-    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **solver_kw(cfg_idx))
+    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, fast=int(fast), **solver_kw(cfg_idx))
     for _ in range(warmup):
         h.solve_device(tb, tx, **sk)
     times, st = time_solves(h, ctx, tb, tx, flush, steps, sk)
     ms = sum(times) / len(times)
     its = int(st.iterations)
-    byts = (gmres_alg_bytes(h, its, prm["coarse_iterations"]) if sk["outer"]
-            else solve_alg_bytes(h, its, prm["coarse_iterations"]))
+    byts = (gmres_alg_bytes(h, its, prm["coarse_iterations"], fast=fast) if sk["outer"]
+            else solve_alg_bytes(h, its, prm["coarse_iterations"], fast=fast))
     peak, _ = hbm_peak()
     out = {"workload": CONFIG_NAMES[cfg_idx], "unknowns": int(p.n), "solver": solver_name(cfg_idx),
+           "mode": "fast" if fast else "exact",
            "value": p.n / (ms / 1e3), "unit": "DOF/s", "ms_per_step": ms, "steps": steps,
            "iterations": its, "final_relative_residual": float(st.final_relative_residual),
            "levels": int(h.n_levels), "setup_ms": setup_ms,
@@ -578,7 +573,9 @@ def run_gpu(args):
     ctx = airg.Context(dev)
     stream = ctx.stream
     p = problems.make(args.config, args.scale)
-    prm = problems.setup_params(args.config)
+    fast = args.mode == "fast"
+    # fast mode: the fused level operators are built inside the timed setup
+    prm = dict(problems.setup_params(args.config), fused_smooths=2 if fast else -1)
     a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
     dA = airg.DeviceCSR.upload(a, ctx)
     ev = _ev
@@ -635,7 +632,8 @@ def run_gpu(args):
         tx = torch.empty(p.n, dtype=torch.float64, device=ctx.tdev)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=ctx.tdev)
     torch.cuda.synchronize()
-    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **solver_kw(args.config))
+    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, fast=int(fast),
+              **solver_kw(args.config))
     for _ in range(args.warmup):
         st, _ = h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
@@ -667,14 +665,27 @@ def run_gpu(args):
     clk.__exit__(None, None, None)  # clocks sampled across the device and e2e timed loops
     e2e_ms = sum(e2e_times) / len(e2e_times)
     e2e_value = p.n / (e2e_ms / 1e3)
+    # the other arithmetic mode on the same hierarchy (exact = the reference's bits)
+    other = {}
+    try:
+        ok = dict(sk, fast=0 if fast else 1)
+        for _ in range(2):
+            h.solve_device(tb, tx, **ok)
+        ot, ost = time_solves(h, ctx, tb, tx, flush, 3, ok)
+        oms = sum(ot) / len(ot)
+        other = {"mode": "exact" if fast else "fast", "value": p.n / (oms / 1e3), "unit": "DOF/s",
+                 "ms_per_step": oms, "iterations": int(ost.iterations),
+                 "final_relative_residual": float(ost.final_relative_residual)}
+    except Exception as exc:
+        other = {"error": str(exc)[:200]}
 
     # ---- roofline. The unit is the whole solve step ("per
     # V-cycle and per solve: sum over every SpMV and vector op"): no single
     # kernel owns more than ~15% of it (profiles/). The level-0 SpMV (the
     # reference's top hot spot, sparse.cpp:185-201) is reported beside it.
     its = int(st.iterations)
-    step_bytes = (gmres_alg_bytes(h, its, prm["coarse_iterations"]) if sk["outer"]
-                  else solve_alg_bytes(h, its, prm["coarse_iterations"]))
+    step_bytes = (gmres_alg_bytes(h, its, prm["coarse_iterations"], fast=fast) if sk["outer"]
+                  else solve_alg_bytes(h, its, prm["coarse_iterations"], fast=fast))
     peak, peak_kind = hbm_peak()
     step_achieved = step_bytes / (ms_per_step / 1e3) / 1e9
     A0 = h.matrix_handle(0, 0) if info.n_levels else dA
@@ -720,7 +731,7 @@ def run_gpu(args):
             if c == args.config:
                 continue
             try:
-                extras[f"C{c}"] = extra_config(ctx, c, flush)
+                extras[f"C{c}"] = extra_config(ctx, c, flush, fast)
             except Exception as exc:  # keep the headline line
                 extras[f"C{c}"] = {"error": str(exc)[:200]}
 
@@ -735,8 +746,9 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, p, "single GPU"),
+        "config": dict(config_dict(args, p, "single GPU"), mode=args.mode),
         "iterations": its, "final_relative_residual": float(rel),
+        "other_mode": other,
         "levels": int(info.n_levels), "operator_complexity": info.operator_complexity,
         "setup_ms": setup_ms, "cf_split_ms": cf_ms, "cf_split_ms_sync_each_level": cf_ms_each,
         "cf_split_roofline": {"bound": "hbm", "achieved": cf_bytes / (cf_ms / 1e3) / 1e9, "peak": peak,
@@ -776,6 +788,9 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the C2 / C3 secondary lines")
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"],
+                    help="solve arithmetic: fast (lane groups, FMA, fused level operators; within the parity "
+                         "tolerance) or exact (the reference's bits)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the distributed (NCCL row-slab) path even on one rank")

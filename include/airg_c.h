@@ -63,6 +63,9 @@ typedef struct airg_setup_config {
   int32_t prolongation;       /* 0 = one-point (1 = ideal: test hook, EINVAL on GPU) */
   int32_t weight_mode;        /* 0 = |S|+|S^T|, 1 = |S u S^T| */
   uint64_t seed;              /* 0 */
+  int32_t fused_smooths;      /* -1 = build the fast V-cycle's fused level operators on the first
+                                 fast solve; k >= 0 = build them at setup for k F-smooths */
+  int32_t _pad;
 } airg_setup_config;
 
 /* Mirrors airgraph::SolveConfig (solve.hpp:11-19) plus the outer solver
@@ -301,7 +304,8 @@ int airg_dist_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* c
 int airg_hier_info_get(const airg_hier* h, airg_hier_info* info);
 int airg_hier_level_info(const airg_hier* h, int64_t level,
                          airg_level_info* info);
-/* which: 0 A, 1 A_ff, 2 A_fc, 3 A_cf, 4 Aff_inv, 5 R, 6 P; level ==
+/* which: 0 A, 1 A_ff, 2 A_fc, 3 A_cf, 4 Aff_inv, 5 R, 6 P, and (fast V-cycle,
+ * once built) 7 A_F P (n_f x n_c), 8 W_k (n_f x n_f); level ==
  * n_levels with which 0 / 4 gives the coarse A / coarse inverse. Returns a
  * borrowed handle owned by the hierarchy. */
 int airg_hier_matrix(const airg_hier* h, int64_t level, int32_t which,

@@ -28,6 +28,8 @@ class SetupConfig(C.Structure):
         ("prolongation", C.c_int32),
         ("weight_mode", C.c_int32),
         ("seed", C.c_uint64),
+        ("fused_smooths", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 
@@ -119,7 +121,7 @@ SETUP_DEFAULTS = dict(
     strength_alpha=0.5, cf=0, ddc_enabled=1, ddc_fraction=0.10, ddc_bins=1000,
     max_loops=3, poly_order=6, sparsity_order=1, drop_coarse=0.001,
     drop_restrict=0.01, coarse_size_target=3000, coarse_poly_order=12,
-    coarse_iterations=3, max_levels=0, prolongation=0, weight_mode=0, seed=0)
+    coarse_iterations=3, max_levels=0, prolongation=0, weight_mode=0, seed=0, fused_smooths=-1, _pad=0)
 
 SOLVE_DEFAULTS = dict(
     rtol=1e-10, max_iterations=200, up_f_smooths=2, down_smooths=0,

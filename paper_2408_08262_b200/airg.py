@@ -606,7 +606,7 @@ def assemble_fixed_sparsity(a, coeffs, effective_order: int, sparsity_order: int
 
 
 # ---- L2 / L3 (air.hpp, solve.hpp) ------------------------------------------------------
-MATRICES = {"a": 0, "a_ff": 1, "a_fc": 2, "a_cf": 3, "ff_inv": 4, "r": 5, "p": 6}
+MATRICES = {"a": 0, "a_ff": 1, "a_fc": 2, "a_cf": 3, "ff_inv": 4, "r": 5, "p": 6, "afp": 7, "w": 8}
 
 
 class Hierarchy:
@@ -645,6 +645,10 @@ class Hierarchy:
         out = _VP()
         _check(lib().airg_hier_matrix(self.h, int(l), w, C.byref(out)))
         return DeviceCSR(self.ctx, out, owned=False, keep=self).download()
+
+    def fused_nnz(self, l: int) -> tuple[int, int]:
+        """(nnz of A_F P, nnz of W) of the fast V-cycle's fused operators."""
+        return (self.matrix_handle(l, 7).dims()[2], self.matrix_handle(l, 8).dims()[2])
 
     def matrix_handle(self, l: int, which) -> DeviceCSR:
         """Borrowed device handle of a level matrix (no copy)."""

@@ -87,6 +87,8 @@ void airg_setup_config_default(airg_setup_config* c) {
   c->prolongation = 0;
   c->weight_mode = 0;
   c->seed = 0;
+  c->fused_smooths = -1;
+  c->_pad = 0;
 }
 
 void airg_solve_config_default(airg_solve_config* c) {
@@ -763,8 +765,10 @@ int airg_hier_matrix(const airg_hier* hp, int64_t l, int32_t which, const airg_c
     } else {
       if (l < 0 || l > nl) throw InvalidArgument("level out of range");
       const Level& L = h->h.levels[l];
-      const Csr* ms[7] = {&L.a, &L.aff, &L.afc, &L.acf, &L.ffinv, &L.r, &L.p};
-      if (which < 0 || which > 6) throw InvalidArgument("bad matrix selector");
+      const Csr* ms[9] = {&L.a, &L.aff, &L.afc, &L.acf, &L.ffinv, &L.r, &L.p, &L.afp, &L.fw};
+      if (which < 0 || which > 8) throw InvalidArgument("bad matrix selector");
+      if (which >= 7 && h->h.fused_smooths < 0)
+        throw InvalidArgument("fast V-cycle operators not built (setup fused_smooths >= 0 or a fast solve)");
       m = ms[which];
     }
     // borrowed view: a handle whose Csr aliases the hierarchy's buffers

@@ -14,6 +14,7 @@ struct Level {
   Csr affg;                  // A_FF with global column indices (later F-smooths)
   Csr ffinv, r, p;
   DBuf<int32_t> pmap;        // one-point P as a map (-1 = empty row)
+  Csr afp, fw;               // fast V-cycle (fused.cu): A_F P (n_f x n_c) and W_k (n_f x n_f)
   // report
   int64_t n_f_pre = 0, n_converted = 0, attempts = 1, eff = 0;
   double max_theta_pre = 0.0, alpha_diag = 0.0, max_theta_post = 0.0, growth = 0.0;
@@ -33,6 +34,7 @@ struct Hier {
   double coarse_growth = 0.0;
   int64_t coarse_iterations = 3;  // SetupConfig (storage metric only)
   double grid_c = 0.0, op_c = 0.0, store_c = 0.0;
+  int64_t fused_smooths = -1;  // up_f_smooths the fused operators were built for (-1: none)
   // coarse workspace
   DBuf<double> cb, cx, cr;
   // top-level solve workspace
@@ -75,6 +77,9 @@ struct RowSplit;
 void setup(Ctx& c, const Csr& a, const airg_setup_config& cfg, const Injection* inj, Hier& h,
            const RowSplit* rs = nullptr);
 void recompute_metrics(Hier& h);
+
+// fused.cu: the fast V-cycle's fused level operators for `smooths` F-smooths
+void build_fused(Ctx& c, Hier& h, int64_t smooths);
 
 // solve.cu
 void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x);

@@ -250,6 +250,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
   h.coarse_growth = coarse.growth;
   recompute_metrics(h);
   alloc_workspace(c, h);
+  if (cfg.fused_smooths >= 0) build_fused(c, h, cfg.fused_smooths);
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 

@@ -148,6 +148,75 @@ struct EpiResid {
   }
 };
 
+// fast V-cycle, fused ascent (fused.cu): r1 = b_F - (A_F P) e_c
+struct EpiFres1P {
+  const double* b;
+  const int32_t* f2f;
+  double* rf;
+  __device__ void row(int k, double acc) const { rf[k] = b[__ldg(f2f + k)] - acc; }
+  __device__ void finish() const {}
+  struct Pre {  // b_l from the descent
+    double bb;
+  };
+  __device__ Pre pre(int k) const { return Pre{b[__ldg(f2f + k)]}; }
+  __device__ void row_pre(int k, double acc, const Pre& p) const { rf[k] = p.bb - acc; }
+};
+// x_l = P e_c + [W r1 on the F rows] in one launch: blocks [0, bf) are lane
+// groups over W's n_f rows, the rest one thread per C point (prolongation
+// only). e_c was written two kernels back (the coarser level's pass), so the
+// prolongated values are loaded before the dependency wait.
+template <int G>
+__global__ void __launch_bounds__(kTileThreads)
+k_fused_x(TileView w, int bf, const double* __restrict__ rf, const int32_t* __restrict__ f2f,
+          const int32_t* __restrict__ c2f, int nc, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
+          double* __restrict__ x) {
+  if ((int)blockIdx.x < bf) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = t / G, lane = t & (G - 1);
+    const bool live = r < w.nrows;
+    LaneRow<G, false> row;
+    int i = 0;
+    double pe = 0.0;
+    if (live) {
+      row.load(w, r, lane);
+      if (lane == 0) {
+        i = __ldg(f2f + r);
+        const int j = __ldg(pmap + i);
+        pe = j >= 0 ? ec[j] : 0.0;
+      }
+    }
+    pdl_wait();
+    pdl_trigger();
+    double sf = 0.0, sc;
+    if (live) row.dot(w, rf, lane, sf, sc);
+    sf = group_sum<G>(sf);
+    if (live && lane == 0) x[i] = pe + sf;
+  } else {
+    const int k = ((int)blockIdx.x - bf) * blockDim.x + threadIdx.x;
+    int i = 0;
+    double pe = 0.0;
+    if (k < nc) {
+      i = __ldg(c2f + k);
+      const int j = __ldg(pmap + i);
+      pe = j >= 0 ? ec[j] : 0.0;
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (k < nc) x[i] = pe;
+  }
+}
+
+void launch_fused_x(Ctx& c, const Level& lv, const double* ec) {
+  const TileView w = tview(lv.fw);
+  const int G = w.lanes;
+  const int bf = (int)(((int64_t)w.nrows * G + kTileThreads - 1) / kTileThreads);
+  const int bc = (lv.map.nc + kTileThreads - 1) / kTileThreads;
+  auto* k = G == 1 ? &k_fused_x<1> : G == 2 ? &k_fused_x<2> : G == 4 ? &k_fused_x<4> : G == 8 ? &k_fused_x<8>
+                                                                                        : &k_fused_x<16>;
+  LAUNCH_PDL(c, k, (unsigned)std::max(1, bf + bc), kTileThreads, 0, w, bf, (const double*)lv.rf.p,
+             lv.map.f_to_fine.p, lv.map.c_to_fine.p, (int)lv.map.nc, lv.pmap.p, ec, lv.x.p);
+}
+
 // Row kernels of the solve in the configured arithmetic mode (tiled.cuh);
 // `fast` must be in scope.
 #define ROWS(Epi, M, x, epi) LAUNCH_ROWS_MODE(c, Epi, tview(M), x, epi, fast)
@@ -354,6 +423,18 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     }
     if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * nco, c.stream));
   }
+  // ascent, fast fused form: two row passes per level (fused.cu)
+  if (fast && h.fused_smooths == cfg.up_f_smooths) {
+    for (int l = L - 1; l >= 0; --l) {
+      Level& lv = h.levels[l];
+      const double* bl = l == 0 ? b0 : lv.b.p;
+      const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
+      if (cfg.up_f_smooths > 0 && lv.map.nf > 0)
+        ROWS(EpiFres1P, lv.afp, ec, (EpiFres1P{bl, lv.map.f_to_fine.p, lv.rf.p}));
+      launch_fused_x(c, lv, ec);
+    }
+    return;
+  }
   // ascent: prolongate and F-smooth
   for (int l = L - 1; l >= 0; --l) {
     Level& lv = h.levels[l];
@@ -385,8 +466,10 @@ void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double*
   LAUNCH_PDL(c, k_sum_partials, 1, 1024, 0, h.part.p, nb, h.scal.p);
 }
 
-int64_t graph_key(const airg_solve_config& cfg) {
-  return (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths) * 2 + (cfg.fast != 0);
+int64_t graph_key(const Hier& h, const airg_solve_config& cfg) {
+  const int fused = cfg.fast != 0 && h.fused_smooths == cfg.up_f_smooths;
+  return (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths) * 4 + (cfg.fast != 0) * 2 +
+         fused;
 }
 
 // Capture `body` into a graph executable; returns the number of kernels.
@@ -499,9 +582,10 @@ void f_smooth_level(Ctx& c, Hier& h, int64_t l, const double* d_b, double* d_x) 
 
 void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x) {
   check_cfg(cfg);
+  if (cfg.fast && h.fused_smooths != cfg.up_f_smooths) build_fused(c, h, cfg.up_f_smooths);
   const int n = h.top_n();
   CUDA_CHECK(cudaMemcpyAsync(h.r.p, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
-  const int64_t key = graph_key(cfg);
+  const int64_t key = graph_key(h, cfg);
   if (!h.g_vc || h.g_key_vc != key) {
     h.g_vc_kernels = capture(c, &h.g_vc, [&] { enqueue_vcycle(c, h, cfg, h.r.p); });
     h.g_key_vc = key;
@@ -520,7 +604,7 @@ namespace {
 // host round trip between iterations. Returns false when the driver refuses
 // the conditional graph (the caller then runs the host loop).
 bool build_device_loop(Ctx& c, Hier& h, const airg_solve_config& cfg) {
-  const int64_t key = graph_key(cfg);
+  const int64_t key = graph_key(h, cfg);
   if (h.g_loop && h.g_key_loop == key) return true;
   if (h.g_loop) {
     cudaGraphExecDestroy(h.g_loop);
@@ -612,7 +696,7 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
     st.converged = 1;
     hist.push_back(0.0);
   } else {
-    const int64_t key = graph_key(cfg);
+    const int64_t key = graph_key(h, cfg);
     if (!h.g_rich || h.g_key_rich != key) {
       h.g_rich_kernels = capture(c, &h.g_rich, [&] {
         enqueue_vcycle(c, h, cfg, h.r.p);
@@ -732,7 +816,7 @@ void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
     hist.push_back(0.0);
     st.final_relative_residual = 0.0;
   } else {
-    const int64_t key = graph_key(cfg);
+    const int64_t key = graph_key(h, cfg);
     if (!h.g_vc || h.g_key_vc != key) {
       h.g_vc_kernels = capture(c, &h.g_vc, [&] { enqueue_vcycle(c, h, cfg, h.r.p); });
       h.g_key_vc = key;
@@ -827,6 +911,7 @@ void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
 void solve(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x,
            airg_solve_stats& st, std::vector<double>& history) {
   check_cfg(cfg);
+  if (cfg.fast && h.fused_smooths != cfg.up_f_smooths) build_fused(c, h, cfg.up_f_smooths);
   std::memset(&st, 0, sizeof st);
   const int n = h.top_n();
   CUDA_CHECK(cudaMemcpyAsync(h.rhs.p, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));

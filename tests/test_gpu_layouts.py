@@ -120,3 +120,24 @@ def test_cf_split_variants_bit_identical():
     for name, env in CF_VARIANTS.items():
         if name != "legacy":
             assert _run(CF_SCRIPT, env, keys) == base, f"CF variant {name} differs from the step-by-step split"
+
+
+def test_fused_operators_match_products():
+    """The fast V-cycle's fused level operators (fused.cu) against scipy
+    products of the hierarchy's own matrices: A_F P and W_2 = 2Q - Q A_ff Q."""
+    import scipy.sparse as sp
+    p = problems.make(4, 0.25)
+    prm = dict(problems.setup_params(4), coarse_size_target=300, fused_smooths=2)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+
+    def csr(m):
+        return sp.csr_matrix((m.values, m.col_indices, m.row_offsets), shape=(m.nrows, m.ncols))
+    for l in range(h.n_levels):
+        A, P, Q, Aff = (csr(h.matrix(l, w)) for w in ("a", "p", "ff_inv", "a_ff"))
+        lab = h.labels(l)
+        f = np.flatnonzero(lab == 0)
+        afp = csr(h.matrix(l, "afp")).toarray()
+        np.testing.assert_allclose(afp, (A[f] @ P).toarray(), rtol=1e-13, atol=1e-14 * abs(A).max())
+        fw = csr(h.matrix(l, "w")).toarray()
+        W = (2 * Q - Q @ Aff @ Q).toarray()
+        np.testing.assert_allclose(fw, W, rtol=1e-12, atol=1e-13 * max(1.0, abs(W).max()))

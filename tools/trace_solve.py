@@ -84,7 +84,8 @@ def main():
         # L-1..0: prolong, fres1, fupd, fres2, fupd, ..., then axpy, resid, sum)
         L = h.n_levels
         nco = 2 * prm["coarse_iterations"] - 1
-        per_it = L + nco + L * (1 + 2 * 2) + 3
+        per_lvl = 2 if args.fast else 1 + 2 * 2
+        per_it = L + nco + L * per_lvl + 3
         if any("k_loop_check" in e["name"] for e in ev):
             per_it += 1  # device-side convergence test (AIRG_DEVLOOP)
         first = 2  # dot_partials, reduce_partials (bnorm)
@@ -94,7 +95,19 @@ def main():
                      f"{seq[-1]['ts'] + seq[-1]['dur'] - seq[0]['ts']:.1f} us")
         lines.append(f"{'lvl':>3} {'n':>8} {'nnzR':>9} {'R us':>7} {'GB/s':>6} | {'nnzAF':>9} {'fres1':>7} {'GB/s':>6}"
                      f" | {'nnzFF':>8} {'fres2':>6} | {'nnzQ':>8} {'fupd':>6} {'GB/s':>6} | {'prol':>5}")
-        asc = seq[L + nco: L + nco + 5 * L]
+        asc = seq[L + nco: L + nco + per_lvl * L]
+        if args.fast:
+            lines[-1] = lines[-1] + "  (fast fused: per level R | A_F P residual | W x-update)"
+            lines.append(f"{'lvl':>3} {'n':>8} {'nnzR':>9} {'R us':>7} | {'nnzAFP':>9} {'fres':>6} {'GB/s':>6} | {'nnzWX':>9} {'xw':>6} {'GB/s':>6}")
+            for l in range(L):
+                info = h.level(l)
+                blk = asc[(L - 1 - l) * 2:(L - l) * 2]
+                af, wx = h.fused_nnz(l)
+                bf = 12 * af + 4 * info.n_f + 8 * info.n_c + 8 * info.n_f + 8 * info.n_f
+                bw = 12 * wx + 4 * info.n_f + 8 * info.n_f + 24 * info.n
+                lines.append(f"{l:3d} {info.n:8d} {info.nnz_r:9d} {seq[l]['marg']:7.1f} | {af:9d} {blk[0]['marg']:6.1f} "
+                             f"{bf / blk[0]['marg'] / 1e3:6.0f} | {wx:9d} {blk[1]['marg']:6.1f} {bw / blk[1]['marg'] / 1e3:6.0f}")
+            L = 0
         for l in range(L):
             info = h.level(l)
             r_us = seq[l]["marg"]
