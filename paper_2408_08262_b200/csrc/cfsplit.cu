@@ -794,14 +794,6 @@ int cf_vec_rows() {
   return v;
 }
 
-// The PMISR weight of row j (coarsening.cpp:50-63): |S_j| + |S^T_j| plus
-// the seeded hash fraction, rebuilt from the counts wherever it is needed
-// (no weight array, no weight pass). cnt[j] = {|S_j|, |S^T_j|}.
-__device__ __forceinline__ double fcf_weight(const int2* __restrict__ cnt, uint64_t key, int j) {
-  const int2 c = cnt[j];
-  const double u = (double)(mix(key, (uint64_t)j) >> 11) * 0x1.0p-53;
-  return __dadd_rn((double)((int64_t)c.x + c.y), u);
-}
 
 // Labels without a label pass: a row with no strong connection (weight < 1)
 // is never marked "not minimal", so the PMISR label is F exactly when

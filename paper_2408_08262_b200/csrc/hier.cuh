@@ -26,6 +26,17 @@ struct Level {
   DBuf<double> sc;           // A_FC x_C kept from the first F-smooth
 };
 
+struct GmDev {
+  long long its;    // Arnoldi steps so far
+  long long cap;    // history capacity
+  long long maxit;  // max_iterations
+  int j;            // column of the current cycle
+  int m;            // restart length
+  int converged;
+  int restarts;
+  double rtol, bnorm, beta, hn, rel, est;
+};
+
 struct Hier {
   std::vector<Level> levels;
   Csr coarse_a, coarse_inv;
@@ -42,6 +53,14 @@ struct Hier {
   // outer GMRES workspace (allocated on first use)
   int64_t gm_restart = 0;
   DBuf<double> V, Z, w, hbuf, ybuf;
+  // device-resident GMRES (solve.cu): state, Hessenberg / rotation scalars,
+  // dot partials, history, the cycle residual and the nested-WHILE graph
+  DBuf<GmDev> gm_st;
+  DBuf<double> gm_H, gm_cs, gm_sn, gm_g, gm_y, gm_h, gm_part, gm_hist, r2;
+  cudaGraphExec_t g_gm = nullptr;
+  int64_t g_key_gm = -1;
+  uint64_t gm_kernels[3] = {0, 0, 0};  // launch, per cycle, per Arnoldi step
+  bool gm_broken = false;
   // device-side Richardson loop (solve.cu): iteration count, residual
   // history, [rtol, max_iterations] and the conditional-WHILE graph
   DBuf<long long> loop_it;
@@ -61,6 +80,7 @@ struct Hier {
     if (g_rich) cudaGraphExecDestroy(g_rich);
     if (g_vc) cudaGraphExecDestroy(g_vc);
     if (g_loop) cudaGraphExecDestroy(g_loop);
+    if (g_gm) cudaGraphExecDestroy(g_gm);
   }
 };
 

@@ -31,10 +31,6 @@ struct EpiFres1 {
   const int32_t* f2f;
   double* rf;
   double* sc_keep;
-  __device__ void row2(int k, double sf, double sc) const {
-    sc_keep[k] = sc;
-    rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc);
-  }
   // b_l comes from the descent (long complete): prefetched before the wait
   struct Pre {
     double bb;
@@ -51,9 +47,6 @@ struct EpiFres2 {
   const int32_t* f2f;
   const double* sc_keep;
   double* rf;
-  __device__ void row(int k, double sf) const {
-    rf[k] = __dsub_rn(__dsub_rn(__ldg(b + __ldg(f2f + k)), sf), sc_keep[k]);
-  }
   __device__ void finish() const {}
   // b_l and A_FC x_C (from the first residual, three kernels back)
   struct Pre {
@@ -68,10 +61,6 @@ struct EpiFres2 {
 struct EpiFupd {
   const int32_t* f2f;
   double* x;
-  __device__ void row(int k, double d) const {
-    const int i = __ldg(f2f + k);
-    x[i] = __dadd_rn(x[i], d);
-  }
   __device__ void finish() const {}
   // x_F was last written two kernels back (prolongation or the previous
   // update; the residual in between only reads it)
@@ -89,7 +78,6 @@ struct EpiFupd {
 struct EpiCres {
   const double* rhs;
   double* r;
-  __device__ void row(int i, double acc) const { r[i] = __dsub_rn(rhs[i], acc); }
   __device__ void finish() const {}
   struct Pre {  // the coarse rhs comes from the descent, >= 2 kernels back
     double rr;
@@ -101,10 +89,6 @@ struct EpiCres {
 struct EpiCupd {
   double* e;
   int first;
-  __device__ void row(int i, double acc) const {
-    const double e0 = first ? 0.0 : e[i];
-    e[i] = __dadd_rn(e0, __dmul_rn(1.0, acc));
-  }
   __device__ void finish() const {}
   struct Pre {  // e from the previous update, two kernels back (a residual between)
     double e0;
@@ -118,11 +102,6 @@ struct EpiResid {
   double* r;
   double* part;
   mutable double s;
-  __device__ void row(int i, double acc) const {
-    const double ri = __dsub_rn(b[i], acc);
-    r[i] = ri;
-    s = fma(ri, ri, s);
-  }
   struct Pre {  // the right-hand side is constant during the solve
     double bb;
   };
@@ -153,7 +132,6 @@ struct EpiFres1P {
   const double* b;
   const int32_t* f2f;
   double* rf;
-  __device__ void row(int k, double acc) const { rf[k] = b[__ldg(f2f + k)] - acc; }
   __device__ void finish() const {}
   struct Pre {  // b_l from the descent
     double bb;
@@ -783,6 +761,537 @@ void richardson(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats&
   st.solve_seconds = std::chrono::duration<double>(t1 - t0).count();
 }
 
+// ---- device-resident GMRES ---------------------------------------------------
+// The whole solve is ONE graph launch: an outer conditional WHILE over restart
+// cycles whose body holds an inner WHILE over Arnoldi steps. Every scalar of
+// the method (Hessenberg column, Givens rotations, g, y, the stopping tests)
+// lives on the device; one readback at the end. One Arnoldi step:
+//   z = M v_j (the captured V-cycle), w = A z with Z_j = z stored by the SpMV,
+//   CGS2 in three sweeps over V_0..V_j (dots; update fused with the second
+//   dots; update fused with the norm), the Givens step (one thread), and
+//   v_{j+1} = w / h_{j+1,j}.
+// The same steps, in the same order, as the host-driven gmres() below and the
+// serial restatement (oracle/airg_oracle.c); reductions are parallel trees.
+constexpr int kGmMax = 32;      // restart lengths served on the device (m <= 32)
+constexpr int kGmThreads = 256;
+
+
+// Sum 32 per-lane vectors over the warp: butterfly transpose-reduce, 31
+// shuffles instead of 32 x 5; on return lane l holds the total of entry l.
+__device__ __forceinline__ double warp_transpose_sum32(double (&v)[kGmMax]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = lane & s;
+#pragma unroll
+    for (int t = 0; t < s; ++t) {
+      const double send = up ? v[t] : v[t + s];
+      const double keep = up ? v[t + s] : v[t];
+      v[t] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+// One element per thread (a grid of n / 256 blocks: enough independent
+// loads in flight to cover the HBM latency); V_0..V_j of the element in
+// registers, so the update and the following dots read V once; the dots of
+// a warp reduced by one transpose-reduce (31 shuffles for all k).
+// MODE 0: dots V_k . w;  1: w -= V h, then dots V_k . w;  2: w -= V h, then |w|^2.
+// Per block, one partial per k: part[k * nblocks + block].
+template <int MODE>
+__global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double* __restrict__ V,
+                                                         double* __restrict__ w, const GmDev* __restrict__ st,
+                                                         const double* __restrict__ h, double* __restrict__ part) {
+  __shared__ double hs[kGmMax];
+  __shared__ double red[kGmThreads / 32][kGmMax];
+  pdl_wait();
+  pdl_trigger();
+  const int jp1 = st->j + 1;
+  if (threadIdx.x < kGmMax) hs[threadIdx.x] = (MODE > 0 && (int)threadIdx.x < jp1) ? h[threadIdx.x] : 0.0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kGmThreads + threadIdx.x;
+  const bool live = i < n;
+  double vk[kGmMax];
+#pragma unroll
+  for (int k = 0; k < kGmMax; ++k) vk[k] = (live && k < jp1) ? __ldg(V + (int64_t)k * n + i) : 0.0;
+  double wi = live ? w[i] : 0.0;
+  if (MODE > 0) {
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k) wi = fma(-hs[k], vk[k], wi);
+    if (live) w[i] = wi;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (MODE < 2) {
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k) vk[k] *= wi;
+    red[warp][lane] = warp_transpose_sum32(vk);
+  } else {
+    double p = wi * wi;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+    if (lane == 0) red[warp][0] = p;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < (MODE < 2 ? jp1 : 1)) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kGmThreads / 32; ++q) v += red[q][threadIdx.x];
+    part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+// h[k] = sum over blocks of part[k][.] (k <= j, or k = 0 for the norm):
+// one 1024-thread block per k, eight independent partial loads per thread
+// in flight, a fixed reduction tree (deterministic)
+constexpr int kFinThreads = 1024;
+__global__ void __launch_bounds__(kFinThreads) k_gm_finish(const double* __restrict__ part, int nb,
+                                                           const GmDev* __restrict__ st, int norm,
+                                                           double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int k = blockIdx.x;
+  if (k > (norm ? 0 : st->j)) return;
+  __shared__ double sm[32];
+  const double* p = part + (int64_t)k * nb;
+  double s = 0.0;
+  for (int b0 = threadIdx.x; b0 < nb; b0 += 8 * kFinThreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + u * kFinThreads;
+      v[u] = b < nb ? __ldg(p + b) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = sm[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[k] = s;
+  }
+}
+
+// w = A z and Z_j = z (z = the V-cycle output; j from the device state)
+struct EpiGmSpmv {
+  double* w;
+  const double* z;
+  double* Z;
+  const GmDev* st;
+  int64_t n;
+  __device__ void row(int i, double acc) const {
+    w[i] = acc;
+    Z[(int64_t)st->j * n + i] = z[i];
+  }
+  __device__ void finish() const {}
+};
+
+// ||b||, the first cycle's start (x = 0, r = b, beta = ||b||)
+__global__ void k_gm_init(cudaGraphConditionalHandle hout, int cond, const double* __restrict__ bb, GmDev* st,
+                          double* __restrict__ hist) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  const double bnorm = sqrt(*bb);
+  st->bnorm = bnorm;
+  st->beta = bnorm;
+  st->its = 0;
+  st->j = 0;
+  st->restarts = 0;
+  st->converged = bnorm == 0.0;
+  st->rel = bnorm == 0.0 ? 0.0 : 1.0;
+  if (st->cap > 0) hist[0] = bnorm == 0.0 ? 0.0 : 1.0;
+  if (cond) cudaGraphSetConditional(hout, (bnorm != 0.0 && st->maxit > 0) ? 1u : 0u);
+}
+
+// cycle start: v_0 = r / beta (into V_0 and the V-cycle input), g = beta e_1
+__global__ void k_gm_cycle(cudaGraphConditionalHandle hin, int cond, int64_t n, const double* __restrict__ r, GmDev* st,
+                           double* __restrict__ V, double* __restrict__ vin, double* __restrict__ g) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r[i] / st->beta;
+    V[i] = v;
+    vin[i] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x <= st->m) g[threadIdx.x] = threadIdx.x == 0 ? st->beta : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->j = 0;
+    if (cond) cudaGraphSetConditional(hin, st->its < st->maxit ? 1u : 0u);
+  }
+}
+
+// the Arnoldi step's scalar work (gmres_poly-free, oracle gmres() order):
+// hcol = h1 + h2, h_{j+1,j} = |w|, previous rotations, the new rotation, g,
+// the history, and the inner-loop test
+__global__ void k_gm_step(cudaGraphConditionalHandle hin, int cond, GmDev* st, const double* __restrict__ h1,
+                          const double* __restrict__ h2, const double* __restrict__ nrm2, double* __restrict__ H,
+                          double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ g,
+                          double* __restrict__ hist) {
+  __shared__ double hcol[kGmMax + 1], c_s[kGmMax], s_s[kGmMax];
+  pdl_wait();
+  pdl_trigger();
+  const int j = st->j, m = st->m, t = threadIdx.x;
+  if (t <= j) hcol[t] = h1[t] + h2[t];  // operands staged by the warp
+  if (t < j) {
+    c_s[t] = cs[t];
+    s_s[t] = sn[t];
+  }
+  __syncwarp();
+  if (t != 0) return;
+  const double hn = sqrt(*nrm2);
+  hcol[j + 1] = hn;
+  for (int k = 0; k < j; ++k) {
+    const double a = c_s[k] * hcol[k] + s_s[k] * hcol[k + 1];
+    hcol[k + 1] = -s_s[k] * hcol[k] + c_s[k] * hcol[k + 1];
+    hcol[k] = a;
+  }
+  const double den = hypot(hcol[j], hcol[j + 1]);
+  const double cj = den > 0.0 ? hcol[j] / den : 1.0;
+  const double sj = den > 0.0 ? hcol[j + 1] / den : 0.0;
+  cs[j] = cj;
+  sn[j] = sj;
+  hcol[j] = den;
+  const double gj = g[j];
+  g[j + 1] = -sj * gj;
+  g[j] = cj * gj;
+  for (int k = 0; k <= j; ++k) H[k + (int64_t)j * (m + 1)] = hcol[k];
+  const long long its = st->its + 1;
+  st->its = its;
+  const double est = fabs(-sj * gj) / st->bnorm;
+  if (its < st->cap) hist[its] = est;
+  st->hn = hn;
+  st->est = est;
+  st->j = j + 1;
+  const bool more = j + 1 < m && its < st->maxit && !(est <= st->rtol) && hn != 0.0;
+  if (cond) cudaGraphSetConditional(hin, more ? 1u : 0u);
+}
+
+// v_{j+1} = w / h_{j+1,j} (j already advanced by k_gm_step), also the V-cycle input
+__global__ void k_gm_next(int64_t n, const double* __restrict__ w, const GmDev* __restrict__ st,
+                          double* __restrict__ V, double* __restrict__ vin) {
+  pdl_wait();
+  pdl_trigger();
+  const double hn = st->hn;
+  double* vj = V + (int64_t)st->j * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = hn > 0.0 ? w[i] / hn : 0.0;
+    vj[i] = v;
+    vin[i] = v;
+  }
+}
+
+// y = H(0:j, 0:j) \ g(0:j) (back substitution, one thread)
+__global__ void k_gm_ysolve(const GmDev* __restrict__ st, const double* __restrict__ H, const double* __restrict__ g,
+                            double* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x != 0) return;
+  const int j = st->j, m = st->m;
+  for (int k = j - 1; k >= 0; --k) {
+    double s = g[k];
+    for (int q = k + 1; q < j; ++q) s -= H[k + (int64_t)q * (m + 1)] * y[q];
+    y[k] = s / H[k + (int64_t)k * (m + 1)];
+  }
+}
+
+// x += Z(:, 0:j) y (element per thread; the sum in column order)
+__global__ void __launch_bounds__(kGmThreads) k_gm_xupdate(int64_t n, const GmDev* __restrict__ st,
+                                                           const double* __restrict__ Z,
+                                                           const double* __restrict__ y, double* __restrict__ x) {
+  __shared__ double ys[kGmMax];
+  pdl_wait();
+  pdl_trigger();
+  const int j = st->j;
+  if (threadIdx.x < kGmMax) ys[threadIdx.x] = (int)threadIdx.x < j ? y[threadIdx.x] : 0.0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double zk[kGmMax];
+#pragma unroll
+  for (int k = 0; k < kGmMax; ++k) zk[k] = k < j ? __ldg(Z + (int64_t)k * n + i) : 0.0;
+  double s = x[i];
+#pragma unroll
+  for (int k = 0; k < kGmMax; ++k)
+    if (k < j) s += ys[k] * zk[k];
+  x[i] = s;
+}
+
+// end of a cycle: beta = ||b - A x||, the outer test
+__global__ void k_gm_restart(cudaGraphConditionalHandle hout, int cond, GmDev* st, const double* __restrict__ rr) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  const double beta = sqrt(*rr);
+  st->beta = beta;
+  const double rel = beta / st->bnorm;
+  st->rel = rel;
+  st->restarts += 1;
+  const bool conv = rel <= st->rtol;
+  st->converged = conv;
+  if (cond) cudaGraphSetConditional(hout, (!conv && beta != 0.0 && st->its < st->maxit) ? 1u : 0u);
+}
+
+int gm_blocks(int64_t n) { return (int)std::max<int64_t>(1, (n + kGmThreads - 1) / kGmThreads); }
+int gm_sweep_blocks(const Ctx&, int64_t n) { return gm_blocks(n); }
+
+// capture helpers for building a graph with nested conditional nodes
+template <class F>
+std::vector<cudaGraphNode_t> capture_into(Ctx& c, cudaGraph_t g, const cudaGraphNode_t* deps, size_t ndeps,
+                                          F&& body) {
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(c.stream, g, deps, nullptr, ndeps, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(c.stream, &dummy);
+    throw;
+  }
+  cudaStreamCaptureStatus stt;
+  const cudaGraphNode_t* sinks = nullptr;
+  size_t ns = 0;
+  CUDA_CHECK(cudaStreamGetCaptureInfo(c.stream, &stt, nullptr, nullptr, &sinks, &ns));
+  std::vector<cudaGraphNode_t> out(sinks, sinks + ns);
+  cudaGraph_t gg;
+  CUDA_CHECK(cudaStreamEndCapture(c.stream, &gg));
+  return out;
+}
+
+bool add_while(cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps, cudaGraphConditionalHandle* hnd,
+               cudaGraphNode_t* node, cudaGraph_t* body) {
+  if (cudaGraphConditionalHandleCreate(hnd, g, 0, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = *hnd;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  if (cudaGraphAddNode(node, g, deps.empty() ? nullptr : deps.data(), deps.size(), &np) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  *body = np.conditional.phGraph_out[0];
+  return true;
+}
+
+// The pieces of the device GMRES, enqueued either into the nested
+// conditional graph (cond = 1: the kernels set the WHILE handles) or, for
+// profiling (AIRG_GM_FLAT=1, cond = 0), one by one under a host loop.
+struct GmPieces {
+  Ctx& c;
+  Hier& h;
+  const airg_solve_config& cfg;
+  int64_t n;
+  int nb, ns;  // element grid, sweep grid
+  GmDev* st;
+  double *V, *Z, *w, *H, *cs, *sn, *g, *y, *h1, *h2, *nrm, *part;
+  GmPieces(Ctx& c_, Hier& h_, const airg_solve_config& cfg_)
+      : c(c_), h(h_), cfg(cfg_), n(h_.top_n()), nb(gm_blocks(h_.top_n())), ns(gm_sweep_blocks(c_, h_.top_n())),
+        st(h_.gm_st.p), V(h_.V.p), Z(h_.Z.p),
+        w(h_.w.p), H(h_.gm_H.p), cs(h_.gm_cs.p), sn(h_.gm_sn.p), g(h_.gm_g.p), y(h_.gm_y.p), h1(h_.gm_h.p),
+        h2(h_.gm_h.p + (kGmMax + 1)), nrm(h_.gm_h.p + 2 * (kGmMax + 1)), part(h_.gm_part.p) {}
+  void norm_b() { dot_async(c, h.rhs.p, h.rhs.p, n, h.scal.p + 1, h.part.p); }
+  void init(cudaGraphConditionalHandle hout, int cond) {
+    LAUNCH(c, k_gm_init, 1, 32, 0, hout, cond, (const double*)(h.scal.p + 1), st, h.gm_hist.p);
+  }
+  void cycle(cudaGraphConditionalHandle hin, int cond) {
+    LAUNCH(c, k_gm_cycle, (unsigned)nb, kGmThreads, 0, hin, cond, n, (const double*)h.r2.p, st, V, h.r.p, g);
+  }
+  void tail(cudaGraphConditionalHandle hout, int cond) {
+    const bool fast = cfg.fast != 0;
+    LAUNCH_PDL(c, k_gm_ysolve, 1, 32, 0, (const GmDev*)st, (const double*)H, (const double*)g, y);
+    LAUNCH_PDL(c, k_gm_xupdate, (unsigned)nb, kGmThreads, 0, n, (const GmDev*)st, (const double*)Z,
+               (const double*)y, h.xsol.p);
+    enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r2.p, fast);
+    LAUNCH_PDL(c, k_gm_restart, 1, 32, 0, hout, cond, st, (const double*)h.scal.p);
+  }
+  void step(cudaGraphConditionalHandle hin, int cond) {
+    const bool fast = cfg.fast != 0;
+    enqueue_vcycle(c, h, cfg, h.r.p);
+    const double* z = vcycle_output(h);
+    ROWS(EpiGmSpmv, h.top(), z, (EpiGmSpmv{w, z, Z, st, n}));
+    LAUNCH_PDL(c, k_gm_sweep<0>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+               (const double*)nullptr, part);
+    LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h1);
+    LAUNCH_PDL(c, k_gm_sweep<1>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+               (const double*)h1, part);
+    LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h2);
+    LAUNCH_PDL(c, k_gm_sweep<2>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+               (const double*)h2, part);
+    LAUNCH_PDL(c, k_gm_finish, 1, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 1, nrm);
+    LAUNCH_PDL(c, k_gm_step, 1, 32, 0, hin, cond, st, (const double*)h1, (const double*)h2, (const double*)nrm, H,
+               cs, sn, g, h.gm_hist.p);
+    LAUNCH_PDL(c, k_gm_next, (unsigned)nb, kGmThreads, 0, n, (const double*)w, (const GmDev*)st, V, h.r.p);
+  }
+};
+
+// Build the device GMRES graph for restart m; false when the driver refuses
+// nested conditional graphs (the host-driven loop is used then).
+bool build_gmres_graph(Ctx& c, Hier& h, const airg_solve_config& cfg, int m) {
+  const int64_t key = graph_key(h, cfg) * 1024 + m;
+  if (h.g_gm && h.g_key_gm == key) return true;
+  if (h.g_gm) {
+    cudaGraphExecDestroy(h.g_gm);
+    h.g_gm = nullptr;
+  }
+  GmPieces pc(c, h, cfg);
+  const uint64_t before = c.launches;
+  cudaGraph_t gr = nullptr;
+  CUDA_CHECK(cudaGraphCreate(&gr, 0));
+  bool ok = true;
+  uint64_t k_init = 0, k_cycle = 0, k_step = 0, k_tail = 0;
+  try {
+    cudaGraphConditionalHandle hout, hin;
+    cudaGraphNode_t nout, nin;
+    cudaGraph_t bout, bin;
+    // top level: ||b||^2, init, outer WHILE
+    uint64_t c0 = c.launches;
+    auto d0 = capture_into(c, gr, nullptr, 0, [&] { pc.norm_b(); });
+    // the handle must exist before k_gm_init is captured: create the outer
+    // node first, then capture the init kernel ahead of it
+    ok = add_while(gr, {}, &hout, &nout, &bout);
+    if (ok) {
+      auto d1 = capture_into(c, gr, d0.data(), d0.size(), [&] { pc.init(hout, 1); });
+      CUDA_CHECK(cudaGraphAddDependencies(gr, d1.data(), std::vector<cudaGraphNode_t>(d1.size(), nout).data(),
+                                          d1.size()));
+      k_init = c.launches - c0;
+      // outer body: cycle start, inner WHILE, cycle end
+      c0 = c.launches;
+      ok = add_while(bout, {}, &hin, &nin, &bin);
+    }
+    if (ok) {
+      auto e0 = capture_into(c, bout, nullptr, 0, [&] { pc.cycle(hin, 1); });
+      CUDA_CHECK(cudaGraphAddDependencies(bout, e0.data(), std::vector<cudaGraphNode_t>(e0.size(), nin).data(),
+                                          e0.size()));
+      k_cycle = c.launches - c0;
+      c0 = c.launches;
+      capture_into(c, bout, &nin, 1, [&] { pc.tail(hout, 1); });
+      k_tail = c.launches - c0;
+      // inner body: one Arnoldi step
+      c0 = c.launches;
+      capture_into(c, bin, nullptr, 0, [&] { pc.step(hin, 1); });
+      k_step = c.launches - c0;
+    }
+  } catch (...) {
+    cudaGraphDestroy(gr);
+    c.launches = before;
+    throw;
+  }
+  c.launches = before;
+  if (!ok) {
+    cudaGraphDestroy(gr);
+    return false;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, gr, 0);
+  cudaGraphDestroy(gr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  h.g_gm = exec;
+  h.g_key_gm = key;
+  h.gm_kernels[0] = k_init;
+  h.gm_kernels[1] = k_cycle + k_tail;
+  h.gm_kernels[2] = k_step;
+  return true;
+}
+
+// the device-resident solve; false: not available (host loop instead)
+bool gmres_device(Ctx& c, Hier& h, const airg_solve_config& cfg, int m, airg_solve_stats& st,
+                  std::vector<double>& hist) {
+  if (!device_loop_enabled() || h.gm_broken || m > kGmMax || cfg.max_iterations <= 0) return false;
+  const int64_t n = h.top_n();
+  const int nb = gm_blocks(n);
+  const int64_t cap = cfg.max_iterations + 1;
+  if (h.gm_restart != m) {
+    h.V.alloc(c, (size_t)n * (m + 1));
+    h.Z.alloc(c, (size_t)n * m);
+    h.gm_restart = m;
+    if (h.g_gm) {
+      cudaGraphExecDestroy(h.g_gm);
+      h.g_gm = nullptr;
+    }
+  }
+  if (!h.w.p) h.w.alloc(c, (size_t)n);
+  if (!h.r2.p) h.r2.alloc(c, (size_t)n);
+  if (!h.gm_st.p) {
+    h.gm_st.alloc(c, 1);
+    h.gm_H.alloc(c, (size_t)(kGmMax + 1) * kGmMax);
+    h.gm_cs.alloc(c, kGmMax);
+    h.gm_sn.alloc(c, kGmMax);
+    h.gm_g.alloc(c, kGmMax + 1);
+    h.gm_y.alloc(c, kGmMax);
+    h.gm_h.alloc(c, 3 * (kGmMax + 1));
+    h.gm_part.alloc(c, (size_t)(kGmMax + 1) * nb);
+  }
+  if (h.gm_hist.n < (size_t)cap) {
+    h.gm_hist.alloc(c, (size_t)cap);
+    if (h.g_gm) {  // the captured kernels hold the history pointer
+      cudaGraphExecDestroy(h.g_gm);
+      h.g_gm = nullptr;
+    }
+  }
+  static const bool flat = [] {
+    const char* e = getenv("AIRG_GM_FLAT");
+    return e && e[0] == '1';
+  }();
+  if (!flat && !build_gmres_graph(c, h, cfg, m)) {
+    h.gm_broken = true;
+    return false;
+  }
+  GmDev s0 = {};
+  s0.cap = (long long)h.gm_hist.n;
+  s0.maxit = cfg.max_iterations;
+  s0.m = m;
+  s0.rtol = cfg.rtol;
+  to_device(c, h.gm_st.p, &s0, 1);
+  CUDA_CHECK(cudaMemsetAsync(h.xsol.p, 0, sizeof(double) * n, c.stream));
+  CUDA_CHECK(cudaMemcpyAsync(h.r2.p, h.rhs.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  GmDev s1;
+  if (flat) {
+    // profiling form: the same kernels launched one by one (no graph), the
+    // loop tests evaluated on the host from the device state
+    GmPieces pc(c, h, cfg);
+    const uint64_t l0 = c.launches;
+    pc.norm_b();
+    pc.init(0, 0);
+    to_host(c, &s1, h.gm_st.p, 1);
+    bool outer = s1.bnorm != 0.0 && s1.maxit > 0;
+    while (outer) {
+      pc.cycle(0, 0);
+      bool more = s1.its < s1.maxit;
+      while (more) {
+        pc.step(0, 0);
+        to_host(c, &s1, h.gm_st.p, 1);
+        more = s1.j < s1.m && s1.its < s1.maxit && !(s1.est <= s1.rtol) && s1.hn != 0.0;
+      }
+      pc.tail(0, 0);
+      to_host(c, &s1, h.gm_st.p, 1);
+      outer = !s1.converged && s1.beta != 0.0 && s1.its < s1.maxit;
+    }
+    c.launches = l0 + (c.launches - l0);
+  } else {
+    CUDA_CHECK(cudaGraphLaunch(h.g_gm, c.stream));
+    to_host(c, &s1, h.gm_st.p, 1);
+  }
+  const long long kept = std::min<long long>(s1.its, (long long)h.gm_hist.n - 1);
+  std::vector<double> hv((size_t)kept + 1);
+  to_host(c, hv.data(), h.gm_hist.p, hv.size());
+  for (double r : hv) hist.push_back(r);
+  st.iterations = s1.its;
+  st.converged = s1.converged;
+  st.final_relative_residual = s1.rel;
+  if (!flat)
+    c.launches += h.gm_kernels[0] + h.gm_kernels[1] * (uint64_t)s1.restarts + h.gm_kernels[2] * (uint64_t)s1.its;
+  return true;
+}
+
 // Right-preconditioned restarted GMRES with flexible storage Z = M V,
 // CGS2 orthogonalisation and Givens rotations; the restatement in
 // oracle/airg_oracle.c (gmres) performs the same steps serially.
@@ -794,6 +1303,27 @@ void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
   if (m > 512) throw InvalidArgument("gmres: restart length above 512");
   uint64_t fc = 0;
   const uint64_t vflops = vcycle_flops(h, cfg);
+  {
+    const auto t0 = Clock::now();
+    if (gmres_device(c, h, cfg, m, st, hist)) {
+      // flops as the host loop counts them: ||b||; per step the V-cycle, A z,
+      // two CGS passes (4 n (j+1) each) and |w|; per cycle A x and |r|
+      const uint64_t nn = (uint64_t)n;
+      fc = 2 * nn;
+      int64_t cycles = 0;
+      for (int64_t k = 0; k < st.iterations; ++k) {
+        const uint64_t j = (uint64_t)(k % m);
+        if (j == 0) ++cycles;
+        fc += vflops + 2 * (uint64_t)a.nnz + 8 * nn * (j + 1) + 2 * nn;
+      }
+      fc += (uint64_t)cycles * (2 * (uint64_t)a.nnz + 2 * nn);
+      st.flops = fc;
+      st.shadow_flops = fc;
+      st.work_units = (double)fc / (2.0 * (double)a.nnz);
+      st.solve_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+      return;
+    }
+  }
   if (h.gm_restart != m) {
     h.V.alloc(c, (size_t)n * (m + 1));
     h.Z.alloc(c, (size_t)n * m);
