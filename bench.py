@@ -360,13 +360,16 @@ def config_dict(args, p, par, cfg_idx=None):
 
 
 def run_gpu_dist(args):
-    """N > 1 (torchrun, one process per GPU): weak scaling of the C2 family
-    (128 x 128 x 128N cells, one 128^3 z-slab = 2,097,152 unknowns per GPU).
-    The setup's row work is split over the ranks and all-gathered
-    (airg_dist_setup: every rank holds the hierarchy), then every rank keeps
-    its row slabs (z-slabs on level 0, the replay halving rule on coarser
-    levels, the coarsest grid gathered on rank 0) and runs the distributed
-    Richardson solve with NCCL halo exchanges and allreduced norms."""
+    """N > 1 (torchrun, one process per GPU): weak scaling of the metric's
+    config C4 -- a 70 x 70 x 68N cube lattice split into z-slabs of 68 cube
+    layers (1,999,200 tets) per GPU, as BASELINE configs[4] states. Each rank
+    generates its own slab (global column indices); the slabs are
+    all-gathered into the global operator for the setup, whose row work is
+    split over the ranks (airg_dist_setup: every rank holds the hierarchy).
+    Then every rank keeps its row slabs (the z-slabs on level 0, the replay
+    halving rule on coarser levels, the coarsest grid gathered on rank 0) and
+    runs the distributed outer GMRES(30) around the row-slab V-cycle with
+    NCCL halo exchanges and allreduced inner products."""
     import torch
     import torch.distributed as dist
     from paper_2408_08262_b200 import airg, problems
@@ -376,8 +379,18 @@ def run_gpu_dist(args):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = airg.Context(local)
     stream = ctx.stream
-    p = problems.c2_structured_3d(128, nz_slabs=ws)
-    prm = problems.setup_params(2)
+    dev = torch.device("cuda", local)
+    nzl = round(68 * args.scale) if args.scale != 1 else 68
+    nxy = round(70 * args.scale) if args.scale != 1 else 70
+    ps = problems.c4_tets_3d(nxy, nxy, nzl, z0=nzl * rank, nz_total=nzl * ws)
+    # all-gather the slabs into the global CSR (problems.gather_csr_slabs)
+    N, rp, cols, vals = problems.gather_csr_slabs(ps, ws, dist.all_gather)
+
+    class _P:  # the global system (b: this rank's slab only)
+        pass
+    p = _P()
+    p.n, p.nnz, p.row_offsets, p.cols, p.vals = N, int(rp[-1]), rp, cols, vals
+    prm = problems.setup_params(4)
     a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
     dA = airg.DeviceCSR.upload(a, ctx)
     uid = [airg.nccl_unique_id() if rank == 0 else None]
@@ -398,7 +411,7 @@ def run_gpu_dist(args):
     tsm = torch.tensor([setup_ms], device=ctx.tdev, dtype=torch.float64)
     dist.all_reduce(tsm, op=dist.ReduceOp.MAX)
     setup_ms = float(tsm[0])
-    slab = p.n // ws
+    slab = ps.n
     starts = np.arange(ws + 1, dtype=np.int64) * slab
     d = airg.Dist(h, ws, rank=rank, comm=comm, threshold=2.0, starts=starts)
     lo, hi = starts[rank], starts[rank + 1]
@@ -421,10 +434,10 @@ def run_gpu_dist(args):
     dist.all_reduce(tcf, op=dist.ReduceOp.MAX)
     cf_ms = float(tcf[0])
     with torch.cuda.stream(stream):
-        tb = torch.from_numpy(p.b[lo:hi].copy()).to(ctx.tdev)
+        tb = torch.from_numpy(ps.b.copy()).to(ctx.tdev)
         tx = torch.empty(hi - lo, dtype=torch.float64, device=ctx.tdev)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=ctx.tdev)
-    sk = dict(coarse_iterations=prm["coarse_iterations"])
+    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **solver_kw(4))
     for _ in range(args.warmup):
         st, _ = d.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
@@ -445,7 +458,7 @@ def run_gpu_dist(args):
         times.append(s0.elapsed_time(s1))
     launches = ctx.launches() - l0
     # e2e: host slab in, host slab out
-    hb = torch.from_numpy(p.b[lo:hi].copy()).pin_memory()
+    hb = torch.from_numpy(ps.b.copy()).pin_memory()
     hx = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
     e2e = []
     for k in range(args.warmup + args.steps):
@@ -469,19 +482,37 @@ def run_gpu_dist(args):
     levels = [d.level_info(l) for l in range(h.n_levels + 1)]
     # roofline of the whole distributed solve step against the N GPUs' HBM
     peak, peak_kind = hbm_peak()
-    step_bytes = solve_alg_bytes(h, int(st.iterations), prm["coarse_iterations"])
+    step_bytes = gmres_alg_bytes(h, int(st.iterations), prm["coarse_iterations"])
     step_ach = step_bytes / (tot_ms / args.steps / 1e3) / 1e9
+    # NVLink: halo bytes every process receives (exact, from the halo plans)
+    # per V-cycle / level-0 SpMV, plus the allreduce payloads of the GMRES
+    # inner products (2 (j + 1) + 1 doubles per step), summed over ranks
+    hv, hs = d.halo_bytes(**sk)
+    its_n = int(st.iterations)
+    m = sk.get("gmres_restart", 30)
+    ar = sum(8 * (2 * (k % m + 1) + 1) for k in range(its_n)) * (ws - 1) / max(1, ws) * 2
+    mine = its_n * (hv + hs) + ((its_n + m - 1) // m + 1) * hs + ar
+    tnv = torch.tensor([float(mine)], device=ctx.tdev, dtype=torch.float64)
+    dist.all_reduce(tnv, op=dist.ReduceOp.SUM)
+    nv_bytes = float(tnv[0])
+    nv_ach = nv_bytes / ws / (tot_ms / args.steps / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": step_ach, "peak": peak * ws, "unit": "GB/s",
             "frac": step_ach / (peak * ws), "traffic": None, "peak_kind": peak_kind,
+            "nvlink": {"bytes_per_step_all_ranks": nv_bytes, "achieved_per_gpu": nv_ach, "peak_per_gpu": 900.0,
+                       "unit": "GB/s", "frac": nv_ach / 900.0,
+                       "rule": "halo entries received per exchange x 8 B (dist.cu dist_halo_bytes) + ring "
+                               "allreduce payloads of the GMRES inner products"},
             "kernel": f"one distributed AIRG solve step over {ws} GPUs (all row kernels + halo exchanges)",
             "alg_bytes_per_step": step_bytes, "avg_step_ms": tot_ms / args.steps}
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C2 family 128 x 128 x {128 * ws} (one 128^3 z-slab per GPU)",
+        "config": {"workload": f"C4 3D unstructured tets, {nxy} x {nxy} x {nzl * ws} cubes x 6 "
+                               f"(one {nzl}-layer z-slab = {ps.n} tets per GPU)",
                    "unknowns": int(p.n), "nnz": int(p.nnz), "alpha": 0.5, "ddc_fraction": 0.1,
-                   "poly_order": 4, "parallelism": f"row slabs x{ws} (NCCL halos, replay halving, "
+                   "poly_order": 4, "solver": solver_name(4) + " to rtol 1e-10 from x = 0", "mode": "exact",
+                   "parallelism": f"row slabs x{ws} (NCCL halos and allreduces, replay halving, "
                    "gathered coarse grid; setup row work split over GPUs)",
                    "l2": "flushed (512 MiB write) before each timed step"},
         "iterations": int(st.iterations), "final_relative_residual": float(st.final_relative_residual),

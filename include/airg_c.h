@@ -378,6 +378,10 @@ int airg_dist_create(airg_ctx* ctx, const airg_hier* h, int32_t nranks,
 int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg,
                     const double* d_b, double* d_x, airg_solve_stats* stats,
                     double* h_history, int64_t history_cap);
+/* Halo bytes this process receives per V-cycle and per level-0 SpMV (all
+ * emulated ranks in emulation mode; NVLink traffic of the solve). */
+int airg_dist_halo_bytes(const airg_dist* d, const airg_solve_config* cfg, int64_t* vcycle_bytes,
+                         int64_t* spmv_bytes);
 /* Per level: active ranks, replay-rule ratios, total halo entries. */
 int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
                          double* ratio_before, double* ratio_after,

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                                  C.c_int64], C.c_int),
+            "airg_dist_halo_bytes": ([_VP, _P(abi.SolveConfig), _P(C.c_int64), _P(C.c_int64)], C.c_int),
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
                                       _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
             "airg_dist_transport": ([_VP, _P(C.c_int32)], C.c_int),
@@ -914,6 +915,14 @@ class Dist:
                                           C.byref(halo), starts.ctypes.data))
         return dict(active=a.value, ratio_before=rb.value, ratio_after=ra.value, triggered=bool(t.value),
                     halo=halo.value, starts=starts)
+
+    def halo_bytes(self, **solve_kw) -> tuple[int, int]:
+        """(bytes per V-cycle, bytes per level-0 SpMV) of halo data this
+        process receives (NVLink traffic of the solve)."""
+        cfg = abi.solve_config(**solve_kw)
+        v, s = C.c_int64(), C.c_int64()
+        _check(lib().airg_dist_halo_bytes(self.d, C.byref(cfg), C.byref(v), C.byref(s)))
+        return v.value, s.value
 
     def solve_device(self, tb, tx, history_cap: int = 0, **solve_kw):
         cfg = abi.solve_config(**solve_kw)

@@ -247,6 +247,8 @@ int airg_memcpy(airg_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t
     need(ctx, "context");
     bind(ctx->c);
     if (!bytes) return;
+    need(dst, "destination pointer");
+    need(src, "source pointer");
     CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
                                ctx->c.stream));
     CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
@@ -564,6 +566,7 @@ int airg_build_restriction(airg_ctx* ctx, const airg_csr* a_cf, const airg_csr* 
     need(aff_inv, "matrix");
     need(out, "output handle");
     bind(ctx->c);
+    if (n < 0 || n > INT32_MAX) throw InvalidArgument("build_restriction: length out of range");
     LabelMap map;
     build_label_map(ctx->c, d_labels, (int32_t)n, map);
     if (a_cf->m.n != map.nc || a_cf->m.m != map.nf || aff_inv->m.n != map.nf || aff_inv->m.m != map.nf)
@@ -605,6 +608,7 @@ int airg_coarse_matrix(airg_ctx* ctx, const airg_csr* r, const airg_csr* a, cons
     need(p, "matrix");
     need(out, "output handle");
     bind(ctx->c);
+    if (a->m.m != p->m.n || r->m.m != a->m.n) throw InvalidArgument("spgemm: dimension mismatch");  // sparse.cpp:206
     Csr ap, rap, res;
     spgemm(ctx->c, a->m, p->m, ap);
     spgemm(ctx->c, r->m, ap, rap);
@@ -932,6 +936,18 @@ int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg, c
     if (hist)
       for (int64_t k = 0; k < cap && k < (int64_t)hv.size(); ++k) hist[k] = hv[k];
     if (st) *st = s;
+  });
+}
+
+int airg_dist_halo_bytes(const airg_dist* dp, const airg_solve_config* cfg, int64_t* vcycle_bytes,
+                         int64_t* spmv_bytes) {
+  return guard([&] {
+    need(dp, "dist");
+    need(cfg, "config");
+    int64_t v = 0, s = 0;
+    dist_halo_bytes(dp->d, *cfg, v, s);
+    if (vcycle_bytes) *vcycle_bytes = v;
+    if (spmv_bytes) *spmv_bytes = s;
   });
 }
 

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <cstring>
 
 #include "dist.cuh"
@@ -1274,11 +1275,305 @@ uint64_t capture_graph(Ctx& c, cudaGraphExec_t* exec, F&& body) {
 
 }  // namespace
 
+namespace {
+
+// ---- outer GMRES over the row slabs ------------------------------------------
+// Local pieces of the single-GPU method (solve.cu gmres): per-rank partial
+// dots of w with V_0..V_j (grid: blocks x (j+1)), summed over the blocks in
+// a fixed order, then over the ranks (rank order in emulation, NCCL
+// allreduce with one rank per GPU).
+constexpr int kGmDotBlocks = 64;
+__global__ void k_gmd_dots(int64_t n, const double* __restrict__ V, const double* __restrict__ w,
+                           double* __restrict__ part) {
+  __shared__ double sm[32];
+  const double* vk = V + (int64_t)blockIdx.y * n;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(vk[i], w[i], s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+__global__ void k_gmd_fold(const double* __restrict__ part, int np, double* __restrict__ out) {
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int b = 0; b < np; ++b) s += part[(int64_t)blockIdx.x * np + b];
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+// w -= V(:, 0..j) h
+__global__ void k_gmd_update(int64_t n, int jp1, const double* __restrict__ V, const double* __restrict__ h,
+                             double* __restrict__ w) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = w[i];
+  for (int k = 0; k < jp1; ++k) s -= h[k] * V[(int64_t)k * n + i];
+  w[i] = s;
+}
+// dst = src * a (and dst2 = the same)
+__global__ void k_gmd_scale(int64_t n, const double* __restrict__ src, double a, double* __restrict__ dst,
+                            double* __restrict__ dst2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = a == 0.0 ? 0.0 : src[i] * a;
+  dst[i] = v;
+  if (dst2) dst2[i] = v;
+}
+// x += Z(:, 0..j-1) y
+__global__ void k_gmd_xupdate(int64_t n, int j, const double* __restrict__ Z, const double* __restrict__ y,
+                              double* __restrict__ x) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = x[i];
+  for (int k = 0; k < j; ++k) s += y[k] * Z[(int64_t)k * n + i];
+  x[i] = s;
+}
+
+}  // namespace
+
+// Right-preconditioned restarted GMRES around the distributed V-cycle (the
+// steps of the single-GPU gmres(), solve.cu, and of the serial restatement,
+// oracle/airg_oracle.c): rows, vectors and Krylov basis are row slabs of
+// level 0; every inner product is a local partial followed by one
+// allreduce of (j + 1) values; the Hessenberg least squares runs on the host.
+void dist_gmres(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
+                airg_solve_stats& st, std::vector<double>& hist) {
+  const int L = (int)d.lv.size();
+  const int P = d.P;
+  const int m = (int)(cfg.gmres_restart > 0 ? cfg.gmres_restart : 30);
+  if (m > 512) throw InvalidArgument("gmres: restart length above 512");
+  DVec& In = L ? d.lv[0].B : d.CB;   // V-cycle input (owned part)
+  DVec& Out = L ? d.lv[0].X : d.CX;  // V-cycle output (owned part)
+  auto own = [&](int r) { return d.XS.rk[r].own; };
+  if (d.gm_m != m || (int)d.gm.size() != P) {
+    d.gm.clear();
+    d.gm.resize(P);
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r)) continue;
+      const size_t o = (size_t)std::max<int64_t>(1, own(r));
+      d.gm[r].V.alloc(c, o * (m + 1));
+      d.gm[r].Z.alloc(c, o * m);
+      d.gm[r].w.alloc(c, o);
+      d.gm[r].x.alloc(c, o);
+      d.gm[r].dots.alloc(c, (size_t)m + 2);
+      d.gm[r].part.alloc(c, (size_t)(m + 2) * kGmDotBlocks);
+    }
+    d.gm_m = m;
+  }
+  const int64_t key = cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31;
+  if (!d.graph_vc || d.graph_vc_key != key) {
+    d.graph_vc_kernels = capture_graph(c, &d.graph_vc, [&] {
+      enqueue_vcycle(c, d, cfg);
+      p2p_flush(c, d);
+    });
+    d.graph_vc_key = key;
+  }
+  // global sums of per-rank device scalars: rank order in emulation, one
+  // NCCL allreduce per call with one rank per process
+  auto allsum = [&](int cnt, const std::function<double*(int)>& dev) {
+    std::vector<double> tot((size_t)cnt, 0.0), tmp((size_t)cnt);
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r)) continue;
+      double* p = dev(r);
+      if (d.me >= 0 && P > 1) NCCL_CHECK(ncclAllReduce(p, p, (size_t)cnt, ncclDouble, ncclSum, d.comm, c.stream));
+      to_host(c, tmp.data(), p, (size_t)cnt);
+      for (int k = 0; k < cnt; ++k) tot[k] += tmp[k];
+    }
+    return tot;
+  };
+  auto local_dots = [&](int r, int jp1, const double* w) {
+    const int64_t o = own(r);
+    DHier::GmRank& G = d.gm[r];
+    if (o)
+      LAUNCH(c, k_gmd_dots, dim3(kGmDotBlocks, jp1), 256, 0, o, (const double*)G.V.p, w, G.part.p);
+    else
+      CUDA_CHECK(cudaMemsetAsync(G.part.p, 0, sizeof(double) * jp1 * kGmDotBlocks, c.stream));
+    LAUNCH(c, k_gmd_fold, jp1, 32, 0, (const double*)G.part.p, kGmDotBlocks, G.dots.p);
+  };
+  // w = A x_in over the level-0 slabs (x_in: the owned part, staged in XS)
+  auto matvec = [&](const std::function<const double*(int)>& xin, const std::function<double*(int)>& out,
+                    bool resid) {
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r) || !own(r)) continue;
+      CUDA_CHECK(cudaMemcpyAsync(d.XS.rk[r].buf.p, xin(r), sizeof(double) * own(r), cudaMemcpyDeviceToDevice,
+                                 c.stream));
+    }
+    exchange(c, d, d.XS);
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r)) continue;
+      const Csr& A = d.rk[r].A0;
+      if (!A.n) {
+        CUDA_CHECK(cudaMemsetAsync(d.part.p + d.part_off[r], 0, sizeof(double), c.stream));
+        continue;
+      }
+      if (resid)
+        launch_rows(c, A, (const double*)d.XS.rk[r].buf.p, LResid{d.rk[r].rhs.p, out(r), d.part.p + d.part_off[r], 0.0});
+      else
+        launch_rows(c, A, (const double*)d.XS.rk[r].buf.p, LStore{out(r)});
+    }
+    release(c, d, d.XS);
+    p2p_flush(c, d);
+  };
+  std::memset(&st, 0, sizeof st);
+  const auto t0 = std::chrono::steady_clock::now();
+  // b, x = 0, r = b
+  for (int r = 0; r < P; ++r) {
+    if (!d.mine(r)) continue;
+    const int64_t o = own(r), lo = d.me < 0 ? d.XS.rk[r].lo : 0;
+    if (o) {
+      CUDA_CHECK(cudaMemcpyAsync(d.rk[r].rhs.p, d_b + lo, sizeof(double) * o, cudaMemcpyDeviceToDevice, c.stream));
+      CUDA_CHECK(cudaMemcpyAsync(d.gm[r].w.p, d_b + lo, sizeof(double) * o, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    CUDA_CHECK(cudaMemsetAsync(d.gm[r].x.p, 0, sizeof(double) * std::max<int64_t>(1, o), c.stream));
+  }
+  auto norm2 = [&](const std::function<const double*(int)>& v) {
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r)) continue;
+      const int64_t o = own(r);
+      if (o)
+        dot_async(c, v(r), v(r), o, d.gm[r].dots.p, d.gm[r].part.p);
+      else
+        CUDA_CHECK(cudaMemsetAsync(d.gm[r].dots.p, 0, sizeof(double), c.stream));
+    }
+    return allsum(1, [&](int r) { return d.gm[r].dots.p; })[0];
+  };
+  const double bnorm = std::sqrt(norm2([&](int r) { return (const double*)d.rk[r].rhs.p; }));
+  int64_t its = 0;
+  if (bnorm == 0.0) {
+    st.converged = 1;
+    hist.push_back(0.0);
+  } else {
+    double beta = bnorm;
+    hist.push_back(1.0);
+    st.final_relative_residual = 1.0;
+    std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), hcol(m + 2), y(m + 1);
+    while (its < cfg.max_iterations) {
+      for (int r = 0; r < P; ++r)  // v_0 = r / beta, also the V-cycle input
+        if (d.mine(r) && own(r))
+          LAUNCH(c, k_gmd_scale, blocks_for(own(r), 256), 256, 0, own(r), (const double*)d.gm[r].w.p, 1.0 / beta,
+                 d.gm[r].V.p, In.rk[r].buf.p);
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int j = 0;
+      for (; j < m && its < cfg.max_iterations; ++j) {
+        CUDA_CHECK(cudaGraphLaunch(d.graph_vc, c.stream));
+        c.launches += d.graph_vc_kernels;
+        for (int r = 0; r < P; ++r)  // Z_j = M v_j
+          if (d.mine(r) && own(r))
+            CUDA_CHECK(cudaMemcpyAsync(d.gm[r].Z.p + (int64_t)j * own(r), Out.rk[r].buf.p, sizeof(double) * own(r),
+                                       cudaMemcpyDeviceToDevice, c.stream));
+        matvec([&](int r) { return (const double*)Out.rk[r].buf.p; }, [&](int r) { return d.gm[r].w.p; }, false);
+        std::fill(hcol.begin(), hcol.end(), 0.0);
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int r = 0; r < P; ++r)
+            if (d.mine(r)) local_dots(r, j + 1, d.gm[r].w.p);
+          const std::vector<double> hk = allsum(j + 1, [&](int r) { return d.gm[r].dots.p; });
+          for (int r = 0; r < P; ++r) {
+            if (!d.mine(r) || !own(r)) continue;
+            to_device(c, d.gm[r].dots.p, hk.data(), hk.size());
+            LAUNCH(c, k_gmd_update, blocks_for(own(r), 256), 256, 0, own(r), j + 1, (const double*)d.gm[r].V.p,
+                   (const double*)d.gm[r].dots.p, d.gm[r].w.p);
+          }
+          for (int k = 0; k <= j; ++k) hcol[k] += hk[k];
+        }
+        const double hn = std::sqrt(norm2([&](int r) { return (const double*)d.gm[r].w.p; }));
+        hcol[j + 1] = hn;
+        for (int r = 0; r < P; ++r)
+          if (d.mine(r) && own(r))
+            LAUNCH(c, k_gmd_scale, blocks_for(own(r), 256), 256, 0, own(r), (const double*)d.gm[r].w.p,
+                   hn > 0.0 ? 1.0 / hn : 0.0, d.gm[r].V.p + (int64_t)(j + 1) * own(r), In.rk[r].buf.p);
+        for (int k = 0; k < j; ++k) {
+          const double t = cs[k] * hcol[k] + sn[k] * hcol[k + 1];
+          hcol[k + 1] = -sn[k] * hcol[k] + cs[k] * hcol[k + 1];
+          hcol[k] = t;
+        }
+        const double den = std::hypot(hcol[j], hcol[j + 1]);
+        cs[j] = den > 0.0 ? hcol[j] / den : 1.0;
+        sn[j] = den > 0.0 ? hcol[j + 1] / den : 0.0;
+        hcol[j] = den;
+        hcol[j + 1] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        for (int k = 0; k <= j; ++k) H[k + (size_t)j * (m + 1)] = hcol[k];
+        ++its;
+        const double est = std::fabs(g[j + 1]) / bnorm;
+        hist.push_back(est);
+        if (est <= cfg.rtol || hn == 0.0) {
+          ++j;
+          break;
+        }
+      }
+      for (int k = j - 1; k >= 0; --k) {
+        double s = g[k];
+        for (int q = k + 1; q < j; ++q) s -= H[k + (size_t)q * (m + 1)] * y[q];
+        y[k] = s / H[k + (size_t)k * (m + 1)];
+      }
+      for (int r = 0; r < P; ++r) {
+        if (!d.mine(r) || !own(r)) continue;
+        to_device(c, d.gm[r].dots.p, y.data(), (size_t)j);
+        LAUNCH(c, k_gmd_xupdate, blocks_for(own(r), 256), 256, 0, own(r), j, (const double*)d.gm[r].Z.p,
+               (const double*)d.gm[r].dots.p, d.gm[r].x.p);
+      }
+      // r = b - A x (into w), beta = ||r||
+      matvec([&](int r) { return (const double*)d.gm[r].x.p; }, [&](int r) { return d.gm[r].w.p; }, true);
+      beta = std::sqrt(norm2([&](int r) { return (const double*)d.gm[r].w.p; }));
+      const double rel = beta / bnorm;
+      st.final_relative_residual = rel;
+      if (rel <= cfg.rtol) {
+        st.converged = 1;
+        break;
+      }
+      if (beta == 0.0) break;
+    }
+  }
+  for (int r = 0; r < P; ++r) {
+    if (!d.mine(r) || !own(r)) continue;
+    const int64_t lo = d.me < 0 ? d.XS.rk[r].lo : 0;
+    CUDA_CHECK(cudaMemcpyAsync(d_x + lo, d.gm[r].x.p, sizeof(double) * own(r), cudaMemcpyDeviceToDevice, c.stream));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  st.iterations = its;
+  st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  st.history_len = (int64_t)hist.size();
+}
+
+// Halo bytes this process receives per V-cycle (the exchanges of
+// enqueue_vcycle, mine ranks only) and per level-0 SpMV (XS).
+void dist_halo_bytes(const DHier& d, const airg_solve_config& cfg, int64_t& vcycle, int64_t& spmv) {
+  auto halo = [&](const DVec& V) {
+    int64_t s = 0;
+    for (int r = 0; r < d.P; ++r)
+      if (d.mine(r) && r < (int)V.rk.size()) s += V.rk[r].nhalo;
+    return s;
+  };
+  const int L = (int)d.lv.size();
+  int64_t e = 0;
+  for (int l = 0; l < L; ++l) {
+    const DLevel& D = d.lv[l];
+    e += halo(D.B);                                        // restriction input
+    e += halo(l + 1 < L ? d.lv[l + 1].X : d.CX);           // prolongation input
+    e += cfg.up_f_smooths * (halo(D.X) + halo(D.RF));      // residual and update inputs
+  }
+  e += cfg.coarse_iterations * halo(d.CR) + std::max<int64_t>(0, cfg.coarse_iterations - 1) * halo(d.CX);
+  vcycle = 8 * e;
+  spmv = 8 * halo(d.XS);
+}
+
 void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
                 airg_solve_stats& st, std::vector<double>& hist) {
   if (cfg.down_smooths != 0) throw InvalidArgument("solve: down_smooths > 0 is not offered by the GPU V-cycle");
   if (cfg.rtol <= 0.0) throw InvalidArgument("richardson_solve: rtol must be positive");
-  if (cfg.outer != 0) throw InvalidArgument("dist: the distributed solve runs Richardson (outer = 0)");
+  if (cfg.outer == 1) {
+    dist_gmres(c, d, cfg, d_b, d_x, st, hist);
+    return;
+  }
+  if (cfg.outer != 0) throw InvalidArgument("dist: outer must be 0 (Richardson) or 1 (GMRES)");
   std::memset(&st, 0, sizeof st);
   const int L = (int)d.lv.size();
   DVec& Rv = L ? d.lv[0].B : d.CB;

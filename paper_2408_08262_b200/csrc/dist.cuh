@@ -132,6 +132,16 @@ struct DHier {
   cudaGraphExec_t graph = nullptr;
   int64_t graph_key = -1;
   uint64_t graph_kernels = 0;
+  // outer GMRES (dist_gmres): the captured V-cycle alone, and per local rank
+  // the Krylov basis V, Z = M V, w, x and the dot outputs
+  cudaGraphExec_t graph_vc = nullptr;
+  int64_t graph_vc_key = -1;
+  uint64_t graph_vc_kernels = 0;
+  struct GmRank {
+    DBuf<double> V, Z, w, x, dots, part;
+  };
+  std::vector<GmRank> gm;
+  int gm_m = 0;
   int64_t top_n = 0;
   // p2p transport: one arena per rank (emulation: all allocated here; NCCL
   // ranks: mine allocated, the peers' opened from their IPC handles)
@@ -167,6 +177,8 @@ void p2p_push_plan(const std::vector<int64_t>& recv_halo, int64_t recv_own, int6
 
 void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double threshold,
                  const int64_t* level0_starts, DHier& d);
+// halo bytes received by this process per V-cycle and per level-0 SpMV
+void dist_halo_bytes(const DHier& d, const airg_solve_config& cfg, int64_t& vcycle, int64_t& spmv);
 // d_b / d_x: global vectors in emulation mode, this rank's slab with NCCL
 void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
                 airg_solve_stats& st, std::vector<double>& history);

@@ -320,6 +320,7 @@ void p2p_free(DHier& d) {
 
 DHier::~DHier() {
   if (graph) cudaGraphExecDestroy(graph);
+  if (graph_vc) cudaGraphExecDestroy(graph_vc);
   p2p_free(*this);
 }
 

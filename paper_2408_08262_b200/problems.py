@@ -414,3 +414,44 @@ def setup_params(config: int) -> dict:
     if config >= 2:
         p.update(coarse_size_target=5000, coarse_poly_order=8)
     return p
+
+
+def gather_csr_slabs(ps: Problem, world: int, all_gather) -> tuple[int, np.ndarray, np.ndarray, np.ndarray]:
+    """The global CSR from every rank's row slab (rows in rank order, global
+    column indices, e.g. the C4 z-slabs of c4_tets_3d(z0=..., nz_total=...)).
+    all_gather(list_of_world_tensors, tensor) is torch.distributed.all_gather
+    (any backend). Returns (N, row_offsets, cols, vals) as numpy arrays."""
+    import torch
+    dev = None
+    probe = torch.zeros(1)
+    try:  # NCCL gathers device tensors; gloo host tensors
+        import torch.distributed as dist
+        if dist.is_initialized() and dist.get_backend() == "nccl":
+            dev = torch.device("cuda", torch.cuda.current_device())
+    except Exception:
+        dev = None
+    mk = (lambda t: t.to(dev)) if dev is not None else (lambda t: t)
+    cnt = mk(torch.tensor([ps.nnz, ps.n], dtype=torch.int64))
+    cnts = [mk(torch.zeros(2, dtype=torch.int64)) for _ in range(world)]
+    all_gather(cnts, cnt)
+    nnz = [int(c[0]) for c in cnts]
+    rows = [int(c[1]) for c in cnts]
+    mz, mr = max(nnz), max(rows)
+    ci = mk(torch.zeros(mz, dtype=torch.int64))
+    va = mk(torch.zeros(mz, dtype=torch.float64))
+    rl = mk(torch.zeros(mr, dtype=torch.int64))
+    ci[: ps.nnz] = mk(torch.from_numpy(np.asarray(ps.cols, np.int64)))
+    va[: ps.nnz] = mk(torch.from_numpy(np.asarray(ps.vals, np.float64)))
+    rl[: ps.n] = mk(torch.from_numpy(np.diff(ps.row_offsets).astype(np.int64)))
+    cis = [torch.empty_like(ci) for _ in range(world)]
+    vas = [torch.empty_like(va) for _ in range(world)]
+    rls = [torch.empty_like(rl) for _ in range(world)]
+    all_gather(cis, ci)
+    all_gather(vas, va)
+    all_gather(rls, rl)
+    n = sum(rows)
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum(np.concatenate([rls[r][: rows[r]].cpu().numpy() for r in range(world)]))
+    cols = np.concatenate([cis[r][: nnz[r]].cpu().numpy() for r in range(world)])
+    vals = np.concatenate([vas[r][: nnz[r]].cpu().numpy() for r in range(world)])
+    return n, rp, cols, vals

@@ -140,3 +140,36 @@ def test_two_rank_gloo_halo_exchange():
     # the upwind slab's boundary plane)
     assert res[0][2] + res[1][2] == 64 and min(res[0][2], res[1][2]) == 0
     assert res[0][3] == res[1][3] and res[0][3] > 2.0
+
+
+def _slab_worker(rank, world, port, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ps = problems.c4_tets_3d(6, 5, 4, z0=4 * rank, nz_total=4 * world)
+        n, rp, ci, v = problems.gather_csr_slabs(ps, world, dist.all_gather)
+        g = problems.c4_tets_3d(6, 5, 4 * world)
+        ok = (n == g.n and np.array_equal(rp, g.row_offsets) and np.array_equal(ci, g.cols)
+              and np.array_equal(v.view(np.uint64), g.vals.view(np.uint64))
+              and np.array_equal(ps.b.view(np.uint64), g.b[ps.n * rank: ps.n * (rank + 1)].view(np.uint64)))
+        result_q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_c4_zslabs_gather_to_global_operator():
+    """The weak-scaling bench's N > 1 input path (bench.py run_gpu_dist): each
+    rank generates its C4 z-slab (global columns) and the all-gathered slabs
+    are the global operator and right-hand side, bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok for _, ok in res), res

@@ -249,3 +249,55 @@ def test_dist_p2p_transport_emulated_bit_identical():
                              timeout=900)
         assert out.returncode == 0, out.stderr[-3000:]
         assert "p2p ok" in out.stdout
+
+
+@pytest.mark.parametrize("P,threshold", [(2, 2.0), (3, 2.0), (4, 1e9)])
+def test_dist_gmres_emulated_matches_one_gpu(P, threshold):
+    """The outer GMRES(30) over the row slabs (dist.cu dist_gmres; the C4
+    solver of the weak-scaling bench): the V-cycle is bit-identical to one
+    GPU's, the inner products are slab partials + one allreduce, so the solve
+    agrees with the one-GPU GMRES to the parity tolerance."""
+    import scipy.sparse as sp
+    p = problems.make(4, 0.25)
+    prm = dict(problems.setup_params(4), coarse_size_target=500)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    ref = airg.gmres_solve(h, p.b, coarse_iterations=3)
+    d = airg.Dist(h, P, threshold=threshold)
+    res = d.solve(p.b, coarse_iterations=3, outer=1, gmres_restart=30)
+    assert res.stats.converged and res.stats.final_relative_residual <= 1e-10
+    assert abs(res.stats.iterations - ref.stats.iterations) <= 1
+    assert np.linalg.norm(res.x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+    A = sp.csr_matrix((p.vals, p.cols, p.row_offsets), shape=(p.n, p.n))
+    assert np.linalg.norm(p.b - A @ res.x) <= 1.05e-10 * np.linalg.norm(p.b)
+
+
+def test_dist_gmres_nccl_single_rank_path():
+    """The NCCL code path of the distributed GMRES (allreduced dots) on a
+    1-rank communicator (one GPU in this run)."""
+    p = problems.make(4, 0.25)
+    prm = dict(problems.setup_params(4), coarse_size_target=500)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    ref = airg.gmres_solve(h, p.b, coarse_iterations=3)
+    comm = airg.NcclComm(1, 0, airg.nccl_unique_id())
+    d = airg.Dist(h, 1, rank=0, comm=comm)
+    tb = h.ctx.to_device(p.b)
+    tx = h.ctx.empty(p.n, h.ctx.torch.float64)
+    st, _ = d.solve_device(tb, tx, coarse_iterations=3, outer=1)
+    x = h.ctx.to_host(tx)
+    assert st.converged and abs(st.iterations - ref.stats.iterations) <= 1
+    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
+def test_dist_halo_bytes_accounting():
+    """The NVLink bytes the N > 1 bench reports: per V-cycle, every exchange
+    of enqueue_vcycle counted from the halo plans (8 B per halo entry)."""
+    p = problems.c2_structured_3d(24)
+    prm = dict(problems.setup_params(2), coarse_size_target=300)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    one = airg.Dist(h, 1)
+    assert one.halo_bytes(coarse_iterations=3) == (0, 0)
+    d = airg.Dist(h, 4, threshold=0.0, starts=np.linspace(0, p.n, 5).astype(np.int64))
+    v, s = d.halo_bytes(coarse_iterations=3)
+    # level 0's X halo is one plane of 24 x 24 cells between each slab pair
+    assert s == 8 * d.level_info(0)["halo"] and s > 0
+    assert v >= 3 * s and v % 8 == 0
