@@ -382,6 +382,9 @@ int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg,
  * emulated ranks in emulation mode; NVLink traffic of the solve). */
 int airg_dist_halo_bytes(const airg_dist* d, const airg_solve_config* cfg, int64_t* vcycle_bytes,
                          int64_t* spmv_bytes);
+/* local_share (partition_model.cpp:66-75) of a level before / after its
+ * halving decision (levels below n_levels). */
+int airg_dist_level_share(const airg_dist* d, int64_t level, double* share_before, double* share_after);
 /* Per level: active ranks, replay-rule ratios, total halo entries. */
 int airg_dist_level_info(const airg_dist* d, int64_t level, int32_t* active,
                          double* ratio_before, double* ratio_after,

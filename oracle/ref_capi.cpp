@@ -368,6 +368,16 @@ int ref_csv_row(const void* hp, int64_t iterations, double work_units, int32_t c
     std::snprintf(out, (size_t)cap, "%s", row.c_str());
   });
 }
+// partition_report(replay_triggers(h, ranks, threshold)).dump() (reports.cpp:75-101,
+// partition_model.cpp:77-112)
+int ref_partition_report(const void* hp, int32_t ranks, double threshold, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    const Hierarchy& h = static_cast<const RefHier*>(hp)->h;
+    const std::string js = partition_report(replay_triggers(h, ranks, threshold)).dump();
+    *len = static_cast<int64_t>(js.size());
+    if (out && cap > 0) std::snprintf(out, (size_t)cap, "%s", js.c_str());
+  });
+}
 int ref_csv_header(char* out, int64_t cap) {
   std::snprintf(out, (size_t)cap, "%s", csv_header().c_str());
   return AIRG_OK;

@@ -346,6 +346,17 @@ class Hier:
         self.lib._chk(f(self.h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
 
+    def partition_report(self, ranks: int, threshold: float) -> str:
+        """reports.cpp partition_report(replay_triggers(h, ranks, threshold))
+        (reference build only)."""
+        f = self.lib.lib.ref_partition_report
+        f.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+        n = C.c_int64()
+        self.lib._chk(f(self.h, int(ranks), float(threshold), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.lib._chk(f(self.h, int(ranks), float(threshold), buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
     def csv_row(self, st, alpha, cf_name, seed) -> str:
         f = self.lib.lib.ref_csv_row
         f.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_char_p,

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                                  C.c_int64], C.c_int),
+            "airg_dist_level_share": ([_VP, C.c_int64, _P(C.c_double), _P(C.c_double)], C.c_int),
             "airg_dist_halo_bytes": ([_VP, _P(abi.SolveConfig), _P(C.c_int64), _P(C.c_int64)], C.c_int),
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
                                       _P(C.c_int32), _P(C.c_int64), _VP], C.c_int),
@@ -913,8 +914,13 @@ class Dist:
         starts = np.zeros(self.P + 1, np.int64)
         _check(lib().airg_dist_level_info(self.d, int(l), C.byref(a), C.byref(rb), C.byref(ra), C.byref(t),
                                           C.byref(halo), starts.ctypes.data))
-        return dict(active=a.value, ratio_before=rb.value, ratio_after=ra.value, triggered=bool(t.value),
-                    halo=halo.value, starts=starts)
+        out = dict(active=a.value, ratio_before=rb.value, ratio_after=ra.value, triggered=bool(t.value),
+                   halo=halo.value, starts=starts)
+        if l < self.h.n_levels:
+            sb, sa = C.c_double(), C.c_double()
+            _check(lib().airg_dist_level_share(self.d, int(l), C.byref(sb), C.byref(sa)))
+            out.update(share_before=sb.value, share_after=sa.value)
+        return out
 
     def halo_bytes(self, **solve_kw) -> tuple[int, int]:
         """(bytes per V-cycle, bytes per level-0 SpMV) of halo data this

@@ -951,6 +951,16 @@ int airg_dist_halo_bytes(const airg_dist* dp, const airg_solve_config* cfg, int6
   });
 }
 
+int airg_dist_level_share(const airg_dist* dp, int64_t l, double* share_before, double* share_after) {
+  return guard([&] {
+    need(dp, "dist");
+    const DHier& d = dp->d;
+    if (l < 0 || l >= (int64_t)d.lv.size()) throw InvalidArgument("level out of range");
+    if (share_before) *share_before = d.lv[l].share_before;
+    if (share_after) *share_after = d.lv[l].share_after;
+  });
+}
+
 int airg_dist_level_info(const airg_dist* dp, int64_t l, int32_t* active, double* rb, double* ra,
                          int32_t* trig, int64_t* halo, int64_t* starts) {
   return guard([&] {

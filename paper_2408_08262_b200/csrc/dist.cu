@@ -371,8 +371,11 @@ Part gathered(int64_t n, int P) {
 }
 
 // mean over ranks of local / non-local nnz (partition_model.cpp:53-64)
-double locality(Ctx& c, const Csr& a, const Part& p) {
+// locality_ratio (partition_model.cpp:53-64) of a contiguous partition;
+// share: local_share (:66-75), the global fraction of on-rank entries
+double locality(Ctx& c, const Csr& a, const Part& p, double* share = nullptr) {
   const int P = p.P();
+  if (share) *share = 1.0;
   if (a.n == 0) return INFINITY;
   DBuf<int64_t> ds(c, (size_t)P + 1);
   to_device(c, ds.p, p.s.data(), (size_t)P + 1);
@@ -383,11 +386,15 @@ double locality(Ctx& c, const Csr& a, const Part& p) {
   to_host(c, h.data(), cnt.p, h.size());
   double sum = 0.0;
   int contributing = 0;
+  unsigned long long loc = 0, tot = 0;
   for (int r = 0; r < P; ++r) {
+    loc += h[r];
+    tot += h[r] + h[P + r];
     if (h[P + r] == 0) continue;
     sum += (double)h[r] / (double)h[P + r];
     ++contributing;
   }
+  if (share && tot) *share = (double)loc / (double)tot;
   return contributing ? sum / contributing : INFINITY;
 }
 
@@ -942,8 +949,9 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
     const Csr& A = h.levels[l].a;
     Part p = (l == 0 && level0_starts) ? Part{std::vector<int64_t>(level0_starts, level0_starts + P + 1)}
                                        : balanced(A.n, active, P);
-    D.ratio_before = locality(c, A, p);
+    D.ratio_before = locality(c, A, p, &D.share_before);
     D.ratio_after = D.ratio_before;
+    D.share_after = D.share_before;
     // A caller-fixed level-0 partition (one process per GPU: the caller's b
     // and x slabs) is kept as given; halving applies from level 1 onward.
     const bool fixed = l == 0 && level0_starts;
@@ -952,14 +960,14 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
       p = merged(p, active, na);
       active = na;
       D.triggered = true;
-      D.ratio_after = locality(c, A, p);
+      D.ratio_after = locality(c, A, p, &D.share_after);
     }
     while (!fixed && min_rows > 0 && active > 1 && (int64_t)A.n < min_rows * (int64_t)active) {
       const int na = (active + 1) / 2;
       p = merged(p, active, na);
       active = na;
       D.triggered = true;
-      D.ratio_after = locality(c, A, p);
+      D.ratio_after = locality(c, A, p, &D.share_after);
     }
     D.active = active;
     D.fine = p;

@@ -101,6 +101,7 @@ struct DLevel {
   Part fine, coarse_part, fpart;  // partitions of level l rows, level l+1 rows, F points
   int active = 1;
   double ratio_before = 0.0, ratio_after = 0.0;
+  double share_before = 1.0, share_after = 1.0;  // local_share (partition_model.cpp:66-75)
   bool triggered = false;
   DVec B, X, RF;  // b_l (input of R_l), x_l (input of AF/AFFg and of P_{l-1}), r_F
   struct Rank {

@@ -66,7 +66,10 @@ def solve_report(res: "airg.SolveResult") -> dict:
 
 
 def partition_report(d: "airg.Dist", initial_ranks: int, threshold: float) -> dict:
-    """partition_report (reports.cpp:75-96) for a row-slab distribution."""
+    """partition_report (reports.cpp:75-101) for the row-slab distribution the
+    GPU actually runs: the reference's replay rule (partition_model.cpp:77-112)
+    on every hierarchy level, then the coarsest grid gathered on one GPU (the
+    reference's model applies the rule once more there; the GPU gathers)."""
     levels, triggers = [], []
     for l in range(d.h.n_levels):
         li = d.level_info(l)
@@ -77,9 +80,14 @@ def partition_report(d: "airg.Dist", initial_ranks: int, threshold: float) -> di
             "triggered": li["triggered"],
             "ratio": li["ratio_after"] if finite else None,
             "ratio_before_trigger": li["ratio_before"] if math.isfinite(li["ratio_before"]) else None,
+            "local_share": li["share_after"] if math.isfinite(li["share_after"]) else 1.0,
         })
         if li["triggered"]:
             triggers.append(l)
+    info = d.h.info()
+    levels.append({"level": d.h.n_levels, "n": info.coarse_n, "nnz": info.coarse_nnz, "active_ranks": 1,
+                   "triggered": False, "ratio": None, "ratio_before_trigger": None, "local_share": 1.0,
+                   "gathered": True})
     return {"initial_ranks": initial_ranks, "threshold": threshold, "levels": levels,
             "trigger_levels": triggers}
 

@@ -298,6 +298,7 @@ def test_dist_halo_bytes_accounting():
     assert one.halo_bytes(coarse_iterations=3) == (0, 0)
     d = airg.Dist(h, 4, threshold=0.0, starts=np.linspace(0, p.n, 5).astype(np.int64))
     v, s = d.halo_bytes(coarse_iterations=3)
-    # level 0's X halo is one plane of 24 x 24 cells between each slab pair
-    assert s == 8 * d.level_info(0)["halo"] and s > 0
-    assert v >= 3 * s and v % 8 == 0
+    # the level-0 SpMV reads one upwind plane of 24 x 24 cells across each of
+    # the three slab boundaries (one-sided halo)
+    assert s == 8 * 3 * 24 * 24
+    assert v > s and v % 8 == 0 and v >= 8 * d.level_info(0)["halo"]

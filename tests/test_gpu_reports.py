@@ -73,3 +73,29 @@ def test_reports_match_reference(ref, path, tmp_path):
     reports.append_csv(f, reports.csv_row(h, res.stats, 0.5, "pmisr-ddc", 1))
     lines = f.read_text().splitlines()
     assert lines[0] == reports.csv_header() and len(lines) == 3
+
+
+@pytest.mark.parametrize("P,threshold", [(2, 2.0), (4, 50.0), (8, 1e9), (3, 500.0)])
+@pytest.mark.parametrize("path", GOLDEN[:4], ids=lambda p: os.path.basename(p)[:-4])
+def test_rank_halving_matches_reference_replay(ref, path, P, threshold):
+    """The GPU distribution's active-rank decisions (dist.cu dist_create) are
+    the reference's replay rule (partition_model.cpp:77-112): on the same
+    hierarchy (coefficient injection), every level's active ranks, trigger,
+    locality ratios and local share equal partition_report(replay_triggers)
+    bit for bit; the coarsest grid is gathered on one GPU (the reference's
+    model applies the rule once more there)."""
+    g = np.load(path)
+    prm = dict(eval(str(g["params"][0])))
+    n = len(g["rp"]) - 1
+    oh = refpy.setup(ref, ref.mat(n, n, g["rp"], g["ci"], g["v"]), **prm)
+    h = airg.setup(airg.SparseMatrix.from_arrays(n, n, g["rp"], g["ci"], g["v"]), injection=_injection(oh, prm),
+                   **prm)
+    theirs = json.loads(oh.partition_report(P, threshold))
+    d = airg.Dist(h, P, threshold=threshold)
+    ours = reports.partition_report(d, P, threshold)
+    assert len(ours["levels"]) == len(theirs["levels"]) == h.n_levels + 1
+    for lo, lt in zip(ours["levels"][:-1], theirs["levels"][:-1]):
+        for k in ("level", "n", "nnz", "active_ranks", "triggered", "ratio", "ratio_before_trigger", "local_share"):
+            assert lo[k] == lt[k], (lo["level"], k, lo[k], lt[k])
+    assert ours["trigger_levels"] == [l for l in theirs["trigger_levels"] if l < h.n_levels]
+    assert ours["levels"][-1]["active_ranks"] == 1 and ours["levels"][-1]["n"] == theirs["levels"][-1]["n"]
