@@ -2,7 +2,9 @@
 // Host code orchestrates; every matrix operation is a device kernel (no CPU
 // fallback). The level loop reads back only scalars (counts, norms, growth)
 // to take the reference's data-dependent branches.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "dist.cuh"
@@ -13,6 +15,45 @@
 namespace airg {
 
 namespace {
+
+// AIRG_CF=legacy: the setup's split as strength -> pmisr -> extract -> ddc
+// kernels with S materialised (the reference's structure; same labels)
+bool fused_cf_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_CF");
+    return !(e && !strcmp(e, "legacy"));
+  }();
+  return v;
+}
+
+// AIRG_SETUP_TIMING=1 (diagnostic): per-phase wall times of the level loop,
+// synchronised at each phase boundary, printed at the end of the setup
+struct PhaseClock {
+  bool on;
+  Ctx& c;
+  std::chrono::steady_clock::time_point t;
+  double acc[8] = {};
+  explicit PhaseClock(Ctx& c_) : c(c_) {
+    const char* e = getenv("AIRG_SETUP_TIMING");
+    on = e && e[0] == '1';
+    if (on) {
+      CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void lap(int k) {
+    if (!on) return;
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    const auto n = std::chrono::steady_clock::now();
+    acc[k] += std::chrono::duration<double, std::milli>(n - t).count();
+    t = n;
+  }
+  void report() const {
+    if (!on) return;
+    fprintf(stderr, "setup phases ms: cf %.2f | inverse %.2f | R %.2f | P %.2f | RAP %.2f | coarse %.2f | fused %.2f\n",
+            acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6]);
+  }
+};
 
 struct Checked {
   std::vector<double> coeffs;
@@ -127,6 +168,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
   constexpr double kCoarseAccept = 0.5;
   Checked coarse;
   Csr current;
+  PhaseClock pc(c);
   with_full_diagonal(c, a0, current);  // air.cpp:307
   for (;;) {
     const int64_t built = (int64_t)h.levels.size();
@@ -138,8 +180,10 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
         break;
       }
     } else if (forced || current.n <= cfg.coarse_size_target) {  // air.cpp:309-320
+      pc.lap(4);
       coarse = make_checked_inverse(c, current, cfg.coarse_poly_order, cfg.sparsity_order,
                                     mix_host(cfg.seed, 0xC0A12534ull + (uint64_t)built), rs);
+      pc.lap(5);
       if (forced || coarse.growth <= kCoarseAccept) break;
       coarse = Checked();
     }
@@ -151,10 +195,22 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
 
     // --- CF split: strength -> PMISR -> extract -> DDC (air.cpp:327-355)
     Strength g;
-    strength(c, L.a, cfg.strength_alpha, g);
     DBuf<uint8_t> labels(c, (size_t)n);
     Blocks blk;
-    if (rs && cfg.cf == 0 && cfg.weight_mode == 0 && (cfg.ddc_enabled == 0 || cfg.ddc_fraction > 0.0)) {
+    // the default PMISR-DDC split runs as the fused, sync-free split of the
+    // CF-split metric (cfsplit.cu, labels bit-identical to the step-by-step
+    // split); S is never materialised (P re-applies the strength test)
+    const bool fused_cf = !rs && cfg.cf == 0 && cfg.weight_mode == 0 && fused_cf_enabled();
+    if (!fused_cf) strength(c, L.a, cfg.strength_alpha, g);
+    if (fused_cf) {
+      const CfFused rep = cf_split_fused(c, L.a, cfg.strength_alpha, level_seed, cfg.ddc_enabled != 0,
+                                         cfg.ddc_fraction, cfg.ddc_bins, labels.p, nullptr);
+      build_label_map(c, labels.p, n, L.map);
+      L.n_f_pre = rep.n_f_pre;
+      L.n_converted = rep.n_converted;
+      L.alpha_diag = rep.alpha_diag;
+      L.max_theta_pre = rep.max_theta;
+    } else if (rs && cfg.cf == 0 && cfg.weight_mode == 0 && (cfg.ddc_enabled == 0 || cfg.ddc_fraction > 0.0)) {
       // row slabs over the ranks (dist.cu): the labels, all-gathered
       const std::vector<int64_t> sl = rs->slabs(n);
       CfReport rep;
@@ -191,6 +247,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     }
     extract_blocks(c, L.a, L.map, blk, /*want_af=*/true);
     L.max_theta_post = dominance_max(c, blk.aff);
+    if (fused_cf && !cfg.ddc_enabled) L.max_theta_pre = L.max_theta_post;  // no DDC: the same A_ff
     L.aff = std::move(blk.aff);
     L.afc = std::move(blk.afc);
     L.acf = std::move(blk.acf);
@@ -211,6 +268,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
                          " coarsened by less than 1% (" + std::to_string(n) + " -> " +
                          std::to_string(nc) + ")");
 
+    pc.lap(0);
     // --- approximate ideal restriction (air.cpp:378-381)
     Checked ff = inj ? injected_inverse(c, L.aff, inj->level_coeffs[built], inj->level_eff[built],
                                         cfg.sparsity_order, rs)
@@ -220,8 +278,14 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     L.eff = ff.eff;
     L.growth = ff.growth;
     L.attempts = ff.attempts;
+    pc.lap(1);
     build_restriction(c, L.acf, L.ffinv, cfg.drop_restrict, L.map, L.r, nullptr, 0, rs);
-    build_prolongation(c, L.map, g, L.a, L.pmap, L.p);
+    pc.lap(2);
+    if (fused_cf)
+      build_prolongation_fused(c, L.map, L.a, cfg.strength_alpha, L.pmap, L.p);
+    else
+      build_prolongation(c, L.map, g, L.a, L.pmap, L.p);
+    pc.lap(3);
 
     // --- Galerkin coarse operator (air.cpp:268-271, :386-387)
     Csr ap, rap;
@@ -233,6 +297,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
       spgemm(c, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
     }
     with_full_diagonal(c, rap, current);
+    pc.lap(4);
   }
   h.coarse_a = std::move(current);
   if (!coarse.valid) {
@@ -250,7 +315,10 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
   h.coarse_growth = coarse.growth;
   recompute_metrics(h);
   alloc_workspace(c, h);
+  pc.lap(4);
   if (cfg.fused_smooths >= 0) build_fused(c, h, cfg.fused_smooths);
+  pc.lap(6);
+  pc.report();
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 

@@ -127,5 +127,8 @@ void prolongation_map_rows(Ctx& c, const LabelMap& map, const Strength& g, const
 void prolongation_from_map(Ctx& c, const int32_t* pmap, int n, int nc, Csr& p);
 void build_prolongation(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a,
                         DBuf<int32_t>& pmap, Csr& p);
+// the same P with the strength test re-applied to A's rows (no S)
+void build_prolongation_fused(Ctx& c, const LabelMap& map, const Csr& a, double alpha, DBuf<int32_t>& pmap,
+                              Csr& p);
 
 }  // namespace airg

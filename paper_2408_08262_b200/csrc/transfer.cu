@@ -81,6 +81,49 @@ __global__ void p_map(int n, const uint8_t* __restrict__ label, const int32_t* _
   pmap[r] = best >= 0 ? f2s[best] : -1;
 }
 
+// The same map with S_i re-derived from A's row (coarsening.cpp:83-105: j != i,
+// |a_ij| > 0, |a_ij| >= alpha * max_{k != i} |a_ik|, the product rounded once):
+// S_i is A's row filtered in column order, so the strong pass visits the
+// same candidates in the same order as p_map -- no S needed.
+__global__ void p_map_fused(int n, const uint8_t* __restrict__ label, const int32_t* __restrict__ f2s,
+                            const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                            const double* __restrict__ av, double alpha, int32_t* __restrict__ pmap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (label[i] == AIRG_C) {
+    pmap[i] = f2s[i];
+    return;
+  }
+  const int s = arp[i], e = arp[i + 1];
+  double off_max = 0.0;
+  for (int k = s; k < e; ++k)
+    if (aci[k] != i) off_max = fmax(off_max, fabs(av[k]));
+  const double thr = __dmul_rn(alpha, off_max);
+  int best = -1;
+  double best_mag = -1.0;
+  for (int k = s; k < e; ++k) {
+    const int j = aci[k];
+    const double mag = fabs(av[k]);
+    if (j == i || !(mag > 0.0) || !(mag >= thr) || label[j] != AIRG_C) continue;
+    if (mag > best_mag) {
+      best_mag = mag;
+      best = j;
+    }
+  }
+  if (best < 0) {
+    for (int k = s; k < e; ++k) {
+      const int j = aci[k];
+      if (j == i || label[j] != AIRG_C) continue;
+      const double mag = fabs(av[k]);
+      if (mag > best_mag) {
+        best_mag = mag;
+        best = j;
+      }
+    }
+  }
+  pmap[i] = best >= 0 ? f2s[best] : -1;
+}
+
 __global__ void p_count(int n, const int32_t* __restrict__ pmap, int32_t* __restrict__ cnt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) cnt[i] = pmap[i] >= 0;
@@ -138,6 +181,16 @@ void prolongation_from_map(Ctx& c, const int32_t* pmap, int n, int nc, Csr& p) {
   out.v.alloc(c, (size_t)out.nnz);
   if (n) LAUNCH(c, p_fill, blocks_for(n, 256), 256, 0, n, pmap, out.rp.p, out.ci.p, out.v.p);
   p = std::move(out);
+}
+
+void build_prolongation_fused(Ctx& c, const LabelMap& map, const Csr& a, double alpha, DBuf<int32_t>& pmap,
+                              Csr& p) {
+  const int n = map.n;
+  pmap.alloc(c, (size_t)std::max(1, n));
+  if (n)
+    LAUNCH(c, p_map_fused, blocks_for(n, 256), 256, 0, n, map.label.p, map.fine_to_sub.p, a.rp.p, a.ci.p, a.v.p,
+           alpha, pmap.p);
+  prolongation_from_map(c, pmap.p, n, map.nc, p);
 }
 
 void build_prolongation(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a,
