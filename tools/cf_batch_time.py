@@ -1,4 +1,4 @@
-"""Batched CF split of all C2 levels (the bench's cf_split_ms): median of 10
+"""Batched CF split of all levels of C<argv[1]> (default C2) (the bench's cf_split_ms): median of 10
 event-timed airg_cf_split_batch calls; labels checked against the setup's."""
 import os
 import sys
@@ -10,8 +10,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2408_08262_b200 import airg, problems  # noqa: E402
 
 ctx = airg.Context(0)
-p = problems.make(2)
-prm = problems.setup_params(2)
+CFG = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+p = problems.make(CFG)
+prm = problems.setup_params(CFG)
 a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
 h = airg.setup(airg.DeviceCSR.upload(a, ctx), ctx=ctx, **prm)
 mats = [h.matrix_handle(l, 0) for l in range(h.n_levels)]
@@ -26,4 +27,4 @@ for _ in range(12):
     e1.synchronize()
     ts.append(e0.elapsed_time(e1))
 ok = all(np.array_equal(labs[l][: mats[l].dims()[0]].cpu().numpy(), h.labels(l)) for l in range(h.n_levels))
-print(f"cf_split_batch ms median {np.median(ts[2:]):.4f} min {np.min(ts[2:]):.4f} labels_ok {ok}")
+print(f"C{CFG} cf_split_batch ms median {np.median(ts[2:]):.4f} min {np.min(ts[2:]):.4f} labels_ok {ok}")
