@@ -235,6 +235,17 @@ int airg_cf_split(airg_ctx* ctx, const airg_csr* a, double alpha,
                   int32_t ddc_enabled, double ddc_fraction, int64_t ddc_bins,
                   uint8_t* d_labels, uint8_t* d_labels_pre,
                   airg_cf_report* report);
+/* pmisr / pmis on a caller-supplied strength pattern S (the reference's
+ * pmisr(const StrengthGraph&, ...) / pmis(g, swap, seed), coarsening.hpp:
+ * 78-90): weights from |S_i| + |S^T_i| (or |S u S^T| for weight_mode 1) and
+ * the seeded hash, d_weights (nullable) receives them. */
+int airg_pmisr_pattern(airg_ctx* ctx, const airg_csr* s_pattern, int64_t max_loops, uint64_t seed,
+                       int32_t weight_mode, uint8_t* d_labels, double* d_weights);
+int airg_pmis_pattern(airg_ctx* ctx, const airg_csr* s_pattern, int32_t swap, uint64_t seed, uint8_t* d_labels);
+/* ddc(a_ff, labels, map, opt) (coarsening.cpp:252-330; coarsening.hpp:133)
+ * on the F block itself: d_labels (n, global) converted in place. */
+int airg_ddc_block(airg_ctx* ctx, const airg_csr* a_ff, uint8_t* d_labels, int64_t n, double fraction,
+                   int64_t bins, int32_t selection, double direct_alpha_diag, airg_cf_report* report);
 /* airg_cf_split (weight_mode 0) on `count` matrices with one
  * synchronisation: the splits are enqueued back to back on the context
  * stream and their reports read once at the end (e.g. re-splitting every
@@ -304,6 +315,14 @@ int airg_dist_setup(airg_ctx* ctx, const airg_csr* a, const airg_setup_config* c
 int airg_hier_info_get(const airg_hier* h, airg_hier_info* info);
 int airg_hier_level_info(const airg_hier* h, int64_t level,
                          airg_level_info* info);
+/* A device hierarchy from given level operators (a host airgraph::Hierarchy
+ * handed to vcycle / richardson_solve / f_smooth through the C++ shim):
+ * mats = n_levels x {A, A_ff, A_fc, A_cf, Aff_inv, R, P} (P one-point),
+ * d_labels = per level n bytes (device), the coarse operator and its
+ * assembled inverse. */
+int airg_hier_from_levels(airg_ctx* ctx, int64_t n_levels, const airg_csr* const* mats,
+                          const uint8_t* const* d_labels, const airg_csr* coarse_a, const airg_csr* coarse_inv,
+                          int64_t coarse_iterations, airg_hier** out);
 /* which: 0 A, 1 A_ff, 2 A_fc, 3 A_cf, 4 Aff_inv, 5 R, 6 P, and (fast V-cycle,
  * once built) 7 A_F P (n_f x n_c), 8 W_k (n_f x n_f); level ==
  * n_levels with which 0 / 4 gives the coarse A / coarse inverse. Returns a

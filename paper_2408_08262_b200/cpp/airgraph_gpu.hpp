@@ -146,6 +146,7 @@ class DeviceBuffer {
   }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ctx_(o.ctx_), p_(o.p_) { o.p_ = nullptr; }
   template <class T>
   T* as() const { return static_cast<T*>(p_); }
   void upload(const void* h, size_t bytes) { check(airg_memcpy(ctx_->get(), p_, h, bytes, 1)); }

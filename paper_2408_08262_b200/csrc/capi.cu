@@ -381,6 +381,104 @@ int airg_pmisr_with_weights(airg_ctx* ctx, const airg_csr* s_pattern, int64_t ma
   });
 }
 
+namespace {
+Csr copy_csr(Ctx& c, const Csr& a) {
+  Csr o;
+  o.alloc(c, a.n, a.m, a.nnz);
+  CUDA_CHECK(cudaMemcpyAsync(o.rp.p, a.rp.p, sizeof(int32_t) * (a.n + 1), cudaMemcpyDeviceToDevice, c.stream));
+  if (a.nnz) {
+    CUDA_CHECK(cudaMemcpyAsync(o.ci.p, a.ci.p, sizeof(int32_t) * a.nnz, cudaMemcpyDeviceToDevice, c.stream));
+    CUDA_CHECK(cudaMemcpyAsync(o.v.p, a.v.p, sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  return o;
+}
+}  // namespace
+
+int airg_pmisr_pattern(airg_ctx* ctx, const airg_csr* s_pattern, int64_t max_loops, uint64_t seed,
+                       int32_t weight_mode, uint8_t* labels, double* weights) {
+  return guard([&] {
+    need(ctx, "context");
+    need(s_pattern, "pattern");
+    need(labels, "labels");
+    bind(ctx->c);
+    Strength g;
+    strength_from_pattern(ctx->c, s_pattern->m, g);
+    pmisr(ctx->c, g, max_loops, seed, weight_mode, labels, weights);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int airg_pmis_pattern(airg_ctx* ctx, const airg_csr* s_pattern, int32_t swap, uint64_t seed, uint8_t* labels) {
+  return guard([&] {
+    need(ctx, "context");
+    need(s_pattern, "pattern");
+    need(labels, "labels");
+    bind(ctx->c);
+    Strength g;
+    strength_from_pattern(ctx->c, s_pattern->m, g);
+    pmis(ctx->c, g, swap != 0, seed, labels);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int airg_ddc_block(airg_ctx* ctx, const airg_csr* a_ff, uint8_t* labels, int64_t n, double fraction, int64_t bins,
+                   int32_t selection, double direct_alpha, airg_cf_report* rep) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a_ff, "matrix");
+    need(labels, "labels");
+    bind(ctx->c);
+    if (n < 0 || n > INT32_MAX) throw InvalidArgument("ddc: length out of range");
+    Ctx& c = ctx->c;
+    LabelMap map;
+    build_label_map(c, labels, (int32_t)n, map);
+    if (a_ff->m.n != map.nf || a_ff->m.m != map.nf) throw InvalidArgument("ddc: a_ff does not match the labels");
+    DdcResult d = ddc(c, a_ff->m, map, labels, fraction, bins, selection, direct_alpha, true);
+    airg_cf_report r;
+    std::memset(&r, 0, sizeof r);
+    r.n_f_pre = map.nf;
+    r.max_theta = d.max_theta;
+    r.alpha_diag = d.alpha_diag;
+    r.n_converted = d.converted;
+    r.n_f = map.nf - d.converted;
+    r.n_c = n - r.n_f;
+    if (rep) *rep = r;
+  });
+}
+
+int airg_hier_from_levels(airg_ctx* ctx, int64_t n_levels, const airg_csr* const* mats,
+                          const uint8_t* const* d_labels, const airg_csr* coarse_a, const airg_csr* coarse_inv,
+                          int64_t coarse_iterations, airg_hier** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(coarse_a, "coarse matrix");
+    need(coarse_inv, "coarse inverse");
+    need(out, "output handle");
+    if (n_levels < 0) throw InvalidArgument("hierarchy: negative level count");
+    if (n_levels && (!mats || !d_labels)) throw InvalidArgument("hierarchy: null level arrays");
+    bind(ctx->c);
+    Ctx& c = ctx->c;
+    std::vector<HostLevel> lv((size_t)n_levels);
+    for (int64_t l = 0; l < n_levels; ++l) {
+      const airg_csr* const* m = mats + 7 * l;
+      for (int k = 0; k < 7; ++k) need(m[k], "level matrix");
+      need(d_labels[l], "level labels");
+      lv[l].a = copy_csr(c, m[0]->m);
+      lv[l].aff = copy_csr(c, m[1]->m);
+      lv[l].afc = copy_csr(c, m[2]->m);
+      lv[l].acf = copy_csr(c, m[3]->m);
+      lv[l].ffinv = copy_csr(c, m[4]->m);
+      lv[l].r = copy_csr(c, m[5]->m);
+      lv[l].p = copy_csr(c, m[6]->m);
+      lv[l].labels = d_labels[l];
+    }
+    auto h = std::make_unique<airg_hier>();
+    h->c = &c;
+    hier_from_levels(c, lv, copy_csr(c, coarse_a->m), copy_csr(c, coarse_inv->m), coarse_iterations, h->h);
+    *out = h.release();
+  });
+}
+
 // AIRG_CF=legacy: the step-by-step split (materialised S, label map, A_ff)
 static bool cf_split_legacy() {
   static const bool v = [] {

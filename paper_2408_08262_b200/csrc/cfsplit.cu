@@ -633,6 +633,41 @@ void theta_pass(Ctx& c, const Csr& aff, ThetaScratch& s, int rb = 0) {
     LAUNCH(c, theta_rows, blocks_for(aff.n, 256), 256, 0, aff.n, aff.rp.p, aff.ci.p, aff.v.p,
            s.theta.p, s.u.p, s.u.p + 1, rb);
 }
+// histogram of one 8-bit digit of the theta bit patterns (theta >= 0: the
+// bit order is the value order) among the values whose higher digits match
+__global__ void theta_digit_hist(int n, const double* __restrict__ theta, unsigned long long prefix,
+                                 unsigned long long mask, int shift, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(theta[i]);
+    if ((bits & mask) == prefix) atomicAdd(&sh[(bits >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+// the k-th smallest theta (0-based) by an 8-pass radix select over the bits
+double theta_kth(Ctx& c, const double* theta, int n, int64_t k) {
+  DBuf<unsigned> hist(c, 256);
+  unsigned long long prefix = 0, mask = 0;
+  const int blocks = (int)std::min<int64_t>(blocks_for(n, 256), 4 * c.num_sms);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    hist.zero(c);
+    LAUNCH(c, theta_digit_hist, blocks, 256, 0, n, theta, prefix, mask, shift, hist.p);
+    unsigned h[256];
+    to_host(c, h, hist.p, 256);
+    int d = 0;
+    for (; d < 255 && (int64_t)h[d] <= k; ++d) k -= h[d];
+    prefix |= (unsigned long long)d << shift;
+    mask |= 255ull << shift;
+  }
+  double v;
+  memcpy(&v, &prefix, sizeof v);
+  return v;
+}
+
 void throw_zero_diag(unsigned long long row) {
   throw RuntimeError("dominance_report: zero diagonal in A_ff row " + std::to_string(row));
 }
@@ -643,9 +678,29 @@ DdcResult ddc(Ctx& c, const Csr& aff, const LabelMap& map, uint8_t* d_labels, do
   if (aff.n != map.nf) throw InvalidArgument("ddc: a_ff does not match label map");
   if (fraction <= 0.0 || fraction > 1.0) throw InvalidArgument("ddc: fraction must be in (0, 1]");
   if (bins < 1) throw InvalidArgument("dominance_report: bins >= 1");
-  if (selection == 1) throw InvalidArgument("ddc: quickselect selection is not offered on the GPU");
   ThetaScratch s;
   theta_pass(c, aff, s);
+  if (selection == 1) {
+    // exact order statistic (coarsening.cpp:270-288): the value with
+    // round(fraction * n_F) rows strictly above it, by a radix select
+    const int nf = aff.n;
+    unsigned long long u0[3];
+    to_host(c, u0, s.u.p, 3);
+    if (u0[1] != ~0ull) throw_zero_diag(u0[1]);
+    double mx;
+    memcpy(&mx, &u0[0], sizeof mx);
+    int64_t target = (int64_t)std::llround(fraction * (double)nf);
+    target = std::min<int64_t>(std::max<int64_t>(target, 0), nf);
+    double a;
+    if (target == 0 || mx == 0.0)
+      a = mx;
+    else if (target == nf)
+      a = -1.0;
+    else
+      a = theta_kth(c, s.theta.p, nf, nf - target - 1);
+    selection = 2;  // then the direct path with the selected value
+    direct_alpha = a;
+  }
   DBuf<unsigned long long> hist(c, (size_t)bins);
   hist.zero(c);
   DBuf<double> sel(c, 2);

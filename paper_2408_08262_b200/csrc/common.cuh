@@ -39,6 +39,7 @@ struct CudaError : std::runtime_error {
 
 inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e != cudaSuccess) {
+    cudaGetLastError();  // a non-sticky error must not resurface at the next launch check
     char buf[512];
     snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
              cudaGetErrorString(e), file, line, what);

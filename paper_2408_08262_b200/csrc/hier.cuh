@@ -97,6 +97,14 @@ struct RowSplit;
 void setup(Ctx& c, const Csr& a, const airg_setup_config& cfg, const Injection* inj, Hier& h,
            const RowSplit* rs = nullptr);
 void recompute_metrics(Hier& h);
+void alloc_workspace(Ctx& c, Hier& h);
+// a device hierarchy from given level operators (host labels per level)
+struct HostLevel {
+  Csr a, aff, afc, acf, ffinv, r, p;
+  const uint8_t* labels = nullptr;  // device, a.n bytes
+};
+void hier_from_levels(Ctx& c, std::vector<HostLevel>& in, Csr&& coarse_a, Csr&& coarse_inv,
+                      int64_t coarse_iterations, Hier& h);
 
 // fused.cu: the fast V-cycle's fused level operators for `smooths` F-smooths
 void build_fused(Ctx& c, Hier& h, int64_t smooths);

@@ -101,9 +101,10 @@ Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs
   return k;
 }
 
-// Solve-side structures: A_FF with global columns, the tile starts of every
-// matrix the V-cycle streams, and the per-level vectors (fixed pointers, so
-// the V-cycle can be captured into a CUDA graph).
+}  // namespace
+
+// Solve-side structures: A_FF with global columns and the per-level vectors
+// (fixed pointers, so the V-cycle can be captured into a CUDA graph).
 void alloc_workspace(Ctx& c, Hier& h) {
   for (size_t l = 0; l < h.levels.size(); ++l) {
     Level& L = h.levels[l];
@@ -127,8 +128,6 @@ void alloc_workspace(Ctx& c, Hier& h) {
   h.part.alloc(c, (size_t)(kReduceBlocks + (int64_t)top.n * 32 / kTileThreads + 8));
   h.scal.alloc(c, 64);
 }
-
-}  // namespace
 
 void recompute_metrics(Hier& h) {
   const Csr& top = h.top();
@@ -319,6 +318,57 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
   if (cfg.fused_smooths >= 0) build_fused(c, h, cfg.fused_smooths);
   pc.lap(6);
   pc.report();
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+// A device hierarchy from given level operators (the C++ airgraph:: shim
+// hands the GPU solve a host airgraph::Hierarchy): per level A, A_ff, A_fc,
+// A_cf, Aff^-1, R, P (one-point: <= 1 entry of 1.0 per row) and the labels;
+// the coarse operator and its assembled inverse. Vector workspace as setup.
+void hier_from_levels(Ctx& c, std::vector<HostLevel>& in, Csr&& coarse_a, Csr&& coarse_inv,
+                      int64_t coarse_iterations, Hier& h) {
+  h.levels.clear();
+  h.coarse_iterations = coarse_iterations;
+  for (HostLevel& hl : in) {
+    h.levels.emplace_back();
+    Level& L = h.levels.back();
+    L.a = std::move(hl.a);
+    if (L.a.n != L.a.m) throw InvalidArgument("vcycle: level operators must be square");
+    build_label_map(c, hl.labels, L.a.n, L.map);
+    Blocks blk;
+    extract_blocks(c, L.a, L.map, blk, /*want_af=*/true);
+    L.af = std::move(blk.af);
+    L.aff = std::move(hl.aff);
+    L.afc = std::move(hl.afc);
+    L.acf = std::move(hl.acf);
+    L.ffinv = std::move(hl.ffinv);
+    L.r = std::move(hl.r);
+    L.p = std::move(hl.p);
+    if (L.aff.n != L.map.nf || L.ffinv.n != L.map.nf)
+      throw InvalidArgument("vcycle: level blocks do not match the labels");
+    // R and P may be absent (0 x 0) on a level built only for F-smoothing
+    if ((L.r.n || L.r.m) && L.r.m != L.a.n) throw InvalidArgument("vcycle: R does not match the level");
+    if ((L.p.n || L.p.m) && L.p.n != L.a.n) throw InvalidArgument("vcycle: P does not match the level");
+    // one-point P -> map (-1 = empty row)
+    L.pmap.alloc(c, (size_t)std::max(1, L.a.n));
+    std::vector<int32_t> prp(L.p.n + 1), pci(L.p.nnz);
+    std::vector<double> pv(L.p.nnz);
+    to_host(c, prp.data(), L.p.rp.p, prp.size());
+    to_host(c, pci.data(), L.p.ci.p, pci.size());
+    to_host(c, pv.data(), L.p.v.p, pv.size());
+    std::vector<int32_t> pm(L.a.n, -1);
+    for (int i = 0; i < L.p.n; ++i) {
+      const int k0 = prp[i], k1 = prp[i + 1];
+      if (k1 - k0 > 1 || (k1 > k0 && pv[k0] != 1.0))
+        throw InvalidArgument("vcycle: the GPU V-cycle takes one-point prolongation only");
+      if (k1 > k0) pm[i] = pci[k0];
+    }
+    if (L.a.n) to_device(c, L.pmap.p, pm.data(), pm.size());
+  }
+  h.coarse_a = std::move(coarse_a);
+  h.coarse_inv = std::move(coarse_inv);
+  recompute_metrics(h);
+  alloc_workspace(c, h);
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 

@@ -219,6 +219,40 @@ def test_ddc_histogram_within_one(be):  # test_coarsening.cpp:241-270
     assert 9 <= rep.n_converted <= 11
 
 
+def test_ddc_quickselect_exact(be):  # test_coarsening.cpp:241-263 (kQuickSelect)
+    n = 100
+    ts = [(i, i, 1.0) for i in range(n)] + [(i, (i + 1) % n, 0.01 * (i + 1)) for i in range(n)]
+    lab, rep = be.ddc(triplets(n, n, ts), np.zeros(n, np.uint8), fraction=0.10, selection=1)
+    assert rep.n_converted == 10 and (np.flatnonzero(lab) >= 90).all() and lab.sum() == 10
+
+
+def test_ddc_quickselect_edges_and_random(be):  # coarsening.cpp:270-288 edge cases
+    for frac in (0.001, 0.999, 1.0):  # target 0, n_f, n_f
+        n = 50
+        ts = [(i, i, 1.0) for i in range(n)] + [(i, (i + 3) % n, 0.02 * ((7 * i) % n + 1)) for i in range(n)]
+        lab, rep = be.ddc(triplets(n, n, ts), np.zeros(n, np.uint8), fraction=frac, selection=1)
+        want = 0 if frac < 0.01 else n
+        assert rep.n_converted == want, (frac, rep.n_converted)
+    for s in range(4):  # random magnitudes: the exact order statistic's conversions
+        a = be.full_diag(random_sparse(60, 0.1, 900 + s))
+        n, _, rp, ci, v = a
+        theta = []
+        for i in range(n):
+            off, dg = 0.0, 0.0
+            for k in range(rp[i], rp[i + 1]):
+                if ci[k] == i:
+                    dg = abs(v[k])
+                else:
+                    off += abs(v[k])
+            theta.append(off / dg)
+        theta = np.array(theta)
+        target = int(np.round(0.25 * n))
+        alpha = np.sort(theta)[n - target - 1]
+        want = np.flatnonzero((theta > alpha) & (theta != 0))
+        lab, rep = be.ddc(a, np.zeros(n, np.uint8), fraction=0.25, selection=1)
+        assert np.array_equal(np.flatnonzero(lab), want), s
+
+
 def test_ddc_measures_theta_once(be):  # test_coarsening.cpp:272-289
     a = triplets(3, 3, [(0, 0, 1.0), (0, 1, 3.0), (1, 0, 3.0), (1, 1, 1.0), (2, 2, 1.0)])
     lab, rep = be.ddc(a, [0, 0, 0], selection=2, direct=2.0)
