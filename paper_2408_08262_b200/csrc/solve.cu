@@ -776,12 +776,20 @@ constexpr int kGmMax = 32;      // restart lengths served on the device (m <= 32
 constexpr int kGmThreads = 256;
 
 
-// Sum 32 per-lane vectors over the warp: butterfly transpose-reduce, 31
-// shuffles instead of 32 x 5; on return lane l holds the total of entry l.
-__device__ __forceinline__ double warp_transpose_sum32(double (&v)[kGmMax]) {
+// Sum K per-lane vectors (K a power of two <= 32) over the warp: butterfly
+// adds over the lane bits >= log2 K, then a transpose-reduce over the low
+// bits (K (5 - log2 K) + K - 1 shuffles instead of 5 K); on return lane l
+// holds the warp total of entry l mod K.
+template <int K>
+__device__ __forceinline__ double warp_transpose_sum(double (&v)[K]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
+  for (int o = 16; o >= K; o >>= 1) {
+#pragma unroll
+    for (int t = 0; t < K; ++t) v[t] += __shfl_xor_sync(0xffffffffu, v[t], o);
+  }
+#pragma unroll
+  for (int s = K / 2; s >= 1; s >>= 1) {
     const bool up = lane & s;
 #pragma unroll
     for (int t = 0; t < s; ++t) {
@@ -796,36 +804,32 @@ __device__ __forceinline__ double warp_transpose_sum32(double (&v)[kGmMax]) {
 // One element per thread (a grid of n / 256 blocks: enough independent
 // loads in flight to cover the HBM latency); V_0..V_j of the element in
 // registers, so the update and the following dots read V once; the dots of
-// a warp reduced by one transpose-reduce (31 shuffles for all k).
+// a warp reduced by one transpose-reduce. The code is specialised on K, the
+// basis size rounded up to a power of two (warp-uniform branch on the
+// device-side j): ncu showed the fixed 32-wide version issue bound (65 %).
 // MODE 0: dots V_k . w;  1: w -= V h, then dots V_k . w;  2: w -= V h, then |w|^2.
 // Per block, one partial per k: part[k * nblocks + block].
-template <int MODE>
-__global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double* __restrict__ V,
-                                                         double* __restrict__ w, const GmDev* __restrict__ st,
-                                                         const double* __restrict__ h, double* __restrict__ part) {
-  __shared__ double hs[kGmMax];
-  __shared__ double red[kGmThreads / 32][kGmMax];
-  pdl_wait();
-  pdl_trigger();
-  const int jp1 = st->j + 1;
-  if (threadIdx.x < kGmMax) hs[threadIdx.x] = (MODE > 0 && (int)threadIdx.x < jp1) ? h[threadIdx.x] : 0.0;
-  __syncthreads();
+template <int MODE, int K>
+__device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* __restrict__ V,
+                                              double* __restrict__ w, const double* hs,
+                                              double (*red)[kGmMax], double* __restrict__ part) {
   const int64_t i = (int64_t)blockIdx.x * kGmThreads + threadIdx.x;
   const bool live = i < n;
-  double vk[kGmMax];
+  double vk[K];
 #pragma unroll
-  for (int k = 0; k < kGmMax; ++k) vk[k] = (live && k < jp1) ? __ldg(V + (int64_t)k * n + i) : 0.0;
+  for (int k = 0; k < K; ++k) vk[k] = (live && k < jp1) ? __ldg(V + (int64_t)k * n + i) : 0.0;
   double wi = live ? w[i] : 0.0;
   if (MODE > 0) {
 #pragma unroll
-    for (int k = 0; k < kGmMax; ++k) wi = fma(-hs[k], vk[k], wi);
+    for (int k = 0; k < K; ++k) wi = fma(-hs[k], vk[k], wi);
     if (live) w[i] = wi;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (MODE < 2) {
 #pragma unroll
-    for (int k = 0; k < kGmMax; ++k) vk[k] *= wi;
-    red[warp][lane] = warp_transpose_sum32(vk);
+    for (int k = 0; k < K; ++k) vk[k] *= wi;
+    const double t = warp_transpose_sum<K>(vk);
+    if (lane < K) red[warp][lane] = t;
   } else {
     double p = wi * wi;
 #pragma unroll
@@ -839,6 +843,27 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double
     for (int q = 0; q < kGmThreads / 32; ++q) v += red[q][threadIdx.x];
     part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double* __restrict__ V,
+                                                         double* __restrict__ w, const GmDev* __restrict__ st,
+                                                         const double* __restrict__ h, double* __restrict__ part) {
+  __shared__ double hs[kGmMax];
+  __shared__ double red[kGmThreads / 32][kGmMax];
+  pdl_wait();
+  pdl_trigger();
+  const int jp1 = st->j + 1;
+  if (threadIdx.x < kGmMax) hs[threadIdx.x] = (MODE > 0 && (int)threadIdx.x < jp1) ? h[threadIdx.x] : 0.0;
+  __syncthreads();
+  if (jp1 <= 4)
+    gm_sweep_body<MODE, 4>(n, jp1, V, w, hs, red, part);
+  else if (jp1 <= 8)
+    gm_sweep_body<MODE, 8>(n, jp1, V, w, hs, red, part);
+  else if (jp1 <= 16)
+    gm_sweep_body<MODE, 16>(n, jp1, V, w, hs, red, part);
+  else
+    gm_sweep_body<MODE, 32>(n, jp1, V, w, hs, red, part);
 }
 
 // h[k] = sum over blocks of part[k][.] (k <= j, or k = 0 for the norm):

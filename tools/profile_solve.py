@@ -10,9 +10,6 @@ import sys
 
 import numpy as np
 
-# profilers see the kernels of the host-driven loop (conditional graph bodies are
-# opaque to CUPTI / ncu)
-os.environ.setdefault("AIRG_DEVLOOP", "0")
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -25,10 +22,19 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--what", default="solve")
     ap.add_argument("--outer", type=int, default=None, help="1 = outer GMRES(30) (default for C0 / C4)")
+    ap.add_argument("--fast", type=int, default=1, help="1 = fast mode (the bench's), 0 = exact")
     args = ap.parse_args()
+    # profilers do not see the kernels of conditional graph bodies: Richardson
+    # runs its host-driven loop (AIRG_DEVLOOP=0), GMRES the device-resident
+    # kernels launched one by one (AIRG_GM_FLAT=1)
+    gm = args.outer if args.outer is not None else int(args.config in (0, 4))
+    if gm:
+        os.environ.setdefault("AIRG_GM_FLAT", "1")
+    else:
+        os.environ.setdefault("AIRG_DEVLOOP", "0")
     ctx = airg.Context(0)
     p = problems.make(args.config, args.scale)
-    prm = problems.setup_params(args.config)
+    prm = dict(problems.setup_params(args.config), fused_smooths=2 if args.fast else -1)
     a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
     dA = airg.DeviceCSR.upload(a, ctx)
     if args.what == "setup":
@@ -43,7 +49,7 @@ def main():
     tb = ctx.to_device(p.b)
     tx = ctx.empty(p.n, torch.float64)
     outer = args.outer if args.outer is not None else int(args.config in (0, 4))
-    sk = dict(coarse_iterations=prm["coarse_iterations"], outer=outer)
+    sk = dict(coarse_iterations=prm["coarse_iterations"], outer=outer, fast=args.fast, max_iterations=400)
     for _ in range(2):
         st, _ = h.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
