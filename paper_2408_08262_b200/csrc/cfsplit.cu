@@ -1066,6 +1066,17 @@ __global__ void fcf_marks_lanes(int n, const int32_t* __restrict__ rp, const int
   if (live && lane == 0 && (any & grp)) notmin[i] = 1;
 }
 
+// zero a level's scratch (counters, histogram, counts, marks) as a kernel, so
+// it joins the PDL chain (a memset node would break it); waits for the
+// previous split that used the same scratch
+__global__ void fcf_zero(unsigned long long* __restrict__ w, int64_t words, unsigned long long* __restrict__ u8) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t k = t; k < words; k += (int64_t)gridDim.x * blockDim.x) w[k] = 0ull;
+  if (u8 && t < 8) u8[t] = 0ull;
+}
+
 // lanes per row of the order-free passes: the fewest lanes (a power of two)
 // with about 4 entries each, at most 4 (1 = the thread-per-row passes).
 // Measured on all levels back to back: C2 2.53 -> 2.32 ms, C4 1.37 -> 1.25
@@ -1214,8 +1225,9 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   const size_t head = (zero_bytes + 15) & ~(size_t)15;
   const size_t bytes = head + 2 * (size_t)n * 8;
   uint8_t* base = static_cast<uint8_t*>(ctx_scratch(c, bytes));
-  unsigned long long* u = reinterpret_cast<unsigned long long*>(base);
-  unsigned long long* hist = u + 8;
+  // the report counters: straight into d_u_out when given (no copy-out node)
+  unsigned long long* u = d_u_out ? d_u_out : reinterpret_cast<unsigned long long*>(base);
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(base) + 8;
   int2* cnt = reinterpret_cast<int2*>(hist + nb);
   uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + n);
   double* thr = reinterpret_cast<double*>(base + head);
@@ -1224,7 +1236,11 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
   const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
-  CUDA_CHECK(cudaMemsetAsync(base, 0, zero_bytes, c.stream));
+  {
+    const int64_t words = (int64_t)((zero_bytes + 7) / 8);
+    const unsigned gz = (unsigned)std::min<int64_t>(4 * c.num_sms, (words + 255) / 256 + 1);
+    LAUNCH_PDL(c, fcf_zero, gz, 256, 0, reinterpret_cast<unsigned long long*>(base), words, d_u_out);
+  }
   auto* k_rows = vec ? fcf_rows<true> : fcf_rows<false>;
   auto* k_marks = vec ? fcf_marks<true> : fcf_marks<false>;
   auto* k_theta = vec ? fcf_theta<true> : fcf_theta<false>;
@@ -1259,9 +1275,7 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
     if (d_labels_pre)
       CUDA_CHECK(cudaMemcpyAsync(d_labels_pre, d_labels, n, cudaMemcpyDeviceToDevice, c.stream));
   }
-  if (!d_u_out) return u;
-  CUDA_CHECK(cudaMemcpyAsync(d_u_out, u, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c.stream));
-  return d_u_out;
+  return u;
 }
 
 CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_enabled, const uint8_t* d_labels) {
