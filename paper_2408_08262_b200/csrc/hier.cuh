@@ -56,7 +56,7 @@ struct Hier {
   // device-resident GMRES (solve.cu): state, Hessenberg / rotation scalars,
   // dot partials, history, the cycle residual and the nested-WHILE graph
   DBuf<GmDev> gm_st;
-  DBuf<double> gm_H, gm_cs, gm_sn, gm_g, gm_y, gm_h, gm_part, gm_hist, r2;
+  DBuf<double> gm_H, gm_cs, gm_sn, gm_g, gm_y, gm_h, gm_part, gm_hist, r2, gm_G;
   cudaGraphExec_t g_gm = nullptr;
   int64_t g_key_gm = -1;
   uint64_t gm_kernels[3] = {0, 0, 0};  // launch, per cycle, per Arnoldi step

@@ -807,12 +807,15 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[K]) {
 // a warp reduced by one transpose-reduce. The code is specialised on K, the
 // basis size rounded up to a power of two (warp-uniform branch on the
 // device-side j): ncu showed the fixed 32-wide version issue bound (65 %).
-// MODE 0: dots V_k . w;  1: w -= V h, then dots V_k . w;  2: w -= V h, then |w|^2.
-// Per block, one partial per k: part[k * nblocks + block].
+// MODE 0: dots V_k . w;  1: w -= V h, then dots V_k . w;  2: w -= V h, then |w|^2;
+// 3: dots V_k . w and V_k . v_j (fast mode's Gram-corrected CGS2, below).
+// Per block, one partial per k: part[k * nblocks + block] (MODE 3: the Gram
+// column at rows kGmMax + 1 + k).
 template <int MODE, int K>
 __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* __restrict__ V,
                                               double* __restrict__ w, const double* hs,
-                                              double (*red)[kGmMax], double* __restrict__ part) {
+                                              double (*red)[kGmMax], double (*red2)[kGmMax],
+                                              double* __restrict__ part) {
   const int64_t i = (int64_t)blockIdx.x * kGmThreads + threadIdx.x;
   const bool live = i < n;
   double vk[K];
@@ -825,7 +828,24 @@ __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* 
     if (live) w[i] = wi;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (MODE < 2) {
+  if (MODE == 3) {  // V^T w and V^T v_j (the Gram column of the newest vector)
+    double vj = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k == jp1 - 1) vj = vk[k];
+    double gk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      gk[k] = vk[k] * vj;
+      vk[k] *= wi;
+    }
+    const double t = warp_transpose_sum<K>(vk);
+    const double tg = warp_transpose_sum<K>(gk);
+    if (lane < K) {
+      red[warp][lane] = t;
+      red2[warp][lane] = tg;
+    }
+  } else if (MODE < 2) {
 #pragma unroll
     for (int k = 0; k < K; ++k) vk[k] *= wi;
     const double t = warp_transpose_sum<K>(vk);
@@ -837,11 +857,18 @@ __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* 
     if (lane == 0) red[warp][0] = p;
   }
   __syncthreads();
-  if ((int)threadIdx.x < (MODE < 2 ? jp1 : 1)) {
+  if ((int)threadIdx.x < (MODE != 2 ? jp1 : 1)) {
     double v = 0.0;
 #pragma unroll
     for (int q = 0; q < kGmThreads / 32; ++q) v += red[q][threadIdx.x];
     part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
+  }
+  if (MODE == 3 && (int)threadIdx.x >= 32 && (int)threadIdx.x < 32 + jp1) {
+    const int k = threadIdx.x - 32;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kGmThreads / 32; ++q) v += red2[q][k];
+    part[(int64_t)(kGmMax + 1 + k) * gridDim.x + blockIdx.x] = v;
   }
 }
 
@@ -851,19 +878,21 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double
                                                          const double* __restrict__ h, double* __restrict__ part) {
   __shared__ double hs[kGmMax];
   __shared__ double red[kGmThreads / 32][kGmMax];
+  __shared__ double red2[MODE == 3 ? kGmThreads / 32 : 1][kGmMax];
   pdl_wait();
   pdl_trigger();
   const int jp1 = st->j + 1;
-  if (threadIdx.x < kGmMax) hs[threadIdx.x] = (MODE > 0 && (int)threadIdx.x < jp1) ? h[threadIdx.x] : 0.0;
+  if (threadIdx.x < kGmMax)
+    hs[threadIdx.x] = ((MODE == 1 || MODE == 2) && (int)threadIdx.x < jp1) ? h[threadIdx.x] : 0.0;
   __syncthreads();
   if (jp1 <= 4)
-    gm_sweep_body<MODE, 4>(n, jp1, V, w, hs, red, part);
+    gm_sweep_body<MODE, 4>(n, jp1, V, w, hs, red, red2, part);
   else if (jp1 <= 8)
-    gm_sweep_body<MODE, 8>(n, jp1, V, w, hs, red, part);
+    gm_sweep_body<MODE, 8>(n, jp1, V, w, hs, red, red2, part);
   else if (jp1 <= 16)
-    gm_sweep_body<MODE, 16>(n, jp1, V, w, hs, red, part);
+    gm_sweep_body<MODE, 16>(n, jp1, V, w, hs, red, red2, part);
   else
-    gm_sweep_body<MODE, 32>(n, jp1, V, w, hs, red, part);
+    gm_sweep_body<MODE, 32>(n, jp1, V, w, hs, red, red2, part);
 }
 
 // h[k] = sum over blocks of part[k][.] (k <= j, or k = 0 for the norm):
@@ -875,10 +904,13 @@ __global__ void __launch_bounds__(kFinThreads) k_gm_finish(const double* __restr
                                                            double* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const int k = blockIdx.x;
+  // blocks 0..kGmMax-1: rows k <= j; blocks kGmMax..: the Gram rows kGmMax+1+k
+  const int kb = blockIdx.x;
+  const int k = kb < kGmMax ? kb : kb - kGmMax;
   if (k > (norm ? 0 : st->j)) return;
+  const int row = kb < kGmMax ? k : kGmMax + 1 + k;
   __shared__ double sm[32];
-  const double* p = part + (int64_t)k * nb;
+  const double* p = part + (int64_t)row * nb;
   double s = 0.0;
   for (int b0 = threadIdx.x; b0 < nb; b0 += 8 * kFinThreads) {
     double v[8];
@@ -898,7 +930,7 @@ __global__ void __launch_bounds__(kFinThreads) k_gm_finish(const double* __restr
     s = sm[threadIdx.x];
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) out[k] = s;
+    if (threadIdx.x == 0) out[row] = s;
   }
 }
 
@@ -948,6 +980,35 @@ __global__ void k_gm_cycle(cudaGraphConditionalHandle hin, int cond, int64_t n, 
     st->j = 0;
     if (cond) cudaGraphSetConditional(hin, st->its < st->maxit ? 1u : 0u);
   }
+}
+
+// Fast mode's CGS2 with one sweep fewer: the reorthogonalisation
+// coefficients h2 = V^T (w - V h1) = h1 - G h1 from the Gram matrix G = V^T V
+// (its newest column comes with the first dots), so w'' = w - V (h1 + h2)
+// is one sweep. Equal to CGS2 in exact arithmetic; it corrects the basis's
+// loss of orthogonality, not the cancellation in forming w - V h1 (the
+// parity tests bound the solve). d[0..j] = h1, d[kGmMax+1..] = G's column j;
+// out: h2 (so k_gm_step's hcol = h1 + h2 is unchanged) and hsum = h1 + h2.
+__global__ void k_gm_gram(const GmDev* __restrict__ st, const double* __restrict__ d, double* __restrict__ G,
+                          double* __restrict__ h2, double* __restrict__ hsum) {
+  __shared__ double h1s[kGmMax];
+  pdl_wait();
+  pdl_trigger();
+  const int j = st->j, t = threadIdx.x;
+  const int m1 = kGmMax + 1;
+  if (t <= j) {
+    h1s[t] = d[t];
+    const double gk = d[kGmMax + 1 + t];
+    G[t * m1 + j] = gk;
+    G[j * m1 + t] = gk;
+  }
+  __syncthreads();
+  if (t > j) return;
+  double s = 0.0;
+  for (int l = 0; l <= j; ++l) s = fma(G[t * m1 + l], h1s[l], s);
+  const double c = h1s[t] - s;
+  h2[t] = c;
+  hsum[t] = h1s[t] + c;
 }
 
 // the Arnoldi step's scalar work (gmres_poly-free, oracle gmres() order):
@@ -1114,12 +1175,13 @@ struct GmPieces {
   int64_t n;
   int nb, ns;  // element grid, sweep grid
   GmDev* st;
-  double *V, *Z, *w, *H, *cs, *sn, *g, *y, *h1, *h2, *nrm, *part;
+  double *V, *Z, *w, *H, *cs, *sn, *g, *y, *h1, *h2, *nrm, *part, *d, *hsum, *G;
   GmPieces(Ctx& c_, Hier& h_, const airg_solve_config& cfg_)
       : c(c_), h(h_), cfg(cfg_), n(h_.top_n()), nb(gm_blocks(h_.top_n())), ns(gm_sweep_blocks(c_, h_.top_n())),
         st(h_.gm_st.p), V(h_.V.p), Z(h_.Z.p),
         w(h_.w.p), H(h_.gm_H.p), cs(h_.gm_cs.p), sn(h_.gm_sn.p), g(h_.gm_g.p), y(h_.gm_y.p), h1(h_.gm_h.p),
-        h2(h_.gm_h.p + (kGmMax + 1)), nrm(h_.gm_h.p + 2 * (kGmMax + 1)), part(h_.gm_part.p) {}
+        h2(h_.gm_h.p + (kGmMax + 1)), nrm(h_.gm_h.p + 2 * (kGmMax + 1)), part(h_.gm_part.p),
+        d(h_.gm_h.p + 3 * (kGmMax + 1)), hsum(h_.gm_h.p + 5 * (kGmMax + 1)), G(h_.gm_G.p) {}
   void norm_b() { dot_async(c, h.rhs.p, h.rhs.p, n, h.scal.p + 1, h.part.p); }
   void init(cudaGraphConditionalHandle hout, int cond) {
     LAUNCH(c, k_gm_init, 1, 32, 0, hout, cond, (const double*)(h.scal.p + 1), st, h.gm_hist.p);
@@ -1140,16 +1202,27 @@ struct GmPieces {
     enqueue_vcycle(c, h, cfg, h.r.p);
     const double* z = vcycle_output(h);
     ROWS(EpiGmSpmv, h.top(), z, (EpiGmSpmv{w, z, Z, st, n}));
-    LAUNCH_PDL(c, k_gm_sweep<0>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-               (const double*)nullptr, part);
-    LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h1);
-    LAUNCH_PDL(c, k_gm_sweep<1>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-               (const double*)h1, part);
-    LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h2);
-    LAUNCH_PDL(c, k_gm_sweep<2>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-               (const double*)h2, part);
+    const double* hcol1 = h1;
+    if (fast) {  // Gram-corrected CGS2: two sweeps (k_gm_gram)
+      LAUNCH_PDL(c, k_gm_sweep<3>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+                 (const double*)nullptr, part);
+      LAUNCH_PDL(c, k_gm_finish, 2 * kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, d);
+      LAUNCH_PDL(c, k_gm_gram, 1, 32, 0, (const GmDev*)st, (const double*)d, G, h2, hsum);
+      LAUNCH_PDL(c, k_gm_sweep<2>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+                 (const double*)hsum, part);
+      hcol1 = d;
+    } else {  // CGS2 as the oracle: three sweeps
+      LAUNCH_PDL(c, k_gm_sweep<0>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+                 (const double*)nullptr, part);
+      LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h1);
+      LAUNCH_PDL(c, k_gm_sweep<1>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+                 (const double*)h1, part);
+      LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h2);
+      LAUNCH_PDL(c, k_gm_sweep<2>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
+                 (const double*)h2, part);
+    }
     LAUNCH_PDL(c, k_gm_finish, 1, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 1, nrm);
-    LAUNCH_PDL(c, k_gm_step, 1, 32, 0, hin, cond, st, (const double*)h1, (const double*)h2, (const double*)nrm, H,
+    LAUNCH_PDL(c, k_gm_step, 1, 32, 0, hin, cond, st, hcol1, (const double*)h2, (const double*)nrm, H,
                cs, sn, g, h.gm_hist.p);
     LAUNCH_PDL(c, k_gm_next, (unsigned)nb, kGmThreads, 0, n, (const double*)w, (const GmDev*)st, V, h.r.p);
   }
@@ -1252,8 +1325,9 @@ bool gmres_device(Ctx& c, Hier& h, const airg_solve_config& cfg, int m, airg_sol
     h.gm_sn.alloc(c, kGmMax);
     h.gm_g.alloc(c, kGmMax + 1);
     h.gm_y.alloc(c, kGmMax);
-    h.gm_h.alloc(c, 3 * (kGmMax + 1));
-    h.gm_part.alloc(c, (size_t)(kGmMax + 1) * nb);
+    h.gm_h.alloc(c, 6 * (kGmMax + 1));
+    h.gm_G.alloc(c, (size_t)(kGmMax + 1) * (kGmMax + 1));
+    h.gm_part.alloc(c, (size_t)2 * (kGmMax + 1) * nb);
   }
   if (h.gm_hist.n < (size_t)cap) {
     h.gm_hist.alloc(c, (size_t)cap);
