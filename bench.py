@@ -98,10 +98,12 @@ def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2, fast=False):
 def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, fast=False):
     """Algorithmic HBM bytes of one GMRES(m) solve. Per Arnoldi step j (one
     outer iteration): the V-cycle (vcycle_alg_bytes), w = A z (SpMV + z
-    written), classical Gram-Schmidt twice -- at least three sweeps over
+    written), classical Gram-Schmidt twice -- exact mode: three sweeps over
     V_0..V_j (dots; first update fused with the second dots; second update
-    with the norm) plus w read/written per sweep -- and v_{j+1} = w / |w|.
-    Per restart: x += Z y (j + 2 vectors), r = b - A x and its norm."""
+    with the norm); fast mode: two (dots with w and v_j; the update with the
+    Gram-corrected coefficients and the norm) -- plus w read / written per
+    sweep, and v_{j+1} = w / |w|. Per restart: x += Z y (j + 2 vectors),
+    r = b - A x and its norm."""
     info = h.info()
     top = h.level(0) if info.n_levels else None
     n = top.n if top else info.coarse_n
@@ -113,7 +115,8 @@ def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, 
     while left > 0:
         j_max = min(restart, left)
         for j in range(j_max):
-            tot += cyc + spmv + 8 * n + 3 * (j + 1) * 8 * n + 5 * 8 * n + 16 * n
+            sweeps = 2 if fast else 3
+            tot += cyc + spmv + 8 * n + sweeps * (j + 1) * 8 * n + (2 * sweeps - 1) * 8 * n + 24 * n
         tot += (j_max + 2) * 8 * n + spmv + 8 * n
         left -= j_max
     return tot
