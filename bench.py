@@ -418,6 +418,12 @@ def run_gpu_dist(args):
     starts = np.arange(ws + 1, dtype=np.int64) * slab
     d = airg.Dist(h, ws, rank=rank, comm=comm, threshold=2.0, starts=starts)
     lo, hi = starts[rank], starts[rank + 1]
+    # device bytes of this rank's slabs (the distribution owns them; the
+    # replicated global hierarchy is only needed by the setup and the CF
+    # split timing below)
+    trb = torch.tensor([float(d.rank_bytes())], device=ctx.tdev, dtype=torch.float64)
+    dist.all_reduce(trb, op=dist.ReduceOp.MAX)
+    max_rank_bytes = float(trb[0])
     # CF split at N GPUs: the row-slab PMISR-DDC (airg_dist_cf_split) on
     # every level's operator with that level's slabs; max over ranks
     cf_ms = 0.0
@@ -521,6 +527,7 @@ def run_gpu_dist(args):
         "iterations": int(st.iterations), "final_relative_residual": float(st.final_relative_residual),
         "levels": int(h.n_levels), "setup_ms": setup_ms,
         "active_ranks": [lv["active"] for lv in levels],
+        "max_rank_solve_bytes": max_rank_bytes,
         "e2e": {"value": p.n / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
                 "d2h_bytes_per_step": 8 * int(hi - lo), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches), "cf_split_ms": cf_ms,

@@ -401,6 +401,10 @@ int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg,
  * emulated ranks in emulation mode; NVLink traffic of the solve). */
 int airg_dist_halo_bytes(const airg_dist* d, const airg_solve_config* cfg, int64_t* vcycle_bytes,
                          int64_t* spmv_bytes);
+/* Device bytes of one rank's share of the distributed hierarchy (its slabs
+ * of every level's operators, maps and solve vectors). The distribution owns
+ * its slabs: the global hierarchy may be destroyed once it is created. */
+int airg_dist_rank_bytes(const airg_dist* d, int32_t rank, int64_t* bytes);
 /* local_share (partition_model.cpp:66-75) of a level before / after its
  * halving decision (levels below n_levels). */
 int airg_dist_level_share(const airg_dist* d, int64_t level, double* share_before, double* share_after);

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                                  C.c_int64], C.c_int),
+            "airg_dist_rank_bytes": ([_VP, C.c_int32, _P(C.c_int64)], C.c_int),
             "airg_dist_level_share": ([_VP, C.c_int64, _P(C.c_double), _P(C.c_double)], C.c_int),
             "airg_dist_halo_bytes": ([_VP, _P(abi.SolveConfig), _P(C.c_int64), _P(C.c_int64)], C.c_int),
             "airg_dist_level_info": ([_VP, C.c_int64, _P(C.c_int32), _P(C.c_double), _P(C.c_double),
@@ -621,6 +622,10 @@ class Hierarchy:
         self.coarse_iterations = int(cfg.coarse_iterations)
 
     def __del__(self):
+        self.close()
+
+    def close(self):
+        """Free the device hierarchy now (e.g. once a Dist holds its slabs)."""
         if getattr(self, "h", None):
             try:
                 lib().airg_hier_destroy(self.h)
@@ -891,6 +896,23 @@ class Dist:
                                       C.byref(out)))
         self.d = out
         self._comm = comm
+        # level sizes kept here: the distribution owns its slabs, so the global
+        # hierarchy may be closed once it exists (release_hierarchy)
+        self.n_levels = h.n_levels
+        self._levels = [(h.level(l).n, h.level(l).nnz) for l in range(self.n_levels)]
+        hi = h.info()
+        self._coarse = (hi.coarse_n, hi.coarse_nnz)
+
+    def release_hierarchy(self):
+        """Drop this distribution's reference to the global hierarchy: only
+        the per-rank slabs stay resident (call h.close() to free it now)."""
+        self.h = None
+
+    def rank_bytes(self, rank: int | None = None) -> int:
+        """Device bytes of one rank's slabs (airg_dist_rank_bytes)."""
+        b = C.c_int64()
+        _check(lib().airg_dist_rank_bytes(self.d, int(self.rank if rank is None else rank), C.byref(b)))
+        return b.value
 
     def __del__(self):
         if getattr(self, "d", None):
@@ -916,7 +938,7 @@ class Dist:
                                           C.byref(halo), starts.ctypes.data))
         out = dict(active=a.value, ratio_before=rb.value, ratio_after=ra.value, triggered=bool(t.value),
                    halo=halo.value, starts=starts)
-        if l < self.h.n_levels:
+        if l < self.n_levels:
             sb, sa = C.c_double(), C.c_double()
             _check(lib().airg_dist_level_share(self.d, int(l), C.byref(sb), C.byref(sa)))
             out.update(share_before=sb.value, share_after=sa.value)

@@ -1049,6 +1049,37 @@ int airg_dist_halo_bytes(const airg_dist* dp, const airg_solve_config* cfg, int6
   });
 }
 
+int airg_dist_rank_bytes(const airg_dist* dp, int32_t rank, int64_t* bytes) {
+  return guard([&] {
+    need(dp, "dist");
+    need(bytes, "bytes");
+    const DHier& d = dp->d;
+    if (rank < 0 || rank >= d.P) throw InvalidArgument("dist: rank out of range");
+    if (!d.mine(rank)) throw InvalidArgument("dist: rank is not held by this process");
+    auto csr = [](const Csr& m) {
+      return (int64_t)(m.rp.n * sizeof(int32_t) + m.ci.n * sizeof(int32_t) + m.v.n * sizeof(double));
+    };
+    auto vec = [&](const DVec& V) {
+      return rank < (int)V.rk.size() ? (int64_t)(V.rk[rank].buf.n * sizeof(double)) : (int64_t)0;
+    };
+    int64_t b = 0;
+    for (const DLevel& D : d.lv) {
+      if (rank < (int)D.rk.size()) {
+        const DLevel::Rank& R = D.rk[rank];
+        b += csr(R.R) + csr(R.AF) + csr(R.AFFG) + csr(R.FINV);
+        b += (int64_t)((R.pmap.n + R.f2f.n) * sizeof(int32_t) + R.sc.n * sizeof(double));
+      }
+      b += vec(D.B) + vec(D.X) + vec(D.RF);
+    }
+    if (rank < (int)d.rk.size()) {
+      const DHier::Rank& T = d.rk[rank];
+      b += csr(T.A0) + csr(T.AC) + csr(T.ACI) + (int64_t)(T.rhs.n * sizeof(double));
+    }
+    b += vec(d.CB) + vec(d.CX) + vec(d.CR) + vec(d.XS);
+    *bytes = b;
+  });
+}
+
 int airg_dist_level_share(const airg_dist* dp, int64_t l, double* share_before, double* share_after) {
   return guard([&] {
     need(dp, "dist");

@@ -71,12 +71,12 @@ def partition_report(d: "airg.Dist", initial_ranks: int, threshold: float) -> di
     on every hierarchy level, then the coarsest grid gathered on one GPU (the
     reference's model applies the rule once more there; the GPU gathers)."""
     levels, triggers = [], []
-    for l in range(d.h.n_levels):
+    for l in range(d.n_levels):
         li = d.level_info(l)
-        lv = d.h.level(l)
+        n, nnz = d._levels[l]
         finite = math.isfinite(li["ratio_after"])
         levels.append({
-            "level": l, "n": lv.n, "nnz": lv.nnz, "active_ranks": li["active"],
+            "level": l, "n": n, "nnz": nnz, "active_ranks": li["active"],
             "triggered": li["triggered"],
             "ratio": li["ratio_after"] if finite else None,
             "ratio_before_trigger": li["ratio_before"] if math.isfinite(li["ratio_before"]) else None,
@@ -84,8 +84,8 @@ def partition_report(d: "airg.Dist", initial_ranks: int, threshold: float) -> di
         })
         if li["triggered"]:
             triggers.append(l)
-    info = d.h.info()
-    levels.append({"level": d.h.n_levels, "n": info.coarse_n, "nnz": info.coarse_nnz, "active_ranks": 1,
+    cn, cz = d._coarse
+    levels.append({"level": d.n_levels, "n": cn, "nnz": cz, "active_ranks": 1,
                    "triggered": False, "ratio": None, "ratio_before_trigger": None, "local_share": 1.0,
                    "gathered": True})
     return {"initial_ranks": initial_ranks, "threshold": threshold, "levels": levels,

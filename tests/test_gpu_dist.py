@@ -302,3 +302,23 @@ def test_dist_halo_bytes_accounting():
     # the three slab boundaries (one-sided halo)
     assert s == 8 * 3 * 24 * 24
     assert v > s and v % 8 == 0 and v >= 8 * d.level_info(0)["halo"]
+
+
+def test_dist_owns_its_slabs_and_memory_scales():
+    """Each rank of a distribution holds only its slabs (operators, maps,
+    vectors; the coarsest grid on rank 0): with 4 ranks the largest share is
+    well under half of the one-rank total, and the global hierarchy can be
+    freed -- the solve still gives the one-GPU bits."""
+    p = problems.c2_structured_3d(24)
+    prm = dict(problems.setup_params(2), coarse_size_target=300)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    ref = airg.richardson_solve(h, p.b, coarse_iterations=3)
+    one = airg.Dist(h, 1).rank_bytes(0)
+    d = airg.Dist(h, 4, threshold=0.0, starts=np.linspace(0, p.n, 5).astype(np.int64))
+    shares = [d.rank_bytes(r) for r in range(4)]
+    assert max(shares) < 0.4 * one and sum(shares) < 1.3 * one, (shares, one)
+    d.release_hierarchy()
+    h.close()
+    del h
+    res = d.solve(p.b, coarse_iterations=3)
+    assert res.stats.iterations == ref.stats.iterations and same_bits(res.x, ref.x)
