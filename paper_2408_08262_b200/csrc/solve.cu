@@ -833,17 +833,34 @@ __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* 
 #pragma unroll
     for (int k = 0; k < K; ++k)
       if (k == jp1 - 1) vj = vk[k];
-    double gk[K];
+    if constexpr (K <= 16) {  // both K-vectors in ONE 2K-wide transpose-reduce
+      double both[2 * K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      gk[k] = vk[k] * vj;
-      vk[k] *= wi;
-    }
-    const double t = warp_transpose_sum<K>(vk);
-    const double tg = warp_transpose_sum<K>(gk);
-    if (lane < K) {
-      red[warp][lane] = t;
-      red2[warp][lane] = tg;
+      for (int k = 0; k < K; ++k) {
+        both[k] = vk[k] * wi;
+        both[K + k] = vk[k] * vj;
+      }
+      const double t = warp_transpose_sum<2 * K>(both);
+      const int e = lane & (2 * K - 1);
+      if (lane < 2 * K) {
+        if (e < K)
+          red[warp][e] = t;
+        else
+          red2[warp][e - K] = t;
+      }
+    } else {
+      double gk[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        gk[k] = vk[k] * vj;
+        vk[k] *= wi;
+      }
+      const double t = warp_transpose_sum<K>(vk);
+      const double tg = warp_transpose_sum<K>(gk);
+      if (lane < K) {
+        red[warp][lane] = t;
+        red2[warp][lane] = tg;
+      }
     }
   } else if (MODE < 2) {
 #pragma unroll
