@@ -322,3 +322,23 @@ def test_dist_owns_its_slabs_and_memory_scales():
     del h
     res = d.solve(p.b, coarse_iterations=3)
     assert res.stats.iterations == ref.stats.iterations and same_bits(res.x, ref.x)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.device_count() < 2, reason="needs two GPUs (one process per GPU)")
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_two_process_nccl_and_p2p_match_one_gpu(transport):
+    """One process per GPU over a real communicator: the NCCL and the NVLink
+    peer-store (p2p) transports, two consecutive Richardson solves bit-identical
+    to one GPU, and the distributed GMRES within the parity tolerance
+    (the p2p path had only run in emulation)."""
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    if transport == "p2p":
+        env["AIRG_TRANSPORT"] = "p2p"
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu2_dist_worker.py")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29571", worker],
+                         env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "RESULT 1" in out.stdout, out.stdout[-2000:]
