@@ -129,6 +129,7 @@ void build_fused(Ctx& c, Hier& h, int64_t smooths) {
   if (h.fused_smooths == smooths) return;
   for (Level& L : h.levels) build_fused_level(c, L, smooths);
   h.fused_smooths = smooths;
+  ++h.fused_gen;
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 

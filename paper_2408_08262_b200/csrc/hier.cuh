@@ -46,6 +46,7 @@ struct Hier {
   int64_t coarse_iterations = 3;  // SetupConfig (storage metric only)
   double grid_c = 0.0, op_c = 0.0, store_c = 0.0;
   int64_t fused_smooths = -1;  // up_f_smooths the fused operators were built for (-1: none)
+  int64_t fused_gen = 0;       // bumped by every build (captured graphs hold the operators' pointers)
   // coarse workspace
   DBuf<double> cb, cx, cr;
   // top-level solve workspace

@@ -445,9 +445,11 @@ void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double*
 }
 
 int64_t graph_key(const Hier& h, const airg_solve_config& cfg) {
-  const int fused = cfg.fast != 0 && h.fused_smooths == cfg.up_f_smooths;
-  return (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths) * 4 + (cfg.fast != 0) * 2 +
-         fused;
+  // the fused operators' generation: a rebuild frees the buffers a cached
+  // graph points to, so every build changes the key of the fused graphs
+  const int64_t fused = (cfg.fast != 0 && h.fused_smooths == cfg.up_f_smooths) ? 1 + h.fused_gen : 0;
+  return ((cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths) * 2 + (cfg.fast != 0)) *
+             4096 + fused;
 }
 
 // Capture `body` into a graph executable; returns the number of kernels.

@@ -141,3 +141,21 @@ def test_fused_operators_match_products():
         fw = csr(h.matrix(l, "w")).toarray()
         W = (2 * Q - Q @ Aff @ Q).toarray()
         np.testing.assert_allclose(fw, W, rtol=1e-12, atol=1e-13 * max(1.0, abs(W).max()))
+
+
+def test_fused_rebuild_invalidates_captured_graphs():
+    """Switching the F-smooth count rebuilds the fused operators (new
+    buffers): every cached graph that captured the old ones must be
+    re-captured, so returning to the first count reproduces its bits."""
+    p = problems.make(4, 0.25)
+    prm = dict(problems.setup_params(4), coarse_size_target=300)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    v2 = h.vcycle(p.b, coarse_iterations=3, fast=1, up_f_smooths=2)
+    g2 = airg.gmres_solve(h, p.b, coarse_iterations=3, fast=1, up_f_smooths=2)
+    v1 = h.vcycle(p.b, coarse_iterations=3, fast=1, up_f_smooths=1)
+    g1 = airg.gmres_solve(h, p.b, coarse_iterations=3, fast=1, up_f_smooths=1)
+    assert g1.stats.converged and not np.array_equal(v1, v2)
+    v2b = h.vcycle(p.b, coarse_iterations=3, fast=1, up_f_smooths=2)
+    g2b = airg.gmres_solve(h, p.b, coarse_iterations=3, fast=1, up_f_smooths=2)
+    assert np.array_equal(v2.view(np.uint64), v2b.view(np.uint64))
+    assert np.array_equal(g2.x.view(np.uint64), g2b.x.view(np.uint64)) and g2.stats.iterations == g2b.stats.iterations
