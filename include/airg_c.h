@@ -394,6 +394,24 @@ int airg_dist_create(airg_ctx* ctx, const airg_hier* h, int32_t nranks,
                      const int64_t* h_level0_starts, airg_dist** out);
 /* Richardson solve over the slabs: emulation takes/returns global device
  * vectors; with NCCL d_b / d_x are this rank's level-0 slab. */
+/* Owned-row distributed setup (SURVEY §8e setup collectives; air.cpp:285-434
+ * per rank): every rank holds and builds only its rows of every level --
+ * CF split on the slabs, A_ff halo rows gathered once for the fixed-sparsity
+ * assembly, distance-2 halo rows of Aff^-1 and A P for Z and R (A P), the
+ * Gram matrix and growth norms reduced over the ranks, the next level's rows
+ * moved to its (halved) partition, the coarsest grid gathered on rank 0.
+ * a: with rank < 0 (emulation) the whole operator, split by starts[0..nranks];
+ * with rank >= 0 this rank's rows starts[rank].. with global columns. The
+ * result solves through airg_dist_solve like airg_dist_create's. Replaces
+ * the replicated airg_dist_setup + airg_dist_create pair. */
+int airg_dist_setup_owned(airg_ctx* ctx, const airg_csr* a, const int64_t* h_starts,
+                          const airg_setup_config* cfg, const airg_injection* inj, int32_t nranks,
+                          int32_t rank, void* nccl_comm, double threshold, airg_dist** out);
+/* Setup report of an owned distribution (identical on every rank): level l
+ * < n_levels as airg_level_info; level n_levels = the coarse grid (n, nnz,
+ * nnz_ffinv = |Ac^-1|, coefficients, effective_order, poly_attempts,
+ * smoother_growth of the coarse polynomial). info may be null (n_levels only). */
+int airg_dist_report(const airg_dist* d, int64_t level, airg_level_info* info, int64_t* n_levels);
 int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg,
                     const double* d_b, double* d_x, airg_solve_stats* stats,
                     double* h_history, int64_t history_cap);

@@ -113,6 +113,9 @@ def lib() -> C.CDLL:
             "airg_nccl_unique_id": ([_VP], C.c_int),
             "airg_nccl_comm_create": ([C.c_int, C.c_int, _VP, _P(_VP)], C.c_int),
             "airg_nccl_comm_destroy": ([_VP], C.c_int),
+            "airg_dist_setup_owned": ([_VP, _VP, _VP, _P(abi.SetupConfig), _P(abi.Injection), C.c_int32, C.c_int32,
+                                       _VP, C.c_double, _P(_VP)], C.c_int),
+            "airg_dist_report": ([_VP, C.c_int64, _P(abi.LevelInfo), _P(C.c_int64)], C.c_int),
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                                  C.c_int64], C.c_int),
@@ -702,6 +705,26 @@ class Hierarchy:
         return st, hist[: min(history_cap, st.history_len)]
 
 
+def _injection(injection: dict | None):
+    """airg_injection from {"levels": [(coeffs, eff), ...], "coarse": (coeffs, eff)}
+    (pointer, arrays to keep alive during the call)."""
+    if injection is None:
+        return None, []
+    levels = injection["levels"]
+    stride = 32
+    lc = np.zeros(max(1, len(levels)) * stride)
+    le = np.zeros(max(1, len(levels)), np.int64)
+    for l, (co, eff) in enumerate(levels):
+        lc[l * stride: l * stride + len(co)] = co
+        le[l] = eff
+    cc = np.zeros(32)
+    cc[: len(injection["coarse"][0])] = injection["coarse"][0]
+    inj = abi.Injection(len(levels), stride, lc.ctypes.data_as(_P(C.c_double)),
+                        le.ctypes.data_as(_P(C.c_int64)), cc.ctypes.data_as(_P(C.c_double)),
+                        int(injection["coarse"][1]))
+    return C.byref(inj), [lc, le, cc, inj]
+
+
 def setup(a, injection: dict | None = None, ctx: Context | None = None, nranks: int = 0, rank: int = -1,
           comm: "NcclComm | None" = None, **cfg_kw) -> Hierarchy:
     """airgraph::setup (air.cpp:285-410) on the GPU. `injection` (optional)
@@ -713,23 +736,7 @@ def setup(a, injection: dict | None = None, ctx: Context | None = None, nranks: 
     ctx = ctx or default_context()
     d = _dev(a, ctx)
     cfg = abi.setup_config(**cfg_kw)
-    inj_p = None
-    keep = []
-    if injection is not None:
-        levels = injection["levels"]
-        stride = 32
-        lc = np.zeros(max(1, len(levels)) * stride)
-        le = np.zeros(max(1, len(levels)), np.int64)
-        for l, (co, eff) in enumerate(levels):
-            lc[l * stride: l * stride + len(co)] = co
-            le[l] = eff
-        cc = np.zeros(32)
-        cc[: len(injection["coarse"][0])] = injection["coarse"][0]
-        keep = [lc, le, cc]
-        inj = abi.Injection(len(levels), stride, lc.ctypes.data_as(_P(C.c_double)),
-                            le.ctypes.data_as(_P(C.c_int64)), cc.ctypes.data_as(_P(C.c_double)),
-                            int(injection["coarse"][1]))
-        inj_p = C.byref(inj)
+    inj_p, keep = _injection(injection)
     out = _VP()
     if nranks > 0:
         _check(lib().airg_dist_setup(ctx.h, d.h, C.byref(cfg), inj_p, int(nranks), int(rank),
@@ -902,6 +909,48 @@ class Dist:
         self._levels = [(h.level(l).n, h.level(l).nnz) for l in range(self.n_levels)]
         hi = h.info()
         self._coarse = (hi.coarse_n, hi.coarse_nnz)
+
+    @classmethod
+    def setup_owned(cls, a, nranks: int, rank: int = -1, comm: NcclComm | None = None, threshold: float = 2.0,
+                    starts=None, injection: dict | None = None, ctx: Context | None = None, **cfg_kw) -> "Dist":
+        """Owned-row distributed setup (airg_dist_setup_owned): every rank
+        builds and keeps only its rows of every level. rank = -1 emulates all
+        ranks from the whole operator `a`; rank >= 0 (one process per GPU,
+        with `comm`) takes this rank's rows starts[rank].. with global
+        columns. starts defaults to balanced slabs of the global size."""
+        ctx = ctx or default_context()
+        d = _dev(a, ctx)
+        n_glob = d.dims()[1]
+        P = int(nranks)
+        if starts is None:
+            base, extra = divmod(n_glob, P)
+            starts = np.concatenate([[0], np.cumsum([base + (1 if r < extra else 0) for r in range(P)])])
+        st = np.ascontiguousarray(starts, np.int64)
+        cfg = abi.setup_config(**cfg_kw)
+        inj_p, keep = _injection(injection)
+        out = _VP()
+        _check(lib().airg_dist_setup_owned(ctx.h, d.h, st.ctypes.data, C.byref(cfg), inj_p, P, int(rank),
+                                           comm.h if comm else None, float(threshold), C.byref(out)))
+        del keep
+        self = cls.__new__(cls)
+        self.h, self.ctx, self.P, self.rank = None, ctx, P, int(rank)
+        self._starts = st
+        self.d = out
+        self._comm = comm
+        nl = C.c_int64()
+        _check(lib().airg_dist_report(self.d, 0, None, C.byref(nl)))
+        self.n_levels = nl.value
+        reps = [self.report(l) for l in range(self.n_levels + 1)]
+        self._levels = [(r.n, r.nnz) for r in reps[:-1]]
+        self._coarse = (reps[-1].n, reps[-1].nnz)
+        return self
+
+    def report(self, l: int) -> abi.LevelInfo:
+        """Setup report of level l of an owned distribution (l = n_levels: the
+        coarse grid; airg_dist_report)."""
+        info = abi.LevelInfo()
+        _check(lib().airg_dist_report(self.d, int(l), C.byref(info), None))
+        return info
 
     def release_hierarchy(self):
         """Drop this distribution's reference to the global hierarchy: only

@@ -1021,6 +1021,81 @@ int airg_dist_create(airg_ctx* ctx, const airg_hier* h, int32_t nranks, int32_t 
   });
 }
 
+int airg_dist_setup_owned(airg_ctx* ctx, const airg_csr* a, const int64_t* starts, const airg_setup_config* cfg,
+                          const airg_injection* inj, int32_t nranks, int32_t rank, void* comm, double threshold,
+                          airg_dist** out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(a, "matrix");
+    need(starts, "starts");
+    need(cfg, "config");
+    need(out, "output handle");
+    bind(ctx->c);
+    if (nranks < 1 || rank >= nranks) throw InvalidArgument("dist: rank out of range");
+    if (rank >= 0 && nranks > 1 && !comm) throw InvalidArgument("dist: a communicator is needed per rank");
+    const std::vector<int64_t> s(starts, starts + nranks + 1);
+    for (int r = 0; r < nranks; ++r)
+      if (s[r + 1] < s[r]) throw InvalidArgument("dist: slab starts must be non-decreasing");
+    if (s[0] != 0) throw InvalidArgument("dist: slab starts must begin at 0");
+    std::unique_ptr<Injection> in;
+    if (inj) {
+      in = std::make_unique<Injection>();
+      in->n_levels = inj->n_levels;
+      for (int64_t l = 0; l < inj->n_levels; ++l) {
+        in->level_coeffs.emplace_back(inj->level_coeffs + l * inj->stride,
+                                      inj->level_coeffs + l * inj->stride + cfg->poly_order + 1);
+        in->level_eff.push_back(inj->level_eff_order[l]);
+      }
+      in->coarse_coeffs.assign(inj->coarse_coeffs, inj->coarse_coeffs + cfg->coarse_poly_order + 1);
+      in->coarse_eff = inj->coarse_eff_order;
+    }
+    std::vector<Csr> rows(nranks);
+    if (rank < 0) {  // emulation: the whole operator, cut into the slabs here
+      if (a->m.n != s[nranks] || a->m.m != s[nranks]) throw InvalidArgument("dist: slab starts must cover the matrix");
+      for (int r = 0; r < nranks; ++r) slice(ctx->c, a->m, s[r], s[r + 1], rows[r]);
+    } else {
+      if (a->m.n != s[rank + 1] - s[rank]) throw InvalidArgument("dist: local rows do not match the slab starts");
+      csr_copy(ctx->c, a->m, rows[rank]);
+    }
+    auto d = std::make_unique<airg_dist>();
+    d->c = &ctx->c;
+    dist_setup_owned(ctx->c, rows, s, *cfg, in.get(), nranks, rank, (ncclComm_t)comm, threshold, d->d);
+    *out = d.release();
+  });
+}
+
+int airg_dist_report(const airg_dist* dp, int64_t level, airg_level_info* info, int64_t* n_levels) {
+  return guard([&] {
+    need(dp, "dist");
+    const DHier& d = dp->d;
+    if (n_levels) *n_levels = (int64_t)d.lv.size();
+    if (!info) return;
+    if (!d.owned) throw InvalidArgument("dist: setup reports exist for the owned setup only");
+    if (level < 0 || level >= (int64_t)d.summary.size()) throw InvalidArgument("level out of range");
+    const DHier::Summary& S = d.summary[level];
+    std::memset(info, 0, sizeof *info);
+    info->n = S.n;
+    info->nnz = S.nnz;
+    info->n_f = S.nf;
+    info->n_c = S.nc;
+    info->n_f_pre = S.n_f_pre;
+    info->ddc_converted = S.n_converted;
+    info->nnz_ff = S.nnz_ff;
+    info->nnz_fc = S.nnz_fc;
+    info->nnz_cf = S.nnz_cf;
+    info->nnz_ffinv = S.nnz_ffinv;
+    info->nnz_r = S.nnz_r;
+    info->nnz_p = S.nnz_p;
+    info->max_theta_pre = S.max_theta_pre;
+    info->alpha_diag = S.alpha_diag;
+    info->max_theta_post = S.max_theta_post;
+    info->smoother_growth = S.growth;
+    info->poly_attempts = S.attempts;
+    info->effective_order = S.eff;
+    for (size_t k = 0; k < S.coeffs.size() && k < 32; ++k) info->coefficients[k] = S.coeffs[k];
+  });
+}
+
 int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg, const double* b,
                     double* x, airg_solve_stats* st, double* hist, int64_t cap) {
   return guard([&] {

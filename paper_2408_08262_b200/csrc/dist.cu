@@ -10,13 +10,6 @@
 
 namespace airg {
 
-#define NCCL_CHECK(x)                                                          \
-  do {                                                                         \
-    ncclResult_t r__ = (x);                                                    \
-    if (r__ != ncclSuccess)                                                    \
-      throw CudaError(std::string("NCCL error: ") + ncclGetErrorString(r__)); \
-  } while (0)
-
 int Part::owner(int64_t g) const {
   return (int)(std::upper_bound(s.begin(), s.end(), g) - s.begin()) - 1;
 }
@@ -320,6 +313,8 @@ void launch_rows_fc(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
   LAUNCH_ROWS_FC_MODE(c, Epi, tview(m), x, epi, false);
 }
 
+}  // namespace
+
 // ---- host helpers ---------------------------------------------------------------
 // partition_rows (partition_model.cpp:8-22) on `active` logical ranks, logical
 // rank k placed on physical rank k * stride
@@ -413,22 +408,17 @@ void slice(Ctx& c, const Csr& a, int64_t lo, int64_t hi, Csr& out) {
     out.rp.zero(c);
 }
 
-// One rank's halo of a DVec from marks over the global index space.
-struct Marks {
-  DBuf<int32_t> m;
-  int64_t N = 0;
-  void init(Ctx& c, int64_t n) {
-    N = n;
-    m.alloc(c, (size_t)std::max<int64_t>(1, n));
-    m.zero(c);
-  }
-  void cols(Ctx& c, const Csr& a, int64_t lo, int64_t hi) {
-    if (a.nnz) LAUNCH(c, k_mark_cols, blocks_for(a.nnz, 256), 256, 0, a.nnz, a.ci.p, lo, hi, m.p);
-  }
-  void vals(Ctx& c, const int32_t* idx, int64_t n, int64_t lo, int64_t hi) {
-    if (n) LAUNCH(c, k_mark_vals, blocks_for(n, 256), 256, 0, n, idx, lo, hi, m.p);
-  }
-};
+void Marks::init(Ctx& c, int64_t n) {
+  N = n;
+  m.alloc(c, (size_t)std::max<int64_t>(1, n));
+  m.zero(c);
+}
+void Marks::cols(Ctx& c, const Csr& a, int64_t lo, int64_t hi) {
+  if (a.nnz) LAUNCH(c, k_mark_cols, blocks_for(a.nnz, 256), 256, 0, a.nnz, a.ci.p, lo, hi, m.p);
+}
+void Marks::vals(Ctx& c, const int32_t* idx, int64_t n, int64_t lo, int64_t hi) {
+  if (n) LAUNCH(c, k_mark_vals, blocks_for(n, 256), 256, 0, n, idx, lo, hi, m.p);
+}
 
 void set_halo(Ctx& c, DVec& V, int r, Marks& mk) {
   DVec::Rank& R = V.rk[r];
@@ -445,7 +435,7 @@ void set_halo(Ctx& c, DVec& V, int r, Marks& mk) {
 }
 
 // After every rank's halo is known: buffers, emulation tables, NCCL lists.
-void finalize(Ctx& c, DVec& V, const DHier& d) {
+void finalize(Ctx& c, DVec& V, const DHier& d, bool peers_known) {
   const int P = V.part.P();
   DBuf<int64_t> ds(c, (size_t)P + 1);
   to_device(c, ds.p, V.part.s.data(), (size_t)P + 1);
@@ -467,7 +457,41 @@ void finalize(Ctx& c, DVec& V, const DHier& d) {
              R.src_idx.p);
     }
   }
-  if (d.me >= 0) {  // my send lists: the entries of every peer's halo that I own
+  if (d.me >= 0 && !peers_known) {
+    // my send lists from the peers' requests: the receive counts of every
+    // rank all-gathered, then each rank's halo segment of owner q sent to q
+    DVec::Rank& M = V.rk[d.me];
+    M.send_off.assign(P, 0);
+    M.send_cnt.assign(P, 0);
+    if (P > 1) {
+      DBuf<int64_t> mine(c, (size_t)P), all(c, (size_t)P * P);
+      to_device(c, mine.p, M.recv_cnt.data(), (size_t)P);
+      NCCL_CHECK(ncclAllGather(mine.p, all.p, (size_t)P, ncclInt64, d.comm, c.stream));
+      std::vector<int64_t> h((size_t)P * P);
+      to_host(c, h.data(), all.p, h.size());
+      int64_t tot = 0;
+      for (int q = 0; q < P; ++q) {
+        M.send_off[q] = tot;
+        M.send_cnt[q] = q == d.me ? 0 : h[(size_t)q * P + d.me];
+        tot += M.send_cnt[q];
+      }
+      M.send_idx.alloc(c, (size_t)std::max<int64_t>(1, tot));
+      NCCL_CHECK(ncclGroupStart());
+      for (int q = 0; q < P; ++q) {
+        if (q == d.me) continue;
+        if (M.recv_cnt[q])
+          NCCL_CHECK(ncclSend(M.halo.p + M.recv_off[q], (size_t)M.recv_cnt[q], ncclInt32, q, d.comm, c.stream));
+        if (M.send_cnt[q])
+          NCCL_CHECK(ncclRecv(M.send_idx.p + M.send_off[q], (size_t)M.send_cnt[q], ncclInt32, q, d.comm, c.stream));
+      }
+      NCCL_CHECK(ncclGroupEnd());
+      if (tot) LAUNCH(c, k_shift, blocks_for(tot, 256), 256, 0, tot, M.send_idx.p, M.lo, M.send_idx.p);
+      M.send_buf.alloc(c, (size_t)std::max<int64_t>(1, tot));
+    } else {
+      M.send_idx.alloc(c, 1);
+      M.send_buf.alloc(c, 1);
+    }
+  } else if (d.me >= 0) {  // my send lists: the entries of every peer's halo that I own
     DVec::Rank& M = V.rk[d.me];
     std::vector<int32_t> idx;
     M.send_off.assign(P, 0);
@@ -538,6 +562,8 @@ void exchange(Ctx& c, DHier& d, DVec& V) {
 void release(Ctx& c, DHier& d, DVec& V) {
   if (d.p2p.on && V.slot >= 0) p2p_release(c, d, V);
 }
+
+namespace {
 
 // ---- distributed CF split kernels (local column indices into [own | halo]) ----
 __device__ __forceinline__ uint64_t dsplitmix(uint64_t x) {
@@ -704,6 +730,8 @@ __global__ void k_f_below(int n, int64_t lo, const double* __restrict__ lab, uns
   block_add(cnt, f ? 1ull : 0ull);
 }
 
+}  // namespace
+
 // reverse exchange: every halo entry is added into its owner's slot
 void reverse_add(Ctx& c, DHier& d, DVec& V) {
   const int P = V.part.P();
@@ -736,45 +764,11 @@ void reverse_add(Ctx& c, DHier& d, DVec& V) {
   if (ns) LAUNCH(c, k_unpack_add, blocks_for(ns, 256), 256, 0, ns, M.send_idx.p, M.send_buf.p, M.buf.p);
 }
 
-}  // namespace
-
-void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const std::vector<int64_t>& starts,
-                   double alpha, int64_t max_loops, uint64_t seed, bool ddc_enabled, double fraction,
-                   int64_t bins, uint8_t* d_labels, CfReport& rep) {
-  if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
-  if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
-  if ((int)starts.size() != P + 1 || starts[0] != 0 || starts[P] != a.n)
-    throw InvalidArgument("dist: slab starts must cover the matrix");
-  if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0)) throw InvalidArgument("ddc: fraction must be in (0, 1]");
-  if (P == 1) {  // one slab: no halo -- the fused one-GPU split (cfsplit.cu)
-    const CfFused f = cf_split_fused(c, a, alpha, seed, ddc_enabled, fraction, bins, d_labels, nullptr);
-    rep = CfReport();
-    rep.s_nnz = f.s_nnz;
-    rep.n_f_pre = f.n_f_pre;
-    rep.n_converted = f.n_converted;
-    rep.n_f = f.n_f_pre - f.n_converted;
-    rep.max_theta = f.max_theta;
-    rep.alpha_diag = f.alpha_diag;
-    CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    return;
-  }
-  DHier d;
-  d.P = P;
-  d.me = me;
-  d.comm = comm;
-  DVec V;  // [own | halo] payloads: |S^T| counts, weights, marks, labels
-  V.part.s = starts;
-  V.N = a.n;
-  V.rk.resize(P);
-  std::vector<Csr> loc(P);
-  for (int r = 0; r < P; ++r) {
-    slice(c, a, V.part.lo(r), V.part.lo(r) + V.part.cnt(r), loc[r]);
-    Marks mk;
-    mk.init(c, a.n);
-    mk.cols(c, loc[r], V.part.lo(r), V.part.lo(r) + V.part.cnt(r));
-    set_halo(c, V, r, mk);
-  }
-  finalize(c, V, d);
+void cf_split_slabs(Ctx& c, DHier& d, DVec& V, std::vector<Csr>& loc, double alpha, uint64_t seed,
+                    bool ddc_enabled, double fraction, int64_t bins, std::vector<DBuf<double>>& labs,
+                    CfReport& rep) {
+  const int P = d.P, me = d.me;
+  const ncclComm_t comm = d.comm;
   // Per rank: thr, |S_i|, w, theta (own rows); labels / marks travel in V's
   // [own | halo] buffers. Global counters: one shared block in emulation, one
   // per process + NCCL allreduces otherwise.
@@ -802,7 +796,6 @@ void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const s
   // 1. thresholds, |S_i|, |S^T| contributions, then the reverse sum of the counts
   mine([&](int r) {
     DVec::Rank& R = V.rk[r];
-    remap(c, loc[r], V, r);
     R.buf.zero(c);
     const int n = (int)R.own;
     rs[r].s_cnt.alloc(c, (size_t)std::max(1, n));
@@ -894,10 +887,68 @@ void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const s
   rep.n_f = rep.n_f_pre - rep.n_converted;
   rep.alpha_diag = hs[0];
   rep.max_theta = hs[1];
+  // the converted labels of the halo (owners' final labels)
   mine([&](int r) {
-    const int64_t n = V.rk[r].own, lo = me < 0 ? V.rk[r].lo : 0;
-    if (n) LAUNCH(c, k_to_u8, blocks_for(n, 256), 256, 0, n, rs[r].lab.p, d_labels + lo);
+    DVec::Rank& R = V.rk[r];
+    if (R.own) CUDA_CHECK(cudaMemcpyAsync(R.buf.p, rs[r].lab.p, sizeof(double) * R.own, cudaMemcpyDeviceToDevice, c.stream));
   });
+  exchange(c, d, V);
+  labs.resize(P);
+  mine([&](int r) {
+    DVec::Rank& R = V.rk[r];
+    const int64_t tot = R.own + R.nhalo;
+    if (tot) CUDA_CHECK(cudaMemcpyAsync(rs[r].lab.p, R.buf.p, sizeof(double) * tot, cudaMemcpyDeviceToDevice, c.stream));
+    labs[r] = std::move(rs[r].lab);
+  });
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+void dist_cf_split(Ctx& c, const Csr& a, int P, int me, ncclComm_t comm, const std::vector<int64_t>& starts,
+                   double alpha, int64_t max_loops, uint64_t seed, bool ddc_enabled, double fraction,
+                   int64_t bins, uint8_t* d_labels, CfReport& rep) {
+  if (max_loops < 1) throw InvalidArgument("pmisr: max_loops must be >= 1");
+  if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
+  if ((int)starts.size() != P + 1 || starts[0] != 0 || starts[P] != a.n)
+    throw InvalidArgument("dist: slab starts must cover the matrix");
+  if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0)) throw InvalidArgument("ddc: fraction must be in (0, 1]");
+  if (P == 1) {  // one slab: no halo -- the fused one-GPU split (cfsplit.cu)
+    const CfFused f = cf_split_fused(c, a, alpha, seed, ddc_enabled, fraction, bins, d_labels, nullptr);
+    rep = CfReport();
+    rep.s_nnz = f.s_nnz;
+    rep.n_f_pre = f.n_f_pre;
+    rep.n_converted = f.n_converted;
+    rep.n_f = f.n_f_pre - f.n_converted;
+    rep.max_theta = f.max_theta;
+    rep.alpha_diag = f.alpha_diag;
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  DHier d;
+  d.P = P;
+  d.me = me;
+  d.comm = comm;
+  DVec V;  // [own | halo] payloads: |S^T| counts, weights, marks, labels
+  V.part.s = starts;
+  V.N = a.n;
+  V.rk.resize(P);
+  std::vector<Csr> loc(P);
+  for (int r = 0; r < P; ++r) {
+    slice(c, a, V.part.lo(r), V.part.lo(r) + V.part.cnt(r), loc[r]);
+    Marks mk;
+    mk.init(c, a.n);
+    mk.cols(c, loc[r], V.part.lo(r), V.part.lo(r) + V.part.cnt(r));
+    set_halo(c, V, r, mk);
+  }
+  finalize(c, V, d);
+  for (int r = 0; r < P; ++r)
+    if (d.mine(r)) remap(c, loc[r], V, r);
+  std::vector<DBuf<double>> labs;
+  cf_split_slabs(c, d, V, loc, alpha, seed, ddc_enabled, fraction, bins, labs, rep);
+  for (int r = 0; r < P; ++r) {
+    if (!d.mine(r)) continue;
+    const int64_t n = V.rk[r].own, lo = me < 0 ? V.rk[r].lo : 0;
+    if (n) LAUNCH(c, k_to_u8, blocks_for(n, 256), 256, 0, n, labs[r].p, d_labels + lo);
+  }
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
@@ -972,24 +1023,79 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
     D.active = active;
     D.fine = p;
   }
-  d.cpart = gathered(h.coarse_a.n, P);
+  // ---- pieces: every rank's slices of the global hierarchy
+  DistPieces pc;
+  pc.all_ranks = true;
+  pc.coarse_n = h.coarse_a.n;
+  pc.lv.resize(L);
+  pc.fpart.resize(L);
+  pc.n.resize(L);
+  pc.nf.resize(L);
   for (int l = 0; l < L; ++l) {
-    DLevel& D = d.lv[l];
-    D.coarse_part = l + 1 < L ? d.lv[l + 1].fine : d.cpart;
-    // F partition: #F points below each fine boundary
+    const DLevel& D = d.lv[l];
     const Level& Lv = h.levels[l];
+    pc.n[l] = Lv.a.n;
+    pc.nf[l] = Lv.map.nf;
+    // F partition: #F points below each fine boundary
     DBuf<int64_t> bnd(c, (size_t)P + 1), cnt(c, (size_t)P + 1);
     to_device(c, bnd.p, D.fine.s.data(), (size_t)P + 1);
     LAUNCH(c, k_count_below, 1, 64, 0, Lv.map.f_to_fine.p, (int64_t)Lv.map.nf, bnd.p, P + 1, cnt.p);
-    D.fpart.s.resize(P + 1);
-    to_host(c, D.fpart.s.data(), cnt.p, (size_t)P + 1);
+    pc.fpart[l].s.resize(P + 1);
+    to_host(c, pc.fpart[l].s.data(), cnt.p, (size_t)P + 1);
+  }
+  const Part cpart = gathered(h.coarse_a.n, P);
+  pc.AC.resize(P);
+  pc.ACI.resize(P);
+  pc.A0.resize(P);
+  for (int l = 0; l < L; ++l) {
+    const Level& Lv = h.levels[l];
+    const Part& coarse = l + 1 < L ? d.lv[l + 1].fine : cpart;
+    pc.lv[l].resize(P);
+    for (int r = 0; r < P; ++r) {
+      DistPieces::LevelRank& R = pc.lv[l][r];
+      const int64_t flo = pc.fpart[l].lo(r), fhi = flo + pc.fpart[l].cnt(r);
+      const int64_t clo = coarse.lo(r), chi = clo + coarse.cnt(r);
+      const int64_t lo = d.lv[l].fine.lo(r), hi = lo + d.lv[l].fine.cnt(r);
+      slice(c, Lv.r, clo, chi, R.R);
+      slice(c, Lv.af, flo, fhi, R.AF);
+      slice(c, Lv.affg, flo, fhi, R.AFFG);
+      slice(c, Lv.ffinv, flo, fhi, R.FINV);
+      R.pmap.alloc(c, (size_t)std::max<int64_t>(1, hi - lo));
+      if (hi > lo)
+        CUDA_CHECK(cudaMemcpyAsync(R.pmap.p, Lv.pmap.p + lo, sizeof(int32_t) * (hi - lo),
+                                   cudaMemcpyDeviceToDevice, c.stream));
+      R.f2f.alloc(c, (size_t)std::max<int64_t>(1, fhi - flo));
+      if (fhi > flo)
+        CUDA_CHECK(cudaMemcpyAsync(R.f2f.p, Lv.map.f_to_fine.p + flo, sizeof(int32_t) * (fhi - flo),
+                                   cudaMemcpyDeviceToDevice, c.stream));
+    }
+  }
+  const Part& top = L ? d.lv[0].fine : cpart;
+  for (int r = 0; r < P; ++r) {
+    slice(c, h.coarse_a, cpart.lo(r), cpart.lo(r) + cpart.cnt(r), pc.AC[r]);
+    slice(c, h.coarse_inv, cpart.lo(r), cpart.lo(r) + cpart.cnt(r), pc.ACI[r]);
+    const Csr& A0 = L ? h.levels[0].a : h.coarse_a;
+    slice(c, A0, top.lo(r), top.lo(r) + top.cnt(r), pc.A0[r]);
+  }
+  dist_build(c, d, pc);
+}
+
+void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
+  const int P = d.P;
+  const int L = (int)d.lv.size();
+  auto have = [&](int r) { return pc.all_ranks || d.mine(r); };
+  d.cpart = gathered(pc.coarse_n, P);
+  for (int l = 0; l < L; ++l) {
+    DLevel& D = d.lv[l];
+    D.coarse_part = l + 1 < L ? d.lv[l + 1].fine : d.cpart;
+    D.fpart = pc.fpart[l];
     D.rk.resize(P);
     D.B.part = D.fine;
-    D.B.N = Lv.a.n;
+    D.B.N = pc.n[l];
     D.X.part = D.fine;
-    D.X.N = Lv.a.n;
+    D.X.N = pc.n[l];
     D.RF.part = D.fpart;
-    D.RF.N = Lv.map.nf;
+    D.RF.N = pc.nf[l];
     D.B.rk.resize(P);
     D.X.rk.resize(P);
     D.RF.rk.resize(P);
@@ -997,39 +1103,34 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
   d.CB.part = d.cpart;
   d.CX.part = d.cpart;
   d.CR.part = d.cpart;
-  d.CB.N = d.CX.N = d.CR.N = h.coarse_a.n;
+  d.CB.N = d.CX.N = d.CR.N = pc.coarse_n;
   d.CB.rk.resize(P);
   d.CX.rk.resize(P);
   d.CR.rk.resize(P);
   d.XS.part = L ? d.lv[0].fine : d.cpart;
-  d.XS.N = h.top_n();
+  d.XS.N = L ? pc.n[0] : pc.coarse_n;
   d.XS.rk.resize(P);
   d.rk.resize(P);
 
-  // ---- local slices with global columns (every rank: the halo lists of all
-  // ranks are needed to derive send lists; only my ranks keep matrices)
+  // ---- the ranks' operators (global columns) and their halos (all ranks
+  // when every piece is here: the peers' halo lists give the send lists)
   for (int l = 0; l < L; ++l) {
     DLevel& D = d.lv[l];
-    const Level& Lv = h.levels[l];
     for (int r = 0; r < P; ++r) {
+      if (!have(r)) continue;
       DLevel::Rank& R = D.rk[r];
+      DistPieces::LevelRank& S = pc.lv[l][r];
       const int64_t flo = D.fpart.lo(r), fhi = flo + D.fpart.cnt(r);
-      const int64_t clo = D.coarse_part.lo(r), chi = clo + D.coarse_part.cnt(r);
       const int64_t lo = D.fine.lo(r), hi = lo + D.fine.cnt(r);
-      slice(c, Lv.r, clo, chi, R.R);
-      slice(c, Lv.af, flo, fhi, R.AF);
-      slice(c, Lv.affg, flo, fhi, R.AFFG);
-      slice(c, Lv.ffinv, flo, fhi, R.FINV);
+      R.R = std::move(S.R);
+      R.AF = std::move(S.AF);
+      R.AFFG = std::move(S.AFFG);
+      R.FINV = std::move(S.FINV);
       R.nf_own = fhi - flo;
       R.n_own = hi - lo;
-      R.pmap.alloc(c, (size_t)std::max<int64_t>(1, hi - lo));
-      if (hi > lo)
-        CUDA_CHECK(cudaMemcpyAsync(R.pmap.p, Lv.pmap.p + lo, sizeof(int32_t) * (hi - lo),
-                                   cudaMemcpyDeviceToDevice, c.stream));
+      R.pmap = std::move(S.pmap);
       R.f2f.alloc(c, (size_t)std::max<int64_t>(1, fhi - flo));
-      if (fhi > flo)
-        LAUNCH(c, k_shift, blocks_for(fhi - flo, 256), 256, 0, fhi - flo, Lv.map.f_to_fine.p + flo, lo,
-               R.f2f.p);
+      if (fhi > flo) LAUNCH(c, k_shift, blocks_for(fhi - flo, 256), 256, 0, fhi - flo, S.f2f.p, lo, R.f2f.p);
       R.sc.alloc(c, (size_t)std::max<int64_t>(1, fhi - flo));
       // halos: B_l <- R_l ; X_l <- AF, AFFG, P_{l-1} ; RF_l <- FINV
       Marks mb, mx, mf;
@@ -1051,10 +1152,11 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
   }
   // coarsest: A_c / Ac^-1 on their owner, CX halo also serves P_{L-1}
   for (int r = 0; r < P; ++r) {
+    if (!have(r)) continue;
     DHier::Rank& T = d.rk[r];
     const int64_t lo = d.cpart.lo(r), hi = lo + d.cpart.cnt(r);
-    slice(c, h.coarse_a, lo, hi, T.AC);
-    slice(c, h.coarse_inv, lo, hi, T.ACI);
+    T.AC = std::move(pc.AC[r]);
+    T.ACI = std::move(pc.ACI[r]);
     Marks mc, mb, mr;
     mc.init(c, d.CX.N);
     mc.cols(c, T.AC, lo, hi);
@@ -1070,9 +1172,8 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
     mr.cols(c, T.ACI, lo, hi);
     set_halo(c, d.CR, r, mr);
     // top operator for the residual
-    const Csr& A0 = L ? h.levels[0].a : h.coarse_a;
     const int64_t tlo = d.XS.part.lo(r), thi = tlo + d.XS.part.cnt(r);
-    slice(c, A0, tlo, thi, T.A0);
+    T.A0 = std::move(pc.A0[r]);
     Marks ms;
     ms.init(c, d.XS.N);
     ms.cols(c, T.A0, tlo, thi);
@@ -1082,14 +1183,14 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
   // ---- buffers, tables, remapped columns
   for (int l = 0; l < L; ++l) {
     DLevel& D = d.lv[l];
-    finalize(c, D.B, d);
-    finalize(c, D.X, d);
-    finalize(c, D.RF, d);
+    finalize(c, D.B, d, pc.all_ranks);
+    finalize(c, D.X, d, pc.all_ranks);
+    finalize(c, D.RF, d, pc.all_ranks);
   }
-  finalize(c, d.CB, d);
-  finalize(c, d.CX, d);
-  finalize(c, d.CR, d);
-  finalize(c, d.XS, d);
+  finalize(c, d.CB, d, pc.all_ranks);
+  finalize(c, d.CX, d, pc.all_ranks);
+  finalize(c, d.CR, d, pc.all_ranks);
+  finalize(c, d.XS, d, pc.all_ranks);
   if (p2p_requested() && P > 1) {  // the solve's exchanged vectors move to the p2p arenas
     std::vector<DVec*> vecs;
     for (int l = 0; l < L; ++l) {

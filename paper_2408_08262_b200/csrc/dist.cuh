@@ -144,6 +144,16 @@ struct DHier {
   std::vector<GmRank> gm;
   int gm_m = 0;
   int64_t top_n = 0;
+  // owned setup (dist_setup_owned): per-level reports, identical on every rank
+  struct Summary {
+    int64_t n = 0, nnz = 0, nf = 0, nc = 0, n_f_pre = 0, n_converted = 0;
+    int64_t nnz_ff = 0, nnz_fc = 0, nnz_cf = 0, nnz_ffinv = 0, nnz_r = 0, nnz_p = 0;
+    int64_t attempts = 1, eff = 0;
+    double max_theta_pre = 0.0, alpha_diag = 0.0, max_theta_post = 0.0, growth = 0.0;
+    std::vector<double> coeffs;
+  };
+  std::vector<Summary> summary;  // fine levels, then the coarse level (n, nnz, nnz_ffinv = |Ac^-1|, ...)
+  bool owned = false;
   // p2p transport: one arena per rank (emulation: all allocated here; NCCL
   // ranks: mine allocated, the peers' opened from their IPC handles)
   struct P2PState {
@@ -176,8 +186,71 @@ void p2p_push_plan(const std::vector<int64_t>& recv_halo, int64_t recv_own, int6
                    int64_t send_lo, int64_t send_own, std::vector<int32_t>& src_idx,
                    std::vector<int64_t>& dst_pos);
 
+#define NCCL_CHECK(x)                                                          \
+  do {                                                                         \
+    ncclResult_t r__ = (x);                                                    \
+    if (r__ != ncclSuccess)                                                    \
+      throw CudaError(std::string("NCCL error: ") + ncclGetErrorString(r__)); \
+  } while (0)
+
+// ---- partition and halo plumbing shared by the solve and the owned setup
+// partition_rows (partition_model.cpp:8-22) on `active` logical ranks placed
+// on every (P / active)-th physical rank; merged: adjacent logical pairs
+// (partition_model.cpp:101-104); gathered: every row on rank 0
+Part balanced(int64_t n, int active, int P);
+Part merged(const Part& p, int active, int new_active);
+Part gathered(int64_t n, int P);
+// rows lo..hi of a (columns unchanged)
+void slice(Ctx& c, const Csr& a, int64_t lo, int64_t hi, Csr& out);
+// One rank's halo of a DVec from marks over the global index space.
+struct Marks {
+  DBuf<int32_t> m;
+  int64_t N = 0;
+  void init(Ctx& c, int64_t n);
+  void cols(Ctx& c, const Csr& a, int64_t lo, int64_t hi);  // columns outside [lo, hi) (bit 31 ignored)
+  void vals(Ctx& c, const int32_t* idx, int64_t n, int64_t lo, int64_t hi);
+};
+void set_halo(Ctx& c, DVec& V, int r, Marks& mk);
+// buffers, emulation tables and NCCL send lists once the halos are set.
+// peers_known: every rank's halo list is in V (all ranks planned here);
+// otherwise (one rank per process, owned setup) each rank's requests travel
+// to their owners over NCCL.
+void finalize(Ctx& c, DVec& V, const DHier& d, bool peers_known = true);
+// columns (global) -> V's [own | halo] layout of rank r
+void remap(Ctx& c, Csr& a, const DVec& V, int r);
+void exchange(Ctx& c, DHier& d, DVec& V);     // halo <- owners
+void reverse_add(Ctx& c, DHier& d, DVec& V);  // owners += halo entries
+void release(Ctx& c, DHier& d, DVec& V);
+
+// Per-rank operator slices a distributed solve is built from (dist_build):
+// rows of the ranks this process runs, global column indices.
+struct DistPieces {
+  struct LevelRank {
+    Csr R;                    // rows of level l+1 owned here (coarse_part), fine columns
+    Csr AF, AFFG, FINV;       // F rows owned here (fpart): A_F (bit 31 = C column), A_FF (fine columns), Aff^-1
+    DBuf<int32_t> pmap;       // own fine rows -> global coarse index (-1: empty row)
+    DBuf<int32_t> f2f;        // own F rows -> global fine row
+  };
+  std::vector<std::vector<LevelRank>> lv;  // [level][rank]
+  std::vector<Part> fpart;                 // F-point partition per level
+  std::vector<int64_t> n, nf;              // global rows / F points per level
+  std::vector<Csr> AC, ACI, A0;            // per rank: coarse rows (cpart), top rows (level-0 partition)
+  int64_t coarse_n = 0;
+  bool all_ranks = false;                  // pieces of every rank present (halo lists of peers known)
+};
+// The solve structures of d from pieces; d.P / me / comm / threshold and
+// every level's partition (d.lv[l].fine, active, ratios) already set.
+void dist_build(Ctx& c, DHier& d, DistPieces& pc);
+
 void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double threshold,
                  const int64_t* level0_starts, DHier& d);
+
+// Owned-row distributed setup (dsetup.cu): every rank holds and builds only
+// its rows of every level. a_rows[r]: rows starts[r].. of the fine operator
+// with global columns (mine ranks). Setup summaries land in d.summary.
+void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_t>& starts,
+                      const airg_setup_config& cfg, const Injection* inj, int P, int me, ncclComm_t comm,
+                      double threshold, DHier& d);
 // halo bytes received by this process per V-cycle and per level-0 SpMV
 void dist_halo_bytes(const DHier& d, const airg_solve_config& cfg, int64_t& vcycle, int64_t& spmv);
 // d_b / d_x: global vectors in emulation mode, this rank's slab with NCCL
@@ -199,6 +272,14 @@ void dist_cf_split(Ctx& c, const Csr& a_global, int P, int me, ncclComm_t comm,
                    const std::vector<int64_t>& starts, double alpha, int64_t max_loops, uint64_t seed,
                    bool ddc_enabled, double fraction, int64_t bins, uint8_t* d_labels,
                    CfReport& rep);
+
+// The split on slabs whose halo plan V is finalized: loc[r] = rank r's rows
+// with columns remapped to V's [own | halo] layout (mine ranks). On return
+// labs[r] holds rank r's final labels (AIRG_F / AIRG_C as doubles) over
+// [own | halo].
+void cf_split_slabs(Ctx& c, DHier& d, DVec& V, std::vector<Csr>& loc, double alpha, uint64_t seed,
+                    bool ddc_enabled, double fraction, int64_t bins, std::vector<DBuf<double>>& labs,
+                    CfReport& rep);
 
 // Host-side halo plan of one rank (same rule as the device build): the
 // sorted distinct referenced indices outside the owned range, with the

@@ -93,6 +93,17 @@ struct Injection {
   int64_t coarse_eff = 0;
 };
 
+// make_checked_inverse (air.cpp:106-129) / a fixed polynomial on one GPU
+struct CheckedInverse {
+  std::vector<double> coeffs;
+  int64_t eff = 0, attempts = 1;
+  double growth = 0.0;
+  Csr q;
+};
+CheckedInverse checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsity, uint64_t seed);
+CheckedInverse fixed_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs, int64_t eff,
+                             int64_t sparsity);
+
 struct RowSplit;
 // rs (nullable): split the setup's heavy row kernels over ranks (rowsplit.cuh)
 void setup(Ctx& c, const Csr& a, const airg_setup_config& cfg, const Injection* inj, Hier& h,

@@ -28,10 +28,10 @@ __device__ __forceinline__ double d_standard_normal(uint64_t seed, uint64_t inde
 }
 
 __global__ void normal_fill(int64_t n, uint64_t seed, double* __restrict__ hi,
-                            double* __restrict__ lo) {
+                            double* __restrict__ lo, int64_t base = 0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  hi[i] = d_standard_normal(seed, (uint64_t)i);
+  hi[i] = d_standard_normal(seed, (uint64_t)(base + i));
   if (lo) lo[i] = 0.0;
 }
 
@@ -377,24 +377,37 @@ PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const 
       LAUNCH(c, dd_spmv, blocks_for(n, 128), 128, 0, (int)n, a.rp.p, a.ci.p, a.v.p,
              kh.p + (k - 1) * n, kl.p + (k - 1) * n, kh.p + k * n, kl.p + k * n);
   }
+  std::vector<dd> G;
+  poly_gram(c, n, nc, kh.p, kl.p, G);
+  return poly_fit_gram(G, nc, m, n);
+}
+
+// G = K^T K in double-double over n rows (K: nc columns of n, hi / lo
+// planes); per-block partials summed on the host in block order.
+void poly_gram(Ctx& c, int64_t n, int nc, const double* kh, const double* kl, std::vector<dd>& G) {
   std::vector<int2> pairs;
   for (int x = 0; x < nc; ++x)
     for (int y = x; y < nc; ++y) pairs.push_back(make_int2(x, y));
+  G.assign((size_t)nc * nc, dd{0.0, 0.0});
+  if (n == 0) return;
   DBuf<int2> dpairs(c, pairs.size());
   to_device(c, dpairs.p, pairs.data(), pairs.size());
   const int gblocks = (int)std::min<int64_t>(64, blocks_for(n, 256));
   DBuf<double> part(c, pairs.size() * gblocks * 2);
-  LAUNCH(c, dd_gram, dim3(gblocks, (unsigned)pairs.size()), 256, 0, n, nc, kh.p, kl.p, dpairs.p,
-         part.p);
+  LAUNCH(c, dd_gram, dim3(gblocks, (unsigned)pairs.size()), 256, 0, n, nc, kh, kl, dpairs.p, part.p);
   std::vector<double> hp(pairs.size() * gblocks * 2);
   to_host(c, hp.data(), part.p, hp.size());
-  std::vector<dd> G((size_t)nc * nc);
   for (size_t pi = 0; pi < pairs.size(); ++pi) {
     dd s = {0.0, 0.0};
     for (int b = 0; b < gblocks; ++b) s = dd_add(s, dd{hp[(pi * gblocks + b) * 2], hp[(pi * gblocks + b) * 2 + 1]});
     G[pairs[pi].x * nc + pairs[pi].y] = s;
     G[pairs[pi].y * nc + pairs[pi].x] = s;
   }
+}
+
+// The host half of compute_coefficients from the Gram matrix of the power
+// basis over n rows (nc = m + 1 columns).
+PolyFit poly_fit_gram(const std::vector<dd>& G, int nc, int64_t m, int64_t n) {
   // normalised Gram and Cholesky (upper R, row-major R[i*nc+j])
   std::vector<dd> scale(nc);
   for (int k = 0; k < nc; ++k) scale[k] = dd_sqrt(G[k * nc + k]);
@@ -466,6 +479,13 @@ PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const 
   return f;
 }
 
+void poly_basis_fill(Ctx& c, int64_t n, int64_t base, uint64_t seed, double* hi, double* lo) {
+  if (n) LAUNCH(c, normal_fill, blocks_for(n, 256), 256, 0, n, seed, hi, lo, base);
+}
+void poly_dd_spmv(Ctx& c, const Csr& a, const double* xh, const double* xl, double* yh, double* yl) {
+  if (a.n) LAUNCH(c, dd_spmv, blocks_for(a.n, 128), 128, 0, a.n, a.rp.p, a.ci.p, a.v.p, xh, xl, yh, yl);
+}
+
 namespace {
 // rows rb.. (n of them) of the sparsity-1 assembly, a local CSR with global columns
 void assemble_slab_s1(Ctx& c, const Csr& a, int rb, int n, const double* d_coeffs, int64_t deg, Csr& r) {
@@ -485,6 +505,16 @@ void assemble_slab_s1(Ctx& c, const Csr& a, int rb, int n, const double* d_coeff
          cur.p, nxt.p, d_coeffs, (int)deg, rb);
 }
 }  // namespace
+
+void poly_assemble_rows(Ctx& c, const Csr& a, int rb, int n, const double* h_coeffs, int64_t ncoeffs,
+                        int64_t deg, Csr& out) {
+  if (ncoeffs < 1) throw InvalidArgument("assemble_fixed_sparsity: empty polynomial");
+  if (deg >= ncoeffs) throw InvalidArgument("assemble_fixed_sparsity: effective order exceeds coefficients");
+  DBuf<double> coeffs(c, (size_t)ncoeffs);
+  to_device(c, coeffs.p, h_coeffs, (size_t)ncoeffs);
+  assemble_slab_s1(c, a, rb, n, coeffs.p, deg, out);
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));  // coeffs scratch freed on return
+}
 
 void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs, int64_t deg,
                    int64_t sparsity_order, Csr& out, const RowSplit* rs) {

@@ -103,6 +103,26 @@ Checked injected_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs
 
 }  // namespace
 
+CheckedInverse checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsity, uint64_t seed) {
+  Checked k = make_checked_inverse(c, a, order, sparsity, seed, nullptr);
+  CheckedInverse o;
+  o.coeffs = k.coeffs;
+  o.eff = k.eff;
+  o.attempts = k.attempts;
+  o.growth = k.growth;
+  o.q = std::move(k.q);
+  return o;
+}
+CheckedInverse fixed_inverse(Ctx& c, const Csr& a, const std::vector<double>& coeffs, int64_t eff,
+                             int64_t sparsity) {
+  Checked k = injected_inverse(c, a, coeffs, eff, sparsity, nullptr);
+  CheckedInverse o;
+  o.coeffs = k.coeffs;
+  o.eff = k.eff;
+  o.q = std::move(k.q);
+  return o;
+}
+
 // Solve-side structures: A_FF with global columns and the per-level vectors
 // (fixed pointers, so the V-cycle can be captured into a CUDA graph).
 void alloc_workspace(Ctx& c, Hier& h) {

@@ -213,8 +213,8 @@ void spmv_thread_rows(Ctx& c, const Csr& a, const double* x, double* y) {
   LAUNCH(c, spmv_rows, blocks_for(a.n, 128), 128, 0, a.n, a.rp.p, a.ci.p, a.v.p, x, y);
 }
 
-void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base) {
-  if (row_base == 0 && a.n != a.m)
+void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base, bool slab) {
+  if (!slab && row_base == 0 && a.n != a.m)
     throw InvalidArgument("SparseMatrix: with_full_diagonal requires a square matrix");
   DBuf<int32_t> cnt(c, (size_t)a.n);
   Csr r;

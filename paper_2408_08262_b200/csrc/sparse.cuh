@@ -2,6 +2,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "dd.cuh"
 
 namespace airg {
 
@@ -10,7 +11,9 @@ void csr_upload(Ctx& c, int64_t n, int64_t m, const int64_t* h_rp, const int64_t
                 const double* h_v, Csr& out);
 void csr_download(Ctx& c, const Csr& a, int64_t* h_rp, int64_t* h_ci, double* h_v);
 void spmv(Ctx& c, const Csr& a, const double* x, double* y);
-void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base = 0);  // row_base: slab rows
+// row_base: the rows are global rows row_base.. of a square operator (slab: a row
+// slab even when row_base is 0)
+void with_full_diagonal(Ctx& c, const Csr& a, Csr& out, int row_base = 0, bool slab = false);
 void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out);
 // entries per batch of the thread-per-row kernels for a matrix of n rows and
 // nnz entries: 8 = aligned vector batches, 4 / 0 = 4- / 8-entry scalar batches
@@ -113,12 +116,30 @@ PolyFit poly_coefficients(Ctx& c, const Csr& a, int64_t m, uint64_t seed, const 
 void poly_assemble(Ctx& c, const Csr& a, const double* h_coeffs, int64_t ncoeffs, int64_t deg,
                    int64_t sparsity_order, Csr& out, const RowSplit* rs = nullptr);
 double smoother_growth(Ctx& c, const Csr& a, const Csr& q, const RowSplit* rs = nullptr);
+// pieces of the fit for a row-distributed operator (dsetup.cu): the power
+// basis start (standard normals of global rows base..), one double-double
+// SpMV of local rows, the Gram matrix of n local rows, the host fit
+void poly_basis_fill(Ctx& c, int64_t n, int64_t base, uint64_t seed, double* hi, double* lo);
+void poly_dd_spmv(Ctx& c, const Csr& a, const double* xh, const double* xl, double* yh, double* yl);
+void poly_gram(Ctx& c, int64_t n, int nc, const double* kh, const double* kl, std::vector<dd>& G);
+PolyFit poly_fit_gram(const std::vector<dd>& G, int nc, int64_t m, int64_t n);
+// sparsity-1 assembly of rows rb..rb+n of a (pattern = row + diagonal, in
+// a's column space; columns outside a's rows must not occur in the pattern)
+void poly_assemble_rows(Ctx& c, const Csr& a, int rb, int n, const double* h_coeffs, int64_t ncoeffs,
+                        int64_t deg, Csr& out);
 
 // transfer.cu -----------------------------------------------------------------
 // R rows of the C points of acf (coarse rows cb..; whole operator: cb = 0);
 // bmap: row of ffinv holding each F column (gathered rows), null = identity
 void build_restriction(Ctx& c, const Csr& acf, const Csr& ffinv, double drop, const LabelMap& map,
                        Csr& r, const int32_t* bmap = nullptr, int cb = 0, const RowSplit* rs = nullptr);
+// R rows [Z | I] from the rows of Z = A_cf Aff^-1: Z's columns mapped by
+// f2f (null: already fine indices), the identity at c2f[row]
+void restriction_from_z(Ctx& c, const Csr& z, const int32_t* f2f, const int32_t* c2f, int64_t ncols, Csr& r);
+// one-point map of the rows of a (row i = column i: own rows first in a
+// local layout), label / f2s per column (f2s: coarse index of C columns)
+void prolongation_map_fused(Ctx& c, const uint8_t* label, const int32_t* f2s, const Csr& a, double alpha,
+                            int32_t* pmap);
 // one-point P (air.cpp:191-238) as pmap[i] (coarse index or -1) and a CSR.
 // one-point P of the slab rows rb.. of `a` (S of the same rows, global map)
 void prolongation_map_rows(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a, int rb,

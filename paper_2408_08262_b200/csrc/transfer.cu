@@ -24,7 +24,7 @@ __global__ void r_fill(int nc, const int32_t* __restrict__ zrp, const int32_t* _
   int o = rrp[c];
   bool placed = false;
   for (int k = zrp[c]; k < zrp[c + 1]; ++k) {
-    const int col = f2f[zci[k]];
+    const int col = f2f ? f2f[zci[k]] : zci[k];
     if (!placed && self < col) {
       rci[o] = self;
       rv[o++] = 1.0;
@@ -146,20 +146,31 @@ void build_restriction(Ctx& c, const Csr& acf, const Csr& ffinv, double drop, co
     split_spgemm(c, *rs, acf, ffinv, z, drop, /*keep_diag=*/false);  // air.cpp:298-299
   else
     spgemm(c, acf, ffinv, z, drop, /*keep_diag=*/false, bmap);
-  const int nc = acf.n;  // the C rows of this slab: coarse rows cb..
+  restriction_from_z(c, z, map.f_to_fine.p, map.c_to_fine.p + cb, map.n, r);
+}
+
+void restriction_from_z(Ctx& c, const Csr& z, const int32_t* f2f, const int32_t* c2f, int64_t ncols, Csr& r) {
+  const int nc = z.n;
   Csr out;
   out.n = nc;
-  out.m = map.n;
+  out.m = (int32_t)ncols;
   out.rp.alloc(c, (size_t)nc + 1);
-  DBuf<int32_t> cnt(c, (size_t)nc);
+  DBuf<int32_t> cnt(c, (size_t)std::max(1, nc));
   if (nc) LAUNCH(c, r_count, blocks_for(nc, 256), 256, 0, nc, z.rp.p, cnt.p);
-  out.nnz = exclusive_scan(c, cnt.p, out.rp.p, nc);
+  out.nnz = nc ? exclusive_scan(c, cnt.p, out.rp.p, nc) : 0;
+  if (!nc) CUDA_CHECK(cudaMemsetAsync(out.rp.p, 0, sizeof(int32_t), c.stream));
   out.ci.alloc(c, (size_t)out.nnz);
   out.v.alloc(c, (size_t)out.nnz);
   if (nc)
-    LAUNCH(c, r_fill, blocks_for(nc, 256), 256, 0, nc, z.rp.p, z.ci.p, z.v.p, map.f_to_fine.p,
-           map.c_to_fine.p + cb, out.rp.p, out.ci.p, out.v.p);
+    LAUNCH(c, r_fill, blocks_for(nc, 256), 256, 0, nc, z.rp.p, z.ci.p, z.v.p, f2f, c2f, out.rp.p, out.ci.p,
+           out.v.p);
   r = std::move(out);
+}
+
+void prolongation_map_fused(Ctx& c, const uint8_t* label, const int32_t* f2s, const Csr& a, double alpha,
+                            int32_t* pmap) {
+  if (a.n)
+    LAUNCH(c, p_map_fused, blocks_for(a.n, 256), 256, 0, a.n, label, f2s, a.rp.p, a.ci.p, a.v.p, alpha, pmap);
 }
 
 void prolongation_map_rows(Ctx& c, const LabelMap& map, const Strength& g, const Csr& a, int rb,
