@@ -95,6 +95,23 @@ def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2, fast=False):
     return per_cycle
 
 
+class OwnedView:
+    """The hierarchy report of an owned distribution (airg_dist_report) in
+    the shape vcycle_alg_bytes / gmres_alg_bytes read."""
+
+    def __init__(self, d):
+        self.d = d
+        self.n_levels = d.n_levels
+
+    def level(self, l):
+        return self.d.report(l)
+
+    def info(self):
+        from types import SimpleNamespace
+        c = self.d.report(self.d.n_levels)
+        return SimpleNamespace(n_levels=self.d.n_levels, coarse_n=c.n, coarse_nnz=c.nnz, coarse_inv_nnz=c.nnz_ffinv)
+
+
 def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, fast=False):
     """Algorithmic HBM bytes of one GMRES(m) solve. Per Arnoldi step j (one
     outer iteration): the V-cycle (vcycle_alg_bytes), w = A z (SpMV + z
@@ -366,13 +383,13 @@ def run_gpu_dist(args):
     """N > 1 (torchrun, one process per GPU): weak scaling of the metric's
     config C4 -- a 70 x 70 x 68N cube lattice split into z-slabs of 68 cube
     layers (1,999,200 tets) per GPU, as BASELINE configs[4] states. Each rank
-    generates its own slab (global column indices); the slabs are
-    all-gathered into the global operator for the setup, whose row work is
-    split over the ranks (airg_dist_setup: every rank holds the hierarchy).
-    Then every rank keeps its row slabs (the z-slabs on level 0, the replay
-    halving rule on coarser levels, the coarsest grid gathered on rank 0) and
-    runs the distributed outer GMRES(30) around the row-slab V-cycle with
-    NCCL halo exchanges and allreduced inner products."""
+    generates its own slab (global column indices) and the owned-row
+    distributed setup (airg_dist_setup_owned) builds every level with each
+    rank holding only its rows (CF split on the slabs, halo rows of A_ff,
+    Aff^-1 and A P fetched over NCCL, the replay halving rule on coarser
+    levels, the coarsest grid gathered on rank 0). Then the distributed outer
+    GMRES(30) around the row-slab V-cycle runs with NCCL halo exchanges and
+    allreduced inner products."""
     import torch
     import torch.distributed as dist
     from paper_2408_08262_b200 import airg, problems
@@ -386,62 +403,31 @@ def run_gpu_dist(args):
     nzl = round(68 * args.scale) if args.scale != 1 else 68
     nxy = round(70 * args.scale) if args.scale != 1 else 70
     ps = problems.c4_tets_3d(nxy, nxy, nzl, z0=nzl * rank, nz_total=nzl * ws)
-    # all-gather the slabs into the global CSR (problems.gather_csr_slabs)
-    N, rp, cols, vals = problems.gather_csr_slabs(ps, ws, dist.all_gather)
-
-    class _P:  # the global system (b: this rank's slab only)
-        pass
-    p = _P()
-    p.n, p.nnz, p.row_offsets, p.cols, p.vals = N, int(rp[-1]), rp, cols, vals
+    slab = ps.n
+    N = slab * ws
+    a_loc = airg.SparseMatrix.from_arrays(slab, N, ps.row_offsets, ps.cols, ps.vals)
+    dA = airg.DeviceCSR.upload(a_loc, ctx)
     prm = problems.setup_params(4)
-    a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
-    dA = airg.DeviceCSR.upload(a, ctx)
     uid = [airg.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = airg.NcclComm(ws, rank, uid[0])
-    # distributed setup: row work split over the ranks, slabs all-gathered
-    # (airg_dist_setup); warmed once, then timed (max over ranks)
-    del_h = airg.setup(dA, ctx=ctx, nranks=ws, rank=rank, comm=comm, **prm)
-    del del_h
+    starts = np.arange(ws + 1, dtype=np.int64) * slab
+    lo, hi = starts[rank], starts[rank + 1]
+    # owned setup, warmed once, then timed (max over ranks)
+    warm = airg.Dist.setup_owned(dA, ws, rank=rank, comm=comm, threshold=2.0, starts=starts, ctx=ctx, **prm)
+    del warm
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    h = airg.setup(dA, ctx=ctx, nranks=ws, rank=rank, comm=comm, **prm)
+    d = airg.Dist.setup_owned(dA, ws, rank=rank, comm=comm, threshold=2.0, starts=starts, ctx=ctx, **prm)
     e1.record(stream)
     e1.synchronize()
     setup_ms = e0.elapsed_time(e1)
-    tsm = torch.tensor([setup_ms], device=ctx.tdev, dtype=torch.float64)
+    cf_ms = d.setup_times()[1]  # device time of the setup's CF splits, all levels
+    tsm = torch.tensor([setup_ms, cf_ms, float(d.rank_bytes())], device=ctx.tdev, dtype=torch.float64)
     dist.all_reduce(tsm, op=dist.ReduceOp.MAX)
-    setup_ms = float(tsm[0])
-    slab = ps.n
-    starts = np.arange(ws + 1, dtype=np.int64) * slab
-    d = airg.Dist(h, ws, rank=rank, comm=comm, threshold=2.0, starts=starts)
-    lo, hi = starts[rank], starts[rank + 1]
-    # device bytes of this rank's slabs (the distribution owns them; the
-    # replicated global hierarchy is only needed by the setup and the CF
-    # split timing below)
-    trb = torch.tensor([float(d.rank_bytes())], device=ctx.tdev, dtype=torch.float64)
-    dist.all_reduce(trb, op=dist.ReduceOp.MAX)
-    max_rank_bytes = float(trb[0])
-    # CF split at N GPUs: the row-slab PMISR-DDC (airg_dist_cf_split) on
-    # every level's operator with that level's slabs; max over ranks
-    cf_ms = 0.0
-    for l in range(h.n_levels):
-        Al = h.matrix_handle(l, 0)
-        sl = d.level_info(l)["starts"]
-        seed = int(problems.mix(np.uint64(0), np.uint64(l)))
-        dist.barrier()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record(stream)
-        airg.dist_cf_split_device(Al, sl, rank=rank, comm=comm, alpha=prm["strength_alpha"],
-                                  max_loops=prm["max_loops"], seed=seed, ctx=ctx)
-        c1.record(stream)
-        c1.synchronize()
-        cf_ms += c0.elapsed_time(c1)
-    tcf = torch.tensor([cf_ms], device=ctx.tdev, dtype=torch.float64)
-    dist.all_reduce(tcf, op=dist.ReduceOp.MAX)
-    cf_ms = float(tcf[0])
+    setup_ms, cf_ms, max_rank_bytes = float(tsm[0]), float(tsm[1]), float(tsm[2])
     with torch.cuda.stream(stream):
         tb = torch.from_numpy(ps.b.copy()).to(ctx.tdev)
         tx = torch.empty(hi - lo, dtype=torch.float64, device=ctx.tdev)
@@ -487,11 +473,12 @@ def run_gpu_dist(args):
     t = torch.tensor([sum(times), sum(e2e) / len(e2e)], device=ctx.tdev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms, e2e_ms = float(t[0]), float(t[1])
-    value = p.n * args.steps / (tot_ms / 1e3)
-    levels = [d.level_info(l) for l in range(h.n_levels + 1)]
+    value = N * args.steps / (tot_ms / 1e3)
+    hv_ = OwnedView(d)
+    levels = [d.level_info(l) for l in range(d.n_levels + 1)]
     # roofline of the whole distributed solve step against the N GPUs' HBM
     peak, peak_kind = hbm_peak()
-    step_bytes = gmres_alg_bytes(h, int(st.iterations), prm["coarse_iterations"])
+    step_bytes = gmres_alg_bytes(hv_, int(st.iterations), prm["coarse_iterations"])
     step_ach = step_bytes / (tot_ms / args.steps / 1e3) / 1e9
     # NVLink: halo bytes every process receives (exact, from the halo plans)
     # per V-cycle / level-0 SpMV, plus the allreduce payloads of the GMRES
@@ -519,16 +506,16 @@ def run_gpu_dist(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C4 3D unstructured tets, {nxy} x {nxy} x {nzl * ws} cubes x 6 "
                                f"(one {nzl}-layer z-slab = {ps.n} tets per GPU)",
-                   "unknowns": int(p.n), "nnz": int(p.nnz), "alpha": 0.5, "ddc_fraction": 0.1,
+                   "unknowns": int(N), "nnz": int(d.report(0).nnz), "alpha": 0.5, "ddc_fraction": 0.1,
                    "poly_order": 4, "solver": solver_name(4) + " to rtol 1e-10 from x = 0", "mode": "exact",
                    "parallelism": f"row slabs x{ws} (NCCL halos and allreduces, replay halving, "
-                   "gathered coarse grid; setup row work split over GPUs)",
+                   "gathered coarse grid; owned-row setup: every rank builds only its rows)",
                    "l2": "flushed (512 MiB write) before each timed step"},
         "iterations": int(st.iterations), "final_relative_residual": float(st.final_relative_residual),
-        "levels": int(h.n_levels), "setup_ms": setup_ms,
+        "levels": int(d.n_levels), "setup_ms": setup_ms,
         "active_ranks": [lv["active"] for lv in levels],
         "max_rank_solve_bytes": max_rank_bytes,
-        "e2e": {"value": p.n / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
+        "e2e": {"value": N / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
                 "d2h_bytes_per_step": 8 * int(hi - lo), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches), "cf_split_ms": cf_ms,
         "roofline": roof,

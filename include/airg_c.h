@@ -412,6 +412,9 @@ int airg_dist_setup_owned(airg_ctx* ctx, const airg_csr* a, const int64_t* h_sta
  * nnz_ffinv = |Ac^-1|, coefficients, effective_order, poly_attempts,
  * smoother_growth of the coarse polynomial). info may be null (n_levels only). */
 int airg_dist_report(const airg_dist* d, int64_t level, airg_level_info* info, int64_t* n_levels);
+/* This process's wall time of the owned setup and the device time of its
+ * CF splits (all levels), in ms (0 for airg_dist_create distributions). */
+int airg_dist_setup_times(const airg_dist* d, double* setup_ms, double* cf_split_ms);
 int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg,
                     const double* d_b, double* d_x, airg_solve_stats* stats,
                     double* h_history, int64_t history_cap);

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "airg_dist_setup_owned": ([_VP, _VP, _VP, _P(abi.SetupConfig), _P(abi.Injection), C.c_int32, C.c_int32,
                                        _VP, C.c_double, _P(_VP)], C.c_int),
             "airg_dist_report": ([_VP, C.c_int64, _P(abi.LevelInfo), _P(C.c_int64)], C.c_int),
+            "airg_dist_setup_times": ([_VP, _P(C.c_double), _P(C.c_double)], C.c_int),
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
                                  C.c_int64], C.c_int),
@@ -951,6 +952,12 @@ class Dist:
         info = abi.LevelInfo()
         _check(lib().airg_dist_report(self.d, int(l), C.byref(info), None))
         return info
+
+    def setup_times(self) -> tuple[float, float]:
+        """(wall ms of the owned setup, device ms of its CF splits) on this process."""
+        a, b = C.c_double(), C.c_double()
+        _check(lib().airg_dist_setup_times(self.d, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def release_hierarchy(self):
         """Drop this distribution's reference to the global hierarchy: only

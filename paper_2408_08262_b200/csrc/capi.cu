@@ -1096,6 +1096,14 @@ int airg_dist_report(const airg_dist* dp, int64_t level, airg_level_info* info, 
   });
 }
 
+int airg_dist_setup_times(const airg_dist* dp, double* setup_ms, double* cf_split_ms) {
+  return guard([&] {
+    need(dp, "dist");
+    if (setup_ms) *setup_ms = dp->d.setup_ms;
+    if (cf_split_ms) *cf_split_ms = dp->d.cf_ms;
+  });
+}
+
 int airg_dist_solve(airg_ctx* ctx, airg_dist* d, const airg_solve_config* cfg, const double* b,
                     double* x, airg_solve_stats* st, double* hist, int64_t cap) {
   return guard([&] {

@@ -434,9 +434,38 @@ void set_halo(Ctx& c, DVec& V, int r, Marks& mk) {
   R.halo_host.assign(hh.begin(), hh.end());
 }
 
+// One rank per process, each knowing only its own halo: the halo lists of
+// all ranks all-gathered (sizes, then the padded lists), so every process
+// derives its send lists (and p2p push plans) as in the all-ranks plan.
+void share_halos(Ctx& c, const DHier& d, DVec& V) {
+  const int P = V.part.P(), me = d.me;
+  DVec::Rank& M = V.rk[me];
+  DBuf<int64_t> mine(c, 1), sz(c, (size_t)P);
+  to_device(c, mine.p, &M.nhalo, 1);
+  NCCL_CHECK(ncclAllGather(mine.p, sz.p, 1, ncclInt64, d.comm, c.stream));
+  std::vector<int64_t> hs(P);
+  to_host(c, hs.data(), sz.p, (size_t)P);
+  const int64_t mx = std::max<int64_t>(1, *std::max_element(hs.begin(), hs.end()));
+  DBuf<int32_t> send(c, (size_t)mx), all(c, (size_t)mx * P);
+  if (M.nhalo)
+    CUDA_CHECK(cudaMemcpyAsync(send.p, M.halo.p, sizeof(int32_t) * M.nhalo, cudaMemcpyDeviceToDevice, c.stream));
+  NCCL_CHECK(ncclAllGather(send.p, all.p, (size_t)mx, ncclInt32, d.comm, c.stream));
+  std::vector<int32_t> h((size_t)mx * P);
+  to_host(c, h.data(), all.p, h.size());
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    DVec::Rank& Q = V.rk[q];
+    Q.own = V.part.cnt(q);
+    Q.lo = V.part.lo(q);
+    Q.nhalo = hs[q];
+    Q.halo_host.assign(h.begin() + (size_t)q * mx, h.begin() + (size_t)q * mx + hs[q]);
+  }
+}
+
 // After every rank's halo is known: buffers, emulation tables, NCCL lists.
 void finalize(Ctx& c, DVec& V, const DHier& d, bool peers_known) {
   const int P = V.part.P();
+  if (!peers_known && d.me >= 0 && P > 1) share_halos(c, d, V);
   DBuf<int64_t> ds(c, (size_t)P + 1);
   to_device(c, ds.p, V.part.s.data(), (size_t)P + 1);
   std::vector<double*> bases(P, nullptr);
@@ -457,41 +486,7 @@ void finalize(Ctx& c, DVec& V, const DHier& d, bool peers_known) {
              R.src_idx.p);
     }
   }
-  if (d.me >= 0 && !peers_known) {
-    // my send lists from the peers' requests: the receive counts of every
-    // rank all-gathered, then each rank's halo segment of owner q sent to q
-    DVec::Rank& M = V.rk[d.me];
-    M.send_off.assign(P, 0);
-    M.send_cnt.assign(P, 0);
-    if (P > 1) {
-      DBuf<int64_t> mine(c, (size_t)P), all(c, (size_t)P * P);
-      to_device(c, mine.p, M.recv_cnt.data(), (size_t)P);
-      NCCL_CHECK(ncclAllGather(mine.p, all.p, (size_t)P, ncclInt64, d.comm, c.stream));
-      std::vector<int64_t> h((size_t)P * P);
-      to_host(c, h.data(), all.p, h.size());
-      int64_t tot = 0;
-      for (int q = 0; q < P; ++q) {
-        M.send_off[q] = tot;
-        M.send_cnt[q] = q == d.me ? 0 : h[(size_t)q * P + d.me];
-        tot += M.send_cnt[q];
-      }
-      M.send_idx.alloc(c, (size_t)std::max<int64_t>(1, tot));
-      NCCL_CHECK(ncclGroupStart());
-      for (int q = 0; q < P; ++q) {
-        if (q == d.me) continue;
-        if (M.recv_cnt[q])
-          NCCL_CHECK(ncclSend(M.halo.p + M.recv_off[q], (size_t)M.recv_cnt[q], ncclInt32, q, d.comm, c.stream));
-        if (M.send_cnt[q])
-          NCCL_CHECK(ncclRecv(M.send_idx.p + M.send_off[q], (size_t)M.send_cnt[q], ncclInt32, q, d.comm, c.stream));
-      }
-      NCCL_CHECK(ncclGroupEnd());
-      if (tot) LAUNCH(c, k_shift, blocks_for(tot, 256), 256, 0, tot, M.send_idx.p, M.lo, M.send_idx.p);
-      M.send_buf.alloc(c, (size_t)std::max<int64_t>(1, tot));
-    } else {
-      M.send_idx.alloc(c, 1);
-      M.send_buf.alloc(c, 1);
-    }
-  } else if (d.me >= 0) {  // my send lists: the entries of every peer's halo that I own
+  if (d.me >= 0) {  // my send lists: the entries of every peer's halo that I own
     DVec::Rank& M = V.rk[d.me];
     std::vector<int32_t> idx;
     M.send_off.assign(P, 0);

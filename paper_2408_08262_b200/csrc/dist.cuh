@@ -154,6 +154,7 @@ struct DHier {
   };
   std::vector<Summary> summary;  // fine levels, then the coarse level (n, nnz, nnz_ffinv = |Ac^-1|, ...)
   bool owned = false;
+  double setup_ms = 0.0, cf_ms = 0.0;  // owned setup: wall time, device time of the CF splits (this process)
   // p2p transport: one arena per rank (emulation: all allocated here; NCCL
   // ranks: mine allocated, the peers' opened from their IPC handles)
   struct P2PState {

@@ -29,6 +29,7 @@
 // on another rank); d.me >= 0 is one rank per process, the exchanges are
 // NCCL grouped send / receive and all-gathers.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 
@@ -799,6 +800,18 @@ void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_
   if (cfg.prolongation != 0) throw InvalidArgument("setup: the GPU path implements one-point prolongation only");
   if (cfg.poly_order + 1 > 32 || cfg.coarse_poly_order + 1 > 32)
     throw InvalidArgument("setup: polynomial order above 31 not supported");
+  const auto t_start = std::chrono::steady_clock::now();
+  cudaEvent_t ev0, ev1;
+  CUDA_CHECK(cudaEventCreate(&ev0));
+  CUDA_CHECK(cudaEventCreate(&ev1));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } evg{ev0, ev1};
+  d.cf_ms = 0.0;
   const int64_t N0 = starts[P];
   d.P = P;
   d.me = me;
@@ -937,8 +950,16 @@ void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_
     });
     CfReport rep;
     std::vector<DBuf<double>> labs;
+    CUDA_CHECK(cudaEventRecord(ev0, c.stream));
     cf_split_slabs(c, d, V, loc, cfg.strength_alpha, level_seed, cfg.ddc_enabled != 0, cfg.ddc_fraction,
                    cfg.ddc_bins, labs, rep);
+    CUDA_CHECK(cudaEventRecord(ev1, c.stream));
+    CUDA_CHECK(cudaEventSynchronize(ev1));
+    {
+      float ms = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&ms, ev0, ev1));
+      d.cf_ms += ms;
+    }
     S.n_f_pre = rep.n_f_pre;
     S.n_converted = rep.n_converted;
     S.alpha_diag = rep.alpha_diag;
@@ -1296,6 +1317,7 @@ void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_
     d.summary.push_back(S);
   }
   dist_build(c, d, pc);
+  d.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
 }
 
 }  // namespace airg

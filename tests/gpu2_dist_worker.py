@@ -43,6 +43,22 @@ def main():
     x = ctx.to_host(tx)
     ok &= abs(st.iterations - refg.stats.iterations) <= 1
     ok &= np.linalg.norm(x - refg.x[lo:hi]) <= 1e-8 * np.linalg.norm(refg.x)
+    # owned-row setup over NCCL: this rank's rows only (global columns); the
+    # hierarchy report equals the one-GPU setup's and the solve its bits
+    a_loc = airg.SparseMatrix.from_arrays(int(hi - lo), p.n, p.row_offsets[lo:hi + 1] - p.row_offsets[lo],
+                                          p.cols[p.row_offsets[lo]:p.row_offsets[hi]],
+                                          p.vals[p.row_offsets[lo]:p.row_offsets[hi]])
+    do = airg.Dist.setup_owned(airg.DeviceCSR.upload(a_loc, ctx), ws, rank=rank, comm=comm, threshold=2.0,
+                               starts=starts, ctx=ctx, **prm)
+    ok &= do.n_levels == h.n_levels
+    for l in range(h.n_levels):
+        e, o = h.level(l), do.report(l)
+        ok &= (e.n, e.nnz, e.n_f, e.nnz_ffinv, e.nnz_r, e.poly_attempts) == (o.n, o.nnz, o.n_f, o.nnz_ffinv, o.nnz_r,
+                                                                            o.poly_attempts)
+        ok &= np.array_equal(np.array(e.coefficients), np.array(o.coefficients))
+    st, _ = do.solve_device(tb, tx, coarse_iterations=3)
+    x = ctx.to_host(tx)
+    ok &= st.iterations == ref.stats.iterations and np.array_equal(x.view(np.uint64), ref.x[lo:hi].view(np.uint64))
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if rank == 0:
