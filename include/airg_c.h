@@ -324,9 +324,11 @@ int airg_hier_from_levels(airg_ctx* ctx, int64_t n_levels, const airg_csr* const
                           const uint8_t* const* d_labels, const airg_csr* coarse_a, const airg_csr* coarse_inv,
                           int64_t coarse_iterations, airg_hier** out);
 /* which: 0 A, 1 A_ff, 2 A_fc, 3 A_cf, 4 Aff_inv, 5 R, 6 P, and (fast V-cycle,
- * once built) 7 A_F P (n_f x n_c), 8 W_k (n_f x n_f); level ==
- * n_levels with which 0 / 4 gives the coarse A / coarse inverse. Returns a
- * borrowed handle owned by the hierarchy. */
+ * once built) 7 A_F P (n_f x n_c), 8 W_k (n_f x n_f), and on levels with the
+ * one-pass ascent 9 K = P_F - W_k A_F P (n_f x n_c), 10 [R; W_k E_F^T]
+ * ((n_c + n_f) x n); level == n_levels with which 0 / 4 / 9 gives the coarse
+ * A / coarse inverse / composed coarse solve E_k. Returns a borrowed handle
+ * owned by the hierarchy. */
 int airg_hier_matrix(const airg_hier* h, int64_t level, int32_t which,
                      const airg_csr** out);
 int airg_hier_labels(airg_ctx* ctx, const airg_hier* h, int64_t level,

@@ -613,7 +613,8 @@ def assemble_fixed_sparsity(a, coeffs, effective_order: int, sparsity_order: int
 
 
 # ---- L2 / L3 (air.hpp, solve.hpp) ------------------------------------------------------
-MATRICES = {"a": 0, "a_ff": 1, "a_fc": 2, "a_cf": 3, "ff_inv": 4, "r": 5, "p": 6, "afp": 7, "w": 8}
+MATRICES = {"a": 0, "a_ff": 1, "a_fc": 2, "a_cf": 3, "ff_inv": 4, "r": 5, "p": 6, "afp": 7, "w": 8,
+            "k": 9, "dsc": 10, "coarse_e": 9}
 
 
 class Hierarchy:
@@ -660,6 +661,18 @@ class Hierarchy:
     def fused_nnz(self, l: int) -> tuple[int, int]:
         """(nnz of A_F P, nnz of W) of the fast V-cycle's fused operators."""
         return (self.matrix_handle(l, 7).dims()[2], self.matrix_handle(l, 8).dims()[2])
+
+    def fused_plan(self) -> dict:
+        """Which levels run the fast V-cycle's one-pass ascent (K operator)
+        and whether the coarse solve is composed (fused.cu)."""
+        def has(l, w):
+            try:
+                self.matrix_handle(l, w)
+                return True
+            except InvalidArgument:
+                return False
+        return {"one_pass": [has(l, 9) for l in range(self.n_levels)],
+                "coarse_composed": has(self.n_levels, 9)}
 
     def matrix_handle(self, l: int, which) -> DeviceCSR:
         """Borrowed device handle of a level matrix (no copy)."""

@@ -863,14 +863,16 @@ int airg_hier_matrix(const airg_hier* hp, int64_t l, int32_t which, const airg_c
     if (l == nl) {
       if (which == 0) m = &h->h.coarse_a;
       else if (which == 4) m = &h->h.coarse_inv;
-      else throw InvalidArgument("coarse level has only A (0) and inverse (4)");
+      else if (which == 9 && h->h.coarse_composed) m = &h->h.coarse_e;
+      else throw InvalidArgument("coarse level has only A (0), inverse (4) and a composed solve (9)");
     } else {
       if (l < 0 || l > nl) throw InvalidArgument("level out of range");
       const Level& L = h->h.levels[l];
-      const Csr* ms[9] = {&L.a, &L.aff, &L.afc, &L.acf, &L.ffinv, &L.r, &L.p, &L.afp, &L.fw};
-      if (which < 0 || which > 8) throw InvalidArgument("bad matrix selector");
+      const Csr* ms[11] = {&L.a, &L.aff, &L.afc, &L.acf, &L.ffinv, &L.r, &L.p, &L.afp, &L.fw, &L.fk, &L.dsc};
+      if (which < 0 || which > 10) throw InvalidArgument("bad matrix selector");
       if (which >= 7 && h->h.fused_smooths < 0)
         throw InvalidArgument("fast V-cycle operators not built (setup fused_smooths >= 0 or a fast solve)");
+      if (which >= 9 && !L.one_pass) throw InvalidArgument("level has no one-pass ascent operators");
       m = ms[which];
     }
     // borrowed view: a handle whose Csr aliases the hierarchy's buffers

@@ -292,6 +292,7 @@ inline void to_device(Ctx& c, T* d, const T* h, size_t count) {
 struct Csr {
   int32_t n = 0, m = 0;
   int64_t nnz = 0;
+  int32_t max_row = -1;  // longest row, when measured (row_max; sizes the fast row kernels)
   DBuf<int32_t> rp, ci;
   DBuf<double> v;
 

@@ -80,10 +80,47 @@ void csr_add(Ctx& c, double alpha, const Csr& a, double beta, const Csr& b, Csr&
   out = std::move(r);
 }
 
+
+// one-point map of the F rows: pmap of the F point's fine index
+__global__ void k_pf_map(int nf, const int32_t* __restrict__ f2f, const int32_t* __restrict__ pmap,
+                         int32_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nf) out[k] = pmap[f2f[k]];
+}
+// [top; bottom] row offsets (same column space)
+__global__ void k_vstack_rp(int nt, int nb, int64_t nnz_t, const int32_t* __restrict__ trp,
+                            const int32_t* __restrict__ brp, int32_t* __restrict__ rp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nt) rp[i] = trp[i];
+  else if (i <= nt + nb) rp[i] = (int32_t)nnz_t + brp[i - nt];
+}
+
+void csr_vstack(Ctx& c, const Csr& t, const Csr& b, Csr& out) {
+  if (t.m != b.m) throw InvalidArgument("csr_vstack: column spaces differ");
+  out.alloc(c, (int64_t)t.n + b.n, t.m, t.nnz + b.nnz);
+  LAUNCH(c, k_vstack_rp, blocks_for((int64_t)t.n + b.n + 1, 256), 256, 0, t.n, b.n, t.nnz, t.rp.p, b.rp.p,
+         out.rp.p);
+  if (t.nnz) {
+    CUDA_CHECK(cudaMemcpyAsync(out.ci.p, t.ci.p, sizeof(int32_t) * t.nnz, cudaMemcpyDeviceToDevice, c.stream));
+    CUDA_CHECK(cudaMemcpyAsync(out.v.p, t.v.p, sizeof(double) * t.nnz, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  if (b.nnz) {
+    CUDA_CHECK(cudaMemcpyAsync(out.ci.p + t.nnz, b.ci.p, sizeof(int32_t) * b.nnz, cudaMemcpyDeviceToDevice,
+                               c.stream));
+    CUDA_CHECK(cudaMemcpyAsync(out.v.p + t.nnz, b.v.p, sizeof(double) * b.nnz, cudaMemcpyDeviceToDevice,
+                               c.stream));
+  }
+}
+
+int64_t env_entries(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return (e && e[0]) ? atoll(e) : dflt;
+}
+
 }  // namespace
 
 void build_fused_level(Ctx& c, Level& L, int64_t smooths) {
-  const int n = L.a.n, nf = L.map.nf;
+  const int n = L.a.n, nf = L.map.nf, nc = L.map.nc;
   // A_F P: A's F rows (global columns, C flags cleared) times the one-point P
   Csr afp;
   {
@@ -120,15 +157,89 @@ void build_fused_level(Ctx& c, Level& L, int64_t smooths) {
     w.rp.alloc(c, (size_t)nf + 1);
     CUDA_CHECK(cudaMemsetAsync(w.rp.p, 0, sizeof(int32_t) * (nf + 1), c.stream));
   }
+  // One-pass ascent. With y = W_k b_F formed on the way DOWN (b_l is known
+  // there: [b_{l+1}; y] = [R; W_k E_F^T] b_l in the restriction's launch),
+  //   x_F = (P e_c)_F + W_k (b_F - A_F P e_c) = y + K e_c,  K = P_F - W_k A_F P,
+  // so the ascent of the level is ONE row pass over K instead of two
+  // dependent passes (A_F P, then W_k). It moves nnz(K) - nnz(A_F P) more
+  // entries and saves one dependent launch and the r1 round trip: taken when
+  // the extra entries stay under AIRG_ONEPASS_EXTRA (default 250 k; C4:
+  // level 0, where K is 1.1x A_F P, and levels 15-18; measured per level in
+  // profiles/r2_onepass_levels.txt: level 0's ascent 30 -> 20 us, the
+  // descent's added W b_F about half of that back).
+  L.one_pass = false;
+  L.fk = Csr();
+  L.dsc = Csr();
+  const int64_t extra_max = env_entries("AIRG_ONEPASS_EXTRA", 250000);
+  if (extra_max >= 0 && nf > 0) {
+    Csr wafp, pf, k;
+    spgemm(c, w, afp, wafp);
+    {
+      DBuf<int32_t> pfm(c, (size_t)nf);
+      LAUNCH(c, k_pf_map, blocks_for(nf, 256), 256, 0, nf, L.map.f_to_fine.p, L.pmap.p, pfm.p);
+      prolongation_from_map(c, pfm.p, nf, nc, pf);
+    }
+    csr_add(c, 1.0, pf, -1.0, wafp, k);
+    if (k.nnz - afp.nnz <= extra_max) {
+      Csr wg;
+      map_columns(c, w, L.map.f_to_fine.p, n, wg);
+      csr_vstack(c, L.r, wg, L.dsc);
+      L.fk = std::move(k);
+      L.one_pass = true;
+    }
+  }
   L.afp = std::move(afp);
   L.fw = std::move(w);
 }
 
-void build_fused(Ctx& c, Hier& h, int64_t smooths) {
+// The coarse solve (solve.cpp:34-59) from e = 0 is linear in the coarse rhs:
+// e_k = E_k b with E_1 = Q, E_{k+1} = Q + E_k - Q A E_k. Composed when
+// nnz(E_k) <= AIRG_COARSE_COMPOSE entries: one row pass instead of 2k - 1
+// dependent ones (C4: 280 k entries for k = 3 instead of five launches over
+// 57 k-entry operators).
+void build_coarse_composed(Ctx& c, Hier& h, int64_t its) {
+  h.coarse_e = Csr();
+  h.coarse_composed = false;
+  const int64_t cap = env_entries("AIRG_COARSE_COMPOSE", 4000000);
+  if (its < 1 || h.coarse_a.n == 0 || cap <= 0 || h.coarse_a.n > 50000) return;
+  Csr e;
+  csr_add(c, 1.0, h.coarse_inv, 0.0, h.coarse_inv, e);
+  for (int64_t k = 1; k < its; ++k) {
+    Csr ae, qae, qe, next;
+    spgemm(c, h.coarse_a, e, ae);
+    spgemm(c, h.coarse_inv, ae, qae);
+    csr_add(c, 1.0, h.coarse_inv, 1.0, e, qe);
+    csr_add(c, 1.0, qe, -1.0, qae, next);
+    e = std::move(next);
+    if (e.nnz > cap) return;
+  }
+  if (e.nnz > cap) return;
+  h.coarse_e = std::move(e);
+  h.coarse_composed = true;
+}
+
+void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its) {
   if (smooths < 0) throw InvalidArgument("fast V-cycle: up_f_smooths must be >= 0");
-  if (h.fused_smooths == smooths) return;
-  for (Level& L : h.levels) build_fused_level(c, L, smooths);
-  h.fused_smooths = smooths;
+  if (fused_ready(h, smooths, coarse_its)) return;
+  if (h.fused_smooths != smooths) {
+    for (Level& L : h.levels) build_fused_level(c, L, smooths);
+    h.fused_smooths = smooths;
+  }
+  if (h.fused_coarse_its != coarse_its) {
+    build_coarse_composed(c, h, coarse_its);
+    h.fused_coarse_its = coarse_its;
+  }
+  // the fast row kernels size their lane groups by the longest row (sparse.cu row_lanes)
+  std::vector<Csr*> ms = {&h.coarse_a, &h.coarse_inv};
+  if (h.coarse_composed) ms.push_back(&h.coarse_e);
+  for (Level& L : h.levels) {
+    for (Csr* m : {&L.r, &L.afp, &L.fw}) ms.push_back(m);
+    if (L.one_pass) {
+      ms.push_back(&L.fk);
+      ms.push_back(&L.dsc);
+    }
+  }
+  row_max(c, ms);
   ++h.fused_gen;
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }

@@ -15,6 +15,10 @@ struct Level {
   Csr ffinv, r, p;
   DBuf<int32_t> pmap;        // one-point P as a map (-1 = empty row)
   Csr afp, fw;               // fast V-cycle (fused.cu): A_F P (n_f x n_c) and W_k (n_f x n_f)
+  // one-pass ascent (fused.cu, chosen per level by the entry count): K = P_F - W_k A_F P
+  // (n_f x n_c) and the descent operator [R; W_k E_F^T] ((n_c + n_f) x n)
+  Csr fk, dsc;
+  bool one_pass = false;
   // report
   int64_t n_f_pre = 0, n_converted = 0, attempts = 1, eff = 0;
   double max_theta_pre = 0.0, alpha_diag = 0.0, max_theta_post = 0.0, growth = 0.0;
@@ -47,6 +51,9 @@ struct Hier {
   double grid_c = 0.0, op_c = 0.0, store_c = 0.0;
   int64_t fused_smooths = -1;  // up_f_smooths the fused operators were built for (-1: none)
   int64_t fused_gen = 0;       // bumped by every build (captured graphs hold the operators' pointers)
+  int64_t fused_coarse_its = -1;  // coarse_iterations the composed coarse operator was built for
+  Csr coarse_e;                   // composed coarse solve E_k (fused.cu); empty when not chosen
+  bool coarse_composed = false;
   // coarse workspace
   DBuf<double> cb, cx, cr;
   // top-level solve workspace
@@ -119,7 +126,12 @@ void hier_from_levels(Ctx& c, std::vector<HostLevel>& in, Csr&& coarse_a, Csr&& 
                       int64_t coarse_iterations, Hier& h);
 
 // fused.cu: the fast V-cycle's fused level operators for `smooths` F-smooths
-void build_fused(Ctx& c, Hier& h, int64_t smooths);
+// and the composed coarse solve for `coarse_its` coarse iterations
+void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its);
+// the fused operators match a solve configuration
+inline bool fused_ready(const Hier& h, int64_t smooths, int64_t coarse_its) {
+  return h.fused_smooths == smooths && h.fused_coarse_its == coarse_its;
+}
 
 // solve.cu
 void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x);

@@ -335,7 +335,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
   recompute_metrics(h);
   alloc_workspace(c, h);
   pc.lap(4);
-  if (cfg.fused_smooths >= 0) build_fused(c, h, cfg.fused_smooths);
+  if (cfg.fused_smooths >= 0) build_fused(c, h, cfg.fused_smooths, cfg.coarse_iterations);
   pc.lap(6);
   pc.report();
   CUDA_CHECK(cudaStreamSynchronize(c.stream));

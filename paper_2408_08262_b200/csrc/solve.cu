@@ -141,59 +141,91 @@ struct EpiFres1P {
 };
 // x_l = P e_c + [W r1 on the F rows] in one launch: blocks [0, bf) are lane
 // groups over W's n_f rows, the rest one thread per C point (prolongation
-// only). e_c was written two kernels back (the coarser level's pass), so the
-// prolongated values are loaded before the dependency wait.
-template <int G>
+// only). One-pass ascent (fused.cu): the same with K over e_c and y = W_k b_F
+// from the descent (loaded with the row) in place of W over r1
+// (ONEPASS: x_F = y + K e_c). When e_c was written two or more kernels back
+// (EC_EARLY: the residual pass sits between), the prolongated values are
+// loaded before the dependency wait; otherwise the predecessor is e_c's
+// producer and they are read after it.
+template <int G, bool ONEPASS, bool EC_EARLY>
 __global__ void __launch_bounds__(kTileThreads)
-k_fused_x(TileView w, int bf, const double* __restrict__ rf, const int32_t* __restrict__ f2f,
+k_fused_x(TileView w, int bf, const double* __restrict__ rv, const int32_t* __restrict__ f2f,
           const int32_t* __restrict__ c2f, int nc, const int32_t* __restrict__ pmap, const double* __restrict__ ec,
           double* __restrict__ x) {
-  if ((int)blockIdx.x < bf) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = t / G, lane = t & (G - 1);
-    const bool live = r < w.nrows;
-    LaneRow<G, false> row;
-    int i = 0;
-    double pe = 0.0;
-    if (live) {
-      row.load(w, r, lane);
-      if (lane == 0) {
-        i = __ldg(f2f + r);
-        const int j = __ldg(pmap + i);
-        pe = j >= 0 ? ec[j] : 0.0;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // every thread also prolongates C point t (C threads share the F rows'
+  // blocks: fewer, fuller waves than separate C blocks)
+  int ci = -1, cj = -1;
+  double cv = 0.0;
+  if (t < nc) {
+    ci = __ldg(c2f + t);
+    cj = __ldg(pmap + ci);
+    if (EC_EARLY) cv = cj >= 0 ? ec[cj] : 0.0;
+  }
+  const int r = t / G, lane = t & (G - 1);
+  const bool live = r < w.nrows;
+  LaneRow<G, false> row;
+  int i = 0, j = -1;
+  double pe = 0.0;
+  if (live) {
+    row.load(w, r, lane);
+    if (lane == 0) {
+      i = __ldg(f2f + r);
+      if (ONEPASS) {
+        pe = rv[r];
+      } else {
+        j = __ldg(pmap + i);
+        if (EC_EARLY) pe = j >= 0 ? ec[j] : 0.0;
       }
     }
-    pdl_wait();
-    pdl_trigger();
-    double sf = 0.0, sc;
-    if (live) row.dot(w, rf, lane, sf, sc);
-    sf = group_sum<G>(sf);
-    if (live && lane == 0) x[i] = pe + sf;
-  } else {
-    const int k = ((int)blockIdx.x - bf) * blockDim.x + threadIdx.x;
-    int i = 0;
-    double pe = 0.0;
-    if (k < nc) {
-      i = __ldg(c2f + k);
-      const int j = __ldg(pmap + i);
-      pe = j >= 0 ? ec[j] : 0.0;
-    }
-    pdl_wait();
-    pdl_trigger();
-    if (k < nc) x[i] = pe;
   }
+  pdl_wait();
+  pdl_trigger();
+  if (!EC_EARLY) {
+    if (ci >= 0) cv = cj >= 0 ? ec[cj] : 0.0;
+    if (!ONEPASS && live && lane == 0) pe = j >= 0 ? ec[j] : 0.0;
+  }
+  double sf = 0.0, sc;
+  if (live) row.dot(w, ONEPASS ? ec : rv, lane, sf, sc);
+  sf = group_sum<G>(sf);
+  if (live && lane == 0) x[i] = pe + sf;
+  if (ci >= 0) x[ci] = cv;
 }
 
-void launch_fused_x(Ctx& c, const Level& lv, const double* ec) {
-  const TileView w = tview(lv.fw);
+template <bool ONEPASS, bool EC_EARLY>
+void launch_fused(Ctx& c, const Level& lv, const Csr& m, const double* ec) {
+  const TileView w = tview(m);
   const int G = w.lanes;
   const int bf = (int)(((int64_t)w.nrows * G + kTileThreads - 1) / kTileThreads);
   const int bc = (lv.map.nc + kTileThreads - 1) / kTileThreads;
-  auto* k = G == 1 ? &k_fused_x<1> : G == 2 ? &k_fused_x<2> : G == 4 ? &k_fused_x<4> : G == 8 ? &k_fused_x<8>
-                                                                                        : &k_fused_x<16>;
-  LAUNCH_PDL(c, k, (unsigned)std::max(1, bf + bc), kTileThreads, 0, w, bf, (const double*)lv.rf.p,
+  auto* k = G == 1 ? &k_fused_x<1, ONEPASS, EC_EARLY> : G == 2 ? &k_fused_x<2, ONEPASS, EC_EARLY>
+          : G == 4 ? &k_fused_x<4, ONEPASS, EC_EARLY> : G == 8 ? &k_fused_x<8, ONEPASS, EC_EARLY>
+          : G == 16 ? &k_fused_x<16, ONEPASS, EC_EARLY> : &k_fused_x<32, ONEPASS, EC_EARLY>;
+  LAUNCH_PDL(c, k, (unsigned)std::max(1, std::max(bf, bc)), kTileThreads, 0, w, bf, (const double*)lv.rf.p,
              lv.map.f_to_fine.p, lv.map.c_to_fine.p, (int)lv.map.nc, lv.pmap.p, ec, lv.x.p);
 }
+// ec_early: e_c was produced two or more kernels back
+void launch_fused_x(Ctx& c, const Level& lv, const double* ec, bool ec_early) {
+  if (ec_early)
+    launch_fused<false, true>(c, lv, lv.fw, ec);
+  else
+    launch_fused<false, false>(c, lv, lv.fw, ec);
+}
+void launch_fused_k(Ctx& c, const Level& lv, const double* ec) { launch_fused<true, false>(c, lv, lv.fk, ec); }
+
+// [b_{l+1}; y] = [R; W_k E_F^T] b_l: rows below n0 to y0, the rest to y1
+struct EpiStore2 {
+  double* y0;
+  int n0;
+  double* y1;
+  __device__ void row(int r, double acc) const {
+    if (r < n0)
+      y0[r] = acc;
+    else
+      y1[r - n0] = acc;
+  }
+  __device__ void finish() const {}
+};
 
 // Row kernels of the solve in the configured arithmetic mode (tiled.cuh);
 // `fast` must be in scope.
@@ -381,16 +413,22 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
   const bool fast = cfg.fast != 0;
   const int L = (int)h.levels.size();
   // descent: b_{l+1} = R_l b_l
+  const bool fused = fast && fused_ready(h, cfg.up_f_smooths, cfg.coarse_iterations);
   for (int l = 0; l < L; ++l) {
     Level& lv = h.levels[l];
     const double* bl = l == 0 ? b0 : lv.b.p;
     double* bn = (l + 1 < L) ? h.levels[l + 1].b.p : h.cb.p;
-    if (lv.r.n) ROWS(EpiStore, lv.r, bl, EpiStore{bn});
+    if (fused && lv.one_pass)  // y = W_k b_F into rf, for the one-pass ascent
+      ROWS(EpiStore2, lv.dsc, bl, (EpiStore2{bn, lv.r.n, lv.rf.p}));
+    else if (lv.r.n)
+      ROWS(EpiStore, lv.r, bl, EpiStore{bn});
   }
   // coarse Richardson with the assembled polynomial (solve.cpp:34-59)
   const int nco = h.coarse_a.n;
   const double* rhs = L == 0 ? b0 : h.cb.p;
-  if (nco) {
+  if (nco && fused && h.coarse_composed) {  // e = E_k rhs (fused.cu)
+    ROWS(EpiStore, h.coarse_e, rhs, EpiStore{h.cx.p});
+  } else if (nco) {
     for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
       const double* r = rhs;
       if (it > 0) {
@@ -402,14 +440,18 @@ void enqueue_vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double*
     if (cfg.coarse_iterations <= 0) CUDA_CHECK(cudaMemsetAsync(h.cx.p, 0, sizeof(double) * nco, c.stream));
   }
   // ascent, fast fused form: two row passes per level (fused.cu)
-  if (fast && h.fused_smooths == cfg.up_f_smooths) {
+  if (fused) {
     for (int l = L - 1; l >= 0; --l) {
       Level& lv = h.levels[l];
       const double* bl = l == 0 ? b0 : lv.b.p;
       const double* ec = (l + 1 < L) ? h.levels[l + 1].x.p : h.cx.p;
-      if (cfg.up_f_smooths > 0 && lv.map.nf > 0)
-        ROWS(EpiFres1P, lv.afp, ec, (EpiFres1P{bl, lv.map.f_to_fine.p, lv.rf.p}));
-      launch_fused_x(c, lv, ec);
+      if (lv.one_pass) {
+        launch_fused_k(c, lv, ec);
+        continue;
+      }
+      const bool res = cfg.up_f_smooths > 0 && lv.map.nf > 0;
+      if (res) ROWS(EpiFres1P, lv.afp, ec, (EpiFres1P{bl, lv.map.f_to_fine.p, lv.rf.p}));
+      launch_fused_x(c, lv, ec, res);
     }
     return;
   }
@@ -447,7 +489,8 @@ void enqueue_residual(Ctx& c, Hier& h, const double* b, const double* x, double*
 int64_t graph_key(const Hier& h, const airg_solve_config& cfg) {
   // the fused operators' generation: a rebuild frees the buffers a cached
   // graph points to, so every build changes the key of the fused graphs
-  const int64_t fused = (cfg.fast != 0 && h.fused_smooths == cfg.up_f_smooths) ? 1 + h.fused_gen : 0;
+  const int64_t fused =
+      (cfg.fast != 0 && fused_ready(h, cfg.up_f_smooths, cfg.coarse_iterations)) ? 1 + h.fused_gen : 0;
   return ((cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31 + cfg.down_smooths) * 2 + (cfg.fast != 0)) *
              4096 + fused;
 }
@@ -562,7 +605,8 @@ void f_smooth_level(Ctx& c, Hier& h, int64_t l, const double* d_b, double* d_x) 
 
 void vcycle(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x) {
   check_cfg(cfg);
-  if (cfg.fast && h.fused_smooths != cfg.up_f_smooths) build_fused(c, h, cfg.up_f_smooths);
+  if (cfg.fast && !fused_ready(h, cfg.up_f_smooths, cfg.coarse_iterations))
+    build_fused(c, h, cfg.up_f_smooths, cfg.coarse_iterations);
   const int n = h.top_n();
   CUDA_CHECK(cudaMemcpyAsync(h.r.p, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   const int64_t key = graph_key(h, cfg);
@@ -813,9 +857,10 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[K]) {
 // 3: dots V_k . w and V_k . v_j (fast mode's Gram-corrected CGS2, below).
 // Per block, one partial per k: part[k * nblocks + block] (MODE 3: the Gram
 // column at rows kGmMax + 1 + k).
-template <int MODE, int K>
+template <int MODE, int K, bool LAZY>
 __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* __restrict__ V,
-                                              double* __restrict__ w, const double* hs,
+                                              double* __restrict__ w, const double* hs, const double* vss,
+                                              double* __restrict__ vnext, double* __restrict__ vin,
                                               double (*red)[kGmMax], double (*red2)[kGmMax],
                                               double* __restrict__ part) {
   const int64_t i = (int64_t)blockIdx.x * kGmThreads + threadIdx.x;
@@ -823,11 +868,22 @@ __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* 
   double vk[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) vk[k] = (live && k < jp1) ? __ldg(V + (int64_t)k * n + i) : 0.0;
+  if (LAZY) {  // V holds each v_k unnormalised; vss[k] = 1 / |v_k| (k_gm_step)
+#pragma unroll
+    for (int k = 0; k < K; ++k) vk[k] *= vss[k];
+  }
   double wi = live ? w[i] : 0.0;
   if (MODE > 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) wi = fma(-hs[k], vk[k], wi);
-    if (live) w[i] = wi;
+    if (live) {
+      if (LAZY && MODE == 2) {  // the next basis vector, unnormalised, and the V-cycle input
+        vnext[i] = wi;
+        vin[i] = wi;
+      } else {
+        w[i] = wi;
+      }
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (MODE == 3) {  // V^T w and V^T v_j (the Gram column of the newest vector)
@@ -891,27 +947,36 @@ __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* 
   }
 }
 
-template <int MODE>
+// LAZY (fast mode): the basis is stored unnormalised with its scales in vs
+// (see GmPieces::step); MODE 2 then writes w'' = w - V h straight into
+// V_{j+1} and the V-cycle input instead of w (no separate v = w / |w| pass).
+template <int MODE, bool LAZY>
 __global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double* __restrict__ V,
                                                          double* __restrict__ w, const GmDev* __restrict__ st,
-                                                         const double* __restrict__ h, double* __restrict__ part) {
+                                                         const double* __restrict__ h, double* __restrict__ part,
+                                                         const double* __restrict__ vs, double* __restrict__ Vw,
+                                                         double* __restrict__ vin) {
   __shared__ double hs[kGmMax];
+  __shared__ double vss[LAZY ? kGmMax : 1];
   __shared__ double red[kGmThreads / 32][kGmMax];
   __shared__ double red2[MODE == 3 ? kGmThreads / 32 : 1][kGmMax];
   pdl_wait();
   pdl_trigger();
   const int jp1 = st->j + 1;
-  if (threadIdx.x < kGmMax)
+  if (threadIdx.x < kGmMax) {
     hs[threadIdx.x] = ((MODE == 1 || MODE == 2) && (int)threadIdx.x < jp1) ? h[threadIdx.x] : 0.0;
+    if (LAZY) vss[threadIdx.x] = (int)threadIdx.x < jp1 ? vs[threadIdx.x] : 0.0;
+  }
   __syncthreads();
+  double* vnext = LAZY ? Vw + (int64_t)jp1 * n : nullptr;
   if (jp1 <= 4)
-    gm_sweep_body<MODE, 4>(n, jp1, V, w, hs, red, red2, part);
+    gm_sweep_body<MODE, 4, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
   else if (jp1 <= 8)
-    gm_sweep_body<MODE, 8>(n, jp1, V, w, hs, red, red2, part);
+    gm_sweep_body<MODE, 8, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
   else if (jp1 <= 16)
-    gm_sweep_body<MODE, 16>(n, jp1, V, w, hs, red, red2, part);
+    gm_sweep_body<MODE, 16, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
   else
-    gm_sweep_body<MODE, 32>(n, jp1, V, w, hs, red, red2, part);
+    gm_sweep_body<MODE, 32, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
 }
 
 // h[k] = sum over blocks of part[k][.] (k <= j, or k = 0 for the norm):
@@ -954,15 +1019,25 @@ __global__ void __launch_bounds__(kFinThreads) k_gm_finish(const double* __restr
 }
 
 // w = A z and Z_j = z (z = the V-cycle output; j from the device state)
+// (lazy basis: the V-cycle ran on the unnormalised v_j, so z and A z are
+// scaled by vs[j] = 1 / |v_j| here -- the V-cycle is linear)
 struct EpiGmSpmv {
   double* w;
   const double* z;
   double* Z;
   const GmDev* st;
   int64_t n;
+  const double* vs;  // null: v_j stored normalised
   __device__ void row(int i, double acc) const {
-    w[i] = acc;
-    Z[(int64_t)st->j * n + i] = z[i];
+    const int j = st->j;
+    if (vs) {
+      const double s = vs[j];
+      w[i] = s * acc;
+      Z[(int64_t)j * n + i] = s * z[i];
+    } else {
+      w[i] = acc;
+      Z[(int64_t)j * n + i] = z[i];
+    }
   }
   __device__ void finish() const {}
 };
@@ -986,7 +1061,8 @@ __global__ void k_gm_init(cudaGraphConditionalHandle hout, int cond, const doubl
 
 // cycle start: v_0 = r / beta (into V_0 and the V-cycle input), g = beta e_1
 __global__ void k_gm_cycle(cudaGraphConditionalHandle hin, int cond, int64_t n, const double* __restrict__ r, GmDev* st,
-                           double* __restrict__ V, double* __restrict__ vin, double* __restrict__ g) {
+                           double* __restrict__ V, double* __restrict__ vin, double* __restrict__ g,
+                           double* __restrict__ vs) {
   pdl_wait();
   pdl_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -996,6 +1072,7 @@ __global__ void k_gm_cycle(cudaGraphConditionalHandle hin, int cond, int64_t n, 
   }
   if (blockIdx.x == 0 && threadIdx.x <= st->m) g[threadIdx.x] = threadIdx.x == 0 ? st->beta : 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (vs) vs[0] = 1.0;  // v_0 is stored normalised
     st->j = 0;
     if (cond) cudaGraphSetConditional(hin, st->its < st->maxit ? 1u : 0u);
   }
@@ -1036,7 +1113,7 @@ __global__ void k_gm_gram(const GmDev* __restrict__ st, const double* __restrict
 __global__ void k_gm_step(cudaGraphConditionalHandle hin, int cond, GmDev* st, const double* __restrict__ h1,
                           const double* __restrict__ h2, const double* __restrict__ nrm2, double* __restrict__ H,
                           double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ g,
-                          double* __restrict__ hist) {
+                          double* __restrict__ hist, double* __restrict__ vs) {
   __shared__ double hcol[kGmMax + 1], c_s[kGmMax], s_s[kGmMax];
   pdl_wait();
   pdl_trigger();
@@ -1071,6 +1148,7 @@ __global__ void k_gm_step(cudaGraphConditionalHandle hin, int cond, GmDev* st, c
   if (its < st->cap) hist[its] = est;
   st->hn = hn;
   st->est = est;
+  if (vs) vs[j + 1] = hn > 0.0 ? 1.0 / hn : 0.0;
   st->j = j + 1;
   const bool more = j + 1 < m && its < st->maxit && !(est <= st->rtol) && hn != 0.0;
   if (cond) cudaGraphSetConditional(hin, more ? 1u : 0u);
@@ -1195,18 +1273,20 @@ struct GmPieces {
   int nb, ns;  // element grid, sweep grid
   GmDev* st;
   double *V, *Z, *w, *H, *cs, *sn, *g, *y, *h1, *h2, *nrm, *part, *d, *hsum, *G;
+  double* vs;  // fast mode: scales of the unnormalised basis (null: normalised basis)
   GmPieces(Ctx& c_, Hier& h_, const airg_solve_config& cfg_)
       : c(c_), h(h_), cfg(cfg_), n(h_.top_n()), nb(gm_blocks(h_.top_n())), ns(gm_sweep_blocks(c_, h_.top_n())),
         st(h_.gm_st.p), V(h_.V.p), Z(h_.Z.p),
         w(h_.w.p), H(h_.gm_H.p), cs(h_.gm_cs.p), sn(h_.gm_sn.p), g(h_.gm_g.p), y(h_.gm_y.p), h1(h_.gm_h.p),
         h2(h_.gm_h.p + (kGmMax + 1)), nrm(h_.gm_h.p + 2 * (kGmMax + 1)), part(h_.gm_part.p),
-        d(h_.gm_h.p + 3 * (kGmMax + 1)), hsum(h_.gm_h.p + 5 * (kGmMax + 1)), G(h_.gm_G.p) {}
+        d(h_.gm_h.p + 3 * (kGmMax + 1)), hsum(h_.gm_h.p + 5 * (kGmMax + 1)), G(h_.gm_G.p),
+        vs(cfg_.fast ? h_.gm_h.p + 6 * (kGmMax + 1) : nullptr) {}
   void norm_b() { dot_async(c, h.rhs.p, h.rhs.p, n, h.scal.p + 1, h.part.p); }
   void init(cudaGraphConditionalHandle hout, int cond) {
     LAUNCH(c, k_gm_init, 1, 32, 0, hout, cond, (const double*)(h.scal.p + 1), st, h.gm_hist.p);
   }
   void cycle(cudaGraphConditionalHandle hin, int cond) {
-    LAUNCH(c, k_gm_cycle, (unsigned)nb, kGmThreads, 0, hin, cond, n, (const double*)h.r2.p, st, V, h.r.p, g);
+    LAUNCH(c, k_gm_cycle, (unsigned)nb, kGmThreads, 0, hin, cond, n, (const double*)h.r2.p, st, V, h.r.p, g, vs);
   }
   void tail(cudaGraphConditionalHandle hout, int cond) {
     const bool fast = cfg.fast != 0;
@@ -1216,34 +1296,41 @@ struct GmPieces {
     enqueue_residual(c, h, h.rhs.p, h.xsol.p, h.r2.p, fast);
     LAUNCH_PDL(c, k_gm_restart, 1, 32, 0, hout, cond, st, (const double*)h.scal.p);
   }
+  // Fast mode keeps the basis UNNORMALISED: the second sweep writes
+  // w'' = w - V (h1 + h2) into V_{j+1} and the V-cycle input directly,
+  // k_gm_step records vs[j+1] = 1 / |w''|, the sweeps scale V_k by vs[k] in
+  // registers and the A z epilogue scales z and A z by vs[j] (M is linear),
+  // so no pass forms v = w / |w| (16 MB read + 32 MB written per step).
   void step(cudaGraphConditionalHandle hin, int cond) {
     const bool fast = cfg.fast != 0;
     enqueue_vcycle(c, h, cfg, h.r.p);
     const double* z = vcycle_output(h);
-    ROWS(EpiGmSpmv, h.top(), z, (EpiGmSpmv{w, z, Z, st, n}));
+    ROWS(EpiGmSpmv, h.top(), z, (EpiGmSpmv{w, z, Z, st, n, vs}));
     const double* hcol1 = h1;
+    const double* cV = V;
     if (fast) {  // Gram-corrected CGS2: two sweeps (k_gm_gram)
-      LAUNCH_PDL(c, k_gm_sweep<3>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-                 (const double*)nullptr, part);
+      LAUNCH_PDL(c, (k_gm_sweep<3, true>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
+                 (const double*)nullptr, part, (const double*)vs, V, h.r.p);
       LAUNCH_PDL(c, k_gm_finish, 2 * kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, d);
       LAUNCH_PDL(c, k_gm_gram, 1, 32, 0, (const GmDev*)st, (const double*)d, G, h2, hsum);
-      LAUNCH_PDL(c, k_gm_sweep<2>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-                 (const double*)hsum, part);
+      LAUNCH_PDL(c, (k_gm_sweep<2, true>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
+                 (const double*)hsum, part, (const double*)vs, V, h.r.p);
       hcol1 = d;
     } else {  // CGS2 as the oracle: three sweeps
-      LAUNCH_PDL(c, k_gm_sweep<0>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-                 (const double*)nullptr, part);
+      LAUNCH_PDL(c, (k_gm_sweep<0, false>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
+                 (const double*)nullptr, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr);
       LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h1);
-      LAUNCH_PDL(c, k_gm_sweep<1>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-                 (const double*)h1, part);
+      LAUNCH_PDL(c, (k_gm_sweep<1, false>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
+                 (const double*)h1, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr);
       LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h2);
-      LAUNCH_PDL(c, k_gm_sweep<2>, (unsigned)ns, kGmThreads, 0, n, (const double*)V, w, (const GmDev*)st,
-                 (const double*)h2, part);
+      LAUNCH_PDL(c, (k_gm_sweep<2, false>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
+                 (const double*)h2, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr);
     }
     LAUNCH_PDL(c, k_gm_finish, 1, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 1, nrm);
     LAUNCH_PDL(c, k_gm_step, 1, 32, 0, hin, cond, st, hcol1, (const double*)h2, (const double*)nrm, H,
-               cs, sn, g, h.gm_hist.p);
-    LAUNCH_PDL(c, k_gm_next, (unsigned)nb, kGmThreads, 0, n, (const double*)w, (const GmDev*)st, V, h.r.p);
+               cs, sn, g, h.gm_hist.p, vs);
+    if (!fast)
+      LAUNCH_PDL(c, k_gm_next, (unsigned)nb, kGmThreads, 0, n, (const double*)w, (const GmDev*)st, V, h.r.p);
   }
 };
 
@@ -1344,7 +1431,7 @@ bool gmres_device(Ctx& c, Hier& h, const airg_solve_config& cfg, int m, airg_sol
     h.gm_sn.alloc(c, kGmMax);
     h.gm_g.alloc(c, kGmMax + 1);
     h.gm_y.alloc(c, kGmMax);
-    h.gm_h.alloc(c, 6 * (kGmMax + 1));
+    h.gm_h.alloc(c, 7 * (kGmMax + 1));
     h.gm_G.alloc(c, (size_t)(kGmMax + 1) * (kGmMax + 1));
     h.gm_part.alloc(c, (size_t)2 * (kGmMax + 1) * nb);
   }
@@ -1559,7 +1646,8 @@ void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
 void solve(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x,
            airg_solve_stats& st, std::vector<double>& history) {
   check_cfg(cfg);
-  if (cfg.fast && h.fused_smooths != cfg.up_f_smooths) build_fused(c, h, cfg.up_f_smooths);
+  if (cfg.fast && !fused_ready(h, cfg.up_f_smooths, cfg.coarse_iterations))
+    build_fused(c, h, cfg.up_f_smooths, cfg.coarse_iterations);
   std::memset(&st, 0, sizeof st);
   const int n = h.top_n();
   CUDA_CHECK(cudaMemcpyAsync(h.rhs.p, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));

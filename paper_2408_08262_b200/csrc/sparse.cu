@@ -145,14 +145,52 @@ int row_vec(int64_t n, int64_t nnz) {
 // at most 16) whose first batch (kLaneBatch = 4 entries per lane, loaded
 // before the dependency wait) covers a mean row, so a typical row is one
 // round of coalesced loads (1 = thread per row).
-int row_lanes(int64_t n, int64_t nnz) {
+//
+// Small operators (the coarse levels) are latency bound, not bandwidth
+// bound: a row longer than the first batch costs a further dependent round
+// of (column, value) then x loads after the wait. When the longest row is
+// known and the rows x lanes stay within AIRG_LANE_WAVE threads (default
+// 150 k, about half a wave of 148 SMs x 2048: measured best on C4 against
+// 75 k and 300 k), the lanes grow (up to a warp) until the first batch
+// covers the longest row.
+int row_lanes(int64_t n, int64_t nnz, int32_t max_row) {
   if (n <= 0) return 1;
   // (2, 3 and 6 entries per lane measured 9 %, 2 % and 4 % slower on the
   // C4 GMRES solve)
   const double mean = (double)nnz / (double)n;
   int g = 1;
   while (g < 16 && mean > 4.0 * g) g *= 2;
+  static const int64_t wave = [] {
+    const char* e = getenv("AIRG_LANE_WAVE");
+    return (e && e[0]) ? atoll(e) : (int64_t)150000;
+  }();
+  if (max_row > 0)
+    while (g < 32 && max_row > 4 * g && n * 2 * g <= wave) g *= 2;
   return g;
+}
+
+namespace {
+__global__ void k_row_max(int n, const int32_t* __restrict__ rp, int* __restrict__ out) {
+  int m = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m = max(m, rp[i + 1] - rp[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, m);
+}
+}  // namespace
+
+void row_max(Ctx& c, const std::vector<Csr*>& ms) {
+  if (ms.empty()) return;
+  DBuf<int> d(c, ms.size());
+  CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(int) * ms.size(), c.stream));
+  for (size_t k = 0; k < ms.size(); ++k)
+    if (ms[k]->n > 0)
+      LAUNCH(c, k_row_max, (unsigned)std::min<int64_t>(blocks_for(ms[k]->n, 256), 1184), 256, 0, ms[k]->n,
+             ms[k]->rp.p, d.p + k);
+  std::vector<int> h(ms.size());
+  to_host(c, h.data(), d.p, ms.size());
+  for (size_t k = 0; k < ms.size(); ++k) ms[k]->max_row = h[k];
 }
 
 void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out) {

@@ -19,7 +19,9 @@ void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out
 // nnz entries: 8 = aligned vector batches, 4 / 0 = 4- / 8-entry scalar batches
 int row_vec(int64_t n, int64_t nnz);
 // lanes per row of the fast-mode row kernels (tiled.cuh rows_lanes)
-int row_lanes(int64_t n, int64_t nnz);
+int row_lanes(int64_t n, int64_t nnz, int32_t max_row = -1);
+// measure the longest row of every matrix into its max_row (one readback)
+void row_max(Ctx& c, const std::vector<Csr*>& ms);
 // out = a with every column j replaced by map[j] (order-preserving maps only)
 void map_columns(Ctx& c, const Csr& a, const int32_t* d_map, int32_t new_ncols, Csr& out);
 

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kTileThreads) rows_lanes_fc(TileView m, const 
 
 // ---- launch ------------------------------------------------------------------------
 inline TileView tview(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, m.n, (int)m.nnz, row_vec(m.n, m.nnz), row_lanes(m.n, m.nnz)};
+  return TileView{m.rp.p, m.ci.p, m.v.p, m.n, (int)m.nnz, row_vec(m.n, m.nnz), row_lanes(m.n, m.nnz, m.max_row)};
 }
 
 inline unsigned rows_grid(const TileView& m, bool fast) {
@@ -229,7 +229,8 @@ inline auto rows_kernel(const TileView& m, bool fast) -> void (*)(TileView, cons
       case 2: return &rows_lanes<Epi, 2>;
       case 4: return &rows_lanes<Epi, 4>;
       case 8: return &rows_lanes<Epi, 8>;
-      default: return &rows_lanes<Epi, 16>;
+      case 16: return &rows_lanes<Epi, 16>;
+      default: return &rows_lanes<Epi, 32>;
     }
   }
   return m.vec == 8 ? &rows_thread<Epi, true, 8> : m.vec == 4 ? &rows_thread<Epi, false, 4>
@@ -243,7 +244,8 @@ inline auto rows_kernel_fc(const TileView& m, bool fast) -> void (*)(TileView, c
       case 2: return &rows_lanes_fc<Epi, 2>;
       case 4: return &rows_lanes_fc<Epi, 4>;
       case 8: return &rows_lanes_fc<Epi, 8>;
-      default: return &rows_lanes_fc<Epi, 16>;
+      case 16: return &rows_lanes_fc<Epi, 16>;
+      default: return &rows_lanes_fc<Epi, 32>;
     }
   }
   return m.vec == 8 ? &rows_thread_fc<Epi, true, 8> : m.vec == 4 ? &rows_thread_fc<Epi, false, 4>

@@ -143,6 +143,78 @@ def test_fused_operators_match_products():
         np.testing.assert_allclose(fw, W, rtol=1e-12, atol=1e-13 * max(1.0, abs(W).max()))
 
 
+def test_one_pass_operators_match_products():
+    """The one-pass ascent's operators against scipy products of the
+    hierarchy's own matrices: K = P_F - W_2 A_F P, the descent operator
+    [R; W_2 E_F^T], and the composed coarse solve E_3 = Q + E_2 - Q A E_2."""
+    import scipy.sparse as sp
+    p = problems.make(4, 0.25)
+    prm = dict(problems.setup_params(4), coarse_size_target=300, fused_smooths=2)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+
+    def csr(m):
+        return sp.csr_matrix((m.values, m.col_indices, m.row_offsets), shape=(m.nrows, m.ncols))
+    plan = h.fused_plan()
+    assert any(plan["one_pass"]) and plan["coarse_composed"]
+    for l in range(h.n_levels):
+        if not plan["one_pass"][l]:
+            continue
+        A, P, Q, Aff, R = (csr(h.matrix(l, w)) for w in ("a", "p", "ff_inv", "a_ff", "r"))
+        f = np.flatnonzero(h.labels(l) == 0)
+        W = 2 * Q - Q @ Aff @ Q
+        K = (P[f] - W @ (A[f] @ P)).toarray()
+        k = csr(h.matrix(l, "k")).toarray()
+        np.testing.assert_allclose(k, K, rtol=1e-12, atol=1e-13 * max(1.0, abs(K).max()))
+        EF = sp.csr_matrix((np.ones(len(f)), (np.arange(len(f)), f)), shape=(len(f), A.shape[0]))
+        D = sp.vstack([R, W @ EF]).toarray()
+        np.testing.assert_allclose(csr(h.matrix(l, "dsc")).toarray(), D, rtol=1e-12,
+                                   atol=1e-13 * max(1.0, abs(D).max()))
+    L = h.n_levels
+    Ac, Qc = csr(h.matrix(L, "a")), csr(h.matrix(L, "ff_inv"))
+    E = Qc.copy()
+    for _ in range(2):
+        E = Qc + E - Qc @ (Ac @ E)
+    E = E.toarray()
+    np.testing.assert_allclose(csr(h.matrix(L, "coarse_e")).toarray(), E, rtol=1e-11,
+                               atol=1e-12 * abs(E).max())
+
+
+ONE_PASS_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+p = problems.make(4, 0.5)
+prm = dict(problems.setup_params(4), fused_smooths=2)
+h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+v = h.vcycle(p.b, coarse_iterations=3, fast=1, up_f_smooths=2)
+g = airg.gmres_solve(h, p.b, coarse_iterations=3, fast=1, up_f_smooths=2)
+plan = h.fused_plan()
+np.save(sys.argv[1], np.concatenate([v, g.x, [g.stats.iterations, g.stats.final_relative_residual,
+        sum(plan["one_pass"]), plan["coarse_composed"]]]))
+"""
+
+
+def test_one_pass_vcycle_matches_two_pass(tmp_path):
+    """The fast V-cycle with the one-pass ascent and the composed coarse solve
+    equals the two-pass fast V-cycle up to rounding, and the GMRES solve keeps
+    its iteration count (+-1) and the 1e-8 solution tolerance."""
+    script = tmp_path / "op.py"
+    script.write_text(ONE_PASS_SCRIPT % REPO)
+    outs = {}
+    for name, env in (("one", {"AIRG_ONEPASS_EXTRA": "100000000"}),
+                      ("two", {"AIRG_ONEPASS_EXTRA": "-1", "AIRG_COARSE_COMPOSE": "0"})):
+        f = tmp_path / f"{name}.npy"
+        subprocess.run([sys.executable, str(script), str(f)], check=True, env={**os.environ, **env})
+        outs[name] = np.load(f)
+    n = (len(outs["one"]) - 4) // 2
+    one, two = outs["one"], outs["two"]
+    assert one[-2] > 0 and one[-1] == 1 and two[-2] == 0 and two[-1] == 0
+    np.testing.assert_allclose(one[:n], two[:n], rtol=0, atol=1e-11 * abs(two[:n]).max())
+    assert abs(one[-4] - two[-4]) <= 1 and one[-3] <= 1e-10
+    x1, x2 = one[n:2 * n], two[n:2 * n]
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
+
+
 def test_fused_rebuild_invalidates_captured_graphs():
     """Switching the F-smooth count rebuilds the fused operators (new
     buffers): every cached graph that captured the old ones must be

@@ -25,6 +25,10 @@ def main():
     prm = dict(problems.setup_params(a.config), fused_smooths=2 if a.fast else -1)
     h = airg.setup(airg.DeviceCSR.upload(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), ctx),
                    ctx=ctx, **prm)
+    if a.fast:
+        plan = h.fused_plan()
+        print("one-pass levels:", [l for l, v in enumerate(plan["one_pass"]) if v],
+              "coarse composed:", plan["coarse_composed"])
     tb = ctx.to_device(p.b)
     tx = ctx.empty(p.n, torch.float64)
     if a.profile:

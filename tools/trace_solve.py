@@ -83,9 +83,10 @@ def main():
         # enqueue_vcycle: R_0..R_{L-1}, coarse (2 ci - 1), then per level
         # L-1..0: prolong, fres1, fupd, fres2, fupd, ..., then axpy, resid, sum)
         L = h.n_levels
-        nco = 2 * prm["coarse_iterations"] - 1
+        plan = h.fused_plan() if args.fast else {"one_pass": [False] * L, "coarse_composed": False}
+        nco = 1 if plan["coarse_composed"] else 2 * prm["coarse_iterations"] - 1
         per_lvl = 2 if args.fast else 1 + 2 * 2
-        per_it = L + nco + L * per_lvl + 3
+        per_it = L + nco + (sum(1 if o else per_lvl for o in plan["one_pass"]) if args.fast else L * per_lvl) + 3
         if any("k_loop_check" in e["name"] for e in ev):
             per_it += 1  # device-side convergence test (AIRG_DEVLOOP)
         first = 2  # dot_partials, reduce_partials (bnorm)
@@ -95,18 +96,31 @@ def main():
                      f"{seq[-1]['ts'] + seq[-1]['dur'] - seq[0]['ts']:.1f} us")
         lines.append(f"{'lvl':>3} {'n':>8} {'nnzR':>9} {'R us':>7} {'GB/s':>6} | {'nnzAF':>9} {'fres1':>7} {'GB/s':>6}"
                      f" | {'nnzFF':>8} {'fres2':>6} | {'nnzQ':>8} {'fupd':>6} {'GB/s':>6} | {'prol':>5}")
-        asc = seq[L + nco: L + nco + per_lvl * L]
+        asc = seq[L + nco:]
         if args.fast:
-            lines[-1] = lines[-1] + "  (fast fused: per level R | A_F P residual | W x-update)"
+            lines[-1] = lines[-1] + "  (fast fused: per level R | A_F P residual | W x-update; 1p = one-pass K)"
+            lines.append(f"coarse: {nco} kernels, " + " ".join(f"{e['marg']:.1f}" for e in seq[L:L + nco]) + " us")
             lines.append(f"{'lvl':>3} {'n':>8} {'nnzR':>9} {'R us':>7} | {'nnzAFP':>9} {'fres':>6} {'GB/s':>6} | {'nnzWX':>9} {'xw':>6} {'GB/s':>6}")
-            for l in range(L):
+            pos = 0
+            rows = []
+            for l in range(L - 1, -1, -1):
                 info = h.level(l)
-                blk = asc[(L - 1 - l) * 2:(L - l) * 2]
                 af, wx = h.fused_nnz(l)
+                if plan["one_pass"][l]:
+                    k = h.matrix_handle(l, 9).dims()[2]
+                    e = asc[pos]
+                    pos += 1
+                    bk = 12 * k + 4 * info.n_f + 8 * info.n_c + 8 * info.n_f + 16 * info.n
+                    rows.append(f"{l:3d} {info.n:8d} {info.nnz_r:9d} {seq[l]['marg']:7.1f} | 1p K {k:9d} {e['marg']:6.1f} "
+                                f"{bk / e['marg'] / 1e3:6.0f}")
+                    continue
+                blk = asc[pos:pos + 2]
+                pos += 2
                 bf = 12 * af + 4 * info.n_f + 8 * info.n_c + 8 * info.n_f + 8 * info.n_f
                 bw = 12 * wx + 4 * info.n_f + 8 * info.n_f + 24 * info.n
-                lines.append(f"{l:3d} {info.n:8d} {info.nnz_r:9d} {seq[l]['marg']:7.1f} | {af:9d} {blk[0]['marg']:6.1f} "
-                             f"{bf / blk[0]['marg'] / 1e3:6.0f} | {wx:9d} {blk[1]['marg']:6.1f} {bw / blk[1]['marg'] / 1e3:6.0f}")
+                rows.append(f"{l:3d} {info.n:8d} {info.nnz_r:9d} {seq[l]['marg']:7.1f} | {af:9d} {blk[0]['marg']:6.1f} "
+                            f"{bf / blk[0]['marg'] / 1e3:6.0f} | {wx:9d} {blk[1]['marg']:6.1f} {bw / blk[1]['marg'] / 1e3:6.0f}")
+            lines.extend(reversed(rows))
             L = 0
         for l in range(L):
             info = h.level(l)
