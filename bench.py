@@ -64,11 +64,19 @@ def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2, fast=False):
     x = P e_c + W r1 (W rows on the F points, the C points prolongated)."""
     info = h.info()
     per_cycle = 0
+    plan = h.fused_plan() if fast else None
     if fast:
         for l in range(info.n_levels):
             lv = h.level(l)
             n, nf, nc = lv.n, lv.n_f, lv.n_c
             afp, wx = h.fused_nnz(l)
+            if plan["one_pass"][l]:
+                # [b_{l+1}; y] = [R; W E_F^T] b_l, then x_F = y + K e_c (+ the C points)
+                k = h.matrix_handle(l, 9).dims()[2]
+                desc = 12 * (lv.nnz_r + wx) + 4 * (nc + nf + 1) + 8 * n + 8 * (nc + nf)
+                asc = 12 * k + 4 * (nf + 1) + 8 * nc + nf * (4 + 8 + 8) + nc * (4 + 4 + 8)
+                per_cycle += desc + asc
+                continue
             r = 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc
             fres = 12 * afp + 4 * (nf + 1) + 8 * nc + nf * (4 + 8 + 8)
             xw = 12 * wx + 4 * (nf + 1) + 8 * nf + n * (4 + 4 + 8) + 8 * nc
@@ -88,6 +96,8 @@ def vcycle_alg_bytes(h, coarse_iterations, up_smooths=2, fast=False):
         smooths = fres1 + fupd + (up_smooths - 1) * (fres2 + fupd)
         per_cycle += r + prol + smooths
     cn = info.coarse_n
+    if fast and plan["coarse_composed"]:  # e = E_k b (fused.cu)
+        return per_cycle + 12 * h.matrix_handle(info.n_levels, 9).dims()[2] + 4 * (cn + 1) + 16 * cn
     for it in range(coarse_iterations):
         per_cycle += 12 * info.coarse_inv_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
         if it:
@@ -119,8 +129,10 @@ def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, 
     V_0..V_j (dots; first update fused with the second dots; second update
     with the norm); fast mode: two (dots with w and v_j; the update with the
     Gram-corrected coefficients and the norm) -- plus w read / written per
-    sweep, and v_{j+1} = w / |w|. Per restart: x += Z y (j + 2 vectors),
-    r = b - A x and its norm."""
+    sweep, and v_{j+1} = w / |w| (exact); the fast mode's second sweep writes
+    the unnormalised v_{j+1} and the V-cycle input instead (solve.cu
+    GmPieces::step). Per restart: x += Z y (j + 2 vectors), r = b - A x and
+    its norm."""
     info = h.info()
     top = h.level(0) if info.n_levels else None
     n = top.n if top else info.coarse_n
@@ -132,8 +144,10 @@ def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, 
     while left > 0:
         j_max = min(restart, left)
         for j in range(j_max):
-            sweeps = 2 if fast else 3
-            tot += cyc + spmv + 8 * n + sweeps * (j + 1) * 8 * n + (2 * sweeps - 1) * 8 * n + 24 * n
+            if fast:  # two sweeps: w read twice, v_{j+1} and the V-cycle input written
+                tot += cyc + spmv + 8 * n + 2 * (j + 1) * 8 * n + 4 * 8 * n
+            else:  # three sweeps, then v_{j+1} = w / |w| (w read, two vectors written)
+                tot += cyc + spmv + 8 * n + 3 * (j + 1) * 8 * n + 5 * 8 * n + 24 * n
         tot += (j_max + 2) * 8 * n + spmv + 8 * n
         left -= j_max
     return tot

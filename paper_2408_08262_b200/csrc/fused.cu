@@ -16,6 +16,9 @@
 // (the F-F graph is sparse), so the fused pass moves fewer bytes as well
 // as halving the dependent launches of the ascent (6 -> 3 per level, with
 // the restriction on the way down).
+#include <chrono>
+#include <cstdio>
+
 #include "hier.cuh"
 
 namespace airg {
@@ -112,6 +115,27 @@ void csr_vstack(Ctx& c, const Csr& t, const Csr& b, Csr& out) {
   }
 }
 
+// products of A B (sum over A's entries of the B row length): the SpGEMM's
+// work, one block atomic
+__global__ void k_products(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                           const int32_t* __restrict__ brp, unsigned long long* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long s = 0;
+  if (i < n)
+    for (int k = arp[i]; k < arp[i + 1]; ++k) s += (unsigned long long)(brp[aci[k] + 1] - brp[aci[k]]);
+  block_add(out, s);
+}
+
+int64_t products(Ctx& c, const Csr& a, const Csr& b) {
+  if (a.n == 0) return 0;
+  DBuf<unsigned long long> d(c, 1);
+  CUDA_CHECK(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), c.stream));
+  LAUNCH(c, k_products, blocks_for(a.n, 256), 256, 0, a.n, a.rp.p, a.ci.p, b.rp.p, d.p);
+  unsigned long long h = 0;
+  to_host(c, &h, d.p, 1);
+  return (int64_t)h;
+}
+
 int64_t env_entries(const char* name, int64_t dflt) {
   const char* e = getenv(name);
   return (e && e[0]) ? atoll(e) : dflt;
@@ -164,14 +188,20 @@ void build_fused_level(Ctx& c, Level& L, int64_t smooths) {
   // dependent passes (A_F P, then W_k). It moves nnz(K) - nnz(A_F P) more
   // entries and saves one dependent launch and the r1 round trip: taken when
   // the extra entries stay under AIRG_ONEPASS_EXTRA (default 250 k; C4:
-  // level 0, where K is 1.1x A_F P, and levels 15-18; measured per level in
-  // profiles/r2_onepass_levels.txt: level 0's ascent 30 -> 20 us, the
+  // level 0, where K is 1.1x A_F P; measured per level in
+  // profiles/r2_onepass_levels.txt: level 0's ascent 30 -> 17-20 us, the
   // descent's added W b_F about half of that back).
   L.one_pass = false;
   L.fk = Csr();
   L.dsc = Csr();
   const int64_t extra_max = env_entries("AIRG_ONEPASS_EXTRA", 250000);
-  if (extra_max >= 0 && nf > 0) {
+  // K is formed only where W A_F P averages at most AIRG_ONEPASS_ROWWORK
+  // products per row (default 16): on C4 level 0 (3.8 per row, 0.5 ms of
+  // setup); the coarse levels' rows take 90-950 products (6-28 ms of SpGEMM
+  // per level for about 1 us per V-cycle on levels 15-18, and K 5-13x A_F P
+  // on the mid levels)
+  const int64_t row_work = env_entries("AIRG_ONEPASS_ROWWORK", 16);
+  if (extra_max >= 0 && nf > 0 && products(c, w, afp) <= row_work * (int64_t)nf) {
     Csr wafp, pf, k;
     spgemm(c, w, afp, wafp);
     {
@@ -221,13 +251,28 @@ void build_coarse_composed(Ctx& c, Hier& h, int64_t its) {
 void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its) {
   if (smooths < 0) throw InvalidArgument("fast V-cycle: up_f_smooths must be >= 0");
   if (fused_ready(h, smooths, coarse_its)) return;
+  const char* te = getenv("AIRG_SETUP_TIMING");
+  const bool timing = te && te[0] == '1';
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what, int64_t l) {
+    if (!timing) return;
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "fused %s %lld: %.2f ms\n", what, (long long)l,
+            std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   if (h.fused_smooths != smooths) {
-    for (Level& L : h.levels) build_fused_level(c, L, smooths);
+    for (size_t l = 0; l < h.levels.size(); ++l) {
+      build_fused_level(c, h.levels[l], smooths);
+      lap(h.levels[l].one_pass ? "level(one-pass)" : "level", (int64_t)l);
+    }
     h.fused_smooths = smooths;
   }
   if (h.fused_coarse_its != coarse_its) {
     build_coarse_composed(c, h, coarse_its);
     h.fused_coarse_its = coarse_its;
+    lap("coarse", coarse_its);
   }
   // the fast row kernels size their lane groups by the longest row (sparse.cu row_lanes)
   std::vector<Csr*> ms = {&h.coarse_a, &h.coarse_inv};

@@ -6,6 +6,7 @@
 #include "dd.cuh"
 #include "rowsplit.cuh"
 #include "sparse.cuh"
+#include "tiled.cuh"
 
 namespace airg {
 
@@ -218,6 +219,62 @@ __global__ void scale_by(int n, double* __restrict__ v, const double* __restrict
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const double gg = *g;
   if (i < n && gg != 0.0) v[i] = v[i] / gg;
+}
+
+// growth guard, one power step in two row passes (single GPU): the iterate u
+// is kept unnormalised with its norm g from the previous step --
+//   av = (A u) / g;   u <- u / g - Q av,  one partial of |u|^2 per block
+struct EpiScaled {  // y = acc / g (g from the predecessor: read after the wait)
+  double* y;
+  const double* g;
+  __device__ void row(int i, double acc) const { y[i] = acc / *g; }
+  __device__ void finish() const {}
+};
+struct EpiGrowth {  // u_i <- u_i / g - (Q av)_i, partial |u|^2
+  double* u;
+  const double* g;
+  double* part;
+  mutable double s;
+  struct Pre {
+    double ui, gg;
+  };
+  __device__ Pre pre(int i) const { return Pre{u[i], *g}; }  // u: three kernels back, g: two
+  __device__ void row_pre(int i, double acc, const Pre& p) const {
+    const double r = p.ui / p.gg - acc;
+    u[i] = r;
+    s += r * r;
+  }
+  __device__ void finish() const {
+    __shared__ double sm[32];
+    double v = s;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+  }
+};
+__global__ void finish_norm_pdl(const double* __restrict__ part, int np, double* __restrict__ g) {
+  __shared__ double sm[32];
+  pdl_wait();
+  pdl_trigger();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *g = sqrt(s);
+  }
 }
 
 }  // namespace
@@ -590,13 +647,26 @@ double smoother_growth(Ctx& c, const Csr& a, const Csr& q, const RowSplit* rs) {
   zero.zero(c);
   LAUNCH(c, sub_partial, blocks, threads, 0, n, v.p, zero.p, part.p);
   LAUNCH(c, finish_norm, 1, 1024, 0, part.p, blocks, g.p + kIters);
-  LAUNCH(c, scale_by, blocks_for(n, 256), 256, 0, n, v.p, g.p + kIters);
+  if (rs) LAUNCH(c, scale_by, blocks_for(n, 256), 256, 0, n, v.p, g.p + kIters);
   RowSlices sa, sq;
   if (rs) {
     sa.build(c, *rs, a);
     sq.build(c, *rs, q);
   }
-  for (int k = 0; k < kIters; ++k) {
+  if (!rs) {
+    // three PDL-chained launches per step instead of five (v is rescaled in
+    // the next step's epilogues instead of by a separate pass)
+    const TileView tq = tview(q);
+    const int nbq = (int)rows_grid(tq, false);
+    DBuf<double> qpart(c, (size_t)nbq);
+    for (int k = 0; k < kIters; ++k) {
+      const double* gprev = k == 0 ? g.p + kIters : g.p + k - 1;
+      LAUNCH_ROWS(c, EpiScaled, tview(a), v.p, (EpiScaled{av.p, gprev}));
+      LAUNCH_ROWS(c, EpiGrowth, tq, av.p, (EpiGrowth{v.p, gprev, qpart.p, 0.0}));
+      LAUNCH_PDL(c, finish_norm_pdl, 1, 1024, 0, (const double*)qpart.p, nbq, g.p + k);
+    }
+  }
+  for (int k = 0; k < (rs ? kIters : 0); ++k) {
     if (rs) {  // slab SpMVs, gathered: the norms below see the same full vectors
       split_spmv(c, *rs, sa, v.p, av.p);
       split_spmv(c, *rs, sq, av.p, qav.p);

@@ -862,12 +862,18 @@ __device__ __forceinline__ void gm_sweep_body(int64_t n, int jp1, const double* 
                                               double* __restrict__ w, const double* hs, const double* vss,
                                               double* __restrict__ vnext, double* __restrict__ vin,
                                               double (*red)[kGmMax], double (*red2)[kGmMax],
-                                              double* __restrict__ part) {
+                                              double* __restrict__ part, int vhint) {
   const int64_t i = (int64_t)blockIdx.x * kGmThreads + threadIdx.x;
   const bool live = i < n;
   double vk[K];
+  if (LAZY && vhint) {  // fast mode: the basis is streamed with L2 evict_first
+    const unsigned long long pol = l2_policy(vhint);
 #pragma unroll
-  for (int k = 0; k < K; ++k) vk[k] = (live && k < jp1) ? __ldg(V + (int64_t)k * n + i) : 0.0;
+    for (int k = 0; k < K; ++k) vk[k] = (live && k < jp1) ? ld_hint(V + (int64_t)k * n + i, pol) : 0.0;
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) vk[k] = (live && k < jp1) ? __ldg(V + (int64_t)k * n + i) : 0.0;
+  }
   if (LAZY) {  // V holds each v_k unnormalised; vss[k] = 1 / |v_k| (k_gm_step)
 #pragma unroll
     for (int k = 0; k < K; ++k) vk[k] *= vss[k];
@@ -955,7 +961,7 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double
                                                          double* __restrict__ w, const GmDev* __restrict__ st,
                                                          const double* __restrict__ h, double* __restrict__ part,
                                                          const double* __restrict__ vs, double* __restrict__ Vw,
-                                                         double* __restrict__ vin) {
+                                                         double* __restrict__ vin, int vhint) {
   __shared__ double hs[kGmMax];
   __shared__ double vss[LAZY ? kGmMax : 1];
   __shared__ double red[kGmThreads / 32][kGmMax];
@@ -970,13 +976,13 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double
   __syncthreads();
   double* vnext = LAZY ? Vw + (int64_t)jp1 * n : nullptr;
   if (jp1 <= 4)
-    gm_sweep_body<MODE, 4, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
+    gm_sweep_body<MODE, 4, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part, vhint);
   else if (jp1 <= 8)
-    gm_sweep_body<MODE, 8, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
+    gm_sweep_body<MODE, 8, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part, vhint);
   else if (jp1 <= 16)
-    gm_sweep_body<MODE, 16, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
+    gm_sweep_body<MODE, 16, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part, vhint);
   else
-    gm_sweep_body<MODE, 32, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part);
+    gm_sweep_body<MODE, 32, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part, vhint);
 }
 
 // h[k] = sum over blocks of part[k][.] (k <= j, or k = 0 for the norm):
@@ -1218,6 +1224,16 @@ __global__ void k_gm_restart(cudaGraphConditionalHandle hout, int cond, GmDev* s
   if (cond) cudaGraphSetConditional(hout, (!conv && beta != 0.0 && st->its < st->maxit) ? 1u : 0u);
 }
 
+// L2 priority of the fast sweeps' basis loads (AIRG_L2_SWEEP: 1 evict_first,
+// the default: 468 -> 466 us per C4 iteration; 0 default priority)
+int sweep_l2() {
+  static const int v = [] {
+    const char* e = getenv("AIRG_L2_SWEEP");
+    return (e && e[0]) ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 int gm_blocks(int64_t n) { return (int)std::max<int64_t>(1, (n + kGmThreads - 1) / kGmThreads); }
 int gm_sweep_blocks(const Ctx&, int64_t n) { return gm_blocks(n); }
 
@@ -1310,21 +1326,21 @@ struct GmPieces {
     const double* cV = V;
     if (fast) {  // Gram-corrected CGS2: two sweeps (k_gm_gram)
       LAUNCH_PDL(c, (k_gm_sweep<3, true>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
-                 (const double*)nullptr, part, (const double*)vs, V, h.r.p);
+                 (const double*)nullptr, part, (const double*)vs, V, h.r.p, sweep_l2());
       LAUNCH_PDL(c, k_gm_finish, 2 * kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, d);
       LAUNCH_PDL(c, k_gm_gram, 1, 32, 0, (const GmDev*)st, (const double*)d, G, h2, hsum);
       LAUNCH_PDL(c, (k_gm_sweep<2, true>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
-                 (const double*)hsum, part, (const double*)vs, V, h.r.p);
+                 (const double*)hsum, part, (const double*)vs, V, h.r.p, sweep_l2());
       hcol1 = d;
     } else {  // CGS2 as the oracle: three sweeps
       LAUNCH_PDL(c, (k_gm_sweep<0, false>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
-                 (const double*)nullptr, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr);
+                 (const double*)nullptr, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr, 0);
       LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h1);
       LAUNCH_PDL(c, (k_gm_sweep<1, false>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
-                 (const double*)h1, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr);
+                 (const double*)h1, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr, 0);
       LAUNCH_PDL(c, k_gm_finish, kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, h2);
       LAUNCH_PDL(c, (k_gm_sweep<2, false>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
-                 (const double*)h2, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr);
+                 (const double*)h2, part, (const double*)nullptr, (double*)nullptr, (double*)nullptr, 0);
     }
     LAUNCH_PDL(c, k_gm_finish, 1, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 1, nrm);
     LAUNCH_PDL(c, k_gm_step, 1, 32, 0, hin, cond, st, hcol1, (const double*)h2, (const double*)nrm, H,

@@ -36,7 +36,7 @@ struct TileView {
   int nrows;
   int nnz;   // bounds the aligned vector loads
   int vec;   // exact mode: entries per vector batch (8), 4-entry scalar (4), 8-entry scalar (0)
-  int lanes; // fast mode: lanes per row (1, 2, 4, 8, 16)
+  int lanes; // fast mode: lanes per row (1, 2, 4, 8, 16, 32)
 };
 
 // Epilogues may expose `Pre pre(int row)`: operands the epilogue reads that

@@ -1,5 +1,5 @@
-"""One batched CF split of every C2 level inside a cudaProfilerStart/Stop
-window, for ncu --profile-from-start off (tools/gpu_ncu_cf.sh)."""
+"""One batched CF split of every level (C2, or CF_CONFIG) inside a
+cudaProfilerStart/Stop window, for ncu --profile-from-start off."""
 import os
 import sys
 
@@ -10,8 +10,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2408_08262_b200 import airg, problems  # noqa: E402
 
 ctx = airg.Context(0)
-p = problems.make(2)
-prm = problems.setup_params(2)
+cfg = int(os.environ.get("CF_CONFIG", "2"))
+p = problems.make(cfg)
+prm = problems.setup_params(cfg)
 a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
 h = airg.setup(airg.DeviceCSR.upload(a, ctx), ctx=ctx, **prm)
 mats = [h.matrix_handle(l, 0) for l in range(h.n_levels)]
