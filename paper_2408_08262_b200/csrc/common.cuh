@@ -112,6 +112,11 @@ __device__ __forceinline__ double ld_hint(const double* a, unsigned long long po
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(d) : "l"(a), "l"(pol));
   return d;
 }
+__device__ __forceinline__ double2 ld2_hint(const double* a, unsigned long long pol) {
+  double2 d;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(d.x), "=d"(d.y) : "l"(a), "l"(pol));
+  return d;
+}
 __device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
   int d;
   asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(d) : "l"(a), "l"(pol));
