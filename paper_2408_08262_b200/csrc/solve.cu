@@ -985,20 +985,23 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep(int64_t n, const double
     gm_sweep_body<MODE, 32, LAZY>(n, jp1, V, w, hs, vss, vnext, vin, red, red2, part, vhint);
 }
 
-// Fast-mode sweeps over the unnormalised basis (n even): two elements per
-// thread with 16-byte loads of every column, the basis streamed in chunks of
-// eight columns whatever j is -- registers no longer scale with the basis
+// Fast-mode sweeps over the unnormalised basis (n even): two or four
+// elements per thread with 16-byte loads of every column, the basis streamed
+// in chunks of eight columns whatever j is -- registers no longer scale with the basis
 // (the K-specialised register tile above needs 94 registers at K = 32: 23 %
 // occupancy). MODE 3: the dots V_k . w and V_k . v_j (Gram column), one
 // 16-wide transpose-reduce per chunk; MODE 2: w'' = w - V h into V_{j+1} and
-// the V-cycle input, |w''|^2. Partials as k_gm_sweep (grid = n / 512).
-template <int MODE>
+// the V-cycle input, |w''|^2. Partials as k_gm_sweep (grid = n / (512 P)).
+template <int MODE, int P>
 __global__ void __launch_bounds__(kGmThreads) k_gm_sweep_fast(int64_t n, const double* __restrict__ V,
                                                               const double* __restrict__ w,
                                                               const GmDev* __restrict__ st,
                                                               const double* __restrict__ h, double* __restrict__ part,
                                                               const double* __restrict__ vs, double* __restrict__ Vw,
                                                               double* __restrict__ vin) {
+  // P double2 pairs (2P elements) per thread, CH columns per chunk (16
+  // measured 1.5-3 % slower per iteration)
+  constexpr int CH = 8;
   __shared__ double hs[kGmMax];
   __shared__ double vss[kGmMax];
   __shared__ double red[kGmThreads / 32][2 * kGmMax];
@@ -1012,29 +1015,51 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep_fast(int64_t n, const d
     hs[threadIdx.x] = (MODE == 2 && in) ? h[threadIdx.x] * sc : 0.0;
   }
   __syncthreads();
-  const int64_t i0 = 2 * ((int64_t)blockIdx.x * kGmThreads + threadIdx.x);
-  const bool live = i0 < n;
+  const int64_t i0 = 2 * P * ((int64_t)blockIdx.x * kGmThreads + threadIdx.x);
   const unsigned long long pol = l2_policy(1);
   const double2 zero2 = make_double2(0.0, 0.0);
-  const double2 wv = live ? *reinterpret_cast<const double2*>(w + i0) : zero2;
+  bool live[P];
+  double2 wv[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) {
+    live[u] = i0 + 2 * u < n;
+    wv[u] = live[u] ? *reinterpret_cast<const double2*>(w + i0 + 2 * u) : zero2;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (MODE == 3) {
-    double2 vj = live ? ld2_hint(V + (int64_t)(jp1 - 1) * n + i0, pol) : zero2;
-    vj.x *= vss[jp1 - 1];
-    vj.y *= vss[jp1 - 1];
-    for (int c0 = 0; c0 < jp1; c0 += 8) {
-      double2 vk[8];
+    double2 vj[P];
+    const double sj = vss[jp1 - 1];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) vk[q] = (live && c0 + q < jp1) ? ld2_hint(V + (int64_t)(c0 + q) * n + i0, pol) : zero2;
-      double both[16];
+    for (int u = 0; u < P; ++u) {
+      vj[u] = live[u] ? ld2_hint(V + (int64_t)(jp1 - 1) * n + i0 + 2 * u, pol) : zero2;
+      vj[u].x *= sj;
+      vj[u].y *= sj;
+    }
+    for (int c0 = 0; c0 < jp1; c0 += CH) {
+      double2 vk[CH][P];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double sk = vss[c0 + q];
-        both[q] = sk * fma(vk[q].x, wv.x, vk[q].y * wv.y);
-        both[8 + q] = sk * fma(vk[q].x, vj.x, vk[q].y * vj.y);
+      for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int u = 0; u < P; ++u)
+          vk[q][u] = (live[u] && c0 + q < jp1) ? ld2_hint(V + (int64_t)(c0 + q) * n + i0 + 2 * u, pol) : zero2;
+      double both[2 * CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        double a = 0.0, g = 0.0;
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+          a = fma(vk[q][u].x, wv[u].x, fma(vk[q][u].y, wv[u].y, a));
+          g = fma(vk[q][u].x, vj[u].x, fma(vk[q][u].y, vj[u].y, g));
+        }
+        const double sk = (c0 + q < kGmMax) ? vss[c0 + q] : 0.0;
+        both[q] = sk * a;
+        both[CH + q] = sk * g;
       }
-      const double t = warp_transpose_sum<16>(both);
-      if (lane < 16) red[warp][lane < 8 ? c0 + lane : kGmMax + c0 + lane - 8] = t;
+      const double t = warp_transpose_sum<2 * CH>(both);
+      if (lane < 2 * CH) {
+        const int k = c0 + (lane < CH ? lane : lane - CH);
+        if (k < kGmMax) red[warp][lane < CH ? k : kGmMax + k] = t;
+      }
     }
     __syncthreads();
     if ((int)threadIdx.x < jp1) {
@@ -1051,23 +1076,35 @@ __global__ void __launch_bounds__(kGmThreads) k_gm_sweep_fast(int64_t n, const d
       part[(int64_t)(kGmMax + 1 + k) * gridDim.x + blockIdx.x] = v;
     }
   } else {
-    double ax = wv.x, ay = wv.y;
-    for (int c0 = 0; c0 < jp1; c0 += 8) {
-      double2 vk[8];
+    double2 acc[P];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) vk[q] = (live && c0 + q < jp1) ? ld2_hint(V + (int64_t)(c0 + q) * n + i0, pol) : zero2;
+    for (int u = 0; u < P; ++u) acc[u] = wv[u];
+    for (int c0 = 0; c0 < jp1; c0 += CH) {
+      double2 vk[CH][P];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double hk = hs[c0 + q];
-        ax = fma(-hk, vk[q].x, ax);
-        ay = fma(-hk, vk[q].y, ay);
+      for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int u = 0; u < P; ++u)
+          vk[q][u] = (live[u] && c0 + q < jp1) ? ld2_hint(V + (int64_t)(c0 + q) * n + i0 + 2 * u, pol) : zero2;
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const double hk = (c0 + q < kGmMax) ? hs[c0 + q] : 0.0;
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+          acc[u].x = fma(-hk, vk[q][u].x, acc[u].x);
+          acc[u].y = fma(-hk, vk[q][u].y, acc[u].y);
+        }
       }
     }
-    if (live) {
-      *reinterpret_cast<double2*>(Vw + (int64_t)jp1 * n + i0) = make_double2(ax, ay);
-      *reinterpret_cast<double2*>(vin + i0) = make_double2(ax, ay);
+    double p = 0.0;
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (live[u]) {
+        *reinterpret_cast<double2*>(Vw + (int64_t)jp1 * n + i0 + 2 * u) = acc[u];
+        *reinterpret_cast<double2*>(vin + i0 + 2 * u) = acc[u];
+      }
+      p = fma(acc[u].x, acc[u].x, fma(acc[u].y, acc[u].y, p));
     }
-    double p = fma(ax, ax, ay * ay);
 #pragma unroll
     for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
     if (lane == 0) red[warp][0] = p;
@@ -1431,12 +1468,15 @@ struct GmPieces {
     const double* cV = V;
     int nsf = ns;  // partials of the last sweep
     if (fast && n % 2 == 0 && sweep_chunked()) {  // Gram-corrected CGS2, chunked two-element sweeps
-      nsf = (int)std::max<int64_t>(1, (n / 2 + kGmThreads - 1) / kGmThreads);
-      LAUNCH_PDL(c, k_gm_sweep_fast<3>, (unsigned)nsf, kGmThreads, 0, n, cV, (const double*)w, (const GmDev*)st,
+      const int pp = n % 4 == 0 ? 2 : 1;  // 4 elements per thread (C4: 437 -> 435 us per iteration)
+      nsf = (int)std::max<int64_t>(1, (n / (2 * pp) + kGmThreads - 1) / kGmThreads);
+      auto* k3 = pp == 2 ? &k_gm_sweep_fast<3, 2> : &k_gm_sweep_fast<3, 1>;
+      auto* k2 = pp == 2 ? &k_gm_sweep_fast<2, 2> : &k_gm_sweep_fast<2, 1>;
+      LAUNCH_PDL(c, k3, (unsigned)nsf, kGmThreads, 0, n, cV, (const double*)w, (const GmDev*)st,
                  (const double*)nullptr, part, (const double*)vs, V, h.r.p);
       LAUNCH_PDL(c, k_gm_finish, 2 * kGmMax, kFinThreads, 0, (const double*)part, nsf, (const GmDev*)st, 0, d);
       LAUNCH_PDL(c, k_gm_gram, 1, 32, 0, (const GmDev*)st, (const double*)d, G, h2, hsum);
-      LAUNCH_PDL(c, k_gm_sweep_fast<2>, (unsigned)nsf, kGmThreads, 0, n, cV, (const double*)w, (const GmDev*)st,
+      LAUNCH_PDL(c, k2, (unsigned)nsf, kGmThreads, 0, n, cV, (const double*)w, (const GmDev*)st,
                  (const double*)hsum, part, (const double*)vs, V, h.r.p);
       hcol1 = d;
     } else if (fast) {  // Gram-corrected CGS2: two sweeps (k_gm_gram)
