@@ -3,9 +3,10 @@
   python tools/results_table.py gpu  > gpurun_out/results_gpu.json   (GPU box)
   python tools/results_table.py cpu  > profiles/results_cpu.json      (reference build, CPU)
 
-GPU: CF split ms (all levels, fused split), setup ms, solve DOF/s (Richardson;
-C0 and C4 with the outer GMRES(30) -- see tests/test_gpu_parity.py), its,
-level-0 SpMV % of HBM. CPU: the reference's own serial build (oracle/_ref):
+GPU: CF split ms (all levels back to back, fused split, one sync), setup ms
+(the fast mode's fused operators included), solve DOF/s in fast mode (the
+bench's) and exact mode (Richardson; C0 and C4 with the outer GMRES(30) --
+see tests/test_gpu_parity.py), its, level-0 SpMV % of HBM. CPU: the reference's own serial build (oracle/_ref):
 setup, CF split summed over its levels, one solve -- at full size where the
 serial setup fits in minutes, else on the stated bounded sample.
 """
@@ -32,7 +33,7 @@ def gpu():
     out = {}
     for cfg in range(5):
         p = problems.make(cfg)
-        prm = problems.setup_params(cfg)
+        prm = dict(problems.setup_params(cfg), fused_smooths=2)  # the fast mode's operators in the setup
         a = airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals)
         dA = airg.DeviceCSR.upload(a, ctx)
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -44,32 +45,36 @@ def gpu():
         e1.record(ctx.stream)
         e1.synchronize()
         setup_ms = e0.elapsed_time(e1)
-        cf = 0.0
-        for rep in range(2):
-            cf = 0.0
-            for l in range(h.n_levels):
-                Al = h.matrix_handle(l, 0)
-                s0, s1 = ev(), ev()
-                s0.record(ctx.stream)
-                airg.cf_split_device(Al, prm["strength_alpha"], prm["max_loops"],
-                                     int(problems.mix(np.uint64(0), np.uint64(l))), ctx=ctx)
-                s1.record(ctx.stream)
-                s1.synchronize()
-                cf += s0.elapsed_time(s1)
-        tb = ctx.to_device(p.b)
-        tx = ctx.empty(p.n, torch.float64)
-        sk = dict(coarse_iterations=prm["coarse_iterations"], outer=OUTER.get(cfg, 0), gmres_restart=30,
-                  max_iterations=1000)
-        h.solve_device(tb, tx, **sk)
-        ts = []
-        for _ in range(3):
+        # CF split of every level back to back, one synchronisation (the bench's cf_split_ms)
+        mats = [h.matrix_handle(l, 0) for l in range(h.n_levels)]
+        seeds = [int(problems.mix(np.uint64(0), np.uint64(l))) for l in range(h.n_levels)]
+        labs = [ctx.empty(max(m.dims()[0], 1), torch.uint8) for m in mats]
+        cfs = []
+        for rep in range(4):
             s0, s1 = ev(), ev()
             s0.record(ctx.stream)
-            st, _ = h.solve_device(tb, tx, **sk)
+            airg.cf_split_batch_device(mats, seeds, prm["strength_alpha"], prm["max_loops"], labels=labs, ctx=ctx)
             s1.record(ctx.stream)
             s1.synchronize()
-            ts.append(s0.elapsed_time(s1))
-        ms = float(np.median(ts))
+            cfs.append(s0.elapsed_time(s1))
+        cf = float(np.median(cfs[1:]))
+        tb = ctx.to_device(p.b)
+        tx = ctx.empty(p.n, torch.float64)
+        def solve_ms(fast):
+            sk = dict(coarse_iterations=prm["coarse_iterations"], outer=OUTER.get(cfg, 0), gmres_restart=30,
+                      max_iterations=1000, fast=fast)
+            h.solve_device(tb, tx, **sk)
+            ts = []
+            for _ in range(3):
+                s0, s1 = ev(), ev()
+                s0.record(ctx.stream)
+                st, _ = h.solve_device(tb, tx, **sk)
+                s1.record(ctx.stream)
+                s1.synchronize()
+                ts.append(s0.elapsed_time(s1))
+            return float(np.median(ts)), st
+        ms_exact, st_exact = solve_ms(0)
+        ms, st = solve_ms(1)
         A0 = h.matrix_handle(0, 0)
         n0, _, nnz0 = A0.dims()
         xv = torch.rand(n0, dtype=torch.float64, device=ctx.tdev)
@@ -86,6 +91,8 @@ def gpu():
         out[f"C{cfg}"] = dict(n=int(p.n), nnz=int(p.nnz), levels=int(h.n_levels), cf_split_ms=cf,
                               setup_ms=setup_ms, solve_ms=ms, dofs=p.n / (ms / 1e3),
                               iterations=int(st.iterations), converged=bool(st.converged),
+                              exact_solve_ms=ms_exact, exact_dofs=p.n / (ms_exact / 1e3),
+                              exact_iterations=int(st_exact.iterations),
                               outer="gmres(30)" if OUTER.get(cfg) else "richardson",
                               spmv_hbm_frac=spmv_gbs / peak)
         del h, dA
