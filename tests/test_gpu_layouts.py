@@ -215,6 +215,36 @@ def test_one_pass_vcycle_matches_two_pass(tmp_path):
     assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
 
 
+@pytest.mark.parametrize("dims", [(9, 9, 9), (7, 5, 3), (8, 8, 6)])
+def test_fast_gmres_sweep_shapes(dims):
+    """The fast GMRES sweeps take 4 elements per thread when n % 4 == 0, 2
+    when n % 4 == 2, and the register-tile kernels when n is odd: every shape
+    converges within the parity tolerance of the exact-mode GMRES."""
+    nx, ny, nz = dims
+    p = problems.c4_tets_3d(nx, ny, nz)
+    n_mod = p.n % 4  # 6 tets per cube: n is even; (7, 5, 3) gives n % 4 == 2
+    prm = dict(problems.setup_params(4), coarse_size_target=100)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    ex = airg.gmres_solve(h, p.b, coarse_iterations=3, max_iterations=300)
+    fa = airg.gmres_solve(h, p.b, coarse_iterations=3, max_iterations=300, fast=1)
+    assert ex.stats.converged and fa.stats.converged and fa.stats.final_relative_residual <= 1e-10
+    assert abs(fa.stats.iterations - ex.stats.iterations) <= 1, (n_mod, fa.stats.iterations, ex.stats.iterations)
+    assert np.linalg.norm(fa.x - ex.x) <= 1e-8 * np.linalg.norm(ex.x)
+
+
+def test_fast_gmres_odd_size():
+    """n odd: the fast GMRES falls back to the register-tile sweeps."""
+    p = problems.c0_structured_2d(97)
+    assert p.n % 2 == 1
+    prm = problems.setup_params(0)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    ex = airg.gmres_solve(h, p.b, coarse_iterations=prm["coarse_iterations"], max_iterations=300)
+    fa = airg.gmres_solve(h, p.b, coarse_iterations=prm["coarse_iterations"], max_iterations=300, fast=1)
+    assert ex.stats.converged and fa.stats.converged and fa.stats.final_relative_residual <= 1e-10
+    assert abs(fa.stats.iterations - ex.stats.iterations) <= 1
+    assert np.linalg.norm(fa.x - ex.x) <= 1e-8 * np.linalg.norm(ex.x)
+
+
 def test_fused_rebuild_invalidates_captured_graphs():
     """Switching the F-smooth count rebuilds the fused operators (new
     buffers): every cached graph that captured the old ones must be
