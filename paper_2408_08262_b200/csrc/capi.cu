@@ -558,9 +558,18 @@ int airg_cf_split_batch(airg_ctx* ctx, const airg_csr* const* mats, int64_t coun
     bind(ctx->c);
     Ctx& c = ctx->c;
     DBuf<unsigned long long> u(c, 8 * (size_t)count);
+    // every level's counters / histogram / counts / marks in one region,
+    // zeroed by one memset before the first split (no zeroing kernel on the
+    // chain of each level)
+    std::vector<size_t> off((size_t)count + 1, 0);
+    for (int64_t i = 0; i < count; ++i)
+      off[i + 1] = off[i] + cf_split_zero_bytes(mats[i]->m.n, ddc_enabled != 0, ddc_bins);
+    DBuf<uint8_t> zr(c, std::max<size_t>(off[count], 16));
+    CUDA_CHECK(cudaMemsetAsync(zr.p, 0, off[count], c.stream));
+    CUDA_CHECK(cudaMemsetAsync(u.p, 0, sizeof(unsigned long long) * 8 * count, c.stream));
     for (int64_t i = 0; i < count; ++i)
       cf_split_fused_enqueue(c, mats[i]->m, alpha, seeds[i], ddc_enabled != 0, ddc_fraction, ddc_bins, labels[i],
-                             nullptr, u.p + 8 * i);
+                             nullptr, u.p + 8 * i, zr.p + off[i]);
     std::vector<unsigned long long> hu(8 * (size_t)count);
     to_host(c, hu.data(), u.p, hu.size());
     for (int64_t i = 0; i < count; ++i) {

@@ -1203,10 +1203,16 @@ void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned lo
   LAUNCH(c, fcf_select, 1, kSelThreads, 0, d_nf, 0ll, d_hist, bins, fraction, d_maxbits, 0, 0.0, d_out);
 }
 
+size_t cf_split_zero_bytes(int64_t n, bool ddc_enabled, int64_t bins) {
+  const size_t nb = ddc_enabled ? (size_t)bins : 0;
+  const size_t zero_bytes = (8 + nb) * 8 + (size_t)n * 8 + (size_t)n;
+  return (zero_bytes + 15) & ~(size_t)15;
+}
+
 const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double alpha, uint64_t seed,
                                                  bool ddc_enabled, double fraction, int64_t bins,
                                                  uint8_t* d_labels, uint8_t* d_labels_pre,
-                                                 unsigned long long* d_u_out) {
+                                                 unsigned long long* d_u_out, void* d_zeroed) {
   if (a.n != a.m) throw InvalidArgument("strength: matrix must be square");
   if (ddc_enabled && (fraction <= 0.0 || fraction > 1.0))
     throw InvalidArgument("ddc: fraction must be in (0, 1]");
@@ -1223,20 +1229,23 @@ const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double al
   const size_t nb = ddc_enabled ? (size_t)bins : 0;
   const size_t zero_bytes = (8 + nb) * 8 + (size_t)n * 8 + (size_t)n;
   const size_t head = (zero_bytes + 15) & ~(size_t)15;
-  const size_t bytes = head + 2 * (size_t)n * 8;
-  uint8_t* base = static_cast<uint8_t*>(ctx_scratch(c, bytes));
+  const bool prezeroed = d_zeroed && d_u_out;
+  // the zeroed part in the caller's region, else at the front of the scratch
+  const size_t bytes = (prezeroed ? 0 : head) + 2 * (size_t)n * 8;
+  uint8_t* sbase = static_cast<uint8_t*>(ctx_scratch(c, bytes));
+  uint8_t* base = prezeroed ? static_cast<uint8_t*>(d_zeroed) : sbase;
   // the report counters: straight into d_u_out when given (no copy-out node)
   unsigned long long* u = d_u_out ? d_u_out : reinterpret_cast<unsigned long long*>(base);
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(base) + 8;
   int2* cnt = reinterpret_cast<int2*>(hist + nb);
   uint8_t* notmin = reinterpret_cast<uint8_t*>(cnt + n);
-  double* thr = reinterpret_cast<double*>(base + head);
+  double* thr = reinterpret_cast<double*>(sbase + (prezeroed ? 0 : head));
   double* theta = thr + n;
   // u: [0] |S| [1] n_f_pre [2] max theta bits [3] ~(first bad row), 0 = none
   //    [4] converted [5] alpha_diag bits [6] max_theta bits (written by fcf_select)
   const bool vec = a.nnz >= (int64_t)cf_vec_rows() * n;
   const uint64_t key = splitmix64_host(seed ^ splitmix64_host(0x57454947ull));
-  {
+  if (!prezeroed) {
     const int64_t words = (int64_t)((zero_bytes + 7) / 8);
     const unsigned gz = (unsigned)std::min<int64_t>(4 * c.num_sms, (words + 255) / 256 + 1);
     LAUNCH_PDL(c, fcf_zero, gz, 256, 0, reinterpret_cast<unsigned long long*>(base), words, d_u_out);

@@ -96,10 +96,15 @@ CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool d
 // used is returned, null for an empty matrix without d_u_out); the finish
 // step turns the host copy of the counters into the report and raises the
 // zero-diagonal error. Lets several splits share one synchronisation.
+// d_zeroed (optional, with d_u_out zeroed too): a region of
+// cf_split_zero_bytes() bytes the caller has zeroed -- the split's counters,
+// histogram, counts and marks live there and no zeroing kernel is launched
+// (a batch zeroes every level's region with one memset).
 const unsigned long long* cf_split_fused_enqueue(Ctx& c, const Csr& a, double alpha, uint64_t seed,
                                                  bool ddc_enabled, double fraction, int64_t bins,
                                                  uint8_t* d_labels, uint8_t* d_labels_pre,
-                                                 unsigned long long* d_u_out);
+                                                 unsigned long long* d_u_out, void* d_zeroed = nullptr);
+size_t cf_split_zero_bytes(int64_t n, bool ddc_enabled, int64_t bins);
 CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_enabled, const uint8_t* d_labels);
 // coarsening.cpp:290-315 on device counters: d_out = {alpha_diag, max_theta}
 void launch_ddc_select(Ctx& c, const unsigned long long* d_nf, const unsigned long long* d_hist, int64_t bins,

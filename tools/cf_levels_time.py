@@ -9,8 +9,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2408_08262_b200 import airg, problems  # noqa: E402
 
-p = problems.make(2)
-prm = problems.setup_params(2)
+CFG = int(os.environ.get("CF_CONFIG", "2"))
+p = problems.make(CFG)
+prm = problems.setup_params(CFG)
 ctx = airg.default_context()
 h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), ctx=ctx, **prm)
 stream = ctx.stream
