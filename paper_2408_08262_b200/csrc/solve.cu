@@ -1376,6 +1376,18 @@ bool sweep_chunked() {
   return v;
 }
 
+// The GMRES orthogonalisation: the Gram-corrected two-sweep CGS2 over the
+// unnormalised basis in BOTH arithmetic modes (GMRES is not part of the
+// reference; exact mode's V-cycle and A z keep the reference's bits), or
+// with AIRG_GM_EXACT_CGS=1 and exact mode the oracle's three-sweep CGS2.
+bool gm_fast_orth(const airg_solve_config& cfg) {
+  static const bool three = [] {
+    const char* e = getenv("AIRG_GM_EXACT_CGS");
+    return e && e[0] == '1';
+  }();
+  return cfg.fast != 0 || !three;
+}
+
 int gm_blocks(int64_t n) { return (int)std::max<int64_t>(1, (n + kGmThreads - 1) / kGmThreads); }
 int gm_sweep_blocks(const Ctx&, int64_t n) { return gm_blocks(n); }
 
@@ -1438,7 +1450,7 @@ struct GmPieces {
         w(h_.w.p), H(h_.gm_H.p), cs(h_.gm_cs.p), sn(h_.gm_sn.p), g(h_.gm_g.p), y(h_.gm_y.p), h1(h_.gm_h.p),
         h2(h_.gm_h.p + (kGmMax + 1)), nrm(h_.gm_h.p + 2 * (kGmMax + 1)), part(h_.gm_part.p),
         d(h_.gm_h.p + 3 * (kGmMax + 1)), hsum(h_.gm_h.p + 5 * (kGmMax + 1)), G(h_.gm_G.p),
-        vs(cfg_.fast ? h_.gm_h.p + 6 * (kGmMax + 1) : nullptr) {}
+        vs(gm_fast_orth(cfg_) ? h_.gm_h.p + 6 * (kGmMax + 1) : nullptr) {}
   void norm_b() { dot_async(c, h.rhs.p, h.rhs.p, n, h.scal.p + 1, h.part.p); }
   void init(cudaGraphConditionalHandle hout, int cond) {
     LAUNCH(c, k_gm_init, 1, 32, 0, hout, cond, (const double*)(h.scal.p + 1), st, h.gm_hist.p);
@@ -1460,14 +1472,15 @@ struct GmPieces {
   // registers and the A z epilogue scales z and A z by vs[j] (M is linear),
   // so no pass forms v = w / |w| (16 MB read + 32 MB written per step).
   void step(cudaGraphConditionalHandle hin, int cond) {
-    const bool fast = cfg.fast != 0;
+    const bool fast = cfg.fast != 0;    // arithmetic of the row kernels (V-cycle, A z)
+    const bool fgm = gm_fast_orth(cfg);  // Gram-corrected CGS2 over the unnormalised basis
     enqueue_vcycle(c, h, cfg, h.r.p);
     const double* z = vcycle_output(h);
     ROWS(EpiGmSpmv, h.top(), z, (EpiGmSpmv{w, z, Z, st, n, vs}));
     const double* hcol1 = h1;
     const double* cV = V;
     int nsf = ns;  // partials of the last sweep
-    if (fast && n % 2 == 0 && sweep_chunked()) {  // Gram-corrected CGS2, chunked two-element sweeps
+    if (fgm && n % 2 == 0 && sweep_chunked()) {  // Gram-corrected CGS2, chunked two-element sweeps
       const int pp = n % 4 == 0 ? 2 : 1;  // 4 elements per thread (C4: 437 -> 435 us per iteration)
       nsf = (int)std::max<int64_t>(1, (n / (2 * pp) + kGmThreads - 1) / kGmThreads);
       auto* k3 = pp == 2 ? &k_gm_sweep_fast<3, 2> : &k_gm_sweep_fast<3, 1>;
@@ -1479,7 +1492,7 @@ struct GmPieces {
       LAUNCH_PDL(c, k2, (unsigned)nsf, kGmThreads, 0, n, cV, (const double*)w, (const GmDev*)st,
                  (const double*)hsum, part, (const double*)vs, V, h.r.p);
       hcol1 = d;
-    } else if (fast) {  // Gram-corrected CGS2: two sweeps (k_gm_gram)
+    } else if (fgm) {  // Gram-corrected CGS2: two sweeps (k_gm_gram)
       LAUNCH_PDL(c, (k_gm_sweep<3, true>), (unsigned)ns, kGmThreads, 0, n, cV, w, (const GmDev*)st,
                  (const double*)nullptr, part, (const double*)vs, V, h.r.p, sweep_l2());
       LAUNCH_PDL(c, k_gm_finish, 2 * kGmMax, kFinThreads, 0, (const double*)part, ns, (const GmDev*)st, 0, d);
@@ -1500,7 +1513,7 @@ struct GmPieces {
     LAUNCH_PDL(c, k_gm_finish, 1, kFinThreads, 0, (const double*)part, nsf, (const GmDev*)st, 1, nrm);
     LAUNCH_PDL(c, k_gm_step, 1, 32, 0, hin, cond, st, hcol1, (const double*)h2, (const double*)nrm, H,
                cs, sn, g, h.gm_hist.p, vs);
-    if (!fast)
+    if (!fgm)
       LAUNCH_PDL(c, k_gm_next, (unsigned)nb, kGmThreads, 0, n, (const double*)w, (const GmDev*)st, V, h.r.p);
   }
 };
