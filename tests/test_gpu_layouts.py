@@ -245,6 +245,38 @@ def test_fast_gmres_odd_size():
     assert np.linalg.norm(fa.x - ex.x) <= 1e-8 * np.linalg.norm(ex.x)
 
 
+COARSE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+p = problems.make(4, 0.25)
+prm = dict(problems.setup_params(4), coarse_size_target=300)
+h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+out = [h.vcycle(p.b, coarse_iterations=k, fast=1, up_f_smooths=2) for k in (1, 2, 3, 4)]
+out.append(h.vcycle(p.b, coarse_iterations=3, fast=1, up_f_smooths=2))  # back to 3: rebuilt, same bits
+np.save(sys.argv[1], np.stack(out + [np.full_like(out[0], float(h.fused_plan()["coarse_composed"]))]))
+"""
+
+
+def test_composed_coarse_solve_any_iteration_count(tmp_path):
+    """The composed coarse solve E_k (k = 1..4, rebuilt when the solve's
+    coarse_iterations changes) equals the k-step coarse Richardson of the
+    uncomposed fast V-cycle up to rounding; returning to k = 3 re-captures
+    the graphs and reproduces its bits."""
+    script = tmp_path / "cs.py"
+    script.write_text(COARSE_SCRIPT % REPO)
+    outs = {}
+    for name, env in (("composed", {}), ("plain", {"AIRG_COARSE_COMPOSE": "0"})):
+        f = tmp_path / f"{name}.npy"
+        subprocess.run([sys.executable, str(script), str(f)], check=True, env={**os.environ, **env})
+        outs[name] = np.load(f)
+    a, b = outs["composed"], outs["plain"]
+    assert a[-1][0] == 1.0 and b[-1][0] == 0.0
+    for k in range(4):
+        np.testing.assert_allclose(a[k], b[k], rtol=0, atol=1e-11 * abs(b[k]).max())
+    assert np.array_equal(a[2].view(np.uint64), a[4].view(np.uint64))
+
+
 def test_fused_rebuild_invalidates_captured_graphs():
     """Switching the F-smooth count rebuilds the fused operators (new
     buffers): every cached graph that captured the old ones must be
