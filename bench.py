@@ -116,10 +116,61 @@ class OwnedView:
     def level(self, l):
         return self.d.report(l)
 
+    def fused_nnz(self, l):
+        return self.d.fused_nnz(l)
+
     def info(self):
         from types import SimpleNamespace
         c = self.d.report(self.d.n_levels)
         return SimpleNamespace(n_levels=self.d.n_levels, coarse_n=c.n, coarse_nnz=c.nnz, coarse_inv_nnz=c.nnz_ffinv)
+
+
+def dist_vcycle_alg_bytes(v, coarse_iterations, up_smooths=2, fast=False):
+    """Algorithmic bytes of one distributed V-cycle (dist.cu enqueue_vcycle,
+    summed over the ranks): exact -- the exact V-cycle's; fast -- per level
+    R b, x = P e_c over every row, r1 = b_F - (A_F P) e_c, x_F += W r1 (no
+    one-pass level, the coarse Richardson uncomposed)."""
+    if not fast:
+        return vcycle_alg_bytes(v, coarse_iterations, up_smooths, False)
+    info = v.info()
+    per_cycle = 0
+    for l in range(info.n_levels):
+        lv = v.level(l)
+        n, nf, nc = lv.n, lv.n_f, lv.n_c
+        afp, wx = v.fused_nnz(l)
+        per_cycle += 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc           # R b
+        per_cycle += n * (4 + 8) + 8 * nc                                     # x = P e_c
+        per_cycle += 12 * afp + 4 * (nf + 1) + 8 * nc + nf * (4 + 8 + 8)      # r1
+        per_cycle += 12 * wx + 4 * (nf + 1) + 8 * nf + nf * (4 + 8 + 8)       # x_F += W r1
+    cn = info.coarse_n
+    for it in range(coarse_iterations):
+        per_cycle += 12 * info.coarse_inv_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+        if it:
+            per_cycle += 12 * info.coarse_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
+    return per_cycle
+
+
+def dist_gmres_alg_bytes(v, iterations, coarse_iterations, restart=30, up_smooths=2, fast=False):
+    """Algorithmic bytes of one distributed GMRES(m) solve (dist.cu
+    dist_gmres, summed over the ranks). Per Arnoldi step: the V-cycle, Z_j =
+    z (copy), w = A z, two CGS passes (dots: V_0..V_j and w read; update: V
+    and w read, w written), |w|, v_{j+1} = w / |w| into V and the V-cycle
+    input. Per restart: x += Z y, r = b - A x and its norm."""
+    info = v.info()
+    top = v.level(0) if info.n_levels else None
+    n = top.n if top else info.coarse_n
+    nnz = top.nnz if top else info.coarse_nnz
+    cyc = dist_vcycle_alg_bytes(v, coarse_iterations, up_smooths, fast)
+    spmv = spmv_bytes(n, n, nnz)
+    tot = 8 * n
+    left = iterations
+    while left > 0:
+        j_max = min(restart, left)
+        for j in range(j_max):
+            tot += cyc + 16 * n + spmv + 4 * (j + 1) * 8 * n + (2 + 4 + 1 + 3) * 8 * n
+        tot += (j_max + 2) * 8 * n + spmv + 8 * n
+        left -= j_max
+    return tot
 
 
 def gmres_alg_bytes(h, iterations, coarse_iterations, restart=30, up_smooths=2, fast=False):
@@ -421,7 +472,9 @@ def run_gpu_dist(args):
     N = slab * ws
     a_loc = airg.SparseMatrix.from_arrays(slab, N, ps.row_offsets, ps.cols, ps.vals)
     dA = airg.DeviceCSR.upload(a_loc, ctx)
-    prm = problems.setup_params(4)
+    fast = args.mode == "fast"
+    # fast mode: the fused level operators (A_F P, W_2) built on the slabs inside the timed setup
+    prm = dict(problems.setup_params(4), fused_smooths=2 if fast else -1)
     uid = [airg.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = airg.NcclComm(ws, rank, uid[0])
@@ -446,7 +499,7 @@ def run_gpu_dist(args):
         tb = torch.from_numpy(ps.b.copy()).to(ctx.tdev)
         tx = torch.empty(hi - lo, dtype=torch.float64, device=ctx.tdev)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=ctx.tdev)
-    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, **solver_kw(4))
+    sk = dict(coarse_iterations=prm["coarse_iterations"], max_iterations=400, fast=int(fast), **solver_kw(4))
     for _ in range(args.warmup):
         st, _ = d.solve_device(tb, tx, **sk)
     torch.cuda.synchronize()
@@ -492,7 +545,7 @@ def run_gpu_dist(args):
     levels = [d.level_info(l) for l in range(d.n_levels + 1)]
     # roofline of the whole distributed solve step against the N GPUs' HBM
     peak, peak_kind = hbm_peak()
-    step_bytes = gmres_alg_bytes(hv_, int(st.iterations), prm["coarse_iterations"])
+    step_bytes = dist_gmres_alg_bytes(hv_, int(st.iterations), prm["coarse_iterations"], fast=fast)
     step_ach = step_bytes / (tot_ms / args.steps / 1e3) / 1e9
     # NVLink: halo bytes every process receives (exact, from the halo plans)
     # per V-cycle / level-0 SpMV, plus the allreduce payloads of the GMRES
@@ -521,7 +574,7 @@ def run_gpu_dist(args):
         "config": {"workload": f"C4 3D unstructured tets, {nxy} x {nxy} x {nzl * ws} cubes x 6 "
                                f"(one {nzl}-layer z-slab = {ps.n} tets per GPU)",
                    "unknowns": int(N), "nnz": int(d.report(0).nnz), "alpha": 0.5, "ddc_fraction": 0.1,
-                   "poly_order": 4, "solver": solver_name(4) + " to rtol 1e-10 from x = 0", "mode": "exact",
+                   "poly_order": 4, "solver": solver_name(4) + " to rtol 1e-10 from x = 0", "mode": args.mode,
                    "parallelism": f"row slabs x{ws} (NCCL halos and allreduces, replay halving, "
                    "gathered coarse grid; owned-row setup: every rank builds only its rows)",
                    "l2": "flushed (512 MiB write) before each timed step"},

@@ -414,6 +414,10 @@ int airg_dist_setup_owned(airg_ctx* ctx, const airg_csr* a, const int64_t* h_sta
  * nnz_ffinv = |Ac^-1|, coefficients, effective_order, poly_attempts,
  * smoother_growth of the coarse polynomial). info may be null (n_levels only). */
 int airg_dist_report(const airg_dist* d, int64_t level, airg_level_info* info, int64_t* n_levels);
+/* Global entries of the fast V-cycle's A_F P and W_k slabs of level `level`
+ * (distributions built with fused operators: owned setup with fused_smooths
+ * in 0..2, or dist_create of a hierarchy whose fused operators exist). */
+int airg_dist_fused_nnz(const airg_dist* d, int64_t level, int64_t* nnz_afp, int64_t* nnz_w);
 /* This process's wall time of the owned setup and the device time of its
  * CF splits (all levels), in ms (0 for airg_dist_create distributions). */
 int airg_dist_setup_times(const airg_dist* d, double* setup_ms, double* cf_split_ms);

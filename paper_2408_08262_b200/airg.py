@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "airg_dist_setup_owned": ([_VP, _VP, _VP, _P(abi.SetupConfig), _P(abi.Injection), C.c_int32, C.c_int32,
                                        _VP, C.c_double, _P(_VP)], C.c_int),
             "airg_dist_report": ([_VP, C.c_int64, _P(abi.LevelInfo), _P(C.c_int64)], C.c_int),
+            "airg_dist_fused_nnz": ([_VP, C.c_int64, _P(C.c_int64), _P(C.c_int64)], C.c_int),
             "airg_dist_setup_times": ([_VP, _P(C.c_double), _P(C.c_double)], C.c_int),
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
@@ -976,6 +977,12 @@ class Dist:
         """Drop this distribution's reference to the global hierarchy: only
         the per-rank slabs stay resident (call h.close() to free it now)."""
         self.h = None
+
+    def fused_nnz(self, l: int) -> tuple[int, int]:
+        """Global entries of the fast V-cycle's (A_F P, W_k) slabs of level l."""
+        a, w = C.c_int64(), C.c_int64()
+        _check(lib().airg_dist_fused_nnz(self.d, int(l), C.byref(a), C.byref(w)))
+        return a.value, w.value
 
     def rank_bytes(self, rank: int | None = None) -> int:
         """Device bytes of one rank's slabs (airg_dist_rank_bytes)."""

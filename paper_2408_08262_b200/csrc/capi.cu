@@ -1075,6 +1075,19 @@ int airg_dist_setup_owned(airg_ctx* ctx, const airg_csr* a, const int64_t* start
   });
 }
 
+int airg_dist_fused_nnz(const airg_dist* dp, int64_t level, int64_t* nnz_afp, int64_t* nnz_w) {
+  return guard([&] {
+    need(dp, "dist");
+    need(nnz_afp, "output");
+    need(nnz_w, "output");
+    const DHier& d = dp->d;
+    if (level < 0 || level >= (int64_t)d.lv.size()) throw InvalidArgument("level out of range");
+    if (d.fused_smooths < 0) throw InvalidArgument("dist: no fast V-cycle operators (setup fused_smooths >= 0)");
+    *nnz_afp = d.lv[(size_t)level].nnz_afp;
+    *nnz_w = d.lv[(size_t)level].nnz_w;
+  });
+}
+
 int airg_dist_report(const airg_dist* dp, int64_t level, airg_level_info* info, int64_t* n_levels) {
   return guard([&] {
     need(dp, "dist");

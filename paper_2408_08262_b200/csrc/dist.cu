@@ -303,10 +303,24 @@ struct LResid {
   }
 };
 
-// exact thread-per-row kernels in the batch kind of the matrix (tiled.cuh)
+// fast V-cycle: r1 = b_F - (A_F P) e_c (solve.cu EpiFres1P)
+struct LFres1P {
+  const double* b;
+  const int32_t* f2f;
+  double* rf;
+  __device__ void finish() const {}
+  struct Pre {
+    double bb;
+  };
+  __device__ Pre pre(int k) const { return Pre{b[f2f[k]]}; }
+  __device__ void row_pre(int k, double acc, const Pre& p) const { rf[k] = p.bb - acc; }
+};
+
+// exact thread-per-row kernels in the batch kind of the matrix (tiled.cuh);
+// fast: lane groups, FMA, tree sums
 template <class Epi>
-void launch_rows(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
-  LAUNCH_ROWS(c, Epi, tview(m), x, epi);
+void launch_rows(Ctx& c, const Csr& m, const double* x, const Epi& epi, bool fast = false) {
+  LAUNCH_ROWS_MODE(c, Epi, tview(m), x, epi, fast);
 }
 template <class Epi>
 void launch_rows_fc(Ctx& c, const Csr& m, const double* x, const Epi& epi) {
@@ -1039,6 +1053,12 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
     to_host(c, pc.fpart[l].s.data(), cnt.p, (size_t)P + 1);
   }
   const Part cpart = gathered(h.coarse_a.n, P);
+  pc.fused_smooths = h.fused_smooths;
+  if (h.fused_smooths >= 0)
+    for (int l = 0; l < L; ++l) {
+      d.lv[l].nnz_afp = h.levels[l].afp.nnz;
+      d.lv[l].nnz_w = h.levels[l].fw.nnz;
+    }
   pc.AC.resize(P);
   pc.ACI.resize(P);
   pc.A0.resize(P);
@@ -1055,6 +1075,10 @@ void dist_create(Ctx& c, Hier& h, int P, int me, ncclComm_t comm, double thresho
       slice(c, Lv.af, flo, fhi, R.AF);
       slice(c, Lv.affg, flo, fhi, R.AFFG);
       slice(c, Lv.ffinv, flo, fhi, R.FINV);
+      if (h.fused_smooths >= 0) {  // the fast V-cycle's fused operators, by F rows
+        slice(c, Lv.afp, flo, fhi, R.AFP);
+        slice(c, Lv.fw, flo, fhi, R.W);
+      }
       R.pmap.alloc(c, (size_t)std::max<int64_t>(1, hi - lo));
       if (hi > lo)
         CUDA_CHECK(cudaMemcpyAsync(R.pmap.p, Lv.pmap.p + lo, sizeof(int32_t) * (hi - lo),
@@ -1121,6 +1145,10 @@ void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
       R.AF = std::move(S.AF);
       R.AFFG = std::move(S.AFFG);
       R.FINV = std::move(S.FINV);
+      if (pc.fused_smooths >= 0) {
+        R.AFP = std::move(S.AFP);
+        R.W = std::move(S.W);
+      }
       R.nf_own = fhi - flo;
       R.n_own = hi - lo;
       R.pmap = std::move(S.pmap);
@@ -1138,10 +1166,12 @@ void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
       if (l > 0) {
         const DLevel::Rank& U = d.lv[l - 1].rk[r];
         mx.vals(c, U.pmap.p, U.n_own, lo, hi);
+        if (pc.fused_smooths >= 0 && U.AFP.n) mx.cols(c, U.AFP, lo, hi);  // the coarser level's A_F P reads X_l
       }
       set_halo(c, D.X, r, mx);
       mf.init(c, D.RF.N);
       mf.cols(c, R.FINV, flo, fhi);
+      if (pc.fused_smooths >= 0 && R.W.n) mf.cols(c, R.W, flo, fhi);
       set_halo(c, D.RF, r, mf);
     }
   }
@@ -1158,6 +1188,7 @@ void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
     if (L) {
       const DLevel::Rank& U = d.lv[L - 1].rk[r];
       mc.vals(c, U.pmap.p, U.n_own, lo, hi);
+      if (pc.fused_smooths >= 0 && U.AFP.n) mc.cols(c, U.AFP, lo, hi);
     }
     set_halo(c, d.CX, r, mc);
     mb.init(c, d.CB.N);
@@ -1211,6 +1242,10 @@ void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
       remap(c, R.AF, D.X, r);
       remap(c, R.AFFG, D.X, r);
       remap(c, R.FINV, D.RF, r);
+      if (pc.fused_smooths >= 0) {
+        remap(c, R.AFP, Xn, r);
+        remap(c, R.W, D.RF, r);
+      }
       const DVec::Rank& XR = Xn.rk[r];
       if (R.n_own)
         LAUNCH(c, k_remap_vals, blocks_for(R.n_own, 256), 256, 0, R.n_own, R.pmap.p, R.pmap.p, XR.lo,
@@ -1233,14 +1268,24 @@ void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
   }
   d.part.alloc(c, (size_t)d.nparts + 8);
   d.scal.alloc(c, 8);
+  d.fused_smooths = pc.fused_smooths;
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 namespace {
 
+bool dist_fast(const DHier& d, const airg_solve_config& cfg) {
+  return cfg.fast != 0 && d.fused_smooths >= 0 && d.fused_smooths == cfg.up_f_smooths;
+}
+
 void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
   const int L = (int)d.lv.size();
   const int P = d.P;
+  // fast mode (the single-GPU fast V-cycle's fused level operators on the
+  // slabs, lane-group row kernels): per level R b on the way down; on the way
+  // up x = P e_c, r1 = b_F - (A_F P) e_c, x_F += W_k r1 -- three passes
+  // instead of 1 + 2 k, same halos plus A_F P's coarse and W's F columns
+  const bool fast = dist_fast(d, cfg);
   auto rank_loop = [&](auto&& f) {
     for (int r = 0; r < P; ++r)
       if (d.mine(r)) f(r);
@@ -1253,7 +1298,7 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
     rank_loop([&](int r) {
       const Csr& R = D.rk[r].R;
       if (R.n)
-        launch_rows(c, R, (const double*)D.B.rk[r].buf.p, LStore{Bn.rk[r].buf.p});
+        launch_rows(c, R, (const double*)D.B.rk[r].buf.p, LStore{Bn.rk[r].buf.p}, fast);
     });
     release(c, d, D.B);
   }
@@ -1285,7 +1330,29 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
     release(c, d, d.CR);
   }
   // ascent
-  for (int l = L - 1; l >= 0; --l) {
+  for (int l = L - 1; fast && l >= 0; --l) {
+    DLevel& D = d.lv[l];
+    DVec& Xn = l + 1 < L ? d.lv[l + 1].X : d.CX;
+    exchange(c, d, Xn);
+    rank_loop([&](int r) {
+      const DLevel::Rank& R = D.rk[r];
+      if (R.n_own)
+        LAUNCH_PDL(c, k_prolong4_l, blocks_for(R.n_own / 4 + 1, 256), 256, 0, (int)R.n_own, R.pmap.p,
+                   Xn.rk[r].buf.p, D.X.rk[r].buf.p);
+      if (R.nf_own && cfg.up_f_smooths > 0)
+        launch_rows(c, R.AFP, (const double*)Xn.rk[r].buf.p, LFres1P{D.B.rk[r].buf.p, R.f2f.p, D.RF.rk[r].buf.p},
+                    true);
+    });
+    release(c, d, Xn);
+    if (cfg.up_f_smooths <= 0) continue;
+    exchange(c, d, D.RF);
+    rank_loop([&](int r) {
+      DLevel::Rank& R = D.rk[r];
+      if (R.nf_own) launch_rows(c, R.W, (const double*)D.RF.rk[r].buf.p, LFupd{R.f2f.p, D.X.rk[r].buf.p}, true);
+    });
+    release(c, d, D.RF);
+  }
+  for (int l = L - 1; !fast && l >= 0; --l) {
     DLevel& D = d.lv[l];
     DVec& Xn = l + 1 < L ? d.lv[l + 1].X : d.CX;
     exchange(c, d, Xn);
@@ -1470,7 +1537,7 @@ void dist_gmres(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_
     }
     d.gm_m = m;
   }
-  const int64_t key = cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31;
+  const int64_t key = (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31) * 2 + (dist_fast(d, cfg) ? 1 : 0);
   if (!d.graph_vc || d.graph_vc_key != key) {
     d.graph_vc_kernels = capture_graph(c, &d.graph_vc, [&] {
       enqueue_vcycle(c, d, cfg);
@@ -1657,12 +1724,16 @@ void dist_halo_bytes(const DHier& d, const airg_solve_config& cfg, int64_t& vcyc
     return s;
   };
   const int L = (int)d.lv.size();
+  const bool fast = dist_fast(d, cfg);
   int64_t e = 0;
   for (int l = 0; l < L; ++l) {
     const DLevel& D = d.lv[l];
     e += halo(D.B);                                        // restriction input
-    e += halo(l + 1 < L ? d.lv[l + 1].X : d.CX);           // prolongation input
-    e += cfg.up_f_smooths * (halo(D.X) + halo(D.RF));      // residual and update inputs
+    e += halo(l + 1 < L ? d.lv[l + 1].X : d.CX);           // prolongation (fast: and A_F P) input
+    if (fast)
+      e += cfg.up_f_smooths > 0 ? halo(D.RF) : 0;          // W_k's input
+    else
+      e += cfg.up_f_smooths * (halo(D.X) + halo(D.RF));    // residual and update inputs
   }
   e += cfg.coarse_iterations * halo(d.CR) + std::max<int64_t>(0, cfg.coarse_iterations - 1) * halo(d.CX);
   vcycle = 8 * e;
@@ -1710,7 +1781,7 @@ void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_
     st.converged = 1;
     hist.push_back(0.0);
   } else {
-    const int64_t key = cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31;
+    const int64_t key = (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31) * 2 + (dist_fast(d, cfg) ? 1 : 0);
     if (!d.graph || d.graph_key != key) {
       d.graph_kernels = capture_graph(c, &d.graph, [&] {
         enqueue_vcycle(c, d, cfg);

@@ -104,8 +104,10 @@ struct DLevel {
   double share_before = 1.0, share_after = 1.0;  // local_share (partition_model.cpp:66-75)
   bool triggered = false;
   DVec B, X, RF;  // b_l (input of R_l), x_l (input of AF/AFFg and of P_{l-1}), r_F
+  int64_t nnz_afp = 0, nnz_w = 0;  // fast V-cycle: global entries of A_F P and W_k
   struct Rank {
     Csr R, AF, AFFG, FINV;    // local rows, remapped columns
+    Csr AFP, W;               // fast V-cycle: A_F P (-> X_{l+1} layout), W_k (-> RF layout); F rows
     DBuf<int32_t> pmap, f2f;  // prolongation map (-> X_{l+1} layout), F row -> local fine row
     DBuf<double> sc;
     int64_t nf_own = 0, n_own = 0;
@@ -119,6 +121,7 @@ struct DHier {
   ncclComm_t comm = nullptr;
   double threshold = 2.0;
   std::vector<DLevel> lv;
+  int64_t fused_smooths = -1;  // up_f_smooths of the fast V-cycle's A_F P / W_k slabs (-1: none)
   Part cpart;            // coarsest rows (gathered on rank 0)
   DVec CB, CX, CR, XS;   // coarse b / e / r and the top solution vector
   struct Rank {
@@ -229,6 +232,7 @@ struct DistPieces {
   struct LevelRank {
     Csr R;                    // rows of level l+1 owned here (coarse_part), fine columns
     Csr AF, AFFG, FINV;       // F rows owned here (fpart): A_F (bit 31 = C column), A_FF (fine columns), Aff^-1
+    Csr AFP, W;               // fast V-cycle (optional): A_F P (global coarse columns), W_k (global F columns)
     DBuf<int32_t> pmap;       // own fine rows -> global coarse index (-1: empty row)
     DBuf<int32_t> f2f;        // own F rows -> global fine row
   };
@@ -237,6 +241,7 @@ struct DistPieces {
   std::vector<int64_t> n, nf;              // global rows / F points per level
   std::vector<Csr> AC, ACI, A0;            // per rank: coarse rows (cpart), top rows (level-0 partition)
   int64_t coarse_n = 0;
+  int64_t fused_smooths = -1;              // AFP / W present, built for this many F-smooths
   bool all_ranks = false;                  // pieces of every rank present (halo lists of peers known)
 };
 // The solve structures of d from pieces; d.P / me / comm / threshold and

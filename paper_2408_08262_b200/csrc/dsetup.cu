@@ -455,6 +455,36 @@ void fetch_rows(Ctx& c, const DHier& d, const Part& part, std::vector<Csr>& M, i
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
+// Rows want[0..nw) (global indices inside [lo, lo + m.n)) of m, in that
+// order, columns unchanged.
+void select_rows(Ctx& c, const Csr& m, int64_t lo, const int32_t* want, int64_t nw, Csr& out) {
+  out = Csr();
+  out.n = (int32_t)nw;
+  out.m = m.m;
+  out.rp.alloc(c, (size_t)nw + 1);
+  const int64_t s[2] = {lo, lo + m.n};
+  DBuf<int64_t> ms(c, 2);
+  to_device(c, ms.p, s, 2);
+  const int32_t* hrp = m.rp.p;
+  const int32_t* hci = m.ci.p;
+  const double* hv = m.v.p;
+  DBuf<const int32_t*> rps(c, 1), cis(c, 1);
+  DBuf<const double*> vs(c, 1);
+  to_device(c, rps.p, &hrp, 1);
+  to_device(c, cis.p, &hci, 1);
+  to_device(c, vs.p, &hv, 1);
+  DBuf<int32_t> len(c, (size_t)std::max<int64_t>(1, nw));
+  if (nw) LAUNCH(c, k_fetch_len, blocks_for(nw, 256), 256, 0, nw, want, ms.p, 1, rps.p, len.p);
+  out.nnz = nw ? exclusive_scan(c, len.p, out.rp.p, nw) : 0;
+  if (!nw) out.rp.zero(c);
+  out.ci.alloc(c, (size_t)out.nnz);
+  out.v.alloc(c, (size_t)out.nnz);
+  if (nw)
+    LAUNCH(c, k_fetch_fill, blocks_for(nw, 128), 128, 0, nw, want, ms.p, 1, rps.p, cis.p, vs.p, out.rp.p, out.ci.p,
+           out.v.p);
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
 // Move the rows of M (partition from) to the partition to.
 void migrate(Ctx& c, const DHier& d, const Part& from, const Part& to, std::vector<Csr>& M, int64_t ncols) {
   if (from.s == to.s) return;
@@ -1219,6 +1249,76 @@ void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_
       CUDA_CHECK(cudaStreamSynchronize(c.stream));
     });
 
+    // ---- the fast V-cycle's fused operators on the own F rows (fused.cu,
+    // same products in the same order as one GPU, so the same bits):
+    // A_F P = the F rows of A P; W_2 = (Q + Q) - (Q A_ff) Q with Q A_ff from
+    // A_ff's F-halo rows and (Q A_ff) Q from the distance-2 rows of Q
+    std::vector<Csr> afp(P), wk(P);
+    const int64_t fsm = cfg.fused_smooths;
+    const bool fused = fsm >= 0 && fsm <= 2;
+    if (fused) {
+      each(d, [&](int r) {
+        const int64_t nfo = nfr[r];
+        select_rows(c, ap[r], held.lo(r), bk[r].f2f.p, nfo, afp[r]);
+        afp[r].m = (int32_t)nc;
+      });
+      std::vector<Csr> u(P);
+      if (fsm == 2) {
+        each(d, [&](int r) {
+          Csr qv, bext;
+          csr_copy(c, inv.q[r], qv);
+          to_layout(c, qv, VF, r, 0);
+          concat_rows(c, {&bk[r].aff, &aff_halo[r]}, {{0, VF.rk[r].own}, {0, VF.rk[r].nhalo}}, nf, bext);
+          spgemm(c, qv, bext, u[r]);  // Q A_ff, global F columns
+          CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        });
+      }
+      DVec VW;  // F-space halo of Q A_ff's columns (distance 2)
+      VW.part = fpart;
+      VW.N = nf;
+      VW.rk.resize(P);
+      std::vector<Csr> q2;
+      if (fsm == 2) {
+        each(d, [&](int r) {
+          plan_rank(c, VW, r, {&u[r]});
+          nw[r] = VW.rk[r].nhalo;
+          want[r].view(VW.rk[r].halo.p, (size_t)std::max<int64_t>(1, nw[r]));
+        });
+        fetch_rows(c, d, fpart, inv.q, nf, want, nw, q2);
+      }
+      each(d, [&](int r) {
+        if (fsm == 0) {  // no F-smooth: an empty W
+          wk[r] = Csr();
+          wk[r].n = (int32_t)nfr[r];
+          wk[r].m = (int32_t)nf;
+          wk[r].rp.alloc(c, (size_t)nfr[r] + 1);
+          wk[r].rp.zero(c);
+          return;
+        }
+        Csr w1;
+        csr_add(c, 1.0, inv.q[r], 0.0, inv.q[r], w1);  // W_1 = Q
+        if (fsm == 1) {
+          wk[r] = std::move(w1);
+          return;
+        }
+        Csr bext, uv, waq, qw;
+        concat_rows(c, {&inv.q[r], &q2[r]}, {{0, VW.rk[r].own}, {0, VW.rk[r].nhalo}}, nf, bext);
+        csr_copy(c, u[r], uv);
+        to_layout(c, uv, VW, r, 0);
+        spgemm(c, uv, bext, waq);
+        csr_add(c, 1.0, inv.q[r], 1.0, w1, qw);
+        csr_add(c, 1.0, qw, -1.0, waq, wk[r]);
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      });
+      std::vector<int64_t> a(P, 0), b(P, 0);
+      each(d, [&](int r) {
+        a[r] = afp[r].nnz;
+        b[r] = wk[r].nnz;
+      });
+      D.nnz_afp = sum_over_ranks(c, d, a);
+      D.nnz_w = sum_over_ranks(c, d, b);
+    }
+
     // ---- R (A P) from the A P halo rows (distance 2), full diagonal
     DVec VR;  // fine-space halo of R's columns
     VR.part = held;
@@ -1253,6 +1353,10 @@ void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_
       L.AF = std::move(bk[r].af);
       L.AFFG = std::move(bk[r].affg);
       L.FINV = std::move(inv.q[r]);
+      if (fused) {
+        L.AFP = std::move(afp[r]);
+        L.W = std::move(wk[r]);
+      }
       L.pmap = std::move(pmap[r]);
       L.f2f = std::move(bk[r].f2f);
     });
@@ -1285,6 +1389,7 @@ void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_
       each(d, [&](int r) { pc.lv.back()[r].R = std::move(pending_r[r]); });
     }
     pc.coarse_n = n_cur;
+    pc.fused_smooths = (cfg.fused_smooths >= 0 && cfg.fused_smooths <= 2) ? cfg.fused_smooths : -1;
     pc.AC.resize(P);
     pc.ACI.resize(P);
     pc.A0.resize(P);

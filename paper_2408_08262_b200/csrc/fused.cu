@@ -65,7 +65,7 @@ __global__ void add_fill(int n, double alpha, const int32_t* __restrict__ arp, c
   }
 }
 
-void csr_add(Ctx& c, double alpha, const Csr& a, double beta, const Csr& b, Csr& out) {
+void csr_add_impl(Ctx& c, double alpha, const Csr& a, double beta, const Csr& b, Csr& out) {
   if (a.n != b.n || a.m != b.m) throw InvalidArgument("csr_add: shape mismatch");
   const int n = a.n;
   Csr r;
@@ -142,6 +142,10 @@ int64_t env_entries(const char* name, int64_t dflt) {
 }
 
 }  // namespace
+
+void csr_add(Ctx& c, double alpha, const Csr& a, double beta, const Csr& b, Csr& out) {
+  csr_add_impl(c, alpha, a, beta, b, out);
+}
 
 void build_fused_level(Ctx& c, Level& L, int64_t smooths) {
   const int n = L.a.n, nf = L.map.nf, nc = L.map.nc;

@@ -125,6 +125,8 @@ struct HostLevel {
 void hier_from_levels(Ctx& c, std::vector<HostLevel>& in, Csr&& coarse_a, Csr&& coarse_inv,
                       int64_t coarse_iterations, Hier& h);
 
+// fused.cu: C = alpha A + beta B (same shape, sorted rows; the union pattern)
+void csr_add(Ctx& c, double alpha, const Csr& a, double beta, const Csr& b, Csr& out);
 // fused.cu: the fast V-cycle's fused level operators for `smooths` F-smooths
 // and the composed coarse solve for `coarse_its` coarse iterations
 void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its);

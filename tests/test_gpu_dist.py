@@ -271,6 +271,31 @@ def test_dist_gmres_emulated_matches_one_gpu(P, threshold):
     assert np.linalg.norm(p.b - A @ res.x) <= 1.05e-10 * np.linalg.norm(p.b)
 
 
+@pytest.mark.parametrize("P,threshold", [(2, 2.0), (3, 1e9), (4, 2.0)])
+def test_dist_fast_mode_emulated_matches_one_gpu(P, threshold):
+    """The fast V-cycle on the row slabs (dist.cu: lane-group rows and the
+    fused A_F P / W_k operators sliced by F rows, their halos planned with the
+    other operators'): Richardson and GMRES(30) agree with the one-GPU fast
+    solves to the parity tolerance, and differ from the exact distributed
+    solve (which is the one-GPU exact solve bit for bit)."""
+    import scipy.sparse as sp
+    p = problems.make(4, 0.25)
+    prm = dict(problems.setup_params(4), coarse_size_target=500, fused_smooths=2)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    A = sp.csr_matrix((p.vals, p.cols, p.row_offsets), shape=(p.n, p.n))
+    d = airg.Dist(h, P, threshold=threshold)
+    for outer in (0, 1):
+        kw = dict(coarse_iterations=3, outer=outer, gmres_restart=30, max_iterations=300)
+        ref = airg.richardson_solve(h, p.b, fast=1, **kw)
+        res = d.solve(p.b, fast=1, **kw)
+        ex = d.solve(p.b, **kw)
+        assert res.stats.converged and res.stats.final_relative_residual <= 1e-10
+        assert abs(res.stats.iterations - ref.stats.iterations) <= 1
+        assert np.linalg.norm(res.x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+        assert np.linalg.norm(p.b - A @ res.x) <= 1.05e-10 * np.linalg.norm(p.b)
+        assert not np.array_equal(res.x.view(np.uint64), ex.x.view(np.uint64))
+
+
 def test_dist_gmres_nccl_single_rank_path():
     """The NCCL code path of the distributed GMRES (allreduced dots) on a
     1-rank communicator (one GPU in this run)."""

@@ -128,6 +128,30 @@ def test_owned_setup_c4_zslabs(P):
     np.testing.assert_allclose(res.x, ref.x, rtol=1e-8 * np.abs(ref.x).max(), atol=1e-12)
 
 
+@pytest.mark.parametrize("P,threshold", [(2, 2.0), (3, 1e9), (4, 2.0)])
+def test_owned_setup_fast_mode(P, threshold):
+    """The owned setup builds the fast V-cycle's A_F P and W_2 slabs from halo
+    rows (dsetup.cu): the same products in the same order as one GPU, so the
+    distributed fast solve equals the fast solve of the distributed global
+    hierarchy (dist_create slicing the one-GPU operators) bit for bit, and
+    the one-GPU fast solve to the parity tolerance."""
+    p, a = _c4(12)
+    prm = dict(problems.setup_params(4), coarse_size_target=400, fused_smooths=2)
+    h = airg.setup(a, **prm)
+    starts = np.linspace(0, p.n, P + 1).astype(np.int64)
+    d = airg.Dist.setup_owned(a, P, starts=starts, threshold=threshold, **prm)
+    dg = airg.Dist(h, P, threshold=threshold, starts=d._starts)
+    for outer in (0, 1):
+        kw = dict(coarse_iterations=3, outer=outer, max_iterations=300, fast=1)
+        res = d.solve(p.b, **kw)
+        rg = dg.solve(p.b, **kw)
+        ref = airg.richardson_solve(h, p.b, **kw)
+        assert res.stats.converged and res.stats.final_relative_residual <= 1e-10
+        assert same_bits(res.x, rg.x) and res.stats.iterations == rg.stats.iterations
+        assert abs(res.stats.iterations - ref.stats.iterations) <= 1
+        assert np.linalg.norm(res.x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
 def test_owned_setup_memory_partitioned():
     """No rank holds a level operator: at P = 4 each rank's resident bytes
     are about a quarter of one rank's at P = 1 (plus halos and the gathered
