@@ -119,6 +119,9 @@ class OwnedView:
     def fused_nnz(self, l):
         return self.d.fused_nnz(l)
 
+    def coarse_e_nnz(self):
+        return self.d.coarse_e_nnz()
+
     def info(self):
         from types import SimpleNamespace
         c = self.d.report(self.d.n_levels)
@@ -128,8 +131,8 @@ class OwnedView:
 def dist_vcycle_alg_bytes(v, coarse_iterations, up_smooths=2, fast=False):
     """Algorithmic bytes of one distributed V-cycle (dist.cu enqueue_vcycle,
     summed over the ranks): exact -- the exact V-cycle's; fast -- per level
-    R b, x = P e_c over every row, r1 = b_F - (A_F P) e_c, x_F += W r1 (no
-    one-pass level, the coarse Richardson uncomposed)."""
+    R b, r1 = b_F - (A_F P) e_c, x = P e_c + [W r1 on the F rows] (no
+    one-pass level), the composed coarse solve when the distribution uses it."""
     if not fast:
         return vcycle_alg_bytes(v, coarse_iterations, up_smooths, False)
     info = v.info()
@@ -139,10 +142,12 @@ def dist_vcycle_alg_bytes(v, coarse_iterations, up_smooths=2, fast=False):
         n, nf, nc = lv.n, lv.n_f, lv.n_c
         afp, wx = v.fused_nnz(l)
         per_cycle += 12 * lv.nnz_r + 4 * (nc + 1) + 8 * n + 8 * nc           # R b
-        per_cycle += n * (4 + 8) + 8 * nc                                     # x = P e_c
         per_cycle += 12 * afp + 4 * (nf + 1) + 8 * nc + nf * (4 + 8 + 8)      # r1
-        per_cycle += 12 * wx + 4 * (nf + 1) + 8 * nf + nf * (4 + 8 + 8)       # x_F += W r1
+        per_cycle += 12 * wx + 4 * (nf + 1) + 8 * nf + n * (4 + 4 + 8) + 8 * nc  # x
     cn = info.coarse_n
+    ce = v.coarse_e_nnz() if hasattr(v, "coarse_e_nnz") else -1
+    if ce >= 0:
+        return per_cycle + 12 * ce + 4 * (cn + 1) + 16 * cn
     for it in range(coarse_iterations):
         per_cycle += 12 * info.coarse_inv_nnz + 4 * (cn + 1) + 8 * cn + 16 * cn
         if it:

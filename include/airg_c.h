@@ -418,6 +418,9 @@ int airg_dist_report(const airg_dist* d, int64_t level, airg_level_info* info, i
  * (distributions built with fused operators: owned setup with fused_smooths
  * in 0..2, or dist_create of a hierarchy whose fused operators exist). */
 int airg_dist_fused_nnz(const airg_dist* d, int64_t level, int64_t* nnz_afp, int64_t* nnz_w);
+/* Entries of the composed coarse solve E_k held by this process (built by the
+ * first fast solve; -1 when the fast V-cycle does not use it). */
+int airg_dist_coarse_e_nnz(const airg_dist* d, int64_t* nnz);
 /* This process's wall time of the owned setup and the device time of its
  * CF splits (all levels), in ms (0 for airg_dist_create distributions). */
 int airg_dist_setup_times(const airg_dist* d, double* setup_ms, double* cf_split_ms);

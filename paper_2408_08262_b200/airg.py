@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
                                        _VP, C.c_double, _P(_VP)], C.c_int),
             "airg_dist_report": ([_VP, C.c_int64, _P(abi.LevelInfo), _P(C.c_int64)], C.c_int),
             "airg_dist_fused_nnz": ([_VP, C.c_int64, _P(C.c_int64), _P(C.c_int64)], C.c_int),
+            "airg_dist_coarse_e_nnz": ([_VP, _P(C.c_int64)], C.c_int),
             "airg_dist_setup_times": ([_VP, _P(C.c_double), _P(C.c_double)], C.c_int),
             "airg_dist_create": ([_VP, _VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _P(_VP)], C.c_int),
             "airg_dist_solve": ([_VP, _VP, _P(abi.SolveConfig), _VP, _VP, _P(abi.SolveStats), _VP,
@@ -983,6 +984,12 @@ class Dist:
         a, w = C.c_int64(), C.c_int64()
         _check(lib().airg_dist_fused_nnz(self.d, int(l), C.byref(a), C.byref(w)))
         return a.value, w.value
+
+    def coarse_e_nnz(self) -> int:
+        """Entries of the composed coarse solve held by this process (-1: not used)."""
+        v = C.c_int64()
+        _check(lib().airg_dist_coarse_e_nnz(self.d, C.byref(v)))
+        return v.value
 
     def rank_bytes(self, rank: int | None = None) -> int:
         """Device bytes of one rank's slabs (airg_dist_rank_bytes)."""

@@ -1088,6 +1088,22 @@ int airg_dist_fused_nnz(const airg_dist* dp, int64_t level, int64_t* nnz_afp, in
   });
 }
 
+int airg_dist_coarse_e_nnz(const airg_dist* dp, int64_t* nnz) {
+  return guard([&] {
+    need(dp, "dist");
+    need(nnz, "output");
+    const DHier& d = dp->d;
+    if (!d.coarse_e_ok) {
+      *nnz = -1;
+      return;
+    }
+    int64_t t = 0;
+    for (int r = 0; r < d.P && r < (int)d.rk.size(); ++r)
+      if (d.mine(r)) t += d.rk[r].ACE.nnz;
+    *nnz = t;
+  });
+}
+
 int airg_dist_report(const airg_dist* dp, int64_t level, airg_level_info* info, int64_t* n_levels) {
   return guard([&] {
     need(dp, "dist");

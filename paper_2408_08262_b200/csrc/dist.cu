@@ -6,6 +6,8 @@
 #include <cstring>
 
 #include "dist.cuh"
+#include "fusedx.cuh"
+#include "gmres.cuh"
 #include "tiled.cuh"
 
 namespace airg {
@@ -1149,6 +1151,19 @@ void dist_build(Ctx& c, DHier& d, DistPieces& pc) {
         R.AFP = std::move(S.AFP);
         R.W = std::move(S.W);
       }
+      if (pc.fused_smooths >= 0 && d.mine(r)) {  // own C rows (the complement of the F rows)
+        std::vector<int32_t> fh((size_t)(fhi - flo));
+        if (fhi > flo) to_host(c, fh.data(), S.f2f.p, fh.size());
+        std::vector<char> isf((size_t)(hi - lo), 0);
+        for (int32_t g : fh) isf[(size_t)(g - lo)] = 1;
+        std::vector<int32_t> ch;
+        ch.reserve((size_t)(hi - lo - (fhi - flo)));
+        for (int64_t i = 0; i < hi - lo; ++i)
+          if (!isf[(size_t)i]) ch.push_back((int32_t)i);
+        R.nc_own = (int64_t)ch.size();
+        R.c2f.alloc(c, std::max<size_t>(1, ch.size()));
+        if (!ch.empty()) to_device(c, R.c2f.p, ch.data(), ch.size());
+      }
       R.nf_own = fhi - flo;
       R.n_own = hi - lo;
       R.pmap = std::move(S.pmap);
@@ -1278,6 +1293,30 @@ bool dist_fast(const DHier& d, const airg_solve_config& cfg) {
   return cfg.fast != 0 && d.fused_smooths >= 0 && d.fused_smooths == cfg.up_f_smooths;
 }
 
+// the composed coarse solve for the fast V-cycle (on the coarse grid's
+// owner; every rank agrees on whether it is used)
+void dist_coarse_compose(Ctx& c, DHier& d, const airg_solve_config& cfg) {
+  if (!dist_fast(d, cfg) || d.coarse_e_its == cfg.coarse_iterations) return;
+  int ok = 1;
+  for (int r = 0; r < d.P; ++r) {
+    if (!d.mine(r)) continue;
+    DHier::Rank& T = d.rk[r];
+    T.ACE = Csr();
+    if (T.AC.n && !compose_coarse(c, T.AC, T.ACI, cfg.coarse_iterations, T.ACE)) ok = 0;
+  }
+  if (d.me >= 0 && d.P > 1) {  // the coarse owner's answer to every rank
+    DBuf<int> f(c, 1);
+    to_device(c, f.p, &ok, 1);
+    NCCL_CHECK(ncclAllReduce(f.p, f.p, 1, ncclInt, ncclMin, d.comm, c.stream));
+    to_host(c, &ok, f.p, 1);
+  }
+  for (int r = 0; r < d.P; ++r)
+    if (d.mine(r) && d.rk[r].ACE.n) row_max(c, {&d.rk[r].ACE});
+  d.coarse_e_ok = ok != 0;
+  d.coarse_e_its = cfg.coarse_iterations;
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
 void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
   const int L = (int)d.lv.size();
   const int P = d.P;
@@ -1303,8 +1342,16 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
     release(c, d, D.B);
   }
   // coarse solve on the coarse owner(s); CB and CR feed Ac^-1 through CR's
-  // layout: copy the owned rhs into CR before the first application
-  for (int64_t it = 0; it < cfg.coarse_iterations; ++it) {
+  // layout: copy the owned rhs into CR before the first application. Fast
+  // mode with the composed E_k (the coarse grid is gathered: no halo): e = E_k b.
+  if (fast && d.coarse_e_ok && d.coarse_e_its == cfg.coarse_iterations) {
+    rank_loop([&](int r) {
+      const Csr& E = d.rk[r].ACE;
+      if (E.n) launch_rows(c, E, (const double*)d.CB.rk[r].buf.p, LStore{d.CX.rk[r].buf.p}, true);
+    });
+  }
+  for (int64_t it = 0; !(fast && d.coarse_e_ok && d.coarse_e_its == cfg.coarse_iterations) &&
+                       it < cfg.coarse_iterations; ++it) {
     if (it == 0) {
       rank_loop([&](int r) {
         const int64_t own = d.CB.rk[r].own;
@@ -1333,24 +1380,26 @@ void enqueue_vcycle(Ctx& c, DHier& d, const airg_solve_config& cfg) {
   for (int l = L - 1; fast && l >= 0; --l) {
     DLevel& D = d.lv[l];
     DVec& Xn = l + 1 < L ? d.lv[l + 1].X : d.CX;
+    const bool smooth = cfg.up_f_smooths > 0;
     exchange(c, d, Xn);
+    if (smooth) {
+      rank_loop([&](int r) {
+        const DLevel::Rank& R = D.rk[r];
+        if (R.nf_own)
+          launch_rows(c, R.AFP, (const double*)Xn.rk[r].buf.p,
+                      LFres1P{D.B.rk[r].buf.p, R.f2f.p, D.RF.rk[r].buf.p}, true);
+      });
+      exchange(c, d, D.RF);
+    }
+    // x_l = P e_c + [W r1 on the F rows] in one pass (fusedx.cuh)
     rank_loop([&](int r) {
       const DLevel::Rank& R = D.rk[r];
       if (R.n_own)
-        LAUNCH_PDL(c, k_prolong4_l, blocks_for(R.n_own / 4 + 1, 256), 256, 0, (int)R.n_own, R.pmap.p,
-                   Xn.rk[r].buf.p, D.X.rk[r].buf.p);
-      if (R.nf_own && cfg.up_f_smooths > 0)
-        launch_rows(c, R.AFP, (const double*)Xn.rk[r].buf.p, LFres1P{D.B.rk[r].buf.p, R.f2f.p, D.RF.rk[r].buf.p},
-                    true);
+        launch_fused_x_raw(c, R.W, D.RF.rk[r].buf.p, R.f2f.p, R.c2f.p, (int)R.nc_own, R.pmap.p, Xn.rk[r].buf.p,
+                           D.X.rk[r].buf.p, false, smooth);
     });
+    if (smooth) release(c, d, D.RF);
     release(c, d, Xn);
-    if (cfg.up_f_smooths <= 0) continue;
-    exchange(c, d, D.RF);
-    rank_loop([&](int r) {
-      DLevel::Rank& R = D.rk[r];
-      if (R.nf_own) launch_rows(c, R.W, (const double*)D.RF.rk[r].buf.p, LFupd{R.f2f.p, D.X.rk[r].buf.p}, true);
-    });
-    release(c, d, D.RF);
   }
   for (int l = L - 1; !fast && l >= 0; --l) {
     DLevel& D = d.lv[l];
@@ -1513,12 +1562,298 @@ __global__ void k_gmd_xupdate(int64_t n, int j, const double* __restrict__ Z, co
 // oracle/airg_oracle.c): rows, vectors and Krylov basis are row slabs of
 // level 0; every inner product is a local partial followed by one
 // allreduce of (j + 1) values; the Hessenberg least squares runs on the host.
+namespace {
+// emulation: every rank's copy of cnt doubles <- their sum in rank order
+__global__ void k_rank_allsum(int P, int cnt, double* const* __restrict__ p) {
+  pdl_wait();
+  pdl_trigger();
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += p[q][k];
+    for (int q = 0; q < P; ++q) p[q][k] = s;
+  }
+}
+// sum of np partials (one block, fixed tree)
+__global__ void k_sum_part(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double sm[32];
+  pdl_wait();
+  pdl_trigger();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *out = s;
+  }
+}
+}  // namespace
+
+// Device-resident distributed GMRES(m): the one-GPU device GMRES's kernels
+// (gmres.cuh: Gram-corrected CGS2 over the unnormalised basis, Givens and
+// the stopping tests on the device) on every rank's slab, the three
+// reductions of a step (the dots with the Gram column, the norm, and per
+// restart the residual norm) summed over the ranks by an NCCL allreduce
+// (emulation: one kernel in rank order), so every rank holds the same
+// scalars. No host round trip inside a restart cycle: the host stays one
+// Arnoldi step ahead and reads the lagged "continue" flag of the previous
+// step (a step enqueued past the end is a no-op in k_gm_step).
+void dist_gmres_dev(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
+                    airg_solve_stats& st, std::vector<double>& hist) {
+  const int L = (int)d.lv.size();
+  const int P = d.P;
+  const int m = (int)(cfg.gmres_restart > 0 ? cfg.gmres_restart : 30);
+  const bool fast = dist_fast(d, cfg);
+  DVec& In = L ? d.lv[0].B : d.CB;
+  DVec& Out = L ? d.lv[0].X : d.CX;
+  auto own = [&](int r) { return d.XS.rk[r].own; };
+  const int64_t cap = std::max<int64_t>(2, cfg.max_iterations + 2);
+  const int rq = d.me < 0 ? 0 : d.me;  // the rank whose (identical) state the host reads
+  if (d.gm_m != m || (int)d.gm.size() != P || !d.gm[rq].st.p || d.gm[rq].hist.n < (size_t)cap) {
+    d.gm.clear();
+    d.gm.resize(P);
+    for (int r = 0; r < P; ++r) {
+      if (!d.mine(r)) continue;
+      const size_t o = (size_t)std::max<int64_t>(1, own(r));
+      DHier::GmRank& G = d.gm[r];
+      // one column beyond V_0..V_m and Z_0..Z_{m-1}: the step enqueued past
+      // the end of a cycle (a no-op for the scalars) still writes V_{j+1}, Z_j
+      G.V.alloc(c, o * (m + 2));
+      G.Z.alloc(c, o * (m + 1));
+      G.w.alloc(c, o);
+      G.x.alloc(c, o);
+      G.st.alloc(c, 1);
+      G.H.alloc(c, (size_t)(kGmMax + 1) * kGmMax);
+      G.cs.alloc(c, kGmMax);
+      G.sn.alloc(c, kGmMax);
+      G.g.alloc(c, kGmMax + 1);
+      G.y.alloc(c, kGmMax);
+      G.hb.alloc(c, 7 * (kGmMax + 1));
+      G.G.alloc(c, (size_t)(kGmMax + 1) * (kGmMax + 1));
+      G.hist.alloc(c, (size_t)cap);
+      G.gpart.alloc(c, (size_t)2 * (kGmMax + 1) * (size_t)std::max(1, gm_blocks(own(r))));
+      G.sc.alloc(c, 2);
+    }
+    d.gm_m = m;
+  }
+  if (!d.gm_flag) CUDA_CHECK(cudaMallocHost(&d.gm_flag, 2 * sizeof(int)));
+  dist_coarse_compose(c, d, cfg);
+  const int64_t vkey = (cfg.up_f_smooths * 1000003 + cfg.coarse_iterations * 31) * 2 + (fast ? 1 : 0);
+  if (!d.graph_vc || d.graph_vc_key != vkey) {
+    d.graph_vc_kernels = capture_graph(c, &d.graph_vc, [&] {
+      enqueue_vcycle(c, d, cfg);
+      p2p_flush(c, d);
+    });
+    d.graph_vc_key = vkey;
+  }
+  auto mine = [&](auto&& f) {
+    for (int r = 0; r < P; ++r)
+      if (d.mine(r)) f(r);
+  };
+  // segments of hb: (h1) | h2 | nrm | d (2 (kGmMax + 1)) | hsum | vs
+  const int S = kGmMax + 1;
+  auto h2 = [&](int r) { return d.gm[r].hb.p + S; };
+  auto nrm = [&](int r) { return d.gm[r].hb.p + 2 * S; };
+  auto dd = [&](int r) { return d.gm[r].hb.p + 3 * S; };
+  auto hsum = [&](int r) { return d.gm[r].hb.p + 5 * S; };
+  auto vs = [&](int r) { return d.gm[r].hb.p + 6 * S; };
+  // allreduce sites: pointer tables for the emulated reduction
+  DBuf<double*> pd(c, (size_t)P), pn(c, (size_t)P), ps(c, (size_t)P);
+  if (d.me < 0 && P > 1) {
+    std::vector<double*> a(P), b(P), e(P);
+    for (int r = 0; r < P; ++r) {
+      a[r] = dd(r);
+      b[r] = nrm(r);
+      e[r] = d.gm[r].sc.p;
+    }
+    to_device(c, pd.p, a.data(), (size_t)P);
+    to_device(c, pn.p, b.data(), (size_t)P);
+    to_device(c, ps.p, e.data(), (size_t)P);
+  }
+  auto allsum = [&](int cnt, double* const* table, const std::function<double*(int)>& mineptr) {
+    if (P == 1) return;
+    if (d.me >= 0) {
+      double* p = mineptr(d.me);
+      NCCL_CHECK(ncclAllReduce(p, p, (size_t)cnt, ncclDouble, ncclSum, d.comm, c.stream));
+    } else {
+      LAUNCH_PDL(c, k_rank_allsum, 1, 256, 0, P, cnt, table);
+    }
+  };
+  // w (or x for the residual) -> A x over the slabs, epilogue per rank
+  auto stage_xs = [&](const std::function<const double*(int)>& xin) {
+    mine([&](int r) {
+      if (own(r))
+        CUDA_CHECK(cudaMemcpyAsync(d.XS.rk[r].buf.p, xin(r), sizeof(double) * own(r), cudaMemcpyDeviceToDevice,
+                                   c.stream));
+    });
+    exchange(c, d, d.XS);
+  };
+  // ---- start: r = b, x = 0, ||b||
+  GmDev s0 = {};
+  s0.cap = cap;
+  s0.maxit = cfg.max_iterations;
+  s0.m = m;
+  s0.rtol = cfg.rtol;
+  mine([&](int r) {
+    const int64_t o = own(r), lo = d.me < 0 ? d.XS.rk[r].lo : 0;
+    if (o) {
+      CUDA_CHECK(cudaMemcpyAsync(d.rk[r].rhs.p, d_b + lo, sizeof(double) * o, cudaMemcpyDeviceToDevice, c.stream));
+      CUDA_CHECK(cudaMemcpyAsync(d.gm[r].w.p, d_b + lo, sizeof(double) * o, cudaMemcpyDeviceToDevice, c.stream));
+      dot_async(c, d.gm[r].w.p, d.gm[r].w.p, o, d.gm[r].sc.p, d.gm[r].gpart.p);
+    } else {
+      CUDA_CHECK(cudaMemsetAsync(d.gm[r].sc.p, 0, sizeof(double), c.stream));
+    }
+    CUDA_CHECK(cudaMemsetAsync(d.gm[r].x.p, 0, sizeof(double) * std::max<int64_t>(1, o), c.stream));
+    to_device(c, d.gm[r].st.p, &s0, 1);
+  });
+  allsum(1, ps.p, [&](int r) { return d.gm[r].sc.p; });
+  mine([&](int r) { LAUNCH(c, k_gm_init, 1, 32, 0, 0, 0, (const double*)d.gm[r].sc.p, d.gm[r].st.p, d.gm[r].hist.p); });
+  GmDev s1;
+  to_host(c, &s1, d.gm[rq].st.p, 1);
+  bool outer = s1.bnorm != 0.0 && s1.maxit > 0;
+  cudaEvent_t ev[2];
+  CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  const uint64_t l0 = c.launches;
+  while (outer) {
+    mine([&](int r) {
+      LAUNCH(c, k_gm_cycle, (unsigned)gm_blocks(std::max<int64_t>(1, own(r))), kGmThreads, 0, 0, 0, own(r),
+             (const double*)d.gm[r].w.p, d.gm[r].st.p, d.gm[r].V.p, In.rk[r].buf.p, d.gm[r].g.p, vs(r));
+    });
+    for (int k = 0;; ++k) {
+      // ---- one Arnoldi step
+      CUDA_CHECK(cudaGraphLaunch(d.graph_vc, c.stream));
+      c.launches += d.graph_vc_kernels;
+      stage_xs([&](int r) { return (const double*)Out.rk[r].buf.p; });
+      mine([&](int r) {
+        const Csr& A = d.rk[r].A0;
+        if (A.n)
+          launch_rows(c, A, (const double*)d.XS.rk[r].buf.p,
+                      EpiGmSpmv{d.gm[r].w.p, Out.rk[r].buf.p, d.gm[r].Z.p, d.gm[r].st.p, own(r), vs(r)}, fast);
+      });
+      release(c, d, d.XS);
+      p2p_flush(c, d);
+      std::vector<int> nsf(P, 1);
+      mine([&](int r) {
+        const int64_t n = own(r);
+        const int pp = n % 4 == 0 ? 2 : (n % 2 == 0 ? 1 : 0);
+        double* part = d.gm[r].gpart.p;
+        const double* V = d.gm[r].V.p;
+        if (pp) {
+          nsf[r] = (int)std::max<int64_t>(1, (n / (2 * pp) + kGmThreads - 1) / kGmThreads);
+          auto* k3 = pp == 2 ? &k_gm_sweep_fast<3, 2> : &k_gm_sweep_fast<3, 1>;
+          LAUNCH_PDL(c, k3, (unsigned)nsf[r], kGmThreads, 0, n, V, (const double*)d.gm[r].w.p,
+                     (const GmDev*)d.gm[r].st.p, (const double*)nullptr, part, (const double*)vs(r), d.gm[r].V.p,
+                     In.rk[r].buf.p);
+        } else {
+          nsf[r] = gm_blocks(n);
+          LAUNCH_PDL(c, (k_gm_sweep<3, true>), (unsigned)nsf[r], kGmThreads, 0, n, V, d.gm[r].w.p,
+                     (const GmDev*)d.gm[r].st.p, (const double*)nullptr, part, (const double*)vs(r), d.gm[r].V.p,
+                     In.rk[r].buf.p, 1);
+        }
+        LAUNCH_PDL(c, k_gm_finish, 2 * kGmMax, kFinThreads, 0, (const double*)part, nsf[r],
+                   (const GmDev*)d.gm[r].st.p, 0, dd(r));
+      });
+      allsum(2 * S, pd.p, dd);
+      mine([&](int r) {
+        LAUNCH_PDL(c, k_gm_gram, 1, 32, 0, (const GmDev*)d.gm[r].st.p, (const double*)dd(r), d.gm[r].G.p, h2(r),
+                   hsum(r));
+        const int64_t n = own(r);
+        const int pp = n % 4 == 0 ? 2 : (n % 2 == 0 ? 1 : 0);
+        double* part = d.gm[r].gpart.p;
+        if (pp) {
+          auto* k2 = pp == 2 ? &k_gm_sweep_fast<2, 2> : &k_gm_sweep_fast<2, 1>;
+          LAUNCH_PDL(c, k2, (unsigned)nsf[r], kGmThreads, 0, n, (const double*)d.gm[r].V.p,
+                     (const double*)d.gm[r].w.p, (const GmDev*)d.gm[r].st.p, (const double*)hsum(r), part,
+                     (const double*)vs(r), d.gm[r].V.p, In.rk[r].buf.p);
+        } else {
+          LAUNCH_PDL(c, (k_gm_sweep<2, true>), (unsigned)nsf[r], kGmThreads, 0, n, (const double*)d.gm[r].V.p,
+                     d.gm[r].w.p, (const GmDev*)d.gm[r].st.p, (const double*)hsum(r), part, (const double*)vs(r),
+                     d.gm[r].V.p, In.rk[r].buf.p, 1);
+        }
+        LAUNCH_PDL(c, k_gm_finish, 1, kFinThreads, 0, (const double*)part, nsf[r], (const GmDev*)d.gm[r].st.p, 1,
+                   nrm(r));
+      });
+      allsum(1, pn.p, nrm);
+      mine([&](int r) {
+        LAUNCH_PDL(c, k_gm_step, 1, 32, 0, 0, 0, d.gm[r].st.p, (const double*)dd(r), (const double*)h2(r),
+                   (const double*)nrm(r), d.gm[r].H.p, d.gm[r].cs.p, d.gm[r].sn.p, d.gm[r].g.p, d.gm[r].hist.p,
+                   vs(r));
+      });
+      // the lagged flag: this step's, read after the next step is enqueued
+      CUDA_CHECK(cudaMemcpyAsync(d.gm_flag + (k & 1), &d.gm[rq].st.p->more, sizeof(int), cudaMemcpyDeviceToHost,
+                                 c.stream));
+      CUDA_CHECK(cudaEventRecord(ev[k & 1], c.stream));
+      if (k >= 1) {
+        CUDA_CHECK(cudaEventSynchronize(ev[(k - 1) & 1]));
+        if (!d.gm_flag[(k - 1) & 1]) break;  // step k was past the end: a no-op
+      }
+      if (k + 1 >= m) break;  // the cycle's last column: no step past it
+    }
+    // ---- end of the cycle: y, x += Z y, r = b - A x, beta, the outer test
+    mine([&](int r) {
+      LAUNCH_PDL(c, k_gm_ysolve, 1, 32, 0, (const GmDev*)d.gm[r].st.p, (const double*)d.gm[r].H.p,
+                 (const double*)d.gm[r].g.p, d.gm[r].y.p);
+      if (own(r))
+        LAUNCH_PDL(c, k_gm_xupdate, (unsigned)gm_blocks(own(r)), kGmThreads, 0, own(r), (const GmDev*)d.gm[r].st.p,
+                   (const double*)d.gm[r].Z.p, (const double*)d.gm[r].y.p, d.gm[r].x.p);
+    });
+    stage_xs([&](int r) { return (const double*)d.gm[r].x.p; });
+    mine([&](int r) {
+      const Csr& A = d.rk[r].A0;
+      if (!A.n) {
+        CUDA_CHECK(cudaMemsetAsync(d.gm[r].sc.p, 0, sizeof(double), c.stream));
+        return;
+      }
+      launch_rows(c, A, (const double*)d.XS.rk[r].buf.p,
+                  LResid{d.rk[r].rhs.p, d.gm[r].w.p, d.part.p + d.part_off[r], 0.0}, false);
+      const int np = (int)rows_grid(tview(A), false);
+      LAUNCH_PDL(c, k_sum_part, 1, 1024, 0, (const double*)(d.part.p + d.part_off[r]), np, d.gm[r].sc.p);
+    });
+    release(c, d, d.XS);
+    p2p_flush(c, d);
+    allsum(1, ps.p, [&](int r) { return d.gm[r].sc.p; });
+    mine([&](int r) { LAUNCH_PDL(c, k_gm_restart, 1, 32, 0, 0, 0, d.gm[r].st.p, (const double*)d.gm[r].sc.p); });
+    to_host(c, &s1, d.gm[rq].st.p, 1);
+    outer = !s1.converged && s1.beta != 0.0 && s1.its < s1.maxit;
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  (void)l0;
+  to_host(c, &s1, d.gm[rq].st.p, 1);
+  const long long kept = std::min<long long>(s1.its, cap - 1);
+  std::vector<double> hv((size_t)kept + 1);
+  to_host(c, hv.data(), d.gm[rq].hist.p, hv.size());
+  for (double v : hv) hist.push_back(v);
+  st.iterations = s1.its;
+  st.converged = s1.converged;
+  st.final_relative_residual = s1.rel;
+  mine([&](int r) {
+    const int64_t o = own(r), lo = d.me < 0 ? d.XS.rk[r].lo : 0;
+    if (o) CUDA_CHECK(cudaMemcpyAsync(d_x + lo, d.gm[r].x.p, sizeof(double) * o, cudaMemcpyDeviceToDevice, c.stream));
+  });
+  CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
 void dist_gmres(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
                 airg_solve_stats& st, std::vector<double>& hist) {
   const int L = (int)d.lv.size();
   const int P = d.P;
   const int m = (int)(cfg.gmres_restart > 0 ? cfg.gmres_restart : 30);
   if (m > 512) throw InvalidArgument("gmres: restart length above 512");
+  static const bool host_gm = [] {
+    const char* e = getenv("AIRG_DIST_GM_HOST");
+    return e && e[0] == '1';
+  }();
+  if (m <= kGmMax && !host_gm && cfg.max_iterations > 0) {
+    dist_gmres_dev(c, d, cfg, d_b, d_x, st, hist);
+    return;
+  }
+  d.gm.clear();  // the host form allocates its own per-rank buffers
   DVec& In = L ? d.lv[0].B : d.CB;   // V-cycle input (owned part)
   DVec& Out = L ? d.lv[0].X : d.CX;  // V-cycle output (owned part)
   auto own = [&](int r) { return d.XS.rk[r].own; };
@@ -1743,6 +2078,7 @@ void dist_halo_bytes(const DHier& d, const airg_solve_config& cfg, int64_t& vcyc
 void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
                 airg_solve_stats& st, std::vector<double>& hist) {
   if (cfg.down_smooths != 0) throw InvalidArgument("solve: down_smooths > 0 is not offered by the GPU V-cycle");
+  dist_coarse_compose(c, d, cfg);
   if (cfg.rtol <= 0.0) throw InvalidArgument("richardson_solve: rtol must be positive");
   if (cfg.outer == 1) {
     dist_gmres(c, d, cfg, d_b, d_x, st, hist);

@@ -109,6 +109,8 @@ struct DLevel {
     Csr R, AF, AFFG, FINV;    // local rows, remapped columns
     Csr AFP, W;               // fast V-cycle: A_F P (-> X_{l+1} layout), W_k (-> RF layout); F rows
     DBuf<int32_t> pmap, f2f;  // prolongation map (-> X_{l+1} layout), F row -> local fine row
+    DBuf<int32_t> c2f;        // fast V-cycle: the own C rows (local fine rows)
+    int64_t nc_own = 0;
     DBuf<double> sc;
     int64_t nf_own = 0, n_own = 0;
   };
@@ -122,10 +124,13 @@ struct DHier {
   double threshold = 2.0;
   std::vector<DLevel> lv;
   int64_t fused_smooths = -1;  // up_f_smooths of the fast V-cycle's A_F P / W_k slabs (-1: none)
+  int64_t coarse_e_its = -1;   // coarse_iterations the composed coarse solve was built for
+  bool coarse_e_ok = false;    // ... and whether it is used
   Part cpart;            // coarsest rows (gathered on rank 0)
   DVec CB, CX, CR, XS;   // coarse b / e / r and the top solution vector
   struct Rank {
     Csr A0, AC, ACI;     // top operator (residual), coarse operator and its inverse
+    Csr ACE;             // fast V-cycle: the composed coarse solve E_k (coarse owner)
     DBuf<double> rhs;    // owned part of b
   };
   std::vector<Rank> rk;
@@ -143,9 +148,14 @@ struct DHier {
   uint64_t graph_vc_kernels = 0;
   struct GmRank {
     DBuf<double> V, Z, w, x, dots, part;
+    // device-resident form (dist_gmres_dev): the GMRES state and scalars of
+    // this rank (identical on every rank: the reductions are allreduced)
+    DBuf<GmDev> st;
+    DBuf<double> H, cs, sn, g, y, hb, G, hist, gpart, sc;
   };
   std::vector<GmRank> gm;
   int gm_m = 0;
+  int* gm_flag = nullptr;  // pinned: the lagged "inner loop continues" flags of the device GMRES
   int64_t top_n = 0;
   // owned setup (dist_setup_owned): per-level reports, identical on every rank
   struct Summary {

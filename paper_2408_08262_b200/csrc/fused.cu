@@ -231,25 +231,28 @@ void build_fused_level(Ctx& c, Level& L, int64_t smooths) {
 // nnz(E_k) <= AIRG_COARSE_COMPOSE entries: one row pass instead of 2k - 1
 // dependent ones (C4: 280 k entries for k = 3 instead of five launches over
 // 57 k-entry operators).
-void build_coarse_composed(Ctx& c, Hier& h, int64_t its) {
-  h.coarse_e = Csr();
-  h.coarse_composed = false;
+bool compose_coarse(Ctx& c, const Csr& a, const Csr& q, int64_t its, Csr& out) {
+  out = Csr();
   const int64_t cap = env_entries("AIRG_COARSE_COMPOSE", 4000000);
-  if (its < 1 || h.coarse_a.n == 0 || cap <= 0 || h.coarse_a.n > 50000) return;
+  if (its < 1 || a.n == 0 || cap <= 0 || a.n > 50000 || a.n != a.m || q.n != a.n || q.m != a.n) return false;
   Csr e;
-  csr_add(c, 1.0, h.coarse_inv, 0.0, h.coarse_inv, e);
+  csr_add(c, 1.0, q, 0.0, q, e);
   for (int64_t k = 1; k < its; ++k) {
     Csr ae, qae, qe, next;
-    spgemm(c, h.coarse_a, e, ae);
-    spgemm(c, h.coarse_inv, ae, qae);
-    csr_add(c, 1.0, h.coarse_inv, 1.0, e, qe);
+    spgemm(c, a, e, ae);
+    spgemm(c, q, ae, qae);
+    csr_add(c, 1.0, q, 1.0, e, qe);
     csr_add(c, 1.0, qe, -1.0, qae, next);
     e = std::move(next);
-    if (e.nnz > cap) return;
+    if (e.nnz > cap) return false;
   }
-  if (e.nnz > cap) return;
-  h.coarse_e = std::move(e);
-  h.coarse_composed = true;
+  if (e.nnz > cap) return false;
+  out = std::move(e);
+  return true;
+}
+
+void build_coarse_composed(Ctx& c, Hier& h, int64_t its) {
+  h.coarse_composed = compose_coarse(c, h.coarse_a, h.coarse_inv, its, h.coarse_e);
 }
 
 void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its) {

@@ -319,6 +319,7 @@ void p2p_free(DHier& d) {
 }
 
 DHier::~DHier() {
+  if (gm_flag) cudaFreeHost(gm_flag);
   if (graph) cudaGraphExecDestroy(graph);
   if (graph_vc) cudaGraphExecDestroy(graph_vc);
   p2p_free(*this);

@@ -38,6 +38,8 @@ struct GmDev {
   int m;            // restart length
   int converged;
   int restarts;
+  int more;  // the inner loop continues (set by k_gm_cycle / k_gm_step; steps after it no-op)
+  int _pad;
   double rtol, bnorm, beta, hn, rel, est;
 };
 
@@ -127,6 +129,10 @@ void hier_from_levels(Ctx& c, std::vector<HostLevel>& in, Csr&& coarse_a, Csr&& 
 
 // fused.cu: C = alpha A + beta B (same shape, sorted rows; the union pattern)
 void csr_add(Ctx& c, double alpha, const Csr& a, double beta, const Csr& b, Csr& out);
+// fused.cu: the composed coarse solve E_k (k coarse Richardson steps from
+// e = 0) of A with its assembled inverse Q; false when not offered
+// (AIRG_COARSE_COMPOSE entries exceeded, k < 1, or a large grid)
+bool compose_coarse(Ctx& c, const Csr& a, const Csr& q, int64_t its, Csr& out);
 // fused.cu: the fast V-cycle's fused level operators for `smooths` F-smooths
 // and the composed coarse solve for `coarse_its` coarse iterations
 void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its);
