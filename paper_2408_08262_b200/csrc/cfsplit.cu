@@ -1310,6 +1310,7 @@ CfFused cf_split_fused_finish(Ctx& c, const unsigned long long* hu, bool ddc_ena
 
 CfFused cf_split_fused(Ctx& c, const Csr& a, double alpha, uint64_t seed, bool ddc_enabled,
                        double fraction, int64_t bins, uint8_t* d_labels, uint8_t* d_labels_pre) {
+  NvtxRange nvtx__("airg CF split");
   const unsigned long long* u =
       cf_split_fused_enqueue(c, a, alpha, seed, ddc_enabled, fraction, bins, d_labels, d_labels_pre, nullptr);
   if (!u) return CfFused{};

@@ -2077,6 +2077,7 @@ void dist_halo_bytes(const DHier& d, const airg_solve_config& cfg, int64_t& vcyc
 
 void dist_solve(Ctx& c, DHier& d, const airg_solve_config& cfg, const double* d_b, double* d_x,
                 airg_solve_stats& st, std::vector<double>& hist) {
+  NvtxRange nvtx__("airg dist solve");
   if (cfg.down_smooths != 0) throw InvalidArgument("solve: down_smooths > 0 is not offered by the GPU V-cycle");
   dist_coarse_compose(c, d, cfg);
   if (cfg.rtol <= 0.0) throw InvalidArgument("richardson_solve: rtol must be positive");

@@ -813,6 +813,7 @@ DistInverse dist_checked_inverse(Ctx& c, DHier& d, DVec& VF, std::vector<FfRank>
 void dist_setup_owned(Ctx& c, std::vector<Csr>& a_rows, const std::vector<int64_t>& starts,
                       const airg_setup_config& cfg, const Injection* inj, int P, int me, ncclComm_t comm,
                       double threshold, DHier& d) {
+  NvtxRange nvtx__("airg dist setup (owned)");
   if (P < 1) throw InvalidArgument("dist: need at least one rank");
   if (me >= P) throw InvalidArgument("dist: rank out of range");
   if (me >= 0 && P > 1 && !comm) throw InvalidArgument("dist: a communicator is needed per rank");

@@ -256,6 +256,7 @@ void build_coarse_composed(Ctx& c, Hier& h, int64_t its) {
 }
 
 void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its) {
+  NvtxRange nvtx__("airg fused operators");
   if (smooths < 0) throw InvalidArgument("fast V-cycle: up_f_smooths must be >= 0");
   if (fused_ready(h, smooths, coarse_its)) return;
   const char* te = getenv("AIRG_SETUP_TIMING");

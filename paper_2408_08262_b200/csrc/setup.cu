@@ -169,6 +169,7 @@ void recompute_metrics(Hier& h) {
 
 void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection* inj, Hier& h,
            const RowSplit* rs) {
+  NvtxRange nvtx__("airg setup");
   if (a0.n != a0.m) throw InvalidArgument("setup: matrix must be square");
   if (cfg.poly_order < 1 || cfg.coarse_poly_order < 1)
     throw InvalidArgument("setup: polynomial orders must be >= 1");

@@ -1237,6 +1237,7 @@ void gmres(Ctx& c, Hier& h, const airg_solve_config& cfg, airg_solve_stats& st,
 
 void solve(Ctx& c, Hier& h, const airg_solve_config& cfg, const double* d_b, double* d_x,
            airg_solve_stats& st, std::vector<double>& history) {
+  NvtxRange nvtx__("airg solve");
   check_cfg(cfg);
   if (cfg.fast && !fused_ready(h, cfg.up_f_smooths, cfg.coarse_iterations))
     build_fused(c, h, cfg.up_f_smooths, cfg.coarse_iterations);
