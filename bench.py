@@ -804,6 +804,17 @@ def run_gpu(args):
     k1.record(stream)
     k1.synchronize()
     kern_ms = k0.elapsed_time(k1) / reps
+    # time per V-cycle: the captured V-cycle graph through the
+    # C-ABI (b copied in, x copied out: two n-vector device copies included)
+    vk = dict(coarse_iterations=prm["coarse_iterations"], fast=int(fast))
+    for _ in range(3):
+        h.vcycle_device(xv, yv, **vk)
+    k0.record(stream)
+    for _ in range(20):
+        h.vcycle_device(xv, yv, **vk)
+    k1.record(stream)
+    k1.synchronize()
+    vcycle_ms = k0.elapsed_time(k1) / 20
     kt = []
     for _ in range(10):
         with torch.cuda.stream(stream):
@@ -868,6 +879,7 @@ def run_gpu(args):
         "iterations": its, "final_relative_residual": float(rel),
         "other_mode": other,
         "levels": int(info.n_levels), "operator_complexity": info.operator_complexity,
+        "vcycle_ms": vcycle_ms,
         "setup_ms": setup_ms, "cf_split_ms": cf_ms, "cf_split_ms_sync_each_level": cf_ms_each,
         "cf_split_roofline": {"bound": "hbm", "achieved": cf_bytes / (cf_ms / 1e3) / 1e9, "peak": peak,
                               "unit": "GB/s", "frac": cf_bytes / (cf_ms / 1e3) / 1e9 / peak,

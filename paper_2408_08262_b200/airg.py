@@ -711,6 +711,11 @@ class Hierarchy:
         _check(lib().airg_vcycle(self.ctx.h, self.h, C.byref(cfg), _ptr(tb), _ptr(tx)))
         return self.ctx.to_host(tx)
 
+    def vcycle_device(self, tb, tx, **solve_kw) -> None:
+        """One V-cycle x = M b with device-resident b / x (torch tensors)."""
+        cfg = abi.solve_config(**solve_kw)
+        _check(lib().airg_vcycle(self.ctx.h, self.h, C.byref(cfg), _ptr(tb), _ptr(tx)))
+
     def solve_device(self, tb, tx, history_cap: int = 0, **solve_kw):
         """Solve with device-resident b / x (torch tensors)."""
         cfg = abi.solve_config(**solve_kw)
