@@ -27,7 +27,7 @@
 
 namespace airg {
 
-constexpr int kTileThreads = 128;  // 4 warps per block (measured: 64 and 256 slower)
+constexpr int kTileThreads = 128;  // 4 warps per block (measured: 64 and 256 slower; fast mode C4: 517 / 440 vs 435 us per iteration)
 
 struct TileView {
   const int32_t* rp;
