@@ -19,6 +19,6 @@ CF_CONFIG=4 timeout 600 ncu --profile-from-start off --metrics $M --clock-contro
 for spec in "desc0:EpiStore2:0" "fusedx0:k_fused_x:18" "fusedx4:k_fused_x:14" "sweep:k_gm_sweep:31"; do
   IFS=: read name kre skip <<< "$spec"
   timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on \
-      -k "regex:$kre" --launch-skip "$skip" -c 1 -o "gpurun_out/r2_${name}_full" -f \
+      --kernel-name-base demangled -k "regex:$kre" --launch-skip "$skip" -c 1 -o "gpurun_out/r2_${name}_full" -f \
       python tools/profile_solve.py --config 4 --what solve > "gpurun_out/p2_${name}.log" 2>&1; echo "$name rc=$?"
 done
