@@ -277,6 +277,28 @@ def test_composed_coarse_solve_any_iteration_count(tmp_path):
     assert np.array_equal(a[2].view(np.uint64), a[4].view(np.uint64))
 
 
+@pytest.mark.parametrize("nx,ct", [(12, 1000), (40, 700), (64, 300)])
+def test_fast_mode_tiny_hierarchies(nx, ct):
+    """Coarse-only (no fine level), one-level and two-level hierarchies: the
+    fast solve (fused operators, composed coarse solve, one-pass choice,
+    device GMRES) matches the exact one to the parity tolerance."""
+    p = problems.c0_structured_2d(nx)
+    prm = dict(problems.setup_params(0), coarse_size_target=ct)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    if nx == 12:
+        assert h.n_levels == 0  # the coarse grid alone
+    for outer in (0, 1):
+        kw = dict(coarse_iterations=prm["coarse_iterations"], outer=outer, max_iterations=500)
+        ex = airg.richardson_solve(h, p.b, **kw)
+        fa = airg.richardson_solve(h, p.b, fast=1, **kw)
+        assert ex.stats.converged == fa.stats.converged
+        if not ex.stats.converged:
+            continue
+        assert fa.stats.final_relative_residual <= 1e-10
+        assert abs(fa.stats.iterations - ex.stats.iterations) <= 1
+        assert np.linalg.norm(fa.x - ex.x) <= 1e-8 * np.linalg.norm(ex.x)
+
+
 def test_fused_rebuild_invalidates_captured_graphs():
     """Switching the F-smooth count rebuilds the fused operators (new
     buffers): every cached graph that captured the old ones must be
