@@ -134,6 +134,27 @@ __global__ void map_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci,
 // levels, ~25-30 entries); rows of <= 5 entries on average (the fine levels'
 // A, R, A_FF, Aff^-1) use 4-entry batches; the rest the 8-entry scalar loop
 // (thresholds measured on the C2 hierarchy, round 1).
+constexpr int kOQLanesSwitch = 4;  // 4 lanes x 4 entries cover rows up to 16; longer -> 8 lanes
+// Exact mode, long rows on small operators (latency bound): AIRG_OLANES_MEAN
+// entries per row and above (default 12; 0 = off) on at most AIRG_OLANES_N
+// rows (default 20 k). C4 exact GMRES 645 -> 633 us per iteration (the first
+// F residuals of levels 9-18: 7.6-9.5 -> 4.6-6.3 us); on 46 k-row operators
+// the ordered-lane kernel is slower (8.6 -> 13.8 us).
+int row_olanes(int64_t n, int64_t nnz) {
+  static const double mean_min = [] {
+    const char* e = getenv("AIRG_OLANES_MEAN");
+    return (e && e[0]) ? atof(e) : 12.0;
+  }();
+  static const int64_t n_max = [] {
+    const char* e = getenv("AIRG_OLANES_N");
+    return (e && e[0]) ? atoll(e) : (int64_t)20000;
+  }();
+  if (mean_min <= 0.0 || n <= 0 || n > n_max) return 0;
+  const double mean = (double)nnz / (double)n;
+  if (mean < mean_min) return 0;
+  return mean > 4.0 * kOQLanesSwitch ? 8 : 4;
+}
+
 int row_vec(int64_t n, int64_t nnz) {
   if (n <= 0) return 0;
   if (nnz >= 12 * n) return 8;

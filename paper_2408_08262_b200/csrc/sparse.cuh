@@ -20,6 +20,9 @@ void drop_entries(Ctx& c, const Csr& a, double tol, bool keep_diagonal, Csr& out
 int row_vec(int64_t n, int64_t nnz);
 // lanes per row of the fast-mode row kernels (tiled.cuh rows_lanes)
 int row_lanes(int64_t n, int64_t nnz, int32_t max_row = -1);
+// lanes of the exact mode's ordered-lane kernel (tiled.cuh rows_olanes) for a
+// matrix of n rows and nnz entries; 0 = thread per row
+int row_olanes(int64_t n, int64_t nnz);
 // measure the longest row of every matrix into its max_row (one readback)
 void row_max(Ctx& c, const std::vector<Csr*>& ms);
 // out = a with every column j replaced by map[j] (order-preserving maps only)

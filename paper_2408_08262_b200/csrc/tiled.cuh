@@ -37,6 +37,7 @@ struct TileView {
   int nnz;   // bounds the aligned vector loads
   int vec;   // exact mode: entries per vector batch (8), 4-entry scalar (4), 8-entry scalar (0)
   int lanes; // fast mode: lanes per row (1, 2, 4, 8, 16, 32)
+  int olanes; // exact mode: lanes of the ordered-lane kernel (0: thread per row)
 };
 
 // Epilogues may expose `Pre pre(int row)`: operands the epilogue reads that
@@ -209,13 +210,99 @@ __global__ void __launch_bounds__(kTileThreads) rows_lanes_fc(TileView m, const 
   if (live && lane == 0) epi.row2_pre(r, sf, sc, pre);
 }
 
+// ---- exact, long rows: G lanes load, one ordered sum ---------------------------
+// A row of the exact mode is one sequential chain of separately rounded
+// products and sums in column order (the reference's bits). With thread per
+// row, a 30-entry row is four dependent batches of loads; here G lanes load
+// Q = 4 entries each in one round (coalesced), form the products, and lane 0
+// adds them in column order from the lanes' registers by shuffles -- the same
+// chain of roundings, one round of loads per 4 G entries. FC: F and C columns
+// into two sums (bit 31 of the column), as rows_thread_fc.
+constexpr int kOQ = 4;
+template <class E, bool = has_pre<E>::value>
+struct PreOf {
+  struct type {};
+};
+template <class E>
+struct PreOf<E, true> {
+  using type = typename E::Pre;
+};
+template <class Epi, int G, bool FC>
+__global__ void __launch_bounds__(kTileThreads) rows_olanes(TileView m, const double* __restrict__ x, Epi epi) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = t / G, lane = t & (G - 1);
+  const bool live = r < m.nrows;
+  int s = 0, len = 0;
+  int c[kOQ];
+  double a[kOQ];
+  if (live) {
+    s = __ldg(m.rp + r);
+    len = __ldg(m.rp + r + 1) - s;
+  }
+#pragma unroll
+  for (int q = 0; q < kOQ; ++q) {
+    const int k = lane + q * G;
+    c[q] = k < len ? __ldg(m.ci + s + k) : 0;
+    a[q] = k < len ? __ldg(m.v + s + k) : 0.0;
+  }
+  typename PreOf<Epi>::type pre{};
+  if constexpr (has_pre<Epi>::value)
+    if (live && lane == 0) pre = epi.pre(r);
+  pdl_wait();
+  pdl_trigger();
+  int maxlen = len;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+  double sf = 0.0, sc = 0.0;
+  for (int base = 0; base < maxlen; base += kOQ * G) {
+    if (base > 0) {
+#pragma unroll
+      for (int q = 0; q < kOQ; ++q) {
+        const int k = base + lane + q * G;
+        c[q] = k < len ? __ldg(m.ci + s + k) : 0;
+        a[q] = k < len ? __ldg(m.v + s + k) : 0.0;
+      }
+    }
+    double p[kOQ];
+#pragma unroll
+    for (int q = 0; q < kOQ; ++q) {
+      const int k = base + lane + q * G;
+      p[q] = k < len ? __dmul_rn(a[q], __ldg(x + (FC ? (c[q] & 0x7fffffff) : c[q]))) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kOQ; ++q) {
+#pragma unroll
+      for (int src = 0; src < G; ++src) {
+        const double v = __shfl_sync(0xffffffffu, p[q], src, G);
+        const int cf = FC ? __shfl_sync(0xffffffffu, c[q], src, G) : 0;
+        if (lane == 0 && base + q * G + src < len) {
+          if (FC && cf < 0)
+            sc = __dadd_rn(sc, v);
+          else
+            sf = __dadd_rn(sf, v);
+        }
+      }
+    }
+  }
+  if (live && lane == 0) {
+    if constexpr (FC)
+      epi.row2_pre(r, sf, sc, pre);
+    else if constexpr (has_pre<Epi>::value)
+      epi.row_pre(r, sf, pre);
+    else
+      epi.row(r, sf);
+  }
+  if constexpr (!FC) epi.finish();
+}
+
 // ---- launch ------------------------------------------------------------------------
 inline TileView tview(const Csr& m) {
-  return TileView{m.rp.p, m.ci.p, m.v.p, m.n, (int)m.nnz, row_vec(m.n, m.nnz), row_lanes(m.n, m.nnz, m.max_row)};
+  return TileView{m.rp.p, m.ci.p, m.v.p, m.n, (int)m.nnz, row_vec(m.n, m.nnz), row_lanes(m.n, m.nnz, m.max_row),
+                  row_olanes(m.n, m.nnz)};
 }
 
 inline unsigned rows_grid(const TileView& m, bool fast) {
-  const int64_t threads = (int64_t)m.nrows * (fast ? m.lanes : 1);
+  const int64_t threads = (int64_t)m.nrows * (fast ? m.lanes : (m.olanes > 1 ? m.olanes : 1));
   const int64_t blocks = (threads + kTileThreads - 1) / kTileThreads;
   return (unsigned)(blocks > 0 ? blocks : 1);
 }
@@ -233,6 +320,8 @@ inline auto rows_kernel(const TileView& m, bool fast) -> void (*)(TileView, cons
       default: return &rows_lanes<Epi, 32>;
     }
   }
+  if (m.olanes == 4) return &rows_olanes<Epi, 4, false>;
+  if (m.olanes == 8) return &rows_olanes<Epi, 8, false>;
   return m.vec == 8 ? &rows_thread<Epi, true, 8> : m.vec == 4 ? &rows_thread<Epi, false, 4>
                                                               : &rows_thread<Epi, false, 8>;
 }
@@ -248,6 +337,8 @@ inline auto rows_kernel_fc(const TileView& m, bool fast) -> void (*)(TileView, c
       default: return &rows_lanes_fc<Epi, 32>;
     }
   }
+  if (m.olanes == 4) return &rows_olanes<Epi, 4, true>;
+  if (m.olanes == 8) return &rows_olanes<Epi, 8, true>;
   return m.vec == 8 ? &rows_thread_fc<Epi, true, 8> : m.vec == 4 ? &rows_thread_fc<Epi, false, 4>
                                                                  : &rows_thread_fc<Epi, false, 8>;
 }
