@@ -125,7 +125,8 @@ class OwnedView:
     def info(self):
         from types import SimpleNamespace
         c = self.d.report(self.d.n_levels)
-        return SimpleNamespace(n_levels=self.d.n_levels, coarse_n=c.n, coarse_nnz=c.nnz, coarse_inv_nnz=c.nnz_ffinv)
+        return SimpleNamespace(n_levels=self.d.n_levels, coarse_n=c.n, coarse_nnz=c.nnz, coarse_inv_nnz=c.nnz_ffinv,
+                               coarse_effective_order=c.effective_order, coarse_attempts=max(1, c.poly_attempts))
 
 
 def dist_vcycle_alg_bytes(v, coarse_iterations, up_smooths=2, fast=False):
@@ -223,6 +224,56 @@ def solve_alg_bytes(h, iterations, coarse_iterations, up_smooths=2, fast=False):
     resid = spmv_bytes(n0, n0, nnz0) + 8 * n0  # + b
     per_iter = per_cycle + resid + 24 * n0
     return iterations * per_iter + resid
+
+
+def csr_bytes(rows, nnz):
+    """One CSR operand read or written once: int32 column + fp64 value per
+    nonzero, int32 row pointer."""
+    return 12 * nnz + 4 * (rows + 1)
+
+
+def setup_alg_bytes(h, cf_bytes, poly_order, coarse_poly_order, fast):
+    """Compulsory HBM bytes of one setup (air.cpp:285-410), the lower bound
+    its time is quoted against: every operation reads each operand once and
+    writes its result once (SpGEMMs and fixed-sparsity products: csr_bytes of
+    the operands and of the result; SpMVs: spmv_bytes), intermediate products
+    that never have to leave the chip (A P inside R (A P), W A_ff inside W_2)
+    not counted. Per level: the CF split (SURVEY 8d rule, cf_bytes), the block
+    extraction (A read, A_ff / A_fc / A_cf written), per fit attempt
+    (poly_attempts) the power basis (poly_order SpMVs over A_ff, the Gram
+    pass over its poly_order + 1 vectors), the fixed-sparsity assembly
+    (effective_order - 1 products on A_ff's pattern: two reads and a write
+    each, then the inverse written) and the growth guard (30 steps of
+    u <- u - Q (A_ff u) with its norm, air.cpp:61-95); R = -A_cf Q + injection;
+    the one-point P from A's rows; the Galerkin product R A P with the drop
+    rule; fast mode: A_F P and W_2. Then the coarse fit."""
+    info = h.info()
+    total = cf_bytes
+    for l in range(info.n_levels):
+        L = h.level(l)
+        nxt_n, nxt_nnz = ((h.level(l + 1).n, h.level(l + 1).nnz) if l + 1 < info.n_levels
+                          else (info.coarse_n, info.coarse_nnz))
+        aff = csr_bytes(L.n_f, L.nnz_ff)
+        q = csr_bytes(L.n_f, L.nnz_ffinv)
+        total += csr_bytes(L.n, L.nnz) + L.n + aff + csr_bytes(L.n_f, L.nnz_fc) + csr_bytes(L.n_c, L.nnz_cf)
+        fit = poly_order * spmv_bytes(L.n_f, L.n_f, L.nnz_ff) + 8 * (poly_order + 1) * L.n_f
+        fit += max(int(L.effective_order) - 1, 0) * 3 * aff + q
+        fit += 30 * (spmv_bytes(L.n_f, L.n_f, L.nnz_ff) + spmv_bytes(L.n_f, L.n_f, L.nnz_ffinv) + 16 * L.n_f)
+        total += int(L.poly_attempts) * fit
+        total += csr_bytes(L.n_c, L.nnz_cf) + q + csr_bytes(L.n_c, L.nnz_r)             # R
+        total += csr_bytes(L.n, L.nnz) + L.n + csr_bytes(L.n, L.nnz_p)                  # P
+        total += (csr_bytes(L.n_c, L.nnz_r) + csr_bytes(L.n, L.nnz) + csr_bytes(L.n, L.nnz_p)
+                  + csr_bytes(nxt_n, nxt_nnz))                                          # R A P
+        if fast:
+            afp, wx = h.fused_nnz(l)
+            total += (csr_bytes(L.n_f, L.nnz_ff + L.nnz_fc) + csr_bytes(L.n, L.nnz_p) + csr_bytes(L.n_f, afp)
+                      + 2 * q + aff + csr_bytes(L.n_f, wx))
+    nc, zc, zq = info.coarse_n, info.coarse_nnz, info.coarse_inv_nnz
+    cfit = coarse_poly_order * spmv_bytes(nc, nc, zc) + 8 * (coarse_poly_order + 1) * nc
+    cfit += max(int(info.coarse_effective_order) - 1, 0) * 3 * csr_bytes(nc, zc) + csr_bytes(nc, zq)
+    cfit += 30 * (spmv_bytes(nc, nc, zc) + spmv_bytes(nc, nc, zq) + 16 * nc)
+    total += int(info.coarse_attempts) * cfit
+    return int(total)
 
 
 def reference_op_bytes(h, iterations, coarse_iterations, up_smooths=2):
@@ -572,6 +623,14 @@ def run_gpu_dist(args):
                                "allreduce payloads of the GMRES inner products"},
             "kernel": f"one distributed AIRG solve step over {ws} GPUs (all row kernels + halo exchanges)",
             "alg_bytes_per_step": step_bytes, "avg_step_ms": tot_ms / args.steps}
+    # setup against the N GPUs' HBM (the CF-split term without |S|: the owned
+    # report does not carry the strength counts)
+    cf_b = sum(2 * (12 * hv_.level(l).nnz + 4 * hv_.level(l).n) + 26 * hv_.level(l).n for l in range(d.n_levels))
+    sb = setup_alg_bytes(hv_, cf_b, prm["poly_order"], prm["coarse_poly_order"], fast)
+    setup_roof = {"bound": "hbm", "achieved": sb / (setup_ms / 1e3) / 1e9, "peak": peak * ws, "unit": "GB/s",
+                  "frac": sb / (setup_ms / 1e3) / 1e9 / (peak * ws), "alg_bytes": sb,
+                  "bytes_rule": "compulsory bytes of every setup operation, each operand read once and each "
+                                "result written once (bench.py setup_alg_bytes)"}
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -590,6 +649,7 @@ def run_gpu_dist(args):
         "e2e": {"value": N / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 8 * int(hi - lo),
                 "d2h_bytes_per_step": 8 * int(hi - lo), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches), "cf_split_ms": cf_ms,
+        "setup_roofline": setup_roof,
         "roofline": roof,
         "clocks": clk.summary(), "cpu_baseline": None,
     }
@@ -722,6 +782,7 @@ def run_gpu(args):
     for Al, rp in zip(mats, cf_reps):
         n_l, _, z_l = Al.dims()
         cf_bytes += 2 * (12 * z_l + 4 * n_l) + 16 * int(rp.s_nnz) + 26 * n_l
+    setup_bytes = setup_alg_bytes(h, cf_bytes, prm["poly_order"], prm["coarse_poly_order"], fast)
     for l in range(info.n_levels):  # the split re-derives the setup's labels (untimed check)
         if not np.array_equal(cf_lab[l][: mats[l].dims()[0]].cpu().numpy(), h.labels(l)):
             raise RuntimeError(f"CF split of level {l} differs from the hierarchy's labels")
@@ -886,6 +947,11 @@ def run_gpu(args):
                               "alg_bytes_all_levels": cf_bytes,
                               "traffic": prof.get("cf_split_dram_bytes_all_levels"),
                               "bytes_rule": "sum over levels of 2(12 nnz + 4n) + 16|S| + 26n (SURVEY 8d)"},
+        "setup_roofline": {"bound": "hbm", "achieved": setup_bytes / (setup_ms / 1e3) / 1e9, "peak": peak,
+                           "unit": "GB/s", "frac": setup_bytes / (setup_ms / 1e3) / 1e9 / peak,
+                           "alg_bytes": setup_bytes,
+                           "bytes_rule": "compulsory bytes of every setup operation, each operand read once and "
+                                         "each result written once (bench.py setup_alg_bytes)"},
         "roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
                      "frac": step_achieved / peak, "traffic": prof.get("solve_dram_bytes_per_step"),
                      "kernel": "one AIRG solve step: every kernel of the solve (V-cycle graphs, "

@@ -230,22 +230,28 @@ struct EpiScaled {  // y = acc / g (g from the predecessor: read after the wait)
   __device__ void row(int i, double acc) const { y[i] = acc / *g; }
   __device__ void finish() const {}
 };
-struct EpiGrowth {  // u_i <- u_i / g - (Q av)_i, partial |u|^2
+struct EpiGrowth {  // u_i <- u_i / g - (Q av)_i, |u| of the new iterate into *gout
   double* u;
   const double* g;
   double* part;
+  unsigned* ticket;  // zero between launches
+  double* gout;
   mutable double s;
   struct Pre {
     double ui, gg;
   };
-  __device__ Pre pre(int i) const { return Pre{u[i], *g}; }  // u: three kernels back, g: two
+  __device__ Pre pre(int i) const { return Pre{u[i], *g}; }  // both from the previous step's launch, two kernels back
   __device__ void row_pre(int i, double acc, const Pre& p) const {
     const double r = p.ui / p.gg - acc;
     u[i] = r;
     s += r * r;
   }
+  // one partial of |u|^2 per block; the block that finishes last sums the
+  // partials in index order (the same sum whichever block it is) and writes
+  // the norm: no separate finishing launch on the step's chain
   __device__ void finish() const {
     __shared__ double sm[32];
+    __shared__ bool last;
     double v = s;
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -255,28 +261,32 @@ struct EpiGrowth {  // u_i <- u_i / g - (Q av)_i, partial |u|^2
       v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (threadIdx.x == 0) part[blockIdx.x] = v;
+      if (threadIdx.x == 0) {
+        part[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+      }
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += __ldcg(part + i);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      t = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) {
+        *gout = sqrt(t);
+        *ticket = 0u;
+      }
     }
   }
 };
-__global__ void finish_norm_pdl(const double* __restrict__ part, int np, double* __restrict__ g) {
-  __shared__ double sm[32];
-  pdl_wait();
-  pdl_trigger();
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) *g = sqrt(s);
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -654,16 +664,18 @@ double smoother_growth(Ctx& c, const Csr& a, const Csr& q, const RowSplit* rs) {
     sq.build(c, *rs, q);
   }
   if (!rs) {
-    // three PDL-chained launches per step instead of five (v is rescaled in
-    // the next step's epilogues instead of by a separate pass)
+    // two PDL-chained launches per step (v is rescaled in the next step's
+    // epilogues instead of by a separate pass; the norm is finished by the
+    // last block of the second launch)
     const TileView tq = tview(q);
     const int nbq = (int)rows_grid(tq, false);
     DBuf<double> qpart(c, (size_t)nbq);
+    DBuf<unsigned> ticket(c, 1);
+    ticket.zero(c);
     for (int k = 0; k < kIters; ++k) {
       const double* gprev = k == 0 ? g.p + kIters : g.p + k - 1;
       LAUNCH_ROWS(c, EpiScaled, tview(a), v.p, (EpiScaled{av.p, gprev}));
-      LAUNCH_ROWS(c, EpiGrowth, tq, av.p, (EpiGrowth{v.p, gprev, qpart.p, 0.0}));
-      LAUNCH_PDL(c, finish_norm_pdl, 1, 1024, 0, (const double*)qpart.p, nbq, g.p + k);
+      LAUNCH_ROWS(c, EpiGrowth, tq, av.p, (EpiGrowth{v.p, gprev, qpart.p, ticket.p, g.p + k, 0.0}));
     }
   }
   for (int k = 0; k < (rs ? kIters : 0); ++k) {

@@ -19,15 +19,28 @@ __device__ __forceinline__ int64_t warp_incl_scan(int64_t v) {
   return v;
 }
 
-// Exclusive scan of one 4096-element tile; writes tile-local exclusive
-// prefixes and the tile total.
-template <class Tin>
-__global__ void __launch_bounds__(kScanThreads) scan_tiles(const Tin* __restrict__ in,
-                                                           int64_t* __restrict__ excl,
-                                                           int64_t* __restrict__ tile_sum,
-                                                           int64_t n) {
+// Single-pass exclusive scan (decoupled look-back): one launch instead of
+// tile scans + a scan of the tile sums + an offset pass (the setup runs
+// about a thousand scans). Tiles of 4096 elements are taken in ticket order
+// (a tile's predecessors are always already running). A tile publishes its
+// aggregate, then its inclusive prefix, as ONE 64-bit descriptor word
+// (status in bits 63..62: 0 empty, 1 aggregate, 2 prefix; the sum below), so
+// no fence orders a flag against its value. Warp 0 looks back 32 tiles at a
+// time. desc[0] is the ticket, desc[1 + t] tile t's descriptor (zeroed
+// before the launch). out[n] and *total get the grand total. Integer sums:
+// the result does not depend on the schedule.
+constexpr unsigned long long kDescMask = (1ull << 62) - 1;
+template <class Tin, class Tout>
+__global__ void __launch_bounds__(kScanThreads) scan_lookback(const Tin* in, Tout* out, int64_t n,
+                                                              unsigned long long* desc,
+                                                              int64_t* __restrict__ total) {
   __shared__ int64_t warp_sums[kScanThreads / 32];
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  __shared__ int64_t s_prefix;
+  __shared__ unsigned s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd((unsigned*)desc, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
   int64_t v[kScanItems];
   int64_t s = 0;
 #pragma unroll
@@ -37,67 +50,66 @@ __global__ void __launch_bounds__(kScanThreads) scan_tiles(const Tin* __restrict
     s += v[k];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t incl = warp_incl_scan(s);
+  const int64_t incl = warp_incl_scan(s);
   if (lane == 31) warp_sums[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    int64_t ws = warp_sums[lane];
-    ws = warp_incl_scan(ws);
+    const int64_t ws = warp_incl_scan(warp_sums[lane]);
     warp_sums[lane] = ws;
+    const int64_t agg = __shfl_sync(0xffffffffu, ws, 31);  // the tile's total
+    int64_t pre = 0;
+    if (tile > 0) {
+      if (lane == 0) atomicExch(desc + 1 + tile, (1ull << 62) | (unsigned long long)agg);
+      int64_t look = tile - 1;
+      while (true) {
+        const int64_t t = look - lane;
+        unsigned long long d = 2ull << 62;  // before tile 0: prefix 0
+        if (t >= 0) {
+          do {
+            d = *(volatile unsigned long long*)(desc + 1 + t);
+          } while ((d >> 62) == 0);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+        int64_t val = (int64_t)(d & kDescMask);
+        if (pm && lane > __ffs(pm) - 1) val = 0;  // beyond the nearest prefix
+#pragma unroll
+        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        pre += val;
+        if (pm) break;
+        look -= 32;
+      }
+    }
+    if (lane == 0) {
+      atomicExch(desc + 1 + tile, (2ull << 62) | (unsigned long long)(agg + pre));
+      s_prefix = pre;
+      if ((tile + 1) * kScanTile >= n) {  // the last tile
+        out[n] = (Tout)(agg + pre);
+        *total = agg + pre;
+      }
+    }
   }
   __syncthreads();
-  int64_t run = incl - s + (warp > 0 ? warp_sums[warp - 1] : 0);
+  int64_t run = incl - s + (warp > 0 ? warp_sums[warp - 1] : 0) + s_prefix;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const int64_t i = base + k;
-    if (i < n) excl[i] = run;
+    if (i < n) out[i] = (Tout)run;
     run += v[k];
   }
-  if (threadIdx.x == kScanThreads - 1) tile_sum[blockIdx.x] = run;
-}
-
-template <class Tout>
-__global__ void add_tile_offsets(const int64_t* __restrict__ excl,
-                                 const int64_t* __restrict__ tile_off, Tout* __restrict__ out,
-                                 int64_t n, const int64_t* __restrict__ total_src) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (Tout)(excl[i] + tile_off[i / kScanTile]);
-  if (i == n) out[n] = (Tout)(*total_src);
-}
-
-// in-place exclusive scan of int64 values with the total appended at [n]
-void scan64_inplace(Ctx& c, int64_t* d, int64_t n, int64_t* d_total) {
-  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  DBuf<int64_t> excl(c, (size_t)n), tsum(c, (size_t)tiles + 1);
-  LAUNCH(c, scan_tiles<int64_t>, (unsigned)tiles, kScanThreads, 0, d, excl.p, tsum.p, n);
-  if (tiles > 1) {
-    scan64_inplace(c, tsum.p, tiles, d_total);
-  } else {
-    CUDA_CHECK(cudaMemcpyAsync(d_total, tsum.p, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
-    CUDA_CHECK(cudaMemsetAsync(tsum.p, 0, sizeof(int64_t), c.stream));
-  }
-  LAUNCH(c, add_tile_offsets<int64_t>, blocks_for(n + 1, 256), 256, 0, excl.p, tsum.p, d, n, d_total);
 }
 
 template <class Tin, class Tout>
 int64_t scan_impl(Ctx& c, const Tin* d_counts, Tout* d_offsets, int64_t n) {
-  DBuf<int64_t> total(c, 1);
   if (n == 0) {
     CUDA_CHECK(cudaMemsetAsync(d_offsets, 0, sizeof(Tout), c.stream));
     return 0;
   }
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  DBuf<int64_t> excl(c, (size_t)n), tsum(c, (size_t)tiles + 1);
-  LAUNCH(c, scan_tiles<Tin>, (unsigned)tiles, kScanThreads, 0, d_counts, excl.p, tsum.p, n);
-  if (tiles > 1) {
-    scan64_inplace(c, tsum.p, tiles, total.p);
-  } else {
-    CUDA_CHECK(cudaMemcpyAsync(total.p, tsum.p, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
-    CUDA_CHECK(cudaMemsetAsync(tsum.p, 0, sizeof(int64_t), c.stream));
-  }
-  LAUNCH(c, add_tile_offsets<Tout>, blocks_for(n + 1, 256), 256, 0, excl.p, tsum.p, d_offsets, n,
-         total.p);
-  return read1(c, total.p);
+  DBuf<unsigned long long> desc(c, (size_t)tiles + 2);
+  CUDA_CHECK(cudaMemsetAsync(desc.p, 0, sizeof(unsigned long long) * (size_t)(tiles + 2), c.stream));
+  int64_t* total = (int64_t*)(desc.p + tiles + 1);
+  LAUNCH(c, (scan_lookback<Tin, Tout>), (unsigned)tiles, kScanThreads, 0, d_counts, d_offsets, n, desc.p, total);
+  return read1(c, total);
 }
 
 __global__ void dot_partials(const double* __restrict__ x, const double* __restrict__ y,
@@ -140,11 +152,10 @@ __global__ void reduce_partials(const double* __restrict__ partials, int np, dou
 void narrow_i64_to_i32(Ctx& c, const int64_t* in, int32_t* out, int64_t n);
 
 int64_t exclusive_scan(Ctx& c, const int32_t* d_counts, int32_t* d_offsets, int64_t n) {
-  // Scan in int64, then check the total fits the int32 offsets.
-  DBuf<int64_t> off64(c, (size_t)n + 1);
-  const int64_t total = scan_impl<int32_t, int64_t>(c, d_counts, off64.p, n);
+  // Summed in int64 (the offsets are narrowed as they are written): a total
+  // beyond the int32 offsets is refused before anything reads them.
+  const int64_t total = scan_impl<int32_t, int32_t>(c, d_counts, d_offsets, n);
   if (total > INT32_MAX) throw InvalidArgument("airg: nonzero count exceeds the int32 range");
-  narrow_i64_to_i32(c, off64.p, d_offsets, n + 1);
   return total;
 }
 
