@@ -130,6 +130,7 @@ int airg_ctx_destroy(airg_ctx* ctx) {
     if (!ctx) return;
     bind(ctx->c);
     cudaStreamSynchronize(ctx->c.stream);
+    ctx_free_workers(ctx->c);
     if (ctx->c.scratch) cudaFree(ctx->c.scratch);
     if (ctx->c.grid_bar) cudaFree(ctx->c.grid_bar);
     if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);

@@ -85,7 +85,18 @@ struct Ctx {
   size_t scratch_bytes = 0;
   // software grid-barrier words of persistent kernels (self-resetting)
   unsigned* grid_bar = nullptr;
+  // worker contexts (ctx_workers): own streams and staging on the same
+  // device, for independent chains enqueued side by side by host threads
+  Ctx* workers = nullptr;
+  int n_workers = 0;
 };
+
+// `count` worker contexts of c (created on first use, kept until the context
+// is destroyed). A worker's stream is not ordered against c.stream: the
+// caller synchronises c.stream before handing work out and every worker's
+// stream before taking results back.
+Ctx* ctx_workers(Ctx& c, int count);
+void ctx_free_workers(Ctx& c);
 
 // Device scratch of at least `bytes` (contents undefined), reused across
 // calls on the context's stream.

@@ -151,6 +151,39 @@ __global__ void reduce_partials(const double* __restrict__ partials, int np, dou
 
 void narrow_i64_to_i32(Ctx& c, const int64_t* in, int32_t* out, int64_t n);
 
+Ctx* ctx_workers(Ctx& c, int count) {
+  if (c.n_workers >= count) return c.workers;
+  Ctx* w = new Ctx[count];
+  for (int k = 0; k < count; ++k) {
+    if (k < c.n_workers) {
+      w[k] = c.workers[k];
+      continue;
+    }
+    w[k].device = c.device;
+    w[k].num_sms = c.num_sms;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&w[k].own_stream, cudaStreamNonBlocking));
+    w[k].stream = w[k].own_stream;
+  }
+  delete[] c.workers;
+  c.workers = w;
+  c.n_workers = count;
+  return w;
+}
+
+void ctx_free_workers(Ctx& c) {
+  for (int k = 0; k < c.n_workers; ++k) {
+    Ctx& w = c.workers[k];
+    cudaStreamSynchronize(w.stream);
+    if (w.scratch) cudaFree(w.scratch);
+    if (w.grid_bar) cudaFree(w.grid_bar);
+    if (w.pinned) cudaFreeHost(w.pinned);
+    if (w.own_stream) cudaStreamDestroy(w.own_stream);
+  }
+  delete[] c.workers;
+  c.workers = nullptr;
+  c.n_workers = 0;
+}
+
 int64_t exclusive_scan(Ctx& c, const int32_t* d_counts, int32_t* d_offsets, int64_t n) {
   // Summed in int64 (the offsets are narrowed as they are written): a total
   // beyond the int32 offsets is refused before anything reads them.
