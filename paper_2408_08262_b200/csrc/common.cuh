@@ -96,6 +96,9 @@ struct Ctx {
 // caller synchronises c.stream before handing work out and every worker's
 // stream before taking results back.
 Ctx* ctx_workers(Ctx& c, int count);
+// AIRG_SETUP_PARALLEL=0: independent setup chains (a level's retry fits, the
+// levels' fused operators) one after the other on the context's stream
+bool setup_parallel();
 void ctx_free_workers(Ctx& c);
 
 // Device scratch of at least `bytes` (contents undefined), reused across

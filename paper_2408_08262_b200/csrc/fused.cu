@@ -19,6 +19,9 @@
 #include <chrono>
 #include <cstdio>
 
+#include <atomic>
+#include <exception>
+#include <thread>
 #include "hier.cuh"
 
 namespace airg {
@@ -270,17 +273,66 @@ void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its) {
             std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  if (h.fused_smooths != smooths) {
-    for (size_t l = 0; l < h.levels.size(); ++l) {
-      build_fused_level(c, h.levels[l], smooths);
-      lap(h.levels[l].one_pass ? "level(one-pass)" : "level", (int64_t)l);
+  const bool do_levels = h.fused_smooths != smooths, do_coarse = h.fused_coarse_its != coarse_its;
+  const int64_t n_tasks = (do_levels ? (int64_t)h.levels.size() : 0) + (do_coarse ? 1 : 0);
+  if (!timing && setup_parallel() && n_tasks > 1) {
+    // The levels' operators (and the composed coarse solve) are independent
+    // of one another and each is a chain of short SpGEMM launches with
+    // readbacks: host threads take them from a counter, finest level first,
+    // each on its own worker stream. Same operators bit for bit.
+    constexpr int kWorkers = 6;
+    const int nw = (int)std::min<int64_t>(kWorkers, n_tasks);
+    Ctx* w = ctx_workers(c, nw);
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    std::atomic<int64_t> next{0};
+    std::vector<std::exception_ptr> err((size_t)nw);
+    std::vector<std::thread> th;
+    const int64_t n_lv = do_levels ? (int64_t)h.levels.size() : 0;
+    for (int k = 0; k < nw; ++k) {
+      th.emplace_back([&, k] {
+        try {
+          Ctx& wc = w[k];
+          CUDA_CHECK(cudaSetDevice(wc.device));
+          for (int64_t t = next.fetch_add(1); t < n_tasks; t = next.fetch_add(1)) {
+            if (t < n_lv)
+              build_fused_level(wc, h.levels[(size_t)t], smooths);
+            else
+              build_coarse_composed(wc, h, coarse_its);
+          }
+          CUDA_CHECK(cudaStreamSynchronize(wc.stream));
+        } catch (...) {
+          err[(size_t)k] = std::current_exception();
+        }
+      });
     }
-    h.fused_smooths = smooths;
-  }
-  if (h.fused_coarse_its != coarse_its) {
-    build_coarse_composed(c, h, coarse_its);
-    h.fused_coarse_its = coarse_its;
-    lap("coarse", coarse_its);
+    for (auto& t : th) t.join();
+    for (int k = 0; k < nw; ++k) {
+      c.launches += w[k].launches;
+      w[k].launches = 0;
+    }
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+    // the operators live on: released on the context's stream
+    auto home = [&](Csr& m) { m.rp.s = m.ci.s = m.v.s = c.stream; };
+    if (do_levels)
+      for (Level& L : h.levels)
+        for (Csr* m : {&L.afp, &L.fw, &L.fk, &L.dsc}) home(*m);
+    if (do_coarse) home(h.coarse_e);
+    if (do_levels) h.fused_smooths = smooths;
+    if (do_coarse) h.fused_coarse_its = coarse_its;
+  } else {
+    if (do_levels) {
+      for (size_t l = 0; l < h.levels.size(); ++l) {
+        build_fused_level(c, h.levels[l], smooths);
+        lap(h.levels[l].one_pass ? "level(one-pass)" : "level", (int64_t)l);
+      }
+      h.fused_smooths = smooths;
+    }
+    if (do_coarse) {
+      build_coarse_composed(c, h, coarse_its);
+      h.fused_coarse_its = coarse_its;
+      lap("coarse", coarse_its);
+    }
   }
   // the fast row kernels size their lane groups by the longest row (sparse.cu row_lanes)
   std::vector<Csr*> ms = {&h.coarse_a, &h.coarse_inv};

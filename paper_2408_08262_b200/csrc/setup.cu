@@ -66,16 +66,6 @@ struct Checked {
   bool valid = false;
 };
 
-// AIRG_SETUP_RETRIES=serial: the retry fits one after the other on the
-// context's stream (the reference's schedule)
-bool parallel_retries() {
-  static const bool v = [] {
-    const char* e = getenv("AIRG_SETUP_RETRIES");
-    return !(e && !strcmp(e, "serial"));
-  }();
-  return v;
-}
-
 // make_checked_inverse (air.cpp:106-129): up to 6 seeded fits, keep the
 // least-growing, stop once growth <= 0.5. The fits are independent (each
 // its own seed, all of the same A_ff), and each is a chain of short
@@ -103,7 +93,7 @@ Checked make_checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsi
       best_growth = growth;
     }
   };
-  const bool side_by_side = !rs && parallel_retries();
+  const bool side_by_side = !rs && setup_parallel();
   for (int64_t attempt = 0; attempt < (side_by_side ? 1 : 6); ++attempt) {
     PolyFit fit = poly_coefficients(c, a, order + 1, seed_of(attempt), rs);
     Csr q;

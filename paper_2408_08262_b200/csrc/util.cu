@@ -170,6 +170,14 @@ Ctx* ctx_workers(Ctx& c, int count) {
   return w;
 }
 
+bool setup_parallel() {
+  static const bool v = [] {
+    const char* e = getenv("AIRG_SETUP_PARALLEL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 void ctx_free_workers(Ctx& c) {
   for (int k = 0; k < c.n_workers; ++k) {
     Ctx& w = c.workers[k];
