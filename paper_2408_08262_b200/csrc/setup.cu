@@ -344,6 +344,34 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
                          std::to_string(nc) + ")");
 
     pc.lap(0);
+    // P and A P need the labels and A only, not the inverse: a host thread
+    // enqueues them on a worker stream (context 5; 0-4 are the retry fits')
+    // while this one fits A_ff^-1 and builds R. Same products, same bits.
+    Csr ap, rap;
+    const bool side_p = fused_cf && !pc.on && setup_parallel();
+    std::thread p_thread;
+    std::exception_ptr p_err;
+    Ctx* pw = nullptr;
+    if (side_p) {
+      pw = ctx_workers(c, 6) + 5;
+      CUDA_CHECK(cudaStreamSynchronize(c.stream));  // A, the map and the blocks complete
+      p_thread = std::thread([&] {
+        try {
+          CUDA_CHECK(cudaSetDevice(pw->device));
+          build_prolongation_fused(*pw, L.map, L.a, cfg.strength_alpha, L.pmap, L.p);
+          spgemm(*pw, L.a, L.p, ap);
+          CUDA_CHECK(cudaStreamSynchronize(pw->stream));
+        } catch (...) {
+          p_err = std::current_exception();
+        }
+      });
+    }
+    struct Joiner {  // an exception on this thread still joins the other
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{p_thread};
     // --- approximate ideal restriction (air.cpp:378-381)
     Checked ff = inj ? injected_inverse(c, L.aff, inj->level_coeffs[built], inj->level_eff[built],
                                         cfg.sparsity_order, rs)
@@ -356,19 +384,27 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     pc.lap(1);
     build_restriction(c, L.acf, L.ffinv, cfg.drop_restrict, L.map, L.r, nullptr, 0, rs);
     pc.lap(2);
-    if (fused_cf)
+    if (side_p) {
+      p_thread.join();
+      c.launches += pw->launches;
+      pw->launches = 0;
+      if (p_err) std::rethrow_exception(p_err);
+      // kept operators are released on the context's stream
+      L.pmap.s = L.p.rp.s = L.p.ci.s = L.p.v.s = c.stream;
+      ap.rp.s = ap.ci.s = ap.v.s = c.stream;
+    } else if (fused_cf) {
       build_prolongation_fused(c, L.map, L.a, cfg.strength_alpha, L.pmap, L.p);
-    else
+    } else {
       build_prolongation(c, L.map, g, L.a, L.pmap, L.p);
+    }
     pc.lap(3);
 
     // --- Galerkin coarse operator (air.cpp:268-271, :386-387)
-    Csr ap, rap;
     if (rs) {  // row slabs over the ranks, gathered (rowsplit.cuh)
       split_spgemm(c, *rs, L.a, L.p, ap, -1.0, true);
       split_spgemm(c, *rs, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
     } else {
-      spgemm(c, L.a, L.p, ap);
+      if (!side_p) spgemm(c, L.a, L.p, ap);
       spgemm(c, L.r, ap, rap, cfg.drop_coarse, /*keep_diag=*/true);
     }
     with_full_diagonal(c, rap, current);
