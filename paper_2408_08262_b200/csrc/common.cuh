@@ -96,9 +96,18 @@ struct Ctx {
 // caller synchronises c.stream before handing work out and every worker's
 // stream before taking results back.
 Ctx* ctx_workers(Ctx& c, int count);
-// AIRG_SETUP_PARALLEL=0: independent setup chains (a level's retry fits, the
-// levels' fused operators) one after the other on the context's stream
-bool setup_parallel();
+// Independent setup chains enqueued side by side by host threads on worker
+// streams: 1 = a level's retry fits, 2 = the levels' fused operators, 4 = P
+// and A P beside the inverse fit. AIRG_SETUP_PARALLEL=<mask>; 0: everything
+// on the context's stream, one chain after the other. Default 1. Measured on
+// C4 (B200): 0 -> 87 ms setup, 1 -> 78 ms, 7 -> 66 ms -- but after a setup
+// with part 2 or 4 every device-resident solve loop (the conditional WHILE
+// graphs of GMRES and Richardson) runs ~15 us per iteration slower (C4 solve
+// 67.8 -> 70.1 ms) although each kernel, launched one by one, takes the same
+// time, wherever the operators and the Krylov basis are placed (one arena,
+// fresh cudaMalloc) and whether or not the worker streams still exist: the
+// solve is the metric, so parts 2 and 4 are opt-in for setup-bound uses.
+bool setup_parallel(int part);
 void ctx_free_workers(Ctx& c);
 
 // Device scratch of at least `bytes` (contents undefined), reused across

@@ -275,7 +275,7 @@ void build_fused(Ctx& c, Hier& h, int64_t smooths, int64_t coarse_its) {
   };
   const bool do_levels = h.fused_smooths != smooths, do_coarse = h.fused_coarse_its != coarse_its;
   const int64_t n_tasks = (do_levels ? (int64_t)h.levels.size() : 0) + (do_coarse ? 1 : 0);
-  if (!timing && setup_parallel() && n_tasks > 1) {
+  if (!timing && setup_parallel(2) && n_tasks > 1) {
     // The levels' operators (and the composed coarse solve) are independent
     // of one another and each is a chain of short SpGEMM launches with
     // readbacks: host threads take them from a counter, finest level first,

@@ -93,7 +93,7 @@ Checked make_checked_inverse(Ctx& c, const Csr& a, int64_t order, int64_t sparsi
       best_growth = growth;
     }
   };
-  const bool side_by_side = !rs && setup_parallel();
+  const bool side_by_side = !rs && setup_parallel(1);
   for (int64_t attempt = 0; attempt < (side_by_side ? 1 : 6); ++attempt) {
     PolyFit fit = poly_coefficients(c, a, order + 1, seed_of(attempt), rs);
     Csr q;
@@ -348,7 +348,7 @@ void setup(Ctx& c, const Csr& a0, const airg_setup_config& cfg, const Injection*
     // enqueues them on a worker stream (context 5; 0-4 are the retry fits')
     // while this one fits A_ff^-1 and builds R. Same products, same bits.
     Csr ap, rap;
-    const bool side_p = fused_cf && !pc.on && setup_parallel();
+    const bool side_p = fused_cf && !pc.on && setup_parallel(4);
     std::thread p_thread;
     std::exception_ptr p_err;
     Ctx* pw = nullptr;

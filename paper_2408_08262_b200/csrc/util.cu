@@ -170,12 +170,12 @@ Ctx* ctx_workers(Ctx& c, int count) {
   return w;
 }
 
-bool setup_parallel() {
-  static const bool v = [] {
+bool setup_parallel(int part) {
+  static const int mask = [] {
     const char* e = getenv("AIRG_SETUP_PARALLEL");
-    return !(e && e[0] == '0');
+    return e ? atoi(e) : 1;
   }();
-  return v;
+  return (mask & part) != 0;
 }
 
 void ctx_free_workers(Ctx& c) {
