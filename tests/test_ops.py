@@ -205,6 +205,26 @@ def test_device_buffer_helpers_round_trip():
     assert same_bits(src, dst)
 
 
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 8192, 135169, 3 * 4096 * 40 + 5, 6_000_001])
+@pytest.mark.parametrize("frac_f", [0.0, 0.37, 1.0])
+def test_label_map_sizes_across_scan_tiles(n, frac_f):
+    """The label map's F/C positions come from the single-pass look-back scan
+    (util.cu scan_lookback: 4096-element tiles, 32-tile look-back windows):
+    one element, tile boundaries, several look-back windows (> 32 tiles), all
+    F / all C / mixed -- against the numpy positions (sparse.cpp:270-290)."""
+    from paper_2408_08262_b200 import airg
+    rng = np.random.default_rng(n)
+    lab = (rng.random(n) >= frac_f).astype(np.uint8)  # 0 = F, 1 = C
+    f2s, f2f, c2f = airg.build_label_map(lab)
+    isf = lab == 0
+    assert np.array_equal(f2f, np.flatnonzero(isf))
+    assert np.array_equal(c2f, np.flatnonzero(~isf))
+    want = np.where(isf, np.cumsum(isf) - 1, np.cumsum(~isf) - 1)
+    assert np.array_equal(f2s, want)
+
+
 _CF_SCRIPT = r"""
 import sys
 import numpy as np
@@ -241,3 +261,56 @@ def test_fused_cf_split_schedules_match_oracle(env):
     full.update(env)
     out = subprocess.run([sys.executable, "-c", script], env=full, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+_SETUP_SCRIPT = r"""
+import hashlib
+import sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2408_08262_b200 import airg, problems
+dg = hashlib.sha256()
+for cfg, scale in ((4, 0.5), (2, 0.25)):
+    p = problems.make(cfg, scale)
+    prm = dict(problems.setup_params(cfg), fused_smooths=2)
+    h = airg.setup(airg.SparseMatrix.from_arrays(p.n, p.n, p.row_offsets, p.cols, p.vals), **prm)
+    retried = 0
+    for l in range(h.n_levels):
+        L = h.level(l)
+        retried += L.smoother_growth > 0.5 or L.poly_attempts > 1
+        dg.update(h.labels(l).tobytes())
+        dg.update(np.array([L.poly_attempts, L.effective_order], np.int64).tobytes())
+        dg.update(np.array([L.smoother_growth], np.float64).tobytes())
+        for which in ("a", "ff_inv", "r", "p", "afp", "w"):
+            m = h.matrix(l, which)
+            for arr in (m.row_offsets, m.col_indices, m.values):
+                dg.update(np.ascontiguousarray(arr).tobytes())
+    res = airg.gmres_solve(h, p.b, coarse_iterations=prm["coarse_iterations"], fast=1)
+    dg.update(res.x.tobytes())
+    print("retried", cfg, int(retried))
+print("digest", dg.hexdigest())
+"""
+
+
+@pytest.mark.gpu
+def test_side_by_side_setup_chains_same_hierarchy():
+    """AIRG_SETUP_PARALLEL (setup.cu / fused.cu: the retry fits, the fused
+    operators, P and A P enqueued by host threads on worker streams) changes
+    the schedule only: labels, attempts, growth, level operators, fused
+    operators and the fast solve are bit-identical for masks 0, 1 and 7 (the
+    mask is read once per process, hence subprocesses). The half-size C4
+    hierarchy has levels whose first fit fails the growth guard."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mask in ("0", "1", "7"):
+        env = dict(os.environ, AIRG_SETUP_PARALLEL=mask)
+        out = subprocess.run([sys.executable, "-c", _SETUP_SCRIPT % repo], env=env, capture_output=True, text=True,
+                             timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs[mask] = out.stdout.strip().splitlines()
+    assert outs["0"][-1].startswith("digest ")
+    assert outs["0"] == outs["1"] == outs["7"], outs
+    assert any(ln.startswith("retried 4 ") and int(ln.split()[-1]) > 0 for ln in outs["0"]), outs["0"]
